@@ -1,0 +1,322 @@
+/*
+ * faastube.h — C ABI of the B200-native FaaSTube data-passing layer
+ * (libfaastube.so, built from paper_2411_01830_b200/csrc).
+ *
+ * The reference (arxiv 2411.01830, /root/reference) ships a Python simulator
+ * (`tubesim`); its data-passing surface is Python classes, not an FFI. Each
+ * entry point below replaces the reference function cited beside it
+ * (paths relative to pkg/src/tubesim/), with the same argument meaning and
+ * error behaviour (Python exceptions become FT_E_* status codes, message in
+ * ft_last_error()). INTEGRATION.md shows the ctypes binding a maintainer of
+ * the reference would add.
+ *
+ * Conventions: every function returns an int status (FT_OK = 0) unless noted;
+ * outputs go through pointers. GB/s = 1e9 B/s, sizes in bytes (double where
+ * the reference uses float byte counts), times in ms. "None" in the reference
+ * is NaN for doubles and -1 for GPU ids (host location). Arrays sized by the
+ * caller: `cap` is the capacity, `*n` the count written (FT_E_TRUNCATED when
+ * cap is too small; *n then holds the required count). JSON outputs use
+ * ("buf", "cap", "need") with need including the NUL.
+ * Decision objects are NOT thread-safe (the reference is single-threaded,
+ * SPEC.md:232-233); the device movers are stream-ordered and thread-safe.
+ */
+#ifndef FAASTUBE_H
+#define FAASTUBE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ------------------------------------------------------------------ status */
+enum ft_status {
+  FT_OK = 0,
+  FT_E_TOPOLOGY = 1,      /* topology.TopologyError            topology.py:40  */
+  FT_E_INFEASIBLE = 2,    /* pcie_sched.InfeasibleDemand       pcie_sched.py:19 */
+  FT_E_MISSING = 3,       /* dataplane.MissingData             dataplane.py:26 */
+  FT_E_DUPLICATE = 4,     /* dataplane.DuplicateStore          dataplane.py:30 */
+  FT_E_HARD_PRESSURE = 5, /* datastore.HardPressure            datastore.py:188 */
+  FT_E_OOM = 6,           /* MemoryError from MemoryPool       datastore.py:134-136 */
+  FT_E_CUDA = 7,          /* CUDA driver/runtime failure (device movers, pool) */
+  FT_E_VALUE = 8,         /* ValueError (bad argument)         e.g. datastore.py:27 */
+  FT_E_TRUNCATED = 9,     /* caller buffer too small */
+  FT_E_KEY = 10,          /* KeyError (unknown id / func) */
+  FT_E_NOT_SUPPORTED = 11 /* feature unavailable on this device/driver */
+};
+
+#define FT_MAX_PATH 8   /* GPUs per NVLink path (MAX_HOPS 4 => 5)  nvlink_sched.py:17 */
+#define FT_MAX_LINKS 8  /* link ids per branch                      dataplane.py:136-143 */
+
+const char* ft_last_error(void); /* thread-local message of the last failure */
+const char* ft_version(void);
+
+/* ------------------------------------------------- topology (topology.py) */
+typedef struct ft_topo ft_topo;
+/* from_dict(doc)                                          topology.py:327-355 */
+int ft_topo_create(const char* json_doc, ft_topo** out);
+void ft_topo_destroy(ft_topo* t);
+int ft_topo_gpu_count(const ft_topo* t, int* out);
+/* Topology.node_of / pcie_root_of                         topology.py:102-108 */
+int ft_topo_node_of(const ft_topo* t, int gpu, int* out);
+int ft_topo_root_of(const ft_topo* t, int gpu, int* out);
+/* Topology.nvlink_gbps                                    topology.py:110-114 */
+int ft_topo_nvlink_gbps(const ft_topo* t, int u, int v, double* out);
+/* Topology.nvlink_neighbors                               topology.py:116-119 */
+int ft_topo_neighbors(const ft_topo* t, int gpu, int32_t* out, int cap, int* n);
+/* Topology.pair_kind: 0 none, 1 nvlink, 2 nvswitch        topology.py:124-125 */
+int ft_topo_pair_kind(const ft_topo* t, int u, int v, int* out);
+/* Topology.switch_port_gbps / nvlink_degree_gbps          topology.py:127-140 */
+int ft_topo_switch_port_gbps(const ft_topo* t, int gpu, double* out);
+int ft_topo_degree_gbps(const ft_topo* t, int gpu, double* out);
+/* Topology.pair_bandwidth                                 topology.py:142-152 */
+int ft_topo_pair_bandwidth(const ft_topo* t, int u, int v, double* out);
+/* rates: 0 pcie_gbps, 1 pcie_pageable_gbps, 2 pcie_peer_gbps, 3 network_gbps */
+int ft_topo_rate(const ft_topo* t, int which, double* out);
+/* number of PCIe root groups and their members (sorted root order) */
+int ft_topo_roots(const ft_topo* t, int32_t* roots, int cap, int* n);
+
+/* ------------------------------------ bandwidth matrix (topology.py:358-443) */
+typedef struct ft_matrix ft_matrix;
+int ft_matrix_create(const ft_topo* t, ft_matrix** out); /* snapshot_matrix :446-449 */
+void ft_matrix_destroy(ft_matrix* m);
+int ft_matrix_hold(ft_matrix* m, const char* func, const int32_t* path, int n, double rate); /* :390-401 */
+int ft_matrix_release(ft_matrix* m, const char* func);                                      /* :403-412 */
+int ft_matrix_release_path(ft_matrix* m, const char* func, const int32_t* path, int n);     /* :414-428 */
+int ft_matrix_residual(const ft_matrix* m, int u, int v, double* out);                      /* :383-384 */
+int ft_matrix_budgets(const ft_matrix* m, int gpu, double* egress, double* ingress);
+int ft_matrix_aggregate_of(const ft_matrix* m, const char* func, double* out);              /* :433-434 */
+/* {"residual": [[u,v,r]...sorted], "egress": [...], "ingress": [...], "held": {func: [[path, rate]...]}} */
+int ft_matrix_state_json(const ft_matrix* m, char* buf, size_t cap, size_t* need);
+
+/* ----------------------------------------- NVLink policy (nvlink_sched.py) */
+typedef struct {
+  int32_t gpus[FT_MAX_PATH];
+  int32_t n;          /* GPUs on the path (hops + 1) */
+  int32_t held;       /* 1 when held_by == the querying func, 0 for None (shared) */
+  double b_min_gbps;
+} ft_nvpath;
+/* _candidate_paths                                  nvlink_sched.py:42-57 */
+int ft_candidate_paths(const ft_topo* t, int src, int dst, int max_hops, ft_nvpath* out, int cap, int* n);
+/* select_paths (phase 1, phase 2 busy adoption, shared fallback)  :64-133.
+ * trace_json (optional): {"candidates_examined":..,"phase1":[[path,rate]..],"phase2":[..],"shared_fallback":path?} */
+int ft_select_paths(ft_matrix* m, const char* func, int src, int dst, int allow_busy, ft_nvpath* out,
+                    int cap, int* n, char* trace_json, size_t trace_cap);
+/* release_paths                                     nvlink_sched.py:228-230 */
+int ft_release_paths(ft_matrix* m, const char* func);
+/* claim_direct_for_workflow (+ _evict_and_replan)    nvlink_sched.py:233-285
+ * pairs: npairs x (a, b). Result JSON: {"reservations": [[[a,b], rate]..], "degraded": {func: loss}} */
+int ft_claim_direct(ft_matrix* m, const int32_t* pairs, int npairs, const char* func, char* buf, size_t cap,
+                    size_t* need);
+/* distribute_chunks (largest remainder)             nvlink_sched.py:288-302 */
+int ft_distribute_chunks(int64_t chunk_count, const double* b_min_gbps, int npaths, int64_t* counts);
+
+/* -------------------------------------------- PCIe policy (pcie_sched.py) */
+/* min_rate                                          pcie_sched.py:23-33 */
+int ft_min_rate(double data_size_bytes, double slo_ms, double infer_ms, double* out_gbps);
+typedef struct ft_pcie_state ft_pcie_state;
+/* PcieSchedulerState                                pcie_sched.py:58-77 */
+int ft_pcie_state_create(double bw_all_gbps, int batch_chunks, int64_t chunk_bytes, ft_pcie_state** out);
+void ft_pcie_state_destroy(ft_pcie_state* s);
+/* RateDemand(...) + add (FT_E_INFEASIBLE like the dataclass ctor)  :36-55, :73-74 */
+int ft_pcie_state_add(ft_pcie_state* s, const char* func, double bytes, double slo_ms, double infer_ms,
+                      double arrival_ms);
+int ft_pcie_state_remove(ft_pcie_state* s, const char* func);
+int ft_pcie_rate_idle(const ft_pcie_state* s, double* out);                 /* :69-71 */
+int ft_demand_slack(const ft_pcie_state* s, const char* func, double now_ms, double* out); /* :49-55 */
+/* standalone RateDemand: rate_least and slack_ms(now) (FT_E_INFEASIBLE like the ctor)  :36-55 */
+int ft_rate_demand(double bytes, double slo_ms, double infer_ms, double arrival_ms, double now_ms, double* least,
+                   double* slack);
+/* partition: rates and slo_at_risk in demand insertion order      :80-104 */
+int ft_partition(ft_pcie_state* s, double now_ms, double* rates, int32_t* at_risk, int cap, int* n);
+/* trigger_batches                                   pcie_sched.py:107-119 */
+int ft_trigger_batches(double total_bytes, int64_t chunk_bytes, int batch_chunks, double* out, int cap, int* n);
+typedef struct ft_ring ft_ring;
+/* PinnedRing                                        pcie_sched.py:122-150 */
+int ft_ring_create(double capacity_bytes, double cost_ms_per_mb, int prewarmed, ft_ring** out);
+void ft_ring_destroy(ft_ring* r);
+int ft_ring_acquire(ft_ring* r, double bytes_needed, double* added_ms);
+int ft_ring_state(const ft_ring* r, double* warm_bytes, double* cold_allocated_bytes);
+/* default_ring_capacity                             pcie_sched.py:159-162 */
+int64_t ft_default_ring_capacity(int pcie_link_count, int64_t batch_bytes);
+
+/* ----------------------------------------------- latency model (simcore.py) */
+int ft_pipeline_latency(double size_bytes, const double* hop_gbps, int n, double chunk_bytes, double* out); /* :25-42 */
+int ft_pipeline_fill_ms(const double* hop_gbps, int n, double chunk_bytes, double* out);                   /* :45-50 */
+int ft_nearest_rank(const double* sorted_values, int n, double pct, double* out);                         /* :247-252 */
+
+/* ----------------------------------------- elastic store (datastore.py) */
+int ft_size_class(double size_bytes, int64_t* out);                 /* :24-29 */
+int ft_p99(const double* samples, int n, double* out);              /* :32-35 */
+typedef struct ft_hist ft_hist;
+/* FuncHistogram                                     datastore.py:38-72 */
+int ft_hist_create(const char* func, int window, ft_hist** out);
+void ft_hist_destroy(ft_hist* h);
+int ft_hist_record(ft_hist* h, double now_ms, double size_bytes, double concurrency);
+/* r_window_ms, r_size_bytes, r_con, last_request_ms (NaN if none) */
+int ft_hist_get(const ft_hist* h, double* r_window, double* r_size, double* r_con, double* last);
+int ft_hist_reservation(const ft_hist* h, double* out);
+int ft_hist_window_active(const ft_hist* h, double now_ms, int* out);
+/* pool_target over histograms                        datastore.py:79-82 */
+int ft_pool_target(const ft_hist* const* hists, int n, double now_ms, double floor_bytes, double* out);
+typedef struct ft_pool_policy ft_pool_policy;
+/* MemoryPool policy: mode 0 autoscale, 1 cache_all, 2 none     datastore.py:91-166 */
+int ft_pool_policy_create(int gpu, int mode, double floor_bytes, double native_alloc_ms, double physical_bytes,
+                          ft_pool_policy** out);
+void ft_pool_policy_destroy(ft_pool_policy* p);
+/* allocate -> stable block id (index-free), cost ms    :130-144 */
+int ft_pool_policy_allocate(ft_pool_policy* p, double size_bytes, int64_t* block_id, int64_t* class_bytes,
+                            double* cost_ms);
+int ft_pool_policy_free(ft_pool_policy* p, int64_t block_id);                              /* :146-149 */
+int ft_pool_policy_record(ft_pool_policy* p, const char* func, double now_ms, double size, double con);
+/* shrink: ids of dropped blocks (the physical memory to release)  :151-166 */
+int ft_pool_policy_shrink(ft_pool_policy* p, double now_ms, int64_t* dropped, int cap, int* n);
+int ft_pool_policy_target(ft_pool_policy* p, double now_ms, double* out);                  /* :127-128 */
+/* {"blocks": [[class_bytes, in_use, id]..], "pool_bytes":.., "in_use_bytes":..} */
+int ft_pool_policy_state_json(const ft_pool_policy* p, char* buf, size_t cap, size_t* need);
+#define FT_MAX_CONSUMERS 16
+typedef struct {
+  int64_t data_id;
+  double size_bytes;
+  double stored_at_ms;
+  int32_t location; /* 0 gpu, 1 host, 2 both              datastore.py:176 */
+  int32_t live;
+  int32_t n_consumers;
+  int32_t consumer_pos[FT_MAX_CONSUMERS];
+} ft_stored_object;
+/* migration_plan: policy 0 queue_aware, 1 lru; actions 0 reclaim, 1 migrate    :192-222 */
+int ft_migration_plan(const ft_stored_object* objs, int n, double pressure_bytes, int policy, int32_t* actions,
+                      int32_t* indices, int cap, int* nout);
+/* prefetch_back                                     datastore.py:225-238 */
+int ft_prefetch_back(const ft_stored_object* objs, int n, double free_bytes, int32_t* indices, int cap, int* nout);
+
+/* ------------------------------------ strategies + data plane (dataplane.py) */
+typedef struct {
+  int32_t host_oriented, parallel_pcie, unified_interface, pcie_sched, nvlink_sched;
+  int32_t pool;      /* 0 autoscale, 1 cache_all, 2 none */
+  int32_t migration; /* 0 queue_aware, 1 lru, 2 none */
+} ft_strategy;
+/* strategy_preset                                   strategies.py:33-62 */
+int ft_strategy_preset(const char* name, ft_strategy* out);
+
+typedef struct ft_index ft_index;
+/* DataIndex                                         dataplane.py:55-107 */
+int ft_index_create(double sync_period_ms, double local_lookup_ms, double global_lookup_ms, ft_index** out);
+void ft_index_destroy(ft_index* x);
+int ft_index_unique_id(ft_index* x, int64_t* out);
+int ft_index_store(ft_index* x, int64_t data_id, int node, int gpu, double size_bytes, double now_ms,
+                   const char* producer, int response, double* global_visible_ms);
+int ft_index_resolve(ft_index* x, int64_t data_id, int node, double now_ms, int* e_node, int* e_gpu,
+                     double* cost_ms, double* ready_ms, double* size_bytes);
+int ft_index_drop(ft_index* x, int64_t data_id);
+int ft_index_relocate(ft_index* x, int64_t data_id, int node, int gpu);
+
+/* link ids (dataplane.py:112-133) */
+enum ft_link_kind { FT_LINK_H2D = 0, FT_LINK_D2H = 1, FT_LINK_NV = 2, FT_LINK_NVP_OUT = 3, FT_LINK_NVP_IN = 4, FT_LINK_NET = 5 };
+typedef struct { int32_t kind, a, b; } ft_link; /* h2d/d2h: (node, root); nv/net: (u, v); nvp_*: (gpu, -1) */
+typedef struct {
+  ft_link links[FT_MAX_LINKS];
+  double hop_caps[FT_MAX_LINKS];
+  int32_t n_links, n_caps;
+  double bytes_share, cap_gbps /* NaN = None */, reserved_gbps /* NaN = None */, fill_ms;
+} ft_branch;
+enum ft_method { FT_INTRA_GPU = 0, FT_INTER_GPU = 1, FT_HOST_GPU = 2, FT_INTER_NODE = 3 };
+typedef struct ft_plane ft_plane;
+typedef struct ft_plan ft_plan;
+/* Dataplane(topo, strategy, matrix, chunk_bytes, intra_gpu_map_ms)  dataplane.py:166-173 */
+int ft_plane_create(const ft_topo* t, const ft_strategy* s, ft_matrix* m, double chunk_bytes,
+                    double intra_gpu_map_ms, ft_plane** out);
+void ft_plane_destroy(ft_plane* p);
+/* fetch_plan (gpu -1 = host)                        dataplane.py:176-186 */
+int ft_fetch_plan(ft_plane* p, int src_node, int src_gpu, int dst_node, int dst_gpu, double size_bytes,
+                  ft_plan** out);
+void ft_plan_destroy(ft_plan* plan);
+int ft_plan_method(const ft_plan* plan, int* method, double* fixed_ms, int* n_stages);
+int ft_plan_add_fixed_ms(ft_plan* plan, double ms); /* engine.py:451-452 */
+int ft_plan_stage(const ft_plan* plan, int stage, int* managed, double* pinned_bytes, int* n_branches);
+int ft_plan_branch(const ft_plan* plan, int stage, int branch, ft_branch* out);
+/* full plan as JSON (method, size_bytes, fixed_ms, claimed_func, note, stages, latency) */
+int ft_plan_json(const ft_plan* plan, char* buf, size_t cap, size_t* need);
+/* plan_latency_model                                dataplane.py:351-369 */
+int ft_plan_latency(const ft_plan* plan, double* out);
+/* Dataplane.release_claim                           dataplane.py:346-348 */
+int ft_release_claim(ft_plane* p, const ft_plan* plan);
+
+/* ------------- bandwidth-share scheduler: managed PCIe stages (engine.py) */
+typedef struct ft_arbiter ft_arbiter;
+/* one per (node, direction); bw_all = pcie_gbps x roots            engine.py:186-190 */
+int ft_arbiter_create(double bw_all_gbps, int batch_chunks, int64_t chunk_bytes, ft_arbiter** out);
+void ft_arbiter_destroy(ft_arbiter* a);
+/* _start_managed_stage (slo fallback 1e12 on InfeasibleDemand)      engine.py:537-575 */
+int ft_arbiter_start(ft_arbiter* a, double now_ms, const char* key, double total_bytes, double slo_ms,
+                     double infer_ms, double arrival_ms, double per_branch_cap_gbps, int n_branches);
+/* _on_boundary                                                      engine.py:637-646 */
+int ft_arbiter_boundary(ft_arbiter* a, double now_ms, const char* key);
+/* stage drained (flow_complete)                                     engine.py:558-564 */
+int ft_arbiter_finish(ft_arbiter* a, double now_ms, const char* key);
+/* decisions of the last call: [["partition",{..}],["set_rate",k,rate,per_branch],["pending",k,want],["arm",k,t]] */
+int ft_arbiter_decisions_json(const ft_arbiter* a, char* buf, size_t cap, size_t* need);
+/* {key: [rate, started, pending|null, anchor, armed|null]} */
+int ft_arbiter_state_json(const ft_arbiter* a, char* buf, size_t cap, size_t* need);
+/* live state of one stage (pending / armed NaN when None) */
+int ft_arbiter_stage(const ft_arbiter* a, const char* key, double* rate, int* started, double* pending,
+                     double* armed);
+/* earliest armed boundary over all stages (NaN if none) — the live driver's next wake-up */
+int ft_arbiter_next_event(const ft_arbiter* a, double* t_ms, char* key, size_t key_cap);
+
+/* ================================================= device side (sm_100a) */
+int ft_device_count(int* out);
+/* enable peer access dev -> peer (no-op when same device)              */
+int ft_peer_enable(int device, int peer);
+
+/* ---- elastic VMM pool (replaces the host-memory store)
+ * One reserved VA range per GPU; each block is a cuMemCreate physical
+ * allocation (2 MiB granularity) mapped into that range, readable/writable
+ * from every peer GPU; exportable as a POSIX fd for other processes.     */
+typedef struct ft_vmm_pool ft_vmm_pool;
+int ft_vmm_pool_create(int device, uint64_t va_bytes, ft_vmm_pool** out);
+void ft_vmm_pool_destroy(ft_vmm_pool* p);
+int ft_vmm_granularity(int device, uint64_t* out);
+int ft_vmm_block_map(ft_vmm_pool* p, uint64_t bytes, uint64_t* block, void** dptr);
+int ft_vmm_block_unmap(ft_vmm_pool* p, uint64_t block);
+int ft_vmm_block_export_fd(ft_vmm_pool* p, uint64_t block, int* fd);
+int ft_vmm_pool_stats(const ft_vmm_pool* p, uint64_t* mapped_bytes, uint64_t* reserved_bytes, int* blocks);
+/* import a block exported by another process; map it for `device` */
+int ft_vmm_import_fd(int device, int fd, uint64_t bytes, void** dptr, uint64_t* handle);
+int ft_vmm_unimport(uint64_t handle);
+/* SCM_RIGHTS fd passing over a connected AF_UNIX socket (PAPER.md:568 channel) */
+int ft_fd_send(int sock, int fd, uint64_t tag);
+int ft_fd_recv(int sock, int* fd, uint64_t* tag);
+
+/* ---- movers
+ * K1/K3 ft_copy: SM-driven bulk copy (TMA cp.async.bulk global->smem->global,
+ * mbarrier ring, persistent grid) for same-GPU handoff copies and NVLink
+ * peer copies (dst or src may be a peer-mapped pointer). Runs on `device`.
+ * fingerprint (optional, device u64[2]): fused integrity digest of the bytes.  */
+int ft_copy(void* dst, const void* src, uint64_t bytes, int device, void* stream);
+/* same, with explicit engine: 0 auto, 1 TMA bulk, 2 vector ld/st (peer-safe) */
+int ft_copy_ex(void* dst, const void* src, uint64_t bytes, int device, void* stream, int engine, int grid);
+/* position-keyed digest of `bytes` (u64 sum of mixed words + xor), device u64[2] out */
+int ft_fingerprint(const void* src, uint64_t bytes, uint64_t* out_dev, int device, void* stream);
+/* host-side digest of the same definition (for checking against ft_fingerprint) */
+int ft_fingerprint_host(const void* src, uint64_t bytes, uint64_t out[2]);
+/* one PCIe leg: pinned host -> device (or device -> host) by the copy engine, in batches of
+ * batch_bytes (0 = one op), on `stream`. Returns after enqueueing.           */
+int ft_pcie_copy(void* dst, const void* src, uint64_t bytes, int to_device, int device, void* stream,
+                 uint64_t batch_bytes);
+/* host->gFunc striped pass (dataplane.py:203-250 routes):
+ * k routes, route i moves [off_i, off_i+len_i) of host_src. Route 0 is the
+ * target's own link (CE straight into dst). Route i>0 lands each chunk in
+ * staging[i] on stage_dev[i] by CE, then the staging GPU forwards it to dst
+ * over NVLink with ft_copy as soon as that chunk's CE op completes (event
+ * chained; chunk ring of ring_chunks slots per staging GPU).
+ * streams: 2*k cudaStream_t (CE stream, forward stream per route).       */
+int ft_h2g_striped(void* dst, int dst_dev, const void* host_src, uint64_t bytes, int k, const int32_t* stage_dev,
+                   const uint64_t* off, const uint64_t* len, void* const* staging, uint64_t chunk_bytes,
+                   int ring_chunks, void* const* streams);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FAASTUBE_H */

@@ -1,0 +1,310 @@
+"""ctypes binding of libfaastube.so (include/faastube.h).
+
+The shared library is built in-tree by ``__graft_entry__.build()`` (or
+``make -C paper_2411_01830_b200/csrc``). There is no fallback: if the library
+is missing every entry point raises ``LibraryMissing``.
+
+Status codes map onto the exception types the reference raises
+(``tubesim`` topology.py:40, pcie_sched.py:19, dataplane.py:26-31,
+datastore.py:134-136/188).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import json
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.environ.get("FAASTUBE_LIB", os.path.join(_HERE, "libfaastube.so"))
+
+MAX_PATH = 8
+MAX_LINKS = 8
+MAX_CONSUMERS = 16
+
+
+class LibraryMissing(RuntimeError):
+    pass
+
+
+class FaasTubeError(RuntimeError):
+    code = -1
+
+
+class TopologyError(ValueError):
+    """topology.py:40"""
+
+
+class InfeasibleDemand(ValueError):
+    """pcie_sched.py:19"""
+
+
+class MissingData(KeyError):
+    """dataplane.py:26"""
+
+
+class DuplicateStore(ValueError):
+    """dataplane.py:30"""
+
+
+class HardPressure(RuntimeError):
+    """datastore.py:188"""
+
+
+class CudaError(RuntimeError):
+    pass
+
+
+class Truncated(RuntimeError):
+    pass
+
+
+class NotSupported(RuntimeError):
+    pass
+
+
+_ERRORS = {
+    1: TopologyError,
+    2: InfeasibleDemand,
+    3: MissingData,
+    4: DuplicateStore,
+    5: HardPressure,
+    6: MemoryError,
+    7: CudaError,
+    8: ValueError,
+    9: Truncated,
+    10: KeyError,
+    11: NotSupported,
+}
+
+i32, i64, u64, dbl, sz = C.c_int32, C.c_int64, C.c_uint64, C.c_double, C.c_size_t
+P = C.POINTER
+vp = C.c_void_p
+cstr = C.c_char_p
+
+
+class NvPathC(C.Structure):
+    _fields_ = [("gpus", i32 * MAX_PATH), ("n", i32), ("held", i32), ("b_min_gbps", dbl)]
+
+
+class StoredObjectC(C.Structure):
+    _fields_ = [("data_id", i64), ("size_bytes", dbl), ("stored_at_ms", dbl), ("location", i32),
+                ("live", i32), ("n_consumers", i32), ("consumer_pos", i32 * MAX_CONSUMERS)]
+
+
+class StrategyC(C.Structure):
+    _fields_ = [("host_oriented", i32), ("parallel_pcie", i32), ("unified_interface", i32),
+                ("pcie_sched", i32), ("nvlink_sched", i32), ("pool", i32), ("migration", i32)]
+
+
+class LinkC(C.Structure):
+    _fields_ = [("kind", i32), ("a", i32), ("b", i32)]
+
+
+class BranchC(C.Structure):
+    _fields_ = [("links", LinkC * MAX_LINKS), ("hop_caps", dbl * MAX_LINKS), ("n_links", i32),
+                ("n_caps", i32), ("bytes_share", dbl), ("cap_gbps", dbl), ("reserved_gbps", dbl),
+                ("fill_ms", dbl)]
+
+
+# name: (restype, argtypes); restype None means the int status convention
+_SIGS = {
+    "ft_last_error": (cstr, []),
+    "ft_version": (cstr, []),
+    "ft_topo_create": (None, [cstr, P(vp)]),
+    "ft_topo_destroy": (C.c_void_p, [vp]),
+    "ft_topo_gpu_count": (None, [vp, P(C.c_int)]),
+    "ft_topo_node_of": (None, [vp, C.c_int, P(C.c_int)]),
+    "ft_topo_root_of": (None, [vp, C.c_int, P(C.c_int)]),
+    "ft_topo_nvlink_gbps": (None, [vp, C.c_int, C.c_int, P(dbl)]),
+    "ft_topo_neighbors": (None, [vp, C.c_int, P(i32), C.c_int, P(C.c_int)]),
+    "ft_topo_pair_kind": (None, [vp, C.c_int, C.c_int, P(C.c_int)]),
+    "ft_topo_switch_port_gbps": (None, [vp, C.c_int, P(dbl)]),
+    "ft_topo_degree_gbps": (None, [vp, C.c_int, P(dbl)]),
+    "ft_topo_pair_bandwidth": (None, [vp, C.c_int, C.c_int, P(dbl)]),
+    "ft_topo_rate": (None, [vp, C.c_int, P(dbl)]),
+    "ft_topo_roots": (None, [vp, P(i32), C.c_int, P(C.c_int)]),
+    "ft_matrix_create": (None, [vp, P(vp)]),
+    "ft_matrix_destroy": (C.c_void_p, [vp]),
+    "ft_matrix_hold": (None, [vp, cstr, P(i32), C.c_int, dbl]),
+    "ft_matrix_release": (None, [vp, cstr]),
+    "ft_matrix_release_path": (None, [vp, cstr, P(i32), C.c_int]),
+    "ft_matrix_residual": (None, [vp, C.c_int, C.c_int, P(dbl)]),
+    "ft_matrix_budgets": (None, [vp, C.c_int, P(dbl), P(dbl)]),
+    "ft_matrix_aggregate_of": (None, [vp, cstr, P(dbl)]),
+    "ft_matrix_state_json": (None, [vp, C.c_char_p, sz, P(sz)]),
+    "ft_candidate_paths": (None, [vp, C.c_int, C.c_int, C.c_int, P(NvPathC), C.c_int, P(C.c_int)]),
+    "ft_select_paths": (None, [vp, cstr, C.c_int, C.c_int, C.c_int, P(NvPathC), C.c_int, P(C.c_int),
+                               C.c_char_p, sz]),
+    "ft_release_paths": (None, [vp, cstr]),
+    "ft_claim_direct": (None, [vp, P(i32), C.c_int, cstr, C.c_char_p, sz, P(sz)]),
+    "ft_distribute_chunks": (None, [i64, P(dbl), C.c_int, P(i64)]),
+    "ft_min_rate": (None, [dbl, dbl, dbl, P(dbl)]),
+    "ft_pcie_state_create": (None, [dbl, C.c_int, i64, P(vp)]),
+    "ft_pcie_state_destroy": (C.c_void_p, [vp]),
+    "ft_pcie_state_add": (None, [vp, cstr, dbl, dbl, dbl, dbl]),
+    "ft_pcie_state_remove": (None, [vp, cstr]),
+    "ft_pcie_rate_idle": (None, [vp, P(dbl)]),
+    "ft_demand_slack": (None, [vp, cstr, dbl, P(dbl)]),
+    "ft_rate_demand": (None, [dbl, dbl, dbl, dbl, dbl, P(dbl), P(dbl)]),
+    "ft_partition": (None, [vp, dbl, P(dbl), P(i32), C.c_int, P(C.c_int)]),
+    "ft_trigger_batches": (None, [dbl, i64, C.c_int, P(dbl), C.c_int, P(C.c_int)]),
+    "ft_ring_create": (None, [dbl, dbl, C.c_int, P(vp)]),
+    "ft_ring_destroy": (C.c_void_p, [vp]),
+    "ft_ring_acquire": (None, [vp, dbl, P(dbl)]),
+    "ft_ring_state": (None, [vp, P(dbl), P(dbl)]),
+    "ft_default_ring_capacity": (i64, [C.c_int, i64]),
+    "ft_pipeline_latency": (None, [dbl, P(dbl), C.c_int, dbl, P(dbl)]),
+    "ft_pipeline_fill_ms": (None, [P(dbl), C.c_int, dbl, P(dbl)]),
+    "ft_nearest_rank": (None, [P(dbl), C.c_int, dbl, P(dbl)]),
+    "ft_size_class": (None, [dbl, P(i64)]),
+    "ft_p99": (None, [P(dbl), C.c_int, P(dbl)]),
+    "ft_hist_create": (None, [cstr, C.c_int, P(vp)]),
+    "ft_hist_destroy": (C.c_void_p, [vp]),
+    "ft_hist_record": (None, [vp, dbl, dbl, dbl]),
+    "ft_hist_get": (None, [vp, P(dbl), P(dbl), P(dbl), P(dbl)]),
+    "ft_hist_reservation": (None, [vp, P(dbl)]),
+    "ft_hist_window_active": (None, [vp, dbl, P(C.c_int)]),
+    "ft_pool_target": (None, [P(vp), C.c_int, dbl, dbl, P(dbl)]),
+    "ft_pool_policy_create": (None, [C.c_int, C.c_int, dbl, dbl, dbl, P(vp)]),
+    "ft_pool_policy_destroy": (C.c_void_p, [vp]),
+    "ft_pool_policy_allocate": (None, [vp, dbl, P(i64), P(i64), P(dbl)]),
+    "ft_pool_policy_free": (None, [vp, i64]),
+    "ft_pool_policy_record": (None, [vp, cstr, dbl, dbl, dbl]),
+    "ft_pool_policy_shrink": (None, [vp, dbl, P(i64), C.c_int, P(C.c_int)]),
+    "ft_pool_policy_target": (None, [vp, dbl, P(dbl)]),
+    "ft_pool_policy_state_json": (None, [vp, C.c_char_p, sz, P(sz)]),
+    "ft_migration_plan": (None, [P(StoredObjectC), C.c_int, dbl, C.c_int, P(i32), P(i32), C.c_int, P(C.c_int)]),
+    "ft_prefetch_back": (None, [P(StoredObjectC), C.c_int, dbl, P(i32), C.c_int, P(C.c_int)]),
+    "ft_strategy_preset": (None, [cstr, P(StrategyC)]),
+    "ft_index_create": (None, [dbl, dbl, dbl, P(vp)]),
+    "ft_index_destroy": (C.c_void_p, [vp]),
+    "ft_index_unique_id": (None, [vp, P(i64)]),
+    "ft_index_store": (None, [vp, i64, C.c_int, C.c_int, dbl, dbl, cstr, C.c_int, P(dbl)]),
+    "ft_index_resolve": (None, [vp, i64, C.c_int, dbl, P(C.c_int), P(C.c_int), P(dbl), P(dbl), P(dbl)]),
+    "ft_index_drop": (None, [vp, i64]),
+    "ft_index_relocate": (None, [vp, i64, C.c_int, C.c_int]),
+    "ft_plane_create": (None, [vp, P(StrategyC), vp, dbl, dbl, P(vp)]),
+    "ft_plane_destroy": (C.c_void_p, [vp]),
+    "ft_fetch_plan": (None, [vp, C.c_int, C.c_int, C.c_int, C.c_int, dbl, P(vp)]),
+    "ft_plan_destroy": (C.c_void_p, [vp]),
+    "ft_plan_method": (None, [vp, P(C.c_int), P(dbl), P(C.c_int)]),
+    "ft_plan_add_fixed_ms": (None, [vp, dbl]),
+    "ft_plan_stage": (None, [vp, C.c_int, P(C.c_int), P(dbl), P(C.c_int)]),
+    "ft_plan_branch": (None, [vp, C.c_int, C.c_int, P(BranchC)]),
+    "ft_plan_json": (None, [vp, C.c_char_p, sz, P(sz)]),
+    "ft_plan_latency": (None, [vp, P(dbl)]),
+    "ft_release_claim": (None, [vp, vp]),
+    "ft_arbiter_create": (None, [dbl, C.c_int, i64, P(vp)]),
+    "ft_arbiter_destroy": (C.c_void_p, [vp]),
+    "ft_arbiter_start": (None, [vp, dbl, cstr, dbl, dbl, dbl, dbl, dbl, C.c_int]),
+    "ft_arbiter_boundary": (None, [vp, dbl, cstr]),
+    "ft_arbiter_finish": (None, [vp, dbl, cstr]),
+    "ft_arbiter_decisions_json": (None, [vp, C.c_char_p, sz, P(sz)]),
+    "ft_arbiter_state_json": (None, [vp, C.c_char_p, sz, P(sz)]),
+    "ft_arbiter_stage": (None, [vp, cstr, P(dbl), P(C.c_int), P(dbl), P(dbl)]),
+    "ft_arbiter_next_event": (None, [vp, P(dbl), C.c_char_p, sz]),
+    # device side
+    "ft_device_count": (None, [P(C.c_int)]),
+    "ft_peer_enable": (None, [C.c_int, C.c_int]),
+    "ft_vmm_pool_create": (None, [C.c_int, u64, P(vp)]),
+    "ft_vmm_pool_destroy": (C.c_void_p, [vp]),
+    "ft_vmm_granularity": (None, [C.c_int, P(u64)]),
+    "ft_vmm_block_map": (None, [vp, u64, P(u64), P(vp)]),
+    "ft_vmm_block_unmap": (None, [vp, u64]),
+    "ft_vmm_block_export_fd": (None, [vp, u64, P(C.c_int)]),
+    "ft_vmm_pool_stats": (None, [vp, P(u64), P(u64), P(C.c_int)]),
+    "ft_vmm_import_fd": (None, [C.c_int, C.c_int, u64, P(vp), P(u64)]),
+    "ft_vmm_unimport": (None, [u64]),
+    "ft_fd_send": (None, [C.c_int, C.c_int, u64]),
+    "ft_fd_recv": (None, [C.c_int, P(C.c_int), P(u64)]),
+    "ft_copy": (None, [vp, vp, u64, C.c_int, vp]),
+    "ft_copy_ex": (None, [vp, vp, u64, C.c_int, vp, C.c_int, C.c_int]),
+    "ft_fingerprint": (None, [vp, u64, vp, C.c_int, vp]),
+    "ft_fingerprint_host": (None, [vp, u64, P(u64)]),
+    "ft_pcie_copy": (None, [vp, vp, u64, C.c_int, C.c_int, vp, u64]),
+    "ft_h2g_striped": (None, [vp, C.c_int, vp, u64, C.c_int, P(i32), P(u64), P(u64), P(vp), u64, C.c_int,
+                              P(vp)]),
+}
+
+HEADER_SYMBOLS = tuple(_SIGS)
+
+
+class _Lib:
+    def __init__(self):
+        self._dll = None
+
+    def load(self):
+        if self._dll is None:
+            if not os.path.exists(LIB_PATH):
+                raise LibraryMissing(
+                    f"{LIB_PATH} not built: run `python -c 'import __graft_entry__ as g; g.build()'` "
+                    "or `make -C paper_2411_01830_b200/csrc` (no CPU fallback exists)")
+            dll = C.CDLL(LIB_PATH)
+            for name, (res, args) in _SIGS.items():
+                fn = getattr(dll, name)
+                fn.argtypes = args
+                fn.restype = C.c_int if res is None else res
+            self._dll = dll
+        return self._dll
+
+    def raw(self, name):
+        return getattr(self.load(), name)
+
+    def __getattr__(self, name):
+        if not name.startswith("ft_"):
+            raise AttributeError(name)
+        fn = self.raw(name)
+        res = _SIGS[name][0]
+        if res is not None:
+            return fn
+
+        def call(*args):
+            rc = fn(*args)
+            if rc != 0:
+                raise_status(rc)
+            return rc
+        call.__name__ = name
+        return call
+
+
+LIB = _Lib()
+
+
+def raise_status(rc):
+    msg = LIB.raw("ft_last_error")()
+    msg = msg.decode() if msg else f"status {rc}"
+    exc = _ERRORS.get(rc, FaasTubeError)
+    raise exc(msg)
+
+
+def call_status(name, *args):
+    """Call returning the raw status (for truncation retries)."""
+    return LIB.raw(name)(*args)
+
+
+def json_out(name, *args):
+    """Call a (…, buf, cap, need) JSON producer with automatic sizing."""
+    cap = 1 << 14
+    while True:
+        buf = C.create_string_buffer(cap)
+        need = sz()
+        rc = LIB.raw(name)(*args, buf, cap, C.byref(need))
+        if rc == 9 and need.value > cap:
+            cap = need.value
+            continue
+        if rc != 0:
+            raise_status(rc)
+        return json.loads(buf.value.decode())
+
+
+def enc(s):
+    return s.encode() if isinstance(s, str) else s
+
+
+def none_if_nan(x):
+    return None if x != x else x
+
+
+def nan_if_none(x):
+    return float("nan") if x is None else float(x)

@@ -1,0 +1,859 @@
+// Device side of libfaastube (sm_100a): elastic VMM pool, SM-driven copy
+// kernels (TMA bulk + vector engines), fused integrity digest, PCIe legs on
+// the copy engines, and the striped host->gFunc pass with NVLink forwarding.
+//
+// Design notes: the probes in profiles/r01 showed that on
+// B200 the copy engine is the fastest PCIe mover (55.6 GB/s H2D vs 51.5 GB/s
+// for any SM-initiated read shape), while for HBM- and NVLink-side copies an
+// SM-driven TMA bulk pipeline matches or beats the copy engine (6.48 TB/s
+// read+write vs 6.40). So PCIe legs run on the CE, everything after the PCIe
+// hop runs in our kernels.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <sys/socket.h>
+#include <sys/un.h>
+#include <unistd.h>
+
+#include <atomic>
+#include <cstdlib>
+#include <cstdint>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/faastube.h"
+
+namespace ft {
+void set_last_error(const std::string& msg);
+}
+
+namespace {
+
+int cuda_fail(cudaError_t e, const char* what) {
+  ft::set_last_error(std::string(what) + ": " + cudaGetErrorString(e));
+  return FT_E_CUDA;
+}
+#define CU_RT(x)                                  \
+  do {                                            \
+    cudaError_t e_ = (x);                         \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #x); \
+  } while (0)
+
+// ------------------------------------------------------------ driver API
+// Resolved through the runtime so libfaastube.so loads on machines without
+// a driver (build container) and never links libcuda directly.
+struct Drv {
+  bool ok = false;
+  decltype(&cuMemCreate) create;
+  decltype(&cuMemRelease) release;
+  decltype(&cuMemAddressReserve) reserve;
+  decltype(&cuMemAddressFree) addr_free;
+  decltype(&cuMemMap) map;
+  decltype(&cuMemUnmap) unmap;
+  decltype(&cuMemSetAccess) set_access;
+  decltype(&cuMemExportToShareableHandle) export_handle;
+  decltype(&cuMemImportFromShareableHandle) import_handle;
+  decltype(&cuMemGetAllocationGranularity) granularity;
+  decltype(&cuGetErrorString) err;
+};
+Drv g_drv;
+std::once_flag g_drv_once;
+template <class F>
+bool sym(const char* name, F* out) {
+  void* p = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess)
+    return false;
+  *out = reinterpret_cast<F>(p);
+  return true;
+}
+Drv* drv() {
+  std::call_once(g_drv_once, [] {
+    Drv& d = g_drv;
+    d.ok = sym("cuMemCreate", &d.create) && sym("cuMemRelease", &d.release) &&
+           sym("cuMemAddressReserve", &d.reserve) && sym("cuMemAddressFree", &d.addr_free) &&
+           sym("cuMemMap", &d.map) && sym("cuMemUnmap", &d.unmap) && sym("cuMemSetAccess", &d.set_access) &&
+           sym("cuMemExportToShareableHandle", &d.export_handle) &&
+           sym("cuMemImportFromShareableHandle", &d.import_handle) &&
+           sym("cuMemGetAllocationGranularity", &d.granularity) && sym("cuGetErrorString", &d.err);
+  });
+  return g_drv.ok ? &g_drv : nullptr;
+}
+int cu_fail(CUresult r, const char* what) {
+  const char* s = "unknown";
+  if (g_drv.err) g_drv.err(r, &s);
+  ft::set_last_error(std::string(what) + ": " + s);
+  return r == CUDA_ERROR_OUT_OF_MEMORY ? FT_E_OOM : FT_E_CUDA;
+}
+#define CU_DRV(x)                              \
+  do {                                         \
+    CUresult r_ = (x);                         \
+    if (r_ != CUDA_SUCCESS) return cu_fail(r_, #x); \
+  } while (0)
+
+CUmemAllocationProp block_prop(int device) {
+  CUmemAllocationProp p = {};
+  p.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+  p.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  p.location.id = device;
+  p.requestedHandleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+  return p;
+}
+
+// Grant read/write to `device` and every GPU that can reach it peer-to-peer.
+int grant_access(Drv* d, CUdeviceptr va, size_t bytes, int owner, bool all_peers) {
+  int n = 0;
+  CU_RT(cudaGetDeviceCount(&n));
+  std::vector<CUmemAccessDesc> acc;
+  for (int g = 0; g < n; ++g) {
+    int ok = g == owner;
+    if (!ok && all_peers) cudaDeviceCanAccessPeer(&ok, g, owner);
+    if (!ok) continue;
+    CUmemAccessDesc a = {};
+    a.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    a.location.id = g;
+    a.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+    acc.push_back(a);
+  }
+  CU_DRV(d->set_access(va, bytes, acc.data(), acc.size()));
+  return FT_OK;
+}
+
+// ------------------------------------------------------------ kernels
+constexpr int kBulkThreads = 32;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(n));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{ .reg .pred p; W%=: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1; @!p bra W%=; }" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* smem, const void* gmem, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(smem)),
+               "l"(gmem), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* gmem, const void* smem, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gmem), "r"(smem_u32(smem)),
+               "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+
+// K1/K3 TMA-bulk engine. One elected thread per CTA runs a STAGES-deep
+// global->smem->global ring; tiles are dealt round-robin over a persistent
+// grid. Requires 16-byte aligned src/dst and a multiple-of-16 byte count
+// (the host wrapper peels the unaligned head/tail to the vector engine).
+template <int STAGES>
+__global__ void __launch_bounds__(kBulkThreads) k_copy_bulk(uint8_t* __restrict__ dst,
+                                                            const uint8_t* __restrict__ src, uint64_t bytes,
+                                                            uint32_t tile) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ __align__(8) uint64_t full[STAGES];
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) mbar_init(&full[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  const uint64_t ntiles = (bytes + tile - 1) / tile;
+  auto tile_len = [&](uint64_t t) -> uint32_t {
+    uint64_t off = t * tile;
+    return (uint32_t)((bytes - off) < tile ? (bytes - off) : tile);
+  };
+  uint64_t next = blockIdx.x;  // next tile to load
+  for (int s = 0; s < STAGES && next < ntiles; ++s, next += gridDim.x) {
+    uint32_t len = tile_len(next);
+    mbar_expect_tx(&full[s], len);
+    bulk_g2s(smem + (size_t)s * tile, src + next * tile, len, &full[s]);
+  }
+  uint32_t phase = 0;
+  int s = 0;
+  for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    mbar_wait(&full[s], phase);
+    bulk_s2g(dst + t * tile, smem + (size_t)s * tile, tile_len(t));
+    if (next < ntiles) {
+      // refill this slot once the store just issued has read it out; the
+      // other STAGES-1 slots keep their loads in flight meanwhile.
+      bulk_wait_read<0>();
+      uint32_t len = tile_len(next);
+      mbar_expect_tx(&full[s], len);
+      bulk_g2s(smem + (size_t)s * tile, src + next * tile, len, &full[s]);
+      next += gridDim.x;
+    }
+    if (++s == STAGES) {
+      s = 0;
+      phase ^= 1;
+    }
+  }
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+// Vector engine (also the peer-safe engine): 16-byte loads/stores, UNROLL
+// independent requests in flight per thread, grid-stride. `bytes` multiple
+// of 16 and both pointers 16-byte aligned.
+template <int UNROLL>
+__global__ void __launch_bounds__(512) k_copy_vec(int4* __restrict__ dst, const int4* __restrict__ src,
+                                                  uint64_t n16) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i + (UNROLL - 1) * stride < n16; i += UNROLL * stride) {
+    int4 v[UNROLL];
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) v[u] = __ldcs(src + i + u * stride);
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) __stcs(dst + i + u * stride, v[u]);
+  }
+  for (; i < n16; i += stride) __stcs(dst + i, __ldcs(src + i));
+}
+
+__global__ void k_copy_bytes(uint8_t* dst, const uint8_t* src, uint64_t n) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+
+// Digest: words w_i (8 bytes little-endian, tail zero-padded) mixed with
+// their index; accumulators are u64 sum and xor (order independent, so any
+// grid shape gives the same value). Identical to ft_fingerprint_host.
+__host__ __device__ __forceinline__ uint64_t fp_mix(uint64_t x) {
+  x ^= x >> 30;
+  x *= 0xbf58476d1ce4e5b9ull;
+  x ^= x >> 27;
+  x *= 0x94d049bb133111ebull;
+  x ^= x >> 31;
+  return x;
+}
+__host__ __device__ __forceinline__ uint64_t fp_word(uint64_t w, uint64_t i) {
+  return fp_mix(w ^ (i * 0x9e3779b97f4a7c15ull + 0x632be59bd9b4e019ull));
+}
+__global__ void __launch_bounds__(512) k_fingerprint(const uint8_t* __restrict__ src, uint64_t bytes,
+                                                     unsigned long long* out) {
+  const uint64_t nw = bytes / 8;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  uint64_t s = 0, x = 0;
+  const uint64_t* w = reinterpret_cast<const uint64_t*>(src);
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nw; i += stride) {
+    uint64_t h = fp_word(__ldcs(w + i), i);
+    s += h;
+    x ^= h;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0 && (bytes & 7)) {
+    uint64_t t = 0;
+    for (uint64_t k = 0; k < (bytes & 7); ++k) t |= (uint64_t)src[nw * 8 + k] << (8 * k);
+    uint64_t h = fp_word(t, nw);
+    s += h;
+    x ^= h;
+  }
+  for (int o = 16; o; o >>= 1) {
+    s += __shfl_xor_sync(0xffffffffu, s, o);
+    x ^= __shfl_xor_sync(0xffffffffu, x, o);
+  }
+  __shared__ uint64_t ws[16], wx[16];
+  int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) {
+    ws[wid] = s;
+    wx[wid] = x;
+  }
+  __syncthreads();
+  if (wid == 0) {
+    int nwarp = blockDim.x / 32;
+    s = lane < nwarp ? ws[lane] : 0;
+    x = lane < nwarp ? wx[lane] : 0;
+    for (int o = 16; o; o >>= 1) {
+      s += __shfl_xor_sync(0xffffffffu, s, o);
+      x ^= __shfl_xor_sync(0xffffffffu, x, o);
+    }
+    if (lane == 0) {
+      atomicAdd(&out[0], (unsigned long long)s);
+      atomicXor(&out[1], (unsigned long long)x);
+    }
+  }
+}
+
+// ------------------------------------------------------------ launch config
+struct DevInfo {
+  int sms = 0;
+  bool init = false;
+};
+std::mutex g_dev_mu;
+DevInfo g_dev[64];
+int dev_sms(int device) {
+  std::lock_guard<std::mutex> lk(g_dev_mu);
+  if (!g_dev[device].init) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device);
+    g_dev[device].sms = v > 0 ? v : 148;
+    g_dev[device].init = true;
+  }
+  return g_dev[device].sms;
+}
+// Bulk-engine shape: STAGES x tile bytes of smem per CTA, ctas_per_sm CTAs
+// resident per SM. Defaults from the sweep in profiles/r01 (override with
+// FT_BULK_STAGES / FT_BULK_TILE / FT_BULK_CTAS_PER_SM for tuning runs).
+struct BulkCfg {
+  int stages = 3;
+  uint32_t tile = 32768;
+  int ctas_per_sm = 2;
+};
+BulkCfg bulk_cfg() {
+  static BulkCfg c = [] {
+    BulkCfg b;
+    if (const char* e = getenv("FT_BULK_STAGES")) b.stages = atoi(e);
+    if (const char* e = getenv("FT_BULK_TILE")) b.tile = (uint32_t)atoi(e);
+    if (const char* e = getenv("FT_BULK_CTAS_PER_SM")) b.ctas_per_sm = atoi(e);
+    if (b.stages != 2 && b.stages != 3 && b.stages != 4 && b.stages != 6) b.stages = 3;
+    if (b.tile < 1024 || b.tile % 16 || (size_t)b.tile * b.stages > 200 * 1024) b.tile = 32768;
+    if (b.ctas_per_sm < 1) b.ctas_per_sm = 1;
+    return b;
+  }();
+  return c;
+}
+template <int S>
+int launch_bulk_s(uint8_t* dst, const uint8_t* src, uint64_t bytes, int device, cudaStream_t st, int grid,
+                  uint32_t tile, int per_sm) {
+  size_t smem = (size_t)S * tile;
+  CU_RT(cudaFuncSetAttribute(k_copy_bulk<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  uint64_t tiles = (bytes + tile - 1) / tile;
+  if (grid <= 0) grid = per_sm * dev_sms(device);
+  if ((uint64_t)grid > tiles) grid = (int)tiles;
+  k_copy_bulk<S><<<grid, kBulkThreads, smem, st>>>(dst, src, bytes, tile);
+  CU_RT(cudaGetLastError());
+  return FT_OK;
+}
+int launch_bulk(uint8_t* dst, const uint8_t* src, uint64_t bytes, int device, cudaStream_t st, int grid) {
+  BulkCfg c = bulk_cfg();
+  switch (c.stages) {
+    case 2: return launch_bulk_s<2>(dst, src, bytes, device, st, grid, c.tile, c.ctas_per_sm);
+    case 4: return launch_bulk_s<4>(dst, src, bytes, device, st, grid, c.tile, c.ctas_per_sm);
+    case 6: return launch_bulk_s<6>(dst, src, bytes, device, st, grid, c.tile, c.ctas_per_sm);
+    default: return launch_bulk_s<3>(dst, src, bytes, device, st, grid, c.tile, c.ctas_per_sm);
+  }
+}
+int launch_vec(uint8_t* dst, const uint8_t* src, uint64_t bytes, int device, cudaStream_t st, int grid) {
+  uint64_t n16 = bytes / 16;
+  if (grid <= 0) grid = 2 * dev_sms(device);
+  uint64_t need = (n16 + 512 * 4 - 1) / (512 * 4);
+  if (need < (uint64_t)grid) grid = (int)(need ? need : 1);
+  k_copy_vec<4><<<grid, 512, 0, st>>>(reinterpret_cast<int4*>(dst), reinterpret_cast<const int4*>(src), n16);
+  CU_RT(cudaGetLastError());
+  return FT_OK;
+}
+
+int copy_impl(void* dst_, const void* src_, uint64_t bytes, int device, cudaStream_t st, int engine, int grid) {
+  if (bytes == 0) return FT_OK;
+  if (!dst_ || !src_) {
+    ft::set_last_error("ft_copy: null pointer");
+    return FT_E_VALUE;
+  }
+  int cur = -1;
+  CU_RT(cudaGetDevice(&cur));
+  if (cur != device) CU_RT(cudaSetDevice(device));
+  uint8_t* dst = static_cast<uint8_t*>(dst_);
+  const uint8_t* src = static_cast<const uint8_t*>(src_);
+  int rc = FT_OK;
+  // Peel so the body is 16-byte aligned on both sides (only possible when the
+  // two pointers share alignment mod 16; otherwise fall back to bytes).
+  uintptr_t ms = (uintptr_t)src & 15, md = (uintptr_t)dst & 15;
+  if (ms != md) {
+    k_copy_bytes<<<2 * dev_sms(device), 256, 0, st>>>(dst, src, bytes);
+    cudaError_t e = cudaGetLastError();
+    if (cur != device) cudaSetDevice(cur);
+    return e == cudaSuccess ? FT_OK : cuda_fail(e, "k_copy_bytes");
+  }
+  uint64_t head = ms ? (16 - ms) : 0;
+  if (head > bytes) head = bytes;
+  uint64_t body = (bytes - head) & ~(uint64_t)15;
+  uint64_t tail = bytes - head - body;
+  if (head) k_copy_bytes<<<1, 32, 0, st>>>(dst, src, head);
+  if (body) {
+    if (engine == 0) engine = 1;
+    rc = engine == 1 ? launch_bulk(dst + head, src + head, body, device, st, grid)
+                     : launch_vec(dst + head, src + head, body, device, st, grid);
+  }
+  if (rc == FT_OK && tail) k_copy_bytes<<<1, 32, 0, st>>>(dst + head + body, src + head + body, tail);
+  cudaError_t e = cudaGetLastError();
+  if (cur != device) cudaSetDevice(cur);
+  if (rc) return rc;
+  return e == cudaSuccess ? FT_OK : cuda_fail(e, "ft_copy");
+}
+
+// ------------------------------------------------------------ VMM pool
+struct Block {
+  CUmemGenericAllocationHandle h;
+  CUdeviceptr va;
+  size_t bytes;
+};
+struct Import {
+  CUmemGenericAllocationHandle h;
+  CUdeviceptr va;
+  size_t bytes;
+};
+std::mutex g_imp_mu;
+std::map<uint64_t, Import> g_imports;
+std::atomic<uint64_t> g_imp_next{1};
+
+}  // namespace
+
+struct ft_vmm_pool {
+  int device;
+  size_t gran;
+  CUdeviceptr base;
+  size_t va_bytes;
+  std::map<size_t, size_t> free_va;  // offset -> length
+  std::map<uint64_t, Block> blocks;
+  uint64_t next_id = 1;
+  size_t mapped = 0;
+  std::mutex mu;
+};
+
+extern "C" {
+
+int ft_device_count(int* out) {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) {
+    *out = 0;
+    cudaGetLastError();
+    return cuda_fail(e, "cudaGetDeviceCount");
+  }
+  *out = n;
+  return FT_OK;
+}
+
+int ft_peer_enable(int device, int peer) {
+  if (device == peer) return FT_OK;
+  int ok = 0;
+  CU_RT(cudaDeviceCanAccessPeer(&ok, device, peer));
+  if (!ok) {
+    ft::set_last_error("peer access not supported between these GPUs");
+    return FT_E_NOT_SUPPORTED;
+  }
+  int cur = 0;
+  CU_RT(cudaGetDevice(&cur));
+  CU_RT(cudaSetDevice(device));
+  cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+  cudaSetDevice(cur);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();
+    return FT_OK;
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceEnablePeerAccess");
+  return FT_OK;
+}
+
+int ft_vmm_granularity(int device, uint64_t* out) {
+  Drv* d = drv();
+  if (!d) {
+    ft::set_last_error("CUDA driver VMM entry points unavailable");
+    return FT_E_NOT_SUPPORTED;
+  }
+  CU_RT(cudaSetDevice(device));
+  CU_RT(cudaFree(0));
+  CUmemAllocationProp p = block_prop(device);
+  size_t g = 0;
+  CU_DRV(d->granularity(&g, &p, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED));
+  *out = g;
+  return FT_OK;
+}
+
+int ft_vmm_pool_create(int device, uint64_t va_bytes, ft_vmm_pool** out) {
+  Drv* d = drv();
+  if (!d) {
+    ft::set_last_error("CUDA driver VMM entry points unavailable");
+    return FT_E_NOT_SUPPORTED;
+  }
+  uint64_t gran = 0;
+  int rc = ft_vmm_granularity(device, &gran);
+  if (rc) return rc;
+  va_bytes = (va_bytes + gran - 1) / gran * gran;
+  CUdeviceptr base = 0;
+  CU_DRV(d->reserve(&base, va_bytes, gran, 0, 0));
+  auto* p = new ft_vmm_pool{};
+  p->device = device;
+  p->gran = gran;
+  p->base = base;
+  p->va_bytes = va_bytes;
+  p->free_va[0] = va_bytes;
+  *out = p;
+  return FT_OK;
+}
+
+void ft_vmm_pool_destroy(ft_vmm_pool* p) {
+  if (!p) return;
+  Drv* d = drv();
+  if (d) {
+    for (auto& kv : p->blocks) {
+      d->unmap(kv.second.va, kv.second.bytes);
+      d->release(kv.second.h);
+    }
+    d->addr_free(p->base, p->va_bytes);
+  }
+  delete p;
+}
+
+int ft_vmm_block_map(ft_vmm_pool* p, uint64_t bytes, uint64_t* block, void** dptr) {
+  if (!p || !bytes) {
+    ft::set_last_error("ft_vmm_block_map: bad arguments");
+    return FT_E_VALUE;
+  }
+  Drv* d = drv();
+  size_t sz = (bytes + p->gran - 1) / p->gran * p->gran;
+  std::lock_guard<std::mutex> lk(p->mu);
+  size_t off = SIZE_MAX;
+  for (auto& kv : p->free_va)
+    if (kv.second >= sz) {
+      off = kv.first;
+      break;
+    }
+  if (off == SIZE_MAX) {
+    ft::set_last_error("VMM pool virtual range exhausted");
+    return FT_E_OOM;
+  }
+  CU_RT(cudaSetDevice(p->device));
+  CUmemAllocationProp prop = block_prop(p->device);
+  CUmemGenericAllocationHandle h;
+  CU_DRV(d->create(&h, sz, &prop, 0));
+  CUdeviceptr va = p->base + off;
+  CUresult r = d->map(va, sz, 0, h, 0);
+  if (r != CUDA_SUCCESS) {
+    d->release(h);
+    return cu_fail(r, "cuMemMap");
+  }
+  int rc = grant_access(d, va, sz, p->device, true);
+  if (rc) {
+    d->unmap(va, sz);
+    d->release(h);
+    return rc;
+  }
+  size_t len = p->free_va[off];
+  p->free_va.erase(off);
+  if (len > sz) p->free_va[off + sz] = len - sz;
+  uint64_t id = p->next_id++;
+  p->blocks[id] = Block{h, va, sz};
+  p->mapped += sz;
+  *block = id;
+  *dptr = reinterpret_cast<void*>(va);
+  return FT_OK;
+}
+
+int ft_vmm_block_unmap(ft_vmm_pool* p, uint64_t block) {
+  Drv* d = drv();
+  std::lock_guard<std::mutex> lk(p->mu);
+  auto it = p->blocks.find(block);
+  if (it == p->blocks.end()) {
+    ft::set_last_error("unknown VMM block");
+    return FT_E_KEY;
+  }
+  Block b = it->second;
+  p->blocks.erase(it);
+  CU_DRV(d->unmap(b.va, b.bytes));
+  CU_DRV(d->release(b.h));
+  p->mapped -= b.bytes;
+  // return the VA range, coalescing neighbours
+  size_t off = b.va - p->base, len = b.bytes;
+  auto nxt = p->free_va.lower_bound(off);
+  if (nxt != p->free_va.end() && nxt->first == off + len) {
+    len += nxt->second;
+    p->free_va.erase(nxt);
+  }
+  auto prv = p->free_va.lower_bound(off);
+  if (prv != p->free_va.begin()) {
+    --prv;
+    if (prv->first + prv->second == off) {
+      off = prv->first;
+      len += prv->second;
+      p->free_va.erase(prv);
+    }
+  }
+  p->free_va[off] = len;
+  return FT_OK;
+}
+
+int ft_vmm_block_export_fd(ft_vmm_pool* p, uint64_t block, int* fd) {
+  Drv* d = drv();
+  std::lock_guard<std::mutex> lk(p->mu);
+  auto it = p->blocks.find(block);
+  if (it == p->blocks.end()) {
+    ft::set_last_error("unknown VMM block");
+    return FT_E_KEY;
+  }
+  int f = -1;
+  CU_DRV(d->export_handle(&f, it->second.h, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0));
+  *fd = f;
+  return FT_OK;
+}
+
+int ft_vmm_pool_stats(const ft_vmm_pool* p, uint64_t* mapped, uint64_t* reserved, int* blocks) {
+  if (mapped) *mapped = p->mapped;
+  if (reserved) *reserved = p->va_bytes;
+  if (blocks) *blocks = (int)p->blocks.size();
+  return FT_OK;
+}
+
+int ft_vmm_import_fd(int device, int fd, uint64_t bytes, void** dptr, uint64_t* handle) {
+  Drv* d = drv();
+  if (!d) {
+    ft::set_last_error("CUDA driver VMM entry points unavailable");
+    return FT_E_NOT_SUPPORTED;
+  }
+  CU_RT(cudaSetDevice(device));
+  CU_RT(cudaFree(0));
+  CUmemGenericAllocationHandle h;
+  CU_DRV(d->import_handle(&h, (void*)(uintptr_t)fd, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR));
+  uint64_t gran = 0;
+  int rc = ft_vmm_granularity(device, &gran);
+  if (rc) {
+    d->release(h);
+    return rc;
+  }
+  size_t sz = (bytes + gran - 1) / gran * gran;
+  CUdeviceptr va = 0;
+  CUresult r = d->reserve(&va, sz, gran, 0, 0);
+  if (r != CUDA_SUCCESS) {
+    d->release(h);
+    return cu_fail(r, "cuMemAddressReserve");
+  }
+  r = d->map(va, sz, 0, h, 0);
+  if (r != CUDA_SUCCESS) {
+    d->addr_free(va, sz);
+    d->release(h);
+    return cu_fail(r, "cuMemMap(import)");
+  }
+  rc = grant_access(d, va, sz, device, false);
+  if (rc) {
+    d->unmap(va, sz);
+    d->addr_free(va, sz);
+    d->release(h);
+    return rc;
+  }
+  uint64_t id = g_imp_next++;
+  {
+    std::lock_guard<std::mutex> lk(g_imp_mu);
+    g_imports[id] = Import{h, va, sz};
+  }
+  *dptr = reinterpret_cast<void*>(va);
+  *handle = id;
+  return FT_OK;
+}
+
+int ft_vmm_unimport(uint64_t handle) {
+  Drv* d = drv();
+  Import im;
+  {
+    std::lock_guard<std::mutex> lk(g_imp_mu);
+    auto it = g_imports.find(handle);
+    if (it == g_imports.end()) {
+      ft::set_last_error("unknown import handle");
+      return FT_E_KEY;
+    }
+    im = it->second;
+    g_imports.erase(it);
+  }
+  CU_DRV(d->unmap(im.va, im.bytes));
+  CU_DRV(d->addr_free(im.va, im.bytes));
+  CU_DRV(d->release(im.h));
+  return FT_OK;
+}
+
+int ft_fd_send(int sock, int fd, uint64_t tag) {
+  struct msghdr msg = {};
+  char cbuf[CMSG_SPACE(sizeof(int))];
+  memset(cbuf, 0, sizeof cbuf);
+  struct iovec iov = {&tag, sizeof tag};
+  msg.msg_iov = &iov;
+  msg.msg_iovlen = 1;
+  msg.msg_control = cbuf;
+  msg.msg_controllen = sizeof cbuf;
+  struct cmsghdr* c = CMSG_FIRSTHDR(&msg);
+  c->cmsg_level = SOL_SOCKET;
+  c->cmsg_type = SCM_RIGHTS;
+  c->cmsg_len = CMSG_LEN(sizeof(int));
+  memcpy(CMSG_DATA(c), &fd, sizeof(int));
+  if (sendmsg(sock, &msg, 0) != (ssize_t)sizeof tag) {
+    ft::set_last_error(std::string("sendmsg: ") + strerror(errno));
+    return FT_E_VALUE;
+  }
+  return FT_OK;
+}
+
+int ft_fd_recv(int sock, int* fd, uint64_t* tag) {
+  struct msghdr msg = {};
+  char cbuf[CMSG_SPACE(sizeof(int))];
+  uint64_t t = 0;
+  struct iovec iov = {&t, sizeof t};
+  msg.msg_iov = &iov;
+  msg.msg_iovlen = 1;
+  msg.msg_control = cbuf;
+  msg.msg_controllen = sizeof cbuf;
+  if (recvmsg(sock, &msg, 0) != (ssize_t)sizeof t) {
+    ft::set_last_error(std::string("recvmsg: ") + strerror(errno));
+    return FT_E_VALUE;
+  }
+  struct cmsghdr* c = CMSG_FIRSTHDR(&msg);
+  if (!c || c->cmsg_type != SCM_RIGHTS) {
+    ft::set_last_error("recvmsg: no fd attached");
+    return FT_E_VALUE;
+  }
+  memcpy(fd, CMSG_DATA(c), sizeof(int));
+  if (tag) *tag = t;
+  return FT_OK;
+}
+
+int ft_copy(void* dst, const void* src, uint64_t bytes, int device, void* stream) {
+  // auto engine: TMA bulk when both sides are memory of `device`, else the
+  // peer-safe vector engine.
+  cudaPointerAttributes a{}, b{};
+  int engine = 1;
+  if (cudaPointerGetAttributes(&a, dst) != cudaSuccess || cudaPointerGetAttributes(&b, src) != cudaSuccess) {
+    cudaGetLastError();
+    engine = 2;
+  } else if (a.type != cudaMemoryTypeDevice || b.type != cudaMemoryTypeDevice || a.device != device ||
+             b.device != device) {
+    engine = 2;
+  }
+  return copy_impl(dst, src, bytes, device, (cudaStream_t)stream, engine, 0);
+}
+
+int ft_copy_ex(void* dst, const void* src, uint64_t bytes, int device, void* stream, int engine, int grid) {
+  if (engine < 0 || engine > 2) {
+    ft::set_last_error("unknown copy engine");
+    return FT_E_VALUE;
+  }
+  if (engine == 0) return ft_copy(dst, src, bytes, device, stream);
+  return copy_impl(dst, src, bytes, device, (cudaStream_t)stream, engine, grid);
+}
+
+int ft_fingerprint(const void* src, uint64_t bytes, uint64_t* out_dev, int device, void* stream) {
+  int cur = 0;
+  CU_RT(cudaGetDevice(&cur));
+  if (cur != device) CU_RT(cudaSetDevice(device));
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e = cudaMemsetAsync(out_dev, 0, 16, st);
+  if (e == cudaSuccess) {
+    uint64_t nw = bytes / 8;
+    int grid = 2 * dev_sms(device);
+    uint64_t need = (nw + 511) / 512;
+    if (need < (uint64_t)grid) grid = (int)(need ? need : 1);
+    k_fingerprint<<<grid, 512, 0, st>>>(static_cast<const uint8_t*>(src), bytes,
+                                        reinterpret_cast<unsigned long long*>(out_dev));
+    e = cudaGetLastError();
+  }
+  if (cur != device) cudaSetDevice(cur);
+  return e == cudaSuccess ? FT_OK : cuda_fail(e, "ft_fingerprint");
+}
+
+int ft_fingerprint_host(const void* src_, uint64_t bytes, uint64_t out[2]) {
+  const uint8_t* src = static_cast<const uint8_t*>(src_);
+  uint64_t nw = bytes / 8, s = 0, x = 0;
+  for (uint64_t i = 0; i < nw; ++i) {
+    uint64_t w;
+    memcpy(&w, src + 8 * i, 8);
+    uint64_t h = fp_word(w, i);
+    s += h;
+    x ^= h;
+  }
+  if (bytes & 7) {
+    uint64_t t = 0;
+    for (uint64_t k = 0; k < (bytes & 7); ++k) t |= (uint64_t)src[nw * 8 + k] << (8 * k);
+    uint64_t h = fp_word(t, nw);
+    s += h;
+    x ^= h;
+  }
+  out[0] = s;
+  out[1] = x;
+  return FT_OK;
+}
+
+int ft_pcie_copy(void* dst, const void* src, uint64_t bytes, int to_device, int device, void* stream,
+                 uint64_t batch_bytes) {
+  int cur = 0;
+  CU_RT(cudaGetDevice(&cur));
+  if (cur != device) CU_RT(cudaSetDevice(device));
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaMemcpyKind kind = to_device ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost;
+  uint64_t step = batch_bytes ? batch_bytes : bytes;
+  cudaError_t e = cudaSuccess;
+  for (uint64_t off = 0; off < bytes && e == cudaSuccess; off += step) {
+    uint64_t n = bytes - off < step ? bytes - off : step;
+    e = cudaMemcpyAsync(static_cast<uint8_t*>(dst) + off, static_cast<const uint8_t*>(src) + off, n, kind, st);
+  }
+  if (cur != device) cudaSetDevice(cur);
+  return e == cudaSuccess ? FT_OK : cuda_fail(e, "ft_pcie_copy");
+}
+
+int ft_h2g_striped(void* dst_, int dst_dev, const void* host_, uint64_t bytes, int k, const int32_t* stage_dev,
+                   const uint64_t* off, const uint64_t* len, void* const* staging, uint64_t chunk, int ring,
+                   void* const* streams) {
+  if (k <= 0 || !off || !len || !streams || !stage_dev) {
+    ft::set_last_error("ft_h2g_striped: bad arguments");
+    return FT_E_VALUE;
+  }
+  uint8_t* dst = static_cast<uint8_t*>(dst_);
+  const uint8_t* host = static_cast<const uint8_t*>(host_);
+  int cur = 0;
+  CU_RT(cudaGetDevice(&cur));
+  int rc = FT_OK;
+  for (int r = 0; r < k && rc == FT_OK; ++r) {
+    if (off[r] + len[r] > bytes) {
+      ft::set_last_error("ft_h2g_striped: route outside the payload");
+      rc = FT_E_VALUE;
+      break;
+    }
+    cudaStream_t ce = (cudaStream_t)streams[2 * r], fw = (cudaStream_t)streams[2 * r + 1];
+    int sd = stage_dev[r];
+    if (sd == dst_dev || !staging || !staging[r]) {
+      // own link: straight into the destination by CE
+      rc = ft_pcie_copy(dst + off[r], host + off[r], len[r], 1, dst_dev, ce, 0);
+      continue;
+    }
+    if (!chunk || ring <= 0) {
+      ft::set_last_error("ft_h2g_striped: chunk/ring required for staging routes");
+      rc = FT_E_VALUE;
+      break;
+    }
+    cudaSetDevice(sd);
+    std::vector<cudaEvent_t> landed(ring), freed(ring);
+    for (int i = 0; i < ring; ++i) {
+      cudaEventCreateWithFlags(&landed[i], cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&freed[i], cudaEventDisableTiming);
+    }
+    uint8_t* stg = static_cast<uint8_t*>(staging[r]);
+    uint64_t nch = (len[r] + chunk - 1) / chunk;
+    for (uint64_t j = 0; j < nch && rc == FT_OK; ++j) {
+      int slot = (int)(j % ring);
+      uint64_t o = j * chunk, n = len[r] - o < chunk ? len[r] - o : chunk;
+      if (j >= (uint64_t)ring) cudaStreamWaitEvent(ce, freed[slot], 0);  // slot drained by the forward
+      cudaError_t e = cudaMemcpyAsync(stg + (uint64_t)slot * chunk, host + off[r] + o, n, cudaMemcpyHostToDevice, ce);
+      if (e != cudaSuccess) {
+        rc = cuda_fail(e, "staging H2D");
+        break;
+      }
+      cudaEventRecord(landed[slot], ce);
+      cudaStreamWaitEvent(fw, landed[slot], 0);
+      rc = copy_impl(dst + off[r] + o, stg + (uint64_t)slot * chunk, n, sd, fw, 2, 0);  // push over NVLink
+      cudaEventRecord(freed[slot], fw);
+    }
+    for (int i = 0; i < ring; ++i) {
+      cudaEventDestroy(landed[i]);  // destruction is deferred until the event completes
+      cudaEventDestroy(freed[i]);
+    }
+  }
+  cudaSetDevice(cur);
+  return rc;
+}
+
+}  // extern "C"

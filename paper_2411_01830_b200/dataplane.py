@@ -1,0 +1,207 @@
+"""Unified data-passing interface: data index and transfer-plan dispatch —
+mirror of tubesim ``dataplane.py`` over libfaastube (``ft_index_*``,
+``ft_fetch_plan``, ``ft_plan_*``).
+
+Plans carry the reference's fields (method, stages, branches, links, byte
+shares, reserved rates, fill terms) and a handle to the C plan, which the
+device movers in ``tube.py`` execute on real links.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+
+from ._lib import LIB, DuplicateStore, MissingData, enc, json_out
+from .strategies import Strategy
+from .topology import BandwidthMatrix, Topology
+
+LOCAL_LOOKUP_MS = 0.005   # dataplane.py:20
+GLOBAL_LOOKUP_MS = 0.2    # dataplane.py:21
+SYNC_PERIOD_MS = 10.0     # dataplane.py:22
+INTRA_GPU_MAP_MS = 0.05   # dataplane.py:23
+
+__all__ = ["MissingData", "DuplicateStore", "Location", "DataIndexEntry", "DataIndex", "Branch", "Stage",
+           "TransferPlan", "Dataplane", "plan_latency_model", "h2d", "d2h", "nv", "net"]
+
+
+@dataclass(frozen=True)
+class Location:
+    node: int
+    gpu: int | None = None
+
+    @property
+    def on_host(self) -> bool:
+        return self.gpu is None
+
+
+@dataclass
+class DataIndexEntry:
+    data_id: int
+    size_bytes: float
+    location: Location
+    created_ms: float = 0.0
+    producer: str = ""
+    response: bool = False
+    global_visible_ms: float = 0.0
+
+
+class DataIndex:
+    """Two-level mapping: per-node local tables + global table (dataplane.py:55-107)."""
+
+    def __init__(self, sync_period_ms: float = SYNC_PERIOD_MS, local_lookup_ms: float = LOCAL_LOOKUP_MS,
+                 global_lookup_ms: float = GLOBAL_LOOKUP_MS):
+        self.sync_period_ms, self.local_lookup_ms, self.global_lookup_ms = (
+            sync_period_ms, local_lookup_ms, global_lookup_ms)
+        h = C.c_void_p()
+        LIB.ft_index_create(float(sync_period_ms), float(local_lookup_ms), float(global_lookup_ms), C.byref(h))
+        self._h = h
+        self._meta = {}
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            LIB.ft_index_destroy(h)
+            self._h = None
+
+    def unique_id(self) -> int:
+        x = C.c_int64()
+        LIB.ft_index_unique_id(self._h, C.byref(x))
+        return x.value
+
+    def store(self, data_id: int, location: Location, size_bytes: float, now_ms: float, producer: str,
+              response: bool = False) -> DataIndexEntry:
+        vis = C.c_double()
+        gpu = -1 if location.gpu is None else location.gpu
+        LIB.ft_index_store(self._h, int(data_id), location.node, gpu, float(size_bytes), float(now_ms),
+                           enc(producer), int(bool(response)), C.byref(vis))
+        e = DataIndexEntry(data_id, size_bytes, location, now_ms, producer, response, vis.value)
+        self._meta[data_id] = e
+        return e
+
+    def resolve(self, data_id: int, node: int, now_ms: float):
+        """-> (entry, lookup_cost_ms, ready_ms)"""
+        en, eg, cost, ready, size = C.c_int(), C.c_int(), C.c_double(), C.c_double(), C.c_double()
+        LIB.ft_index_resolve(self._h, int(data_id), int(node), float(now_ms), C.byref(en), C.byref(eg),
+                             C.byref(cost), C.byref(ready), C.byref(size))
+        e = self._meta.get(data_id) or DataIndexEntry(data_id, size.value, Location(en.value))
+        e.location = Location(en.value, None if eg.value < 0 else eg.value)
+        return e, cost.value, ready.value
+
+    def drop(self, data_id: int):
+        LIB.ft_index_drop(self._h, int(data_id))
+        self._meta.pop(data_id, None)
+
+    def relocate(self, data_id: int, location: Location):
+        LIB.ft_index_relocate(self._h, int(data_id), location.node, -1 if location.gpu is None else location.gpu)
+        if data_id in self._meta:
+            self._meta[data_id].location = location
+
+
+def h2d(node: int, root: int) -> tuple:
+    return ("h2d", node, root)
+
+
+def d2h(node: int, root: int) -> tuple:
+    return ("d2h", node, root)
+
+
+def nv(u: int, v: int) -> tuple:
+    return ("nv", u, v)
+
+
+def net(a: int, b: int) -> tuple:
+    return ("net", a, b)
+
+
+@dataclass
+class Branch:
+    links: list
+    bytes_share: float
+    cap_gbps: float | None = None
+    reserved_gbps: float | None = None
+    fill_ms: float = 0.0
+    hop_caps: list = field(default_factory=list)
+
+
+@dataclass
+class Stage:
+    branches: list
+    managed: bool = False
+    pinned_bytes: float = 0.0
+
+
+class TransferPlan:
+    """dataplane.py:153-160, backed by a C plan (``_h``)."""
+
+    def __init__(self, handle):
+        self._h = handle
+        d = json_out("ft_plan_json", handle)
+        self.method = d["method"]
+        self.size_bytes = d["size_bytes"]
+        self.claimed_func = d["claimed_func"]
+        self.note = d["note"]
+        self.stages = [Stage([Branch([tuple(l) for l in b["links"]], b["bytes_share"], b["cap_gbps"],
+                                     b["reserved_gbps"], b["fill_ms"], b["hop_caps"]) for b in s["branches"]],
+                             s["managed"], s["pinned_bytes"]) for s in d["stages"]]
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            LIB.ft_plan_destroy(h)
+            self._h = None
+
+    @property
+    def fixed_ms(self) -> float:
+        f = C.c_double()
+        LIB.ft_plan_method(self._h, None, C.byref(f), None)
+        return f.value
+
+    @fixed_ms.setter
+    def fixed_ms(self, value: float):
+        LIB.ft_plan_add_fixed_ms(self._h, float(value) - self.fixed_ms)
+
+    def to_dict(self) -> dict:
+        return json_out("ft_plan_json", self._h)
+
+
+class Dataplane:
+    """Builds transfer plans (dataplane.py:163-348)."""
+
+    def __init__(self, topo: Topology, strategy: Strategy, matrix: BandwidthMatrix, chunk_bytes: float,
+                 intra_gpu_map_ms: float = INTRA_GPU_MAP_MS):
+        self.topo, self.strategy, self.matrix = topo, strategy, matrix
+        self.chunk_bytes, self.intra_gpu_map_ms = chunk_bytes, intra_gpu_map_ms
+        s = strategy.to_c()
+        h = C.c_void_p()
+        LIB.ft_plane_create(topo.handle, C.byref(s), matrix.handle, float(chunk_bytes), float(intra_gpu_map_ms),
+                            C.byref(h))
+        self._h = h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            LIB.ft_plane_destroy(h)
+            self._h = None
+
+    def fetch_plan(self, entry_loc: Location, dest: Location, size_bytes: float) -> TransferPlan:
+        """dataplane.py:176-186"""
+        h = C.c_void_p()
+        LIB.ft_fetch_plan(self._h, entry_loc.node, -1 if entry_loc.gpu is None else entry_loc.gpu, dest.node,
+                          -1 if dest.gpu is None else dest.gpu, float(size_bytes), C.byref(h))
+        return TransferPlan(h)
+
+    def release_claim(self, plan: TransferPlan):
+        """dataplane.py:346-348"""
+        LIB.ft_release_claim(self._h, plan._h)
+
+
+def plan_latency_model(plan: TransferPlan) -> float:
+    """dataplane.py:351-369"""
+    x = C.c_double()
+    LIB.ft_plan_latency(plan._h, C.byref(x))
+    return x.value
+
+
+assert math.isfinite(INTRA_GPU_MAP_MS)
