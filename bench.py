@@ -1,0 +1,400 @@
+#!/usr/bin/env python
+"""FaaSTube-on-B200 benchmark (BASELINE.json metric: "H2G/G2G pass GB/s &
+p99 latency vs PCIe/NVLink peak; workflow req/s").
+
+Headline workload (config 1): a 2-function pipeline — the
+producer gFunc stores its 64 MiB fp16 output, the consumer gFunc fetches it
+into its own input buffer, through the Listing-1 API (FaaSTube.store /
+FaaSTube.fetch). One step = one such pass. At N=1 both functions share GPU 0;
+under torchrun each rank runs its own pipeline on its GPU (weak scaling,
+replicas — the data path has no collective).
+
+  value  : payload bytes delivered / device time, inputs resident in HBM
+  e2e    : same pass through the public API with the producer's input coming
+           from pinned host memory (tube.fetch of a host object) and the
+           consumer's digest read back to the host, wall-clocked
+  roofline: the dominant kernel (k_copy_bulk, TMA bulk copy) vs measured HBM
+  cpu_baseline / --impl reference: the reference's CPU host-memory path
+           (oracle/host_path.py — infless_plus: store into host shared
+           memory, fetch out of it) on the host cores
+
+Extras: h2g (config 2 at k=1: 1 GiB pinned -> GPU over the copy engine, vs
+the live-measured CE peak) and a same-GPU size sweep (config 3 at 1 GPU:
+zero-copy handoff latency and copy-into-input bandwidth, p50/p99).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+MIB = 1 << 20
+PAYLOAD_SHAPE = (32, 1024, 1024)          # fp16 -> 64 MiB (config 1)
+METRIC = "H2G/G2G pass GB/s & p99 latency vs PCIe/NVLink peak; workflow req/s"
+L2_FLUSH_BYTES = 256 * MIB
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-sample-s", type=float, default=10.0)
+    ap.add_argument("--no-extras", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def nearest_rank(sorted_vals, pct):
+    import math
+    return sorted_vals[max(1, math.ceil(pct / 100.0 * len(sorted_vals))) - 1]   # simcore.py:247-252
+
+
+# ----------------------------------------------------------------- CPU path
+def cpu_host_path(sample_s: float, nbytes: int, threads: int | None = None) -> dict:
+    """The reference's CPU host-memory path (oracle port), bounded sample."""
+    import numpy as np
+    from oracle.host_path import HostMemoryStore
+    hs = HostMemoryStore(threads=threads)
+    rng = np.random.default_rng(0)
+    payload = rng.integers(0, 256, nbytes, dtype=np.uint8)
+    out = np.empty(nbytes, dtype=np.uint8)
+    times = []
+    t_end = time.perf_counter() + sample_s
+    for i in range(3):  # warm-up
+        did = hs.unique_id()
+        hs.store(did, payload)
+        hs.fetch(did, out)
+        hs.drop(did)
+    while time.perf_counter() < t_end or len(times) < 3:
+        did = hs.unique_id()
+        t0 = time.perf_counter()
+        hs.store(did, payload)          # producer output -> host shared memory
+        hs.fetch(did, out)              # host shared memory -> consumer input
+        times.append(time.perf_counter() - t0)
+        hs.drop(did)
+    assert np.array_equal(out, payload)
+    hs.close()
+    times.sort()
+    return {"pass_ms_p50": nearest_rank(times, 50) * 1e3, "pass_ms_p99": nearest_rank(times, 99) * 1e3,
+            "gbps": nbytes / statistics.mean(times) / 1e9, "passes": len(times), "threads": hs.threads}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    nbytes = 2 * PAYLOAD_SHAPE[0] * PAYLOAD_SHAPE[1] * PAYLOAD_SHAPE[2]
+    threads = len(os.sched_getaffinity(0))
+    per = []
+    for _ in range(args.warmup):
+        cpu_host_path(0.05, nbytes, threads)
+    t_all = time.perf_counter()
+    for _ in range(args.steps):
+        r = cpu_host_path(max(0.2, args.cpu_sample_s / max(1, args.steps)), nbytes, threads)
+        per.append(r)
+    wall = time.perf_counter() - t_all
+    gbps = statistics.mean(r["gbps"] for r in per)
+    p99 = max(r["pass_ms_p99"] for r in per)
+    line = {"metric": METRIC, "value": round(gbps, 4), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(wall / args.steps * 1e3, 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": "config1: 2-function pipeline, 64 MiB fp16 put/get (reference CPU host-memory path)",
+                       "payload_bytes": nbytes, "path": "oracle/host_path.py infless_plus restatement"},
+            "p99_pass_ms": round(p99, 4),
+            "cpu_baseline": {"value": round(gbps, 4), "unit": "GB/s", "cores": threads, "kind": "port",
+                             "sample": f"{sum(r['passes'] for r in per)} store+fetch passes of 64 MiB"},
+            "e2e": {"value": round(gbps, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------- GPU path
+class Clocks:
+    """nvidia-smi sampler during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.out = ""
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                self.out, _ = self.proc.communicate()
+
+    def summary(self) -> dict:
+        rows = [r.split(",") for r in (self.out or "").strip().splitlines() if r.count(",") >= 7]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = sorted(float(r[1]) for r in rows)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[4 + i].strip() == "Active"})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": float(rows[0][2]), "reasons": reasons,
+                "samples": len(rows)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh), "MEASURED_PEAKS.json"
+    except OSError:
+        return {"hbm_gbs": 6650.0}, "fallback (B200_PROFILING.md)"
+
+
+def profile_traffic():
+    """dram bytes per launch of the copy kernel from the committed ncu capture."""
+    p = os.path.join(ROOT, "profiles", "ncu_copy_summary.json")
+    try:
+        with open(p) as fh:
+            return json.load(fh).get("dram_bytes_per_launch")
+    except OSError:
+        return None
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    rank, world, local = dist_env()
+    if world > 1:
+        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+    torch.cuda.set_device(local)
+    g = local
+    from paper_2411_01830_b200 import device as dev
+    from paper_2411_01830_b200.tube import FaaSTube
+
+    tube = FaaSTube("faastube", topology=_single_gpu_topology(g) if world > 1 else None, gpus=[g])
+    gen = torch.Generator(device="cpu").manual_seed(0)
+    x = torch.randn(PAYLOAD_SHAPE, generator=gen).half().to(f"cuda:{g}")   # producer output (in HBM)
+    nbytes = x.nbytes
+    inp = torch.empty_like(x)                                                # consumer input buffer
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=f"cuda:{g}")
+    s = torch.cuda.current_stream(g)
+
+    def one_pass():
+        did = tube.unique_id()
+        tube.store(did, x, producer="producer")
+        tube.fetch(did, device=g, out=inp, consumer="consumer")
+
+    for _ in range(max(3, args.warmup)):
+        flush.fill_(1)
+        one_pass()
+    torch.cuda.synchronize()
+    assert torch.equal(inp.view(torch.uint8), x.view(torch.uint8)), "delivered bytes differ"
+
+    # ---- timed region: K passes, device-timed, L2 flushed before each pass
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = tube.stats["bytes_local"]
+    with Clocks(g) as clk:
+        for i in range(args.steps):
+            flush.fill_(i & 0xFF)                  # inputs < L2: flush between passes
+            starts[i].record(s)
+            one_pass()
+            ends[i].record(s)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    per_ms = sorted(a.elapsed_time(b) for a, b in zip(starts, ends))
+    total_ms = sum(per_ms)
+    copies = (tube.stats["bytes_local"] - launches0) // nbytes
+    gpu_launches = int(copies)                       # one k_copy_bulk per store + one per fetch
+    assert torch.equal(inp.view(torch.uint8), x.view(torch.uint8)), "delivered bytes differ"
+
+    # ---- dominant kernel: k_copy_bulk on the same buffers, CUDA events on its stream
+    kern = []
+    for i in range(args.steps):
+        flush.fill_(i & 0xFF)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(s)
+        dev.copy(inp.data_ptr(), x.data_ptr(), nbytes, g, s, dev.ENGINE_BULK)
+        b.record(s)
+        kern.append((a, b))
+    torch.cuda.synchronize()
+    kern_ms = statistics.mean(a.elapsed_time(b) for a, b in kern)
+    peaks, peak_src = measured_peaks()
+    achieved = 2 * nbytes / (kern_ms * 1e-3) / 1e9   # read + write bytes per launch
+
+    # ---- e2e through the public API with host buffers
+    host_in = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    host_in.copy_(x.view(-1).view(torch.uint8).cpu())
+    prod_out = torch.empty_like(x)
+    fp = dev.Fingerprint(g)
+    e2e = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        d_in = tube.unique_id()
+        tube.store(d_in, host_in, producer="decode")                 # request payload (host)
+        tube.fetch(d_in, device=g, out=prod_out.view(-1).view(torch.uint8), consumer="producer")  # H2G
+        did = tube.unique_id()
+        tube.store(did, prod_out, producer="producer")               # G2G put
+        tube.fetch(did, device=g, out=inp, consumer="consumer")      # G2G get
+        fp.launch(inp.data_ptr(), nbytes, s)
+        digest = fp.value()                                          # D2H of the result
+        if i >= args.warmup:
+            e2e.append(time.perf_counter() - t0)
+    ref_digest = dev.fingerprint_host(host_in)
+    assert digest == ref_digest, "e2e digest mismatch"
+    e2e_gbps = nbytes / statistics.mean(e2e) / 1e9
+
+    # ---- aggregate over ranks (max time)
+    t_tensor = torch.tensor([total_ms, statistics.mean(e2e)], dtype=torch.float64, device=f"cuda:{g}")
+    if world > 1:
+        dist.all_reduce(t_tensor, op=dist.ReduceOp.MAX)
+    total_ms_max, e2e_max = t_tensor.tolist()
+    value = world * args.steps * nbytes / (total_ms_max * 1e-3) / 1e9
+
+    extras = {} if args.no_extras or rank != 0 else run_extras(tube, g, dev, torch)
+
+    if rank == 0:
+        cpu = cpu_host_path(args.cpu_sample_s, nbytes) if world == 1 else None
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(total_ms_max / args.steps, 5), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "config": {"workload": "config1: 2-function pipeline, producer store(64 MiB fp16) -> consumer "
+                                   "fetch(into its input buffer), same GPU per rank",
+                       "payload_bytes": nbytes, "strategy": "faastube", "l2": "flushed (256 MiB write) before each pass",
+                       "parallelism": f"replicas x{world}"},
+            "p50_pass_ms": round(nearest_rank(per_ms, 50), 5), "p99_pass_ms": round(nearest_rank(per_ms, 99), 5),
+            "e2e": {"value": round(world * nbytes / e2e_max / 1e9, 3), "unit": "GB/s",
+                    "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": 16,
+                    "path": "store(host payload) -> fetch H2G -> store -> fetch -> digest D2H"},
+            "roofline": {"bound": "hbm", "kernel": "k_copy_bulk (TMA cp.async.bulk ring)",
+                         "achieved": round(achieved, 1), "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
+                         "frac": round(achieved / peaks.get("hbm_gbs", 6650.0), 4), "traffic": profile_traffic(),
+                         "algorithmic_bytes_per_launch": 2 * nbytes, "kernel_ms": round(kern_ms, 5),
+                         "peak_source": peak_src},
+            "gpu_launches": gpu_launches,
+            "clocks": clk.summary(),
+        }
+        if cpu:
+            line["cpu_baseline"] = {"value": round(cpu["gbps"], 3), "unit": "GB/s", "cores": cpu["threads"],
+                                    "kind": "port", "sample": f"{cpu['passes']} store+fetch passes of 64 MiB "
+                                                              f"through host memory ({args.cpu_sample_s:.0f} s)",
+                                    "p99_pass_ms": round(cpu["pass_ms_p99"], 3)}
+        line.update(extras)
+        print(json.dumps(line), flush=True)
+    tube.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def _single_gpu_topology(g):
+    """Under torchrun each rank drives only its own GPU (CUDA_VISIBLE_DEVICES
+    is not narrowed), so the tube's topology covers devices 0..g."""
+    from paper_2411_01830_b200.topology import build_preset
+    return build_preset("b200", n_gpus=g + 1)
+
+
+def run_extras(tube, g, dev, torch):
+    out = {}
+    # config 2 at k = 1: 1 GiB pinned -> GPU through tube.fetch vs the live CE peak
+    n = 1 << 30
+    host = torch.empty(n, dtype=torch.uint8).pin_memory()
+    host.fill_(7)
+    dst = torch.empty(n, dtype=torch.uint8, device=f"cuda:{g}")
+    s = torch.cuda.current_stream(g)
+    ce = []
+    for _ in range(3):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(s)
+        dev.pcie_copy(dst.data_ptr(), host.data_ptr(), n, True, g, s)
+        b.record(s)
+        b.synchronize()
+        ce.append(a.elapsed_time(b))
+    ce_peak = n / (min(ce) * 1e-3) / 1e9
+    h2g = []
+    for i in range(4):
+        did = tube.unique_id()
+        tube.store(did, host, producer="decode")
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(s)
+        tube.fetch(did, device=g, out=dst, consumer="preproc")
+        b.record(s)
+        b.synchronize()
+        if i:
+            h2g.append(a.elapsed_time(b))
+    h2g_gbps = n / (statistics.mean(h2g) * 1e-3) / 1e9
+    out["h2g"] = {"workload": "config2 at k=1 (one PCIe link): 1 GiB pinned -> GPU via FaaSTube.fetch",
+                  "value": round(h2g_gbps, 3), "unit": "GB/s", "peak": round(ce_peak, 3),
+                  "peak_source": "live: best-of-3 cudaMemcpyAsync 1 GiB pinned H2D", "frac": round(h2g_gbps / ce_peak, 4)}
+    # config 3 at 1 GPU: zero-copy handoff latency and copy-into-input bandwidth, 4 KiB .. 1 GiB
+    sweep = []
+    for lg in range(12, 31, 2):
+        n = 1 << lg
+        xs = torch.empty(n, dtype=torch.uint8, device=f"cuda:{g}").fill_(3)
+        ys = torch.empty_like(xs)
+        reps = 30 if n <= (64 << 20) else 6
+        zc, cp = [], []
+        for r in range(reps + 2):
+            did = tube.unique_id()
+            tube.store(did, xs)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            v = tube.fetch(did, device=g)              # zero-copy view (map only)
+            t1 = time.perf_counter()
+            del v
+            did = tube.unique_id()
+            tube.store(did, xs)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(s)
+            tube.fetch(did, device=g, out=ys)
+            b.record(s)
+            b.synchronize()
+            if r >= 2:
+                zc.append((t1 - t0) * 1e3)
+                cp.append(a.elapsed_time(b))
+        zc.sort()
+        cp.sort()
+        sweep.append({"bytes": n, "zero_copy_ms_p50": round(nearest_rank(zc, 50), 4),
+                      "zero_copy_ms_p99": round(nearest_rank(zc, 99), 4),
+                      "copy_ms_p50": round(nearest_rank(cp, 50), 5), "copy_ms_p99": round(nearest_rank(cp, 99), 5),
+                      "copy_gbps": round(n / (nearest_rank(cp, 50) * 1e-3) / 1e9, 2)})
+    out["g2g_same_gpu_sweep"] = sweep
+    return out
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

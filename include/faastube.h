@@ -173,6 +173,8 @@ int ft_pool_policy_record(ft_pool_policy* p, const char* func, double now_ms, do
 /* shrink: ids of dropped blocks (the physical memory to release)  :151-166 */
 int ft_pool_policy_shrink(ft_pool_policy* p, double now_ms, int64_t* dropped, int cap, int* n);
 int ft_pool_policy_target(ft_pool_policy* p, double now_ms, double* out);                  /* :127-128 */
+/* R_window and last_request of func's histogram (NaN last if none) — the shrink timer engine.py:656-659 */
+int ft_pool_policy_hist(const ft_pool_policy* p, const char* func, double* r_window, double* last);
 /* {"blocks": [[class_bytes, in_use, id]..], "pool_bytes":.., "in_use_bytes":..} */
 int ft_pool_policy_state_json(const ft_pool_policy* p, char* buf, size_t cap, size_t* need);
 #define FT_MAX_CONSUMERS 16
@@ -306,8 +308,9 @@ int ft_fingerprint_host(const void* src, uint64_t bytes, uint64_t out[2]);
 int ft_pcie_copy(void* dst, const void* src, uint64_t bytes, int to_device, int device, void* stream,
                  uint64_t batch_bytes);
 /* host->gFunc striped pass (dataplane.py:203-250 routes):
- * k routes, route i moves [off_i, off_i+len_i) of host_src. Route 0 is the
- * target's own link (CE straight into dst). Route i>0 lands each chunk in
+ * k routes, route i moves [off_i, off_i+len_i) of host_src. A route with
+ * staging[i] == NULL is a direct link (CE straight into dst, e.g. the
+ * target's own root). A route with a staging buffer lands each chunk in
  * staging[i] on stage_dev[i] by CE, then the staging GPU forwards it to dst
  * over NVLink with ft_copy as soon as that chunk's CE op completes (event
  * chained; chunk ring of ring_chunks slots per staging GPU).

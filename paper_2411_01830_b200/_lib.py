@@ -173,6 +173,7 @@ _SIGS = {
     "ft_pool_policy_record": (None, [vp, cstr, dbl, dbl, dbl]),
     "ft_pool_policy_shrink": (None, [vp, dbl, P(i64), C.c_int, P(C.c_int)]),
     "ft_pool_policy_target": (None, [vp, dbl, P(dbl)]),
+    "ft_pool_policy_hist": (None, [vp, cstr, P(dbl), P(dbl)]),
     "ft_pool_policy_state_json": (None, [vp, C.c_char_p, sz, P(sz)]),
     "ft_migration_plan": (None, [P(StoredObjectC), C.c_int, dbl, C.c_int, P(i32), P(i32), C.c_int, P(C.c_int)]),
     "ft_prefetch_back": (None, [P(StoredObjectC), C.c_int, dbl, P(i32), C.c_int, P(C.c_int)]),

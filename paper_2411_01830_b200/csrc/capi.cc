@@ -341,6 +341,13 @@ int ft_pool_policy_shrink(ft_pool_policy* p, double now, int64_t* dropped, int c
   FT_CATCH
 }
 int ft_pool_policy_target(ft_pool_policy* p, double now, double* out) { NEED(p); *out = p->p.target(now); return FT_OK; }
+int ft_pool_policy_hist(const ft_pool_policy* p, const char* func, double* rw, double* last) {
+  NEED(p);
+  const Hist* h = p->p.hists.find(sfunc(func));
+  if (rw) *rw = h ? h->r_window : 0.0;
+  if (last) *last = h && h->has_last ? h->last : none();
+  return FT_OK;
+}
 int ft_pool_policy_state_json(const ft_pool_policy* p, char* buf, size_t cap, size_t* need) {
   NEED(p);
   return emit_json(p->p.state_json(), buf, cap, need);

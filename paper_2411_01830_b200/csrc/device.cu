@@ -815,7 +815,7 @@ int ft_h2g_striped(void* dst_, int dst_dev, const void* host_, uint64_t bytes, i
     }
     cudaStream_t ce = (cudaStream_t)streams[2 * r], fw = (cudaStream_t)streams[2 * r + 1];
     int sd = stage_dev[r];
-    if (sd == dst_dev || !staging || !staging[r]) {
+    if (!staging || !staging[r]) {
       // own link: straight into the destination by CE
       rc = ft_pcie_copy(dst + off[r], host + off[r], len[r], 1, dst_dev, ce, 0);
       continue;

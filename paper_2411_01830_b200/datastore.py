@@ -142,6 +142,12 @@ class MemoryPool:
     def in_use_bytes(self) -> float:
         return self.state()["in_use_bytes"]
 
+    def hist_window(self, func: str):
+        """(R_window, last_request_ms or None) of func's histogram."""
+        rw, last = C.c_double(), C.c_double()
+        LIB.ft_pool_policy_hist(self._h, enc(func), C.byref(rw), C.byref(last))
+        return rw.value, (None if last.value != last.value else last.value)
+
     def histogram(self, func: str) -> "_PolicyHist":
         if func not in self.histograms:
             self.histograms[func] = _PolicyHist(self, func)

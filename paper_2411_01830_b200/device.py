@@ -1,0 +1,226 @@
+"""Device side: elastic VMM pool per GPU + the sm_100a movers (libfaastube).
+
+``DevicePool`` pairs the reference's pool POLICY (``datastore.MemoryPool``,
+datastore.py:91-166: exact size-class reuse, growth, histogram-driven shrink)
+with real memory: each policy block is backed by a ``cuMemCreate`` physical
+allocation mapped into one reserved VA range per GPU, readable/writable from
+every peer GPU and exportable to other processes as a POSIX fd
+("auto-scaling memory pool"). When the policy drops a block
+the physical memory is unmapped and returned to the driver — that is the
+"shrink" the paper measures.
+
+torch is used only for device selection, streams, events and to wrap pool
+memory as tensors (``__cuda_array_interface__``); all bytes move in our
+kernels or on the copy engines.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import threading
+import weakref
+
+import torch
+
+from . import datastore
+from ._lib import LIB
+
+GiB = 1 << 30
+ENGINE_AUTO, ENGINE_BULK, ENGINE_VEC = 0, 1, 2
+
+_TYPESTR = {torch.uint8: "|u1", torch.int8: "|i1", torch.float16: "<f2", torch.bfloat16: "<f2",
+            torch.float32: "<f4", torch.float64: "<f8", torch.int16: "<i2", torch.int32: "<i4",
+            torch.int64: "<i8", torch.bool: "|b1"}
+
+
+def require_cuda():
+    if not torch.cuda.is_available():
+        raise RuntimeError("FaaSTube device path needs a CUDA GPU (no CPU fallback exists)")
+    n = C.c_int()
+    LIB.ft_device_count(C.byref(n))
+    return n.value
+
+
+def stream_ptr(stream: torch.cuda.Stream | None) -> int:
+    return 0 if stream is None else stream.cuda_stream
+
+
+class _Mem:
+    """__cuda_array_interface__ exporter over raw device memory. The owner
+    reference keeps the backing pool block alive while any tensor view lives."""
+
+    def __init__(self, ptr: int, nbytes: int, device: int, owner=None):
+        self.ptr, self.nbytes, self.device, self.owner = ptr, nbytes, device, owner
+        self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
+def as_tensor(ptr: int, nbytes: int, device: int, dtype=torch.uint8, shape=None, owner=None) -> torch.Tensor:
+    """Zero-copy tensor over device memory at ``ptr`` (owner pinned by the view)."""
+    with torch.cuda.device(device):
+        t = torch.as_tensor(_Mem(ptr, nbytes, device, owner), device=f"cuda:{device}")
+    if dtype != torch.uint8:
+        t = t.view(dtype)
+    if shape is not None:
+        t = t.view(shape)
+    return t
+
+
+def copy(dst_ptr: int, src_ptr: int, nbytes: int, device: int, stream=None, engine=ENGINE_AUTO, grid=0):
+    """K1/K3: SM-driven copy on ``device`` (TMA bulk locally, vector engine for peers)."""
+    if engine == ENGINE_AUTO and grid == 0:
+        LIB.ft_copy(C.c_void_p(dst_ptr), C.c_void_p(src_ptr), int(nbytes), int(device), C.c_void_p(stream_ptr(stream)))
+    else:
+        LIB.ft_copy_ex(C.c_void_p(dst_ptr), C.c_void_p(src_ptr), int(nbytes), int(device),
+                       C.c_void_p(stream_ptr(stream)), int(engine), int(grid))
+
+
+def copy_tensor(dst: torch.Tensor, src: torch.Tensor, stream=None, engine=ENGINE_AUTO):
+    assert dst.is_contiguous() and src.is_contiguous() and dst.nbytes == src.nbytes
+    dev = dst.device.index if dst.is_cuda else src.device.index
+    copy(dst.data_ptr(), src.data_ptr(), dst.nbytes, dev, stream, engine)
+
+
+def pcie_copy(dst_ptr: int, src_ptr: int, nbytes: int, to_device: bool, device: int, stream=None, batch_bytes=0):
+    """One PCIe leg on the copy engine (pinned host <-> device)."""
+    LIB.ft_pcie_copy(C.c_void_p(dst_ptr), C.c_void_p(src_ptr), int(nbytes), int(bool(to_device)), int(device),
+                     C.c_void_p(stream_ptr(stream)), int(batch_bytes))
+
+
+class Fingerprint:
+    """Fused integrity digest (u64 sum + xor of index-mixed words)."""
+
+    def __init__(self, device: int):
+        self.device = device
+        self.buf = torch.zeros(2, dtype=torch.int64, device=f"cuda:{device}")
+
+    def launch(self, ptr: int, nbytes: int, stream=None):
+        LIB.ft_fingerprint(C.c_void_p(ptr), int(nbytes), C.c_void_p(self.buf.data_ptr()), int(self.device),
+                           C.c_void_p(stream_ptr(stream)))
+        return self.buf
+
+    def value(self) -> tuple:
+        v = self.buf.cpu().tolist()
+        return tuple(x & 0xFFFFFFFFFFFFFFFF for x in v)
+
+
+def fingerprint_host(buf) -> tuple:
+    """Same digest on host memory (numpy array / bytes / pinned tensor)."""
+    import numpy as np
+    if isinstance(buf, torch.Tensor):
+        buf = buf.contiguous().view(torch.uint8).numpy()
+    a = np.ascontiguousarray(np.frombuffer(buf, dtype=np.uint8) if isinstance(buf, (bytes, bytearray)) else buf)
+    out = (C.c_uint64 * 2)()
+    LIB.ft_fingerprint_host(C.c_void_p(a.ctypes.data), int(a.nbytes), out)
+    return out[0], out[1]
+
+
+class PoolBlock:
+    """A live pool block: policy block + mapped device memory."""
+
+    __slots__ = ("policy_block", "vmm_id", "ptr", "nbytes", "device", "__weakref__")
+
+    def __init__(self, policy_block, vmm_id, ptr, nbytes, device):
+        self.policy_block, self.vmm_id, self.ptr, self.nbytes, self.device = (
+            policy_block, vmm_id, ptr, nbytes, device)
+
+
+class DevicePool:
+    """Elastic VMM-backed store for one GPU, driven by the reference pool policy."""
+
+    def __init__(self, device: int, mode: str = "autoscale", floor_bytes: float = datastore.POOL_FLOOR_BYTES,
+                 native_alloc_ms: float = datastore.NATIVE_ALLOC_MS, va_bytes: int = 256 * GiB,
+                 physical_bytes: float | None = None):
+        require_cuda()
+        self.device = device
+        if physical_bytes is None:
+            physical_bytes = float(torch.cuda.get_device_properties(device).total_memory)
+        self.policy = datastore.MemoryPool(device, mode, floor_bytes, native_alloc_ms, physical_bytes)
+        h = C.c_void_p()
+        LIB.ft_vmm_pool_create(int(device), int(va_bytes), C.byref(h))
+        self._h = h
+        self._mapped = {}  # policy block id -> (vmm id, ptr, bytes)
+        self._lock = threading.Lock()
+        self.grow_events = 0
+
+    def close(self):
+        h = getattr(self, "_h", None)
+        if h:
+            torch.cuda.synchronize(self.device)
+            LIB.ft_vmm_pool_destroy(h)
+            self._h = None
+
+    __del__ = close
+
+    def allocate(self, nbytes: int) -> PoolBlock:
+        """Policy decision (reuse exact class or grow) + physical mapping on growth."""
+        with self._lock:
+            b, _model_ms = self.policy.allocate(max(1, nbytes))
+            m = self._mapped.get(b.block_id)
+            if m is None:
+                vid, ptr = C.c_uint64(), C.c_void_p()
+                LIB.ft_vmm_block_map(self._h, int(b.class_bytes), C.byref(vid), C.byref(ptr))
+                m = self._mapped[b.block_id] = (vid.value, ptr.value, b.class_bytes)
+                self.grow_events += 1
+            return PoolBlock(b, m[0], m[1], m[2], self.device)
+
+    def free(self, blk: PoolBlock):
+        with self._lock:
+            self.policy.free(blk.policy_block)
+            if self.policy.mode == "none":
+                self._unmap(blk.policy_block.block_id)
+
+    def record(self, func: str, now_ms: float, size: float, concurrency: float):
+        with self._lock:
+            self.policy.histogram(func).record_execution(now_ms, size, concurrency)
+
+    def shrink(self, now_ms: float) -> int:
+        """Apply the policy's shrink; unmap what it drops. Returns bytes released."""
+        with self._lock:
+            dropped = self.policy.shrink(now_ms)
+            return sum(self._unmap(b.block_id) for b in dropped)
+
+    def _unmap(self, block_id) -> int:
+        m = self._mapped.pop(block_id, None)
+        if m is None:
+            return 0
+        torch.cuda.synchronize(self.device)  # no in-flight kernel may touch it
+        LIB.ft_vmm_block_unmap(self._h, m[0])
+        return m[2]
+
+    def export_fd(self, blk: PoolBlock) -> int:
+        fd = C.c_int()
+        LIB.ft_vmm_block_export_fd(self._h, blk.vmm_id, C.byref(fd))
+        return fd.value
+
+    def stats(self) -> dict:
+        mapped, reserved, n = C.c_uint64(), C.c_uint64(), C.c_int()
+        LIB.ft_vmm_pool_stats(self._h, C.byref(mapped), C.byref(reserved), C.byref(n))
+        return {"mapped_bytes": mapped.value, "reserved_va": reserved.value, "blocks": n.value,
+                "policy_pool_bytes": self.policy.pool_bytes, "in_use_bytes": self.policy.in_use_bytes}
+
+
+class ImportedBlock:
+    """A pool block exported by another process and mapped here (zero copy)."""
+
+    def __init__(self, device: int, fd: int, nbytes: int):
+        ptr, h = C.c_void_p(), C.c_uint64()
+        LIB.ft_vmm_import_fd(int(device), int(fd), int(nbytes), C.byref(ptr), C.byref(h))
+        self.device, self.nbytes, self.ptr, self._h = device, nbytes, ptr.value, h.value
+        self._fin = weakref.finalize(self, LIB.ft_vmm_unimport, h.value)
+
+    def tensor(self, dtype=torch.uint8, shape=None) -> torch.Tensor:
+        return as_tensor(self.ptr, self.nbytes, self.device, dtype, shape, owner=self)
+
+    def close(self):
+        self._fin()
+
+
+def send_fd(sock, fd: int, tag: int = 0):
+    LIB.ft_fd_send(sock.fileno(), int(fd), int(tag))
+
+
+def recv_fd(sock) -> tuple:
+    fd, tag = C.c_int(), C.c_uint64()
+    LIB.ft_fd_recv(sock.fileno(), C.byref(fd), C.byref(tag))
+    return fd.value, tag.value

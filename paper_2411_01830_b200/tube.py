@@ -1,0 +1,501 @@
+"""FaaSTube put/get API on B200 — the drop-in for the reference's
+data-passing path (Listing 1):
+
+    tube = FaaSTube()                       # one per box (the daemon)
+    did = tube.unique_id()                  # FaaSTube.unique_id
+    tube.store(did, output, response=0)     # FaaSTube.store(index, output, response)
+    x = tube.fetch(did, device=1, out=buf)  # FaaSTube.fetch(index, input)
+
+Control decisions (index, transfer method, NVLink paths, PCIe routes and
+byte shares, pool reuse/growth/shrink, per-function PCIe rates) come from
+libfaastube's restatement of the reference (bit-identical to tubesim);
+bytes move on real links:
+
+* same GPU      — zero-copy view of the pool block, or one TMA-bulk copy into
+                  the caller's input buffer (``out=``);
+* GPU -> GPU    — SM-driven copy over NVLink (peer-mapped pool memory);
+* host -> GPU   — copy-engine DMA on the target's own PCIe link plus, per
+                  extra PCIe root, CE into a staging GPU and an NVLink forward
+                  kernel into the target, chunk-pipelined (dataplane.py:203-250);
+* GPU -> host   — copy-engine DMA;
+* host-oriented strategies (infless_plus, deepplan_plus) stage GPU->GPU
+  through pinned host memory, as the reference's baselines do.
+
+Stream semantics: ``store`` orders after the producer's current stream;
+``fetch`` enqueues on the consumer device's current stream, so consumer
+kernels issued afterwards see the data. No call synchronizes the host
+unless the caller asks for a host tensor.
+"""
+
+from __future__ import annotations
+
+import heapq
+import itertools
+import math
+import threading
+import time
+import weakref
+
+import torch
+
+from . import datastore, device as dev
+from .dataplane import DataIndex, Dataplane, Location
+from .pcie_sched import BATCH_CHUNKS, CHUNK_BYTES
+from .stage_sched import StageArbiter
+from .strategies import Strategy, strategy_preset
+from .topology import Topology, build_preset, snapshot_matrix
+
+__all__ = ["FaaSTube"]
+
+_ALIGN = 256  # stripe boundaries (bytes)
+
+
+class _Obj:
+    __slots__ = ("did", "nbytes", "dtype", "shape", "gpu", "block", "host", "producer", "remaining", "ready",
+                 "pins", "retired", "response_host", "response_event", "stored_at", "__weakref__")
+
+    def __init__(self, did, nbytes, dtype, shape, gpu, producer, consumers, now):
+        self.did, self.nbytes, self.dtype, self.shape, self.gpu = did, nbytes, dtype, shape, gpu
+        self.block = None      # device.PoolBlock when on a GPU
+        self.host = None       # pinned host tensor when in host memory
+        self.producer = producer
+        self.remaining = consumers
+        self.ready = None      # cuda event: bytes in place
+        self.pins = 0          # live zero-copy views
+        self.retired = False
+        self.response_host = None
+        self.response_event = None
+        self.stored_at = now
+
+
+class FaaSTube:
+    def __init__(self, strategy: str | Strategy = "faastube", topology: Topology | None = None,
+                 pcie_gbps: float = 55.0, chunk_bytes: int = CHUNK_BYTES, batch_chunks: int = BATCH_CHUNKS,
+                 pool_floor_bytes: float = datastore.POOL_FLOOR_BYTES, node: int = 0, map_ms: float = 0.05,
+                 gpus: list | None = None):
+        n = dev.require_cuda()
+        self.topo = topology or build_preset("b200", n_gpus=n, pcie_gbps=pcie_gbps)
+        if self.topo.gpu_count > n:
+            raise ValueError(f"topology has {self.topo.gpu_count} GPUs but only {n} are visible")
+        self.strategy = strategy_preset(strategy) if isinstance(strategy, str) else strategy
+        self.node = node
+        self.chunk_bytes, self.batch_chunks = int(chunk_bytes), int(batch_chunks)
+        self.matrix = snapshot_matrix(self.topo)
+        self.plane = Dataplane(self.topo, self.strategy, self.matrix, float(chunk_bytes), map_ms)
+        self.index = DataIndex()
+        self.gpus = list(gpus) if gpus is not None else self.topo.gpus()   # GPUs this process drives
+        for a in self.gpus:
+            for b in self.gpus:
+                if a != b and self.topo.nvlink_gbps(a, b) > 0:
+                    try:
+                        dev.LIB.ft_peer_enable(a, b)
+                    except Exception:  # noqa: BLE001 - fabric without P2P: plans avoid NVLink
+                        pass
+        self.pools = {}
+        if self.strategy.gpu_store():
+            for g in self.gpus:
+                self.pools[g] = dev.DevicePool(g, self.strategy.pool, pool_floor_bytes)
+        roots = self.topo.roots()
+        bw_all = self.topo.pcie_gbps * len(roots)  # engine.py:186-190
+        self.arbiters = {d: StageArbiter(bw_all, batch_chunks, chunk_bytes) for d in ("h2d", "d2h")}
+        self._t0 = time.perf_counter()
+        self._objs: dict[int, _Obj] = {}
+        self._lock = threading.RLock()
+        self._side = {g: torch.cuda.Stream(g) for g in self.gpus}        # store / forward stream
+        self._ce = {g: [torch.cuda.Stream(g) for _ in range(2)] for g in self.gpus}  # copy-engine streams
+        self._staging = {}
+        self._pending_release = []   # (event, plan): NVLink claims held until the copy lands
+        self._shrink_due = []        # heap of (due_ms, gpu)
+        self._managed_ids = itertools.count(1)
+        self.stats = {"stores": 0, "fetches": 0, "bytes_h2d": 0, "bytes_d2h": 0, "bytes_nvlink": 0,
+                      "bytes_local": 0, "zero_copy": 0}
+
+    # ------------------------------------------------------------ helpers
+    def now_ms(self) -> float:
+        return (time.perf_counter() - self._t0) * 1e3
+
+    def _loc(self, gpu) -> Location:
+        return Location(self.node, gpu)
+
+    def _reap(self):
+        """Release NVLink claims of transfers that have landed; run due shrinks."""
+        keep = []
+        for ev, plan in self._pending_release:
+            if ev.query():
+                self.plane.release_claim(plan)
+            else:
+                keep.append((ev, plan))
+        self._pending_release = keep
+        now = self.now_ms()
+        while self._shrink_due and self._shrink_due[0][0] <= now:
+            _, g = heapq.heappop(self._shrink_due)
+            if g in self.pools:
+                self.pools[g].shrink(now)
+
+    def _stream(self, g):
+        return torch.cuda.current_stream(g)
+
+    @staticmethod
+    def _stripes(nbytes, shares):
+        """Integer byte ranges for fractional shares (dataplane.py:215/288)."""
+        total = sum(shares)
+        bounds = [0]
+        acc = 0.0
+        for s in shares[:-1]:
+            acc += s
+            b = int(nbytes * (acc / total)) // _ALIGN * _ALIGN
+            bounds.append(max(bounds[-1], min(nbytes, b)))
+        bounds.append(nbytes)
+        return [(bounds[i], bounds[i + 1] - bounds[i]) for i in range(len(shares))]
+
+    def _pinned(self, nbytes) -> torch.Tensor:
+        return torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+
+    def _staging_buf(self, g, nbytes) -> torch.Tensor:
+        buf = self._staging.get(g)
+        if buf is None or buf.nbytes < nbytes:
+            buf = self._staging[g] = torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{g}")
+        return buf
+
+    # ------------------------------------------------------------ API
+    def unique_id(self) -> int:
+        """FaaSTube.unique_id (dataplane.py:69-70)."""
+        return self.index.unique_id()
+
+    def empty(self, shape, dtype=torch.float16, device: int = 0) -> torch.Tensor:
+        """An output buffer carved from the tube's pool: storing it is zero-copy."""
+        nbytes = math.prod(shape) * torch.empty((), dtype=dtype).element_size()
+        blk = self.pools[device].allocate(nbytes)
+        t = dev.as_tensor(blk.ptr, nbytes, device, dtype, tuple(shape), owner=blk)
+        t._ft_block = blk  # noqa: SLF001 - marks pool-backed outputs
+        return t
+
+    def store(self, data_id: int, output: torch.Tensor, response: bool = False, producer: str = "func",
+              consumers: int = 1) -> None:
+        """FaaSTube.store(index, output, response) — engine.py:342-423."""
+        with self._lock:
+            self._reap()
+            if data_id in self._objs:
+                from ._lib import DuplicateStore
+                raise DuplicateStore(f"data id {data_id} already stored")
+            t = output.contiguous() if not output.is_contiguous() else output
+            nbytes = t.nbytes
+            now = self.now_ms()
+            obj = _Obj(data_id, nbytes, t.dtype, tuple(t.shape), None, producer, consumers, now)
+            if t.is_cuda and self.strategy.gpu_store():
+                g = t.device.index
+                obj.gpu = g
+                pool = self.pools[g]
+                blk = getattr(t, "_ft_block", None)
+                live_here = sum(1 for o in self._objs.values() if o.producer == producer and o.gpu == g
+                                and not o.retired)
+                if blk is not None and blk.ptr == t.data_ptr():
+                    obj.block = blk                      # zero-copy store of a pool-backed output
+                    ev = torch.cuda.Event()
+                    ev.record(self._stream(g))
+                    obj.ready = ev
+                else:
+                    blk = pool.allocate(nbytes)          # datastore.py:130-144
+                    obj.block = blk
+                    s = self._side[g]
+                    s.wait_stream(self._stream(g))       # after the producer's kernels
+                    dev.copy(blk.ptr, t.data_ptr(), nbytes, g, s)
+                    t.record_stream(s)
+                    ev = torch.cuda.Event()
+                    ev.record(s)
+                    obj.ready = ev
+                    self.stats["bytes_local"] += nbytes
+                pool.record(producer, now, nbytes, live_here + 1)   # datastore.py:51-62
+                self._push_shrink(g, producer, now)
+                self.index.store(data_id, self._loc(g), nbytes, now, producer, response)
+                if response:
+                    self._respond(obj)
+            elif t.is_cuda:
+                # host-oriented store: the output lands in host memory (engine.py:361-381)
+                g = t.device.index
+                host = self._pinned(nbytes)
+                s = self._ce[g][0]
+                s.wait_stream(self._stream(g))
+                dev.pcie_copy(host.data_ptr(), t.data_ptr(), nbytes, False, g, s)
+                t.record_stream(s)
+                ev = torch.cuda.Event()
+                ev.record(s)
+                obj.host, obj.ready = host, ev
+                self.stats["bytes_d2h"] += nbytes
+                self.index.store(data_id, self._loc(None), nbytes, now, producer, response)
+            else:
+                # cFunc output / request payload: host resident (pinned for DMA)
+                host = t.view(-1).view(torch.uint8) if t.is_pinned() else self._pinned(nbytes).copy_(
+                    t.reshape(-1).view(torch.uint8))
+                obj.host = host
+                self.index.store(data_id, self._loc(None), nbytes, now, producer, response)
+            self._objs[data_id] = obj
+            self.stats["stores"] += 1
+
+    def fetch(self, data_id: int, device: int | None = None, out: torch.Tensor | None = None,
+              consumer: str = "func", slo_ms: float | None = None, infer_ms: float | None = None) -> torch.Tensor:
+        """FaaSTube.fetch(index, input) — dataplane.py:176-186 + engine.py:440-511.
+
+        ``device=None`` fetches into host memory. With ``out`` the bytes land
+        in the caller's buffer (Listing-1 semantics); without it a same-GPU
+        fetch is a zero-copy view of the stored block."""
+        with self._lock:
+            self._reap()
+            obj = self._objs.get(data_id)
+            entry, _lookup_ms, _ready = self.index.resolve(data_id, self.node, self.now_ms())
+            if obj is None:
+                from ._lib import MissingData
+                raise MissingData(f"data id {data_id} has no live payload")
+            if out is not None:
+                if not out.is_contiguous() or out.nbytes != obj.nbytes:
+                    raise ValueError("out must be contiguous with exactly the stored byte count")
+                device = out.device.index if out.is_cuda else None
+            src = entry.location
+            dst = self._loc(device)
+            plan = self.plane.fetch_plan(src, dst, obj.nbytes)
+            result = self._execute(obj, plan, src, dst, out, slo_ms, infer_ms)
+            self.stats["fetches"] += 1
+            self._consumed(obj)
+            return result
+
+    def release(self, data_id: int):
+        """Drop a stored object regardless of remaining consumers."""
+        with self._lock:
+            obj = self._objs.get(data_id)
+            if obj is not None:
+                obj.remaining = 0
+                self._retire(obj)
+
+    def response(self, data_id: int) -> torch.Tensor:
+        """Host copy of a ``store(..., response=True)`` output (waits for it)."""
+        obj = self._objs.get(data_id)
+        if obj is None or obj.response_host is None:
+            from ._lib import MissingData
+            raise MissingData(f"no response for data id {data_id}")
+        obj.response_event.synchronize()
+        return obj.response_host.view(obj.dtype).view(obj.shape)
+
+    def close(self):
+        for g in self.gpus:
+            torch.cuda.synchronize(g)
+        self._objs.clear()
+        for p in self.pools.values():
+            p.close()
+
+    # ------------------------------------------------------------ internals
+    def _push_shrink(self, g, func, now):
+        """Shrink timer at last_request + R_window (engine.py:656-659)."""
+        r_window, last = self.pools[g].policy.hist_window(func)
+        heapq.heappush(self._shrink_due, ((last if last is not None else now) + r_window, g))
+
+    def _respond(self, obj: _Obj):
+        g = obj.gpu
+        host = self._pinned(obj.nbytes)
+        s = self._ce[g][1]
+        s.wait_event(obj.ready)
+        dev.pcie_copy(host.data_ptr(), obj.block.ptr, obj.nbytes, False, g, s)
+        ev = torch.cuda.Event()
+        ev.record(s)
+        obj.response_host, obj.response_event = host, ev
+        self.stats["bytes_d2h"] += obj.nbytes
+
+    def _consumed(self, obj: _Obj):
+        obj.remaining -= 1
+        if obj.remaining <= 0:
+            self._retire(obj)
+
+    def _retire(self, obj: _Obj):
+        """engine.py:667-679: last consumer done -> drop index entry, free block."""
+        if obj.retired:
+            return
+        obj.retired = True
+        self.index.drop(obj.did)
+        self._objs.pop(obj.did, None)
+        self._maybe_free(obj)
+
+    def _maybe_free(self, obj: _Obj):
+        if obj.block is not None and obj.pins == 0 and obj.retired:
+            blk, obj.block = obj.block, None
+            # later writers of this block must order after our readers
+            ev = torch.cuda.Event()
+            ev.record(self._stream(blk.device))
+            self._side[blk.device].wait_event(ev)
+            self.pools[blk.device].free(blk)
+            self._push_shrink(blk.device, obj.producer, self.now_ms())
+
+    def _unpin(self, ref):
+        obj = ref()
+        if obj is None:
+            return
+        with self._lock:
+            obj.pins -= 1
+            self._maybe_free(obj)
+
+    def _view(self, obj: _Obj) -> torch.Tensor:
+        obj.pins += 1
+        t = dev.as_tensor(obj.block.ptr, obj.nbytes, obj.gpu, obj.dtype, obj.shape, owner=obj.block)
+        weakref.finalize(t, self._unpin, weakref.ref(obj))
+        self.stats["zero_copy"] += 1
+        return t
+
+    def _execute(self, obj, plan, src, dst, out, slo_ms, infer_ms):
+        m = plan.method
+        if m == "intra_gpu":
+            if src.on_host:  # host -> host shared memory
+                if out is None:
+                    return obj.host.view(obj.dtype).view(obj.shape)
+                out.view(-1).view(torch.uint8).copy_(obj.host)
+                return out
+            s = self._stream(dst.gpu)
+            s.wait_event(obj.ready)
+            if out is None:
+                return self._view(obj)
+            dev.copy(out.data_ptr(), obj.block.ptr, obj.nbytes, dst.gpu, s)
+            self.stats["bytes_local"] += obj.nbytes
+            return out
+        if m == "inter_gpu":
+            return self._inter_gpu(obj, plan, src, dst, out)
+        if m == "host_gpu":
+            if dst.on_host:
+                return self._gpu_to_host(obj, plan, out)
+            return self._host_to_gpu(obj, plan, dst, out, slo_ms, infer_ms)
+        from ._lib import NotSupported
+        raise NotSupported("inter-node transfers need a multi-node deployment (SURVEY §8f row 4)")
+
+    def _out(self, obj, gpu, out):
+        if out is not None:
+            return out
+        return torch.empty(obj.nbytes, dtype=torch.uint8, device=f"cuda:{gpu}").view(obj.dtype).view(obj.shape)
+
+    def _inter_gpu(self, obj, plan, src, dst, out):
+        res = self._out(obj, dst.gpu, out)
+        s = self._stream(dst.gpu)
+        s.wait_event(obj.ready)
+        if len(plan.stages) == 2:
+            # host-oriented baseline: D2H to host, then H2D (dataplane.py:265-272)
+            host = self._pinned(obj.nbytes)
+            ce = self._ce[src.gpu][0]
+            ce.wait_event(obj.ready)
+            dev.pcie_copy(host.data_ptr(), obj.block.ptr if obj.block else obj.host.data_ptr(), obj.nbytes,
+                          False, src.gpu, ce)
+            ev = torch.cuda.Event()
+            ev.record(ce)
+            s.wait_event(ev)
+            dev.pcie_copy(res.data_ptr(), host.data_ptr(), obj.nbytes, True, dst.gpu, s)
+            host.record_stream(s) if hasattr(host, "record_stream") else None
+            self.stats["bytes_d2h"] += obj.nbytes
+            self.stats["bytes_h2d"] += obj.nbytes
+            return res
+        br = plan.stages[0].branches
+        ranges = self._stripes(obj.nbytes, [b.bytes_share for b in br])
+        for b, (off, n) in zip(br, ranges):
+            if n == 0:
+                continue
+            hops = _hops(b.links)
+            if len(hops) == 1:
+                # direct NVLink: pull over the peer mapping on the consumer's stream
+                dev.copy(res.data_ptr() + off, obj.block.ptr + off, n, dst.gpu, s, dev.ENGINE_VEC)
+            else:
+                self._relay(hops, obj.block.ptr + off, res.data_ptr() + off, n, s)
+            self.stats["bytes_nvlink"] += n
+        ev = torch.cuda.Event()
+        ev.record(s)
+        if plan.claimed_func:
+            self._pending_release.append((ev, plan))
+        self._hold_until(obj, ev)
+        return res
+
+    def _relay(self, hops, src_ptr, dst_ptr, n, s):
+        """Multi-hop NVLink branch (non-uniform fabrics): store-and-forward in
+        chunks through each intermediate GPU's staging buffer."""
+        chunk = self.chunk_bytes
+        cur = src_ptr
+        for u, v in hops[:-1]:
+            buf = self._staging_buf(v, n)
+            for o in range(0, n, chunk):
+                dev.copy(buf.data_ptr() + o, cur + o, min(chunk, n - o), v, s, dev.ENGINE_VEC)
+            cur = buf.data_ptr()
+        u, v = hops[-1]
+        for o in range(0, n, chunk):
+            dev.copy(dst_ptr + o, cur + o, min(chunk, n - o), v, s, dev.ENGINE_VEC)
+
+    def _hold_until(self, obj, ev):
+        """Keep the source block alive until a reader's event completes."""
+        if obj.block is not None:
+            self._side[obj.block.device].wait_event(ev)
+
+    def _host_to_gpu(self, obj, plan, dst, out, slo_ms, infer_ms):
+        res = self._out(obj, dst.gpu, out)
+        stage = plan.stages[0]
+        br = stage.branches
+        ranges = self._stripes(obj.nbytes, [b.bytes_share for b in br])
+        s = self._stream(dst.gpu)
+        if obj.ready is not None:
+            s.wait_event(obj.ready)
+        host_ptr = obj.host.data_ptr()
+        events = []
+        for b, (off, n) in zip(br, ranges):
+            if n == 0:
+                continue
+            stage_gpu = _staging_gpu(b.links, dst.gpu)
+            if stage_gpu == dst.gpu:
+                ce = self._ce[dst.gpu][0]
+                ce.wait_stream(s)
+                dev.pcie_copy(res.data_ptr() + off, host_ptr + off, n, True, dst.gpu, ce)
+            else:
+                ce, fw = self._ce[stage_gpu]
+                ce.wait_stream(s)
+                ring = 4
+                stg = self._staging_buf(stage_gpu, ring * self.chunk_bytes)
+                import ctypes as C
+                streams = (C.c_void_p * 2)(ce.cuda_stream, fw.cuda_stream)
+                offs, lens = (C.c_uint64 * 1)(0), (C.c_uint64 * 1)(n)
+                sd = (C.c_int32 * 1)(stage_gpu)
+                stgp = (C.c_void_p * 1)(stg.data_ptr())
+                dev.LIB.ft_h2g_striped(C.c_void_p(res.data_ptr() + off), dst.gpu, C.c_void_p(host_ptr + off), n,
+                                       1, sd, offs, lens, stgp, self.chunk_bytes, ring, streams)
+                ce = fw
+                self.stats["bytes_nvlink"] += n
+            ev = torch.cuda.Event()
+            ev.record(ce)
+            events.append(ev)
+            self.stats["bytes_h2d"] += n
+        for ev in events:
+            s.wait_event(ev)
+        return res
+
+    def _gpu_to_host(self, obj, plan, out):
+        res = out if out is not None else self._pinned(obj.nbytes).view(obj.dtype).view(obj.shape)
+        g = obj.gpu
+        ce = self._ce[g][0]
+        ce.wait_event(obj.ready)
+        dev.pcie_copy(res.data_ptr(), obj.block.ptr, obj.nbytes, False, g, ce)
+        ev = torch.cuda.Event()
+        ev.record(ce)
+        ev.synchronize()
+        self.stats["bytes_d2h"] += obj.nbytes
+        return res
+
+
+def _hops(links):
+    """GPU hops of an NVLink branch from its link ids (dataplane.py:128-133)."""
+    hops = []
+    pending = None
+    for l in links:
+        if l[0] == "nv":
+            hops.append((l[1], l[2]))
+        elif l[0] == "nvp_out":
+            pending = l[1]
+        elif l[0] == "nvp_in":
+            hops.append((pending, l[1]))
+    return hops
+
+
+def _staging_gpu(links, target):
+    """First GPU a host->GPU branch lands on (its PCIe root's staging GPU)."""
+    for l in links:
+        if l[0] == "nvp_out":
+            return l[1]
+        if l[0] == "nv":
+            return l[1]
+    return target

@@ -1,0 +1,160 @@
+"""GPU parity of the put/get API (tube.FaaSTube) against the oracle's CPU
+host-memory path: for every transfer method the consumer must receive
+exactly the bytes the reference path (store into host memory, fetch out of
+it — oracle/host_path.py) delivers, compared as uint8."""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+MB = 1 << 20
+
+
+@pytest.fixture(scope="module")
+def tube():
+    from paper_2411_01830_b200.tube import FaaSTube
+    t = FaaSTube("faastube", pool_floor_bytes=0.0)
+    yield t
+    t.close()
+
+
+def payload(seed=0, shape=(32, 1024, 1024), dtype=torch.float16, device="cuda:0"):
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    return torch.randn(shape, generator=g).to(dtype).to(device)
+
+
+def oracle_bytes(t: torch.Tensor) -> np.ndarray:
+    from oracle.host_path import HostMemoryStore
+    hs = HostMemoryStore(threads=4)
+    did = hs.unique_id()
+    hs.store(did, t.detach().cpu().contiguous().view(torch.uint8).numpy())
+    out = hs.fetch(did)
+    hs.close()
+    return out
+
+
+def as_u8(t):
+    return t.detach().contiguous().view(torch.uint8).reshape(-1).cpu().numpy()
+
+
+def test_config1_same_gpu_copy_into_input(tube):
+    x = payload(0)                                   # 64 MiB fp16, seed 0
+    did = tube.unique_id()
+    tube.store(did, x, producer="producer")
+    inp = torch.empty_like(x)
+    got = tube.fetch(did, device=0, out=inp, consumer="consumer")
+    torch.cuda.synchronize()
+    assert got.data_ptr() == inp.data_ptr()
+    assert np.array_equal(as_u8(got), oracle_bytes(x))
+
+
+def test_config1_zero_copy_view(tube):
+    x = payload(1)
+    did = tube.unique_id()
+    tube.store(did, x)
+    v = tube.fetch(did, device=0)
+    assert v.shape == x.shape and v.dtype == x.dtype
+    assert torch.equal(v.view(torch.uint8), x.view(torch.uint8))
+    assert tube.stats["zero_copy"] >= 1
+
+
+def test_zero_copy_store_from_pool_output(tube):
+    out = tube.empty((1024, 1024), torch.float16, device=0)
+    out.copy_(payload(2, (1024, 1024)))
+    did = tube.unique_id()
+    before = tube.stats["bytes_local"]
+    tube.store(did, out)
+    assert tube.stats["bytes_local"] == before               # no copy on store
+    got = tube.fetch(did, device=0, out=torch.empty_like(out))
+    assert torch.equal(got.view(torch.uint8), out.view(torch.uint8))
+
+
+@pytest.mark.parametrize("n", [1, 4095, 4096, 2 * 10**6 + 1, 64 * MB])
+def test_host_to_gpu(tube, n):
+    rng = np.random.default_rng(n)
+    host = torch.from_numpy(rng.integers(0, 256, n, dtype=np.uint8))
+    did = tube.unique_id()
+    tube.store(did, host, producer="decode")                  # cFunc output: host resident
+    got = tube.fetch(did, device=0, consumer="preproc")
+    torch.cuda.synchronize()
+    assert np.array_equal(as_u8(got), oracle_bytes(host))
+
+
+def test_gpu_to_host_and_response(tube):
+    x = payload(3, (4, 1024, 1024))
+    did = tube.unique_id()
+    tube.store(did, x, response=True, consumers=2)
+    assert np.array_equal(as_u8(tube.response(did)), oracle_bytes(x))
+    h = tube.fetch(did, device=None)
+    assert not h.is_cuda and np.array_equal(as_u8(h), oracle_bytes(x))
+    tube.fetch(did, device=0, out=torch.empty_like(x))        # second consumer retires it
+    from paper_2411_01830_b200 import MissingData
+    with pytest.raises(MissingData):
+        tube.fetch(did, device=0)
+
+
+def test_multiple_consumers_and_retire(tube):
+    x = payload(4, (2, 1024, 1024))
+    did = tube.unique_id()
+    tube.store(did, x, consumers=3)
+    outs = [tube.fetch(did, device=0, out=torch.empty_like(x)) for _ in range(3)]
+    for o in outs:
+        assert torch.equal(o.view(torch.uint8), x.view(torch.uint8))
+    from paper_2411_01830_b200 import MissingData
+    with pytest.raises(MissingData):
+        tube.fetch(did, device=0)
+
+
+def test_duplicate_store(tube):
+    from paper_2411_01830_b200 import DuplicateStore
+    x = payload(5, (16,))
+    did = tube.unique_id()
+    tube.store(did, x, consumers=2)
+    with pytest.raises(DuplicateStore):
+        tube.store(did, x)
+    tube.release(did)
+
+
+def test_pool_reuse_no_growth(tube):
+    x = payload(6, (8, 1024, 1024))
+    pool = tube.pools[0]
+    did = tube.unique_id()
+    tube.store(did, x)
+    tube.fetch(did, device=0, out=torch.empty_like(x))
+    grown = pool.grow_events
+    for _ in range(5):
+        did = tube.unique_id()
+        tube.store(did, x)
+        tube.fetch(did, device=0, out=torch.empty_like(x))
+    assert pool.grow_events == grown                           # same class served from the cache
+
+
+def test_view_pins_block(tube):
+    """A zero-copy view keeps its block from being reused by later stores."""
+    x = payload(7, (1024, 1024))
+    did = tube.unique_id()
+    tube.store(did, x)
+    v = tube.fetch(did, device=0)
+    y = payload(8, (1024, 1024))
+    for _ in range(3):
+        d2 = tube.unique_id()
+        tube.store(d2, y)
+        tube.fetch(d2, device=0, out=torch.empty_like(y))
+    torch.cuda.synchronize()
+    assert torch.equal(v.view(torch.uint8), x.view(torch.uint8))
+    del v
+
+
+@pytest.mark.parametrize("strategy", ["infless_plus", "faastube_star", "deepplan_plus"])
+def test_baseline_strategies_bit_exact(strategy):
+    from paper_2411_01830_b200.tube import FaaSTube
+    t = FaaSTube(strategy)
+    x = payload(9, (8, 1024, 1024))
+    did = t.unique_id()
+    t.store(did, x)
+    got = t.fetch(did, device=0, out=torch.empty_like(x))
+    torch.cuda.synchronize()
+    assert np.array_equal(as_u8(got), oracle_bytes(x))
+    t.close()
