@@ -29,6 +29,7 @@ unless the caller asks for a host tensor.
 
 from __future__ import annotations
 
+import ctypes as C
 import heapq
 import itertools
 import math
@@ -101,6 +102,7 @@ class FaaSTube:
         self._t0 = time.perf_counter()
         self._objs: dict[int, _Obj] = {}
         self._lock = threading.RLock()
+        self._sched_lock = threading.Lock()
         self._side = {g: torch.cuda.Stream(g) for g in self.gpus}        # store / forward stream
         self._ce = {g: [torch.cuda.Stream(g) for _ in range(2)] for g in self.gpus}  # copy-engine streams
         self._staging = {}
@@ -253,10 +255,20 @@ class FaaSTube:
             src = entry.location
             dst = self._loc(device)
             plan = self.plane.fetch_plan(src, dst, obj.nbytes)
-            result = self._execute(obj, plan, src, dst, out, slo_ms, infer_ms)
+            managed = (plan.method == "host_gpu" and not dst.on_host and self.strategy.pcie_sched
+                       and plan.stages[0].managed)
+            if not managed:
+                result = self._execute(obj, plan, src, dst, out, slo_ms, infer_ms)
+                self.stats["fetches"] += 1
+                self._consumed(obj)
+                return result
+            res = self._out(obj, dst.gpu, out)
+        # managed PCIe stage: paced outside the tube lock so tenants run concurrently
+        self._managed_h2g(obj, plan, dst, res, consumer, slo_ms, infer_ms)
+        with self._lock:
             self.stats["fetches"] += 1
             self._consumed(obj)
-            return result
+        return res
 
     def release(self, data_id: int):
         """Drop a stored object regardless of remaining consumers."""
@@ -424,45 +436,111 @@ class FaaSTube:
         if obj.block is not None:
             self._side[obj.block.device].wait_event(ev)
 
+    def _issue_h2g(self, b, host_ptr, dst_ptr, n, dst_gpu, after: torch.cuda.Stream) -> torch.cuda.Event:
+        """One branch's byte range host -> dst_gpu: CE straight in on the target's
+        own root, or CE into the staging GPU's chunk ring + NVLink forward."""
+        stage_gpu = _staging_gpu(b.links, dst_gpu)
+        if stage_gpu == dst_gpu:
+            ce = self._ce[dst_gpu][0]
+            ce.wait_stream(after)
+            dev.pcie_copy(dst_ptr, host_ptr, n, True, dst_gpu, ce, self.batch_chunks * self.chunk_bytes)
+            last = ce
+        else:
+            ce, fw = self._ce[stage_gpu]
+            ce.wait_stream(after)
+            ring = 4
+            stg = self._staging_buf(stage_gpu, ring * self.chunk_bytes)
+            streams = (C.c_void_p * 2)(ce.cuda_stream, fw.cuda_stream)
+            offs, lens = (C.c_uint64 * 1)(0), (C.c_uint64 * 1)(n)
+            sd = (C.c_int32 * 1)(stage_gpu)
+            stgp = (C.c_void_p * 1)(stg.data_ptr())
+            dev.LIB.ft_h2g_striped(C.c_void_p(dst_ptr), dst_gpu, C.c_void_p(host_ptr), n, 1, sd, offs, lens, stgp,
+                                   self.chunk_bytes, ring, streams)
+            last = fw
+            self.stats["bytes_nvlink"] += n
+        ev = torch.cuda.Event()
+        ev.record(last)
+        self.stats["bytes_h2d"] += n
+        return ev
+
     def _host_to_gpu(self, obj, plan, dst, out, slo_ms, infer_ms):
         res = self._out(obj, dst.gpu, out)
-        stage = plan.stages[0]
-        br = stage.branches
+        br = plan.stages[0].branches
         ranges = self._stripes(obj.nbytes, [b.bytes_share for b in br])
         s = self._stream(dst.gpu)
         if obj.ready is not None:
             s.wait_event(obj.ready)
-        host_ptr = obj.host.data_ptr()
-        events = []
-        for b, (off, n) in zip(br, ranges):
-            if n == 0:
-                continue
-            stage_gpu = _staging_gpu(b.links, dst.gpu)
-            if stage_gpu == dst.gpu:
-                ce = self._ce[dst.gpu][0]
-                ce.wait_stream(s)
-                dev.pcie_copy(res.data_ptr() + off, host_ptr + off, n, True, dst.gpu, ce)
-            else:
-                ce, fw = self._ce[stage_gpu]
-                ce.wait_stream(s)
-                ring = 4
-                stg = self._staging_buf(stage_gpu, ring * self.chunk_bytes)
-                import ctypes as C
-                streams = (C.c_void_p * 2)(ce.cuda_stream, fw.cuda_stream)
-                offs, lens = (C.c_uint64 * 1)(0), (C.c_uint64 * 1)(n)
-                sd = (C.c_int32 * 1)(stage_gpu)
-                stgp = (C.c_void_p * 1)(stg.data_ptr())
-                dev.LIB.ft_h2g_striped(C.c_void_p(res.data_ptr() + off), dst.gpu, C.c_void_p(host_ptr + off), n,
-                                       1, sd, offs, lens, stgp, self.chunk_bytes, ring, streams)
-                ce = fw
-                self.stats["bytes_nvlink"] += n
-            ev = torch.cuda.Event()
-            ev.record(ce)
-            events.append(ev)
-            self.stats["bytes_h2d"] += n
+        events = [self._issue_h2g(b, obj.host.data_ptr() + off, res.data_ptr() + off, n, dst.gpu, s)
+                  for b, (off, n) in zip(br, ranges) if n]
         for ev in events:
             s.wait_event(ev)
         return res
+
+    # -------------------------------------------------- live bandwidth-share scheduler
+    def _deliver_due(self, arb: StageArbiter):
+        """Fire every armed batch boundary that is due (engine.py:628-646)."""
+        while True:
+            t, key = arb.next_event()
+            if t is None or t > self.now_ms():
+                return
+            arb.boundary(t, key)
+
+    def _managed_h2g(self, obj, plan, dst, res, consumer, slo_ms, infer_ms):
+        """A scheduler-managed PCIe stage (engine.py:537-575): the stage's
+        demand enters the SLO partition; its bytes move in batch-sized pieces
+        (batch = 5 x 2 MB, pcie_sched.py:14-15) split over the branches by
+        byte share, issued at the arbiter's rate; rate changes land on batch
+        boundaries. Returns when every byte has landed."""
+        arb = self.arbiters["h2d"]
+        br = plan.stages[0].branches
+        ranges = [r for r in self._stripes(obj.nbytes, [b.bytes_share for b in br])]
+        per_branch_cap = min(min(b.hop_caps) for b in br)
+        slo = slo_ms if slo_ms else 1e9                   # engine.py:546-547
+        infer = infer_ms if infer_ms is not None else 0.0
+        key = f"m{next(self._managed_ids)}"
+        s = self._stream(dst.gpu)
+        if obj.ready is not None:
+            s.wait_event(obj.ready)
+        with self._sched_lock:
+            now = self.now_ms()
+            arb.start(now, key, float(obj.nbytes), slo, infer, now, per_branch_cap, len(br))
+        batch = self.batch_chunks * self.chunk_bytes
+        done = [0] * len(br)
+        inflight = []
+        next_t = None
+        host_ptr, dst_ptr = obj.host.data_ptr(), res.data_ptr()
+        while any(done[i] < ranges[i][1] for i in range(len(br))):
+            with self._sched_lock:
+                self._deliver_due(arb)
+                st = arb.stage(key)
+                nxt, _ = arb.next_event()
+            now = self.now_ms()
+            if not st["started"] or st["rate"] <= 0:
+                _sleep_until(nxt if nxt is not None else now + 0.05, self.now_ms)
+                continue
+            dur = batch / (st["rate"] * 1e6)              # ms per batch at the stage rate
+            if next_t is None:
+                next_t = now
+            if now < next_t - dur:                          # one batch of lookahead keeps the CE busy
+                _sleep_until(min(next_t - dur, nxt if nxt is not None else next_t), self.now_ms)
+                continue
+            while len(inflight) >= 3:
+                inflight.pop(0).synchronize()
+            evs = []
+            for i, b in enumerate(br):
+                off, n = ranges[i]
+                take = min(n - done[i], int(batch * n / obj.nbytes) // _ALIGN * _ALIGN or n - done[i])
+                if take <= 0:
+                    continue
+                evs.append(self._issue_h2g(b, host_ptr + off + done[i], dst_ptr + off + done[i], take, dst.gpu, s))
+                done[i] += take
+            inflight.extend(evs)
+            next_t += dur
+        for ev in inflight:
+            ev.synchronize()
+        with self._sched_lock:
+            arb.finish(self.now_ms(), key)
+        self.stats["managed_stages"] = self.stats.get("managed_stages", 0) + 1
 
     def _gpu_to_host(self, obj, plan, out):
         res = out if out is not None else self._pinned(obj.nbytes).view(obj.dtype).view(obj.shape)
@@ -475,6 +553,16 @@ class FaaSTube:
         ev.synchronize()
         self.stats["bytes_d2h"] += obj.nbytes
         return res
+
+
+def _sleep_until(t_ms, clock):
+    """Sub-millisecond wait: sleep for the bulk, spin the last 0.2 ms."""
+    while True:
+        left = t_ms - clock()
+        if left <= 0:
+            return
+        if left > 0.3:
+            time.sleep((left - 0.2) / 1e3)
 
 
 def _hops(links):
