@@ -186,13 +186,15 @@ __global__ void __launch_bounds__(kBulkThreads) k_copy_bulk(uint8_t* __restrict_
   for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
     mbar_wait(&full[s], phase);
     bulk_s2g(dst + t * tile, smem + (size_t)s * tile, tile_len(t));
-    if (next < ntiles) {
-      // refill this slot once the store just issued has read it out; the
-      // other STAGES-1 slots keep their loads in flight meanwhile.
-      bulk_wait_read<0>();
+    if (t != blockIdx.x && next < ntiles) {
+      // refill the PREVIOUS slot: its store was issued one tile ago, so waiting
+      // for all but the newest store group to finish reading smem rarely
+      // stalls, and the store just issued keeps streaming meanwhile.
+      const int ps = s == 0 ? STAGES - 1 : s - 1;
+      bulk_wait_read<1>();
       uint32_t len = tile_len(next);
-      mbar_expect_tx(&full[s], len);
-      bulk_g2s(smem + (size_t)s * tile, src + next * tile, len, &full[s]);
+      mbar_expect_tx(&full[ps], len);
+      bulk_g2s(smem + (size_t)ps * tile, src + next * tile, len, &full[ps]);
       next += gridDim.x;
     }
     if (++s == STAGES) {

@@ -135,16 +135,28 @@ class Stage:
 class TransferPlan:
     """dataplane.py:153-160, backed by a C plan (``_h``)."""
 
+    _METHODS = ("intra_gpu", "inter_gpu", "host_gpu", "inter_node")
+
     def __init__(self, handle):
         self._h = handle
-        d = json_out("ft_plan_json", handle)
-        self.method = d["method"]
-        self.size_bytes = d["size_bytes"]
-        self.claimed_func = d["claimed_func"]
-        self.note = d["note"]
-        self.stages = [Stage([Branch([tuple(l) for l in b["links"]], b["bytes_share"], b["cap_gbps"],
-                                     b["reserved_gbps"], b["fill_ms"], b["hop_caps"]) for b in s["branches"]],
-                             s["managed"], s["pinned_bytes"]) for s in d["stages"]]
+        m = C.c_int()
+        LIB.ft_plan_method(handle, C.byref(m), None, None)
+        self.method = self._METHODS[m.value]
+        self._d = None  # full plan parsed lazily (the same-GPU fast path never needs it)
+
+    def _full(self):
+        if self._d is None:
+            d = json_out("ft_plan_json", self._h)
+            d["stages"] = [Stage([Branch([tuple(l) for l in b["links"]], b["bytes_share"], b["cap_gbps"],
+                                         b["reserved_gbps"], b["fill_ms"], b["hop_caps"]) for b in s["branches"]],
+                                 s["managed"], s["pinned_bytes"]) for s in d["stages"]]
+            self._d = d
+        return self._d
+
+    size_bytes = property(lambda self: self._full()["size_bytes"])
+    claimed_func = property(lambda self: self._full()["claimed_func"])
+    note = property(lambda self: self._full()["note"])
+    stages = property(lambda self: self._full()["stages"])
 
     def __del__(self):
         h = getattr(self, "_h", None)

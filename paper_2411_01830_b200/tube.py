@@ -105,6 +105,10 @@ class FaaSTube:
         self._sched_lock = threading.Lock()
         self._side = {g: torch.cuda.Stream(g) for g in self.gpus}        # store / forward stream
         self._ce = {g: [torch.cuda.Stream(g) for _ in range(2)] for g in self.gpus}  # copy-engine streams
+        # per-transfer CE stream pairs (PCIe leg, NVLink forward): concurrent tenants'
+        # DMA must not queue FIFO behind each other on one stream
+        self._ce_pairs = {g: [(torch.cuda.Stream(g), torch.cuda.Stream(g)) for _ in range(8)] for g in self.gpus}
+        self._ce_rr = itertools.count()
         self._staging = {}
         self._pending_release = []   # (event, plan): NVLink claims held until the copy lands
         self._shrink_due = []        # heap of (due_ms, gpu)
@@ -436,17 +440,21 @@ class FaaSTube:
         if obj.block is not None:
             self._side[obj.block.device].wait_event(ev)
 
-    def _issue_h2g(self, b, host_ptr, dst_ptr, n, dst_gpu, after: torch.cuda.Stream) -> torch.cuda.Event:
+    def _pair(self, g, slot=None):
+        pairs = self._ce_pairs[g]
+        return pairs[(next(self._ce_rr) if slot is None else slot) % len(pairs)]
+
+    def _issue_h2g(self, b, host_ptr, dst_ptr, n, dst_gpu, after: torch.cuda.Stream, slot=None) -> torch.cuda.Event:
         """One branch's byte range host -> dst_gpu: CE straight in on the target's
         own root, or CE into the staging GPU's chunk ring + NVLink forward."""
         stage_gpu = _staging_gpu(b.links, dst_gpu)
         if stage_gpu == dst_gpu:
-            ce = self._ce[dst_gpu][0]
+            ce = self._pair(dst_gpu, slot)[0]
             ce.wait_stream(after)
-            dev.pcie_copy(dst_ptr, host_ptr, n, True, dst_gpu, ce, self.batch_chunks * self.chunk_bytes)
+            dev.pcie_copy(dst_ptr, host_ptr, n, True, dst_gpu, ce, 0)   # one DMA op per range
             last = ce
         else:
-            ce, fw = self._ce[stage_gpu]
+            ce, fw = self._pair(stage_gpu, slot)
             ce.wait_stream(after)
             ring = 4
             stg = self._staging_buf(stage_gpu, ring * self.chunk_bytes)
@@ -498,6 +506,7 @@ class FaaSTube:
         slo = slo_ms if slo_ms else 1e9                   # engine.py:546-547
         infer = infer_ms if infer_ms is not None else 0.0
         key = f"m{next(self._managed_ids)}"
+        slot = next(self._ce_rr)                             # this stage's own CE streams
         s = self._stream(dst.gpu)
         if obj.ready is not None:
             s.wait_event(obj.ready)
@@ -532,7 +541,8 @@ class FaaSTube:
                 take = min(n - done[i], int(batch * n / obj.nbytes) // _ALIGN * _ALIGN or n - done[i])
                 if take <= 0:
                     continue
-                evs.append(self._issue_h2g(b, host_ptr + off + done[i], dst_ptr + off + done[i], take, dst.gpu, s))
+                evs.append(self._issue_h2g(b, host_ptr + off + done[i], dst_ptr + off + done[i], take, dst.gpu, s,
+                                           slot))
                 done[i] += take
             inflight.extend(evs)
             next_t += dur

@@ -560,6 +560,50 @@ def gen_arbiter(docs):
     return {"scenarios": scen}
 
 
+def gen_harness(docs):
+    """Workflow presets (as data for the package), arrival traces, per-request
+    draws, placement and SLO calibration — the live runtime's inputs."""
+    from tubesim import workflow
+    presets = {n: workflow.preset_workflow(n).to_dict() for n in workflow.PRESET_NAMES}
+    pkg = os.path.join(os.path.dirname(os.path.dirname(OUT)), "paper_2411_01830_b200", "workflows.json")
+    with open(pkg, "w") as fh:
+        json.dump(presets, fh, indent=1, sort_keys=True)
+    traces = []
+    for pattern in ("sporadic", "periodic", "bursty"):
+        for rate in (5.0, 20.0):
+            for dur in (1.0, 5.0):
+                for seed in (0, 1, 2):
+                    tr = harness.gen_workload(pattern, rate, dur, seed)
+                    traces.append({"pattern": pattern, "rate": rate, "duration": dur, "seed": seed,
+                                   "times": tr.timestamps_ms})
+    reqs = []
+    for name in workflow.PRESET_NAMES:
+        wf = workflow.preset_workflow(name)
+        tr = harness.gen_workload("bursty", 20.0, 2.0, 3)
+        specs = harness.build_requests(wf, tr, 3, rid_start=100)
+        reqs.append({"workflow": name, "requests": [
+            {"rid": s.rid, "arrival": s.arrival_ms, "fired": sorted(list(map(list, s.fired))),
+             "edge_bytes": sorted([[a, b, v] for (a, b), v in s.edge_bytes.items()]),
+             "input": s.input_bytes, "response": s.response_bytes} for s in specs]})
+    calib = []
+    for tname in ("b200_k8", "b200_k4", "dgx_v100", "dgx_a100"):
+        t = topology.from_dict(docs[tname])
+        for name in workflow.PRESET_NAMES:
+            for limit in (1, 2):
+                wf = workflow.preset_workflow(name)
+                try:
+                    pl = workflow.place(wf, t, {}, limit)
+                except Exception as exc:  # noqa: BLE001
+                    calib.append({"topology": tname, "workflow": name, "limit": limit, "error": err_name(exc)})
+                    continue
+                rt = harness.calibrate_slo(wf, t, pl, engine_mod.EngineConfig(), 1.5)
+                calib.append({"topology": tname, "workflow": name, "limit": limit,
+                              "placement": {k: list(v) for k, v in pl.mapping.items()},
+                              "runtime": rt, "slo": wf.slo_ms,
+                              "funcs": {f.id: [f.slo_ms, f.infer_latency_ms] for f in wf.functions}})
+    return {"traces": traces, "requests": reqs, "calibration": calib}
+
+
 def main():
     docs = topo_docs()
     parts = {
@@ -570,6 +614,7 @@ def main():
         "datastore": gen_datastore,
         "dataplane": lambda: gen_dataplane(docs),
         "arbiter": lambda: gen_arbiter(docs),
+        "harness": lambda: gen_harness(docs),
     }
     only = sys.argv[1:] or list(parts)
     for name in only:

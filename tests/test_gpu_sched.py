@@ -1,6 +1,12 @@
 """Live per-function PCIe bandwidth-share scheduler (isolation quotas,
-engine.py:537-646 driven on real copy engines): concurrent host->GPU fetches
-from two functions share one PCIe link by the SLO partition; bytes stay exact."""
+engine.py:537-646 driven on real copy engines).
+
+Semantics inherited from the reference: every demand gets its Rate_least =
+bytes / (slo - infer) and the idle bandwidth goes to the tightest slack —
+which, because the reference's slack keeps the full demand size
+(pcie_sched.py:49-55), is the EARLIEST arrival. The isolation guarantee is
+the SPEC invariant "every feasible demand completes by slo - infer absent
+oversubscription" (SPEC pcie_sched invariants)."""
 
 import threading
 import time
@@ -27,40 +33,52 @@ def test_managed_fetch_bit_exact_and_logged():
     tube.close()
 
 
-def test_isolation_tight_slo_wins():
+def _contend(strategy, n_loose=3, loose_bytes=1000 * MB, tight_bytes=256 * MB, window_ms=10.0):
+    """3 loose tenants start first; then a tight tenant needing tight_bytes/window."""
     from paper_2411_01830_b200.tube import FaaSTube
-    tube = FaaSTube("faastube", pool_floor_bytes=0.0)
-    n = 512 * MB
+    tube = FaaSTube(strategy, pool_floor_bytes=0.0)
     rng = np.random.default_rng(12)
-    payload = {k: torch.from_numpy(rng.integers(0, 256, n, dtype=np.uint8)).pin_memory() for k in "AB"}
+    names = [f"L{i}" for i in range(n_loose)] + ["T"]
+    payload = {k: torch.from_numpy(rng.integers(0, 256, loose_bytes if k != "T" else tight_bytes,
+                                                dtype=np.uint8)).pin_memory() for k in names}
     ids = {}
-    for k in "AB":
+    for k in names:
         ids[k] = tube.unique_id()
         tube.store(ids[k], payload[k], producer=f"decode{k}")
-    # warm the staging / CE path once
     w = tube.unique_id()
-    tube.store(w, payload["A"][: 16 * MB].clone(), producer="warm")
+    tube.store(w, payload["T"][: 16 * MB].clone(), producer="warm")
     tube.fetch(w, device=0)
     torch.cuda.synchronize()
-    slo = {"A": (25.0, 5.0), "B": (5000.0, 5.0)}      # A needs 512MB/20ms = 25.6 GB/s, B ~0.1 GB/s
     out, t_done = {}, {}
-    barrier = threading.Barrier(2)
+    go = threading.Event()
 
-    def run(k):
-        barrier.wait()
+    def run(k, delay):
+        go.wait()
+        time.sleep(delay)
         t0 = time.perf_counter()
-        out[k] = tube.fetch(ids[k], device=0, consumer=f"gfunc{k}", slo_ms=slo[k][0], infer_ms=slo[k][1])
+        # loose tenants: least 0.5 GB/s (batch boundaries every 20 ms, so a
+        # starved stage picks up idle bandwidth quickly — engine.py:135-142)
+        slo, infer = (window_ms + 5.0, 5.0) if k == "T" else (2005.0, 5.0)
+        out[k] = tube.fetch(ids[k], device=0, consumer=f"g{k}", slo_ms=slo, infer_ms=infer)
         torch.cuda.synchronize()
-        t_done[k] = time.perf_counter() - t0
+        t_done[k] = (time.perf_counter() - t0) * 1e3
 
-    th = [threading.Thread(target=run, args=(k,)) for k in "AB"]
+    th = [threading.Thread(target=run, args=(k, 0.0 if k != "T" else 0.004)) for k in names]
     for t in th:
         t.start()
+    go.set()
     for t in th:
         t.join()
-    for k in "AB":
+    for k in names:
         assert torch.equal(out[k].cpu(), payload[k]), k
-    # the tight-SLO function gets its least rate plus all idle bandwidth: it must
-    # finish clearly before the loose one on a single shared link
-    assert t_done["A"] < t_done["B"], t_done
     tube.close()
+    return t_done
+
+
+def test_isolation_tight_tenant_meets_its_window():
+    managed = _contend("faastube")
+    shared = _contend("faastube_star")     # no PCIe scheduler: native sharing among 4 tenants
+    # the tight tenant needs 256 MB / 10 ms = 25.6 GB/s; 4-way native sharing of a
+    # ~55 GB/s link gives it ~14 GB/s (~18 ms); the partition guarantees its least rate
+    assert managed["T"] < 0.8 * shared["T"], (managed, shared)
+    assert managed["T"] < 16.0, managed
