@@ -418,6 +418,65 @@ def run_extras(tube, g, dev, torch):
                       "copy_ms_p50": round(nearest_rank(cp, 50), 5), "copy_ms_p99": round(nearest_rank(cp, 99), 5),
                       "copy_gbps": round(n / (nearest_rank(cp, 50) * 1e-3) / 1e9, 2)})
     out["g2g_same_gpu_sweep"] = sweep
+    try:
+        out.update(run_workflows())
+    except Exception as exc:  # noqa: BLE001 - extras never hide the headline line
+        out["workflows_error"] = repr(exc)
+    return out
+
+
+def run_workflows(dur_s=2.0):
+    """Configs 4 and 5 on the live runtime (one GPU): the reference's traces,
+    placement and SLOs; FaaSTube vs the INFless+ host-memory baseline."""
+    from paper_2411_01830_b200 import workload
+    from paper_2411_01830_b200.runtime import Runtime
+    from paper_2411_01830_b200.tube import FaaSTube
+
+    def one(strategy, jobs_fn, compute):
+        tube = FaaSTube(strategy)
+        jobs = jobs_fn(tube)
+        rt = Runtime(tube, compute=compute)
+        t0 = time.perf_counter()
+        res = rt.run(jobs, dur_s, drain_s=60)
+        res["wall_s"] = round(time.perf_counter() - t0, 3)
+        res["pool_timeline_points"] = len(rt.pool_timeline)
+        tube.close()
+        return res
+
+    def traffic(tube):
+        wf = workload.preset_workflow("traffic")
+        where = workload.place(wf, tube.topo, {}, limit=len(wf.gfuncs()))
+        workload.calibrate_slo(wf, tube.topo, where, 1.5)
+        reqs = workload.build_requests(wf, workload.gen_workload("bursty", 10.0, dur_s, 0), 0)
+        return [(wf, where, reqs)]
+
+    def pairs(tube):
+        jobs, occ = [], {}
+        for i, mb in enumerate((1, 4, 16, 32, 64, 128, 256, 512)):
+            wf = workload.Workflow.parse({
+                "name": f"pair{mb}", "functions": [
+                    {"id": f"prod{mb}", "kind": "gFunc", "compute_latency_ms": 2.0},
+                    {"id": f"cons{mb}", "kind": "gFunc", "compute_latency_ms": 2.0}],
+                "edges": [{"src": f"prod{mb}", "dst": f"cons{mb}", "size": {"const_mb": mb}}],
+                "input_size": {"const_mb": 1}, "response_size": {"const_mb": 1}})
+            where = workload.place(wf, tube.topo, occ, limit=16)
+            for k, (kind, g) in where.items():
+                if kind == "gpu":
+                    occ[g] = occ.get(g, 0) + 1
+            workload.calibrate_slo(wf, tube.topo, where, 1.5)
+            reqs = workload.build_requests(wf, workload.gen_workload("bursty", 5.0, dur_s, i), i, rid_start=1000 * i)
+            jobs.append((wf, where, reqs))
+        return jobs
+
+    out = {}
+    t4 = {s: one(s, traffic, "model") for s in ("faastube", "infless_plus")}
+    out["config4_traffic"] = {"workload": "traffic DAG (decode->preproc->yolo_det->resnet_ped/veh, p=0.6), "
+                                          "bursty 10 rps, random-init conv models on synthetic 1080p frames",
+                              "faastube": t4["faastube"], "infless_plus": t4["infless_plus"]}
+    t5 = {s: one(s, pairs, "sleep") for s in ("faastube", "infless_plus")}
+    out["config5_multitenant"] = {"workload": "16 functions = 8 producer->consumer pairs, edges 1..512 MB, bursty "
+                                              "5 rps each, elastic VMM pool (floor 300 MB)",
+                                  "faastube": t5["faastube"], "infless_plus": t5["infless_plus"]}
     return out
 
 

@@ -299,6 +299,10 @@ int ft_fd_recv(int sock, int* fd, uint64_t* tag);
 int ft_copy(void* dst, const void* src, uint64_t bytes, int device, void* stream);
 /* same, with explicit engine: 0 auto, 1 TMA bulk, 2 vector ld/st (peer-safe) */
 int ft_copy_ex(void* dst, const void* src, uint64_t bytes, int device, void* stream, int engine, int grid);
+/* TMA-bulk copy with L2 policies: hints bits 0-1 = source, bits 2-3 = destination
+ * (0 evict_normal, 1 evict_first, 2 evict_last) — e.g. a store keeps the pool block
+ * L2-resident (dst evict_last) for a same-GPU fetch that follows.            */
+int ft_copy_hint(void* dst, const void* src, uint64_t bytes, int device, void* stream, uint32_t hints);
 /* position-keyed digest of `bytes` (u64 sum of mixed words + xor), device u64[2] out */
 int ft_fingerprint(const void* src, uint64_t bytes, uint64_t* out_dev, int device, void* stream);
 /* host-side digest of the same definition (for checking against ft_fingerprint) */

@@ -221,6 +221,7 @@ _SIGS = {
     "ft_fd_recv": (None, [C.c_int, P(C.c_int), P(u64)]),
     "ft_copy": (None, [vp, vp, u64, C.c_int, vp]),
     "ft_copy_ex": (None, [vp, vp, u64, C.c_int, vp, C.c_int, C.c_int]),
+    "ft_copy_hint": (None, [vp, vp, u64, C.c_int, vp, C.c_uint32]),
     "ft_fingerprint": (None, [vp, u64, vp, C.c_int, vp]),
     "ft_fingerprint_host": (None, [vp, u64, P(u64)]),
     "ft_pcie_copy": (None, [vp, vp, u64, C.c_int, C.c_int, vp, u64]),

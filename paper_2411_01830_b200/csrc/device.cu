@@ -149,6 +149,32 @@ __device__ __forceinline__ void bulk_s2g(void* gmem, const void* smem, uint32_t 
                : "memory");
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
+// L2 cache-policy variants (createpolicy + .L2::cache_hint): used to keep a
+// freshly stored pool block resident for the consumer's fetch that follows.
+__device__ __forceinline__ uint64_t l2_policy(uint32_t kind) {
+  uint64_t p;
+  if (kind == 1)
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  else if (kind == 2)
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  else
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void bulk_g2s_hint(void* smem, const void* gmem, uint32_t bytes, uint64_t* bar,
+                                              uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(smem)),
+      "l"(gmem), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_s2g_hint(void* gmem, const void* smem, uint32_t bytes, uint64_t pol) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(gmem),
+               "r"(smem_u32(smem)), "r"(bytes), "l"(pol)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
 template <int N>
 __device__ __forceinline__ void bulk_wait_read() {
   asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
@@ -158,10 +184,10 @@ __device__ __forceinline__ void bulk_wait_read() {
 // global->smem->global ring; tiles are dealt round-robin over a persistent
 // grid. Requires 16-byte aligned src/dst and a multiple-of-16 byte count
 // (the host wrapper peels the unaligned head/tail to the vector engine).
-template <int STAGES>
+template <int STAGES, bool HINT>
 __global__ void __launch_bounds__(kBulkThreads) k_copy_bulk(uint8_t* __restrict__ dst,
                                                             const uint8_t* __restrict__ src, uint64_t bytes,
-                                                            uint32_t tile) {
+                                                            uint32_t tile, uint32_t hints) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t full[STAGES];
   if (threadIdx.x == 0) {
@@ -170,6 +196,19 @@ __global__ void __launch_bounds__(kBulkThreads) k_copy_bulk(uint8_t* __restrict_
   }
   __syncthreads();
   if (threadIdx.x != 0) return;
+  uint64_t psrc = 0, pdst = 0;
+  if (HINT) {
+    psrc = l2_policy(hints & 3);
+    pdst = l2_policy((hints >> 2) & 3);
+  }
+  auto load = [&](void* sm, const void* g, uint32_t n, uint64_t* bar) {
+    if (HINT) bulk_g2s_hint(sm, g, n, bar, psrc);
+    else bulk_g2s(sm, g, n, bar);
+  };
+  auto store = [&](void* g, const void* sm, uint32_t n) {
+    if (HINT) bulk_s2g_hint(g, sm, n, pdst);
+    else bulk_s2g(g, sm, n);
+  };
   const uint64_t ntiles = (bytes + tile - 1) / tile;
   auto tile_len = [&](uint64_t t) -> uint32_t {
     uint64_t off = t * tile;
@@ -179,13 +218,13 @@ __global__ void __launch_bounds__(kBulkThreads) k_copy_bulk(uint8_t* __restrict_
   for (int s = 0; s < STAGES && next < ntiles; ++s, next += gridDim.x) {
     uint32_t len = tile_len(next);
     mbar_expect_tx(&full[s], len);
-    bulk_g2s(smem + (size_t)s * tile, src + next * tile, len, &full[s]);
+    load(smem + (size_t)s * tile, src + next * tile, len, &full[s]);
   }
   uint32_t phase = 0;
   int s = 0;
   for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
     mbar_wait(&full[s], phase);
-    bulk_s2g(dst + t * tile, smem + (size_t)s * tile, tile_len(t));
+    store(dst + t * tile, smem + (size_t)s * tile, tile_len(t));
     if (t != blockIdx.x && next < ntiles) {
       // refill the PREVIOUS slot: its store was issued one tile ago, so waiting
       // for all but the newest store group to finish reading smem rarely
@@ -194,7 +233,7 @@ __global__ void __launch_bounds__(kBulkThreads) k_copy_bulk(uint8_t* __restrict_
       bulk_wait_read<1>();
       uint32_t len = tile_len(next);
       mbar_expect_tx(&full[ps], len);
-      bulk_g2s(smem + (size_t)ps * tile, src + next * tile, len, &full[ps]);
+      load(smem + (size_t)ps * tile, src + next * tile, len, &full[ps]);
       next += gridDim.x;
     }
     if (++s == STAGES) {
@@ -307,9 +346,9 @@ int dev_sms(int device) {
 // resident per SM. Defaults from the sweep in profiles/r01 (override with
 // FT_BULK_STAGES / FT_BULK_TILE / FT_BULK_CTAS_PER_SM for tuning runs).
 struct BulkCfg {
-  int stages = 3;
-  uint32_t tile = 32768;
-  int ctas_per_sm = 2;
+  int stages = 2;
+  uint32_t tile = 16384;
+  int ctas_per_sm = 3;
 };
 BulkCfg bulk_cfg() {
   static BulkCfg c = [] {
@@ -317,32 +356,39 @@ BulkCfg bulk_cfg() {
     if (const char* e = getenv("FT_BULK_STAGES")) b.stages = atoi(e);
     if (const char* e = getenv("FT_BULK_TILE")) b.tile = (uint32_t)atoi(e);
     if (const char* e = getenv("FT_BULK_CTAS_PER_SM")) b.ctas_per_sm = atoi(e);
-    if (b.stages != 2 && b.stages != 3 && b.stages != 4 && b.stages != 6) b.stages = 3;
-    if (b.tile < 1024 || b.tile % 16 || (size_t)b.tile * b.stages > 200 * 1024) b.tile = 32768;
+    if (b.stages != 2 && b.stages != 3 && b.stages != 4 && b.stages != 6) b.stages = 2;
+    if (b.tile < 1024 || b.tile % 16 || (size_t)b.tile * b.stages > 200 * 1024) b.tile = 16384;
     if (b.ctas_per_sm < 1) b.ctas_per_sm = 1;
     return b;
   }();
   return c;
 }
-template <int S>
+template <int S, bool H>
 int launch_bulk_s(uint8_t* dst, const uint8_t* src, uint64_t bytes, int device, cudaStream_t st, int grid,
-                  uint32_t tile, int per_sm) {
+                  uint32_t tile, int per_sm, uint32_t hints) {
   size_t smem = (size_t)S * tile;
-  CU_RT(cudaFuncSetAttribute(k_copy_bulk<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  CU_RT(cudaFuncSetAttribute(k_copy_bulk<S, H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   uint64_t tiles = (bytes + tile - 1) / tile;
   if (grid <= 0) grid = per_sm * dev_sms(device);
   if ((uint64_t)grid > tiles) grid = (int)tiles;
-  k_copy_bulk<S><<<grid, kBulkThreads, smem, st>>>(dst, src, bytes, tile);
+  k_copy_bulk<S, H><<<grid, kBulkThreads, smem, st>>>(dst, src, bytes, tile, hints);
   CU_RT(cudaGetLastError());
   return FT_OK;
 }
-int launch_bulk(uint8_t* dst, const uint8_t* src, uint64_t bytes, int device, cudaStream_t st, int grid) {
+template <int S>
+int launch_bulk_h(uint8_t* dst, const uint8_t* src, uint64_t bytes, int device, cudaStream_t st, int grid,
+                  uint32_t tile, int per_sm, uint32_t hints) {
+  return hints ? launch_bulk_s<S, true>(dst, src, bytes, device, st, grid, tile, per_sm, hints)
+               : launch_bulk_s<S, false>(dst, src, bytes, device, st, grid, tile, per_sm, 0);
+}
+int launch_bulk(uint8_t* dst, const uint8_t* src, uint64_t bytes, int device, cudaStream_t st, int grid,
+                uint32_t hints) {
   BulkCfg c = bulk_cfg();
   switch (c.stages) {
-    case 2: return launch_bulk_s<2>(dst, src, bytes, device, st, grid, c.tile, c.ctas_per_sm);
-    case 4: return launch_bulk_s<4>(dst, src, bytes, device, st, grid, c.tile, c.ctas_per_sm);
-    case 6: return launch_bulk_s<6>(dst, src, bytes, device, st, grid, c.tile, c.ctas_per_sm);
-    default: return launch_bulk_s<3>(dst, src, bytes, device, st, grid, c.tile, c.ctas_per_sm);
+    case 3: return launch_bulk_h<3>(dst, src, bytes, device, st, grid, c.tile, c.ctas_per_sm, hints);
+    case 4: return launch_bulk_h<4>(dst, src, bytes, device, st, grid, c.tile, c.ctas_per_sm, hints);
+    case 6: return launch_bulk_h<6>(dst, src, bytes, device, st, grid, c.tile, c.ctas_per_sm, hints);
+    default: return launch_bulk_h<2>(dst, src, bytes, device, st, grid, c.tile, c.ctas_per_sm, hints);
   }
 }
 int launch_vec(uint8_t* dst, const uint8_t* src, uint64_t bytes, int device, cudaStream_t st, int grid) {
@@ -355,7 +401,8 @@ int launch_vec(uint8_t* dst, const uint8_t* src, uint64_t bytes, int device, cud
   return FT_OK;
 }
 
-int copy_impl(void* dst_, const void* src_, uint64_t bytes, int device, cudaStream_t st, int engine, int grid) {
+int copy_impl(void* dst_, const void* src_, uint64_t bytes, int device, cudaStream_t st, int engine, int grid,
+              uint32_t hints = 0) {
   if (bytes == 0) return FT_OK;
   if (!dst_ || !src_) {
     ft::set_last_error("ft_copy: null pointer");
@@ -383,7 +430,7 @@ int copy_impl(void* dst_, const void* src_, uint64_t bytes, int device, cudaStre
   if (head) k_copy_bytes<<<1, 32, 0, st>>>(dst, src, head);
   if (body) {
     if (engine == 0) engine = 1;
-    rc = engine == 1 ? launch_bulk(dst + head, src + head, body, device, st, grid)
+    rc = engine == 1 ? launch_bulk(dst + head, src + head, body, device, st, grid, hints)
                      : launch_vec(dst + head, src + head, body, device, st, grid);
   }
   if (rc == FT_OK && tail) k_copy_bytes<<<1, 32, 0, st>>>(dst + head + body, src + head + body, tail);
@@ -737,6 +784,10 @@ int ft_copy_ex(void* dst, const void* src, uint64_t bytes, int device, void* str
   }
   if (engine == 0) return ft_copy(dst, src, bytes, device, stream);
   return copy_impl(dst, src, bytes, device, (cudaStream_t)stream, engine, grid);
+}
+
+int ft_copy_hint(void* dst, const void* src, uint64_t bytes, int device, void* stream, uint32_t hints) {
+  return copy_impl(dst, src, bytes, device, (cudaStream_t)stream, 1, 0, hints & 15u);
 }
 
 int ft_fingerprint(const void* src, uint64_t bytes, uint64_t* out_dev, int device, void* stream) {

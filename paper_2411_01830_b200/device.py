@@ -75,6 +75,16 @@ def copy(dst_ptr: int, src_ptr: int, nbytes: int, device: int, stream=None, engi
                        C.c_void_p(stream_ptr(stream)), int(engine), int(grid))
 
 
+L2_NORMAL, L2_EVICT_FIRST, L2_EVICT_LAST = 0, 1, 2
+
+
+def copy_hint(dst_ptr: int, src_ptr: int, nbytes: int, device: int, stream=None, src_policy=L2_NORMAL,
+              dst_policy=L2_NORMAL):
+    """TMA-bulk copy with L2 eviction policies on the source reads / destination writes."""
+    LIB.ft_copy_hint(C.c_void_p(dst_ptr), C.c_void_p(src_ptr), int(nbytes), int(device),
+                     C.c_void_p(stream_ptr(stream)), int(src_policy | (dst_policy << 2)))
+
+
 def copy_tensor(dst: torch.Tensor, src: torch.Tensor, stream=None, engine=ENGINE_AUTO):
     assert dst.is_contiguous() and src.is_contiguous() and dst.nbytes == src.nbytes
     dev = dst.device.index if dst.is_cuda else src.device.index

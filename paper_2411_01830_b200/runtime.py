@@ -1,0 +1,234 @@
+"""Live workflow runtime on B200: requests walk their
+workflow DAG, gFuncs run on their placed GPU in FIFO order (temporal sharing,
+engine.py:310-338), and every intermediate payload moves through the
+FaaSTube put/get API — host->gFunc for request inputs, gFunc->gFunc between
+stages, gFunc->host for responses (engine.py:284-298, 342-464).
+
+The request trace, branch draws, payload sizes, placement and per-function
+SLOs are the reference's (``workload.py``, golden-checked), so the same seed
+replays the simulator's workload on real hardware; latency percentiles use the
+reference's nearest-rank estimator (simcore.py:247-252).
+
+Compute stand-ins: ``"sleep"`` spins the GPU for the function's
+compute_latency_ms (a timed kernel on its stream — keeps the reference's
+compute model); ``"model"`` runs random-init convolutional models on the
+payload (config 4: decode -> detector -> recognizers on 1080p frames).
+"""
+
+from __future__ import annotations
+
+import math
+import threading
+import time
+from concurrent.futures import ThreadPoolExecutor
+from dataclasses import dataclass, field
+
+import torch
+
+from .simcore import PHASES
+from .workload import Request, Workflow
+
+FRAME = (3, 1080, 1920)   # synthetic 1080p RGB uint8 frame = 6,220,800 B
+
+
+def nearest_rank(vals, pct):
+    vals = sorted(vals)
+    return vals[max(1, math.ceil(pct / 100.0 * len(vals))) - 1] if vals else None
+
+
+@dataclass
+class Record:
+    rid: int
+    workflow: str
+    arrival_ms: float
+    slo_ms: float
+    start_ms: float = 0.0
+    end_ms: float | None = None
+    phases: dict = field(default_factory=lambda: {p: 0.0 for p in PHASES})
+
+
+class _Models:
+    """Random-init conv stand-ins (bf16), one set per GPU."""
+
+    def __init__(self, device):
+        g = torch.Generator(device="cpu").manual_seed(1234)
+        mk = lambda co, ci, k: (torch.randn(co, ci, k, k, generator=g) * (ci * k * k) ** -0.5).to(
+            device=device, dtype=torch.bfloat16)
+        self.pre = mk(3, 3, 3)
+        self.det = [mk(32, 3, 3), mk(64, 32, 3), mk(64, 64, 3)]
+        self.rec = [mk(64, 3, 3), mk(128, 64, 3), mk(128, 128, 3)]
+
+    def run(self, fid, x: torch.Tensor, out_bytes: int) -> torch.Tensor:
+        import torch.nn.functional as F
+        n = x.numel() * x.element_size()
+        frames = max(1, n // (FRAME[0] * FRAME[1] * FRAME[2]))
+        if n < FRAME[0] * FRAME[1] * FRAME[2]:   # sub-frame payload: pad to one frame
+            pad = torch.zeros(FRAME[0] * FRAME[1] * FRAME[2], dtype=torch.uint8, device=x.device)
+            pad[:n] = x.reshape(-1).view(torch.uint8)
+            x = pad
+        h = x.view(torch.uint8)[: frames * FRAME[0] * FRAME[1] * FRAME[2]].view(frames, *FRAME).to(torch.bfloat16)
+        if "pre" in fid or "denoise" in fid:
+            h = F.conv2d(h, self.pre, padding=1)
+        elif "det" in fid or "yolo" in fid:
+            h = F.avg_pool2d(h, 4)
+            for w in self.det:
+                h = F.relu(F.conv2d(h, w, padding=1, stride=2))
+        else:
+            h = F.avg_pool2d(h, 8)
+            for w in self.rec:
+                h = F.relu(F.conv2d(h, w, padding=1, stride=2))
+        flat = h.reshape(-1).view(torch.uint8)
+        out = torch.empty(out_bytes, dtype=torch.uint8, device=x.device)
+        k = min(out_bytes, flat.numel())
+        out[:k] = flat[:k]
+        if k < out_bytes:
+            out[k:] = 0
+        return out
+
+
+class Runtime:
+    def __init__(self, tube, compute: str = "sleep", workers: int = 32):
+        self.tube = tube
+        self.compute = compute
+        self.pool = ThreadPoolExecutor(workers)
+        self.gpu_locks = {g: threading.Lock() for g in tube.gpus}
+        self.models = {}
+        self._host_bufs = {}
+        self.records: list[Record] = []
+        self._rec_lock = threading.Lock()
+        self.pool_timeline = []
+        self._clock_hz = {g: torch.cuda.get_device_properties(g).clock_rate * 1e3 if hasattr(
+            torch.cuda.get_device_properties(g), "clock_rate") else 1.965e9 for g in tube.gpus}
+
+    # ------------------------------------------------------------ one request
+    def _host_out(self, fid, nbytes):
+        """Synthetic cFunc output (pinned, reused: content is not request specific)."""
+        key = (fid, nbytes)
+        with self._rec_lock:
+            buf = self._host_bufs.get(key)
+            if buf is None:
+                buf = self._host_bufs[key] = torch.empty(nbytes, dtype=torch.uint8).pin_memory().fill_(7)
+        return buf
+
+    def _compute(self, fid, gpu, ms, x, out_bytes):
+        if self.compute == "model":
+            if gpu not in self.models:
+                self.models[gpu] = _Models(f"cuda:{gpu}")
+            return self.models[gpu].run(fid, x, out_bytes)
+        torch.cuda._sleep(int(ms * 1e-3 * self._clock_hz[gpu]))
+        return torch.empty(out_bytes, dtype=torch.uint8, device=f"cuda:{gpu}").fill_(len(fid) & 0xFF)
+
+    def _request(self, wf: Workflow, where: dict, req: Request, rec: Record, t0: float):
+        tube = self.tube
+        now = lambda: (time.perf_counter() - t0) * 1e3
+        rec.start_ms = now()
+        active = set(wf.entries())
+        for fid in wf.order():
+            if fid not in active and any(e.src in active and (e.src, e.dst) in req.fired for e in wf.ins(fid)):
+                active.add(fid)
+        # request payload arrives at the gateway (host memory)
+        in_id = tube.unique_id()
+        payload = self._host_out("gateway", int(req.input_bytes))
+        entries = [f for f in wf.entries() if f in active]
+        tube.store(in_id, payload, producer="gateway", consumers=max(1, len(entries)))
+        outputs = {}
+        for fid in wf.order():
+            if fid not in active:
+                continue
+            f = wf.func(fid)
+            kind, loc = where[fid]
+            gpu = loc if kind == "gpu" else None
+            ins = [e for e in wf.ins(fid) if (e.src, e.dst) in req.fired and e.src in active]
+            t_in = now()
+            if not ins:
+                x = tube.fetch(in_id, device=gpu, consumer=fid, slo_ms=f.slo_ms, infer_ms=f.infer_ms)
+                rec.phases["host_to_gfunc"] += now() - t_in
+            else:
+                xs = []
+                for e in ins:
+                    xs.append(tube.fetch(outputs[e.src], device=gpu, consumer=fid, slo_ms=f.slo_ms,
+                                         infer_ms=f.infer_ms))
+                phase = "gfunc_to_gfunc" if gpu is not None and where[ins[0].src][0] == "gpu" else "host_to_gfunc"
+                rec.phases[phase] += now() - t_in
+                x = xs[0]
+            outs = [e for e in wf.outs(fid) if (e.src, e.dst) in req.fired and e.dst in active]
+            sink = not outs
+            out_bytes = int(req.response_bytes if sink else max(req.edge_bytes[(e.src, e.dst)] for e in outs))
+            t_c = now()
+            if gpu is None:
+                time.sleep(f.compute_ms / 1e3)              # cFunc on a host core
+                y = self._host_out(fid, out_bytes)
+            else:
+                with self.gpu_locks[gpu], torch.cuda.device(gpu):   # GPU FIFO (temporal sharing)
+                    t_q = now()
+                    rec.phases["queuing"] += t_q - t_c
+                    y = self._compute(fid, gpu, f.compute_ms, x, out_bytes)
+                    torch.cuda.current_stream(gpu).synchronize()
+                    rec.phases["compute"] += now() - t_q
+            did = tube.unique_id()
+            t_s = now()
+            tube.store(did, y, producer=fid, response=sink and gpu is not None, consumers=max(1, len(outs)))
+            if sink:
+                if gpu is not None:
+                    tube.response(did)                      # D2H of the response lands on the host
+                    tube.release(did)
+                rec.phases["host_to_gfunc"] += now() - t_s
+            outputs[fid] = did
+        rec.end_ms = now()
+
+    # ------------------------------------------------------------ driver
+    def run(self, jobs: list, duration_s: float, drain_s: float = 30.0, sample_ms: float = 50.0) -> dict:
+        """jobs: [(workflow, placement, [Request])]; arrivals replayed in real time."""
+        events = sorted(((r.arrival_ms, i, wf, where, r) for i, (wf, where, reqs) in enumerate(jobs) for r in reqs),
+                        key=lambda e: (e[0], e[1], e[4].rid))
+        t0 = time.perf_counter()
+        futs = []
+        stop = threading.Event()
+
+        def sampler():
+            while not stop.is_set():
+                st = {g: p.stats() for g, p in self.tube.pools.items()}
+                self.pool_timeline.append(((time.perf_counter() - t0) * 1e3,
+                                           sum(s["mapped_bytes"] for s in st.values()),
+                                           sum(s["in_use_bytes"] for s in st.values())))
+                stop.wait(sample_ms / 1e3)
+
+        smp = threading.Thread(target=sampler, daemon=True)
+        smp.start()
+        for t_ms, _, wf, where, r in events:
+            dt = t_ms / 1e3 - (time.perf_counter() - t0)
+            if dt > 0:
+                time.sleep(dt)
+            rec = Record(r.rid, wf.name, t_ms, wf.slo_ms or float("inf"))
+            with self._rec_lock:
+                self.records.append(rec)
+            futs.append(self.pool.submit(self._request, wf, where, r, rec, t0))
+        deadline = time.perf_counter() + drain_s
+        errors = []
+        for fu in futs:
+            try:
+                fu.result(timeout=max(0.1, deadline - time.perf_counter()))
+            except Exception as exc:  # noqa: BLE001 - reported, not hidden
+                errors.append(repr(exc))
+        stop.set()
+        smp.join()
+        return self.summary(duration_s, errors)
+
+    def summary(self, duration_s: float, errors=()) -> dict:
+        done = [r for r in self.records if r.end_ms is not None]
+        lat = [r.end_ms - r.arrival_ms for r in done]
+        out = {"requests_seen": len(self.records), "requests_completed": len(done),
+               "throughput_rps": round(len(done) / duration_s, 3), "errors": list(errors)[:5],
+               "peak_pool_bytes": max((p[1] for p in self.pool_timeline), default=0),
+               "final_pool_bytes": self.pool_timeline[-1][1] if self.pool_timeline else 0}
+        if done:
+            out["p50_ms"] = round(nearest_rank(lat, 50), 4)
+            out["p99_ms"] = round(nearest_rank(lat, 99), 4)
+            out["slo_violation_rate"] = round(sum(1 for r in done if r.end_ms - r.arrival_ms > r.slo_ms + 1e-9)
+                                              / len(done), 4)
+            out["phase_p99_ms"] = {p: round(nearest_rank([r.phases[p] for r in done], 99), 4) for p in PHASES}
+            per = {}
+            for r in done:
+                per.setdefault(r.workflow, []).append(r.end_ms - r.arrival_ms)
+            out["per_workflow_p99_ms"] = {k: round(nearest_rank(v, 99), 4) for k, v in sorted(per.items())}
+        return out

@@ -49,6 +49,7 @@ from .topology import Topology, build_preset, snapshot_matrix
 __all__ = ["FaaSTube"]
 
 _ALIGN = 256  # stripe boundaries (bytes)
+_L2_KEEP = 96 << 20  # stored blocks up to this size stay L2-resident (126 MB L2) for the next fetch
 
 
 class _Obj:
@@ -205,7 +206,11 @@ class FaaSTube:
                     obj.block = blk
                     s = self._side[g]
                     s.wait_stream(self._stream(g))       # after the producer's kernels
-                    dev.copy(blk.ptr, t.data_ptr(), nbytes, g, s)
+                    if nbytes <= _L2_KEEP:
+                        # keep the fresh block L2-resident for the consumer's fetch
+                        dev.copy_hint(blk.ptr, t.data_ptr(), nbytes, g, s, dev.L2_EVICT_FIRST, dev.L2_EVICT_LAST)
+                    else:
+                        dev.copy(blk.ptr, t.data_ptr(), nbytes, g, s)
                     t.record_stream(s)
                     ev = torch.cuda.Event()
                     ev.record(s)
@@ -366,7 +371,9 @@ class FaaSTube:
             s.wait_event(obj.ready)
             if out is None:
                 return self._view(obj)
-            dev.copy(out.data_ptr(), obj.block.ptr, obj.nbytes, dst.gpu, s)
+            last = obj.remaining <= 1
+            dev.copy_hint(out.data_ptr(), obj.block.ptr, obj.nbytes, dst.gpu, s,
+                          dev.L2_EVICT_FIRST if last else dev.L2_NORMAL, dev.L2_NORMAL)
             self.stats["bytes_local"] += obj.nbytes
             return out
         if m == "inter_gpu":
