@@ -445,7 +445,7 @@ def run_workflows(dur_s=2.0):
 
     def traffic(tube):
         wf = workload.preset_workflow("traffic")
-        where = workload.place(wf, tube.topo, {}, limit=len(wf.gfuncs()))
+        where = workload.place(wf, tube.topo, {}, colocate=tube.topo.gpu_count < len(wf.gfuncs()))
         workload.calibrate_slo(wf, tube.topo, where, 1.5)
         reqs = workload.build_requests(wf, workload.gen_workload("bursty", 10.0, dur_s, 0), 0)
         return [(wf, where, reqs)]
@@ -459,7 +459,7 @@ def run_workflows(dur_s=2.0):
                     {"id": f"cons{mb}", "kind": "gFunc", "compute_latency_ms": 2.0}],
                 "edges": [{"src": f"prod{mb}", "dst": f"cons{mb}", "size": {"const_mb": mb}}],
                 "input_size": {"const_mb": 1}, "response_size": {"const_mb": 1}})
-            where = workload.place(wf, tube.topo, occ, limit=16)
+            where = workload.place(wf, tube.topo, occ, limit=2, colocate=tube.topo.gpu_count < 16)
             for k, (kind, g) in where.items():
                 if kind == "gpu":
                     occ[g] = occ.get(g, 0) + 1

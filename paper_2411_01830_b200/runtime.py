@@ -48,7 +48,10 @@ class Record:
 
 
 class _Models:
-    """Random-init conv stand-ins (bf16), one set per GPU."""
+    """Random-init conv stand-ins (bf16), one set per GPU; each call processes a
+    fixed batch of BATCH 1080p frames taken from the payload."""
+
+    BATCH = 4
 
     def __init__(self, device):
         g = torch.Generator(device="cpu").manual_seed(1234)
@@ -61,12 +64,14 @@ class _Models:
     def run(self, fid, x: torch.Tensor, out_bytes: int) -> torch.Tensor:
         import torch.nn.functional as F
         n = x.numel() * x.element_size()
-        frames = max(1, n // (FRAME[0] * FRAME[1] * FRAME[2]))
-        if n < FRAME[0] * FRAME[1] * FRAME[2]:   # sub-frame payload: pad to one frame
-            pad = torch.zeros(FRAME[0] * FRAME[1] * FRAME[2], dtype=torch.uint8, device=x.device)
-            pad[:n] = x.reshape(-1).view(torch.uint8)
-            x = pad
-        h = x.view(torch.uint8)[: frames * FRAME[0] * FRAME[1] * FRAME[2]].view(frames, *FRAME).to(torch.bfloat16)
+        fb = FRAME[0] * FRAME[1] * FRAME[2]
+        frames = self.BATCH                      # fixed shapes: no per-request kernel selection
+        flat_in = x.reshape(-1).view(torch.uint8)
+        if n < frames * fb:                      # short payload: zero-pad the frame batch
+            pad = torch.zeros(frames * fb, dtype=torch.uint8, device=x.device)
+            pad[:n] = flat_in
+            flat_in = pad
+        h = flat_in[: frames * fb].view(frames, *FRAME).to(torch.bfloat16)
         if "pre" in fid or "denoise" in fid:
             h = F.conv2d(h, self.pre, padding=1)
         elif "det" in fid or "yolo" in fid:
@@ -177,10 +182,19 @@ class Runtime:
         rec.end_ms = now()
 
     # ------------------------------------------------------------ driver
-    def run(self, jobs: list, duration_s: float, drain_s: float = 30.0, sample_ms: float = 50.0) -> dict:
+    def run(self, jobs: list, duration_s: float, drain_s: float = 30.0, sample_ms: float = 50.0,
+            idle_s: float = 1.0) -> dict:
         """jobs: [(workflow, placement, [Request])]; arrivals replayed in real time."""
         events = sorted(((r.arrival_ms, i, wf, where, r) for i, (wf, where, reqs) in enumerate(jobs) for r in reqs),
                         key=lambda e: (e[0], e[1], e[4].rid))
+        if self.compute == "model":              # build/warm the models outside the trace
+            for wf, where, _ in jobs:
+                for fid, (kind, g) in where.items():
+                    if kind == "gpu":
+                        with torch.cuda.device(g):
+                            self._compute(fid, g, 0.0, torch.zeros(1 << 20, dtype=torch.uint8, device=f"cuda:{g}"),
+                                          1 << 20)
+            torch.cuda.synchronize()
         t0 = time.perf_counter()
         futs = []
         stop = threading.Event()
@@ -212,7 +226,16 @@ class Runtime:
                 errors.append(repr(exc))
         stop.set()
         smp.join()
-        return self.summary(duration_s, errors)
+        out = self.summary(duration_s, errors)
+        # elasticity: after the trace, idle past the reservation windows and let
+        # the pool policy shrink (engine.py:656-665)
+        t_idle = time.perf_counter()
+        while time.perf_counter() - t_idle < idle_s:
+            self.tube.maintain()
+            time.sleep(0.05)
+        self.tube.maintain()
+        out["pool_after_idle_bytes"] = sum(p.stats()["mapped_bytes"] for p in self.tube.pools.values())
+        return out
 
     def summary(self, duration_s: float, errors=()) -> dict:
         done = [r for r in self.records if r.end_ms is not None]

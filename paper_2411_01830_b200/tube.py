@@ -54,10 +54,13 @@ _L2_KEEP = 96 << 20  # stored blocks up to this size stay L2-resident (126 MB L2
 
 class _Obj:
     __slots__ = ("did", "nbytes", "dtype", "shape", "gpu", "block", "host", "producer", "remaining", "ready",
-                 "pins", "retired", "response_host", "response_event", "stored_at", "__weakref__")
+                 "pins", "retired", "response_host", "response_event", "stored_at", "home", "queue_pos",
+                 "__weakref__")
 
     def __init__(self, did, nbytes, dtype, shape, gpu, producer, consumers, now):
         self.did, self.nbytes, self.dtype, self.shape, self.gpu = did, nbytes, dtype, shape, gpu
+        self.home = None       # GPU whose store holds / held it (migration target for prefetch)
+        self.queue_pos = 0     # request-queue position of its next consumer (datastore.py:177)
         self.block = None      # device.PoolBlock when on a GPU
         self.host = None       # pinned host tensor when in host memory
         self.producer = producer
@@ -74,7 +77,7 @@ class FaaSTube:
     def __init__(self, strategy: str | Strategy = "faastube", topology: Topology | None = None,
                  pcie_gbps: float = 55.0, chunk_bytes: int = CHUNK_BYTES, batch_chunks: int = BATCH_CHUNKS,
                  pool_floor_bytes: float = datastore.POOL_FLOOR_BYTES, node: int = 0, map_ms: float = 0.05,
-                 gpus: list | None = None):
+                 gpus: list | None = None, capacity_limit_bytes: float = datastore.CAPACITY_LIMIT_BYTES):
         n = dev.require_cuda()
         self.topo = topology or build_preset("b200", n_gpus=n, pcie_gbps=pcie_gbps)
         if self.topo.gpu_count > n:
@@ -104,6 +107,7 @@ class FaaSTube:
         self._objs: dict[int, _Obj] = {}
         self._lock = threading.RLock()
         self._sched_lock = threading.Lock()
+        self._sched_cv = threading.Condition(self._sched_lock)   # wakes parked managed stages
         self._side = {g: torch.cuda.Stream(g) for g in self.gpus}        # store / forward stream
         self._ce = {g: [torch.cuda.Stream(g) for _ in range(2)] for g in self.gpus}  # copy-engine streams
         # per-transfer CE stream pairs (PCIe leg, NVLink forward): concurrent tenants'
@@ -114,8 +118,10 @@ class FaaSTube:
         self._pending_release = []   # (event, plan): NVLink claims held until the copy lands
         self._shrink_due = []        # heap of (due_ms, gpu)
         self._managed_ids = itertools.count(1)
+        self._queue = itertools.count(1)
+        self.capacity_limit = float(capacity_limit_bytes)   # per-GPU store cap (datastore.py:19)
         self.stats = {"stores": 0, "fetches": 0, "bytes_h2d": 0, "bytes_d2h": 0, "bytes_nvlink": 0,
-                      "bytes_local": 0, "zero_copy": 0}
+                      "bytes_local": 0, "zero_copy": 0, "migrated_bytes": 0, "reload_bytes": 0}
 
     # ------------------------------------------------------------ helpers
     def now_ms(self) -> float:
@@ -178,8 +184,12 @@ class FaaSTube:
         return t
 
     def store(self, data_id: int, output: torch.Tensor, response: bool = False, producer: str = "func",
-              consumers: int = 1) -> None:
-        """FaaSTube.store(index, output, response) — engine.py:342-423."""
+              consumers: int = 1, queue_pos: int | None = None) -> None:
+        """FaaSTube.store(index, output, response) — engine.py:342-423.
+
+        ``queue_pos``: request-queue position of the object's next consumer
+        (the runtime knows it; default: store order) — drives queue-aware
+        migration under memory pressure (datastore.py:192-222)."""
         with self._lock:
             self._reap()
             if data_id in self._objs:
@@ -189,9 +199,10 @@ class FaaSTube:
             nbytes = t.nbytes
             now = self.now_ms()
             obj = _Obj(data_id, nbytes, t.dtype, tuple(t.shape), None, producer, consumers, now)
+            obj.queue_pos = queue_pos if queue_pos is not None else next(self._queue)
             if t.is_cuda and self.strategy.gpu_store():
                 g = t.device.index
-                obj.gpu = g
+                obj.gpu = obj.home = g
                 pool = self.pools[g]
                 blk = getattr(t, "_ft_block", None)
                 live_here = sum(1 for o in self._objs.values() if o.producer == producer and o.gpu == g
@@ -204,8 +215,10 @@ class FaaSTube:
                 else:
                     blk = pool.allocate(nbytes)          # datastore.py:130-144
                     obj.block = blk
-                    s = self._side[g]
-                    s.wait_stream(self._stream(g))       # after the producer's kernels
+                    # snapshot on the producer's stream: ordered after the kernels that
+                    # wrote the output AND before any later kernel that overwrites it
+                    s = self._stream(g)
+                    s.wait_stream(self._side[g])         # the block's previous readers are done
                     if nbytes <= _L2_KEEP:
                         # keep the fresh block L2-resident for the consumer's fetch
                         dev.copy_hint(blk.ptr, t.data_ptr(), nbytes, g, s, dev.L2_EVICT_FIRST, dev.L2_EVICT_LAST)
@@ -232,6 +245,8 @@ class FaaSTube:
                 ev = torch.cuda.Event()
                 ev.record(s)
                 obj.host, obj.ready = host, ev
+                if response:                               # already in host memory
+                    obj.response_host, obj.response_event = host, ev
                 self.stats["bytes_d2h"] += nbytes
                 self.index.store(data_id, self._loc(None), nbytes, now, producer, response)
             else:
@@ -242,6 +257,81 @@ class FaaSTube:
                 self.index.store(data_id, self._loc(None), nbytes, now, producer, response)
             self._objs[data_id] = obj
             self.stats["stores"] += 1
+            if obj.block is not None and self.strategy.migration != "none":
+                self._check_pressure(obj.gpu)                # engine.py:685-702
+
+    # ------------------------------------------------ queue-aware migration (§8f row 1)
+    def _stored_on(self, g) -> int:
+        return sum(o.nbytes for o in self._objs.values() if o.block is not None and o.gpu == g)
+
+    def _policy_objs(self, g):
+        from .datastore import StoredObject
+        objs = sorted((o for o in self._objs.values() if o.home == g), key=lambda o: o.did)
+        recs = [StoredObject(o.did, float(o.nbytes), o.producer, g, o.stored_at,
+                             "gpu" if o.block is not None else "host",
+                             {("c", i): o.queue_pos for i in range(max(1, o.remaining))}, not o.retired)
+                for o in objs]
+        return objs, recs
+
+    def _check_pressure(self, g):
+        """Store cap exceeded -> migrate the objects whose consumers sit farthest
+        back in the queue to host memory (datastore.py:192-222)."""
+        stored = self._stored_on(g)
+        if stored <= self.capacity_limit:
+            return
+        from .datastore import migration_plan
+        objs, recs = self._policy_objs(g)
+        try:
+            plan = migration_plan(recs, stored - self.capacity_limit, self.strategy.migration)
+        except Exception:  # noqa: BLE001 - HardPressure: nothing migratable (engine.py:696-697)
+            return
+        by_id = {o.did: o for o in objs}
+        for action, rec in plan:
+            o = by_id[rec.data_id]
+            if action == "migrate" and o.block is not None and o.pins == 0:
+                self._migrate_out(o)
+
+    def _migrate_out(self, o: _Obj):
+        """D2H on the GPU's own link, then the block goes back to the pool (engine.py:704-715)."""
+        g = o.gpu
+        host = self._pinned(o.nbytes)
+        ce = self._ce[g][1]
+        ce.wait_event(o.ready)
+        dev.pcie_copy(host.data_ptr(), o.block.ptr, o.nbytes, False, g, ce)
+        ev = torch.cuda.Event()
+        ev.record(ce)
+        blk, o.block = o.block, None
+        self._side[g].wait_event(ev)                         # later writers of the block wait for the D2H
+        self.pools[g].free(blk)
+        o.host, o.ready, o.gpu = host, ev, None
+        self.index.relocate(o.did, self._loc(None))
+        self.stats["migrated_bytes"] += o.nbytes
+        self.stats["bytes_d2h"] += o.nbytes
+
+    def _maybe_prefetch(self, g):
+        """Room freed -> reload migrated objects, nearest consumer first (datastore.py:225-238)."""
+        free = self.capacity_limit - self._stored_on(g)
+        if free <= 0:
+            return
+        from .datastore import prefetch_back
+        objs, recs = self._policy_objs(g)
+        by_id = {o.did: o for o in objs}
+        for rec in prefetch_back(recs, free):
+            o = by_id[rec.data_id]
+            if o.host is None or o.block is not None:
+                continue
+            blk = self.pools[g].allocate(o.nbytes)
+            ce = self._ce[g][0]
+            if o.ready is not None:
+                ce.wait_event(o.ready)
+            ce.wait_stream(self._side[g])
+            dev.pcie_copy(blk.ptr, o.host.data_ptr(), o.nbytes, True, g, ce)
+            ev = torch.cuda.Event()
+            ev.record(ce)
+            o.block, o.ready, o.gpu, o.host = blk, ev, g, None
+            self.index.relocate(o.did, self._loc(g))
+            self.stats["reload_bytes"] += o.nbytes
+            self.stats["bytes_h2d"] += o.nbytes
 
     def fetch(self, data_id: int, device: int | None = None, out: torch.Tensor | None = None,
               consumer: str = "func", slo_ms: float | None = None, infer_ms: float | None = None) -> torch.Tensor:
@@ -343,6 +433,8 @@ class FaaSTube:
             self._side[blk.device].wait_event(ev)
             self.pools[blk.device].free(blk)
             self._push_shrink(blk.device, obj.producer, self.now_ms())
+            if self.strategy.migration != "none":
+                self._maybe_prefetch(blk.device)             # engine.py:678-679, 717-736
 
     def _unpin(self, ref):
         obj = ref()
@@ -499,6 +591,7 @@ class FaaSTube:
             if t is None or t > self.now_ms():
                 return
             arb.boundary(t, key)
+            self._sched_cv.notify_all()
 
     def _managed_h2g(self, obj, plan, dst, res, consumer, slo_ms, infer_ms):
         """A scheduler-managed PCIe stage (engine.py:537-575): the stage's
@@ -520,6 +613,7 @@ class FaaSTube:
         with self._sched_lock:
             now = self.now_ms()
             arb.start(now, key, float(obj.nbytes), slo, infer, now, per_branch_cap, len(br))
+            self._sched_cv.notify_all()
         batch = self.batch_chunks * self.chunk_bytes
         done = [0] * len(br)
         inflight = []
@@ -532,7 +626,9 @@ class FaaSTube:
                 nxt, _ = arb.next_event()
             now = self.now_ms()
             if not st["started"] or st["rate"] <= 0:
-                _sleep_until(nxt if nxt is not None else now + 0.05, self.now_ms)
+                # parked until a boundary, another stage's finish, or a new stage re-partitions
+                with self._sched_cv:
+                    self._sched_cv.wait(max(0.0, (nxt - now) / 1e3) if nxt is not None else 0.002)
                 continue
             dur = batch / (st["rate"] * 1e6)              # ms per batch at the stage rate
             if next_t is None:
@@ -557,7 +653,13 @@ class FaaSTube:
             ev.synchronize()
         with self._sched_lock:
             arb.finish(self.now_ms(), key)
+            self._sched_cv.notify_all()
         self.stats["managed_stages"] = self.stats.get("managed_stages", 0) + 1
+
+    def maintain(self):
+        """Release landed NVLink claims and run due pool shrinks (idle housekeeping)."""
+        with self._lock:
+            self._reap()
 
     def _gpu_to_host(self, obj, plan, out):
         res = out if out is not None else self._pinned(obj.nbytes).view(obj.dtype).view(obj.shape)
@@ -573,13 +675,11 @@ class FaaSTube:
 
 
 def _sleep_until(t_ms, clock):
-    """Sub-millisecond wait: sleep for the bulk, spin the last 0.2 ms."""
-    while True:
-        left = t_ms - clock()
-        if left <= 0:
-            return
-        if left > 0.3:
-            time.sleep((left - 0.2) / 1e3)
+    """Wait without spinning: sleeping releases the GIL, so concurrent tenants'
+    pacing loops never starve each other (waits under 50 us count as due)."""
+    left = t_ms - clock()
+    if left > 0.05:
+        time.sleep(left / 1e3)
 
 
 def _hops(links):

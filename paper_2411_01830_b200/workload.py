@@ -201,9 +201,21 @@ def build_requests(wf: Workflow, arrivals: list, seed: int, rid_start: int = 0) 
 
 
 # ----------------------------------------------------------------- placement + SLOs
-def place(wf: Workflow, topo: Topology, occupancy: dict | None = None, limit: int = 1) -> dict:
+def place(wf: Workflow, topo: Topology, occupancy: dict | None = None, limit: int = 1,
+          colocate: bool = False) -> dict:
     """Greedy NVLink-aware placement (workflow.py:375-438): heaviest gFunc edges
-    onto the best free pair, leftovers onto the GPUs with the most NVLink."""
+    onto the best free pair, leftovers onto the GPUs with the most NVLink.
+
+    The reference gives every gFunc of a workflow its own GPU, so it cannot
+    place a multi-gFunc workflow on a box with fewer GPUs. ``colocate=True``
+    (used when the box is smaller, e.g. one B200) shares GPUs round-robin
+    instead — same-GPU edges then take the zero-copy intra-GPU method."""
+    if colocate:
+        gpus = topo.gpus()
+        where = {fid: ("gpu", gpus[i % len(gpus)]) for i, fid in enumerate(wf.gfuncs())}
+        home = topo.node_of(gpus[0])
+        where.update({f.id: ("host", home) for f in wf.funcs if f.kind == "cFunc"})
+        return where
     occ = dict(occupancy or {})
     free = [g for g in topo.gpus() if occ.get(g, 0) < limit]
     if len(wf.gfuncs()) > len(free):

@@ -1,0 +1,53 @@
+"""Queue-aware migration and prefetch on a real GPU store (SURVEY §8f row 1,
+datastore.py:192-238, engine.py:685-736): over the store cap, the object
+whose consumer is farthest back in the queue moves to host memory; fetches
+stay bit-exact; retiring frees room and the migrated object is reloaded."""
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+MB = 1 << 20
+
+
+def test_migrate_then_prefetch_bit_exact():
+    from paper_2411_01830_b200.tube import FaaSTube
+    tube = FaaSTube("faastube", pool_floor_bytes=0.0, capacity_limit_bytes=100 * MB)
+    xs = [torch.randint(0, 256, (40 * MB,), dtype=torch.uint8, device="cuda:0") for _ in range(3)]
+    ids = []
+    for i, x in enumerate(xs):
+        d = tube.unique_id()
+        tube.store(d, x, producer="p", queue_pos=10 * (i + 1))    # consumers at queue positions 10, 20, 30
+        ids.append(d)
+    # 120 MB > 100 MB: the farthest-back consumer's object (queue 30) is migrated
+    assert tube.stats["migrated_bytes"] == 40 * MB
+    assert tube.index.resolve(ids[2], 0, 0.0)[0].location.gpu is None
+    assert tube.index.resolve(ids[0], 0, 0.0)[0].location.gpu == 0
+    # first consumer fetches (retires object 0) -> room -> object 2 prefetched back
+    got0 = tube.fetch(ids[0], device=0, out=torch.empty_like(xs[0]))
+    assert tube.stats["reload_bytes"] == 40 * MB
+    assert tube.index.resolve(ids[2], 0, 0.0)[0].location.gpu == 0
+    got1 = tube.fetch(ids[1], device=0, out=torch.empty_like(xs[1]))
+    got2 = tube.fetch(ids[2], device=0, out=torch.empty_like(xs[2]))
+    torch.cuda.synchronize()
+    for g, x in zip((got0, got1, got2), xs):
+        assert torch.equal(g, x)
+    tube.close()
+
+
+def test_lru_policy_evicts_oldest():
+    from paper_2411_01830_b200.strategies import strategy_preset
+    from paper_2411_01830_b200.tube import FaaSTube
+    tube = FaaSTube(strategy_preset("faastube", migration="lru"), pool_floor_bytes=0.0,
+                    capacity_limit_bytes=100 * MB)
+    xs = [torch.randint(0, 256, (40 * MB,), dtype=torch.uint8, device="cuda:0") for _ in range(3)]
+    ids = []
+    for i, x in enumerate(xs):
+        d = tube.unique_id()
+        tube.store(d, x, producer="p", queue_pos=10 * (i + 1))
+        ids.append(d)
+    assert tube.index.resolve(ids[0], 0, 0.0)[0].location.gpu is None     # oldest stored goes first
+    got = tube.fetch(ids[0], device=0, out=torch.empty_like(xs[0]))        # served from host memory
+    torch.cuda.synchronize()
+    assert torch.equal(got, xs[0])
+    tube.close()

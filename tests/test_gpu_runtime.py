@@ -13,7 +13,7 @@ def _run(strategy, preset="yelp", rate=20.0, dur=1.0, compute="sleep", seed=0):
     from paper_2411_01830_b200.tube import FaaSTube
     tube = FaaSTube(strategy)
     wf = workload.preset_workflow(preset)
-    where = workload.place(wf, tube.topo, {}, limit=len(wf.gfuncs()))
+    where = workload.place(wf, tube.topo, {}, colocate=tube.topo.gpu_count < len(wf.gfuncs()))
     workload.calibrate_slo(wf, tube.topo, where, 1.5)
     reqs = workload.build_requests(wf, workload.gen_workload("sporadic", rate, dur, seed), seed)
     rt = Runtime(tube, compute=compute)
