@@ -174,27 +174,46 @@ class DevicePool:
                 self.grow_events += 1
             return PoolBlock(b, m[0], m[1], m[2], self.device)
 
-    def free(self, blk: PoolBlock):
+    def free(self, blk: PoolBlock, fence: torch.cuda.Stream | None = None):
         with self._lock:
             self.policy.free(blk.policy_block)
-            if self.policy.mode == "none":
-                self._unmap(blk.policy_block.block_id)
+            if self.policy.mode == "none":           # temporary allocations: give it back now
+                self._unmap(blk.policy_block.block_id, fence)
 
     def record(self, func: str, now_ms: float, size: float, concurrency: float):
         with self._lock:
             self.policy.histogram(func).record_execution(now_ms, size, concurrency)
 
-    def shrink(self, now_ms: float) -> int:
-        """Apply the policy's shrink; unmap what it drops. Returns bytes released."""
+    def shrink(self, now_ms: float, fence: torch.cuda.Stream | None = None) -> int:
+        """Apply the policy's shrink and unmap what it drops; returns bytes
+        released. ``fence``: a stream that already waits on every reader of a
+        freed block (the tube's side stream) — synchronizing it, instead of the
+        whole device, is enough before the physical memory goes back."""
         with self._lock:
             dropped = self.policy.shrink(now_ms)
-            return sum(self._unmap(b.block_id) for b in dropped)
+            gone = [self._mapped.pop(b.block_id) for b in dropped if b.block_id in self._mapped]
+        if not gone:
+            return 0
+        if fence is not None:
+            fence.synchronize()
+        else:
+            torch.cuda.synchronize(self.device)
+        for vid, _ptr, _n in gone:
+            LIB.ft_vmm_block_unmap(self._h, vid)
+        return sum(n for _, _, n in gone)
 
-    def _unmap(self, block_id) -> int:
+    def hist_window(self, func: str):
+        with self._lock:
+            return self.policy.hist_window(func)
+
+    def _unmap(self, block_id, fence: torch.cuda.Stream | None = None) -> int:
         m = self._mapped.pop(block_id, None)
         if m is None:
             return 0
-        torch.cuda.synchronize(self.device)  # no in-flight kernel may touch it
+        if fence is not None:                   # no in-flight kernel may touch it
+            fence.synchronize()
+        else:
+            torch.cuda.synchronize(self.device)
         LIB.ft_vmm_block_unmap(self._h, m[0])
         return m[2]
 

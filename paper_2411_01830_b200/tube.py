@@ -119,6 +119,10 @@ class FaaSTube:
         self._shrink_due = []        # heap of (due_ms, gpu)
         self._managed_ids = itertools.count(1)
         self._queue = itertools.count(1)
+        self._maint_cv = threading.Condition()
+        self._closing = False
+        self._maint = threading.Thread(target=self._maint_loop, name="faastube-shrink", daemon=True)
+        self._maint.start()
         self.capacity_limit = float(capacity_limit_bytes)   # per-GPU store cap (datastore.py:19)
         self.stats = {"stores": 0, "fetches": 0, "bytes_h2d": 0, "bytes_d2h": 0, "bytes_nvlink": 0,
                       "bytes_local": 0, "zero_copy": 0, "migrated_bytes": 0, "reload_bytes": 0}
@@ -139,11 +143,26 @@ class FaaSTube:
             else:
                 keep.append((ev, plan))
         self._pending_release = keep
-        now = self.now_ms()
-        while self._shrink_due and self._shrink_due[0][0] <= now:
-            _, g = heapq.heappop(self._shrink_due)
-            if g in self.pools:
-                self.pools[g].shrink(now)
+
+    def _maint_loop(self):
+        """Pool shrink timer (engine.py:656-665): at last_request + R_window the
+        policy drops idle blocks and their physical memory is unmapped — off the
+        request path, fenced on the side stream only."""
+        while True:
+            with self._maint_cv:
+                if self._closing:
+                    return
+                now = self.now_ms()
+                due = set()
+                while self._shrink_due and self._shrink_due[0][0] <= now:
+                    due.add(heapq.heappop(self._shrink_due)[1])
+                if not due:
+                    wait = (self._shrink_due[0][0] - now) / 1e3 if self._shrink_due else 0.1
+                    self._maint_cv.wait(min(0.1, max(0.001, wait)))
+                    continue
+            for g in sorted(due):
+                if g in self.pools:
+                    self.pools[g].shrink(self.now_ms(), fence=self._side[g])
 
     def _stream(self, g):
         return torch.cuda.current_stream(g)
@@ -302,7 +321,7 @@ class FaaSTube:
         ev.record(ce)
         blk, o.block = o.block, None
         self._side[g].wait_event(ev)                         # later writers of the block wait for the D2H
-        self.pools[g].free(blk)
+        self.pools[g].free(blk, fence=self._side[g])
         o.host, o.ready, o.gpu = host, ev, None
         self.index.relocate(o.did, self._loc(None))
         self.stats["migrated_bytes"] += o.nbytes
@@ -387,6 +406,10 @@ class FaaSTube:
         return obj.response_host.view(obj.dtype).view(obj.shape)
 
     def close(self):
+        with self._maint_cv:
+            self._closing = True
+            self._maint_cv.notify()
+        self._maint.join(timeout=5)
         for g in self.gpus:
             torch.cuda.synchronize(g)
         self._objs.clear()
@@ -396,8 +419,10 @@ class FaaSTube:
     # ------------------------------------------------------------ internals
     def _push_shrink(self, g, func, now):
         """Shrink timer at last_request + R_window (engine.py:656-659)."""
-        r_window, last = self.pools[g].policy.hist_window(func)
-        heapq.heappush(self._shrink_due, ((last if last is not None else now) + r_window, g))
+        r_window, last = self.pools[g].hist_window(func)
+        with self._maint_cv:
+            heapq.heappush(self._shrink_due, ((last if last is not None else now) + r_window, g))
+            self._maint_cv.notify()
 
     def _respond(self, obj: _Obj):
         g = obj.gpu
@@ -431,15 +456,12 @@ class FaaSTube:
             ev = torch.cuda.Event()
             ev.record(self._stream(blk.device))
             self._side[blk.device].wait_event(ev)
-            self.pools[blk.device].free(blk)
+            self.pools[blk.device].free(blk, fence=self._side[blk.device])
             self._push_shrink(blk.device, obj.producer, self.now_ms())
             if self.strategy.migration != "none":
                 self._maybe_prefetch(blk.device)             # engine.py:678-679, 717-736
 
-    def _unpin(self, ref):
-        obj = ref()
-        if obj is None:
-            return
+    def _unpin(self, obj):
         with self._lock:
             obj.pins -= 1
             self._maybe_free(obj)
@@ -447,7 +469,7 @@ class FaaSTube:
     def _view(self, obj: _Obj) -> torch.Tensor:
         obj.pins += 1
         t = dev.as_tensor(obj.block.ptr, obj.nbytes, obj.gpu, obj.dtype, obj.shape, owner=obj.block)
-        weakref.finalize(t, self._unpin, weakref.ref(obj))
+        weakref.finalize(t, self._unpin, obj)   # strong ref: the object may already be retired
         self.stats["zero_copy"] += 1
         return t
 
