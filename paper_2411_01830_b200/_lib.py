@@ -259,6 +259,7 @@ class _Lib:
         fn = self.raw(name)
         res = _SIGS[name][0]
         if res is not None:
+            setattr(self, name, fn)          # cached: later lookups skip __getattr__
             return fn
 
         def call(*args):
@@ -267,6 +268,7 @@ class _Lib:
                 raise_status(rc)
             return rc
         call.__name__ = name
+        setattr(self, name, call)
         return call
 
 

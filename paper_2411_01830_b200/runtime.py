@@ -187,6 +187,16 @@ class Runtime:
         """jobs: [(workflow, placement, [Request])]; arrivals replayed in real time."""
         events = sorted(((r.arrival_ms, i, wf, where, r) for i, (wf, where, reqs) in enumerate(jobs) for r in reqs),
                         key=lambda e: (e[0], e[1], e[4].rid))
+        # warm-up outside the trace: spin up every worker thread's CUDA state and
+        # run one request per workflow (pool blocks, pinned buffers, kernels loaded)
+        list(self.pool.map(lambda _: torch.cuda.current_stream(self.tube.gpus[0]).synchronize(),
+                           range(self.pool._max_workers)))  # noqa: SLF001
+        for wf, where, reqs in jobs:
+            if reqs:
+                r0 = reqs[0]
+                warm = Request(-1, r0.workflow, 0.0, r0.edge_bytes, r0.fired, r0.input_bytes, r0.response_bytes)
+                self.pool.submit(self._request, wf, where, warm, Record(-1, wf.name, 0.0, 0.0),
+                                 time.perf_counter()).result()
         if self.compute == "model":              # build/warm the models outside the trace
             for wf, where, _ in jobs:
                 for fid, (kind, g) in where.items():

@@ -115,6 +115,7 @@ class FaaSTube:
         self._ce_pairs = {g: [(torch.cuda.Stream(g), torch.cuda.Stream(g)) for _ in range(8)] for g in self.gpus}
         self._ce_rr = itertools.count()
         self._staging = {}
+        self._pinned_ring = None     # shared warm staging ring for pageable host payloads
         self._pending_release = []   # (event, plan): NVLink claims held until the copy lands
         self._shrink_due = []        # heap of (due_ms, gpu)
         self._managed_ids = itertools.count(1)
@@ -269,14 +270,22 @@ class FaaSTube:
                 self.stats["bytes_d2h"] += nbytes
                 self.index.store(data_id, self._loc(None), nbytes, now, producer, response)
             else:
-                # cFunc output / request payload: host resident (pinned for DMA)
-                host = t.view(-1).view(torch.uint8) if t.is_pinned() else self._pinned(nbytes).copy_(
-                    t.reshape(-1).view(torch.uint8))
+                # cFunc output / request payload: host resident. With the PCIe scheduler
+                # a pageable payload is kept as is (ownership passes to the tube) and
+                # staged through the shared warm pinned ring at fetch time
+                # (pcie_sched.py:122-162); other strategies pin a
+                # private staging copy per object (their cold-pin behaviour).
+                flat = t.reshape(-1).view(torch.uint8)
+                if t.is_pinned() or self.strategy.pcie_sched:
+                    host = flat
+                else:
+                    host = self._pinned(nbytes).copy_(flat)
                 obj.host = host
                 self.index.store(data_id, self._loc(None), nbytes, now, producer, response)
             self._objs[data_id] = obj
             self.stats["stores"] += 1
-            if obj.block is not None and self.strategy.migration != "none":
+            if obj.block is not None and self.strategy.migration != "none" and \
+                    self._stored_on(obj.gpu) > self.capacity_limit:
                 self._check_pressure(obj.gpu)                # engine.py:685-702
 
     # ------------------------------------------------ queue-aware migration (§8f row 1)
@@ -329,6 +338,8 @@ class FaaSTube:
 
     def _maybe_prefetch(self, g):
         """Room freed -> reload migrated objects, nearest consumer first (datastore.py:225-238)."""
+        if not any(o.home == g and o.block is None and o.host is not None for o in self._objs.values()):
+            return                                    # nothing migrated off this GPU
         free = self.capacity_limit - self._stored_on(g)
         if free <= 0:
             return
@@ -599,11 +610,29 @@ class FaaSTube:
         s = self._stream(dst.gpu)
         if obj.ready is not None:
             s.wait_event(obj.ready)
-        events = [self._issue_h2g(b, obj.host.data_ptr() + off, res.data_ptr() + off, n, dst.gpu, s)
-                  for b, (off, n) in zip(br, ranges) if n]
+        events = []
+        for b, (off, n) in zip(br, ranges):
+            if n:
+                events += self._h2g_range(b, obj.host, off, n, res.data_ptr() + off, dst.gpu, s)
         for ev in events:
             s.wait_event(ev)
         return res
+
+    def _h2g_range(self, b, host: torch.Tensor, off, n, dst_ptr, dst_gpu, after, slot=None) -> list:
+        """Bytes [off, off+n) of a host object onto a branch: straight DMA from
+        pinned memory, or chunk by chunk through the shared pinned ring."""
+        if host.is_pinned():
+            return [self._issue_h2g(b, host.data_ptr() + off, dst_ptr, n, dst_gpu, after, slot)]
+        ring = self._ring()
+        return ring.stage(host, off, n, lambda sptr, o, m: self._issue_h2g(b, sptr, dst_ptr + o, m, dst_gpu, after,
+                                                                           slot))
+
+    def _ring(self) -> "_PinnedRing":
+        if self._pinned_ring is None:
+            from .pcie_sched import default_ring_capacity
+            cap = default_ring_capacity(len(self.topo.roots()), self.batch_chunks * self.chunk_bytes)
+            self._pinned_ring = _PinnedRing(cap, self.chunk_bytes)
+        return self._pinned_ring
 
     # -------------------------------------------------- live bandwidth-share scheduler
     def _deliver_due(self, arb: StageArbiter):
@@ -666,8 +695,7 @@ class FaaSTube:
                 take = min(n - done[i], int(batch * n / obj.nbytes) // _ALIGN * _ALIGN or n - done[i])
                 if take <= 0:
                     continue
-                evs.append(self._issue_h2g(b, host_ptr + off + done[i], dst_ptr + off + done[i], take, dst.gpu, s,
-                                           slot))
+                evs += self._h2g_range(b, obj.host, off + done[i], take, dst_ptr + off + done[i], dst.gpu, s, slot)
                 done[i] += take
             inflight.extend(evs)
             next_t += dur
@@ -694,6 +722,46 @@ class FaaSTube:
         ev.synchronize()
         self.stats["bytes_d2h"] += obj.nbytes
         return res
+
+
+class _PinnedRing:
+    """Circular pinned staging buffer shared by all functions (pcie_sched.py:122-162,
+    PAPER.md:620): 2 x batch x PCIe roots bytes in chunk-sized slots. A pageable
+    payload is copied into a free slot by host threads and DMA'd from there;
+    a slot is reused once its DMA event completes, so the host copy of chunk
+    k+1 overlaps the DMA of chunk k and only the ring is ever pinned."""
+
+    def __init__(self, capacity: int, chunk: int):
+        from concurrent.futures import ThreadPoolExecutor
+        self.chunk = int(chunk)
+        self.slots = max(4, int(capacity) // self.chunk)
+        self.buf = torch.empty(self.slots * self.chunk, dtype=torch.uint8).pin_memory()
+        self.events = [None] * self.slots
+        self.next = 0
+        self.lock = threading.Lock()
+        self.workers = ThreadPoolExecutor(4, thread_name_prefix="faastube-ring")
+
+    def _one(self, host, o, m, issue):
+        with self.lock:
+            k = self.next
+            self.next = (k + 1) % self.slots
+            prev = self.events[k]
+            self.events[k] = None
+        if prev is not None:
+            prev.synchronize()                       # the slot's previous DMA has drained it
+        view = self.buf[k * self.chunk: k * self.chunk + m]
+        view.copy_(host[o:o + m])
+        ev = issue(view.data_ptr(), o, m)
+        with self.lock:
+            self.events[k] = ev
+        return ev
+
+    def stage(self, host: torch.Tensor, off: int, n: int, issue) -> list:
+        """issue(slot_ptr, offset_within_range, nbytes) -> event; returns the events."""
+        jobs = [(off + o, min(self.chunk, n - o), o) for o in range(0, n, self.chunk)]
+        futs = [self.workers.submit(self._one, host, a, m, lambda p, _o, mm, rel=rel: issue(p, rel, mm))
+                for a, m, rel in jobs]
+        return [f.result() for f in futs]
 
 
 def _sleep_until(t_ms, clock):
