@@ -33,6 +33,7 @@ import ctypes as C
 import heapq
 import itertools
 import math
+import os
 import threading
 import time
 import weakref
@@ -116,6 +117,7 @@ class FaaSTube:
         self._ce_rr = itertools.count()
         self._staging = {}
         self._pinned_ring = None     # shared warm staging ring for pageable host payloads
+        self._trace = [] if os.environ.get("FT_TRACE") else None   # managed-stage issue log
         self._pending_release = []   # (event, plan): NVLink claims held until the copy lands
         self._shrink_due = []        # heap of (due_ms, gpu)
         self._managed_ids = itertools.count(1)
@@ -669,7 +671,10 @@ class FaaSTube:
         done = [0] * len(br)
         inflight = []
         next_t = None
-        host_ptr, dst_ptr = obj.host.data_ptr(), res.data_ptr()
+        last_rate = None
+        dst_ptr = res.data_ptr()
+        if self._trace is not None:
+            self._trace.append((self.now_ms(), key, "start", obj.nbytes))
         while any(done[i] < ranges[i][1] for i in range(len(br))):
             with self._sched_lock:
                 self._deliver_due(arb)
@@ -682,8 +687,13 @@ class FaaSTube:
                     self._sched_cv.wait(max(0.0, (nxt - now) / 1e3) if nxt is not None else 0.002)
                 continue
             dur = batch / (st["rate"] * 1e6)              # ms per batch at the stage rate
-            if next_t is None:
-                next_t = now
+            if next_t is None or st["rate"] != last_rate:
+                # (re)anchor the issue schedule when the rate changes: a stage that
+                # was paced slowly must not keep waiting on its old, far-out slot
+                next_t = now if next_t is None else min(next_t, now + dur)
+                last_rate = st["rate"]
+                if self._trace is not None:
+                    self._trace.append((now, key, "rate", st["rate"]))
             if now < next_t - dur:                          # one batch of lookahead keeps the CE busy
                 _sleep_until(min(next_t - dur, nxt if nxt is not None else next_t), self.now_ms)
                 continue
@@ -699,6 +709,8 @@ class FaaSTube:
                 done[i] += take
             inflight.extend(evs)
             next_t += dur
+            if self._trace is not None:
+                self._trace.append((now, key, "issue", sum(done)))
         for ev in inflight:
             ev.synchronize()
         with self._sched_lock:
