@@ -186,10 +186,13 @@ def run_ours(args):
     import torch.distributed as dist
 
     rank, world, local = dist_env()
+    ndev = torch.cuda.device_count()
+    shared = world > ndev          # more ranks than GPUs (path smoke test): ranks share devices
     if world > 1:
-        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
-    torch.cuda.set_device(local)
-    g = local
+        # only barriers and one max-reduction of timings go through the process group
+        dist.init_process_group("gloo" if shared else "nccl")
+    g = local % ndev
+    torch.cuda.set_device(g)
     from paper_2411_01830_b200 import device as dev
     from paper_2411_01830_b200.tube import FaaSTube
 
@@ -200,8 +203,23 @@ def run_ours(args):
     inp = torch.empty_like(x)                                                # consumer input buffer
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=f"cuda:{g}")
     s = torch.cuda.current_stream(g)
+    pair, pair_error = None, None
+    if world > 1:
+        # N > 1: rank r's producer hands its output to rank r+1's consumer over
+        # NVLink (exported pool block + device doorbells) — pairs.CrossPair
+        try:
+            from paper_2411_01830_b200.pairs import CrossPair
+            sock_dir = f"/tmp/ft_bench_{os.environ.get('MASTER_PORT', '0')}"
+            os.makedirs(sock_dir, exist_ok=True)
+            pair = CrossPair(tube, g, rank, world, sock_dir, nbytes, dist.barrier)
+        except Exception as exc:  # noqa: BLE001 - reported; falls back to same-GPU replicas
+            pair_error = repr(exc)
 
     def one_pass():
+        if pair is not None:
+            pair.produce(x)
+            pair.consume(inp)
+            return
         did = tube.unique_id()
         tube.store(did, x, producer="producer")
         tube.fetch(did, device=g, out=inp, consumer="consumer")
@@ -242,6 +260,8 @@ def run_ours(args):
     total_ms = sum(per_ms)
     copies = (tube.stats["bytes_local"] - launches0) // nbytes
     gpu_launches = int(copies)                       # one k_copy_bulk per store + one per fetch
+    if pair is not None:                             # wait+copy+signal on each side
+        gpu_launches = 6 * args.steps
     assert torch.equal(inp.view(torch.uint8), x.view(torch.uint8)), "delivered bytes differ"
 
     # ---- dominant kernel: k_copy_bulk on the same buffers, CUDA events on its stream
@@ -299,7 +319,8 @@ def run_ours(args):
     e2e_gbps = nbytes / statistics.mean(e2e) / 1e9
 
     # ---- aggregate over ranks (max time)
-    t_tensor = torch.tensor([total_ms, statistics.mean(e2e)], dtype=torch.float64, device=f"cuda:{g}")
+    t_tensor = torch.tensor([total_ms, statistics.mean(e2e)], dtype=torch.float64,
+                            device="cpu" if shared else f"cuda:{g}")
     if world > 1:
         dist.all_reduce(t_tensor, op=dist.ReduceOp.MAX)
     total_ms_max, e2e_max = t_tensor.tolist()
@@ -314,9 +335,12 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": round(total_ms_max / args.steps, 5), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
             "config": {"workload": "config1: 2-function pipeline, producer store(64 MiB fp16) -> consumer "
-                                   "fetch(into its input buffer), same GPU per rank",
+                                   + ("fetch(into its input buffer), same GPU" if pair is None else
+                                      "on the next rank's GPU: pull over NVLink from the exported pool block, "
+                                      "device doorbells (pairs.CrossPair)"),
                        "payload_bytes": nbytes, "strategy": "faastube", "l2": "flushed before each pass (256 MiB write + read, outside the timed pass)",
-                       "parallelism": f"replicas x{world}"},
+                       "parallelism": f"replicas x{world}" if pair is None else f"ring of {world} producer->consumer pairs",
+                       **({"cross_gpu_setup_error": pair_error} if pair_error else {})},
             "p50_pass_ms": round(nearest_rank(per_ms, 50), 5), "p99_pass_ms": round(nearest_rank(per_ms, 99), 5),
             "e2e": {"value": round(world * nbytes / e2e_max / 1e9, 3), "unit": "GB/s",
                     "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": 16,
@@ -340,6 +364,8 @@ def run_ours(args):
                                     "p99_pass_ms": round(cpu["pass_ms_p99"], 3)}
         line.update(extras)
         print(json.dumps(line), flush=True)
+    if pair is not None:
+        pair.close()
     tube.close()
     if world > 1:
         dist.destroy_process_group()

@@ -303,6 +303,12 @@ int ft_copy_ex(void* dst, const void* src, uint64_t bytes, int device, void* str
  * (0 evict_normal, 1 evict_first, 2 evict_last) — e.g. a store keeps the pool block
  * L2-resident (dst evict_last) for a same-GPU fetch that follows.            */
 int ft_copy_hint(void* dst, const void* src, uint64_t bytes, int device, void* stream, uint32_t hints);
+/* stream-ordered doorbells on (peer-)mapped device memory (cross-process handoff
+ * without host round trips): ft_signal stores `value` with system-scope release
+ * after all prior work on `stream`; ft_wait parks `stream` until *flag >= value
+ * (wrap-around compare). */
+int ft_signal(uint32_t* flag, uint32_t value, int device, void* stream);
+int ft_wait(const uint32_t* flag, uint32_t value, int device, void* stream);
 /* position-keyed digest of `bytes` (u64 sum of mixed words + xor), device u64[2] out */
 int ft_fingerprint(const void* src, uint64_t bytes, uint64_t* out_dev, int device, void* stream);
 /* host-side digest of the same definition (for checking against ft_fingerprint) */

@@ -222,6 +222,8 @@ _SIGS = {
     "ft_copy": (None, [vp, vp, u64, C.c_int, vp]),
     "ft_copy_ex": (None, [vp, vp, u64, C.c_int, vp, C.c_int, C.c_int]),
     "ft_copy_hint": (None, [vp, vp, u64, C.c_int, vp, C.c_uint32]),
+    "ft_signal": (None, [vp, C.c_uint32, C.c_int, vp]),
+    "ft_wait": (None, [vp, C.c_uint32, C.c_int, vp]),
     "ft_fingerprint": (None, [vp, u64, vp, C.c_int, vp]),
     "ft_fingerprint_host": (None, [vp, u64, P(u64)]),
     "ft_pcie_copy": (None, [vp, vp, u64, C.c_int, C.c_int, vp, u64]),

