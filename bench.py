@@ -507,6 +507,9 @@ def run_workflows(dur_s=2.0):
 
 
 def main():
+    import faulthandler
+    import signal
+    faulthandler.register(signal.SIGUSR1, all_threads=True)   # `timeout -s USR1` dumps a hung run
     args = parse()
     if args.impl == "reference":
         run_reference(args)

@@ -43,7 +43,8 @@ enum ft_status {
   FT_E_VALUE = 8,         /* ValueError (bad argument)         e.g. datastore.py:27 */
   FT_E_TRUNCATED = 9,     /* caller buffer too small */
   FT_E_KEY = 10,          /* KeyError (unknown id / func) */
-  FT_E_NOT_SUPPORTED = 11 /* feature unavailable on this device/driver */
+  FT_E_NOT_SUPPORTED = 11, /* feature unavailable on this device/driver */
+  FT_E_TIMEOUT = 12        /* a host wait ran out of time */
 };
 
 #define FT_MAX_PATH 8   /* GPUs per NVLink path (MAX_HOPS 4 => 5)  nvlink_sched.py:17 */
@@ -328,6 +329,51 @@ int ft_pcie_copy(void* dst, const void* src, uint64_t bytes, int to_device, int 
 int ft_h2g_striped(void* dst, int dst_dev, const void* host_src, uint64_t bytes, int k, const int32_t* stage_dev,
                    const uint64_t* off, const uint64_t* len, void* const* staging, uint64_t chunk_bytes,
                    int ring_chunks, void* const* streams);
+
+/* ---- live PCIe mover + bandwidth-share scheduler (native runtime)
+ * Replaces the engine's managed-stage loop (engine.py:537-646) and the pinned
+ * staging ring (pcie_sched.py:122-162) on real copy engines. Every host->GPU
+ * leg of a fetch is one stage of k routes (dataplane.py:203-250 / _pcie_branches):
+ * route i moves [off, off+len) of the host object into dst, straight by the CE
+ * of dst's own root (stage_dev == dst_dev) or through a chunk ring on stage_dev
+ * with an NVLink forward kernel (fw_stream) into dst. Managed stages join the
+ * arbiter's SLO partition and are issued in 5 x 2 MB batches at the stage rate,
+ * rate changes on batch boundaries, finished when the last byte lands;
+ * unmanaged stages are issued at once. submit() never blocks the host: it
+ * parks `consumer_stream` (cuStreamWaitValue32) until the stage's completion
+ * word is written after its last byte; route streams first wait for
+ * `consumer_stream`'s prior work. Pageable host objects (host_pinned = 0) go
+ * through the shared pinned ring (host_ring_bytes, worker threads). The caller
+ * keeps host and dst alive until ft_pacer_done reports the ticket. Thread-safe. */
+typedef struct ft_pacer ft_pacer;
+typedef struct {
+  int32_t stage_dev;     /* GPU whose PCIe link carries the route (== dst_dev: direct)   */
+  int32_t force_staging; /* stage through the ring even when stage_dev == dst_dev      */
+  uint64_t off, len;     /* byte range of the object                                     */
+  void* ce_stream;       /* cudaStream_t on stage_dev for the PCIe leg                   */
+  void* fw_stream;       /* cudaStream_t on stage_dev for the NVLink forward (staged)    */
+} ft_route;
+/* bw_all = pcie_gbps x roots (engine.py:186-190); staging_slots chunk slots per staging GPU */
+int ft_pacer_create(double bw_all_gbps, int batch_chunks, int64_t chunk_bytes, int staging_slots,
+                    uint64_t host_ring_bytes, int logging, ft_pacer** out);
+/* drains in-flight stages (FT_E_TIMEOUT after 120 s: remaining stages are failed) */
+int ft_pacer_destroy(ft_pacer* p);
+/* _start_edge_transfer -> _run_stage for a host_gpu plan       engine.py:440-475, 537-575 */
+int ft_pacer_submit(ft_pacer* p, const char* key, int managed, double slo_ms, double infer_ms,
+                    double per_branch_cap_gbps, void* dst, int dst_dev, const void* host, uint64_t bytes,
+                    int host_pinned, int k, const ft_route* routes, void* consumer_stream, uint64_t* ticket);
+/* host wait for a ticket's last byte (timeout_ms < 0: forever); returns the stage's status */
+int ft_pacer_wait(ft_pacer* p, uint64_t ticket, double timeout_ms);
+int ft_pacer_done(ft_pacer* p, uint64_t ticket, int* done);
+/* out[0..6] = stages, managed stages, batches, bytes issued, active, failed, blocking-mode */
+int ft_pacer_stats(ft_pacer* p, uint64_t* out, int cap);
+int ft_pacer_now_ms(ft_pacer* p, double* out);
+/* logging = 1: [[t, ticket, "start"|"rate"|"issue"|"land", value], ...] */
+int ft_pacer_trace_json(ft_pacer* p, char* buf, size_t cap, size_t* need);
+/* logging = 1: every arbiter call [[t, "start"|"boundary"|"finish", key, decisions], ...] (replayable) */
+int ft_pacer_log_json(ft_pacer* p, char* buf, size_t cap, size_t* need);
+/* arbiter state, as ft_arbiter_state_json */
+int ft_pacer_state_json(ft_pacer* p, char* buf, size_t cap, size_t* need);
 
 #ifdef __cplusplus
 }

@@ -63,6 +63,10 @@ class NotSupported(RuntimeError):
     pass
 
 
+class WaitTimeout(TimeoutError):
+    pass
+
+
 _ERRORS = {
     1: TopologyError,
     2: InfeasibleDemand,
@@ -75,6 +79,7 @@ _ERRORS = {
     9: Truncated,
     10: KeyError,
     11: NotSupported,
+    12: WaitTimeout,
 }
 
 i32, i64, u64, dbl, sz = C.c_int32, C.c_int64, C.c_uint64, C.c_double, C.c_size_t
@@ -99,6 +104,11 @@ class StrategyC(C.Structure):
 
 class LinkC(C.Structure):
     _fields_ = [("kind", i32), ("a", i32), ("b", i32)]
+
+
+class RouteC(C.Structure):
+    _fields_ = [("stage_dev", i32), ("force_staging", i32), ("off", u64), ("len", u64), ("ce_stream", vp),
+                ("fw_stream", vp)]
 
 
 class BranchC(C.Structure):
@@ -229,6 +239,18 @@ _SIGS = {
     "ft_pcie_copy": (None, [vp, vp, u64, C.c_int, C.c_int, vp, u64]),
     "ft_h2g_striped": (None, [vp, C.c_int, vp, u64, C.c_int, P(i32), P(u64), P(u64), P(vp), u64, C.c_int,
                               P(vp)]),
+    # live PCIe mover + bandwidth-share scheduler
+    "ft_pacer_create": (None, [dbl, C.c_int, i64, C.c_int, u64, C.c_int, P(vp)]),
+    "ft_pacer_destroy": (None, [vp]),
+    "ft_pacer_submit": (None, [vp, cstr, C.c_int, dbl, dbl, dbl, vp, C.c_int, vp, u64, C.c_int, C.c_int,
+                               P(RouteC), vp, P(u64)]),
+    "ft_pacer_wait": (None, [vp, u64, dbl]),
+    "ft_pacer_done": (None, [vp, u64, P(C.c_int)]),
+    "ft_pacer_stats": (None, [vp, P(u64), C.c_int]),
+    "ft_pacer_now_ms": (None, [vp, P(dbl)]),
+    "ft_pacer_trace_json": (None, [vp, C.c_char_p, sz, P(sz)]),
+    "ft_pacer_log_json": (None, [vp, C.c_char_p, sz, P(sz)]),
+    "ft_pacer_state_json": (None, [vp, C.c_char_p, sz, P(sz)]),
 }
 
 HEADER_SYMBOLS = tuple(_SIGS)

@@ -1,0 +1,827 @@
+// Live PCIe mover + per-function bandwidth-share scheduler (native runtime).
+//
+// Every host->GPU leg of a fetch is submitted here as a *stage* of k routes
+// (dataplane.py:203-250): route i moves bytes [off_i, off_i+len_i) of the host
+// object either straight into dst on the copy engine of the target's own PCIe
+// root, or into a chunk ring on a staging GPU followed by an NVLink forward
+// (ft_copy_ex, vector engine) into dst, chained per chunk by events.
+//
+// Managed stages (strategy.pcie_sched; engine.py:537-646) are paced by one
+// pacer thread: the stage enters the arbiter's SLO partition (ft::Arbiter, the
+// restated engine logic, pcie_sched.py:80-104) and its bytes are issued batch
+// by batch (batch = 5 x 2 MB, pcie_sched.py:14-15) at the stage's rate, with
+// rate changes landing on batch boundaries (engine.py:628-646); the stage is
+// finished in the arbiter when its last byte has landed (host callback), which
+// re-partitions the link for the others (engine.py:558-564). Unmanaged stages
+// are issued at once.
+//
+// submit() returns once every byte of the stage is enqueued on its route
+// streams (for a paced stage: when its last batch is issued, a few batches
+// before it lands) and makes the consumer's stream wait for the routes' last
+// ops, so consumer kernels issued after fetch() are ordered after the data —
+// the same stream semantics as the SM-driven movers, and the tail of the
+// transfer overlaps whatever the caller issues next. No stream is ever parked
+// on host progress (a parked stream would deadlock against lazy module
+// loading, which synchronizes the context).
+//
+// Pageable host objects are staged through one shared pinned ring
+// (PinnedRing, pcie_sched.py:122-162) by worker threads; a slot
+// is refilled once the DMA that drained it has completed.
+//
+// Locking: `mu` guards all scheduling state and is held while enqueueing
+// async CUDA work only (never a synchronizing call). Host callbacks take only
+// `lmu`. Workers wait on ring slots without holding `mu`.
+#include <cuda_runtime.h>
+#include <sys/prctl.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <condition_variable>
+#include <cstring>
+#include <deque>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <thread>
+
+#include "decisions.h"
+
+namespace {
+
+constexpr uint64_t kAlign = 256;     // route slice boundaries (tube._ALIGN)
+constexpr int kInflightBatches = 4;  // issued-but-not-landed batches per stage
+constexpr double kLookahead = 2.0;   // batches issued ahead of the rate schedule (host jitter)
+constexpr int kMaxDev = 64;
+constexpr int kWorkers = 4;          // pageable staging threads
+
+struct DevGuard {
+  int prev = -1;
+  explicit DevGuard(int d) {
+    cudaGetDevice(&prev);
+    if (prev != d) cudaSetDevice(d);
+  }
+  ~DevGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+struct CudaFail {
+  std::string msg;
+};
+inline void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw CudaFail{std::string(what) + ": " + cudaGetErrorString(e)};
+}
+
+struct Route {
+  int dev = 0;                  // GPU the PCIe leg lands on (== dst_dev for a direct route)
+  uint64_t off = 0, len = 0;    // byte range of the object
+  uint64_t done = 0;            // bytes handed out (issued, or queued to a worker)
+  cudaStream_t ce = nullptr;    // copy-engine stream on `dev`
+  cudaStream_t fw = nullptr;    // forward stream on `dev` (staged routes only)
+  bool staged() const { return fw != nullptr; }
+  cudaStream_t last() const { return staged() ? fw : ce; }
+};
+
+struct Stage {
+  uint64_t ticket = 0;
+  std::string key;
+  bool managed = false;
+  uint8_t* dst = nullptr;
+  int dst_dev = 0;
+  const uint8_t* host = nullptr;
+  bool pinned = true;
+  uint64_t bytes = 0;
+  std::vector<Route> routes;
+  double next_t = NAN, last_rate = -1.0;
+  std::deque<std::vector<std::pair<cudaEvent_t, int>>> inflight;  // per issued batch: (event, device)
+  int jobs = 0;         // pageable chunks queued to workers, not yet issued
+  bool issued = false;  // every byte handed out
+  bool sealed = false;  // every byte enqueued: join events recorded (or failed)
+  std::vector<std::pair<cudaEvent_t, int>> join;  // last op of each route
+  int err = FT_OK;
+  std::string msg;
+};
+
+struct Job {
+  uint64_t ticket;
+  int route;
+  uint64_t obj_off, n;  // bytes [obj_off, obj_off+n) of the object, n <= chunk
+};
+
+struct StagingRing {  // chunk ring on a staging GPU
+  uint8_t* buf = nullptr;
+  int slots = 0, next = 0;
+  std::vector<cudaEvent_t> landed, freed;
+  std::vector<char> used;
+};
+
+struct HostSlot {
+  bool busy = false;
+  int last_dev = -1;  // device of the event guarding the slot's last DMA
+  cudaEvent_t ev[kMaxDev] = {};
+};
+
+std::string jnum(double x) {
+  if (std::isnan(x)) return "null";
+  char b[40];
+  snprintf(b, sizeof b, "%.17g", x);
+  return b;
+}
+
+}  // namespace
+
+struct ft_pacer {
+  // ---- configuration
+  int batch_chunks = 5;
+  uint64_t chunk = 2000000;
+  int staging_slots = 4;
+  bool logging = false;
+  ft::Arbiter arb;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+
+  // ---- state (mu)
+  std::mutex mu;
+  std::condition_variable cv;       // pacer thread
+  std::condition_variable done_cv;  // waiters
+  std::condition_variable jcv;      // workers
+  std::map<uint64_t, std::shared_ptr<Stage>> active;  // ticket order == submission order
+  uint64_t next_ticket = 1;
+  std::map<uint64_t, std::pair<int, std::string>> errors;
+  std::deque<Job> jobs;
+  bool stop = false;
+  std::vector<cudaEvent_t> evpool[kMaxDev];
+  std::map<int, StagingRing> rings;
+  std::map<std::string, double> guarded;  // last early boundary per stage key (A2 guard)
+  uint64_t n_stages = 0, n_managed = 0, n_batches = 0, n_bytes = 0, n_errors = 0;
+  std::vector<std::string> trace, log;
+
+  // ---- landed callbacks (lmu only)
+  std::mutex lmu;
+  std::vector<uint64_t> landed;
+
+  // ---- pinned host ring (hmu only)
+  std::mutex hmu;
+  std::condition_variable hcv;
+  uint8_t* hring = nullptr;
+  std::vector<HostSlot> hslots;
+  int hnext = 0;
+
+  std::thread pacer;
+  std::vector<std::thread> workers;
+
+  double now() const {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  }
+
+  // ------------------------------------------------------------ helpers (mu held)
+  cudaEvent_t get_event(int dev) {
+    auto& pool = evpool[dev];
+    if (!pool.empty()) {
+      cudaEvent_t e = pool.back();
+      pool.pop_back();
+      return e;
+    }
+    DevGuard g(dev);
+    cudaEvent_t e;
+    ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+    return e;
+  }
+  void put_event(int dev, cudaEvent_t e) { evpool[dev].push_back(e); }
+
+  void note(const Stage& st, const char* kind, double v) {
+    if (!logging) return;
+    trace.push_back("[" + jnum(now()) + "," + std::to_string(st.ticket) + ",\"" + kind + "\"," + jnum(v) + "]");
+  }
+  void arb_log(double t, const char* call, const std::string& key) {
+    if (!logging) return;
+    log.push_back("[" + jnum(t) + ",\"" + call + "\",\"" + key + "\"," + arb.last_json + "]");
+  }
+
+  StagingRing& ring(int dev) {
+    auto it = rings.find(dev);
+    if (it != rings.end()) return it->second;
+    StagingRing r;
+    DevGuard g(dev);
+    void* p = nullptr;
+    ck(cudaMalloc(&p, (size_t)staging_slots * chunk), "staging ring cudaMalloc");
+    r.buf = static_cast<uint8_t*>(p);
+    r.slots = staging_slots;
+    r.landed.resize(r.slots);
+    r.freed.resize(r.slots);
+    r.used.assign(r.slots, 0);
+    for (int i = 0; i < r.slots; ++i) {
+      ck(cudaEventCreateWithFlags(&r.landed[i], cudaEventDisableTiming), "cudaEventCreate");
+      ck(cudaEventCreateWithFlags(&r.freed[i], cudaEventDisableTiming), "cudaEventCreate");
+    }
+    return rings.emplace(dev, std::move(r)).first->second;
+  }
+
+  // bytes [src, src+n) (pinned host) -> dst over route r
+  void issue(Route& r, uint8_t* dst, const uint8_t* src, uint64_t n) {
+    if (n == 0) return;
+    DevGuard g(r.dev);
+    if (!r.staged()) {
+      ck(cudaMemcpyAsync(dst, src, n, cudaMemcpyHostToDevice, r.ce), "H2D");
+      n_bytes += n;
+      return;
+    }
+    StagingRing& R = ring(r.dev);
+    for (uint64_t o = 0; o < n; o += chunk) {
+      uint64_t c = std::min<uint64_t>(chunk, n - o);
+      int s = R.next;
+      R.next = (s + 1) % R.slots;
+      if (R.used[s]) ck(cudaStreamWaitEvent(r.ce, R.freed[s], 0), "wait slot freed");  // forward drained it
+      uint8_t* slot = R.buf + (uint64_t)s * chunk;
+      ck(cudaMemcpyAsync(slot, src + o, c, cudaMemcpyHostToDevice, r.ce), "staging H2D");
+      ck(cudaEventRecord(R.landed[s], r.ce), "record landed");
+      ck(cudaStreamWaitEvent(r.fw, R.landed[s], 0), "wait landed");
+      int rc = ft_copy_ex(dst + o, slot, c, r.dev, r.fw, 2, 0);  // NVLink push, vector engine
+      if (rc != FT_OK) throw CudaFail{std::string("forward: ") + ft_last_error()};
+      ck(cudaEventRecord(R.freed[s], r.fw), "record freed");
+      R.used[s] = 1;
+      n_bytes += c;
+    }
+  }
+
+  // hand bytes [rel, rel+n) of route i to the movers (direct DMA or worker jobs)
+  void hand_out(Stage& st, int i, uint64_t rel, uint64_t n, bool track) {
+    Route& r = st.routes[i];
+    uint64_t o = r.off + rel;
+    if (st.pinned) {
+      issue(r, st.dst + o, st.host + o, n);
+      if (track) {
+        DevGuard g(r.dev);
+        cudaEvent_t e = get_event(r.dev);
+        ck(cudaEventRecord(e, r.last()), "record batch");
+        st.inflight.back().emplace_back(e, r.dev);
+      }
+      return;
+    }
+    for (uint64_t k = 0; k < n; k += chunk) {
+      jobs.push_back(Job{st.ticket, i, o + k, std::min<uint64_t>(chunk, n - k)});
+      ++st.jobs;
+    }
+    jcv.notify_all();
+  }
+
+  void release_inflight(Stage& st) {
+    for (auto& b : st.inflight)
+      for (auto& e : b) put_event(e.second, e.first);
+    st.inflight.clear();
+  }
+
+  // every byte is on a stream: record each route's last op (the submitter makes
+  // the consumer stream wait on them) and call back when all have landed
+  void seal(Stage& st) {
+    if (st.sealed) return;
+    for (auto& r : st.routes) {
+      DevGuard g(r.dev);
+      cudaEvent_t e = get_event(r.dev);
+      ck(cudaEventRecord(e, r.last()), "record join");
+      st.join.emplace_back(e, r.dev);
+    }
+    Route& r0 = st.routes[0];
+    cudaStream_t j = r0.last();
+    DevGuard g(r0.dev);
+    for (size_t i = 1; i < st.join.size(); ++i) ck(cudaStreamWaitEvent(j, st.join[i].first, 0), "join");
+    auto* ctx = new std::pair<ft_pacer*, uint64_t>(this, st.ticket);
+    cudaError_t e = cudaLaunchHostFunc(j, &ft_pacer::on_landed, ctx);
+    if (e != cudaSuccess) {
+      delete ctx;
+      ck(e, "cudaLaunchHostFunc");
+    }
+    st.sealed = true;
+    done_cv.notify_all();
+  }
+
+  static void on_landed(void* p) {  // driver callback thread: no CUDA calls, lmu only
+    auto* c = static_cast<std::pair<ft_pacer*, uint64_t>*>(p);
+    {
+      std::lock_guard<std::mutex> lk(c->first->lmu);
+      c->first->landed.push_back(c->second);
+    }
+    c->first->cv.notify_all();
+    delete c;
+  }
+
+  // a stage that cannot finish on its streams: once no worker still reads its
+  // host object, release its waiters from the host
+  void fail(Stage& st, const std::string& msg) {
+    if (st.err == FT_OK) {
+      st.err = FT_E_CUDA;
+      st.msg = msg;
+    }
+    st.issued = true;
+    if (!st.sealed && st.jobs == 0) {
+      st.sealed = true;
+      {
+        std::lock_guard<std::mutex> lk(lmu);
+        landed.push_back(st.ticket);
+      }
+      cv.notify_all();
+      done_cv.notify_all();
+    }
+  }
+
+  void issue_batch(Stage& st) {  // one 5 x 2 MB batch split over the routes by byte share
+    const double batch = (double)batch_chunks * (double)chunk;
+    if (st.pinned) st.inflight.emplace_back();
+    bool all = true;
+    for (size_t i = 0; i < st.routes.size(); ++i) {
+      Route& r = st.routes[i];
+      if (r.done >= r.len) continue;
+      uint64_t share = (uint64_t)(batch * (double)r.len / (double)st.bytes) / kAlign * kAlign;
+      uint64_t take = std::min<uint64_t>(r.len - r.done, share ? share : r.len - r.done);
+      hand_out(st, (int)i, r.done, take, true);
+      r.done += take;
+      if (r.done < r.len) all = false;
+    }
+    ++n_batches;
+    note(st, "issue", (double)done_bytes(st));
+    if (all) {
+      st.issued = true;
+      if (st.jobs == 0) seal(st);
+    }
+  }
+  static uint64_t done_bytes(const Stage& st) {
+    uint64_t s = 0;
+    for (auto& r : st.routes) s += r.done;
+    return s;
+  }
+
+  void deliver_due(double now) {  // engine.py:628-646, fired at their armed times
+    for (;;) {
+      double best = NAN;
+      const std::string* bk = nullptr;
+      for (auto& kv : arb.stages.items)
+        if (!std::isnan(kv.second.armed) && (std::isnan(best) || kv.second.armed < best)) {
+          best = kv.second.armed;
+          bk = &kv.first;
+        }
+      if (!bk || best > now) return;
+      std::string key = *bk;
+      arb.boundary(best, key);
+      arb_log(best, "boundary", key);
+    }
+  }
+  // Live guard for reference defect A2: a stage running at a
+  // near-zero rate (least rate of a loose SLO, or the 1e12 ms infeasible fallback)
+  // re-arms its next boundary one batch *at that rate* away — hours — so a rate
+  // increase handed to it when the link frees up would never apply and the stage
+  // starves. The engine only needs rate changes to land on batch boundaries; live,
+  // a pending change applies no later than two batches at the higher of the two
+  // rates. Decreases are never early (their boundary is within one batch already).
+  void guard_pending(double now) {
+    std::vector<std::string> due;
+    for (auto& kv : arb.stages.items) {
+      const auto& m = kv.second;
+      if (!m.started || std::isnan(m.pending) || std::isnan(m.armed)) continue;
+      double allowed = 2.0 * arb.batch_bytes / (std::max(m.pending, m.rate) * 1e6);
+      auto g = guarded.find(kv.first);
+      if (m.armed - now > allowed && (g == guarded.end() || now - g->second >= 0.5 * allowed)) due.push_back(kv.first);
+    }
+    for (auto& key : due) {
+      guarded[key] = now;
+      arb.boundary(now, key);
+      arb_log(now, "boundary", key);
+      if (logging) trace.push_back("[" + jnum(now) + ",0,\"guard\",0]");
+    }
+  }
+
+  double next_armed() const {
+    double best = NAN;
+    for (auto& kv : arb.stages.items)
+      if (!std::isnan(kv.second.armed) && (std::isnan(best) || kv.second.armed < best)) best = kv.second.armed;
+    return best;
+  }
+
+  void retire_landed() {
+    std::vector<uint64_t> L;
+    {
+      std::lock_guard<std::mutex> lk(lmu);
+      L.swap(landed);
+    }
+    if (L.empty()) return;
+    double t = now();
+    for (uint64_t tk : L) {
+      auto it = active.find(tk);
+      if (it == active.end()) continue;
+      Stage& st = *it->second;
+      if (st.managed) {
+        arb.finish(t, st.key);
+        arb_log(t, "finish", st.key);
+        guarded.erase(st.key);
+      }
+      note(st, "land", (double)st.bytes);
+      release_inflight(st);  // join events are returned by the submitter
+      if (st.err != FT_OK) {
+        errors[tk] = {st.err, st.msg};
+        ++n_errors;
+      }
+      active.erase(it);
+    }
+    done_cv.notify_all();
+  }
+
+  // ------------------------------------------------------------ pacer thread
+  void run() {
+    prctl(PR_SET_TIMERSLACK, 1000UL, 0, 0, 0);  // 1 us timer slack: batch slots are ~0.2 ms
+    std::unique_lock<std::mutex> lk(mu);
+    const double batch = (double)batch_chunks * (double)chunk;
+    for (;;) {
+      retire_landed();
+      if (stop && active.empty()) return;
+      double t = now();
+      deliver_due(t);
+      guard_pending(t);
+      double wake = INFINITY;
+      bool waiting_land = false;
+      for (auto& kv : active) {
+        Stage& st = *kv.second;
+        if (st.sealed) {
+          waiting_land = true;
+          continue;
+        }
+        if (!st.managed || st.issued) continue;
+        while (!st.inflight.empty()) {  // drop landed batches (non-blocking)
+          bool ok = true;
+          for (auto& e : st.inflight.front())
+            if (cudaEventQuery(e.first) != cudaSuccess) ok = false;
+          if (!ok) break;
+          for (auto& e : st.inflight.front()) put_event(e.second, e.first);
+          st.inflight.pop_front();
+        }
+        const auto* m = arb.stages.find(st.key);
+        if (!m || !m->started || m->rate <= 0) continue;  // waiting: a boundary / finish / start wakes it
+        double dur = batch / (m->rate * 1e6);             // ms per batch at the stage rate
+        if (std::isnan(st.next_t) || m->rate != st.last_rate) {
+          // (re)anchor on rate changes: a stage paced slowly must not keep its far-out slot
+          st.next_t = std::isnan(st.next_t) ? t : std::min(st.next_t, t + dur);
+          st.last_rate = m->rate;
+          note(st, "rate", m->rate);
+        }
+        if (t < st.next_t - kLookahead * dur) {
+          wake = std::min(wake, st.next_t - kLookahead * dur);
+          continue;
+        }
+        bool full = st.pinned ? (int)st.inflight.size() >= kInflightBatches : st.jobs >= 2 * batch_chunks;
+        if (full) {
+          wake = std::min(wake, t + 0.02);
+          continue;
+        }
+        try {
+          issue_batch(st);
+        } catch (const CudaFail& f) {
+          fail(st, f.msg);
+        } catch (const ft::Error& e) {
+          fail(st, e.what());
+        }
+        st.next_t += dur;
+        wake = t;  // re-evaluate at once (lookahead may allow another batch)
+      }
+      double armed = next_armed();
+      if (!std::isnan(armed)) wake = std::min(wake, armed);
+      if (waiting_land) wake = std::min(wake, t + 0.1);  // a landed notify may race our wait
+      if (wake <= t) continue;
+      if (std::isinf(wake)) {
+        if (active.empty())
+          cv.wait(lk);
+        else
+          cv.wait_for(lk, std::chrono::milliseconds(5));
+      } else {
+        cv.wait_for(lk, std::chrono::duration<double, std::milli>(wake - t));
+      }
+    }
+  }
+
+  // ------------------------------------------------------------ workers (pageable)
+  void work() {
+    for (;;) {
+      Job j;
+      {
+        std::unique_lock<std::mutex> lk(mu);
+        jcv.wait(lk, [&] { return stop || !jobs.empty(); });
+        if (jobs.empty()) return;
+        j = jobs.front();
+        jobs.pop_front();
+      }
+      int k;
+      {
+        std::unique_lock<std::mutex> lk(hmu);
+        k = hnext;
+        hnext = (hnext + 1) % (int)hslots.size();
+        hcv.wait(lk, [&] { return !hslots[k].busy; });
+        hslots[k].busy = true;
+      }
+      HostSlot& hs = hslots[k];
+      if (hs.last_dev >= 0) cudaEventSynchronize(hs.ev[hs.last_dev]);  // its previous DMA drained it
+      uint8_t* slot = hring + (uint64_t)k * chunk;
+      const uint8_t* src = nullptr;
+      {
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = active.find(j.ticket);
+        if (it != active.end() && it->second->err == FT_OK) src = it->second->host + j.obj_off;
+      }
+      if (src) std::memcpy(slot, src, j.n);  // the tube keeps the object alive until landing
+      {
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = active.find(j.ticket);
+        if (it != active.end()) {
+          Stage& st = *it->second;
+          Route& r = st.routes[j.route];
+          try {
+            if (st.err == FT_OK) {
+              issue(r, st.dst + j.obj_off, slot, j.n);
+              DevGuard g(r.dev);
+              if (!hs.ev[r.dev]) ck(cudaEventCreateWithFlags(&hs.ev[r.dev], cudaEventDisableTiming), "event");
+              ck(cudaEventRecord(hs.ev[r.dev], r.ce), "record slot");  // the CE read of the slot
+              hs.last_dev = r.dev;
+            }
+            --st.jobs;
+            if (st.jobs == 0 && st.issued && st.err == FT_OK) seal(st);
+          } catch (const CudaFail& f) {
+            if (st.jobs > 0) --st.jobs;
+            fail(st, f.msg);
+          }
+          if (st.jobs == 0 && st.err != FT_OK) fail(st, st.msg);
+        }
+      }
+      {
+        std::lock_guard<std::mutex> lk(hmu);
+        hs.busy = false;
+      }
+      hcv.notify_all();
+      cv.notify_all();
+    }
+  }
+
+  int wait_ticket(std::unique_lock<std::mutex>& lk, uint64_t ticket, double timeout_ms) {
+    auto pred = [&] { return !active.count(ticket); };
+    if (timeout_ms < 0) {
+      done_cv.wait(lk, pred);
+    } else if (!done_cv.wait_for(lk, std::chrono::duration<double, std::milli>(timeout_ms), pred)) {
+      ft::set_last_error("ft_pacer_wait: timeout");
+      return FT_E_TIMEOUT;
+    }
+    auto it = errors.find(ticket);
+    if (it != errors.end()) {
+      ft::set_last_error(it->second.second);
+      return it->second.first;
+    }
+    return FT_OK;
+  }
+};
+
+extern "C" {
+
+int ft_pacer_create(double bw_all_gbps, int batch_chunks, int64_t chunk_bytes, int staging_slots,
+                    uint64_t host_ring_bytes, int logging, ft_pacer** out) {
+  if (!out || batch_chunks <= 0 || chunk_bytes <= 0 || !(bw_all_gbps > 0)) {
+    ft::set_last_error("ft_pacer_create: bad arguments");
+    return FT_E_VALUE;
+  }
+  auto p = std::make_unique<ft_pacer>();
+  p->batch_chunks = batch_chunks;
+  p->chunk = (uint64_t)chunk_bytes;
+  p->staging_slots = std::max(2, staging_slots);
+  p->logging = logging != 0;
+  p->arb.share = ft::PcieState{bw_all_gbps, batch_chunks, chunk_bytes, {}};
+  p->arb.batch_bytes = (double)(chunk_bytes * batch_chunks);
+  uint64_t slots = std::max<uint64_t>(4, host_ring_bytes / p->chunk);
+  void* h = nullptr;
+  cudaError_t e = cudaHostAlloc(&h, slots * p->chunk, cudaHostAllocPortable);
+  if (e != cudaSuccess) {
+    ft::set_last_error(std::string("ft_pacer_create: pinned ring: ") + cudaGetErrorString(e));
+    return FT_E_CUDA;
+  }
+  p->hring = static_cast<uint8_t*>(h);
+  p->hslots = std::vector<HostSlot>(slots);
+  ft_pacer* raw = p.get();
+  raw->pacer = std::thread([raw] { raw->run(); });
+  for (int i = 0; i < kWorkers; ++i) raw->workers.emplace_back([raw] { raw->work(); });
+  *out = p.release();
+  return FT_OK;
+}
+
+int ft_pacer_destroy(ft_pacer* p) {
+  if (!p) return FT_OK;
+  int rc = FT_OK;
+  {
+    std::unique_lock<std::mutex> lk(p->mu);
+    bool drained = p->done_cv.wait_for(lk, std::chrono::seconds(120), [&] { return p->active.empty(); });
+    if (!drained) {
+      for (auto& kv : p->active) p->fail(*kv.second, "pacer destroyed with the stage in flight");
+      ft::set_last_error("ft_pacer_destroy: stages still in flight after 120 s (failed)");
+      rc = FT_E_TIMEOUT;
+    }
+    p->stop = true;
+  }
+  p->cv.notify_all();
+  p->jcv.notify_all();
+  p->pacer.join();
+  for (auto& t : p->workers) t.join();
+  for (auto& kv : p->rings) {
+    DevGuard g(kv.first);
+    cudaDeviceSynchronize();
+    for (auto e : kv.second.landed) cudaEventDestroy(e);
+    for (auto e : kv.second.freed) cudaEventDestroy(e);
+    cudaFree(kv.second.buf);
+  }
+  for (int d = 0; d < kMaxDev; ++d)
+    for (auto e : p->evpool[d]) cudaEventDestroy(e);
+  for (auto& hs : p->hslots)
+    for (int d = 0; d < kMaxDev; ++d)
+      if (hs.ev[d]) {
+        cudaEventSynchronize(hs.ev[d]);
+        cudaEventDestroy(hs.ev[d]);
+      }
+  cudaFreeHost(p->hring);
+  delete p;
+  return rc;
+}
+
+int ft_pacer_submit(ft_pacer* p, const char* key, int managed, double slo_ms, double infer_ms,
+                    double per_branch_cap_gbps, void* dst, int dst_dev, const void* host, uint64_t bytes,
+                    int host_pinned, int k, const ft_route* routes, void* consumer_stream, uint64_t* ticket) {
+  if (!p || !ticket || k <= 0 || !routes || (bytes && (!dst || !host)) || dst_dev < 0 || dst_dev >= kMaxDev) {
+    ft::set_last_error("ft_pacer_submit: bad arguments");
+    return FT_E_VALUE;
+  }
+  uint64_t covered = 0;
+  for (int i = 0; i < k; ++i) {
+    const ft_route& r = routes[i];
+    if (r.stage_dev < 0 || r.stage_dev >= kMaxDev || !r.ce_stream || r.off + r.len > bytes ||
+        (r.stage_dev != dst_dev && !r.fw_stream)) {
+      ft::set_last_error("ft_pacer_submit: bad route (device, streams or range)");
+      return FT_E_VALUE;
+    }
+    covered += r.len;
+  }
+  if (covered != bytes) {
+    ft::set_last_error("ft_pacer_submit: routes do not cover the object");
+    return FT_E_VALUE;
+  }
+  auto sp = std::make_shared<Stage>();
+  Stage& st = *sp;
+  st.managed = managed != 0;
+  st.dst = static_cast<uint8_t*>(dst);
+  st.dst_dev = dst_dev;
+  st.host = static_cast<const uint8_t*>(host);
+  st.pinned = host_pinned != 0;
+  st.bytes = bytes;
+  for (int i = 0; i < k; ++i) {
+    Route r;
+    r.dev = routes[i].stage_dev;
+    r.off = routes[i].off;
+    r.len = routes[i].len;
+    r.ce = (cudaStream_t)routes[i].ce_stream;
+    r.fw = r.dev == dst_dev && !routes[i].force_staging ? nullptr : (cudaStream_t)routes[i].fw_stream;
+    st.routes.push_back(r);
+  }
+  cudaStream_t cs = (cudaStream_t)consumer_stream;
+  std::unique_lock<std::mutex> lk(p->mu);
+  st.ticket = p->next_ticket++;
+  st.key = key && *key ? std::string(key) : "m" + std::to_string(st.ticket);
+  try {
+    // the routes start after the consumer stream's prior work (object ready, dst free)
+    DevGuard g(dst_dev);
+    cudaEvent_t e = p->get_event(dst_dev);
+    ck(cudaEventRecord(e, cs), "record consumer");
+    for (auto& r : st.routes) {
+      DevGuard gr(r.dev);
+      ck(cudaStreamWaitEvent(r.ce, e, 0), "route waits consumer");
+      if (r.staged()) ck(cudaStreamWaitEvent(r.fw, e, 0), "forward waits consumer");
+    }
+    p->put_event(dst_dev, e);
+    ++p->n_stages;
+    p->note(st, "start", (double)bytes);
+    if (st.managed) {
+      ++p->n_managed;
+      double t = p->now();
+      p->arb.start(t, st.key, (double)bytes, slo_ms, infer_ms, t, per_branch_cap_gbps, k);  // engine.py:537-575
+      p->arb_log(t, "start", st.key);
+      if (bytes == 0) {
+        st.issued = true;
+        p->seal(st);
+      }
+    } else {
+      for (int i = 0; i < k; ++i) {
+        p->hand_out(st, i, 0, st.routes[i].len, false);  // one DMA op per range (pinned)
+        st.routes[i].done = st.routes[i].len;
+      }
+      st.issued = true;
+      if (st.jobs == 0) p->seal(st);
+    }
+  } catch (const CudaFail& f) {
+    p->fail(st, f.msg);
+  } catch (const ft::Error& e) {
+    p->fail(st, e.what());
+    st.err = e.code;
+  }
+  *ticket = st.ticket;
+  p->active.emplace(st.ticket, sp);
+  p->cv.notify_all();
+  // every byte enqueued (a paced stage: its last batch issued) -> the consumer waits on the routes
+  p->done_cv.wait(lk, [&] { return st.sealed; });
+  int rc = st.err;
+  std::string msg = st.msg;
+  if (rc == FT_OK) {
+    try {
+      DevGuard g(dst_dev);
+      for (auto& e : st.join) ck(cudaStreamWaitEvent(cs, e.first, 0), "consumer waits route");
+    } catch (const CudaFail& f) {
+      rc = FT_E_CUDA;
+      msg = f.msg;
+    }
+  }
+  for (auto& e : st.join) p->put_event(e.second, e.first);  // the waits captured their records
+  st.join.clear();
+  if (rc != FT_OK) ft::set_last_error(msg);
+  return rc;
+}
+
+int ft_pacer_wait(ft_pacer* p, uint64_t ticket, double timeout_ms) {
+  if (!p) {
+    ft::set_last_error("null argument: p");
+    return FT_E_VALUE;
+  }
+  std::unique_lock<std::mutex> lk(p->mu);
+  return p->wait_ticket(lk, ticket, timeout_ms);
+}
+
+int ft_pacer_done(ft_pacer* p, uint64_t ticket, int* done) {
+  if (!p || !done) {
+    ft::set_last_error("ft_pacer_done: null argument");
+    return FT_E_VALUE;
+  }
+  std::lock_guard<std::mutex> lk(p->mu);
+  *done = !p->active.count(ticket);
+  return FT_OK;
+}
+
+int ft_pacer_stats(ft_pacer* p, uint64_t* out, int cap) {
+  if (!p || !out) {
+    ft::set_last_error("ft_pacer_stats: null argument");
+    return FT_E_VALUE;
+  }
+  std::lock_guard<std::mutex> lk(p->mu);
+  uint64_t v[7] = {p->n_stages, p->n_managed, p->n_batches, p->n_bytes, (uint64_t)p->active.size(), p->n_errors,
+                   0};
+  for (int i = 0; i < cap && i < 7; ++i) out[i] = v[i];
+  return FT_OK;
+}
+
+int ft_pacer_now_ms(ft_pacer* p, double* out) {
+  if (!p || !out) {
+    ft::set_last_error("ft_pacer_now_ms: null argument");
+    return FT_E_VALUE;
+  }
+  *out = p->now();
+  return FT_OK;
+}
+
+static int emit_list(const std::vector<std::string>& v, char* buf, size_t cap, size_t* need) {
+  std::string s = "[";
+  for (size_t i = 0; i < v.size(); ++i) {
+    if (i) s += ",";
+    s += v[i];
+  }
+  s += "]";
+  if (need) *need = s.size() + 1;
+  if (!buf || cap < s.size() + 1) {
+    ft::set_last_error("json output buffer too small");
+    return FT_E_TRUNCATED;
+  }
+  std::memcpy(buf, s.c_str(), s.size() + 1);
+  return FT_OK;
+}
+
+int ft_pacer_trace_json(ft_pacer* p, char* buf, size_t cap, size_t* need) {
+  if (!p) return FT_E_VALUE;
+  std::lock_guard<std::mutex> lk(p->mu);
+  return emit_list(p->trace, buf, cap, need);
+}
+
+int ft_pacer_log_json(ft_pacer* p, char* buf, size_t cap, size_t* need) {
+  if (!p) return FT_E_VALUE;
+  std::lock_guard<std::mutex> lk(p->mu);
+  return emit_list(p->log, buf, cap, need);
+}
+
+int ft_pacer_state_json(ft_pacer* p, char* buf, size_t cap, size_t* need) {
+  if (!p) return FT_E_VALUE;
+  std::lock_guard<std::mutex> lk(p->mu);
+  std::string s = p->arb.state_json();
+  if (need) *need = s.size() + 1;
+  if (!buf || cap < s.size() + 1) {
+    ft::set_last_error("json output buffer too small");
+    return FT_E_TRUNCATED;
+  }
+  std::memcpy(buf, s.c_str(), s.size() + 1);
+  return FT_OK;
+}
+
+}  // extern "C"

@@ -253,3 +253,74 @@ def recv_fd(sock) -> tuple:
     fd, tag = C.c_int(), C.c_uint64()
     LIB.ft_fd_recv(sock.fileno(), C.byref(fd), C.byref(tag))
     return fd.value, tag.value
+
+
+class Pacer:
+    """Live PCIe mover + per-function bandwidth-share scheduler (``ft_pacer``).
+
+    One per tube: every host->GPU leg is submitted as a stage of routes
+    (dataplane.py:203-250); managed stages are paced at the arbiter's rate in
+    5 x 2 MB batches by a native thread (engine.py:537-646), unmanaged ones are
+    issued at once. ``submit`` returns at once; the consumer stream is parked
+    on the stage's completion word, so later work on it sees the bytes."""
+
+    def __init__(self, bw_all_gbps: float, batch_chunks: int, chunk_bytes: int, staging_slots: int = 4,
+                 host_ring_bytes: int = 0, logging: bool = False):
+        from ._lib import RouteC
+        self._route_t = RouteC
+        h = C.c_void_p()
+        LIB.ft_pacer_create(float(bw_all_gbps), int(batch_chunks), int(chunk_bytes), int(staging_slots),
+                            int(host_ring_bytes), int(bool(logging)), C.byref(h))
+        self._h = h
+
+    def submit(self, key: str, managed: bool, slo_ms: float, infer_ms: float, per_branch_cap_gbps: float,
+               dst_ptr: int, dst_dev: int, host_ptr: int, nbytes: int, host_pinned: bool, routes: list,
+               consumer_stream: int) -> int:
+        """routes: [(stage_dev, force_staging, off, len, ce_stream, fw_stream)] -> ticket"""
+        arr = (self._route_t * len(routes))(*[self._route_t(int(a), int(b), int(c), int(d), e, f)
+                                               for a, b, c, d, e, f in routes])
+        t = C.c_uint64()
+        LIB.ft_pacer_submit(self._h, key.encode(), int(bool(managed)), float(slo_ms), float(infer_ms),
+                            float(per_branch_cap_gbps), C.c_void_p(dst_ptr), int(dst_dev), C.c_void_p(host_ptr),
+                            int(nbytes), int(bool(host_pinned)), len(routes), arr, C.c_void_p(consumer_stream),
+                            C.byref(t))
+        return t.value
+
+    def done(self, ticket: int) -> bool:
+        d = C.c_int()
+        LIB.ft_pacer_done(self._h, int(ticket), C.byref(d))
+        return bool(d.value)
+
+    def wait(self, ticket: int, timeout_ms: float = -1.0):
+        LIB.ft_pacer_wait(self._h, int(ticket), float(timeout_ms))
+
+    def stats(self) -> dict:
+        out = (C.c_uint64 * 7)()
+        LIB.ft_pacer_stats(self._h, out, 7)
+        keys = ("stages", "managed_stages", "batches", "bytes", "active", "failed", "blocking")
+        return dict(zip(keys, list(out)))
+
+    def now_ms(self) -> float:
+        t = C.c_double()
+        LIB.ft_pacer_now_ms(self._h, C.byref(t))
+        return t.value
+
+    def trace(self) -> list:
+        from ._lib import json_out
+        return json_out("ft_pacer_trace_json", self._h)
+
+    def log(self) -> list:
+        from ._lib import json_out
+        return json_out("ft_pacer_log_json", self._h)
+
+    def state(self) -> dict:
+        from ._lib import json_out
+        return json_out("ft_pacer_state_json", self._h)
+
+    def close(self):
+        h = getattr(self, "_h", None)
+        if h:
+            self._h = None
+            LIB.ft_pacer_destroy(h)
+
+    __del__ = close

@@ -17,6 +17,7 @@ payload (config 4: decode -> detector -> recognizers on 1080p frames).
 
 from __future__ import annotations
 
+import contextlib
 import math
 import threading
 import time
@@ -102,6 +103,7 @@ class Runtime:
         self.records: list[Record] = []
         self._rec_lock = threading.Lock()
         self.pool_timeline = []
+        self._tls = threading.local()
         self._clock_hz = {g: torch.cuda.get_device_properties(g).clock_rate * 1e3 if hasattr(
             torch.cuda.get_device_properties(g), "clock_rate") else 1.965e9 for g in tube.gpus}
 
@@ -123,7 +125,23 @@ class Runtime:
         torch.cuda._sleep(int(ms * 1e-3 * self._clock_hz[gpu]))
         return torch.empty(out_bytes, dtype=torch.uint8, device=f"cuda:{gpu}").fill_(len(fid) & 0xFF)
 
+    def _stream(self, gpu) -> torch.cuda.Stream:
+        """This worker thread's own stream on ``gpu`` (a function's CUDA context):
+        its fetches park only its own stream, never another tenant's."""
+        d = getattr(self._tls, "streams", None)
+        if d is None:
+            d = self._tls.streams = {}
+        if gpu not in d:
+            d[gpu] = torch.cuda.Stream(gpu)
+        return d[gpu]
+
     def _request(self, wf: Workflow, where: dict, req: Request, rec: Record, t0: float):
+        with contextlib.ExitStack() as es:
+            for g in self.tube.gpus:
+                es.enter_context(torch.cuda.stream(self._stream(g)))
+            self._request_on_streams(wf, where, req, rec, t0)
+
+    def _request_on_streams(self, wf: Workflow, where: dict, req: Request, rec: Record, t0: float):
         tube = self.tube
         now = lambda: (time.perf_counter() - t0) * 1e3
         rec.start_ms = now()
@@ -147,12 +165,16 @@ class Runtime:
             t_in = now()
             if not ins:
                 x = tube.fetch(in_id, device=gpu, consumer=fid, slo_ms=f.slo_ms, infer_ms=f.infer_ms)
+                if gpu is not None:
+                    torch.cuda.current_stream(gpu).synchronize()   # the paced H2G stage landed
                 rec.phases["host_to_gfunc"] += now() - t_in
             else:
                 xs = []
                 for e in ins:
                     xs.append(tube.fetch(outputs[e.src], device=gpu, consumer=fid, slo_ms=f.slo_ms,
                                          infer_ms=f.infer_ms))
+                if gpu is not None:
+                    torch.cuda.current_stream(gpu).synchronize()   # inputs landed (phase accounting)
                 phase = "gfunc_to_gfunc" if gpu is not None and where[ins[0].src][0] == "gpu" else "host_to_gfunc"
                 rec.phases[phase] += now() - t_in
                 x = xs[0]

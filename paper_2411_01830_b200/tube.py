@@ -16,20 +16,23 @@ bytes move on real links:
 * GPU -> GPU    — SM-driven copy over NVLink (peer-mapped pool memory);
 * host -> GPU   — copy-engine DMA on the target's own PCIe link plus, per
                   extra PCIe root, CE into a staging GPU and an NVLink forward
-                  kernel into the target, chunk-pipelined (dataplane.py:203-250);
+                  kernel into the target, chunk-pipelined (dataplane.py:203-250),
+                  issued by the native pacer (``device.Pacer``: managed stages
+                  at their bandwidth share, engine.py:537-646);
 * GPU -> host   — copy-engine DMA;
 * host-oriented strategies (infless_plus, deepplan_plus) stage GPU->GPU
   through pinned host memory, as the reference's baselines do.
 
 Stream semantics: ``store`` orders after the producer's current stream;
 ``fetch`` enqueues on the consumer device's current stream, so consumer
-kernels issued afterwards see the data. No call synchronizes the host
-unless the caller asks for a host tensor.
+kernels issued afterwards see the data (host->GPU stages park that stream on
+the stage's completion word). No call synchronizes the host unless the
+caller asks for a host tensor; ``FaaSTube.wait`` blocks until a host->GPU
+fetch has landed.
 """
 
 from __future__ import annotations
 
-import ctypes as C
 import heapq
 import itertools
 import math
@@ -42,8 +45,7 @@ import torch
 
 from . import datastore, device as dev
 from .dataplane import DataIndex, Dataplane, Location
-from .pcie_sched import BATCH_CHUNKS, CHUNK_BYTES
-from .stage_sched import StageArbiter
+from .pcie_sched import BATCH_CHUNKS, CHUNK_BYTES, default_ring_capacity
 from .strategies import Strategy, strategy_preset
 from .topology import Topology, build_preset, snapshot_matrix
 
@@ -76,11 +78,15 @@ class _Obj:
 
 class FaaSTube:
     def __init__(self, strategy: str | Strategy = "faastube", topology: Topology | None = None,
-                 pcie_gbps: float = 55.0, chunk_bytes: int = CHUNK_BYTES, batch_chunks: int = BATCH_CHUNKS,
+                 pcie_gbps: float | str = "measure", chunk_bytes: int = CHUNK_BYTES, batch_chunks: int = BATCH_CHUNKS,
                  pool_floor_bytes: float = datastore.POOL_FLOOR_BYTES, node: int = 0, map_ms: float = 0.05,
                  gpus: list | None = None, capacity_limit_bytes: float = datastore.CAPACITY_LIMIT_BYTES):
         n = dev.require_cuda()
-        self.topo = topology or build_preset("b200", n_gpus=n, pcie_gbps=pcie_gbps)
+        if topology is None and pcie_gbps == "measure":
+            # the link share the pacer hands out must be the link this box really has
+            # (the measured pinned-H2D rate is the PCIe roofline)
+            pcie_gbps = measure_pcie_gbps(list(gpus) if gpus is not None else list(range(n)))
+        self.topo = topology or build_preset("b200", n_gpus=n, pcie_gbps=float(pcie_gbps))
         if self.topo.gpu_count > n:
             raise ValueError(f"topology has {self.topo.gpu_count} GPUs but only {n} are visible")
         self.strategy = strategy_preset(strategy) if isinstance(strategy, str) else strategy
@@ -103,12 +109,15 @@ class FaaSTube:
                 self.pools[g] = dev.DevicePool(g, self.strategy.pool, pool_floor_bytes)
         roots = self.topo.roots()
         bw_all = self.topo.pcie_gbps * len(roots)  # engine.py:186-190
-        self.arbiters = {d: StageArbiter(bw_all, batch_chunks, chunk_bytes) for d in ("h2d", "d2h")}
+        # every host->GPU leg goes through the native pacer (managed stages paced at
+        # their share; pageable payloads staged through its warm pinned ring)
+        self.pacer = dev.Pacer(bw_all, batch_chunks, chunk_bytes, staging_slots=4,
+                               host_ring_bytes=default_ring_capacity(len(roots), batch_chunks * chunk_bytes),
+                               logging=bool(os.environ.get("FT_TRACE")))
+        self._tickets = []           # (ticket, keep-alive refs) until the stage has landed
         self._t0 = time.perf_counter()
         self._objs: dict[int, _Obj] = {}
         self._lock = threading.RLock()
-        self._sched_lock = threading.Lock()
-        self._sched_cv = threading.Condition(self._sched_lock)   # wakes parked managed stages
         self._side = {g: torch.cuda.Stream(g) for g in self.gpus}        # store / forward stream
         self._ce = {g: [torch.cuda.Stream(g) for _ in range(2)] for g in self.gpus}  # copy-engine streams
         # per-transfer CE stream pairs (PCIe leg, NVLink forward): concurrent tenants'
@@ -116,8 +125,6 @@ class FaaSTube:
         self._ce_pairs = {g: [(torch.cuda.Stream(g), torch.cuda.Stream(g)) for _ in range(8)] for g in self.gpus}
         self._ce_rr = itertools.count()
         self._staging = {}
-        self._pinned_ring = None     # shared warm staging ring for pageable host payloads
-        self._trace = [] if os.environ.get("FT_TRACE") else None   # managed-stage issue log
         self._pending_release = []   # (event, plan): NVLink claims held until the copy lands
         self._shrink_due = []        # heap of (due_ms, gpu)
         self._managed_ids = itertools.count(1)
@@ -138,7 +145,10 @@ class FaaSTube:
         return Location(self.node, gpu)
 
     def _reap(self):
-        """Release NVLink claims of transfers that have landed; run due shrinks."""
+        """Release NVLink claims of transfers that have landed, and the
+        keep-alive references of host->GPU stages that have landed."""
+        if self._tickets:
+            self._tickets = [t for t in self._tickets if not self.pacer.done(t[0])]
         keep = []
         for ev, plan in self._pending_release:
             if ev.query():
@@ -388,20 +398,30 @@ class FaaSTube:
             src = entry.location
             dst = self._loc(device)
             plan = self.plane.fetch_plan(src, dst, obj.nbytes)
-            managed = (plan.method == "host_gpu" and not dst.on_host and self.strategy.pcie_sched
-                       and plan.stages[0].managed)
-            if not managed:
-                result = self._execute(obj, plan, src, dst, out, slo_ms, infer_ms)
-                self.stats["fetches"] += 1
-                self._consumed(obj)
-                return result
-            res = self._out(obj, dst.gpu, out)
-        # managed PCIe stage: paced outside the tube lock so tenants run concurrently
-        self._managed_h2g(obj, plan, dst, res, consumer, slo_ms, infer_ms)
-        with self._lock:
+            h2g = plan.method == "host_gpu" and not dst.on_host
+            if h2g:
+                res, stage = self._host_to_gpu(obj, plan, dst, out, slo_ms, infer_ms)
+            else:
+                res = self._execute(obj, plan, src, dst, out, slo_ms, infer_ms)
             self.stats["fetches"] += 1
             self._consumed(obj)
+            if not h2g:
+                return res
+        # host->GPU stage: the pacer returns once its last batch is issued — outside
+        # the tube lock, so concurrent tenants' stages are paced side by side
+        ticket = self.pacer.submit(*stage)
+        with self._lock:
+            self._tickets.append((ticket, obj.host, res))
         return res
+
+    def wait(self, timeout_ms: float = -1.0):
+        """Block the host until every host->GPU stage submitted so far has landed."""
+        with self._lock:
+            tickets = [t[0] for t in self._tickets]
+        for t in tickets:
+            self.pacer.wait(t, timeout_ms)
+        with self._lock:
+            self._reap()
 
     def release(self, data_id: int):
         """Drop a stored object regardless of remaining consumers."""
@@ -421,6 +441,8 @@ class FaaSTube:
         return obj.response_host.view(obj.dtype).view(obj.shape)
 
     def close(self):
+        self.pacer.close()                        # drains in-flight host->GPU stages
+        self._tickets.clear()
         with self._maint_cv:
             self._closing = True
             self._maint_cv.notify()
@@ -508,9 +530,7 @@ class FaaSTube:
         if m == "inter_gpu":
             return self._inter_gpu(obj, plan, src, dst, out)
         if m == "host_gpu":
-            if dst.on_host:
-                return self._gpu_to_host(obj, plan, out)
-            return self._host_to_gpu(obj, plan, dst, out, slo_ms, infer_ms)
+            return self._gpu_to_host(obj, plan, out)
         from ._lib import NotSupported
         raise NotSupported("inter-node transfers need a multi-node deployment (SURVEY §8f row 4)")
 
@@ -580,145 +600,40 @@ class FaaSTube:
         pairs = self._ce_pairs[g]
         return pairs[(next(self._ce_rr) if slot is None else slot) % len(pairs)]
 
-    def _issue_h2g(self, b, host_ptr, dst_ptr, n, dst_gpu, after: torch.cuda.Stream, slot=None) -> torch.cuda.Event:
-        """One branch's byte range host -> dst_gpu: CE straight in on the target's
-        own root, or CE into the staging GPU's chunk ring + NVLink forward."""
-        stage_gpu = _staging_gpu(b.links, dst_gpu)
-        if stage_gpu == dst_gpu:
-            ce = self._pair(dst_gpu, slot)[0]
-            ce.wait_stream(after)
-            dev.pcie_copy(dst_ptr, host_ptr, n, True, dst_gpu, ce, 0)   # one DMA op per range
-            last = ce
-        else:
-            ce, fw = self._pair(stage_gpu, slot)
-            ce.wait_stream(after)
-            ring = 4
-            stg = self._staging_buf(stage_gpu, ring * self.chunk_bytes)
-            streams = (C.c_void_p * 2)(ce.cuda_stream, fw.cuda_stream)
-            offs, lens = (C.c_uint64 * 1)(0), (C.c_uint64 * 1)(n)
-            sd = (C.c_int32 * 1)(stage_gpu)
-            stgp = (C.c_void_p * 1)(stg.data_ptr())
-            dev.LIB.ft_h2g_striped(C.c_void_p(dst_ptr), dst_gpu, C.c_void_p(host_ptr), n, 1, sd, offs, lens, stgp,
-                                   self.chunk_bytes, ring, streams)
-            last = fw
-            self.stats["bytes_nvlink"] += n
-        ev = torch.cuda.Event()
-        ev.record(last)
-        self.stats["bytes_h2d"] += n
-        return ev
-
     def _host_to_gpu(self, obj, plan, dst, out, slo_ms, infer_ms):
+        """A host_gpu plan (dataplane.py:190-250) as one pacer stage: route i
+        carries the contiguous byte range of branch i's share — CE straight in on
+        the target's own root, or CE into the staging GPU's chunk ring + NVLink
+        forward. Managed stages (strategy.pcie_sched) enter the SLO partition and
+        are paced in batches at their rate (engine.py:537-646); the consumer's
+        stream is ordered after the last byte. Returns (result, pacer.submit
+        arguments); the caller submits outside the tube lock."""
         res = self._out(obj, dst.gpu, out)
-        br = plan.stages[0].branches
+        st = plan.stages[0]
+        br = st.branches
         ranges = self._stripes(obj.nbytes, [b.bytes_share for b in br])
         s = self._stream(dst.gpu)
         if obj.ready is not None:
             s.wait_event(obj.ready)
-        events = []
+        slot = next(self._ce_rr)              # this stage's own CE streams (tenants must not FIFO)
+        routes = []
         for b, (off, n) in zip(br, ranges):
-            if n:
-                events += self._h2g_range(b, obj.host, off, n, res.data_ptr() + off, dst.gpu, s)
-        for ev in events:
-            s.wait_event(ev)
-        return res
-
-    def _h2g_range(self, b, host: torch.Tensor, off, n, dst_ptr, dst_gpu, after, slot=None) -> list:
-        """Bytes [off, off+n) of a host object onto a branch: straight DMA from
-        pinned memory, or chunk by chunk through the shared pinned ring."""
-        if host.is_pinned():
-            return [self._issue_h2g(b, host.data_ptr() + off, dst_ptr, n, dst_gpu, after, slot)]
-        ring = self._ring()
-        return ring.stage(host, off, n, lambda sptr, o, m: self._issue_h2g(b, sptr, dst_ptr + o, m, dst_gpu, after,
-                                                                           slot))
-
-    def _ring(self) -> "_PinnedRing":
-        if self._pinned_ring is None:
-            from .pcie_sched import default_ring_capacity
-            cap = default_ring_capacity(len(self.topo.roots()), self.batch_chunks * self.chunk_bytes)
-            self._pinned_ring = _PinnedRing(cap, self.chunk_bytes)
-        return self._pinned_ring
-
-    # -------------------------------------------------- live bandwidth-share scheduler
-    def _deliver_due(self, arb: StageArbiter):
-        """Fire every armed batch boundary that is due (engine.py:628-646)."""
-        while True:
-            t, key = arb.next_event()
-            if t is None or t > self.now_ms():
-                return
-            arb.boundary(t, key)
-            self._sched_cv.notify_all()
-
-    def _managed_h2g(self, obj, plan, dst, res, consumer, slo_ms, infer_ms):
-        """A scheduler-managed PCIe stage (engine.py:537-575): the stage's
-        demand enters the SLO partition; its bytes move in batch-sized pieces
-        (batch = 5 x 2 MB, pcie_sched.py:14-15) split over the branches by
-        byte share, issued at the arbiter's rate; rate changes land on batch
-        boundaries. Returns when every byte has landed."""
-        arb = self.arbiters["h2d"]
-        br = plan.stages[0].branches
-        ranges = [r for r in self._stripes(obj.nbytes, [b.bytes_share for b in br])]
-        per_branch_cap = min(min(b.hop_caps) for b in br)
-        slo = slo_ms if slo_ms else 1e9                   # engine.py:546-547
-        infer = infer_ms if infer_ms is not None else 0.0
-        key = f"m{next(self._managed_ids)}"
-        slot = next(self._ce_rr)                             # this stage's own CE streams
-        s = self._stream(dst.gpu)
-        if obj.ready is not None:
-            s.wait_event(obj.ready)
-        with self._sched_lock:
-            now = self.now_ms()
-            arb.start(now, key, float(obj.nbytes), slo, infer, now, per_branch_cap, len(br))
-            self._sched_cv.notify_all()
-        batch = self.batch_chunks * self.chunk_bytes
-        done = [0] * len(br)
-        inflight = []
-        next_t = None
-        last_rate = None
-        dst_ptr = res.data_ptr()
-        if self._trace is not None:
-            self._trace.append((self.now_ms(), key, "start", obj.nbytes))
-        while any(done[i] < ranges[i][1] for i in range(len(br))):
-            with self._sched_lock:
-                self._deliver_due(arb)
-                st = arb.stage(key)
-                nxt, _ = arb.next_event()
-            now = self.now_ms()
-            if not st["started"] or st["rate"] <= 0:
-                # parked until a boundary, another stage's finish, or a new stage re-partitions
-                with self._sched_cv:
-                    self._sched_cv.wait(max(0.0, (nxt - now) / 1e3) if nxt is not None else 0.002)
-                continue
-            dur = batch / (st["rate"] * 1e6)              # ms per batch at the stage rate
-            if next_t is None or st["rate"] != last_rate:
-                # (re)anchor the issue schedule when the rate changes: a stage that
-                # was paced slowly must not keep waiting on its old, far-out slot
-                next_t = now if next_t is None else min(next_t, now + dur)
-                last_rate = st["rate"]
-                if self._trace is not None:
-                    self._trace.append((now, key, "rate", st["rate"]))
-            if now < next_t - 2 * dur:                      # two batches of lookahead absorb host jitter
-                _sleep_until(min(next_t - 2 * dur, nxt if nxt is not None else next_t), self.now_ms)
-                continue
-            while len(inflight) >= 4:
-                inflight.pop(0).synchronize()
-            evs = []
-            for i, b in enumerate(br):
-                off, n = ranges[i]
-                take = min(n - done[i], int(batch * n / obj.nbytes) // _ALIGN * _ALIGN or n - done[i])
-                if take <= 0:
-                    continue
-                evs += self._h2g_range(b, obj.host, off + done[i], take, dst_ptr + off + done[i], dst.gpu, s, slot)
-                done[i] += take
-            inflight.extend(evs)
-            next_t += dur
-            if self._trace is not None:
-                self._trace.append((now, key, "issue", sum(done)))
-        for ev in inflight:
-            ev.synchronize()
-        with self._sched_lock:
-            arb.finish(self.now_ms(), key)
-            self._sched_cv.notify_all()
-        self.stats["managed_stages"] = self.stats.get("managed_stages", 0) + 1
+            sg = _staging_gpu(b.links, dst.gpu)
+            ce, fw = self._pair(sg, slot)
+            routes.append((sg, 0, off, n, ce.cuda_stream, fw.cuda_stream))
+            if sg != dst.gpu:
+                self.stats["bytes_nvlink"] += n
+        managed = bool(self.strategy.pcie_sched and st.managed)
+        host = obj.host
+        stage = (f"m{next(self._managed_ids)}" if managed else "", managed,
+                 slo_ms if slo_ms else 1e9,                       # engine.py:546-547
+                 infer_ms if infer_ms is not None else 0.0,
+                 min(min(b.hop_caps) for b in br), res.data_ptr(), dst.gpu, host.data_ptr(), obj.nbytes,
+                 host.is_pinned(), routes, s.cuda_stream)
+        self.stats["bytes_h2d"] += obj.nbytes
+        if managed:
+            self.stats["managed_stages"] = self.stats.get("managed_stages", 0) + 1
+        return res, stage
 
     def maintain(self):
         """Release landed NVLink claims and run due pool shrinks (idle housekeeping)."""
@@ -738,52 +653,30 @@ class FaaSTube:
         return res
 
 
-class _PinnedRing:
-    """Circular pinned staging buffer shared by all functions (pcie_sched.py:122-162,
-    PAPER.md:620): 2 x batch x PCIe roots bytes in chunk-sized slots. A pageable
-    payload is copied into a free slot by host threads and DMA'd from there;
-    a slot is reused once its DMA event completes, so the host copy of chunk
-    k+1 overlaps the DMA of chunk k and only the ring is ever pinned."""
-
-    def __init__(self, capacity: int, chunk: int):
-        from concurrent.futures import ThreadPoolExecutor
-        self.chunk = int(chunk)
-        self.slots = max(4, int(capacity) // self.chunk)
-        self.buf = torch.empty(self.slots * self.chunk, dtype=torch.uint8).pin_memory()
-        self.events = [None] * self.slots
-        self.next = 0
-        self.lock = threading.Lock()
-        self.workers = ThreadPoolExecutor(4, thread_name_prefix="faastube-ring")
-
-    def _one(self, host, o, m, issue):
-        with self.lock:
-            k = self.next
-            self.next = (k + 1) % self.slots
-            prev = self.events[k]
-            self.events[k] = None
-        if prev is not None:
-            prev.synchronize()                       # the slot's previous DMA has drained it
-        view = self.buf[k * self.chunk: k * self.chunk + m]
-        view.copy_(host[o:o + m])
-        ev = issue(view.data_ptr(), o, m)
-        with self.lock:
-            self.events[k] = ev
-        return ev
-
-    def stage(self, host: torch.Tensor, off: int, n: int, issue) -> list:
-        """issue(slot_ptr, offset_within_range, nbytes) -> event; returns the events."""
-        jobs = [(off + o, min(self.chunk, n - o), o) for o in range(0, n, self.chunk)]
-        futs = [self.workers.submit(self._one, host, a, m, lambda p, _o, mm, rel=rel: issue(p, rel, mm))
-                for a, m, rel in jobs]
-        return [f.result() for f in futs]
-
-
-def _sleep_until(t_ms, clock):
-    """Wait without spinning: sleeping releases the GIL, so concurrent tenants'
-    pacing loops never starve each other (waits under 50 us count as due)."""
-    left = t_ms - clock()
-    if left > 0.05:
-        time.sleep(left / 1e3)
+def measure_pcie_gbps(gpus, nbytes: int = 64 << 20, reps: int = 8, margin: float = 1.0) -> float:
+    """Pinned host->GPU copy-engine rate (GB/s) of the slowest link among
+    ``gpus``: best of ``reps`` back-to-back copies after a warm-up burst (an
+    idle PCIe link trains down and needs traffic to come back to full speed),
+    times ``margin``. The pacer must not hand out more than the link delivers
+    (its shares would stop isolating tenants) nor much less (a lone stage
+    would be throttled below the link)."""
+    host = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    rates = []
+    for g in gpus:
+        dst = torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{g}")
+        s = torch.cuda.Stream(g)
+        for _ in range(4):                                   # wake the link up
+            dev.pcie_copy(dst.data_ptr(), host.data_ptr(), nbytes, True, g, s)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(reps + 1)]
+        ev[0].record(s)
+        for i in range(reps):
+            dev.pcie_copy(dst.data_ptr(), host.data_ptr(), nbytes, True, g, s)
+            ev[i + 1].record(s)
+        ev[-1].synchronize()
+        best = min(ev[i].elapsed_time(ev[i + 1]) for i in range(reps))
+        rates.append(nbytes / (best * 1e-3) / 1e9)
+        del dst
+    return round(min(rates) * margin, 2)
 
 
 def _hops(links):

@@ -33,10 +33,12 @@ def test_managed_fetch_bit_exact_and_logged():
     tube.close()
 
 
-def _contend(strategy, n_loose=3, loose_bytes=1000 * MB, tight_bytes=256 * MB, window_ms=10.0):
-    """3 loose tenants start first; then a tight tenant needing tight_bytes/window."""
+def _contend(strategy, link_gbps, n_loose=3, loose_bytes=1000 * MB, tight_bytes=256 * MB):
+    """3 loose tenants start first; then a tight tenant whose window needs 45%
+    of the link (the box's measured pinned-H2D rate)."""
     from paper_2411_01830_b200.tube import FaaSTube
-    tube = FaaSTube(strategy, pool_floor_bytes=0.0)
+    tube = FaaSTube(strategy, pool_floor_bytes=0.0, pcie_gbps=link_gbps)
+    window_ms = tight_bytes / (0.45 * link_gbps * 1e6)
     rng = np.random.default_rng(12)
     names = [f"L{i}" for i in range(n_loose)] + ["T"]
     payload = {k: torch.from_numpy(rng.integers(0, 256, loose_bytes if k != "T" else tight_bytes,
@@ -45,6 +47,9 @@ def _contend(strategy, n_loose=3, loose_bytes=1000 * MB, tight_bytes=256 * MB, w
     for k in names:
         ids[k] = tube.unique_id()
         tube.store(ids[k], payload[k], producer=f"decode{k}")
+    # each tenant fetches into its own input buffer (Listing 1: fetch(index, input)),
+    # allocated up front so allocator latency does not stagger the tenants' starts
+    bufs = {k: torch.empty(payload[k].numel(), dtype=torch.uint8, device="cuda:0") for k in names}
     w = tube.unique_id()
     tube.store(w, payload["T"][: 16 * MB].clone(), producer="warm")
     tube.fetch(w, device=0)
@@ -53,14 +58,16 @@ def _contend(strategy, n_loose=3, loose_bytes=1000 * MB, tight_bytes=256 * MB, w
     go = threading.Event()
 
     def run(k, delay):
+        s = torch.cuda.Stream(0)           # each tenant function has its own stream
         go.wait()
         time.sleep(delay)
         t0 = time.perf_counter()
         # loose tenants: least 0.5 GB/s (batch boundaries every 20 ms, so a
         # starved stage picks up idle bandwidth quickly — engine.py:135-142)
         slo, infer = (window_ms + 5.0, 5.0) if k == "T" else (2005.0, 5.0)
-        out[k] = tube.fetch(ids[k], device=0, consumer=f"g{k}", slo_ms=slo, infer_ms=infer)
-        torch.cuda.synchronize()
+        with torch.cuda.stream(s):
+            out[k] = tube.fetch(ids[k], out=bufs[k], consumer=f"g{k}", slo_ms=slo, infer_ms=infer)
+        s.synchronize()
         t_done[k] = (time.perf_counter() - t0) * 1e3
 
     th = [threading.Thread(target=run, args=(k, 0.0 if k != "T" else 0.004)) for k in names]
@@ -72,14 +79,17 @@ def _contend(strategy, n_loose=3, loose_bytes=1000 * MB, tight_bytes=256 * MB, w
     for k in names:
         assert torch.equal(out[k].cpu(), payload[k]), k
     tube.close()
-    return t_done
+    return t_done, window_ms
 
 
 def test_isolation_tight_tenant_meets_its_window():
-    managed = _contend("faastube")
-    shared = _contend("faastube_star")     # no PCIe scheduler: native sharing among 4 tenants
-    # the tight tenant needs 256 MB / 10 ms = 25.6 GB/s; 4-way native sharing of a
-    # ~55 GB/s link gives it ~14 GB/s (~18 ms); the partition guarantees its least rate
-    # (host-paced batches on a shared link: allow thread-scheduling jitter)
-    assert managed["T"] < 0.6 * shared["T"], (managed, shared)
-    assert managed["T"] < 25.0, managed
+    from paper_2411_01830_b200.tube import measure_pcie_gbps
+    link = measure_pcie_gbps([0])
+    managed, window = _contend("faastube", link)
+    shared, _ = _contend("faastube_star", link)   # no PCIe scheduler: native sharing among 4 tenants
+    # the tight tenant needs 45% of the link; native sharing (FIFO-ish copy engines
+    # behind 3 x 1 GB loose transfers) gives it far less; the partition guarantees its
+    # least rate (batches paced by the native pacer: allow a few batches of jitter)
+    info = (link, window, managed, shared)
+    assert managed["T"] < 0.6 * shared["T"], info
+    assert managed["T"] < 1.5 * window + 5.0, info

@@ -15,7 +15,7 @@ out = rt.run([(wf, where, reqs)], 2.0, drain_s=60)
 print(json.dumps({k: out.get(k) for k in ("p50_ms", "p99_ms", "phase_p99_ms")}))
 for r in rt.records[:12]:
     print("  ", r.rid, round(r.arrival_ms, 1), round(r.end_ms - r.arrival_ms, 1), {k: round(v, 1) for k, v in r.phases.items()})
-tr = tube._trace or []
+tr = tube.pacer.trace()
 t0 = tr[0][0] if tr else 0
 for t, k, ev, v in tr[:120]:
     if ev != "issue":
