@@ -119,7 +119,10 @@ double p99(std::vector<double> xs);
 struct Hist {
   std::string func;
   size_t window;
-  std::deque<double> gaps, sizes, conc;
+  std::deque<double> gaps, sizes, conc;  // arrival order (window eviction)
+  // the same windows kept sorted, equal values in arrival order == sorted() of
+  // the deque (Python's sort is stable): p99 is one index, not a sort per record
+  std::vector<double> gaps_s, sizes_s, conc_s;
   bool has_last = false;
   double last = 0.0, r_window = 0.0, r_size = 0.0, r_con = 0.0;
   void record(double now, double size, double con);

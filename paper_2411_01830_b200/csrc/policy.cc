@@ -135,20 +135,32 @@ double p99(std::vector<double> xs) {  // datastore.py:32-35
   int64_t rank = std::max<int64_t>(1, py_ceil(0.99 * (double)xs.size()));
   return xs[rank - 1];
 }
+namespace {
+// nearest-rank p99 (datastore.py:32-35) of an already sorted window
+double p99_sorted(const std::vector<double>& v) {
+  int64_t rank = std::max<int64_t>(1, py_ceil(0.99 * (double)v.size()));
+  return v[rank - 1];
+}
+}  // namespace
 void Hist::record(double now, double size, double con) {  // datastore.py:51-62
   if (size < 0 || con < 0) fail(FT_E_VALUE, "histogram samples must be >= 0");
-  auto push = [this](std::deque<double>& q, double x) {
+  auto push = [this](std::deque<double>& q, std::vector<double>& s, double x) {
     q.push_back(x);
-    if (q.size() > window) q.pop_front();
+    s.insert(std::upper_bound(s.begin(), s.end(), x), x);  // after its equals: arrival order
+    if (q.size() > window) {
+      double old = q.front();  // the oldest sample: first of its equal range
+      q.pop_front();
+      s.erase(std::lower_bound(s.begin(), s.end(), old));
+    }
   };
-  if (has_last) push(gaps, now - last);
+  if (has_last) push(gaps, gaps_s, now - last);
   last = now;
   has_last = true;
-  push(sizes, size);
-  push(conc, con);
-  if (!gaps.empty()) r_window = p99({gaps.begin(), gaps.end()});
-  r_size = p99({sizes.begin(), sizes.end()});
-  r_con = p99({conc.begin(), conc.end()});
+  push(sizes, sizes_s, size);
+  push(conc, conc_s, con);
+  if (!gaps_s.empty()) r_window = p99_sorted(gaps_s);
+  r_size = p99_sorted(sizes_s);
+  r_con = p99_sorted(conc_s);
 }
 double Hist::reservation() const {  // datastore.py:64-67
   if (sizes.empty()) return 0.0;

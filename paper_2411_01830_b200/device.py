@@ -126,13 +126,21 @@ def fingerprint_host(buf) -> tuple:
 
 
 class PoolBlock:
-    """A live pool block: policy block + mapped device memory."""
+    """A live pool block: policy block + mapped device memory. ``fences``:
+    events of the previous holder's last readers/writers — a new writer's
+    stream waits on them before touching the memory (``wait_fences``)."""
 
-    __slots__ = ("policy_block", "vmm_id", "ptr", "nbytes", "device", "__weakref__")
+    __slots__ = ("policy_block", "vmm_id", "ptr", "nbytes", "device", "fences", "__weakref__")
 
-    def __init__(self, policy_block, vmm_id, ptr, nbytes, device):
+    def __init__(self, policy_block, vmm_id, ptr, nbytes, device, fences=()):
         self.policy_block, self.vmm_id, self.ptr, self.nbytes, self.device = (
             policy_block, vmm_id, ptr, nbytes, device)
+        self.fences = fences
+
+    def wait_fences(self, stream: torch.cuda.Stream):
+        for ev in self.fences:
+            stream.wait_event(ev)
+        self.fences = ()
 
 
 class DevicePool:
@@ -150,6 +158,7 @@ class DevicePool:
         LIB.ft_vmm_pool_create(int(device), int(va_bytes), C.byref(h))
         self._h = h
         self._mapped = {}  # policy block id -> (vmm id, ptr, bytes)
+        self._fences = {}  # policy block id -> events the freed block's last users recorded
         self._lock = threading.Lock()
         self.grow_events = 0
 
@@ -163,41 +172,48 @@ class DevicePool:
     __del__ = close
 
     def allocate(self, nbytes: int) -> PoolBlock:
-        """Policy decision (reuse exact class or grow) + physical mapping on growth."""
+        """Policy decision (reuse exact class or grow) + physical mapping on growth.
+        The mapping (cuMemCreate + cuMemMap + cuMemSetAccess, milliseconds for a
+        large block) runs outside the pool lock: the policy already marked the
+        block in use, so no other allocation or shrink can touch it."""
         with self._lock:
             b, _model_ms = self.policy.allocate(max(1, nbytes))
             m = self._mapped.get(b.block_id)
-            if m is None:
-                vid, ptr = C.c_uint64(), C.c_void_p()
-                LIB.ft_vmm_block_map(self._h, int(b.class_bytes), C.byref(vid), C.byref(ptr))
+            fences = self._fences.pop(b.block_id, ())
+        if m is None:
+            vid, ptr = C.c_uint64(), C.c_void_p()
+            LIB.ft_vmm_block_map(self._h, int(b.class_bytes), C.byref(vid), C.byref(ptr))
+            with self._lock:
                 m = self._mapped[b.block_id] = (vid.value, ptr.value, b.class_bytes)
                 self.grow_events += 1
-            return PoolBlock(b, m[0], m[1], m[2], self.device)
+        return PoolBlock(b, m[0], m[1], m[2], self.device, fences)
 
-    def free(self, blk: PoolBlock, fence: torch.cuda.Stream | None = None):
+    def free(self, blk: PoolBlock, fences=()):
+        """Return a block to the policy. ``fences``: events after which no
+        kernel or copy of the old holder touches it any more."""
         with self._lock:
             self.policy.free(blk.policy_block)
+            if fences:
+                self._fences[blk.policy_block.block_id] = tuple(fences)
             if self.policy.mode == "none":           # temporary allocations: give it back now
-                self._unmap(blk.policy_block.block_id, fence)
+                self._unmap(blk.policy_block.block_id)
 
     def record(self, func: str, now_ms: float, size: float, concurrency: float):
         with self._lock:
             self.policy.histogram(func).record_execution(now_ms, size, concurrency)
 
-    def shrink(self, now_ms: float, fence: torch.cuda.Stream | None = None) -> int:
+    def shrink(self, now_ms: float) -> int:
         """Apply the policy's shrink and unmap what it drops; returns bytes
-        released. ``fence``: a stream that already waits on every reader of a
-        freed block (the tube's side stream) — synchronizing it, instead of the
-        whole device, is enough before the physical memory goes back."""
+        released. Each dropped block's fences (its last users' events) are
+        waited on before its physical memory goes back — never the device."""
         with self._lock:
             dropped = self.policy.shrink(now_ms)
             gone = [self._mapped.pop(b.block_id) for b in dropped if b.block_id in self._mapped]
+            fences = [ev for b in dropped for ev in self._fences.pop(b.block_id, ())]
         if not gone:
             return 0
-        if fence is not None:
-            fence.synchronize()
-        else:
-            torch.cuda.synchronize(self.device)
+        for ev in fences:
+            ev.synchronize()
         for vid, _ptr, _n in gone:
             LIB.ft_vmm_block_unmap(self._h, vid)
         return sum(n for _, _, n in gone)
@@ -206,14 +222,12 @@ class DevicePool:
         with self._lock:
             return self.policy.hist_window(func)
 
-    def _unmap(self, block_id, fence: torch.cuda.Stream | None = None) -> int:
+    def _unmap(self, block_id) -> int:
         m = self._mapped.pop(block_id, None)
         if m is None:
             return 0
-        if fence is not None:                   # no in-flight kernel may touch it
-            fence.synchronize()
-        else:
-            torch.cuda.synchronize(self.device)
+        for ev in self._fences.pop(block_id, ()):  # no in-flight kernel may touch it
+            ev.synchronize()
         LIB.ft_vmm_block_unmap(self._h, m[0])
         return m[2]
 

@@ -204,6 +204,14 @@ class Runtime:
         rec.end_ms = now()
 
     # ------------------------------------------------------------ driver
+    @staticmethod
+    def warm_daemon(tube, jobs: list, compute: str = "sleep", seconds: float = 0.5):
+        """One untimed pass over the first ``seconds`` of the trace on ``tube``
+        (pool blocks, pinned buffers, allocator segments, kernels): measured
+        runs then see a warm daemon, as a long-running deployment does."""
+        warm = [(wf, where, [r for r in reqs if r.arrival_ms < seconds * 1e3]) for wf, where, reqs in jobs]
+        Runtime(tube, compute=compute).run(warm, seconds, drain_s=60)
+
     def run(self, jobs: list, duration_s: float, drain_s: float = 30.0, sample_ms: float = 50.0,
             idle_s: float = 1.0) -> dict:
         """jobs: [(workflow, placement, [Request])]; arrivals replayed in real time."""

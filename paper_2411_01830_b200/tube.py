@@ -52,13 +52,14 @@ from .topology import Topology, build_preset, snapshot_matrix
 __all__ = ["FaaSTube"]
 
 _ALIGN = 256  # stripe boundaries (bytes)
-_L2_KEEP = 96 << 20  # stored blocks up to this size stay L2-resident (126 MB L2) for the next fetch
+_L2_KEEP = 96 << 20
+SHRINK_MIN_GAP_MS = 2.0  # stored blocks up to this size stay L2-resident (126 MB L2) for the next fetch
 
 
 class _Obj:
     __slots__ = ("did", "nbytes", "dtype", "shape", "gpu", "block", "host", "producer", "remaining", "ready",
                  "pins", "retired", "response_host", "response_event", "stored_at", "home", "queue_pos",
-                 "__weakref__")
+                 "readers", "__weakref__")
 
     def __init__(self, did, nbytes, dtype, shape, gpu, producer, consumers, now):
         self.did, self.nbytes, self.dtype, self.shape, self.gpu = did, nbytes, dtype, shape, gpu
@@ -74,6 +75,7 @@ class _Obj:
         self.response_host = None
         self.response_event = None
         self.stored_at = now
+        self.readers = []      # events of copies on other streams/GPUs that read the block
 
 
 class FaaSTube:
@@ -118,11 +120,10 @@ class FaaSTube:
         self._t0 = time.perf_counter()
         self._objs: dict[int, _Obj] = {}
         self._lock = threading.RLock()
-        self._side = {g: torch.cuda.Stream(g) for g in self.gpus}        # store / forward stream
         self._ce = {g: [torch.cuda.Stream(g) for _ in range(2)] for g in self.gpus}  # copy-engine streams
         # per-transfer CE stream pairs (PCIe leg, NVLink forward): concurrent tenants'
         # DMA must not queue FIFO behind each other on one stream
-        self._ce_pairs = {g: [(torch.cuda.Stream(g), torch.cuda.Stream(g)) for _ in range(8)] for g in self.gpus}
+        self._ce_pairs = {g: [(torch.cuda.Stream(g), torch.cuda.Stream(g)) for _ in range(16)] for g in self.gpus}
         self._ce_rr = itertools.count()
         self._staging = {}
         self._pending_release = []   # (event, plan): NVLink claims held until the copy lands
@@ -160,12 +161,19 @@ class FaaSTube:
     def _maint_loop(self):
         """Pool shrink timer (engine.py:656-665): at last_request + R_window the
         policy drops idle blocks and their physical memory is unmapped — off the
-        request path, fenced on the side stream only."""
+        request path, fenced on each dropped block's own events. Live, due timers are
+        coalesced to at most one shrink per GPU every SHRINK_MIN_GAP_MS: under
+        a request every ~100 us, R_window is that small and a shrink per
+        request would compete with the request path for the GIL."""
+        last_run = -1e18
         while True:
             with self._maint_cv:
                 if self._closing:
                     return
                 now = self.now_ms()
+                if now - last_run < SHRINK_MIN_GAP_MS:
+                    self._maint_cv.wait((SHRINK_MIN_GAP_MS - (now - last_run)) / 1e3)
+                    continue
                 due = set()
                 while self._shrink_due and self._shrink_due[0][0] <= now:
                     due.add(heapq.heappop(self._shrink_due)[1])
@@ -173,9 +181,10 @@ class FaaSTube:
                     wait = (self._shrink_due[0][0] - now) / 1e3 if self._shrink_due else 0.1
                     self._maint_cv.wait(min(0.1, max(0.001, wait)))
                     continue
+            last_run = self.now_ms()
             for g in sorted(due):
                 if g in self.pools:
-                    self.pools[g].shrink(self.now_ms(), fence=self._side[g])
+                    self.pools[g].shrink(self.now_ms())
 
     def _stream(self, g):
         return torch.cuda.current_stream(g)
@@ -213,6 +222,7 @@ class FaaSTube:
         """An output buffer carved from the tube's pool: storing it is zero-copy."""
         nbytes = math.prod(shape) * torch.empty((), dtype=dtype).element_size()
         blk = self.pools[device].allocate(nbytes)
+        blk.wait_fences(self._stream(device))      # the block's previous users are done
         t = dev.as_tensor(blk.ptr, nbytes, device, dtype, tuple(shape), owner=blk)
         t._ft_block = blk  # noqa: SLF001 - marks pool-backed outputs
         return t
@@ -224,6 +234,25 @@ class FaaSTube:
         ``queue_pos``: request-queue position of the object's next consumer
         (the runtime knows it; default: store order) — drives queue-aware
         migration under memory pressure (datastore.py:192-222)."""
+        # pinned host buffers are allocated before taking the tube lock (cudaHostAlloc
+        # can take milliseconds and must not stall other tenants' calls)
+        pre_host = pre_blk = None
+        if output.is_cuda and (response or not self.strategy.gpu_store()):
+            pre_host = self._pinned(output.nbytes)
+        if output.is_cuda and self.strategy.gpu_store():
+            fb = getattr(output, "_ft_block", None)
+            if fb is None or fb.ptr != output.data_ptr():
+                # the pool block for the snapshot: growth maps physical memory, which
+                # must not happen under the tube lock
+                pre_blk = self.pools[output.device.index].allocate(output.nbytes)
+        try:
+            self._store_locked(data_id, output, response, producer, consumers, queue_pos, pre_host, pre_blk)
+        except BaseException:
+            if pre_blk is not None:
+                self.pools[output.device.index].free(pre_blk, list(pre_blk.fences))
+            raise
+
+    def _store_locked(self, data_id, output, response, producer, consumers, queue_pos, pre_host, pre_blk):
         with self._lock:
             self._reap()
             if data_id in self._objs:
@@ -247,12 +276,12 @@ class FaaSTube:
                     ev.record(self._stream(g))
                     obj.ready = ev
                 else:
-                    blk = pool.allocate(nbytes)          # datastore.py:130-144
+                    blk = pre_blk                        # datastore.py:130-144 (allocated above)
                     obj.block = blk
                     # snapshot on the producer's stream: ordered after the kernels that
                     # wrote the output AND before any later kernel that overwrites it
                     s = self._stream(g)
-                    s.wait_stream(self._side[g])         # the block's previous readers are done
+                    blk.wait_fences(s)                   # the block's previous users are done
                     if nbytes <= _L2_KEEP:
                         # keep the fresh block L2-resident for the consumer's fetch
                         dev.copy_hint(blk.ptr, t.data_ptr(), nbytes, g, s, dev.L2_EVICT_FIRST, dev.L2_EVICT_LAST)
@@ -267,11 +296,11 @@ class FaaSTube:
                 self._push_shrink(g, producer, now)
                 self.index.store(data_id, self._loc(g), nbytes, now, producer, response)
                 if response:
-                    self._respond(obj)
+                    self._respond(obj, pre_host)
             elif t.is_cuda:
                 # host-oriented store: the output lands in host memory (engine.py:361-381)
                 g = t.device.index
-                host = self._pinned(nbytes)
+                host = pre_host
                 s = self._ce[g][0]
                 s.wait_stream(self._stream(g))
                 dev.pcie_copy(host.data_ptr(), t.data_ptr(), nbytes, False, g, s)
@@ -343,8 +372,8 @@ class FaaSTube:
         ev = torch.cuda.Event()
         ev.record(ce)
         blk, o.block = o.block, None
-        self._side[g].wait_event(ev)                         # later writers of the block wait for the D2H
-        self.pools[g].free(blk, fence=self._side[g])
+        self.pools[g].free(blk, [ev] + o.readers)            # later writers of the block wait for the D2H
+        o.readers = []
         o.host, o.ready, o.gpu = host, ev, None
         self.index.relocate(o.did, self._loc(None))
         self.stats["migrated_bytes"] += o.nbytes
@@ -368,7 +397,7 @@ class FaaSTube:
             ce = self._ce[g][0]
             if o.ready is not None:
                 ce.wait_event(o.ready)
-            ce.wait_stream(self._side[g])
+            blk.wait_fences(ce)
             dev.pcie_copy(blk.ptr, o.host.data_ptr(), o.nbytes, True, g, ce)
             ev = torch.cuda.Event()
             ev.record(ce)
@@ -384,6 +413,12 @@ class FaaSTube:
         ``device=None`` fetches into host memory. With ``out`` the bytes land
         in the caller's buffer (Listing-1 semantics); without it a same-GPU
         fetch is a zero-copy view of the stored block."""
+        if out is None and device is not None:
+            o = self._objs.get(data_id)
+            if o is not None and o.gpu != device:
+                # a fresh input buffer (not a same-GPU view): allocated outside the tube
+                # lock — the caching allocator can stall for milliseconds
+                out = self._out(o, device, None)
         with self._lock:
             self._reap()
             obj = self._objs.get(data_id)
@@ -397,7 +432,10 @@ class FaaSTube:
                 device = out.device.index if out.is_cuda else None
             src = entry.location
             dst = self._loc(device)
-            plan = self.plane.fetch_plan(src, dst, obj.nbytes)
+            if src.node == dst.node and src.gpu is not None and src.gpu == dst.gpu:
+                plan = _INTRA_GPU        # dataplane.py:184-185: same GPU -> map only (no plan object)
+            else:
+                plan = self.plane.fetch_plan(src, dst, obj.nbytes)
             h2g = plan.method == "host_gpu" and not dst.on_host
             if h2g:
                 res, stage = self._host_to_gpu(obj, plan, dst, out, slo_ms, infer_ms)
@@ -457,19 +495,23 @@ class FaaSTube:
     def _push_shrink(self, g, func, now):
         """Shrink timer at last_request + R_window (engine.py:656-659)."""
         r_window, last = self.pools[g].hist_window(func)
+        due = (last if last is not None else now) + r_window
         with self._maint_cv:
-            heapq.heappush(self._shrink_due, ((last if last is not None else now) + r_window, g))
-            self._maint_cv.notify()
+            wake = not self._shrink_due or due < self._shrink_due[0][0]
+            heapq.heappush(self._shrink_due, (due, g))
+            if wake:                                  # only an earlier deadline needs the timer thread
+                self._maint_cv.notify()
 
-    def _respond(self, obj: _Obj):
+    def _respond(self, obj: _Obj, host=None):
         g = obj.gpu
-        host = self._pinned(obj.nbytes)
+        host = host if host is not None else self._pinned(obj.nbytes)
         s = self._ce[g][1]
         s.wait_event(obj.ready)
         dev.pcie_copy(host.data_ptr(), obj.block.ptr, obj.nbytes, False, g, s)
         ev = torch.cuda.Event()
         ev.record(s)
         obj.response_host, obj.response_event = host, ev
+        obj.readers.append(ev)
         self.stats["bytes_d2h"] += obj.nbytes
 
     def _consumed(self, obj: _Obj):
@@ -492,8 +534,9 @@ class FaaSTube:
             # later writers of this block must order after our readers
             ev = torch.cuda.Event()
             ev.record(self._stream(blk.device))
-            self._side[blk.device].wait_event(ev)
-            self.pools[blk.device].free(blk, fence=self._side[blk.device])
+            fences = [ev] + obj.readers + ([obj.ready] if obj.ready is not None else [])
+            obj.readers = []
+            self.pools[blk.device].free(blk, fences)
             self._push_shrink(blk.device, obj.producer, self.now_ms())
             if self.strategy.migration != "none":
                 self._maybe_prefetch(blk.device)             # engine.py:678-679, 717-736
@@ -552,6 +595,8 @@ class FaaSTube:
                           False, src.gpu, ce)
             ev = torch.cuda.Event()
             ev.record(ce)
+            if obj.block is not None:
+                obj.readers.append(ev)
             s.wait_event(ev)
             dev.pcie_copy(res.data_ptr(), host.data_ptr(), obj.nbytes, True, dst.gpu, s)
             host.record_stream(s) if hasattr(host, "record_stream") else None
@@ -594,7 +639,7 @@ class FaaSTube:
     def _hold_until(self, obj, ev):
         """Keep the source block alive until a reader's event completes."""
         if obj.block is not None:
-            self._side[obj.block.device].wait_event(ev)
+            obj.readers.append(ev)
 
     def _pair(self, g, slot=None):
         pairs = self._ce_pairs[g]
@@ -615,7 +660,9 @@ class FaaSTube:
         s = self._stream(dst.gpu)
         if obj.ready is not None:
             s.wait_event(obj.ready)
-        slot = next(self._ce_rr)              # this stage's own CE streams (tenants must not FIFO)
+        # CE streams keyed by the consumer's stream: a tenant's stages stay in its own
+        # FIFO, other tenants' stages (other streams) do not queue behind them
+        slot = (s.cuda_stream >> 4) * 0x9E3779B1 >> 16
         routes = []
         for b, (off, n) in zip(br, ranges):
             sg = _staging_gpu(b.links, dst.gpu)
@@ -653,7 +700,15 @@ class FaaSTube:
         return res
 
 
-def measure_pcie_gbps(gpus, nbytes: int = 64 << 20, reps: int = 8, margin: float = 1.0) -> float:
+class _IntraPlan:
+    method = "intra_gpu"
+    claimed_func = None
+
+
+_INTRA_GPU = _IntraPlan()
+
+
+def measure_pcie_gbps(gpus, nbytes: int = 64 << 20, reps: int = 12, margin: float = 1.0) -> float:
     """Pinned host->GPU copy-engine rate (GB/s) of the slowest link among
     ``gpus``: best of ``reps`` back-to-back copies after a warm-up burst (an
     idle PCIe link trains down and needs traffic to come back to full speed),

@@ -49,3 +49,24 @@ def test_tube_needs_a_gpu():
     from paper_2411_01830_b200.tube import FaaSTube
     with pytest.raises(RuntimeError):
         FaaSTube()
+
+
+def test_histogram_windows_match_oracle_with_eviction():
+    """FuncHistogram keeps its windows sorted incrementally (one insert + one
+    erase per record); p99s must equal sorted()-per-record nearest rank
+    (datastore.py:32-62) through window eviction and heavy duplicates."""
+    import random
+
+    from oracle.decisions import Hist
+    from paper_2411_01830_b200.datastore import FuncHistogram
+    rnd = random.Random(5)
+    for window in (1, 2, 7, 100, 1000):
+        h, o = FuncHistogram("f", window), Hist("f", window)
+        now = 0.0
+        for i in range(2500 if window >= 100 else 300):
+            now += rnd.choice([0.0, 0.5, 1.0, rnd.random() * 10])
+            size = float(rnd.choice([0, 2e6, 4e6, rnd.randrange(0, 10**9)]))
+            con = float(rnd.choice([0, 1, 2, 3, rnd.random() * 5]))
+            h.record_execution(now, size, con)
+            o.record(now, size, con)
+            assert (h.r_window_ms, h.r_size_bytes, h.r_con) == (o.r_window, o.r_size, o.r_con), (window, i)

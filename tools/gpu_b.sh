@@ -1,3 +1,3 @@
 mkdir -p gpurun_out
-FT_TRACE=1 timeout 120 python tools/diag_e2e.py > gpurun_out/diag_e2e_d.txt 2>&1
-timeout -s USR1 -k 30 400 python bench.py --no-extras > gpurun_out/bench_d.json 2> gpurun_out/bench_d.err; echo "bench rc=$?" >> gpurun_out/bench_d.err
+timeout 600 python -m pytest tests -q -m gpu --timeout 120 > gpurun_out/pytest_g.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_g.log
+timeout -s USR1 -k 30 600 python bench.py > gpurun_out/bench_g.json 2> gpurun_out/bench_g.err; echo "bench rc=$?" >> gpurun_out/bench_g.err

@@ -12,7 +12,7 @@ import torch  # noqa: E402
 
 from paper_2411_01830_b200.tube import FaaSTube  # noqa: E402
 
-tube = FaaSTube("faastube", pool_floor_bytes=0.0)
+tube = FaaSTube("faastube")
 x = torch.ones(4096, dtype=torch.uint8, device="cuda:0")
 out = torch.empty_like(x)
 
@@ -38,5 +38,5 @@ pr = cProfile.Profile()
 pr.enable()
 loop(2000, False)
 pr.disable()
-pstats.Stats(pr).sort_stats("tottime").print_stats(18)
+pstats.Stats(pr).sort_stats("tottime").print_stats(30)
 torch.cuda.synchronize()
