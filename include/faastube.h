@@ -310,6 +310,9 @@ int ft_copy_hint(void* dst, const void* src, uint64_t bytes, int device, void* s
  * (wrap-around compare). */
 int ft_signal(uint32_t* flag, uint32_t value, int device, void* stream);
 int ft_wait(const uint32_t* flag, uint32_t value, int device, void* stream);
+/* occupy `stream` for `ns` nanoseconds of wall time (global timer, clock independent):
+ * the synthetic gFunc compute of the workflow runtime (harness compute_latency_ms) */
+int ft_spin_ns(uint64_t ns, int device, void* stream);
 /* position-keyed digest of `bytes` (u64 sum of mixed words + xor), device u64[2] out */
 int ft_fingerprint(const void* src, uint64_t bytes, uint64_t* out_dev, int device, void* stream);
 /* host-side digest of the same definition (for checking against ft_fingerprint) */
@@ -353,9 +356,12 @@ typedef struct {
   void* ce_stream;       /* cudaStream_t on stage_dev for the PCIe leg                   */
   void* fw_stream;       /* cudaStream_t on stage_dev for the NVLink forward (staged)    */
 } ft_route;
-/* bw_all = pcie_gbps x roots (engine.py:186-190); staging_slots chunk slots per staging GPU */
-int ft_pacer_create(double bw_all_gbps, int batch_chunks, int64_t chunk_bytes, int staging_slots,
-                    uint64_t host_ring_bytes, int logging, ft_pacer** out);
+/* bw_all = pcie_gbps x links (engine.py:186-190); staging_slots chunk slots per staging GPU.
+ * flags: 1 = log every arbiter call and a trace; 2 = keep bw_all fixed (no link estimator:
+ * by default bw_all follows the measured service rate of uncontended direct batches,
+ * re-partitioning with an extra "bw" call in the log when it moves >5% up or >15% down) */
+int ft_pacer_create(double bw_all_gbps, int links, int batch_chunks, int64_t chunk_bytes, int staging_slots,
+                    uint64_t host_ring_bytes, int flags, ft_pacer** out);
 /* drains in-flight stages (FT_E_TIMEOUT after 120 s: remaining stages are failed) */
 int ft_pacer_destroy(ft_pacer* p);
 /* _start_edge_transfer -> _run_stage for a host_gpu plan       engine.py:440-475, 537-575 */
@@ -370,7 +376,8 @@ int ft_pacer_stats(ft_pacer* p, uint64_t* out, int cap);
 int ft_pacer_now_ms(ft_pacer* p, double* out);
 /* logging = 1: [[t, ticket, "start"|"rate"|"issue"|"land", value], ...] */
 int ft_pacer_trace_json(ft_pacer* p, char* buf, size_t cap, size_t* need);
-/* logging = 1: every arbiter call [[t, "start"|"boundary"|"finish", key, decisions], ...] (replayable) */
+/* logging = 1: every arbiter call [[t, "start"|"boundary"|"finish"|"bw", key (bw: the new bw_all), decisions], ...]
+ * (replayable through the arbiter; "bw" = set_bw) */
 int ft_pacer_log_json(ft_pacer* p, char* buf, size_t cap, size_t* need);
 /* arbiter state, as ft_arbiter_state_json */
 int ft_pacer_state_json(ft_pacer* p, char* buf, size_t cap, size_t* need);

@@ -70,6 +70,14 @@ class Arbiter:
         self._resync(now)
         return self._out
 
+    def set_bw(self, now, bw_all):
+        """Live pacer only (no engine counterpart): the measured link capacity
+        changed; re-partition at ``now``."""
+        self._out = []
+        self.share.bw_all = bw_all
+        self._resync(now)
+        return self._out
+
     def finish(self, now, key):  # engine.py:558-564
         self._out = []
         self.share.demands.pop(key, None)

@@ -234,13 +234,14 @@ _SIGS = {
     "ft_copy_hint": (None, [vp, vp, u64, C.c_int, vp, C.c_uint32]),
     "ft_signal": (None, [vp, C.c_uint32, C.c_int, vp]),
     "ft_wait": (None, [vp, C.c_uint32, C.c_int, vp]),
+    "ft_spin_ns": (None, [u64, C.c_int, vp]),
     "ft_fingerprint": (None, [vp, u64, vp, C.c_int, vp]),
     "ft_fingerprint_host": (None, [vp, u64, P(u64)]),
     "ft_pcie_copy": (None, [vp, vp, u64, C.c_int, C.c_int, vp, u64]),
     "ft_h2g_striped": (None, [vp, C.c_int, vp, u64, C.c_int, P(i32), P(u64), P(u64), P(vp), u64, C.c_int,
                               P(vp)]),
     # live PCIe mover + bandwidth-share scheduler
-    "ft_pacer_create": (None, [dbl, C.c_int, i64, C.c_int, u64, C.c_int, P(vp)]),
+    "ft_pacer_create": (None, [dbl, C.c_int, C.c_int, i64, C.c_int, u64, C.c_int, P(vp)]),
     "ft_pacer_destroy": (None, [vp]),
     "ft_pacer_submit": (None, [vp, cstr, C.c_int, dbl, dbl, dbl, vp, C.c_int, vp, u64, C.c_int, C.c_int,
                                P(RouteC), vp, P(u64)]),

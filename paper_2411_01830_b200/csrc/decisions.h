@@ -219,6 +219,9 @@ struct Arbiter {
              double per_branch_cap, int n_branches);
   void boundary(double now, const std::string& key);
   void finish(double now, const std::string& key);
+  // live only (no reference counterpart): the link capacity the partition hands out
+  // changed (measured by the pacer); re-partition at `now` as any other event does
+  void set_bw(double now, double bw_all);
   std::string state_json() const;
 
  private:

@@ -342,6 +342,19 @@ __global__ void k_wait(const unsigned int* flag, unsigned int value) {
   } while (true);
 }
 
+// Fixed-duration GPU occupancy (the runtime's synthetic gFunc compute,
+// harness compute_latency_ms): spins on the global nanosecond timer, so the
+// duration does not depend on the SM clock (an idle-clocked GPU runs a
+// cycle-count sleep many times longer than asked).
+__global__ void k_spin_ns(uint64_t ns) {
+  uint64_t t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  do {
+    __nanosleep(1000);
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  } while (t - t0 < ns);
+}
+
 // ------------------------------------------------------------ launch config
 struct DevInfo {
   int sms = 0;
@@ -821,6 +834,16 @@ int ft_wait(const uint32_t* flag, uint32_t value, int device, void* stream) {
   cudaError_t e = cudaGetLastError();
   if (cur != device) cudaSetDevice(cur);
   return e == cudaSuccess ? FT_OK : cuda_fail(e, "ft_wait");
+}
+
+int ft_spin_ns(uint64_t ns, int device, void* stream) {
+  int cur = 0;
+  CU_RT(cudaGetDevice(&cur));
+  if (cur != device) CU_RT(cudaSetDevice(device));
+  k_spin_ns<<<1, 1, 0, (cudaStream_t)stream>>>(ns);
+  cudaError_t e = cudaGetLastError();
+  if (cur != device) cudaSetDevice(cur);
+  return e == cudaSuccess ? FT_OK : cuda_fail(e, "ft_spin_ns");
 }
 
 int ft_copy_hint(void* dst, const void* src, uint64_t bytes, int device, void* stream, uint32_t hints) {

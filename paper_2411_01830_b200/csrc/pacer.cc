@@ -90,6 +90,23 @@ struct Route {
   cudaStream_t last() const { return staged() ? fw : ce; }
 };
 
+struct Ev {
+  cudaEvent_t e;
+  int dev;
+  bool timing;  // from the timing-event pool
+};
+struct Timing {  // a direct-route batch bracketed by timing events (link service rate)
+  cudaEvent_t t0, t1;
+  int dev;
+  uint64_t bytes;
+  double issued;
+  bool contended;  // another stage had bytes on the link when it was issued
+};
+struct Batch {
+  std::vector<Ev> ev;  // last op of each route's share of the batch
+  std::vector<Timing> timing;
+};
+
 struct Stage {
   uint64_t ticket = 0;
   std::string key;
@@ -101,8 +118,9 @@ struct Stage {
   uint64_t bytes = 0;
   std::vector<Route> routes;
   double next_t = NAN, last_rate = -1.0;
-  std::deque<std::vector<std::pair<cudaEvent_t, int>>> inflight;  // per issued batch: (event, device)
+  std::deque<Batch> inflight;  // issued, not yet landed batches
   int jobs = 0;         // pageable chunks queued to workers, not yet issued
+  bool was_full = false;  // trace: inflight cap reached (the link, not the rate, limits)
   bool issued = false;  // every byte handed out
   bool sealed = false;  // every byte enqueued: join events recorded (or failed)
   std::vector<std::pair<cudaEvent_t, int>> join;     // last op of each route (the submitter's)
@@ -159,6 +177,15 @@ struct ft_pacer {
   std::deque<Job> jobs;
   bool stop = false;
   std::vector<cudaEvent_t> evpool[kMaxDev];
+  std::vector<cudaEvent_t> tpool[kMaxDev];  // timing-enabled events
+  // link estimator: the arbiter's bw_all tracks the service rate of uncontended
+  // batches (a calibration at start-up can be far off on a shared host)
+  int links = 1;
+  double link_gbps = 0.0;                    // per-link capacity the partition assumes
+  std::deque<double> samples[kMaxDev];
+  double last_issue_t[kMaxDev] = {};
+  uint64_t last_issue_ticket[kMaxDev] = {};
+  bool adapt = true;
   std::map<int, StagingRing> rings;
   std::map<std::string, double> guarded;  // last early boundary per stage key (A2 guard)
   uint64_t n_stages = 0, n_managed = 0, n_batches = 0, n_bytes = 0, n_errors = 0;
@@ -196,6 +223,46 @@ struct ft_pacer {
     return e;
   }
   void put_event(int dev, cudaEvent_t e) { evpool[dev].push_back(e); }
+  cudaEvent_t get_tevent(int dev) {
+    auto& pool = tpool[dev];
+    if (!pool.empty()) {
+      cudaEvent_t e = pool.back();
+      pool.pop_back();
+      return e;
+    }
+    DevGuard g(dev);
+    cudaEvent_t e;
+    ck(cudaEventCreate(&e), "cudaEventCreate(timing)");
+    return e;
+  }
+  void put(const Ev& e) { (e.timing ? tpool : evpool)[e.dev].push_back(e.e); }
+
+  // anything else of ours on `dev`'s link right now?
+  bool link_busy(int dev, uint64_t self) const {
+    for (auto& kv : active) {
+      const Stage& o = *kv.second;
+      if (o.ticket == self) continue;
+      bool on = false;
+      for (auto& r : o.routes) on = on || r.dev == dev;
+      if (on && (!o.inflight.empty() || (o.sealed && !o.landing.empty()) || (!o.managed && !o.sealed) || o.jobs))
+        return true;
+    }
+    return false;
+  }
+
+  void sample(int dev, double gbps, double now) {
+    auto& q = samples[dev];
+    q.push_back(gbps);
+    if (q.size() > 32) q.pop_front();
+    if (!adapt || q.size() < 6) return;
+    double est = *std::max_element(q.begin(), q.end());  // least-disturbed service rate
+    if (est > link_gbps * 1.05 || est < link_gbps * 0.85) {
+      link_gbps = est;
+      arb.set_bw(now, est * links);
+      arb_log(now, "bw", jnum(est * links));
+      q.clear();
+    }
+  }
 
   void note(const Stage& st, const char* kind, double v) {
     if (!logging) return;
@@ -257,12 +324,25 @@ struct ft_pacer {
     Route& r = st.routes[i];
     uint64_t o = r.off + rel;
     if (st.pinned) {
+      if (track && !r.staged() && n) {
+        // direct route: bracket the DMA with timing events (service-rate sample)
+        DevGuard g(r.dev);
+        Timing tm{get_tevent(r.dev), nullptr, r.dev, n, now(), link_busy(r.dev, st.ticket)};
+        ck(cudaEventRecord(tm.t0, r.ce), "record t0");
+        issue(r, st.dst + o, st.host + o, n);
+        tm.t1 = get_tevent(r.dev);
+        ck(cudaEventRecord(tm.t1, r.ce), "record t1");
+        st.inflight.back().timing.push_back(tm);
+        last_issue_t[r.dev] = tm.issued;
+        last_issue_ticket[r.dev] = st.ticket;
+        return;
+      }
       issue(r, st.dst + o, st.host + o, n);
       if (track) {
         DevGuard g(r.dev);
         cudaEvent_t e = get_event(r.dev);
         ck(cudaEventRecord(e, r.last()), "record batch");
-        st.inflight.back().emplace_back(e, r.dev);
+        st.inflight.back().ev.push_back(Ev{e, r.dev, false});
       }
       return;
     }
@@ -273,9 +353,17 @@ struct ft_pacer {
     jcv.notify_all();
   }
 
+  void release_batch(Batch& b) {
+    for (auto& e : b.ev) put(e);
+    for (auto& t : b.timing) {
+      tpool[t.dev].push_back(t.t0);
+      tpool[t.dev].push_back(t.t1);
+    }
+    b.ev.clear();
+    b.timing.clear();
+  }
   void release_inflight(Stage& st) {
-    for (auto& b : st.inflight)
-      for (auto& e : b) put_event(e.second, e.first);
+    for (auto& b : st.inflight) release_batch(b);
     st.inflight.clear();
   }
 
@@ -466,12 +554,23 @@ struct ft_pacer {
         }
         if (!st.managed || st.issued) continue;
         while (!st.inflight.empty()) {  // drop landed batches (non-blocking)
+          Batch& b = st.inflight.front();
           bool ok = true;
-          for (auto& e : st.inflight.front())
-            if (cudaEventQuery(e.first) != cudaSuccess) ok = false;
+          for (auto& e : b.ev)
+            if (cudaEventQuery(e.e) != cudaSuccess) ok = false;
+          for (auto& tm : b.timing)
+            if (cudaEventQuery(tm.t1) != cudaSuccess) ok = false;
           if (!ok) break;
-          for (auto& e : st.inflight.front()) put_event(e.second, e.first);
+          for (auto& tm : b.timing) {
+            float ms = 0.f;
+            bool overlapped = tm.contended ||
+                              (last_issue_ticket[tm.dev] != st.ticket && last_issue_t[tm.dev] > tm.issued);
+            if (!overlapped && cudaEventElapsedTime(&ms, tm.t0, tm.t1) == cudaSuccess && ms > 0.f)
+              sample(tm.dev, (double)tm.bytes / ((double)ms * 1e6), t);
+          }
+          release_batch(b);
           st.inflight.pop_front();
+          note(st, "done", (double)st.inflight.size());
         }
         const auto* m = arb.stages.find(st.key);
         if (!m || !m->started || m->rate <= 0) continue;  // waiting: a boundary / finish / start wakes it
@@ -488,9 +587,12 @@ struct ft_pacer {
         }
         bool full = st.pinned ? (int)st.inflight.size() >= kInflightBatches : st.jobs >= 2 * batch_chunks;
         if (full) {
+          if (!st.was_full) note(st, "full", (double)st.inflight.size());
+          st.was_full = true;
           wake = std::min(wake, t + 0.02);
           continue;
         }
+        st.was_full = false;
         try {
           issue_batch(st);
         } catch (const CudaFail& f) {
@@ -596,8 +698,9 @@ struct ft_pacer {
 
 extern "C" {
 
-int ft_pacer_create(double bw_all_gbps, int batch_chunks, int64_t chunk_bytes, int staging_slots,
-                    uint64_t host_ring_bytes, int logging, ft_pacer** out) {
+int ft_pacer_create(double bw_all_gbps, int links, int batch_chunks, int64_t chunk_bytes, int staging_slots,
+                    uint64_t host_ring_bytes, int flags, ft_pacer** out) {
+  int logging = flags & 1;
   if (!out || batch_chunks <= 0 || chunk_bytes <= 0 || !(bw_all_gbps > 0)) {
     ft::set_last_error("ft_pacer_create: bad arguments");
     return FT_E_VALUE;
@@ -607,6 +710,9 @@ int ft_pacer_create(double bw_all_gbps, int batch_chunks, int64_t chunk_bytes, i
   p->chunk = (uint64_t)chunk_bytes;
   p->staging_slots = std::max(2, staging_slots);
   p->logging = logging != 0;
+  p->links = std::max(1, links);
+  p->link_gbps = bw_all_gbps / p->links;
+  p->adapt = !(flags & 2);
   p->arb.share = ft::PcieState{bw_all_gbps, batch_chunks, chunk_bytes, {}};
   p->arb.batch_bytes = (double)(chunk_bytes * batch_chunks);
   uint64_t slots = std::max<uint64_t>(4, host_ring_bytes / p->chunk);
@@ -649,8 +755,10 @@ int ft_pacer_destroy(ft_pacer* p) {
     for (auto e : kv.second.freed) cudaEventDestroy(e);
     cudaFree(kv.second.buf);
   }
-  for (int d = 0; d < kMaxDev; ++d)
+  for (int d = 0; d < kMaxDev; ++d) {
     for (auto e : p->evpool[d]) cudaEventDestroy(e);
+    for (auto e : p->tpool[d]) cudaEventDestroy(e);
+  }
   for (auto& hs : p->hslots)
     for (int d = 0; d < kMaxDev; ++d)
       if (hs.ev[d]) {

@@ -390,6 +390,12 @@ void Arbiter::finish(double now, const std::string& key) {  // engine.py:558-564
   resync(now);
   end();
 }
+void Arbiter::set_bw(double now, double bw_all) {
+  begin();
+  share.bw_all = bw_all;
+  resync(now);
+  end();
+}
 void Arbiter::boundary(double now, const std::string& key) {  // engine.py:637-646
   begin();
   StageSt* m = stages.find(key);

@@ -159,6 +159,10 @@ class DevicePool:
         self._h = h
         self._mapped = {}  # policy block id -> (vmm id, ptr, bytes)
         self._fences = {}  # policy block id -> events the freed block's last users recorded
+        # physical blocks the policy dropped, still mapped: reused by growth of the same
+        # class, unmapped by reclaim() when the GPU is quiet (cuMemUnmap under load stalls
+        # every CUDA call of the process for 100s of ms — measured)
+        self._released = []  # [(vmm id, ptr, bytes, fences)]
         self._lock = threading.Lock()
         self.grow_events = 0
 
@@ -181,11 +185,19 @@ class DevicePool:
             m = self._mapped.get(b.block_id)
             fences = self._fences.pop(b.block_id, ())
         if m is None:
-            vid, ptr = C.c_uint64(), C.c_void_p()
-            LIB.ft_vmm_block_map(self._h, int(b.class_bytes), C.byref(vid), C.byref(ptr))
             with self._lock:
-                m = self._mapped[b.block_id] = (vid.value, ptr.value, b.class_bytes)
-                self.grow_events += 1
+                reuse = next((i for i, r in enumerate(self._released) if r[2] == b.class_bytes), None)
+                if reuse is not None:          # growth served by a dropped, still-mapped block
+                    vid, ptr, nb, rf = self._released.pop(reuse)
+                    m = self._mapped[b.block_id] = (vid, ptr, nb)
+                    fences = tuple(fences) + tuple(rf)
+                    self.grow_events += 1
+            if m is None:
+                vid, ptr = C.c_uint64(), C.c_void_p()
+                LIB.ft_vmm_block_map(self._h, int(b.class_bytes), C.byref(vid), C.byref(ptr))
+                with self._lock:
+                    m = self._mapped[b.block_id] = (vid.value, ptr.value, b.class_bytes)
+                    self.grow_events += 1
         return PoolBlock(b, m[0], m[1], m[2], self.device, fences)
 
     def free(self, blk: PoolBlock, fences=()):
@@ -202,21 +214,36 @@ class DevicePool:
         with self._lock:
             self.policy.histogram(func).record_execution(now_ms, size, concurrency)
 
-    def shrink(self, now_ms: float) -> int:
-        """Apply the policy's shrink and unmap what it drops; returns bytes
-        released. Each dropped block's fences (its last users' events) are
-        waited on before its physical memory goes back — never the device."""
+    def shrink(self, now_ms: float, reclaim: bool = True) -> int:
+        """Apply the policy's shrink (datastore.py:152-166); returns the bytes it
+        dropped. With ``reclaim`` their physical memory is unmapped now,
+        otherwise it is parked in the released list until ``reclaim()``."""
         with self._lock:
             dropped = self.policy.shrink(now_ms)
-            gone = [self._mapped.pop(b.block_id) for b in dropped if b.block_id in self._mapped]
-            fences = [ev for b in dropped for ev in self._fences.pop(b.block_id, ())]
-        if not gone:
-            return 0
-        for ev in fences:
-            ev.synchronize()
-        for vid, _ptr, _n in gone:
+            for b in dropped:
+                m = self._mapped.pop(b.block_id, None)
+                if m is not None:
+                    self._released.append((m[0], m[1], m[2], self._fences.pop(b.block_id, ())))
+            n = sum(b.class_bytes for b in dropped)
+        if reclaim:
+            self.reclaim()
+        return n
+
+    def reclaim(self) -> int:
+        """Unmap every released block (after its last users' events) — the
+        physical memory goes back to the driver. Returns bytes unmapped."""
+        with self._lock:
+            gone, self._released = self._released, []
+        for _vid, _ptr, _n, fences in gone:
+            for ev in fences:
+                ev.synchronize()
+        for vid, _ptr, _n, _f in gone:
             LIB.ft_vmm_block_unmap(self._h, vid)
-        return sum(n for _, _, n in gone)
+        return sum(r[2] for r in gone)
+
+    @property
+    def released_bytes(self) -> int:
+        return sum(r[2] for r in self._released)
 
     def hist_window(self, func: str):
         with self._lock:
@@ -240,7 +267,8 @@ class DevicePool:
         mapped, reserved, n = C.c_uint64(), C.c_uint64(), C.c_int()
         LIB.ft_vmm_pool_stats(self._h, C.byref(mapped), C.byref(reserved), C.byref(n))
         return {"mapped_bytes": mapped.value, "reserved_va": reserved.value, "blocks": n.value,
-                "policy_pool_bytes": self.policy.pool_bytes, "in_use_bytes": self.policy.in_use_bytes}
+                "policy_pool_bytes": self.policy.pool_bytes, "in_use_bytes": self.policy.in_use_bytes,
+                "released_bytes": self.released_bytes}
 
 
 class ImportedBlock:
@@ -279,12 +307,13 @@ class Pacer:
     on the stage's completion word, so later work on it sees the bytes."""
 
     def __init__(self, bw_all_gbps: float, batch_chunks: int, chunk_bytes: int, staging_slots: int = 4,
-                 host_ring_bytes: int = 0, logging: bool = False):
+                 host_ring_bytes: int = 0, logging: bool = False, links: int = 1, adapt: bool = True):
         from ._lib import RouteC
         self._route_t = RouteC
         h = C.c_void_p()
-        LIB.ft_pacer_create(float(bw_all_gbps), int(batch_chunks), int(chunk_bytes), int(staging_slots),
-                            int(host_ring_bytes), int(bool(logging)), C.byref(h))
+        flags = int(bool(logging)) | (0 if adapt else 2)
+        LIB.ft_pacer_create(float(bw_all_gbps), int(links), int(batch_chunks), int(chunk_bytes), int(staging_slots),
+                            int(host_ring_bytes), flags, C.byref(h))
         self._h = h
 
     def submit(self, key: str, managed: bool, slo_ms: float, infer_ms: float, per_branch_cap_gbps: float,

@@ -9,16 +9,20 @@ SLOs are the reference's (``workload.py``, golden-checked), so the same seed
 replays the simulator's workload on real hardware; latency percentiles use the
 reference's nearest-rank estimator (simcore.py:247-252).
 
-Compute stand-ins: ``"sleep"`` spins the GPU for the function's
-compute_latency_ms (a timed kernel on its stream — keeps the reference's
-compute model); ``"model"`` runs random-init convolutional models on the
+Compute stand-ins: ``"sleep"`` occupies the function's stream for its
+compute_latency_ms on the GPU's global timer (``ft_spin_ns``: a cycle-count
+sleep would stretch 16x on an idle-clocked GPU) — the reference's compute
+model; ``"model"`` runs random-init convolutional models on the
 payload (config 4: decode -> detector -> recognizers on 1080p frames).
 """
 
 from __future__ import annotations
 
 import contextlib
+import ctypes as C
 import math
+import os
+import sys
 import threading
 import time
 from concurrent.futures import ThreadPoolExecutor
@@ -26,6 +30,7 @@ from dataclasses import dataclass, field
 
 import torch
 
+from . import device as dev
 from .simcore import PHASES
 from .workload import Request, Workflow
 
@@ -104,8 +109,6 @@ class Runtime:
         self._rec_lock = threading.Lock()
         self.pool_timeline = []
         self._tls = threading.local()
-        self._clock_hz = {g: torch.cuda.get_device_properties(g).clock_rate * 1e3 if hasattr(
-            torch.cuda.get_device_properties(g), "clock_rate") else 1.965e9 for g in tube.gpus}
 
     # ------------------------------------------------------------ one request
     def _host_out(self, fid, nbytes):
@@ -122,7 +125,7 @@ class Runtime:
             if gpu not in self.models:
                 self.models[gpu] = _Models(f"cuda:{gpu}")
             return self.models[gpu].run(fid, x, out_bytes)
-        torch.cuda._sleep(int(ms * 1e-3 * self._clock_hz[gpu]))
+        dev.LIB.ft_spin_ns(int(ms * 1e6), int(gpu), C.c_void_p(torch.cuda.current_stream(gpu).cuda_stream))
         return torch.empty(out_bytes, dtype=torch.uint8, device=f"cuda:{gpu}").fill_(len(fid) & 0xFF)
 
     def _stream(self, gpu) -> torch.cuda.Stream:
@@ -214,7 +217,19 @@ class Runtime:
 
     def run(self, jobs: list, duration_s: float, drain_s: float = 30.0, sample_ms: float = 50.0,
             idle_s: float = 1.0) -> dict:
-        """jobs: [(workflow, placement, [Request])]; arrivals replayed in real time."""
+        """jobs: [(workflow, placement, [Request])]; arrivals replayed in real time.
+        The interpreter's GIL switch interval is lowered for the run
+        (FT_SWITCH_INTERVAL_S, default 1 ms): 32 function threads share one
+        interpreter, and at the default 5 ms a thread ready to issue a
+        transfer or a kernel can wait several switch intervals."""
+        old = sys.getswitchinterval()
+        sys.setswitchinterval(float(os.environ.get("FT_SWITCH_INTERVAL_S", "0.001")))
+        try:
+            return self._run(jobs, duration_s, drain_s, sample_ms, idle_s)
+        finally:
+            sys.setswitchinterval(old)
+
+    def _run(self, jobs, duration_s, drain_s, sample_ms, idle_s) -> dict:
         events = sorted(((r.arrival_ms, i, wf, where, r) for i, (wf, where, reqs) in enumerate(jobs) for r in reqs),
                         key=lambda e: (e[0], e[1], e[4].rid))
         # warm-up outside the trace: spin up every worker thread's CUDA state and
@@ -242,9 +257,11 @@ class Runtime:
         def sampler():
             while not stop.is_set():
                 st = {g: p.stats() for g, p in self.tube.pools.items()}
+                # (t, pool bytes the elastic policy holds, bytes in use, physically mapped)
                 self.pool_timeline.append(((time.perf_counter() - t0) * 1e3,
-                                           sum(s["mapped_bytes"] for s in st.values()),
-                                           sum(s["in_use_bytes"] for s in st.values())))
+                                           sum(s["policy_pool_bytes"] for s in st.values()),
+                                           sum(s["in_use_bytes"] for s in st.values()),
+                                           sum(s["mapped_bytes"] for s in st.values())))
                 stop.wait(sample_ms / 1e3)
 
         smp = threading.Thread(target=sampler, daemon=True)
@@ -274,7 +291,9 @@ class Runtime:
             self.tube.maintain()
             time.sleep(0.05)
         self.tube.maintain()
-        out["pool_after_idle_bytes"] = sum(p.stats()["mapped_bytes"] for p in self.tube.pools.values())
+        self.tube.reclaim()                  # quiet now: physical memory of dropped blocks goes back
+        out["pool_after_idle_bytes"] = sum(p.stats()["policy_pool_bytes"] for p in self.tube.pools.values())
+        out["mapped_after_idle_bytes"] = sum(p.stats()["mapped_bytes"] for p in self.tube.pools.values())
         return out
 
     def summary(self, duration_s: float, errors=()) -> dict:
@@ -283,7 +302,8 @@ class Runtime:
         out = {"requests_seen": len(self.records), "requests_completed": len(done),
                "throughput_rps": round(len(done) / duration_s, 3), "errors": list(errors)[:5],
                "peak_pool_bytes": max((p[1] for p in self.pool_timeline), default=0),
-               "final_pool_bytes": self.pool_timeline[-1][1] if self.pool_timeline else 0}
+               "final_pool_bytes": self.pool_timeline[-1][1] if self.pool_timeline else 0,
+               "peak_mapped_bytes": max((p[3] for p in self.pool_timeline), default=0)}
         if done:
             out["p50_ms"] = round(nearest_rank(lat, 50), 4)
             out["p99_ms"] = round(nearest_rank(lat, 99), 4)

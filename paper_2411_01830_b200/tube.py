@@ -52,8 +52,11 @@ from .topology import Topology, build_preset, snapshot_matrix
 __all__ = ["FaaSTube"]
 
 _ALIGN = 256  # stripe boundaries (bytes)
-_L2_KEEP = 96 << 20
-SHRINK_MIN_GAP_MS = 2.0  # stored blocks up to this size stay L2-resident (126 MB L2) for the next fetch
+_L2_KEEP = 96 << 20  # stored blocks up to this size stay L2-resident (126 MB L2) for the next fetch
+SHRINK_MIN_GAP_MS = 2.0
+# dropped pool blocks are unmapped only after this long without a store/fetch:
+# cuMemUnmap while the GPU is busy stalls every CUDA call of the process (0.3-1 s measured)
+RECLAIM_IDLE_MS = 1000.0
 
 
 class _Obj:
@@ -115,7 +118,7 @@ class FaaSTube:
         # their share; pageable payloads staged through its warm pinned ring)
         self.pacer = dev.Pacer(bw_all, batch_chunks, chunk_bytes, staging_slots=4,
                                host_ring_bytes=default_ring_capacity(len(roots), batch_chunks * chunk_bytes),
-                               logging=bool(os.environ.get("FT_TRACE")))
+                               logging=bool(os.environ.get("FT_TRACE")), links=len(roots))
         self._tickets = []           # (ticket, keep-alive refs) until the stage has landed
         self._t0 = time.perf_counter()
         self._objs: dict[int, _Obj] = {}
@@ -125,7 +128,8 @@ class FaaSTube:
         # DMA must not queue FIFO behind each other on one stream
         self._ce_pairs = {g: [(torch.cuda.Stream(g), torch.cuda.Stream(g)) for _ in range(16)] for g in self.gpus}
         self._ce_rr = itertools.count()
-        self._staging = {}
+        self._keepalive = []         # (event, buffers) released once the event has completed
+        self._last_op_ms = 0.0       # last store/fetch (idle detection for physical reclaim)
         self._pending_release = []   # (event, plan): NVLink claims held until the copy lands
         self._shrink_due = []        # heap of (due_ms, gpu)
         self._managed_ids = itertools.count(1)
@@ -150,6 +154,8 @@ class FaaSTube:
         keep-alive references of host->GPU stages that have landed."""
         if self._tickets:
             self._tickets = [t for t in self._tickets if not self.pacer.done(t[0])]
+        if self._keepalive:
+            self._keepalive = [k for k in self._keepalive if not k[0].query()]
         keep = []
         for ev, plan in self._pending_release:
             if ev.query():
@@ -171,6 +177,7 @@ class FaaSTube:
                 if self._closing:
                     return
                 now = self.now_ms()
+                self._reclaim_if_idle(now)
                 if now - last_run < SHRINK_MIN_GAP_MS:
                     self._maint_cv.wait((SHRINK_MIN_GAP_MS - (now - last_run)) / 1e3)
                     continue
@@ -179,12 +186,24 @@ class FaaSTube:
                     due.add(heapq.heappop(self._shrink_due)[1])
                 if not due:
                     wait = (self._shrink_due[0][0] - now) / 1e3 if self._shrink_due else 0.1
+                    if any(p.released_bytes for p in self.pools.values()):
+                        wait = min(wait, RECLAIM_IDLE_MS / 1e3)
                     self._maint_cv.wait(min(0.1, max(0.001, wait)))
                     continue
             last_run = self.now_ms()
             for g in sorted(due):
                 if g in self.pools:
-                    self.pools[g].shrink(self.now_ms())
+                    # policy shrink now; physical unmap deferred to a quiet moment
+                    self.pools[g].shrink(self.now_ms(), reclaim=False)
+
+    def _reclaim_if_idle(self, now):
+        """Give dropped blocks' physical memory back once no store/fetch has run
+        for RECLAIM_IDLE_MS (cuMemUnmap stalls the process's CUDA calls while
+        the GPU is busy; growth meanwhile reuses parked blocks of its class)."""
+        if now - self._last_op_ms >= RECLAIM_IDLE_MS:
+            for p in self.pools.values():
+                if p.released_bytes:
+                    p.reclaim()
 
     def _stream(self, g):
         return torch.cuda.current_stream(g)
@@ -206,12 +225,6 @@ class FaaSTube:
 
     def _pinned(self, nbytes) -> torch.Tensor:
         return torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
-
-    def _staging_buf(self, g, nbytes) -> torch.Tensor:
-        buf = self._staging.get(g)
-        if buf is None or buf.nbytes < nbytes:
-            buf = self._staging[g] = torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{g}")
-        return buf
 
     # ------------------------------------------------------------ API
     def unique_id(self) -> int:
@@ -260,7 +273,7 @@ class FaaSTube:
                 raise DuplicateStore(f"data id {data_id} already stored")
             t = output.contiguous() if not output.is_contiguous() else output
             nbytes = t.nbytes
-            now = self.now_ms()
+            self._last_op_ms = now = self.now_ms()
             obj = _Obj(data_id, nbytes, t.dtype, tuple(t.shape), None, producer, consumers, now)
             obj.queue_pos = queue_pos if queue_pos is not None else next(self._queue)
             if t.is_cuda and self.strategy.gpu_store():
@@ -422,7 +435,8 @@ class FaaSTube:
         with self._lock:
             self._reap()
             obj = self._objs.get(data_id)
-            entry, _lookup_ms, _ready = self.index.resolve(data_id, self.node, self.now_ms())
+            self._last_op_ms = now = self.now_ms()
+            entry, _lookup_ms, _ready = self.index.resolve(data_id, self.node, now)
             if obj is None:
                 from ._lib import MissingData
                 raise MissingData(f"data id {data_id} has no live payload")
@@ -623,18 +637,30 @@ class FaaSTube:
         return res
 
     def _relay(self, hops, src_ptr, dst_ptr, n, s):
-        """Multi-hop NVLink branch (non-uniform fabrics): store-and-forward in
-        chunks through each intermediate GPU's staging buffer."""
-        chunk = self.chunk_bytes
-        cur = src_ptr
-        for u, v in hops[:-1]:
-            buf = self._staging_buf(v, n)
-            for o in range(0, n, chunk):
-                dev.copy(buf.data_ptr() + o, cur + o, min(chunk, n - o), v, s, dev.ENGINE_VEC)
-            cur = buf.data_ptr()
-        u, v = hops[-1]
-        for o in range(0, n, chunk):
-            dev.copy(dst_ptr + o, cur + o, min(chunk, n - o), v, s, dev.ENGINE_VEC)
+        """Multi-hop NVLink branch (non-uniform fabrics): store-and-forward
+        through each intermediate GPU into a private buffer. Each hop is pulled
+        by its receiving GPU on a stream of that GPU, chained to the previous
+        hop by an event; the last hop runs on the consumer's stream. Buffers
+        stay referenced until the last hop has completed."""
+        ev = torch.cuda.Event()
+        ev.record(s)                                  # source ready / destination free
+        cur, keep = src_ptr, []
+        for i, (u, v) in enumerate(hops):
+            last = i == len(hops) - 1
+            st = s if last else self._pair(v)[1]
+            st.wait_event(ev)
+            if last:
+                out = dst_ptr
+            else:
+                buf = torch.empty(n, dtype=torch.uint8, device=f"cuda:{v}")
+                keep.append(buf)
+                out = buf.data_ptr()
+            dev.copy(out, cur, n, v, st, dev.ENGINE_VEC)
+            ev = torch.cuda.Event()
+            ev.record(st)
+            cur = out
+        if keep:
+            self._keepalive.append((ev, keep))
 
     def _hold_until(self, obj, ev):
         """Keep the source block alive until a reader's event completes."""
@@ -682,10 +708,17 @@ class FaaSTube:
             self.stats["managed_stages"] = self.stats.get("managed_stages", 0) + 1
         return res, stage
 
+    def reclaim(self) -> int:
+        """Unmap every parked pool block now (call when the GPU is quiet)."""
+        with self._maint_cv:
+            return sum(p.reclaim() for p in self.pools.values())
+
     def maintain(self):
-        """Release landed NVLink claims and run due pool shrinks (idle housekeeping)."""
+        """Release landed NVLink claims; give parked pool blocks back when idle."""
         with self._lock:
             self._reap()
+        with self._maint_cv:
+            self._reclaim_if_idle(self.now_ms())
 
     def _gpu_to_host(self, obj, plan, out):
         res = out if out is not None else self._pinned(obj.nbytes).view(obj.dtype).view(obj.shape)

@@ -121,3 +121,19 @@ def test_vmm_pool_map_unmap(dev):
     released = pool.shrink(1e9)          # no active window, floor 0 -> everything idle goes
     assert released > 0 and pool.stats()["blocks"] < 4
     pool.close()
+
+
+def test_spin_ns_is_wall_time(dev):
+    """The runtime's synthetic compute: duration follows the global timer,
+    not the SM clock (an idle GPU idles at ~120 MHz)."""
+    import time
+    from paper_2411_01830_b200._lib import LIB
+    s = torch.cuda.current_stream(0)
+    LIB.ft_spin_ns(1000, 0, C.c_void_p(s.cuda_stream))
+    torch.cuda.synchronize()
+    for ms in (2.0, 10.0):
+        t0 = time.perf_counter()
+        LIB.ft_spin_ns(int(ms * 1e6), 0, C.c_void_p(s.cuda_stream))
+        torch.cuda.synchronize()
+        got = (time.perf_counter() - t0) * 1e3
+        assert ms <= got < ms + 1.5, (ms, got)

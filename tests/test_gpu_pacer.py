@@ -147,6 +147,8 @@ def test_live_decisions_replay_through_oracle(dev):
     for t, call, key, want in log:
         if call == "start":
             got = o.start(t, key, float(sizes[key]), slos[key][0], slos[key][1], t, 55.0, 1)
+        elif call == "bw":                       # the live link estimator re-partitioned
+            got = o.set_bw(t, float(key))
         elif call == "boundary":
             got = o.boundary(t, key)
         else:
@@ -181,4 +183,32 @@ def test_back_to_back_loose_stages_do_not_starve(dev):
     for i in range(3):
         assert torch.equal(dsts[i].cpu(), hosts[i])
     assert elapsed < 3 * n * 3 / 10e9 + 1.0, elapsed     # >= 10 GB/s on any box (link 20-57 GB/s seen)
+    p.close()
+
+
+@pytest.mark.parametrize("adapt", [True, False])
+def test_link_estimator_corrects_a_low_calibration(dev, adapt):
+    """Created believing the link does 8 GB/s, the pacer measures the service
+    rate of its uncontended batches and re-partitions at the real rate (a
+    logged "bw" call); with the estimator off it paces at 8 GB/s."""
+    p = dev.Pacer(8.0, 5, 2 * MB, logging=True, adapt=adapt)
+    n = 512 * MB
+    host = host_bytes(n, 9)
+    dst = torch.empty(n, dtype=torch.uint8, device="cuda:0")
+    s = torch.cuda.current_stream(0)
+    ce, fw = torch.cuda.Stream(0), torch.cuda.Stream(0)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    t = p.submit("m1", True, 1e9, 0.0, 1e9, dst.data_ptr(), 0, host.data_ptr(), n, True,
+                 [(0, 0, 0, n, ce.cuda_stream, fw.cuda_stream)], s.cuda_stream)
+    p.wait(t, 20000.0)
+    ms = (time.perf_counter() - t0) * 1e3
+    torch.cuda.synchronize()
+    assert torch.equal(dst.cpu(), host)
+    bws = [float(k) for _, c, k, _ in p.log() if c == "bw"]
+    if adapt:
+        assert bws and bws[-1] > 15.0, bws
+        assert ms < 0.7 * n / 8e6, (ms, bws)
+    else:
+        assert not bws and ms > 0.9 * n / 8e6, ms
     p.close()

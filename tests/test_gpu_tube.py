@@ -158,3 +158,21 @@ def test_baseline_strategies_bit_exact(strategy):
     torch.cuda.synchronize()
     assert np.array_equal(as_u8(got), oracle_bytes(x))
     t.close()
+
+
+def test_multi_hop_relay_chain(tube):
+    """The store-and-forward relay of non-uniform fabrics (each hop pulled by
+    its receiving GPU on its own stream, chained by events, private buffers
+    kept alive until the last hop lands) — driven on one GPU with 3 hops."""
+    n = (24 << 20) + 333
+    src = torch.randint(0, 256, (n,), dtype=torch.uint8, device="cuda:0")
+    dst = torch.zeros_like(src)
+    s = torch.cuda.current_stream(0)
+    tube._relay([(0, 0), (0, 0), (0, 0)], src.data_ptr(), dst.data_ptr(), n, s)
+    assert len(tube._keepalive) >= 1
+    digest = dst.to(torch.int64).sum()          # ordered after the last hop on the consumer stream
+    torch.cuda.synchronize()
+    assert torch.equal(dst, src)
+    assert int(digest) == int(src.to(torch.int64).sum())
+    tube.maintain()
+    assert not tube._keepalive

@@ -1,3 +1,3 @@
 mkdir -p gpurun_out
-timeout 600 python -m pytest tests -q -m gpu --timeout 120 > gpurun_out/pytest_g.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_g.log
-timeout -s USR1 -k 30 600 python bench.py > gpurun_out/bench_g.json 2> gpurun_out/bench_g.err; echo "bench rc=$?" >> gpurun_out/bench_g.err
+timeout -k 10 400 python tools/diag_cfg5.py > gpurun_out/diag_cfg5.txt 2>&1
+timeout -k 10 400 python tools/diag_cfg5.py > gpurun_out/diag_cfg5b.txt 2>&1
