@@ -310,6 +310,17 @@ int ft_copy_hint(void* dst, const void* src, uint64_t bytes, int device, void* s
  * (wrap-around compare). */
 int ft_signal(uint32_t* flag, uint32_t value, int device, void* stream);
 int ft_wait(const uint32_t* flag, uint32_t value, int device, void* stream);
+/* raw CUDA events for stream ordering on the request path (no torch objects) */
+int ft_event_create(int device, void** ev);
+int ft_event_destroy(void* ev);
+int ft_event_record(void* ev, void* stream);
+int ft_event_query(void* ev, int* done);
+int ft_event_synchronize(void* ev);
+int ft_stream_wait_events(void* stream, void* const* evs, int n);
+/* a request-path copy in one call: `stream` waits on `waits` (NULL entries skipped),
+ * TMA-bulk copy with L2 `hints` (as ft_copy_hint), then records `done` (may be NULL) */
+int ft_copy_ordered(void* dst, const void* src, uint64_t bytes, int device, void* stream, uint32_t hints,
+                    void* const* waits, int nwaits, void* done);
 /* occupy `stream` for `ns` nanoseconds of wall time (global timer, clock independent):
  * the synthetic gFunc compute of the workflow runtime (harness compute_latency_ms) */
 int ft_spin_ns(uint64_t ns, int device, void* stream);

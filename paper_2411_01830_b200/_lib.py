@@ -234,6 +234,13 @@ _SIGS = {
     "ft_copy_hint": (None, [vp, vp, u64, C.c_int, vp, C.c_uint32]),
     "ft_signal": (None, [vp, C.c_uint32, C.c_int, vp]),
     "ft_wait": (None, [vp, C.c_uint32, C.c_int, vp]),
+    "ft_event_create": (None, [C.c_int, P(vp)]),
+    "ft_event_destroy": (None, [vp]),
+    "ft_event_record": (None, [vp, vp]),
+    "ft_event_query": (None, [vp, P(C.c_int)]),
+    "ft_event_synchronize": (None, [vp]),
+    "ft_stream_wait_events": (None, [vp, P(vp), C.c_int]),
+    "ft_copy_ordered": (None, [vp, vp, u64, C.c_int, vp, C.c_uint32, P(vp), C.c_int, vp]),
     "ft_spin_ns": (None, [u64, C.c_int, vp]),
     "ft_fingerprint": (None, [vp, u64, vp, C.c_int, vp]),
     "ft_fingerprint_host": (None, [vp, u64, P(u64)]),

@@ -836,6 +836,57 @@ int ft_wait(const uint32_t* flag, uint32_t value, int device, void* stream) {
   return e == cudaSuccess ? FT_OK : cuda_fail(e, "ft_wait");
 }
 
+// ---- raw events (the request path's ordering, without torch.cuda.Event objects)
+int ft_event_create(int device, void** ev) {
+  int cur = 0;
+  CU_RT(cudaGetDevice(&cur));
+  if (cur != device) CU_RT(cudaSetDevice(device));
+  cudaEvent_t e = nullptr;
+  cudaError_t r = cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+  if (cur != device) cudaSetDevice(cur);
+  if (r != cudaSuccess) return cuda_fail(r, "ft_event_create");
+  *ev = e;
+  return FT_OK;
+}
+int ft_event_destroy(void* ev) {
+  CU_RT(cudaEventDestroy((cudaEvent_t)ev));
+  return FT_OK;
+}
+int ft_event_record(void* ev, void* stream) {
+  CU_RT(cudaEventRecord((cudaEvent_t)ev, (cudaStream_t)stream));
+  return FT_OK;
+}
+int ft_event_query(void* ev, int* done) {
+  cudaError_t r = cudaEventQuery((cudaEvent_t)ev);
+  if (r == cudaErrorNotReady) {
+    *done = 0;
+    return FT_OK;
+  }
+  if (r != cudaSuccess) return cuda_fail(r, "ft_event_query");
+  *done = 1;
+  return FT_OK;
+}
+int ft_event_synchronize(void* ev) {
+  CU_RT(cudaEventSynchronize((cudaEvent_t)ev));
+  return FT_OK;
+}
+int ft_stream_wait_events(void* stream, void* const* evs, int n) {
+  for (int i = 0; i < n; ++i)
+    if (evs[i]) CU_RT(cudaStreamWaitEvent((cudaStream_t)stream, (cudaEvent_t)evs[i], 0));
+  return FT_OK;
+}
+// one call for a request-path copy: wait on `waits`, TMA-bulk copy with L2 hints,
+// record `done` (any of them may be absent)
+int ft_copy_ordered(void* dst, const void* src, uint64_t bytes, int device, void* stream, uint32_t hints,
+                    void* const* waits, int nwaits, void* done) {
+  int rc = ft_stream_wait_events(stream, waits, nwaits);
+  if (rc != FT_OK) return rc;
+  rc = copy_impl(dst, src, bytes, device, (cudaStream_t)stream, 1, 0, hints & 15u);
+  if (rc != FT_OK) return rc;
+  if (done) CU_RT(cudaEventRecord((cudaEvent_t)done, (cudaStream_t)stream));
+  return FT_OK;
+}
+
 int ft_spin_ns(uint64_t ns, int device, void* stream) {
   int cur = 0;
   CU_RT(cudaGetDevice(&cur));

@@ -532,11 +532,62 @@ struct ft_pacer {
     done_cv.notify_all();
   }
 
+  // One pacing step of a managed stage at time t: drop its landed batches (and
+  // sample the link), then issue its next batch if the rate schedule (with
+  // lookahead) and the in-flight cap allow. Returns when to look again.
+  double step(Stage& st, double t) {
+    const double batch = (double)batch_chunks * (double)chunk;
+    while (!st.inflight.empty()) {  // drop landed batches (non-blocking)
+      Batch& b = st.inflight.front();
+      bool ok = true;
+      for (auto& e : b.ev)
+        if (cudaEventQuery(e.e) != cudaSuccess) ok = false;
+      for (auto& tm : b.timing)
+        if (cudaEventQuery(tm.t1) != cudaSuccess) ok = false;
+      if (!ok) break;
+      for (auto& tm : b.timing) {
+        float ms = 0.f;
+        bool overlapped = tm.contended ||
+                          (last_issue_ticket[tm.dev] != st.ticket && last_issue_t[tm.dev] > tm.issued);
+        if (!overlapped && cudaEventElapsedTime(&ms, tm.t0, tm.t1) == cudaSuccess && ms > 0.f)
+          sample(tm.dev, (double)tm.bytes / ((double)ms * 1e6), t);
+      }
+      release_batch(b);
+      st.inflight.pop_front();
+      note(st, "done", (double)st.inflight.size());
+    }
+    const auto* m = arb.stages.find(st.key);
+    if (!m || !m->started || m->rate <= 0) return INFINITY;  // waiting: a boundary / finish / start wakes it
+    double dur = batch / (m->rate * 1e6);                     // ms per batch at the stage rate
+    if (std::isnan(st.next_t) || m->rate != st.last_rate) {
+      // (re)anchor on rate changes: a stage paced slowly must not keep its far-out slot
+      st.next_t = std::isnan(st.next_t) ? t : std::min(st.next_t, t + dur);
+      st.last_rate = m->rate;
+      note(st, "rate", m->rate);
+    }
+    if (t < st.next_t - kLookahead * dur) return st.next_t - kLookahead * dur;
+    bool full = st.pinned ? (int)st.inflight.size() >= kInflightBatches : st.jobs >= 2 * batch_chunks;
+    if (full) {
+      if (!st.was_full) note(st, "full", (double)st.inflight.size());
+      st.was_full = true;
+      return t + 0.02;
+    }
+    st.was_full = false;
+    try {
+      issue_batch(st);
+    } catch (const CudaFail& f) {
+      fail(st, f.msg);
+    } catch (const ft::Error& e) {
+      fail(st, e.what());
+    }
+    st.next_t += dur;
+    return t;  // re-evaluate at once (lookahead may allow another batch)
+  }
+
   // ------------------------------------------------------------ pacer thread
   void run() {
     prctl(PR_SET_TIMERSLACK, 1000UL, 0, 0, 0);  // 1 us timer slack: batch slots are ~0.2 ms
     std::unique_lock<std::mutex> lk(mu);
-    const double batch = (double)batch_chunks * (double)chunk;
     for (;;) {
       bool draining = poll_landing();
       retire_landed();
@@ -553,55 +604,7 @@ struct ft_pacer {
           continue;
         }
         if (!st.managed || st.issued) continue;
-        while (!st.inflight.empty()) {  // drop landed batches (non-blocking)
-          Batch& b = st.inflight.front();
-          bool ok = true;
-          for (auto& e : b.ev)
-            if (cudaEventQuery(e.e) != cudaSuccess) ok = false;
-          for (auto& tm : b.timing)
-            if (cudaEventQuery(tm.t1) != cudaSuccess) ok = false;
-          if (!ok) break;
-          for (auto& tm : b.timing) {
-            float ms = 0.f;
-            bool overlapped = tm.contended ||
-                              (last_issue_ticket[tm.dev] != st.ticket && last_issue_t[tm.dev] > tm.issued);
-            if (!overlapped && cudaEventElapsedTime(&ms, tm.t0, tm.t1) == cudaSuccess && ms > 0.f)
-              sample(tm.dev, (double)tm.bytes / ((double)ms * 1e6), t);
-          }
-          release_batch(b);
-          st.inflight.pop_front();
-          note(st, "done", (double)st.inflight.size());
-        }
-        const auto* m = arb.stages.find(st.key);
-        if (!m || !m->started || m->rate <= 0) continue;  // waiting: a boundary / finish / start wakes it
-        double dur = batch / (m->rate * 1e6);             // ms per batch at the stage rate
-        if (std::isnan(st.next_t) || m->rate != st.last_rate) {
-          // (re)anchor on rate changes: a stage paced slowly must not keep its far-out slot
-          st.next_t = std::isnan(st.next_t) ? t : std::min(st.next_t, t + dur);
-          st.last_rate = m->rate;
-          note(st, "rate", m->rate);
-        }
-        if (t < st.next_t - kLookahead * dur) {
-          wake = std::min(wake, st.next_t - kLookahead * dur);
-          continue;
-        }
-        bool full = st.pinned ? (int)st.inflight.size() >= kInflightBatches : st.jobs >= 2 * batch_chunks;
-        if (full) {
-          if (!st.was_full) note(st, "full", (double)st.inflight.size());
-          st.was_full = true;
-          wake = std::min(wake, t + 0.02);
-          continue;
-        }
-        st.was_full = false;
-        try {
-          issue_batch(st);
-        } catch (const CudaFail& f) {
-          fail(st, f.msg);
-        } catch (const ft::Error& e) {
-          fail(st, e.what());
-        }
-        st.next_t += dur;
-        wake = t;  // re-evaluate at once (lookahead may allow another batch)
+        wake = std::min(wake, step(st, t));
       }
       double armed = next_armed();
       if (!std::isnan(armed)) wake = std::min(wake, armed);
@@ -833,6 +836,10 @@ int ft_pacer_submit(ft_pacer* p, const char* key, int managed, double slo_ms, do
       if (bytes == 0) {
         st.issued = true;
         p->seal(st);
+      } else if (st.pinned) {
+        // the first batches go out from the submitting thread: no pacer wake-up latency
+        for (int i = 0; i < kInflightBatches && !st.issued && p->step(st, t) <= t; ++i) {
+        }
       }
     } else {
       for (int i = 0; i < k; ++i) {

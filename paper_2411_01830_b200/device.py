@@ -41,8 +41,69 @@ def require_cuda():
     return n.value
 
 
-def stream_ptr(stream: torch.cuda.Stream | None) -> int:
-    return 0 if stream is None else stream.cuda_stream
+def stream_ptr(stream) -> int:
+    """cudaStream_t of a torch stream, a raw pointer (int) or None (legacy default)."""
+    if stream is None:
+        return 0
+    return stream if isinstance(stream, int) else stream.cuda_stream
+
+
+def current_stream(device: int) -> int:
+    """Raw pointer of the current stream on ``device`` (no torch.cuda.Stream object)."""
+    return torch._C._cuda_getCurrentRawStream(device)
+
+
+class Ev:
+    """A raw CUDA event (libfaastube ``ft_event_*``): request-path stream
+    ordering without torch.cuda.Event objects. Destroyed with the object
+    (CUDA defers the destruction of an event still pending)."""
+
+    __slots__ = ("h", "device", "__weakref__")
+
+    def __init__(self, device: int):
+        h = C.c_void_p()
+        LIB.ft_event_create(int(device), C.byref(h))
+        self.h, self.device = h.value, device
+
+    def record(self, stream):
+        LIB.ft_event_record(C.c_void_p(self.h), C.c_void_p(stream_ptr(stream)))
+        return self
+
+    def wait(self, stream):
+        """``stream`` waits for the work this event captured."""
+        LIB.ft_stream_wait_events(C.c_void_p(stream_ptr(stream)), (C.c_void_p * 1)(self.h), 1)
+
+    def query(self) -> bool:
+        d = C.c_int()
+        LIB.ft_event_query(C.c_void_p(self.h), C.byref(d))
+        return bool(d.value)
+
+    def synchronize(self):
+        LIB.ft_event_synchronize(C.c_void_p(self.h))
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h:
+            self.h = None
+            try:
+                LIB.raw("ft_event_destroy")(C.c_void_p(h))
+            except Exception:  # noqa: BLE001 - interpreter teardown
+                pass
+
+
+def wait_events(stream, events):
+    evs = [e.h for e in events if e is not None]
+    if evs:
+        LIB.ft_stream_wait_events(C.c_void_p(stream_ptr(stream)), (C.c_void_p * len(evs))(*evs), len(evs))
+
+
+def copy_ordered(dst_ptr: int, src_ptr: int, nbytes: int, device: int, stream, hints: int = 0, waits=(),
+                 done: "Ev | None" = None):
+    """One call: ``stream`` waits on ``waits``, TMA-bulk copy with L2 ``hints``, record ``done``."""
+    evs = [e.h for e in waits if e is not None]
+    LIB.ft_copy_ordered(C.c_void_p(dst_ptr), C.c_void_p(src_ptr), int(nbytes), int(device),
+                        C.c_void_p(stream_ptr(stream)), int(hints), (C.c_void_p * max(1, len(evs)))(*evs),
+                        len(evs), C.c_void_p(done.h if done is not None else None))
 
 
 class _Mem:
@@ -137,10 +198,13 @@ class PoolBlock:
             policy_block, vmm_id, ptr, nbytes, device)
         self.fences = fences
 
-    def wait_fences(self, stream: torch.cuda.Stream):
-        for ev in self.fences:
-            stream.wait_event(ev)
+    def wait_fences(self, stream):
+        wait_events(stream, self.fences)
         self.fences = ()
+
+    def take_fences(self) -> tuple:
+        f, self.fences = self.fences, ()
+        return f
 
 
 class DevicePool:

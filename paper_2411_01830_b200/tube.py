@@ -205,8 +205,10 @@ class FaaSTube:
                 if p.released_bytes:
                     p.reclaim()
 
-    def _stream(self, g):
-        return torch.cuda.current_stream(g)
+    @staticmethod
+    def _stream(g) -> int:
+        """Raw pointer of the caller's current stream on GPU ``g``."""
+        return dev.current_stream(g)
 
     @staticmethod
     def _stripes(nbytes, shares):
@@ -285,25 +287,20 @@ class FaaSTube:
                                 and not o.retired)
                 if blk is not None and blk.ptr == t.data_ptr():
                     obj.block = blk                      # zero-copy store of a pool-backed output
-                    ev = torch.cuda.Event()
-                    ev.record(self._stream(g))
-                    obj.ready = ev
+                    obj.ready = dev.Ev(g).record(self._stream(g))
                 else:
                     blk = pre_blk                        # datastore.py:130-144 (allocated above)
                     obj.block = blk
                     # snapshot on the producer's stream: ordered after the kernels that
                     # wrote the output AND before any later kernel that overwrites it
-                    s = self._stream(g)
-                    blk.wait_fences(s)                   # the block's previous users are done
-                    if nbytes <= _L2_KEEP:
-                        # keep the fresh block L2-resident for the consumer's fetch
-                        dev.copy_hint(blk.ptr, t.data_ptr(), nbytes, g, s, dev.L2_EVICT_FIRST, dev.L2_EVICT_LAST)
-                    else:
-                        dev.copy(blk.ptr, t.data_ptr(), nbytes, g, s)
-                    t.record_stream(s)
-                    ev = torch.cuda.Event()
-                    ev.record(s)
-                    obj.ready = ev
+                    so = torch.cuda.current_stream(g)
+                    # keep a fresh block that fits L2 resident for the consumer's fetch
+                    hints = dev.L2_EVICT_FIRST | (dev.L2_EVICT_LAST << 2) if nbytes <= _L2_KEEP else 0
+                    obj.ready = dev.Ev(g)
+                    # waits for the block's previous users, copies, records `ready`: one call
+                    dev.copy_ordered(blk.ptr, t.data_ptr(), nbytes, g, so.cuda_stream, hints, blk.take_fences(),
+                                     obj.ready)
+                    t.record_stream(so)
                     self.stats["bytes_local"] += nbytes
                 pool.record(producer, now, nbytes, live_here + 1)   # datastore.py:51-62
                 self._push_shrink(g, producer, now)
@@ -315,11 +312,10 @@ class FaaSTube:
                 g = t.device.index
                 host = pre_host
                 s = self._ce[g][0]
-                s.wait_stream(self._stream(g))
+                dev.Ev(g).record(self._stream(g)).wait(s)    # the producer's output is written
                 dev.pcie_copy(host.data_ptr(), t.data_ptr(), nbytes, False, g, s)
                 t.record_stream(s)
-                ev = torch.cuda.Event()
-                ev.record(s)
+                ev = dev.Ev(g).record(s)
                 obj.host, obj.ready = host, ev
                 if response:                               # already in host memory
                     obj.response_host, obj.response_event = host, ev
@@ -380,10 +376,9 @@ class FaaSTube:
         g = o.gpu
         host = self._pinned(o.nbytes)
         ce = self._ce[g][1]
-        ce.wait_event(o.ready)
+        o.ready.wait(ce)
         dev.pcie_copy(host.data_ptr(), o.block.ptr, o.nbytes, False, g, ce)
-        ev = torch.cuda.Event()
-        ev.record(ce)
+        ev = dev.Ev(g).record(ce)
         blk, o.block = o.block, None
         self.pools[g].free(blk, [ev] + o.readers)            # later writers of the block wait for the D2H
         o.readers = []
@@ -409,11 +404,10 @@ class FaaSTube:
             blk = self.pools[g].allocate(o.nbytes)
             ce = self._ce[g][0]
             if o.ready is not None:
-                ce.wait_event(o.ready)
+                o.ready.wait(ce)
             blk.wait_fences(ce)
             dev.pcie_copy(blk.ptr, o.host.data_ptr(), o.nbytes, True, g, ce)
-            ev = torch.cuda.Event()
-            ev.record(ce)
+            ev = dev.Ev(g).record(ce)
             o.block, o.ready, o.gpu, o.host = blk, ev, g, None
             self.index.relocate(o.did, self._loc(g))
             self.stats["reload_bytes"] += o.nbytes
@@ -520,10 +514,9 @@ class FaaSTube:
         g = obj.gpu
         host = host if host is not None else self._pinned(obj.nbytes)
         s = self._ce[g][1]
-        s.wait_event(obj.ready)
+        obj.ready.wait(s)
         dev.pcie_copy(host.data_ptr(), obj.block.ptr, obj.nbytes, False, g, s)
-        ev = torch.cuda.Event()
-        ev.record(s)
+        ev = dev.Ev(g).record(s)
         obj.response_host, obj.response_event = host, ev
         obj.readers.append(ev)
         self.stats["bytes_d2h"] += obj.nbytes
@@ -546,8 +539,7 @@ class FaaSTube:
         if obj.block is not None and obj.pins == 0 and obj.retired:
             blk, obj.block = obj.block, None
             # later writers of this block must order after our readers
-            ev = torch.cuda.Event()
-            ev.record(self._stream(blk.device))
+            ev = dev.Ev(blk.device).record(self._stream(blk.device))
             fences = [ev] + obj.readers + ([obj.ready] if obj.ready is not None else [])
             obj.readers = []
             self.pools[blk.device].free(blk, fences)
@@ -576,12 +568,13 @@ class FaaSTube:
                 out.view(-1).view(torch.uint8).copy_(obj.host)
                 return out
             s = self._stream(dst.gpu)
-            s.wait_event(obj.ready)
             if out is None:
+                obj.ready.wait(s)
                 return self._view(obj)
             last = obj.remaining <= 1
-            dev.copy_hint(out.data_ptr(), obj.block.ptr, obj.nbytes, dst.gpu, s,
-                          dev.L2_EVICT_FIRST if last else dev.L2_NORMAL, dev.L2_NORMAL)
+            # wait for the stored bytes and copy into the caller's input: one call
+            dev.copy_ordered(out.data_ptr(), obj.block.ptr, obj.nbytes, dst.gpu, s,
+                             dev.L2_EVICT_FIRST if last else dev.L2_NORMAL, (obj.ready,))
             self.stats["bytes_local"] += obj.nbytes
             return out
         if m == "inter_gpu":
@@ -599,21 +592,20 @@ class FaaSTube:
     def _inter_gpu(self, obj, plan, src, dst, out):
         res = self._out(obj, dst.gpu, out)
         s = self._stream(dst.gpu)
-        s.wait_event(obj.ready)
+        obj.ready.wait(s)
         if len(plan.stages) == 2:
             # host-oriented baseline: D2H to host, then H2D (dataplane.py:265-272)
             host = self._pinned(obj.nbytes)
             ce = self._ce[src.gpu][0]
-            ce.wait_event(obj.ready)
+            obj.ready.wait(ce)
             dev.pcie_copy(host.data_ptr(), obj.block.ptr if obj.block else obj.host.data_ptr(), obj.nbytes,
                           False, src.gpu, ce)
-            ev = torch.cuda.Event()
-            ev.record(ce)
+            ev = dev.Ev(src.gpu).record(ce)
             if obj.block is not None:
                 obj.readers.append(ev)
-            s.wait_event(ev)
+            ev.wait(s)
             dev.pcie_copy(res.data_ptr(), host.data_ptr(), obj.nbytes, True, dst.gpu, s)
-            host.record_stream(s) if hasattr(host, "record_stream") else None
+            host.record_stream(torch.cuda.current_stream(dst.gpu))
             self.stats["bytes_d2h"] += obj.nbytes
             self.stats["bytes_h2d"] += obj.nbytes
             return res
@@ -629,8 +621,7 @@ class FaaSTube:
             else:
                 self._relay(hops, obj.block.ptr + off, res.data_ptr() + off, n, s)
             self.stats["bytes_nvlink"] += n
-        ev = torch.cuda.Event()
-        ev.record(s)
+        ev = dev.Ev(dst.gpu).record(s)
         if plan.claimed_func:
             self._pending_release.append((ev, plan))
         self._hold_until(obj, ev)
@@ -642,13 +633,12 @@ class FaaSTube:
         by its receiving GPU on a stream of that GPU, chained to the previous
         hop by an event; the last hop runs on the consumer's stream. Buffers
         stay referenced until the last hop has completed."""
-        ev = torch.cuda.Event()
-        ev.record(s)                                  # source ready / destination free
+        ev = dev.Ev(hops[-1][1]).record(s)            # source ready / destination free
         cur, keep = src_ptr, []
         for i, (u, v) in enumerate(hops):
             last = i == len(hops) - 1
-            st = s if last else self._pair(v)[1]
-            st.wait_event(ev)
+            st = s if last else self._pair(v)[1].cuda_stream
+            ev.wait(st)
             if last:
                 out = dst_ptr
             else:
@@ -656,8 +646,7 @@ class FaaSTube:
                 keep.append(buf)
                 out = buf.data_ptr()
             dev.copy(out, cur, n, v, st, dev.ENGINE_VEC)
-            ev = torch.cuda.Event()
-            ev.record(st)
+            ev = dev.Ev(v).record(st)
             cur = out
         if keep:
             self._keepalive.append((ev, keep))
@@ -685,10 +674,10 @@ class FaaSTube:
         ranges = self._stripes(obj.nbytes, [b.bytes_share for b in br])
         s = self._stream(dst.gpu)
         if obj.ready is not None:
-            s.wait_event(obj.ready)
+            obj.ready.wait(s)
         # CE streams keyed by the consumer's stream: a tenant's stages stay in its own
         # FIFO, other tenants' stages (other streams) do not queue behind them
-        slot = (s.cuda_stream >> 4) * 0x9E3779B1 >> 16
+        slot = (s >> 4) * 0x9E3779B1 >> 16
         routes = []
         for b, (off, n) in zip(br, ranges):
             sg = _staging_gpu(b.links, dst.gpu)
@@ -702,7 +691,7 @@ class FaaSTube:
                  slo_ms if slo_ms else 1e9,                       # engine.py:546-547
                  infer_ms if infer_ms is not None else 0.0,
                  min(min(b.hop_caps) for b in br), res.data_ptr(), dst.gpu, host.data_ptr(), obj.nbytes,
-                 host.is_pinned(), routes, s.cuda_stream)
+                 host.is_pinned(), routes, s)
         self.stats["bytes_h2d"] += obj.nbytes
         if managed:
             self.stats["managed_stages"] = self.stats.get("managed_stages", 0) + 1
@@ -724,11 +713,9 @@ class FaaSTube:
         res = out if out is not None else self._pinned(obj.nbytes).view(obj.dtype).view(obj.shape)
         g = obj.gpu
         ce = self._ce[g][0]
-        ce.wait_event(obj.ready)
+        obj.ready.wait(ce)
         dev.pcie_copy(res.data_ptr(), obj.block.ptr, obj.nbytes, False, g, ce)
-        ev = torch.cuda.Event()
-        ev.record(ce)
-        ev.synchronize()
+        dev.Ev(g).record(ce).synchronize()
         self.stats["bytes_d2h"] += obj.nbytes
         return res
 

@@ -1,3 +1,3 @@
 mkdir -p gpurun_out
-timeout -k 10 400 python tools/diag_cfg5.py > gpurun_out/diag_cfg5.txt 2>&1
-timeout -k 10 400 python tools/diag_cfg5.py > gpurun_out/diag_cfg5b.txt 2>&1
+timeout 200 python tools/prof_ffi.py > gpurun_out/prof_ffi.txt 2>&1
+timeout 600 python -m pytest tests -q -m gpu --timeout 120 -x > gpurun_out/pytest_m.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_m.log
