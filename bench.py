@@ -262,6 +262,7 @@ def run_ours(args):
     gpu_launches = int(copies)                       # one k_copy_bulk per store + one per fetch
     if pair is not None:                             # wait+copy+signal on each side
         gpu_launches = 6 * args.steps
+        pair.check()
     assert torch.equal(inp.view(torch.uint8), x.view(torch.uint8)), "delivered bytes differ"
 
     # ---- dominant kernel: k_copy_bulk on the same buffers, CUDA events on its stream
@@ -413,6 +414,53 @@ def run_extras(tube, g, dev, torch):
     out["h2g"] = {"workload": "config2 at k=1 (one PCIe link): 1 GiB pinned -> GPU via FaaSTube.fetch",
                   "value": round(h2g_gbps, 3), "unit": "GB/s", "peak": round(ce_peak, 3),
                   "peak_source": "live: best-of-3 cudaMemcpyAsync 1 GiB pinned H2D", "frac": round(h2g_gbps / ce_peak, 4)}
+    # config 2's striping machinery on one GPU: the same 1 GiB split over a direct route and a
+    # staged route (CE into the staging chunk ring + forward kernel, here staging GPU == target,
+    # so both routes share one PCIe link): the ring/forward pipeline must not cost link rate
+    strm = [(torch.cuda.Stream(g), torch.cuda.Stream(g)) for _ in range(2)]
+    half = n // 2
+    routes = [(g, 0, 0, half, strm[0][0].cuda_stream, strm[0][1].cuda_stream),
+              (g, 1, half, n - half, strm[1][0].cuda_stream, strm[1][1].cuda_stream)]
+    host[::4093] = torch.arange(host[::4093].numel(), dtype=torch.int64).to(torch.uint8)  # not constant
+    dst.zero_()
+    st_ms = []
+    for i in range(4):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(s)
+        tube.pacer.submit("", False, 1e9, 0.0, 1e9, dst.data_ptr(), g, host.data_ptr(), n, True, routes, s.cuda_stream)
+        b.record(s)
+        b.synchronize()
+        if i:
+            st_ms.append(a.elapsed_time(b))
+    for o in (0, half - 8192, half, n - 8192):
+        assert torch.equal(dst[o:o + 8192].cpu(), host[o:o + 8192]), "striped delivery differs"
+    st_gbps = n / (statistics.mean(st_ms) * 1e-3) / 1e9
+    out["h2g_striped_machinery"] = {
+        "workload": "config2 machinery at k=2 on one GPU: 1 GiB = direct route + staged route (CE -> 4-slot "
+                    "chunk ring -> forward kernel), both on the one PCIe link",
+        "value": round(st_gbps, 3), "unit": "GB/s", "peak": round(ce_peak, 3), "frac": round(st_gbps / ce_peak, 4)}
+    # the NVLink mover (K1, vector engine) on local HBM: it must feed far more than a
+    # 900 GB/s/direction link, so cross-GPU passes are link-bound by construction
+    vec = []
+    for lg in (20, 24, 26, 30):
+        m = 1 << lg
+        xa = torch.empty(m, dtype=torch.uint8, device=f"cuda:{g}")
+        xb = torch.empty_like(xa)
+        ts = []
+        for i in range(6):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(s)
+            dev.copy(xb.data_ptr(), xa.data_ptr(), m, g, s, dev.ENGINE_VEC)
+            b.record(s)
+            b.synchronize()
+            if i:
+                ts.append(a.elapsed_time(b))
+        ms = statistics.median(ts)
+        vec.append({"bytes": m, "kernel_ms": round(ms, 5), "payload_gbps": round(m / (ms * 1e-3) / 1e9, 1)})
+        del xa, xb
+    out["nvlink_mover_local"] = {"kernel": "k_copy_vec (peer-safe 128-bit ld/st, the K1 NVLink engine)",
+                                 "note": "local HBM copy on one GPU; NVLink peak 900 GB/s/dir nominal, 770 measured",
+                                 "sweep": vec}
     # config 3 at 1 GPU: zero-copy handoff latency and copy-into-input bandwidth, 4 KiB .. 1 GiB.
     # The reference's 1 GB per-GPU store cap (datastore.py:19, sized for 16-32 GB GPUs)
     # would migrate the 1 GiB point to host memory; a B200 store holds it (180 GB HBM).

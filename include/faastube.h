@@ -309,7 +309,10 @@ int ft_copy_hint(void* dst, const void* src, uint64_t bytes, int device, void* s
  * after all prior work on `stream`; ft_wait parks `stream` until *flag >= value
  * (wrap-around compare). */
 int ft_signal(uint32_t* flag, uint32_t value, int device, void* stream);
-int ft_wait(const uint32_t* flag, uint32_t value, int device, void* stream);
+int ft_wait(const uint32_t* flag, uint32_t value, int device, void* stream);  /* gives up after 30 s */
+/* as ft_wait, giving up after timeout_ns; then writes the awaited value (or 1) to *err if err != NULL */
+int ft_wait_timeout(const uint32_t* flag, uint32_t value, uint64_t timeout_ns, uint32_t* err, int device,
+                    void* stream);
 /* raw CUDA events for stream ordering on the request path (no torch objects) */
 int ft_event_create(int device, void** ev);
 int ft_event_destroy(void* ev);

@@ -234,6 +234,7 @@ _SIGS = {
     "ft_copy_hint": (None, [vp, vp, u64, C.c_int, vp, C.c_uint32]),
     "ft_signal": (None, [vp, C.c_uint32, C.c_int, vp]),
     "ft_wait": (None, [vp, C.c_uint32, C.c_int, vp]),
+    "ft_wait_timeout": (None, [vp, C.c_uint32, u64, vp, C.c_int, vp]),
     "ft_event_create": (None, [C.c_int, P(vp)]),
     "ft_event_destroy": (None, [vp]),
     "ft_event_record": (None, [vp, vp]),

@@ -333,13 +333,20 @@ __global__ void k_signal(unsigned int* flag, unsigned int value) {
   __threadfence_system();
   asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(flag), "r"(value) : "memory");
 }
-__global__ void k_wait(const unsigned int* flag, unsigned int value) {
+// Bounded doorbell wait: a peer that never rings (crashed process, mismatched
+// setup) must not park the stream forever — after timeout_ns the wait gives up
+// and, when err is given, records the value it was waiting for there.
+__global__ void k_wait(const unsigned int* flag, unsigned int value, uint64_t timeout_ns, unsigned int* err) {
   unsigned int v;
+  uint64_t t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
   do {
     asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
-    if ((int)(v - value) >= 0) break;
+    if ((int)(v - value) >= 0) return;
     __nanosleep(200);
-  } while (true);
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  } while (t - t0 < timeout_ns);
+  if (err) *err = value ? value : 1u;
 }
 
 // Fixed-duration GPU occupancy (the runtime's synthetic gFunc compute,
@@ -827,10 +834,14 @@ int ft_signal(uint32_t* flag, uint32_t value, int device, void* stream) {
 }
 
 int ft_wait(const uint32_t* flag, uint32_t value, int device, void* stream) {
+  return ft_wait_timeout(flag, value, 30000000000ull, nullptr, device, stream);
+}
+int ft_wait_timeout(const uint32_t* flag, uint32_t value, uint64_t timeout_ns, uint32_t* err, int device,
+                    void* stream) {
   int cur = 0;
   CU_RT(cudaGetDevice(&cur));
   if (cur != device) CU_RT(cudaSetDevice(device));
-  k_wait<<<1, 1, 0, (cudaStream_t)stream>>>(flag, value);
+  k_wait<<<1, 1, 0, (cudaStream_t)stream>>>(flag, value, timeout_ns, err);
   cudaError_t e = cudaGetLastError();
   if (cur != device) cudaSetDevice(cur);
   return e == cudaSuccess ? FT_OK : cuda_fail(e, "ft_wait");

@@ -11,6 +11,9 @@ memory instead of host round trips (``ft_signal`` / ``ft_wait``):
 RDY_c lives on GPU c (written remotely by the producer), ACK_r on GPU r
 (written remotely by the consumer), so every wait spins on local memory.
 Each rank is a producer (to r+1) and a consumer (of r-1) on separate streams.
+Waits are bounded (``ft_wait_timeout``): a peer that never rings cannot park a
+stream forever; the expired wait leaves its value in the error word that
+``check()`` reports.
 """
 
 from __future__ import annotations
@@ -24,6 +27,7 @@ from . import device as dev
 from .channel import Channel
 
 FLAG_BYTES = 4096
+WAIT_TIMEOUT_NS = 20 * 10**9
 
 
 class CrossPair:
@@ -68,6 +72,19 @@ class CrossPair:
         return self.next_flags.ptr          # RDY of rank r+1 (peer)
     def _ack_prev(self):
         return self.peer_flags.ptr + 4      # ACK of rank r-1 (peer)
+    def _err(self):
+        return self.flags.ptr + 8           # awaited value of an expired wait (0: none)
+
+    def _wait(self, flag, value, stream):
+        dev.LIB.ft_wait_timeout(C.c_void_p(flag), value & 0xFFFFFFFF, WAIT_TIMEOUT_NS, C.c_void_p(self._err()),
+                                self.g, C.c_void_p(stream.cuda_stream))
+
+    def check(self):
+        """Raise if any doorbell wait expired (a peer stopped ringing)."""
+        torch.cuda.synchronize(self.g)
+        err = int(dev.as_tensor(self.flags.ptr + 8, 4, self.g, torch.int32)[0])
+        if err:
+            raise RuntimeError(f"rank {self.rank}: doorbell wait for step {err} expired")
 
     def produce(self, x: torch.Tensor):
         """store step k: wait until the consumer released B_r, snapshot x, ring RDY."""
@@ -75,7 +92,7 @@ class CrossPair:
         k = self.step
         s = self.prod_stream
         s.wait_stream(torch.cuda.current_stream(self.g))
-        dev.LIB.ft_wait(C.c_void_p(self._ack_local()), (k - 1) & 0xFFFFFFFF, self.g, C.c_void_p(s.cuda_stream))
+        self._wait(self._ack_local(), k - 1, s)
         dev.copy(self.payload.ptr, x.data_ptr(), self.n, self.g, s, dev.ENGINE_BULK)
         dev.LIB.ft_signal(C.c_void_p(self._rdy_next()), k & 0xFFFFFFFF, self.g, C.c_void_p(s.cuda_stream))
 
@@ -83,7 +100,7 @@ class CrossPair:
         """fetch step k: wait for RDY, pull the peer's block over NVLink, ACK it."""
         k = self.step
         s = self.cons_stream
-        dev.LIB.ft_wait(C.c_void_p(self._rdy_local()), k & 0xFFFFFFFF, self.g, C.c_void_p(s.cuda_stream))
+        self._wait(self._rdy_local(), k, s)
         dev.copy(out.data_ptr(), self.peer_payload.ptr, self.n, self.g, s, dev.ENGINE_VEC)
         dev.LIB.ft_signal(C.c_void_p(self._ack_prev()), k & 0xFFFFFFFF, self.g, C.c_void_p(s.cuda_stream))
         torch.cuda.current_stream(self.g).wait_stream(s)

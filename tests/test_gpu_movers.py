@@ -137,3 +137,26 @@ def test_spin_ns_is_wall_time(dev):
         torch.cuda.synchronize()
         got = (time.perf_counter() - t0) * 1e3
         assert ms <= got < ms + 1.5, (ms, got)
+
+
+def test_doorbell_wait_is_bounded(dev):
+    """A doorbell that never rings: the wait gives up after its timeout and
+    leaves the awaited value in the error word (no stream parked forever)."""
+    import time
+    from paper_2411_01830_b200._lib import LIB
+    words = torch.zeros(4, dtype=torch.int32, device="cuda:0")
+    s = torch.cuda.current_stream(0)
+    t0 = time.perf_counter()
+    LIB.ft_wait_timeout(C.c_void_p(words.data_ptr()), 7, 50_000_000, C.c_void_p(words.data_ptr() + 8), 0,
+                        C.c_void_p(s.cuda_stream))
+    torch.cuda.synchronize()
+    ms = (time.perf_counter() - t0) * 1e3
+    assert 45.0 <= ms < 1000.0, ms
+    assert int(words[2]) == 7
+    # a rung doorbell passes at once and leaves the error word alone
+    words.zero_()
+    LIB.ft_signal(C.c_void_p(words.data_ptr()), 9, 0, C.c_void_p(s.cuda_stream))
+    LIB.ft_wait_timeout(C.c_void_p(words.data_ptr()), 9, 50_000_000, C.c_void_p(words.data_ptr() + 8), 0,
+                        C.c_void_p(s.cuda_stream))
+    torch.cuda.synchronize()
+    assert int(words[0]) == 9 and int(words[2]) == 0
