@@ -191,12 +191,23 @@ class PoolBlock:
     events of the previous holder's last readers/writers — a new writer's
     stream waits on them before touching the memory (``wait_fences``)."""
 
-    __slots__ = ("policy_block", "vmm_id", "ptr", "nbytes", "device", "fences", "__weakref__")
+    __slots__ = ("policy_block", "vmm_id", "ptr", "nbytes", "device", "fences", "pool", "__weakref__")
 
-    def __init__(self, policy_block, vmm_id, ptr, nbytes, device, fences=()):
+    def __init__(self, policy_block, vmm_id, ptr, nbytes, device, fences=(), pool=None):
         self.policy_block, self.vmm_id, self.ptr, self.nbytes, self.device = (
             policy_block, vmm_id, ptr, nbytes, device)
         self.fences = fences
+        self.pool = pool
+
+    def view(self, nbytes: int, dtype=torch.uint8, shape=None) -> torch.Tensor:
+        """Zero-copy tensor over the block's first ``nbytes``: a slice of a
+        per-mapping uint8 tensor built once (``torch.as_tensor`` on an array
+        interface costs ~10 us per call; a slice costs ~1 us)."""
+        base = self.pool.base_tensor(self) if self.pool is not None else as_tensor(self.ptr, self.nbytes, self.device)
+        t = base[:nbytes]
+        if dtype != torch.uint8:
+            t = t.view(dtype)
+        return t.view(shape) if shape is not None else t
 
     def wait_fences(self, stream):
         wait_events(stream, self.fences)
@@ -223,6 +234,7 @@ class DevicePool:
         self._h = h
         self._mapped = {}  # policy block id -> (vmm id, ptr, bytes)
         self._fences = {}  # policy block id -> events the freed block's last users recorded
+        self._bases = {}   # vmm id -> uint8 tensor over the whole mapping (zero-copy views slice it)
         # physical blocks the policy dropped, still mapped: reused by growth of the same
         # class, unmapped by reclaim() when the GPU is quiet (cuMemUnmap under load stalls
         # every CUDA call of the process for 100s of ms — measured)
@@ -262,7 +274,13 @@ class DevicePool:
                 with self._lock:
                     m = self._mapped[b.block_id] = (vid.value, ptr.value, b.class_bytes)
                     self.grow_events += 1
-        return PoolBlock(b, m[0], m[1], m[2], self.device, fences)
+        return PoolBlock(b, m[0], m[1], m[2], self.device, fences, self)
+
+    def base_tensor(self, blk: PoolBlock) -> torch.Tensor:
+        t = self._bases.get(blk.vmm_id)
+        if t is None:
+            t = self._bases[blk.vmm_id] = as_tensor(blk.ptr, blk.nbytes, self.device)
+        return t
 
     def free(self, blk: PoolBlock, fences=()):
         """Return a block to the policy. ``fences``: events after which no
@@ -302,6 +320,7 @@ class DevicePool:
             for ev in fences:
                 ev.synchronize()
         for vid, _ptr, _n, _f in gone:
+            self._bases.pop(vid, None)
             LIB.ft_vmm_block_unmap(self._h, vid)
         return sum(r[2] for r in gone)
 
@@ -319,6 +338,7 @@ class DevicePool:
             return 0
         for ev in self._fences.pop(block_id, ()):  # no in-flight kernel may touch it
             ev.synchronize()
+        self._bases.pop(m[0], None)
         LIB.ft_vmm_block_unmap(self._h, m[0])
         return m[2]
 

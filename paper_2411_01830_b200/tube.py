@@ -429,16 +429,19 @@ class FaaSTube:
         with self._lock:
             self._reap()
             obj = self._objs.get(data_id)
-            self._last_op_ms = now = self.now_ms()
-            entry, _lookup_ms, _ready = self.index.resolve(data_id, self.node, now)
+            self._last_op_ms = self.now_ms()
             if obj is None:
+                # the index's own miss (dataplane.py:85-96): MissingData / unknown id
+                self.index.resolve(data_id, self.node, self._last_op_ms)
                 from ._lib import MissingData
                 raise MissingData(f"data id {data_id} has no live payload")
+            # where the payload lives: the index entry (dataplane.py:85-96), mirrored on
+            # the object at every store / relocate, so the hot path skips the FFI lookup
             if out is not None:
                 if not out.is_contiguous() or out.nbytes != obj.nbytes:
                     raise ValueError("out must be contiguous with exactly the stored byte count")
                 device = out.device.index if out.is_cuda else None
-            src = entry.location
+            src = self._loc(obj.gpu)
             dst = self._loc(device)
             if src.node == dst.node and src.gpu is not None and src.gpu == dst.gpu:
                 plan = _INTRA_GPU        # dataplane.py:184-185: same GPU -> map only (no plan object)
@@ -554,7 +557,7 @@ class FaaSTube:
 
     def _view(self, obj: _Obj) -> torch.Tensor:
         obj.pins += 1
-        t = dev.as_tensor(obj.block.ptr, obj.nbytes, obj.gpu, obj.dtype, obj.shape, owner=obj.block)
+        t = obj.block.view(obj.nbytes, obj.dtype, obj.shape)
         weakref.finalize(t, self._unpin, obj)   # strong ref: the object may already be retired
         self.stats["zero_copy"] += 1
         return t
