@@ -497,7 +497,41 @@ def run_extras(tube, g, dev, torch):
                       "zero_copy_ms_p99": round(nearest_rank(zc, 99), 4),
                       "copy_ms_p50": round(nearest_rank(cp, 50), 5), "copy_ms_p99": round(nearest_rank(cp, 99), 5),
                       "copy_gbps": round(n / (nearest_rank(cp, 50) * 1e-3) / 1e9, 2)})
+    # small handoffs: 64 objects fetched one call each vs one fetch_many (one batched launch)
+    batched = []
+    for lg in (16, 20, 22):
+        m, k = 1 << lg, 64
+        xs = torch.empty(k, m, dtype=torch.uint8, device=f"cuda:{g}").fill_(5)
+        ys = torch.empty_like(xs)
+        row = {"bytes": m, "objects": k}
+        for mode in ("one_by_one", "fetch_many"):
+            ts = []
+            for r in range(4):
+                ids = []
+                for j in range(k):
+                    d = tube.unique_id()
+                    tube.store(d, xs[j], producer="p")
+                    ids.append(d)
+                torch.cuda.synchronize()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(s)
+                if mode == "fetch_many":
+                    tube.fetch_many([(d, ys[j]) for j, d in enumerate(ids)])
+                else:
+                    for j, d in enumerate(ids):
+                        tube.fetch(d, device=g, out=ys[j])
+                b.record(s)
+                b.synchronize()
+                if r:
+                    ts.append(a.elapsed_time(b))
+            ms = statistics.median(ts)
+            row[mode + "_ms"] = round(ms, 4)
+            row[mode + "_gbps"] = round(k * m / (ms * 1e-3) / 1e9, 1)
+        assert torch.equal(ys, xs)
+        batched.append(row)
+        del xs, ys
     tube.capacity_limit = cap0
+    out["g2g_same_gpu_batched"] = batched
     out["g2g_same_gpu_sweep"] = sweep
     out["g2g_same_gpu_sweep_store_cap_bytes"] = 64e9
     try:

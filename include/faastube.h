@@ -313,6 +313,14 @@ int ft_wait(const uint32_t* flag, uint32_t value, int device, void* stream);  /*
 /* as ft_wait, giving up after timeout_ns; then writes the awaited value (or 1) to *err if err != NULL */
 int ft_wait_timeout(const uint32_t* flag, uint32_t value, uint64_t timeout_ns, uint32_t* err, int device,
                     void* stream);
+/* batched small-message copies: every segment in one launch per 64 segments
+ * (local or peer pointers, any alignment) — the launch is paid once per batch */
+typedef struct {
+  void* dst;
+  const void* src;
+  uint64_t bytes;
+} ft_segment;
+int ft_copy_batch(const ft_segment* segs, int n, int device, void* stream);
 /* raw CUDA events for stream ordering on the request path (no torch objects) */
 int ft_event_create(int device, void** ev);
 int ft_event_destroy(void* ev);

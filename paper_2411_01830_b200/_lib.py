@@ -111,6 +111,10 @@ class RouteC(C.Structure):
                 ("fw_stream", vp)]
 
 
+class SegmentC(C.Structure):
+    _fields_ = [("dst", vp), ("src", vp), ("bytes", u64)]
+
+
 class BranchC(C.Structure):
     _fields_ = [("links", LinkC * MAX_LINKS), ("hop_caps", dbl * MAX_LINKS), ("n_links", i32),
                 ("n_caps", i32), ("bytes_share", dbl), ("cap_gbps", dbl), ("reserved_gbps", dbl),
@@ -235,6 +239,7 @@ _SIGS = {
     "ft_signal": (None, [vp, C.c_uint32, C.c_int, vp]),
     "ft_wait": (None, [vp, C.c_uint32, C.c_int, vp]),
     "ft_wait_timeout": (None, [vp, C.c_uint32, u64, vp, C.c_int, vp]),
+    "ft_copy_batch": (None, [P(SegmentC), C.c_int, C.c_int, vp]),
     "ft_event_create": (None, [C.c_int, P(vp)]),
     "ft_event_destroy": (None, [vp]),
     "ft_event_record": (None, [vp, vp]),

@@ -14,6 +14,7 @@
 #include <sys/un.h>
 #include <unistd.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cstdlib>
 #include <cstdint>
@@ -260,6 +261,49 @@ __global__ void __launch_bounds__(512) k_copy_vec(int4* __restrict__ dst, const 
     for (int u = 0; u < UNROLL; ++u) __stcs(dst + i + u * stride, v[u]);
   }
   for (; i < n16; i += stride) __stcs(dst + i, __ldcs(src + i));
+}
+
+// Many segments in one launch (batched small-message passing): the launch is
+// paid once for the whole batch. Segments are cut into 32 KiB tiles dealt
+// over the grid; a CTA copies a tile with 128-bit loads/stores (4 in flight per
+// thread) when both ends are 16-byte aligned, bytewise otherwise and for tails.
+// Peer (NVLink) pointers work like local ones.
+constexpr int kMultiMax = 64;
+constexpr uint32_t kMultiTile = 32768;
+struct MultiArgs {
+  uint8_t* dst[kMultiMax];
+  const uint8_t* src[kMultiMax];
+  uint64_t bytes[kMultiMax];
+  uint64_t first_tile[kMultiMax + 1];  // prefix sum of tiles per segment
+  int n;
+};
+__global__ void __launch_bounds__(512) k_copy_multi(const __grid_constant__ MultiArgs a) {
+  const uint64_t tiles = a.first_tile[a.n];
+  for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+    int s = 0;
+    while (a.first_tile[s + 1] <= t) ++s;  // <= 64 segments: a short scan
+    const uint64_t off = (t - a.first_tile[s]) * kMultiTile;
+    const uint64_t len = min((uint64_t)kMultiTile, a.bytes[s] - off);
+    uint8_t* d = a.dst[s] + off;
+    const uint8_t* x = a.src[s] + off;
+    if ((((uintptr_t)d | (uintptr_t)x) & 15) == 0) {
+      const uint64_t n16 = len / 16;
+      int4* d4 = reinterpret_cast<int4*>(d);
+      const int4* x4 = reinterpret_cast<const int4*>(x);
+      for (uint64_t i = threadIdx.x; i < n16; i += blockDim.x * 4) {
+        int4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (i + u * blockDim.x < n16) v[u] = __ldcs(x4 + i + u * blockDim.x);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (i + u * blockDim.x < n16) __stcs(d4 + i + u * blockDim.x, v[u]);
+      }
+      for (uint64_t i = n16 * 16 + threadIdx.x; i < len; i += blockDim.x) d[i] = x[i];
+    } else {
+      for (uint64_t i = threadIdx.x; i < len; i += blockDim.x) d[i] = x[i];
+    }
+  }
 }
 
 __global__ void k_copy_bytes(uint8_t* dst, const uint8_t* src, uint64_t n) {
@@ -845,6 +889,38 @@ int ft_wait_timeout(const uint32_t* flag, uint32_t value, uint64_t timeout_ns, u
   cudaError_t e = cudaGetLastError();
   if (cur != device) cudaSetDevice(cur);
   return e == cudaSuccess ? FT_OK : cuda_fail(e, "ft_wait");
+}
+
+// ---- batched copies: one launch per <= 64 segments
+int ft_copy_batch(const ft_segment* segs, int n, int device, void* stream) {
+  if (n < 0 || (n && !segs)) {
+    ft::set_last_error("ft_copy_batch: bad arguments");
+    return FT_E_VALUE;
+  }
+  int cur = 0;
+  CU_RT(cudaGetDevice(&cur));
+  if (cur != device) CU_RT(cudaSetDevice(device));
+  cudaError_t e = cudaSuccess;
+  for (int base = 0; base < n && e == cudaSuccess;) {
+    MultiArgs a;
+    a.n = 0;
+    a.first_tile[0] = 0;
+    for (; base < n && a.n < kMultiMax; ++base) {
+      if (!segs[base].bytes) continue;
+      int k = a.n++;
+      a.dst[k] = static_cast<uint8_t*>(segs[base].dst);
+      a.src[k] = static_cast<const uint8_t*>(segs[base].src);
+      a.bytes[k] = segs[base].bytes;
+      a.first_tile[k + 1] = a.first_tile[k] + (segs[base].bytes + kMultiTile - 1) / kMultiTile;
+    }
+    if (!a.n) break;
+    uint64_t tiles = a.first_tile[a.n];
+    int grid = (int)std::min<uint64_t>(tiles, (uint64_t)4 * dev_sms(device));
+    k_copy_multi<<<grid, 512, 0, (cudaStream_t)stream>>>(a);
+    e = cudaGetLastError();
+  }
+  if (cur != device) cudaSetDevice(cur);
+  return e == cudaSuccess ? FT_OK : cuda_fail(e, "ft_copy_batch");
 }
 
 // ---- raw events (the request path's ordering, without torch.cuda.Event objects)

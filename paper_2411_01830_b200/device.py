@@ -91,6 +91,13 @@ class Ev:
                 pass
 
 
+def copy_batch(segments, device: int, stream=None):
+    """[(dst_ptr, src_ptr, nbytes)] in one launch per 64 segments (ft_copy_batch)."""
+    from ._lib import SegmentC
+    arr = (SegmentC * len(segments))(*[SegmentC(d, x, int(n)) for d, x, n in segments])
+    LIB.ft_copy_batch(arr, len(segments), int(device), C.c_void_p(stream_ptr(stream)))
+
+
 def wait_events(stream, events):
     evs = [e.h for e in events if e is not None]
     if evs:

@@ -160,3 +160,20 @@ def test_doorbell_wait_is_bounded(dev):
                         C.c_void_p(s.cuda_stream))
     torch.cuda.synchronize()
     assert int(words[0]) == 9 and int(words[2]) == 0
+
+
+def test_copy_batch_segments(dev):
+    """ft_copy_batch: >64 segments (several launches), ragged sizes, misaligned
+    and empty segments — every byte lands."""
+    rng = np.random.default_rng(3)
+    sizes = [0, 1, 15, 16, 17, 4096, 4097, 32768, 32769, 65536 + 3, (1 << 20) + 5] * 7
+    srcs = [rnd(max(n, 1) + 8, 100 + i) for i, n in enumerate(sizes)]
+    dsts = [torch.zeros(max(n, 1) + 8, dtype=torch.uint8, device="cuda:0") for n in sizes]
+    shifts = [int(rng.integers(0, 4)) for _ in sizes]
+    segs = [(d.data_ptr() + sh, x.data_ptr() + sh2, n)
+            for d, x, n, sh, sh2 in zip(dsts, srcs, sizes, shifts, reversed(shifts))]
+    dev.copy_batch(segs, 0, None)
+    torch.cuda.synchronize()
+    for d, x, n, sh, sh2 in zip(dsts, srcs, sizes, shifts, reversed(shifts)):
+        assert torch.equal(d[sh:sh + n], x[sh2:sh2 + n])
+        assert not d[:sh].any() and not d[sh + n:].any()

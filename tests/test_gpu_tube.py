@@ -176,3 +176,25 @@ def test_multi_hop_relay_chain(tube):
     assert int(digest) == int(src.to(torch.int64).sum())
     tube.maintain()
     assert not tube._keepalive
+
+
+def test_fetch_many_batched_handoff(tube):
+    """fetch_many: same-GPU objects in one batched copy, others (a host object)
+    through fetch — all bytes exact, objects retired."""
+    xs = [torch.randint(0, 256, (n,), dtype=torch.uint8, device="cuda:0") for n in (1, 4097, 1 << 20, 3 << 20)]
+    ids = []
+    for x in xs:
+        d = tube.unique_id()
+        tube.store(d, x, producer="p")
+        ids.append(d)
+    h = torch.randint(0, 256, (12345,), dtype=torch.uint8).pin_memory()
+    hd = tube.unique_id()
+    tube.store(hd, h, producer="gw")
+    outs = [torch.empty_like(x) for x in xs] + [torch.empty(12345, dtype=torch.uint8, device="cuda:0")]
+    got = tube.fetch_many(list(zip(ids + [hd], outs)), consumer="c")
+    torch.cuda.synchronize()
+    for x, o in zip(xs, got):
+        assert torch.equal(x, o)
+    assert torch.equal(got[-1].cpu(), h)
+    for d in ids + [hd]:
+        assert d not in tube._objs
