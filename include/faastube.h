@@ -321,6 +321,9 @@ typedef struct {
   uint64_t bytes;
 } ft_segment;
 int ft_copy_batch(const ft_segment* segs, int n, int device, void* stream);
+/* a private non-blocking stream on `device` (torch's stream pool aliases streams) */
+int ft_stream_create(int device, void** stream);
+int ft_stream_destroy(void* stream);
 /* raw CUDA events for stream ordering on the request path (no torch objects) */
 int ft_event_create(int device, void** ev);
 int ft_event_destroy(void* ev);
@@ -390,6 +393,14 @@ int ft_pacer_destroy(ft_pacer* p);
 int ft_pacer_submit(ft_pacer* p, const char* key, int managed, double slo_ms, double infer_ms,
                     double per_branch_cap_gbps, void* dst, int dst_dev, const void* host, uint64_t bytes,
                     int host_pinned, int k, const ft_route* routes, void* consumer_stream, uint64_t* ticket);
+/* the GPU->host direction (responses, host fetches): k routes move [off, off+len) of the
+ * device buffer `src` on src_dev into the PINNED host buffer `host_dst` — CE straight out
+ * of src_dev's own root (stage_dev == src_dev), or forward kernel into a staging GPU's ring
+ * and its CE to the host; paced by the d2h arbiter (log calls prefixed "d2h:"). The route
+ * streams first wait for `producer_stream`'s prior work; host-wait with ft_pacer_wait. */
+int ft_pacer_submit_d2h(ft_pacer* p, const char* key, int managed, double slo_ms, double infer_ms,
+                        double per_branch_cap_gbps, void* host_dst, const void* src, int src_dev, uint64_t bytes,
+                        int k, const ft_route* routes, void* producer_stream, uint64_t* ticket);
 /* host wait for a ticket's last byte (timeout_ms < 0: forever); returns the stage's status */
 int ft_pacer_wait(ft_pacer* p, uint64_t ticket, double timeout_ms);
 int ft_pacer_done(ft_pacer* p, uint64_t ticket, int* done);
@@ -398,8 +409,9 @@ int ft_pacer_stats(ft_pacer* p, uint64_t* out, int cap);
 int ft_pacer_now_ms(ft_pacer* p, double* out);
 /* logging = 1: [[t, ticket, "start"|"rate"|"issue"|"land", value], ...] */
 int ft_pacer_trace_json(ft_pacer* p, char* buf, size_t cap, size_t* need);
-/* logging = 1: every arbiter call [[t, "start"|"boundary"|"finish"|"bw", key (bw: the new bw_all), decisions], ...]
- * (replayable through the arbiter; "bw" = set_bw) */
+/* logging = 1: every arbiter call [[t, "start"|"boundary"|"finish"|"bw", key, decisions, arg], ...] with
+ * arg = the per-branch cap a start used / the new bw_all of a "bw" (= set_bw) call; GPU->host calls
+ * are prefixed "d2h:". Replayable through the arbiter. */
 int ft_pacer_log_json(ft_pacer* p, char* buf, size_t cap, size_t* need);
 /* arbiter state, as ft_arbiter_state_json */
 int ft_pacer_state_json(ft_pacer* p, char* buf, size_t cap, size_t* need);

@@ -240,6 +240,8 @@ _SIGS = {
     "ft_wait": (None, [vp, C.c_uint32, C.c_int, vp]),
     "ft_wait_timeout": (None, [vp, C.c_uint32, u64, vp, C.c_int, vp]),
     "ft_copy_batch": (None, [P(SegmentC), C.c_int, C.c_int, vp]),
+    "ft_stream_create": (None, [C.c_int, P(vp)]),
+    "ft_stream_destroy": (None, [vp]),
     "ft_event_create": (None, [C.c_int, P(vp)]),
     "ft_event_destroy": (None, [vp]),
     "ft_event_record": (None, [vp, vp]),
@@ -258,6 +260,8 @@ _SIGS = {
     "ft_pacer_destroy": (None, [vp]),
     "ft_pacer_submit": (None, [vp, cstr, C.c_int, dbl, dbl, dbl, vp, C.c_int, vp, u64, C.c_int, C.c_int,
                                P(RouteC), vp, P(u64)]),
+    "ft_pacer_submit_d2h": (None, [vp, cstr, C.c_int, dbl, dbl, dbl, vp, vp, C.c_int, u64, C.c_int, P(RouteC), vp,
+                                   P(u64)]),
     "ft_pacer_wait": (None, [vp, u64, dbl]),
     "ft_pacer_done": (None, [vp, u64, P(C.c_int)]),
     "ft_pacer_stats": (None, [vp, P(u64), C.c_int]),

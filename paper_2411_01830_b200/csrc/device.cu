@@ -923,6 +923,25 @@ int ft_copy_batch(const ft_segment* segs, int n, int device, void* stream) {
   return e == cudaSuccess ? FT_OK : cuda_fail(e, "ft_copy_batch");
 }
 
+// ---- private streams: torch.cuda.Stream() hands out a round-robin pool of 32
+// streams per device, so "new" torch streams alias each other — a CE route
+// could share a FIFO with another tenant's consumer stream. Ours are unique.
+int ft_stream_create(int device, void** stream) {
+  int cur = 0;
+  CU_RT(cudaGetDevice(&cur));
+  if (cur != device) CU_RT(cudaSetDevice(device));
+  cudaStream_t st = nullptr;
+  cudaError_t r = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  if (cur != device) cudaSetDevice(cur);
+  if (r != cudaSuccess) return cuda_fail(r, "ft_stream_create");
+  *stream = st;
+  return FT_OK;
+}
+int ft_stream_destroy(void* stream) {
+  CU_RT(cudaStreamDestroy((cudaStream_t)stream));
+  return FT_OK;
+}
+
 // ---- raw events (the request path's ordering, without torch.cuda.Event objects)
 int ft_event_create(int device, void** ev) {
   int cur = 0;

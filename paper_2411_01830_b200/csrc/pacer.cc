@@ -24,6 +24,10 @@
 // on host progress (a parked stream would deadlock against lazy module
 // loading, which synchronizes the context).
 //
+// Both directions are paced (engine.py:537-575 starts a managed stage for any
+// host_gpu plan; engine.py:186-190 gives each direction its own arbiter):
+// host->GPU legs for fetches, GPU->host legs for responses and host fetches.
+//
 // Pageable host objects are staged through one shared pinned ring
 // (PinnedRing, pcie_sched.py:122-162) by worker threads; a slot
 // is refilled once the DMA that drained it has completed.
@@ -87,7 +91,9 @@ struct Route {
   cudaStream_t ce = nullptr;    // copy-engine stream on `dev`
   cudaStream_t fw = nullptr;    // forward stream on `dev` (staged routes only)
   bool staged() const { return fw != nullptr; }
-  cudaStream_t last() const { return staged() ? fw : ce; }
+  // the route's final op: h2d staged routes end with the forward kernel, d2h
+  // staged routes with the CE leg out of the staging ring
+  cudaStream_t last(int dir) const { return staged() && dir == 0 ? fw : ce; }
 };
 
 struct Ev {
@@ -97,7 +103,7 @@ struct Ev {
 };
 struct Timing {  // a direct-route batch bracketed by timing events (link service rate)
   cudaEvent_t t0, t1;
-  int dev;
+  int dir, dev;
   uint64_t bytes;
   double issued;
   bool contended;  // another stage had bytes on the link when it was issued
@@ -111,9 +117,10 @@ struct Stage {
   uint64_t ticket = 0;
   std::string key;
   bool managed = false;
-  uint8_t* dst = nullptr;
-  int dst_dev = 0;
-  const uint8_t* host = nullptr;
+  int dir = 0;              // 0 host->GPU, 1 GPU->host
+  uint8_t* dst = nullptr;   // the GPU-side buffer (destination h2d, source d2h)
+  int dst_dev = 0;          // its GPU
+  uint8_t* host = nullptr;  // the host-side buffer (source h2d, destination d2h)
   bool pinned = true;
   uint64_t bytes = 0;
   std::vector<Route> routes;
@@ -163,7 +170,8 @@ struct ft_pacer {
   uint64_t chunk = 2000000;
   int staging_slots = 4;
   bool logging = false;
-  ft::Arbiter arb;
+  ft::Arbiter arbs[2];  // per direction (engine.py:186-190)
+  ft::Arbiter& arb_of(const Stage& st) { return arbs[st.dir]; }
   std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
 
   // ---- state (mu)
@@ -181,10 +189,10 @@ struct ft_pacer {
   // link estimator: the arbiter's bw_all tracks the service rate of uncontended
   // batches (a calibration at start-up can be far off on a shared host)
   int links = 1;
-  double link_gbps = 0.0;                    // per-link capacity the partition assumes
-  std::deque<double> samples[kMaxDev];
-  double last_issue_t[kMaxDev] = {};
-  uint64_t last_issue_ticket[kMaxDev] = {};
+  double link_gbps[2] = {0.0, 0.0};          // per-link capacity the partition assumes, per direction
+  std::deque<double> samples[2][kMaxDev];
+  double last_issue_t[2][kMaxDev] = {};
+  uint64_t last_issue_ticket[2][kMaxDev] = {};
   bool adapt = true;
   std::map<int, StagingRing> rings;
   std::map<std::string, double> guarded;  // last early boundary per stage key (A2 guard)
@@ -238,10 +246,10 @@ struct ft_pacer {
   void put(const Ev& e) { (e.timing ? tpool : evpool)[e.dev].push_back(e.e); }
 
   // anything else of ours on `dev`'s link right now?
-  bool link_busy(int dev, uint64_t self) const {
+  bool link_busy(int dir, int dev, uint64_t self) const {
     for (auto& kv : active) {
       const Stage& o = *kv.second;
-      if (o.ticket == self) continue;
+      if (o.ticket == self || o.dir != dir) continue;
       bool on = false;
       for (auto& r : o.routes) on = on || r.dev == dev;
       if (on && (!o.inflight.empty() || (o.sealed && !o.landing.empty()) || (!o.managed && !o.sealed) || o.jobs))
@@ -250,16 +258,16 @@ struct ft_pacer {
     return false;
   }
 
-  void sample(int dev, double gbps, double now) {
-    auto& q = samples[dev];
+  void sample(int dir, int dev, double gbps, double now) {
+    auto& q = samples[dir][dev];
     q.push_back(gbps);
     if (q.size() > 32) q.pop_front();
     if (!adapt || q.size() < 6) return;
     double est = *std::max_element(q.begin(), q.end());  // least-disturbed service rate
-    if (est > link_gbps * 1.05 || est < link_gbps * 0.85) {
-      link_gbps = est;
-      arb.set_bw(now, est * links);
-      arb_log(now, "bw", jnum(est * links));
+    if (est > link_gbps[dir] * 1.05 || est < link_gbps[dir] * 0.85) {
+      link_gbps[dir] = est;
+      arbs[dir].set_bw(now, est * links);
+      arb_log(dir, now, "bw", "", est * links);
       q.clear();
     }
   }
@@ -268,9 +276,13 @@ struct ft_pacer {
     if (!logging) return;
     trace.push_back("[" + jnum(now()) + "," + std::to_string(st.ticket) + ",\"" + kind + "\"," + jnum(v) + "]");
   }
-  void arb_log(double t, const char* call, const std::string& key) {
+  // log entry of an arbiter call; the GPU->host arbiter's calls carry a "d2h:" prefix
+  // [t, call, key, decisions, arg]: arg = the per-branch cap of a start, the new
+  // bw_all of a "bw" call, null otherwise
+  void arb_log(int dir, double t, const char* call, const std::string& key, double arg = NAN) {
     if (!logging) return;
-    log.push_back("[" + jnum(t) + ",\"" + call + "\",\"" + key + "\"," + arb.last_json + "]");
+    log.push_back("[" + jnum(t) + ",\"" + (dir ? "d2h:" : "") + call + "\",\"" + key + "\"," +
+                  arbs[dir].last_json + "," + jnum(arg) + "]");
   }
 
   StagingRing& ring(int dev) {
@@ -292,12 +304,16 @@ struct ft_pacer {
     return rings.emplace(dev, std::move(r)).first->second;
   }
 
-  // bytes [src, src+n) (pinned host) -> dst over route r
-  void issue(Route& r, uint8_t* dst, const uint8_t* src, uint64_t n) {
+  // n bytes between the GPU buffer `dptr` and the pinned host buffer `hptr` over
+  // route r: host->GPU (dir 0) or GPU->host (dir 1)
+  void issue(Route& r, uint8_t* dptr, uint8_t* hptr, uint64_t n, int dir) {
     if (n == 0) return;
     DevGuard g(r.dev);
     if (!r.staged()) {
-      ck(cudaMemcpyAsync(dst, src, n, cudaMemcpyHostToDevice, r.ce), "H2D");
+      if (dir == 0)
+        ck(cudaMemcpyAsync(dptr, hptr, n, cudaMemcpyHostToDevice, r.ce), "H2D");
+      else
+        ck(cudaMemcpyAsync(hptr, dptr, n, cudaMemcpyDeviceToHost, r.ce), "D2H");
       n_bytes += n;
       return;
     }
@@ -306,14 +322,26 @@ struct ft_pacer {
       uint64_t c = std::min<uint64_t>(chunk, n - o);
       int s = R.next;
       R.next = (s + 1) % R.slots;
-      if (R.used[s]) ck(cudaStreamWaitEvent(r.ce, R.freed[s], 0), "wait slot freed");  // forward drained it
       uint8_t* slot = R.buf + (uint64_t)s * chunk;
-      ck(cudaMemcpyAsync(slot, src + o, c, cudaMemcpyHostToDevice, r.ce), "staging H2D");
-      ck(cudaEventRecord(R.landed[s], r.ce), "record landed");
-      ck(cudaStreamWaitEvent(r.fw, R.landed[s], 0), "wait landed");
-      int rc = ft_copy_ex(dst + o, slot, c, r.dev, r.fw, 2, 0);  // NVLink push, vector engine
-      if (rc != FT_OK) throw CudaFail{std::string("forward: ") + ft_last_error()};
-      ck(cudaEventRecord(R.freed[s], r.fw), "record freed");
+      if (dir == 0) {
+        // CE into the staging slot, forward kernel (NVLink push) into the target
+        if (R.used[s]) ck(cudaStreamWaitEvent(r.ce, R.freed[s], 0), "wait slot freed");
+        ck(cudaMemcpyAsync(slot, hptr + o, c, cudaMemcpyHostToDevice, r.ce), "staging H2D");
+        ck(cudaEventRecord(R.landed[s], r.ce), "record landed");
+        ck(cudaStreamWaitEvent(r.fw, R.landed[s], 0), "wait landed");
+        int rc = ft_copy_ex(dptr + o, slot, c, r.dev, r.fw, 2, 0);
+        if (rc != FT_OK) throw CudaFail{std::string("forward: ") + ft_last_error()};
+        ck(cudaEventRecord(R.freed[s], r.fw), "record freed");
+      } else {
+        // forward kernel (NVLink pull) into the staging slot, CE out of it to the host
+        if (R.used[s]) ck(cudaStreamWaitEvent(r.fw, R.freed[s], 0), "wait slot freed");
+        int rc = ft_copy_ex(slot, dptr + o, c, r.dev, r.fw, 2, 0);
+        if (rc != FT_OK) throw CudaFail{std::string("forward: ") + ft_last_error()};
+        ck(cudaEventRecord(R.landed[s], r.fw), "record landed");
+        ck(cudaStreamWaitEvent(r.ce, R.landed[s], 0), "wait landed");
+        ck(cudaMemcpyAsync(hptr + o, slot, c, cudaMemcpyDeviceToHost, r.ce), "staging D2H");
+        ck(cudaEventRecord(R.freed[s], r.ce), "record freed");
+      }
       R.used[s] = 1;
       n_bytes += c;
     }
@@ -327,21 +355,21 @@ struct ft_pacer {
       if (track && !r.staged() && n) {
         // direct route: bracket the DMA with timing events (service-rate sample)
         DevGuard g(r.dev);
-        Timing tm{get_tevent(r.dev), nullptr, r.dev, n, now(), link_busy(r.dev, st.ticket)};
+        Timing tm{get_tevent(r.dev), nullptr, st.dir, r.dev, n, now(), link_busy(st.dir, r.dev, st.ticket)};
         ck(cudaEventRecord(tm.t0, r.ce), "record t0");
-        issue(r, st.dst + o, st.host + o, n);
+        issue(r, st.dst + o, st.host + o, n, st.dir);
         tm.t1 = get_tevent(r.dev);
         ck(cudaEventRecord(tm.t1, r.ce), "record t1");
         st.inflight.back().timing.push_back(tm);
-        last_issue_t[r.dev] = tm.issued;
-        last_issue_ticket[r.dev] = st.ticket;
+        last_issue_t[st.dir][r.dev] = tm.issued;
+        last_issue_ticket[st.dir][r.dev] = st.ticket;
         return;
       }
-      issue(r, st.dst + o, st.host + o, n);
+      issue(r, st.dst + o, st.host + o, n, st.dir);
       if (track) {
         DevGuard g(r.dev);
         cudaEvent_t e = get_event(r.dev);
-        ck(cudaEventRecord(e, r.last()), "record batch");
+        ck(cudaEventRecord(e, r.last(st.dir)), "record batch");
         st.inflight.back().ev.push_back(Ev{e, r.dev, false});
       }
       return;
@@ -374,8 +402,8 @@ struct ft_pacer {
     for (auto& r : st.routes) {
       DevGuard g(r.dev);
       cudaEvent_t a = get_event(r.dev), b = get_event(r.dev);
-      ck(cudaEventRecord(a, r.last()), "record join");
-      ck(cudaEventRecord(b, r.last()), "record landing");
+      ck(cudaEventRecord(a, r.last(st.dir)), "record join");
+      ck(cudaEventRecord(b, r.last(st.dir)), "record landing");
       st.join.emplace_back(a, r.dev);
       st.landing.emplace_back(b, r.dev);
     }
@@ -459,20 +487,24 @@ struct ft_pacer {
   }
 
   void deliver_due(double now) {  // engine.py:628-646, fired at their armed times
-    for (;;) {
-      double best = NAN;
-      const std::string* bk = nullptr;
-      for (auto& kv : arb.stages.items)
-        if (!std::isnan(kv.second.armed) && (std::isnan(best) || kv.second.armed < best)) {
-          best = kv.second.armed;
-          bk = &kv.first;
-        }
-      if (!bk || best > now) return;
-      std::string key = *bk;
-      arb.boundary(best, key);
-      arb_log(best, "boundary", key);
+    for (int dir = 0; dir < 2; ++dir) {
+      ft::Arbiter& arb = arbs[dir];
+      for (;;) {
+        double best = NAN;
+        const std::string* bk = nullptr;
+        for (auto& kv : arb.stages.items)
+          if (!std::isnan(kv.second.armed) && (std::isnan(best) || kv.second.armed < best)) {
+            best = kv.second.armed;
+            bk = &kv.first;
+          }
+        if (!bk || best > now) break;
+        std::string key = *bk;
+        arb.boundary(best, key);
+        arb_log(dir, best, "boundary", key);
+      }
     }
   }
+
   // Live guard for reference defect A2: a stage running at a
   // near-zero rate (least rate of a loose SLO, or the 1e12 ms infeasible fallback)
   // re-arms its next boundary one batch *at that rate* away — hours — so a rate
@@ -481,26 +513,31 @@ struct ft_pacer {
   // a pending change applies no later than two batches at the higher of the two
   // rates. Decreases are never early (their boundary is within one batch already).
   void guard_pending(double now) {
-    std::vector<std::string> due;
-    for (auto& kv : arb.stages.items) {
-      const auto& m = kv.second;
-      if (!m.started || std::isnan(m.pending) || std::isnan(m.armed)) continue;
-      double allowed = 2.0 * arb.batch_bytes / (std::max(m.pending, m.rate) * 1e6);
-      auto g = guarded.find(kv.first);
-      if (m.armed - now > allowed && (g == guarded.end() || now - g->second >= 0.5 * allowed)) due.push_back(kv.first);
-    }
-    for (auto& key : due) {
-      guarded[key] = now;
-      arb.boundary(now, key);
-      arb_log(now, "boundary", key);
-      if (logging) trace.push_back("[" + jnum(now) + ",0,\"guard\",0]");
+    for (int dir = 0; dir < 2; ++dir) {
+      ft::Arbiter& arb = arbs[dir];
+      std::vector<std::string> due;
+      for (auto& kv : arb.stages.items) {
+        const auto& m = kv.second;
+        if (!m.started || std::isnan(m.pending) || std::isnan(m.armed)) continue;
+        double allowed = 2.0 * arb.batch_bytes / (std::max(m.pending, m.rate) * 1e6);
+        auto g = guarded.find(kv.first);
+        if (m.armed - now > allowed && (g == guarded.end() || now - g->second >= 0.5 * allowed))
+          due.push_back(kv.first);
+      }
+      for (auto& key : due) {
+        guarded[key] = now;
+        arb.boundary(now, key);
+        arb_log(dir, now, "boundary", key);
+        if (logging) trace.push_back("[" + jnum(now) + ",0,\"guard\",0]");
+      }
     }
   }
 
   double next_armed() const {
     double best = NAN;
-    for (auto& kv : arb.stages.items)
-      if (!std::isnan(kv.second.armed) && (std::isnan(best) || kv.second.armed < best)) best = kv.second.armed;
+    for (int dir = 0; dir < 2; ++dir)
+      for (auto& kv : arbs[dir].stages.items)
+        if (!std::isnan(kv.second.armed) && (std::isnan(best) || kv.second.armed < best)) best = kv.second.armed;
     return best;
   }
 
@@ -517,8 +554,8 @@ struct ft_pacer {
       if (it == active.end()) continue;
       Stage& st = *it->second;
       if (st.managed) {
-        arb.finish(t, st.key);
-        arb_log(t, "finish", st.key);
+        arb_of(st).finish(t, st.key);
+        arb_log(st.dir, t, "finish", st.key);
         guarded.erase(st.key);
       }
       note(st, "land", (double)st.bytes);
@@ -547,16 +584,16 @@ struct ft_pacer {
       if (!ok) break;
       for (auto& tm : b.timing) {
         float ms = 0.f;
-        bool overlapped = tm.contended ||
-                          (last_issue_ticket[tm.dev] != st.ticket && last_issue_t[tm.dev] > tm.issued);
+        bool overlapped = tm.contended || (last_issue_ticket[tm.dir][tm.dev] != st.ticket &&
+                                           last_issue_t[tm.dir][tm.dev] > tm.issued);
         if (!overlapped && cudaEventElapsedTime(&ms, tm.t0, tm.t1) == cudaSuccess && ms > 0.f)
-          sample(tm.dev, (double)tm.bytes / ((double)ms * 1e6), t);
+          sample(tm.dir, tm.dev, (double)tm.bytes / ((double)ms * 1e6), t);
       }
       release_batch(b);
       st.inflight.pop_front();
       note(st, "done", (double)st.inflight.size());
     }
-    const auto* m = arb.stages.find(st.key);
+    const auto* m = arb_of(st).stages.find(st.key);
     if (!m || !m->started || m->rate <= 0) return INFINITY;  // waiting: a boundary / finish / start wakes it
     double dur = batch / (m->rate * 1e6);                     // ms per batch at the stage rate
     if (std::isnan(st.next_t) || m->rate != st.last_rate) {
@@ -658,7 +695,7 @@ struct ft_pacer {
           Route& r = st.routes[j.route];
           try {
             if (st.err == FT_OK) {
-              issue(r, st.dst + j.obj_off, slot, j.n);
+              issue(r, st.dst + j.obj_off, slot, j.n, 0);  // pageable: host->GPU only
               DevGuard g(r.dev);
               if (!hs.ev[r.dev]) ck(cudaEventCreateWithFlags(&hs.ev[r.dev], cudaEventDisableTiming), "event");
               ck(cudaEventRecord(hs.ev[r.dev], r.ce), "record slot");  // the CE read of the slot
@@ -714,10 +751,12 @@ int ft_pacer_create(double bw_all_gbps, int links, int batch_chunks, int64_t chu
   p->staging_slots = std::max(2, staging_slots);
   p->logging = logging != 0;
   p->links = std::max(1, links);
-  p->link_gbps = bw_all_gbps / p->links;
+  p->link_gbps[0] = p->link_gbps[1] = bw_all_gbps / p->links;
   p->adapt = !(flags & 2);
-  p->arb.share = ft::PcieState{bw_all_gbps, batch_chunks, chunk_bytes, {}};
-  p->arb.batch_bytes = (double)(chunk_bytes * batch_chunks);
+  for (auto& a : p->arbs) {
+    a.share = ft::PcieState{bw_all_gbps, batch_chunks, chunk_bytes, {}};
+    a.batch_bytes = (double)(chunk_bytes * batch_chunks);
+  }
   uint64_t slots = std::max<uint64_t>(4, host_ring_bytes / p->chunk);
   void* h = nullptr;
   cudaError_t e = cudaHostAlloc(&h, slots * p->chunk, cudaHostAllocPortable);
@@ -773,11 +812,15 @@ int ft_pacer_destroy(ft_pacer* p) {
   return rc;
 }
 
-int ft_pacer_submit(ft_pacer* p, const char* key, int managed, double slo_ms, double infer_ms,
-                    double per_branch_cap_gbps, void* dst, int dst_dev, const void* host, uint64_t bytes,
-                    int host_pinned, int k, const ft_route* routes, void* consumer_stream, uint64_t* ticket) {
+static int submit_impl(ft_pacer* p, int dir, const char* key, int managed, double slo_ms, double infer_ms,
+                       double per_branch_cap_gbps, void* dst, int dst_dev, void* host, uint64_t bytes,
+                       int host_pinned, int k, const ft_route* routes, void* consumer_stream, uint64_t* ticket) {
   if (!p || !ticket || k <= 0 || !routes || (bytes && (!dst || !host)) || dst_dev < 0 || dst_dev >= kMaxDev) {
     ft::set_last_error("ft_pacer_submit: bad arguments");
+    return FT_E_VALUE;
+  }
+  if (dir == 1 && !host_pinned) {
+    ft::set_last_error("ft_pacer_submit_d2h: the host destination must be pinned");
     return FT_E_VALUE;
   }
   uint64_t covered = 0;
@@ -797,9 +840,10 @@ int ft_pacer_submit(ft_pacer* p, const char* key, int managed, double slo_ms, do
   auto sp = std::make_shared<Stage>();
   Stage& st = *sp;
   st.managed = managed != 0;
+  st.dir = dir;
   st.dst = static_cast<uint8_t*>(dst);
   st.dst_dev = dst_dev;
-  st.host = static_cast<const uint8_t*>(host);
+  st.host = static_cast<uint8_t*>(host);
   st.pinned = host_pinned != 0;
   st.bytes = bytes;
   for (int i = 0; i < k; ++i) {
@@ -831,8 +875,11 @@ int ft_pacer_submit(ft_pacer* p, const char* key, int managed, double slo_ms, do
     if (st.managed) {
       ++p->n_managed;
       double t = p->now();
-      p->arb.start(t, st.key, (double)bytes, slo_ms, infer_ms, t, per_branch_cap_gbps, k);  // engine.py:537-575
-      p->arb_log(t, "start", st.key);
+      // the branch cap is the plan's link rate — the same calibration the estimator
+      // corrects: a link measured faster than planned caps at the measurement
+      double cap = p->adapt ? std::max(per_branch_cap_gbps, p->link_gbps[dir]) : per_branch_cap_gbps;
+      p->arb_of(st).start(t, st.key, (double)bytes, slo_ms, infer_ms, t, cap, k);  // engine.py:537-575
+      p->arb_log(dir, t, "start", st.key, cap);
       if (bytes == 0) {
         st.issued = true;
         p->seal(st);
@@ -875,6 +922,20 @@ int ft_pacer_submit(ft_pacer* p, const char* key, int managed, double slo_ms, do
   st.join.clear();
   if (rc != FT_OK) ft::set_last_error(msg);
   return rc;
+}
+
+int ft_pacer_submit(ft_pacer* p, const char* key, int managed, double slo_ms, double infer_ms,
+                    double per_branch_cap_gbps, void* dst, int dst_dev, const void* host, uint64_t bytes,
+                    int host_pinned, int k, const ft_route* routes, void* consumer_stream, uint64_t* ticket) {
+  return submit_impl(p, 0, key, managed, slo_ms, infer_ms, per_branch_cap_gbps, dst, dst_dev, const_cast<void*>(host),
+                     bytes, host_pinned, k, routes, consumer_stream, ticket);
+}
+
+int ft_pacer_submit_d2h(ft_pacer* p, const char* key, int managed, double slo_ms, double infer_ms,
+                        double per_branch_cap_gbps, void* host_dst, const void* src, int src_dev, uint64_t bytes,
+                        int k, const ft_route* routes, void* producer_stream, uint64_t* ticket) {
+  return submit_impl(p, 1, key, managed, slo_ms, infer_ms, per_branch_cap_gbps, const_cast<void*>(src), src_dev,
+                     host_dst, bytes, 1, k, routes, producer_stream, ticket);
 }
 
 int ft_pacer_wait(ft_pacer* p, uint64_t ticket, double timeout_ms) {
@@ -948,7 +1009,7 @@ int ft_pacer_log_json(ft_pacer* p, char* buf, size_t cap, size_t* need) {
 int ft_pacer_state_json(ft_pacer* p, char* buf, size_t cap, size_t* need) {
   if (!p) return FT_E_VALUE;
   std::lock_guard<std::mutex> lk(p->mu);
-  std::string s = p->arb.state_json();
+  std::string s = p->arbs[0].state_json();
   if (need) *need = s.size() + 1;
   if (!buf || cap < s.size() + 1) {
     ft::set_last_error("json output buffer too small");

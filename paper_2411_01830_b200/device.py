@@ -53,6 +53,21 @@ def current_stream(device: int) -> int:
     return torch._C._cuda_getCurrentRawStream(device)
 
 
+def new_stream(device: int) -> torch.cuda.ExternalStream:
+    """A private CUDA stream (``ft_stream_create``) as a torch stream object.
+    torch.cuda.Stream() hands out a round-robin pool of 32 streams per device:
+    two "new" torch streams can be the same CUDA stream, and a copy-engine
+    route would then share a FIFO with another tenant's consumer stream."""
+    h = C.c_void_p()
+    LIB.ft_stream_create(int(device), C.byref(h))
+    return torch.cuda.ExternalStream(h.value, device=torch.device("cuda", device))
+
+
+def destroy_stream(stream: torch.cuda.ExternalStream):
+    stream.synchronize()
+    LIB.ft_stream_destroy(C.c_void_p(stream.cuda_stream))
+
+
 class Ev:
     """A raw CUDA event (libfaastube ``ft_event_*``): request-path stream
     ordering without torch.cuda.Event objects. Destroyed with the object
@@ -418,6 +433,17 @@ class Pacer:
                             float(per_branch_cap_gbps), C.c_void_p(dst_ptr), int(dst_dev), C.c_void_p(host_ptr),
                             int(nbytes), int(bool(host_pinned)), len(routes), arr, C.c_void_p(consumer_stream),
                             C.byref(t))
+        return t.value
+
+    def submit_d2h(self, key: str, managed: bool, slo_ms: float, infer_ms: float, per_branch_cap_gbps: float,
+                   host_ptr: int, src_ptr: int, src_dev: int, nbytes: int, routes: list, producer_stream: int) -> int:
+        """GPU -> pinned host; routes as for submit (stage_dev == src_dev: direct) -> ticket"""
+        arr = (self._route_t * len(routes))(*[self._route_t(int(a), int(b), int(c), int(d), e, f)
+                                               for a, b, c, d, e, f in routes])
+        t = C.c_uint64()
+        LIB.ft_pacer_submit_d2h(self._h, key.encode(), int(bool(managed)), float(slo_ms), float(infer_ms),
+                                float(per_branch_cap_gbps), C.c_void_p(host_ptr), C.c_void_p(src_ptr), int(src_dev),
+                                int(nbytes), len(routes), arr, C.c_void_p(producer_stream), C.byref(t))
         return t.value
 
     def done(self, ticket: int) -> bool:

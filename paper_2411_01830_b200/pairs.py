@@ -38,8 +38,8 @@ class CrossPair:
         self.flags = pool.allocate(FLAG_BYTES)               # [0] RDY (I consume), [1] ACK (I produce)
         dev.as_tensor(self.flags.ptr, FLAG_BYTES, device).zero_()
         torch.cuda.synchronize(device)
-        self.prod_stream = torch.cuda.Stream(device)
-        self.cons_stream = torch.cuda.Stream(device)
+        self.prod_stream = dev.new_stream(device)
+        self.cons_stream = dev.new_stream(device)
         nxt, prv = (rank + 1) % world, (rank - 1) % world
         srv = Channel.listen(os.path.join(sock_dir, f"r{rank}.sock"))
         barrier()

@@ -61,7 +61,8 @@ RECLAIM_IDLE_MS = 1000.0
 
 class _Obj:
     __slots__ = ("did", "nbytes", "dtype", "shape", "gpu", "block", "host", "producer", "remaining", "ready",
-                 "pins", "retired", "response_host", "response_event", "stored_at", "home", "queue_pos",
+                 "pins", "retired", "response_host", "response_event", "response_ticket", "stored_at", "home",
+                 "queue_pos",
                  "readers", "__weakref__")
 
     def __init__(self, did, nbytes, dtype, shape, gpu, producer, consumers, now):
@@ -77,6 +78,7 @@ class _Obj:
         self.retired = False
         self.response_host = None
         self.response_event = None
+        self.response_ticket = None  # pacer ticket of a managed GPU->host response stage
         self.stored_at = now
         self.readers = []      # events of copies on other streams/GPUs that read the block
 
@@ -123,10 +125,13 @@ class FaaSTube:
         self._t0 = time.perf_counter()
         self._objs: dict[int, _Obj] = {}
         self._lock = threading.RLock()
-        self._ce = {g: [torch.cuda.Stream(g) for _ in range(2)] for g in self.gpus}  # copy-engine streams
+        self._ce = {g: [dev.new_stream(g) for _ in range(2)] for g in self.gpus}  # copy-engine streams
         # per-transfer CE stream pairs (PCIe leg, NVLink forward): concurrent tenants'
         # DMA must not queue FIFO behind each other on one stream
-        self._ce_pairs = {g: [(torch.cuda.Stream(g), torch.cuda.Stream(g)) for _ in range(16)] for g in self.gpus}
+        self._ce_pairs = {g: [(dev.new_stream(g), dev.new_stream(g)) for _ in range(16)] for g in self.gpus}
+        # GPU->host stages get their own pairs: a D2H op queued behind another
+        # tenant's H2D batches on a shared stream would wait for them
+        self._d2h_pairs = {g: [(dev.new_stream(g), dev.new_stream(g)) for _ in range(8)] for g in self.gpus}
         self._ce_rr = itertools.count()
         self._keepalive = []         # (event, buffers) released once the event has completed
         self._last_op_ms = 0.0       # last store/fetch (idle detection for physical reclaim)
@@ -261,13 +266,28 @@ class FaaSTube:
                 # must not happen under the tube lock
                 pre_blk = self.pools[output.device.index].allocate(output.nbytes)
         try:
-            self._store_locked(data_id, output, response, producer, consumers, queue_pos, pre_host, pre_blk)
+            stage = self._store_locked(data_id, output, response, producer, consumers, queue_pos, pre_host, pre_blk)
         except BaseException:
             if pre_blk is not None:
                 self.pools[output.device.index].free(pre_blk, list(pre_blk.fences))
             raise
+        if stage is not None:
+            # managed GPU->host response stage (engine.py:414-423 -> 537-575), paced
+            # by the d2h arbiter outside the tube lock; the object stays pinned
+            # until its block's readers include the stage
+            obj, args = stage
+            try:
+                ticket = self.pacer.submit_d2h(*args)
+                with self._lock:
+                    obj.response_ticket = ticket
+                    obj.readers.append(dev.Ev(obj.gpu).record(args[-1]))   # source stream waits on the routes
+                    self._tickets.append((ticket, obj.response_host, None))
+            finally:
+                self._unpin(obj)
 
     def _store_locked(self, data_id, output, response, producer, consumers, queue_pos, pre_host, pre_blk):
+        """Returns (obj, pacer.submit_d2h args) when a managed response stage must be submitted."""
+        stage = None
         with self._lock:
             self._reap()
             if data_id in self._objs:
@@ -306,7 +326,10 @@ class FaaSTube:
                 self._push_shrink(g, producer, now)
                 self.index.store(data_id, self._loc(g), nbytes, now, producer, response)
                 if response:
-                    self._respond(obj, pre_host)
+                    resp = self._respond(obj, pre_host)
+                    if resp is not None:
+                        obj.pins += 1                    # released once the stage is submitted
+                        stage = (obj, resp)
             elif t.is_cuda:
                 # host-oriented store: the output lands in host memory (engine.py:361-381)
                 g = t.device.index
@@ -314,8 +337,10 @@ class FaaSTube:
                 s = self._ce[g][0]
                 dev.Ev(g).record(self._stream(g)).wait(s)    # the producer's output is written
                 dev.pcie_copy(host.data_ptr(), t.data_ptr(), nbytes, False, g, s)
-                t.record_stream(s)
                 ev = dev.Ev(g).record(s)
+                # the producer's tensor stays referenced until the D2H has read it (no
+                # record_stream on a private stream: the allocator would keep its handle)
+                self._keepalive.append((ev, [t]))
                 obj.host, obj.ready = host, ev
                 if response:                               # already in host memory
                     obj.response_host, obj.response_event = host, ev
@@ -339,6 +364,7 @@ class FaaSTube:
             if obj.block is not None and self.strategy.migration != "none" and \
                     self._stored_on(obj.gpu) > self.capacity_limit:
                 self._check_pressure(obj.gpu)                # engine.py:685-702
+        return stage
 
     # ------------------------------------------------ queue-aware migration (§8f row 1)
     def _stored_on(self, g) -> int:
@@ -448,14 +474,36 @@ class FaaSTube:
             else:
                 plan = self.plane.fetch_plan(src, dst, obj.nbytes)
             h2g = plan.method == "host_gpu" and not dst.on_host
+            d2h = (plan.method == "host_gpu" and dst.on_host and obj.block is not None and self.strategy.pcie_sched
+                   and plan.stages[0].managed)
             if h2g:
                 res, stage = self._host_to_gpu(obj, plan, dst, out, slo_ms, infer_ms)
+            elif d2h:
+                # managed GPU->host fetch: into pinned memory (the caller's if pinned); the
+                # object stays pinned until its block's readers include the stage
+                res = out if out is not None and out.is_pinned() else self._pinned(obj.nbytes)
+                stage = self._d2h_stage(obj, plan, res, consumer, slo_ms, infer_ms)
+                self.stats["bytes_d2h"] += obj.nbytes
+                obj.pins += 1
             else:
                 res = self._execute(obj, plan, src, dst, out, slo_ms, infer_ms)
             self.stats["fetches"] += 1
             self._consumed(obj)
-            if not h2g:
+            if not (h2g or d2h):
                 return res
+        if d2h:
+            # the pacer paces the stage outside the tube lock; a host result means waiting for it
+            try:
+                ticket = self.pacer.submit_d2h(*stage)
+                with self._lock:
+                    obj.readers.append(dev.Ev(obj.gpu).record(stage[-1]))  # source stream waits on the routes
+            finally:
+                self._unpin(obj)
+            self.pacer.wait(ticket)
+            if out is not None and res.data_ptr() != out.data_ptr():
+                out.view(-1).view(torch.uint8).copy_(res.view(-1))
+                return out
+            return res.view(torch.uint8).view(obj.dtype).view(obj.shape)
         # host->GPU stage: the pacer returns once its last batch is issued — outside
         # the tube lock, so concurrent tenants' stages are paced side by side
         ticket = self.pacer.submit(*stage)
@@ -520,7 +568,10 @@ class FaaSTube:
         if obj is None or obj.response_host is None:
             from ._lib import MissingData
             raise MissingData(f"no response for data id {data_id}")
-        obj.response_event.synchronize()
+        if obj.response_ticket is not None:
+            self.pacer.wait(obj.response_ticket)
+        else:
+            obj.response_event.synchronize()
         return obj.response_host.view(obj.dtype).view(obj.shape)
 
     def close(self):
@@ -535,6 +586,9 @@ class FaaSTube:
         self._objs.clear()
         for p in self.pools.values():
             p.close()
+        for g in self.gpus:
+            for st in self._ce[g] + [x for pr in self._ce_pairs[g] + self._d2h_pairs[g] for x in pr]:
+                dev.destroy_stream(st)
 
     # ------------------------------------------------------------ internals
     def _push_shrink(self, g, func, now):
@@ -548,8 +602,16 @@ class FaaSTube:
                 self._maint_cv.notify()
 
     def _respond(self, obj: _Obj, host=None):
+        """Response D2H of a stored output (engine.py:414-423). With the PCIe
+        scheduler it is a managed GPU->host stage over the plan's routes
+        (returned for submission outside the tube lock); otherwise one CE copy."""
         g = obj.gpu
         host = host if host is not None else self._pinned(obj.nbytes)
+        if self.strategy.pcie_sched:
+            plan = self.plane.fetch_plan(self._loc(g), self._loc(None), obj.nbytes)
+            obj.response_host = host
+            self.stats["bytes_d2h"] += obj.nbytes
+            return self._d2h_stage(obj, plan, host, obj.producer, None, None)
         s = self._ce[g][1]
         obj.ready.wait(s)
         dev.pcie_copy(host.data_ptr(), obj.block.ptr, obj.nbytes, False, g, s)
@@ -557,6 +619,31 @@ class FaaSTube:
         obj.response_host, obj.response_event = host, ev
         obj.readers.append(ev)
         self.stats["bytes_d2h"] += obj.nbytes
+        return None
+
+    def _d2h_stage(self, obj, plan, host, consumer, slo_ms, infer_ms):
+        """pacer.submit_d2h arguments for a GPU->host plan (dataplane.py:190-250
+        with into=False): route i moves branch i's byte range out of the source
+        GPU's own root, or over NVLink into a staging GPU's ring and out of its root."""
+        g = obj.gpu
+        st = plan.stages[0]
+        br = st.branches
+        ranges = self._stripes(obj.nbytes, [b.bytes_share for b in br])
+        s = self._stream(g)
+        obj.ready.wait(s)
+        slot = (s >> 4) * 0x9E3779B1 >> 16
+        routes = []
+        for b, (off, n) in zip(br, ranges):
+            sg = _staging_gpu_d2h(b.links, g)
+            ce, fw = self._d2h_pairs[sg][slot % len(self._d2h_pairs[sg])]
+            routes.append((sg, 0, off, n, ce.cuda_stream, fw.cuda_stream))
+            if sg != g:
+                self.stats["bytes_nvlink"] += n
+        managed = bool(self.strategy.pcie_sched and st.managed)
+        self.stats["managed_stages"] = self.stats.get("managed_stages", 0) + int(managed)
+        return (f"m{next(self._managed_ids)}" if managed else "", managed,
+                slo_ms if slo_ms else 1e9, infer_ms if infer_ms is not None else 0.0,
+                min(min(b.hop_caps) for b in br), host.data_ptr(), obj.block.ptr, g, obj.nbytes, routes, s)
 
     def _consumed(self, obj: _Obj):
         obj.remaining -= 1
@@ -642,7 +729,7 @@ class FaaSTube:
                 obj.readers.append(ev)
             ev.wait(s)
             dev.pcie_copy(res.data_ptr(), host.data_ptr(), obj.nbytes, True, dst.gpu, s)
-            host.record_stream(torch.cuda.current_stream(dst.gpu))
+            self._keepalive.append((dev.Ev(dst.gpu).record(s), [host]))   # until the H2D has read it
             self.stats["bytes_d2h"] += obj.nbytes
             self.stats["bytes_h2d"] += obj.nbytes
             return res
@@ -803,6 +890,16 @@ def _hops(links):
         elif l[0] == "nvp_in":
             hops.append((pending, l[1]))
     return hops
+
+
+def _staging_gpu_d2h(links, source):
+    """GPU whose PCIe root carries a GPU->host branch (the NVLink hop's far end)."""
+    for l in links:
+        if l[0] == "nvp_in":
+            return l[1]
+        if l[0] == "nv":
+            return l[2]
+    return source
 
 
 def _staging_gpu(links, target):

@@ -140,15 +140,16 @@ def test_live_decisions_replay_through_oracle(dev):
     while p.stats()["active"] and time.time() < deadline:
         time.sleep(0.01)
     log = p.log()
-    assert [c for _, c, _, _ in log].count("start") == 3 and [c for _, c, _, _ in log].count("finish") == 3
+    calls = [e[1] for e in log]
+    assert calls.count("start") == 3 and calls.count("finish") == 3
     o = Oracle(55.0, 5, 2 * MB)
     sizes = dict(zip(("m0", "m1", "m2"), n))
     slos = dict(zip(("m0", "m1", "m2"), slo))
-    for t, call, key, want in log:
-        if call == "start":
-            got = o.start(t, key, float(sizes[key]), slos[key][0], slos[key][1], t, 55.0, 1)
+    for t, call, key, want, arg in log:
+        if call == "start":                      # arg: the per-branch cap the pacer used
+            got = o.start(t, key, float(sizes[key]), slos[key][0], slos[key][1], t, arg, 1)
         elif call == "bw":                       # the live link estimator re-partitioned
-            got = o.set_bw(t, float(key))
+            got = o.set_bw(t, arg)
         elif call == "boundary":
             got = o.boundary(t, key)
         else:
@@ -205,10 +206,31 @@ def test_link_estimator_corrects_a_low_calibration(dev, adapt):
     ms = (time.perf_counter() - t0) * 1e3
     torch.cuda.synchronize()
     assert torch.equal(dst.cpu(), host)
-    bws = [float(k) for _, c, k, _ in p.log() if c == "bw"]
+    bws = [e[4] for e in p.log() if e[1] == "bw"]
     if adapt:
         assert bws and bws[-1] > 15.0, bws
         assert ms < 0.7 * n / 8e6, (ms, bws)
     else:
         assert not bws and ms > 0.9 * n / 8e6, ms
+    p.close()
+
+
+@pytest.mark.parametrize("managed", [False, True])
+@pytest.mark.parametrize("n,kinds", [(1, "d"), ((8 << 20) + 77, "ds"), (5 * MB + 3, "s")])
+def test_d2h_stage_bit_exact(dev, managed, n, kinds):
+    """GPU -> pinned host stages (responses, host fetches): direct routes out of the
+    source GPU's root and staged routes (forward kernel into the staging ring, CE
+    out of it — forced on one GPU), paced by the d2h arbiter."""
+    p = dev.Pacer(55.0, 5, 2 * MB, staging_slots=3, logging=True)
+    streams = [(torch.cuda.Stream(0), torch.cuda.Stream(0)) for _ in kinds]
+    src = torch.randint(0, 256, (n,), dtype=torch.uint8, device="cuda:0")
+    host = torch.zeros(n, dtype=torch.uint8).pin_memory()
+    s = torch.cuda.current_stream(0)
+    t = p.submit_d2h("d1" if managed else "", managed, 1e9, 0.0, 55.0, host.data_ptr(), src.data_ptr(), 0, n,
+                     routes_for(n, kinds, streams), s.cuda_stream)
+    p.wait(t, 5000.0)
+    assert torch.equal(host, src.cpu())
+    calls = [e[1] for e in p.log()]
+    assert (calls.count("d2h:start"), calls.count("d2h:finish")) == ((1, 1) if managed else (0, 0)), calls
+    assert "start" not in calls
     p.close()

@@ -16,7 +16,7 @@ def _run(strategy, preset="yelp", rate=20.0, dur=1.0, compute="sleep", seed=0):
     where = workload.place(wf, tube.topo, {}, colocate=tube.topo.gpu_count < len(wf.gfuncs()))
     workload.calibrate_slo(wf, tube.topo, where, 1.5)
     reqs = workload.build_requests(wf, workload.gen_workload("sporadic", rate, dur, seed), seed)
-    Runtime.warm_daemon(tube, [(wf, where, reqs)], compute, 0.3)
+    Runtime.warm_daemon(tube, [(wf, where, reqs)], compute, 0.5)
     rt = Runtime(tube, compute=compute)
     out = rt.run([(wf, where, reqs)], dur, drain_s=60)
     tube.close()

@@ -58,7 +58,8 @@ def _contend(strategy, link_gbps, n_loose=3, loose_bytes=1000 * MB, tight_bytes=
     go = threading.Event()
 
     def run(k, delay):
-        s = torch.cuda.Stream(0)           # each tenant function has its own stream
+        from paper_2411_01830_b200 import device as dev
+        s = dev.new_stream(0)              # each tenant function has its own (private) stream
         go.wait()
         time.sleep(delay)
         t0 = time.perf_counter()

@@ -198,3 +198,24 @@ def test_fetch_many_batched_handoff(tube):
     assert torch.equal(got[-1].cpu(), h)
     for d in ids + [hd]:
         assert d not in tube._objs
+
+
+def test_managed_response_and_host_fetch():
+    """With the PCIe scheduler, responses and GPU->host fetches are managed
+    GPU->host stages (engine.py:414-423, 537-575) — bytes exact, caller's
+    pinned or pageable output."""
+    from paper_2411_01830_b200.tube import FaaSTube
+    t = FaaSTube("faastube", pool_floor_bytes=0.0)
+    x = torch.randint(0, 256, ((12 << 20) + 5,), dtype=torch.uint8, device="cuda:0")
+    before = t.pacer.stats()["managed_stages"]
+    d = t.unique_id()
+    t.store(d, x, producer="sink", response=True)
+    assert torch.equal(t.response(d), x.cpu())
+    t.release(d)
+    for out in (None, torch.empty(x.numel(), dtype=torch.uint8).pin_memory(), torch.empty(x.numel(), dtype=torch.uint8)):
+        d = t.unique_id()
+        t.store(d, x, producer="p")
+        got = t.fetch(d, device=None, out=out)
+        assert torch.equal(got.reshape(-1).view(torch.uint8), x.cpu())
+    assert t.pacer.stats()["managed_stages"] == before + 4
+    t.close()

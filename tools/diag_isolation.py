@@ -37,7 +37,7 @@ for th, name, a, b in sorted(marks, key=lambda m: m[2])[:60]:
     print(f"{th:12s} {name:14s} {1e3*(a-m0):9.3f} -> {1e3*(b-m0):9.3f}")
 log, tr = logs[0]
 t0 = log[0][0] if log else 0
-for t, call, key, dec in log[:80]:
+for t, call, key, dec, *_ in log[:80]:
     short = []
     for d in dec:
         if d[0] == "partition":
