@@ -70,11 +70,13 @@ class Arbiter:
         self._resync(now)
         return self._out
 
-    def set_bw(self, now, bw_all):
+    def set_bw(self, now, bw_all, link_gbps):
         """Live pacer only (no engine counterpart): the measured link capacity
-        changed; re-partition at ``now``."""
+        changed; stage caps rise to at least the link per flow; re-partition."""
         self._out = []
         self.share.bw_all = bw_all
+        for st in self.stages.values():
+            st.cap = max(st.cap, link_gbps * st.n_flows)
         self._resync(now)
         return self._out
 

@@ -221,7 +221,9 @@ struct Arbiter {
   void finish(double now, const std::string& key);
   // live only (no reference counterpart): the link capacity the partition hands out
   // changed (measured by the pacer); re-partition at `now` as any other event does
-  void set_bw(double now, double bw_all);
+  // (each stage's cap is raised to at least link_gbps per flow: caps come from the
+  // same planned link rate the measurement replaces)
+  void set_bw(double now, double bw_all, double link_gbps);
   std::string state_json() const;
 
  private:

@@ -266,8 +266,8 @@ struct ft_pacer {
     double est = *std::max_element(q.begin(), q.end());  // least-disturbed service rate
     if (est > link_gbps[dir] * 1.05 || est < link_gbps[dir] * 0.85) {
       link_gbps[dir] = est;
-      arbs[dir].set_bw(now, est * links);
-      arb_log(dir, now, "bw", "", est * links);
+      arbs[dir].set_bw(now, est * links, est);
+      arb_log(dir, now, "bw", jnum(est), est * links);  // key: the per-link estimate
       q.clear();
     }
   }

@@ -390,9 +390,10 @@ void Arbiter::finish(double now, const std::string& key) {  // engine.py:558-564
   resync(now);
   end();
 }
-void Arbiter::set_bw(double now, double bw_all) {
+void Arbiter::set_bw(double now, double bw_all, double link_gbps) {
   begin();
   share.bw_all = bw_all;
+  for (auto& kv : stages.items) kv.second.cap = std::max(kv.second.cap, link_gbps * kv.second.n_flows);
   resync(now);
   end();
 }

@@ -149,7 +149,7 @@ def test_live_decisions_replay_through_oracle(dev):
         if call == "start":                      # arg: the per-branch cap the pacer used
             got = o.start(t, key, float(sizes[key]), slos[key][0], slos[key][1], t, arg, 1)
         elif call == "bw":                       # the live link estimator re-partitioned
-            got = o.set_bw(t, arg)
+            got = o.set_bw(t, arg, float(key))
         elif call == "boundary":
             got = o.boundary(t, key)
         else:

@@ -96,3 +96,27 @@ def test_isolation_tight_tenant_meets_its_window():
     info = (link, window, managed, shared)
     assert managed["T"] < shared["T"], info
     assert managed["T"] < 1.5 * window + 5.0, info
+
+
+def test_tube_recovers_from_a_low_link_calibration():
+    """A tube told its PCIe link does 10 GB/s (a calibration taken while the host
+    was busy) learns the real rate from its own batches: a 1 GiB host->GPU fetch
+    still runs near the link, and so does the next one."""
+    from paper_2411_01830_b200.tube import FaaSTube, measure_pcie_gbps
+    link = measure_pcie_gbps([0])
+    tube = FaaSTube("faastube", pool_floor_bytes=0.0, pcie_gbps=10.0)
+    n = 1 << 30
+    host = torch.from_numpy(np.random.default_rng(5).integers(0, 256, n, dtype=np.uint8)).pin_memory()
+    out = torch.empty(n, dtype=torch.uint8, device="cuda:0")
+    times = []
+    for _ in range(2):
+        d = tube.unique_id()
+        tube.store(d, host, producer="gw")
+        t0 = time.perf_counter()
+        tube.fetch(d, out=out, consumer="f")
+        torch.cuda.synchronize()
+        times.append(time.perf_counter() - t0)
+    assert torch.equal(out[:1 << 20].cpu(), host[:1 << 20]) and torch.equal(out[-(1 << 20):].cpu(), host[-(1 << 20):])
+    gbps = [n / t / 1e9 for t in times]
+    tube.close()
+    assert gbps[0] > 2 * 10.0 and gbps[1] > 0.7 * link, (gbps, link)
