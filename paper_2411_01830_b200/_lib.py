@@ -317,6 +317,20 @@ class _Lib:
 LIB = _Lib()
 
 
+def destroyer(name):
+    """A finalizer for handles released by ``name``: holds the library itself, so it
+    still works while the interpreter tears module globals down (no stray
+    "NoneType has no attribute" errors at exit) and never raises."""
+    lib = LIB
+
+    def destroy(h):
+        try:
+            lib.raw(name)(h)
+        except Exception:  # noqa: BLE001 - best effort in finalizers
+            pass
+    return destroy
+
+
 def raise_status(rc):
     msg = LIB.raw("ft_last_error")()
     msg = msg.decode() if msg else f"status {rc}"

@@ -13,7 +13,7 @@ import ctypes as C
 import math
 from dataclasses import dataclass, field
 
-from ._lib import LIB, DuplicateStore, MissingData, enc, json_out
+from ._lib import LIB, destroyer, DuplicateStore, MissingData, enc, json_out
 from .strategies import Strategy
 from .topology import BandwidthMatrix, Topology
 
@@ -59,11 +59,11 @@ class DataIndex:
         self._h = h
         self._meta = {}
 
-    def __del__(self):
+    def __del__(self, _destroy=destroyer("ft_index_destroy")):
         h = getattr(self, "_h", None)
         if h:
-            LIB.ft_index_destroy(h)
             self._h = None
+            _destroy(h)
 
     def unique_id(self) -> int:
         x = C.c_int64()
@@ -158,11 +158,11 @@ class TransferPlan:
     note = property(lambda self: self._full()["note"])
     stages = property(lambda self: self._full()["stages"])
 
-    def __del__(self):
+    def __del__(self, _destroy=destroyer("ft_plan_destroy")):
         h = getattr(self, "_h", None)
         if h:
-            LIB.ft_plan_destroy(h)
             self._h = None
+            _destroy(h)
 
     @property
     def fixed_ms(self) -> float:
@@ -191,11 +191,11 @@ class Dataplane:
                             C.byref(h))
         self._h = h
 
-    def __del__(self):
+    def __del__(self, _destroy=destroyer("ft_plane_destroy")):
         h = getattr(self, "_h", None)
         if h:
-            LIB.ft_plane_destroy(h)
             self._h = None
+            _destroy(h)
 
     def fetch_plan(self, entry_loc: Location, dest: Location, size_bytes: float) -> TransferPlan:
         """dataplane.py:176-186"""

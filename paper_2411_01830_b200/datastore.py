@@ -12,7 +12,7 @@ from __future__ import annotations
 import ctypes as C
 from dataclasses import dataclass, field
 
-from ._lib import LIB, MAX_CONSUMERS, HardPressure, StoredObjectC, enc, json_out
+from ._lib import LIB, destroyer, MAX_CONSUMERS, HardPressure, StoredObjectC, enc, json_out
 
 HISTOGRAM_WINDOW = 1000          # datastore.py:17
 POOL_FLOOR_BYTES = 300 * 10**6   # datastore.py:18
@@ -48,11 +48,11 @@ class FuncHistogram:
         LIB.ft_hist_create(enc(func), int(window), C.byref(h))
         self._h = h
 
-    def __del__(self):
+    def __del__(self, _destroy=destroyer("ft_hist_destroy")):
         h = getattr(self, "_h", None)
         if h:
-            LIB.ft_hist_destroy(h)
             self._h = None
+            _destroy(h)
 
     def _get(self):
         a, b, c, d = C.c_double(), C.c_double(), C.c_double(), C.c_double()
@@ -114,11 +114,11 @@ class MemoryPool:
         self._blocks = {}
         self.histograms = {}
 
-    def __del__(self):
+    def __del__(self, _destroy=destroyer("ft_pool_policy_destroy")):
         h = getattr(self, "_h", None)
         if h:
-            LIB.ft_pool_policy_destroy(h)
             self._h = None
+            _destroy(h)
 
     def state(self) -> dict:
         return json_out("ft_pool_policy_state_json", self._h)

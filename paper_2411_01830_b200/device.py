@@ -271,7 +271,11 @@ class DevicePool:
             LIB.ft_vmm_pool_destroy(h)
             self._h = None
 
-    __del__ = close
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001 - interpreter teardown
+            pass
 
     def allocate(self, nbytes: int) -> PoolBlock:
         """Policy decision (reuse exact class or grow) + physical mapping on growth.
@@ -483,4 +487,8 @@ class Pacer:
             self._h = None
             LIB.ft_pacer_destroy(h)
 
-    __del__ = close
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001 - interpreter teardown
+            pass

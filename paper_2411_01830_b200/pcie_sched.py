@@ -7,7 +7,7 @@ from __future__ import annotations
 import ctypes as C
 from dataclasses import dataclass, field
 
-from ._lib import LIB, InfeasibleDemand, enc
+from ._lib import LIB, destroyer, InfeasibleDemand, enc
 
 CHUNK_BYTES = 2 * 10**6      # pcie_sched.py:14
 BATCH_CHUNKS = 5             # pcie_sched.py:15
@@ -59,11 +59,11 @@ class PcieSchedulerState:
         LIB.ft_pcie_state_create(self.bw_all_gbps, self.batch_chunks, self.chunk_bytes, C.byref(h))
         self._h = h
 
-    def __del__(self):
+    def __del__(self, _destroy=destroyer("ft_pcie_state_destroy")):
         h = getattr(self, "_h", None)
         if h:
-            LIB.ft_pcie_state_destroy(h)
             self._h = None
+            _destroy(h)
 
     @property
     def batch_bytes(self) -> int:
@@ -128,11 +128,11 @@ class PinnedRing:
         LIB.ft_ring_create(float(capacity_bytes), float(cost_ms_per_mb), 1 if prewarmed else 0, C.byref(h))
         self._h = h
 
-    def __del__(self):
+    def __del__(self, _destroy=destroyer("ft_ring_destroy")):
         h = getattr(self, "_h", None)
         if h:
-            LIB.ft_ring_destroy(h)
             self._h = None
+            _destroy(h)
 
     def _state(self):
         w, c = C.c_double(), C.c_double()

@@ -16,7 +16,7 @@ from __future__ import annotations
 
 import ctypes as C
 
-from ._lib import LIB, enc, json_out
+from ._lib import LIB, destroyer, enc, json_out
 
 
 class StageArbiter:
@@ -27,11 +27,11 @@ class StageArbiter:
         LIB.ft_arbiter_create(float(bw_all_gbps), int(batch_chunks), int(chunk_bytes), C.byref(h))
         self._h = h
 
-    def __del__(self):
+    def __del__(self, _destroy=destroyer("ft_arbiter_destroy")):
         h = getattr(self, "_h", None)
         if h:
-            LIB.ft_arbiter_destroy(h)
             self._h = None
+            _destroy(h)
 
     def start(self, now_ms, key, total_bytes, slo_ms, infer_ms, arrival_ms, per_branch_cap_gbps, n_branches):
         LIB.ft_arbiter_start(self._h, float(now_ms), enc(key), float(total_bytes), float(slo_ms), float(infer_ms),

@@ -10,7 +10,7 @@ from __future__ import annotations
 import ctypes as C
 import json
 
-from ._lib import LIB, TopologyError, enc, json_out
+from ._lib import LIB, destroyer, TopologyError, enc, json_out
 
 __all__ = ["Topology", "TopologyError", "BandwidthMatrix", "build_preset", "b200_doc", "from_dict",
            "load_custom", "snapshot_matrix", "PRESET_NAMES"]
@@ -48,11 +48,11 @@ class Topology:
             rates.append(x.value)
         self.pcie_gbps, self.pcie_pageable_gbps, self.pcie_peer_gbps, self.network_gbps = rates
 
-    def __del__(self):
+    def __del__(self, _destroy=destroyer("ft_topo_destroy")):
         h = getattr(self, "_h", None)
         if h:
-            LIB.ft_topo_destroy(h)
             self._h = None
+            _destroy(h)
 
     @property
     def handle(self):
@@ -176,11 +176,11 @@ class BandwidthMatrix:
         LIB.ft_matrix_create(topo.handle, C.byref(h))
         self._h = h
 
-    def __del__(self):
+    def __del__(self, _destroy=destroyer("ft_matrix_destroy")):
         h = getattr(self, "_h", None)
         if h:
-            LIB.ft_matrix_destroy(h)
             self._h = None
+            _destroy(h)
 
     @property
     def handle(self):
