@@ -97,6 +97,11 @@ class _Models:
         return out
 
 
+def build_requests_for(wf: Workflow, pattern: str, rate: float, duration_s: float, seed: int) -> list:
+    from .workload import build_requests, gen_workload
+    return build_requests(wf, gen_workload(pattern, rate, duration_s, seed), seed)
+
+
 class Runtime:
     def __init__(self, tube, compute: str = "sleep", workers: int = 32):
         self.tube = tube
@@ -218,6 +223,50 @@ class Runtime:
         warm = [(wf, where, [r for r in reqs if r.arrival_ms < seconds * 1e3]) for wf, where, reqs in jobs]
         Runtime(tube, compute=compute).run(warm, seconds, drain_s=60)
 
+    @staticmethod
+    def max_throughput(tube, wf, where, pattern: str = "sporadic", duration_s: float = 1.0,
+                       compute: str = "sleep", rate_lo: float = 1.0, rate_hi: float = 256.0,
+                       iterations: int = 4, seed: int = 0, slo_ms: float | None = None) -> dict:
+        """harness.max_throughput (harness.py:383-428) on the live runtime: the
+        highest offered rate whose p99 stays within the workflow SLO with >= 95%
+        of the offered requests completed — doubling from ``rate_lo``, then
+        ``iterations`` bisection steps. Each trial replays the reference's trace
+        for that rate on ``tube`` (a warm daemon)."""
+        slo = slo_ms if slo_ms else (wf.slo_ms or 1e12)
+        trials = []
+
+        def trial(rate):
+            reqs = build_requests_for(wf, pattern, rate, duration_s, seed)
+            rt = Runtime(tube, compute=compute)
+            rep = rt.run([(wf, where, reqs)], duration_s, drain_s=30, idle_s=0.0)
+            ok = not reqs or (rep["requests_completed"] >= 0.95 * len(reqs) and rep.get("p99_ms") is not None
+                              and rep["p99_ms"] <= slo)       # no arrival drawn: vacuously met
+            trials.append({"rate": round(rate, 3), "ok": ok, "p99_ms": rep.get("p99_ms"),
+                           "completed": rep["requests_completed"], "offered": len(reqs)})
+            return ok, rep
+
+        lo, hi, last = 0.0, None, None
+        rate = rate_lo
+        while rate <= rate_hi:
+            ok, rep = trial(rate)
+            if not ok:
+                hi = rate
+                break
+            lo, last = rate, rep
+            rate *= 2
+        if lo == 0.0:
+            return {"max_rps": 0.0, "slo_ms": slo, "trials": trials, "diagnostic": "SLO unachievable at the lowest rate"}
+        if hi is not None:
+            for _ in range(iterations):
+                mid = (lo + hi) / 2
+                ok, rep = trial(mid)
+                if ok:
+                    lo, last = mid, rep
+                else:
+                    hi = mid
+        return {"max_rps": round(lo, 3), "slo_ms": round(slo, 3), "p99_ms_at_max": last.get("p99_ms"),
+                "trials": trials}
+
     def run(self, jobs: list, duration_s: float, drain_s: float = 30.0, sample_ms: float = 50.0,
             idle_s: float = 1.0) -> dict:
         """jobs: [(workflow, placement, [Request])]; arrivals replayed in real time.
@@ -294,7 +343,8 @@ class Runtime:
             self.tube.maintain()
             time.sleep(0.05)
         self.tube.maintain()
-        self.tube.reclaim()                  # quiet now: physical memory of dropped blocks goes back
+        if idle_s > 0:
+            self.tube.reclaim()              # quiet now: physical memory of dropped blocks goes back
         out["pool_after_idle_bytes"] = sum(p.stats()["policy_pool_bytes"] for p in self.tube.pools.values())
         out["mapped_after_idle_bytes"] = sum(p.stats()["mapped_bytes"] for p in self.tube.pools.values())
         return out

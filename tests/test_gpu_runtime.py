@@ -35,3 +35,22 @@ def test_yelp_runs_and_beats_host_oriented():
 def test_traffic_with_models():
     out, n = _run("faastube", preset="traffic", rate=5.0, dur=1.0, compute="model")
     assert out["errors"] == [] and out["requests_completed"] == n, out
+
+
+def test_max_throughput_search_live():
+    """harness.max_throughput (harness.py:383-428) on the live runtime: doubling
+    then bisection; the answer is a rate whose trial met the SLO."""
+    from paper_2411_01830_b200 import workload
+    from paper_2411_01830_b200.runtime import Runtime
+    from paper_2411_01830_b200.tube import FaaSTube
+    tube = FaaSTube("faastube")
+    wf = workload.preset_workflow("yelp")
+    where = workload.place(wf, tube.topo, {}, colocate=tube.topo.gpu_count < len(wf.gfuncs()))
+    workload.calibrate_slo(wf, tube.topo, where, 1.5)
+    res = Runtime.max_throughput(tube, wf, where, "sporadic", 1.0, "sleep", rate_lo=1.0, rate_hi=8.0,
+                                 iterations=1, slo_ms=10_000.0)
+    tube.close()
+    assert res["max_rps"] >= 1.0, res
+    ok_rates = [t["rate"] for t in res["trials"] if t["ok"]]
+    assert res["max_rps"] in ok_rates and all(t["ok"] == (t["p99_ms"] is None or t["p99_ms"] <= 10_000.0)
+                                              or t["completed"] < 0.95 * t["offered"] for t in res["trials"])

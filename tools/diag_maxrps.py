@@ -1,0 +1,7 @@
+import json, os, sys, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import bench
+t0 = time.time()
+out = bench.run_workflows()
+print(json.dumps(out["config4_max_throughput"]))
+print("wall", time.time() - t0)
