@@ -194,6 +194,7 @@ struct ft_pacer {
   double last_issue_t[2][kMaxDev] = {};
   uint64_t last_issue_ticket[2][kMaxDev] = {};
   bool adapt = true;
+  uint64_t timed_skip = 0;
   std::map<int, StagingRing> rings;
   std::map<std::string, double> guarded;  // last early boundary per stage key (A2 guard)
   uint64_t n_stages = 0, n_managed = 0, n_batches = 0, n_bytes = 0, n_errors = 0;
@@ -352,8 +353,10 @@ struct ft_pacer {
     Route& r = st.routes[i];
     uint64_t o = r.off + rel;
     if (st.pinned) {
-      if (track && !r.staged() && n) {
-        // direct route: bracket the DMA with timing events (service-rate sample)
+      if (track && !r.staged() && n && (samples[st.dir][r.dev].size() < 6 || ++timed_skip % 8 == 0)) {
+        // direct route: bracket the DMA with timing events (service-rate sample) —
+        // every batch until the estimator has its window, then every 8th (a timed
+        // event between two DMAs costs copy-engine time)
         DevGuard g(r.dev);
         Timing tm{get_tevent(r.dev), nullptr, st.dir, r.dev, n, now(), link_busy(st.dir, r.dev, st.ticket)};
         ck(cudaEventRecord(tm.t0, r.ce), "record t0");

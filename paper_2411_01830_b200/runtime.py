@@ -89,7 +89,7 @@ class _Models:
             for w in self.rec:
                 h = F.relu(F.conv2d(h, w, padding=1, stride=2))
         flat = h.reshape(-1).view(torch.uint8)
-        out = torch.empty(out_bytes, dtype=torch.uint8, device=x.device)
+        out = dev.empty_shared(out_bytes, x.device.index)
         k = min(out_bytes, flat.numel())
         out[:k] = flat[:k]
         if k < out_bytes:
@@ -131,7 +131,7 @@ class Runtime:
                 self.models[gpu] = _Models(f"cuda:{gpu}")
             return self.models[gpu].run(fid, x, out_bytes)
         dev.LIB.ft_spin_ns(int(ms * 1e6), int(gpu), C.c_void_p(torch.cuda.current_stream(gpu).cuda_stream))
-        return torch.empty(out_bytes, dtype=torch.uint8, device=f"cuda:{gpu}").fill_(len(fid) & 0xFF)
+        return dev.empty_shared(out_bytes, gpu).fill_(len(fid) & 0xFF)
 
     def _stream(self, gpu) -> torch.cuda.Stream:
         """This worker thread's own stream on ``gpu`` (a function's CUDA context):

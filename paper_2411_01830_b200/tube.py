@@ -711,7 +711,7 @@ class FaaSTube:
     def _out(self, obj, gpu, out):
         if out is not None:
             return out
-        return torch.empty(obj.nbytes, dtype=torch.uint8, device=f"cuda:{gpu}").view(obj.dtype).view(obj.shape)
+        return dev.empty_shared(obj.nbytes, gpu).view(obj.dtype).view(obj.shape)
 
     def _inter_gpu(self, obj, plan, src, dst, out):
         res = self._out(obj, dst.gpu, out)

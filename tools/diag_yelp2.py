@@ -8,11 +8,12 @@ from paper_2411_01830_b200 import workload, device
 from paper_2411_01830_b200.runtime import Runtime
 from paper_2411_01830_b200.tube import FaaSTube
 if len(sys.argv) > 1 and sys.argv[1] == "pre":
-    import test_gpu_pacer as P
-    P.test_concurrent_stages_share_staging_ring(device)
-    P.test_submit_returns_before_landing(device)
-    P.test_back_to_back_loose_stages_do_not_starve(device)
-    print("pre done", flush=True)
+    import subprocess
+    # run the GPU test files that precede test_gpu_runtime, in this process
+    import pytest
+    rc = pytest.main(["-q", "-m", "gpu", "-x", "tests/test_gpu_ipc.py", "tests/test_gpu_migration.py",
+                      "tests/test_gpu_movers.py", "tests/test_gpu_pacer.py", "tests/test_gpu_pairs.py"])
+    print("pre done", rc, flush=True)
 import threading, functools
 from paper_2411_01830_b200 import tube as tube_mod, runtime as rt_mod
 marks = []
@@ -36,6 +37,7 @@ _sync = torch.cuda.Stream.synchronize
 torch.cuda.Stream.synchronize = timed("stream.sync", _sync)
 for strategy in ("faastube", "infless_plus", "faastube"):
     marks.clear()
+    print("pinned cache / torch mem", torch.cuda.memory_reserved() >> 20, "MiB reserved", flush=True)
     tube = FaaSTube(strategy)
     wf = workload.preset_workflow("yelp")
     where = workload.place(wf, tube.topo, {}, colocate=True)
