@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-sample-s", type=float, default=10.0)
     ap.add_argument("--no-extras", action="store_true")
+    ap.add_argument("--max-throughput", action="store_true",
+                    help="also search config 4's max req/s per strategy (harness.max_throughput; minutes)")
     return ap.parse_args()
 
 
@@ -327,7 +329,7 @@ def run_ours(args):
     total_ms_max, e2e_max = t_tensor.tolist()
     value = world * args.steps * nbytes / (total_ms_max * 1e-3) / 1e9
 
-    extras = {} if args.no_extras or rank != 0 else run_extras(tube, g, dev, torch)
+    extras = {} if args.no_extras or rank != 0 else run_extras(tube, g, dev, torch, args.max_throughput)
 
     if rank == 0:
         cpu = cpu_host_path(args.cpu_sample_s, nbytes) if world == 1 else None
@@ -382,7 +384,7 @@ def _single_gpu_topology(g):
     return build_preset("b200", n_gpus=g + 1)
 
 
-def run_extras(tube, g, dev, torch):
+def run_extras(tube, g, dev, torch, max_throughput=False):
     out = {}
     # config 2 at k = 1: 1 GiB pinned -> GPU through tube.fetch vs the live CE peak
     n = 1 << 30
@@ -535,13 +537,13 @@ def run_extras(tube, g, dev, torch):
     out["g2g_same_gpu_sweep"] = sweep
     out["g2g_same_gpu_sweep_store_cap_bytes"] = 64e9
     try:
-        out.update(run_workflows())
+        out.update(run_workflows(max_throughput=max_throughput))
     except Exception as exc:  # noqa: BLE001 - extras never hide the headline line
         out["workflows_error"] = repr(exc)
     return out
 
 
-def run_workflows(dur_s=2.0):
+def run_workflows(dur_s=2.0, max_throughput=False, trial_s=10.0):
     """Configs 4 and 5 on the live runtime (one GPU): the reference's traces,
     placement and SLOs; FaaSTube vs the INFless+ host-memory baseline."""
     from paper_2411_01830_b200 import workload
@@ -593,40 +595,30 @@ def run_workflows(dur_s=2.0):
                                           "bursty 10 rps, random-init conv models on synthetic 1080p frames; "
                                           "warm daemon (0.5 s untimed warm-up trace per strategy)",
                               "faastube": t4["faastube"], "infless_plus": t4["infless_plus"]}
-    def max_rps(strategy, slo=None):
+    def max_rps(strategy):
         # harness.max_throughput (harness.py:383-428) on the live runtime: highest Poisson
-        # rate whose p99 meets the SLO with >= 95% completed; reference compute model.
-        # SLO = 1.5 x the unloaded runtime (harness.py:198-208) — measured live under
-        # FaaSTube (periodic requests that never overlap), the same SLO for both strategies
-        from paper_2411_01830_b200.runtime import build_requests_for
+        # rate whose p99 meets the workflow SLO (harness.calibrate_slo: 1.5 x the modelled
+        # unloaded runtime, the same for both strategies) with >= 95% completed; the
+        # reference compute model (each gFunc occupies its GPU for compute_latency_ms)
         tube = FaaSTube(strategy)
         wf = workload.preset_workflow("traffic")
         where = workload.place(wf, tube.topo, {}, colocate=tube.topo.gpu_count < len(wf.gfuncs()))
         workload.calibrate_slo(wf, tube.topo, where, 1.5)
-        Runtime.warm_daemon(tube, [(wf, where, build_requests_for(wf, "sporadic", 8.0, 0.5, 0))], "sleep", 0.5)
-        unloaded = None
-        if slo is None:
-            solo = Runtime(tube, compute="sleep").run(
-                [(wf, where, build_requests_for(wf, "periodic", 4.0, 2.0, 1))], 2.0, drain_s=30, idle_s=0.0)
-            unloaded = solo["p50_ms"]
-            slo = 1.5 * unloaded
         t0 = time.perf_counter()
-        res = Runtime.max_throughput(tube, wf, where, "sporadic", 3.0, "sleep", rate_lo=1.0, rate_hi=512.0,
-                                     slo_ms=slo)
+        res = Runtime.max_throughput(tube, wf, where, "sporadic", trial_s, "sleep", rate_lo=1.0, rate_hi=512.0)
         res["wall_s"] = round(time.perf_counter() - t0, 2)
-        if unloaded is not None:
-            res["unloaded_ms"] = unloaded
         tube.close()
         return res
 
-    mt = {"faastube": max_rps("faastube")}
-    mt["infless_plus"] = max_rps("infless_plus", mt["faastube"]["slo_ms"])
-    out["config4_max_throughput"] = {
-        "workload": "traffic DAG, Poisson arrivals, reference compute model (compute_latency_ms per gFunc), "
-                    "SLO = 1.5 x live unloaded runtime under FaaSTube; binary search as harness.max_throughput",
-        "faastube": mt["faastube"], "infless_plus": mt["infless_plus"],
-        "gain": round(mt["faastube"]["max_rps"] / mt["infless_plus"]["max_rps"], 3)
-        if mt["infless_plus"]["max_rps"] else None}
+    mt = {s: max_rps(s) for s in ("faastube", "infless_plus")} if max_throughput else None
+    if mt:
+        out["config4_max_throughput"] = {
+            "workload": "traffic DAG, Poisson arrivals, reference compute model (compute_latency_ms per gFunc), "
+                        "SLO = 1.5 x modelled unloaded runtime (harness.calibrate_slo); binary search as "
+                        "harness.max_throughput; each trial after an untimed warm-up at its rate",
+            "faastube": mt["faastube"], "infless_plus": mt["infless_plus"],
+            "gain": round(mt["faastube"]["max_rps"] / mt["infless_plus"]["max_rps"], 3)
+            if mt["infless_plus"]["max_rps"] else None}
     t5 = {s: one(s, pairs, "sleep") for s in ("faastube", "infless_plus")}
     out["config5_multitenant"] = {"workload": "16 functions = 8 producer->consumer pairs, edges 1..512 MB, bursty "
                                               "5 rps each, elastic VMM pool (floor 300 MB)",

@@ -237,6 +237,10 @@ class Runtime:
 
         def trial(rate):
             reqs = build_requests_for(wf, pattern, rate, duration_s, seed)
+            # a daemon that has been serving this rate: replay the trace's first
+            # requests untimed (the pool may have shrunk while the previous trial drained)
+            Runtime.warm_daemon(tube, [(wf, where, build_requests_for(wf, pattern, max(rate, 4.0), 0.5, seed + 1))],
+                                compute, 0.5)
             rt = Runtime(tube, compute=compute)
             rep = rt.run([(wf, where, reqs)], duration_s, drain_s=30, idle_s=0.0)
             ok = not reqs or (rep["requests_completed"] >= 0.95 * len(reqs) and rep.get("p99_ms") is not None
