@@ -310,7 +310,15 @@ class DevicePool:
                     self.grow_events += 1
             if m is None:
                 vid, ptr = C.c_uint64(), C.c_void_p()
-                LIB.ft_vmm_block_map(self._h, int(b.class_bytes), C.byref(vid), C.byref(ptr))
+                try:
+                    LIB.ft_vmm_block_map(self._h, int(b.class_bytes), C.byref(vid), C.byref(ptr))
+                except MemoryError:
+                    # physical pressure: give parked blocks back, then try once more
+                    if not self.reclaim():
+                        with self._lock:
+                            self.policy.free(b)
+                        raise
+                    LIB.ft_vmm_block_map(self._h, int(b.class_bytes), C.byref(vid), C.byref(ptr))
                 with self._lock:
                     m = self._mapped[b.block_id] = (vid.value, ptr.value, b.class_bytes)
                     self.grow_events += 1

@@ -55,8 +55,11 @@ _ALIGN = 256  # stripe boundaries (bytes)
 _L2_KEEP = 96 << 20  # stored blocks up to this size stay L2-resident (126 MB L2) for the next fetch
 SHRINK_MIN_GAP_MS = 2.0
 # dropped pool blocks are unmapped only after this long without a store/fetch:
-# cuMemUnmap while the GPU is busy stalls every CUDA call of the process (0.3-1 s measured)
-RECLAIM_IDLE_MS = 1000.0
+# cuMemUnmap while the GPU is busy stalls every CUDA call of the process (0.3-1 s
+# measured; at 1 req/s a 1 s threshold fired between requests and stalled the next
+# one for 0.7 s). Until then they stay mapped, reused by growth of their class, and a
+# failed physical allocation reclaims them first (memory pressure)
+RECLAIM_IDLE_MS = 10000.0
 
 
 class _Obj:
