@@ -259,7 +259,7 @@ class DevicePool:
 
     def __init__(self, device: int, mode: str = "autoscale", floor_bytes: float = datastore.POOL_FLOOR_BYTES,
                  native_alloc_ms: float = datastore.NATIVE_ALLOC_MS, va_bytes: int = 256 * GiB,
-                 physical_bytes: float | None = None):
+                 physical_bytes: float | None = None, spare_cap_bytes: int = 4 * GiB):
         require_cuda()
         self.device = device
         if physical_bytes is None:
@@ -277,13 +277,65 @@ class DevicePool:
         self._released = []  # [(vmm id, ptr, bytes, fences)]
         self._lock = threading.Lock()
         self.grow_events = 0
+        # spares: after growth of a class, a background thread maps one more block of
+        # that class into the parked list, so the next growth of the class is a reuse.
+        # cuMemMap waits for the GPU's running kernels (measured 30-80 ms while tenants
+        # compute) — a cost for this thread, not for the request that needs the block
+        self.spare_cap_bytes = spare_cap_bytes
+        self._spare_q = []
+        self._spare_cv = threading.Condition(self._lock)
+        self._spare_thread = None
+        self.spares_mapped = 0
 
     def close(self):
         h = getattr(self, "_h", None)
         if h:
+            th = self._spare_thread
+            with self._lock:
+                self._spare_q = None                   # stops the spare thread
+                self._spare_cv.notify_all()
+            if th is not None:
+                th.join(timeout=10)
             torch.cuda.synchronize(self.device)
             LIB.ft_vmm_pool_destroy(h)
             self._h = None
+
+    # ---- spare mappings (background growth)
+    def _want_spare(self, class_bytes: int):
+        """Called with the lock held after a growth of ``class_bytes``."""
+        if self._spare_q is None or self.spare_cap_bytes <= 0:
+            return
+        parked = sum(r[2] for r in self._released)
+        if parked + class_bytes > self.spare_cap_bytes:
+            return
+        if any(r[2] == class_bytes for r in self._released) or class_bytes in self._spare_q:
+            return
+        self._spare_q.append(class_bytes)
+        if self._spare_thread is None:
+            self._spare_thread = threading.Thread(target=self._spare_loop, name=f"faastube-spares{self.device}",
+                                                  daemon=True)
+            self._spare_thread.start()
+        self._spare_cv.notify()
+
+    def _spare_loop(self):
+        torch.cuda.set_device(self.device)
+        while True:
+            with self._lock:
+                while self._spare_q is not None and not self._spare_q:
+                    self._spare_cv.wait()
+                if self._spare_q is None:
+                    return
+                cls = self._spare_q.pop(0)
+            vid, ptr = C.c_uint64(), C.c_void_p()
+            try:
+                LIB.ft_vmm_block_map(self._h, int(cls), C.byref(vid), C.byref(ptr))
+            except Exception:  # noqa: BLE001 - a spare is an optimisation; pressure wins
+                continue
+            with self._lock:
+                if self._spare_q is None:            # closing: the pool unmaps everything
+                    return
+                self._released.append((vid.value, ptr.value, int(cls), ()))
+                self.spares_mapped += 1
 
     def __del__(self):
         try:
@@ -302,12 +354,16 @@ class DevicePool:
             fences = self._fences.pop(b.block_id, ())
         if m is None:
             with self._lock:
-                reuse = next((i for i, r in enumerate(self._released) if r[2] == b.class_bytes), None)
-                if reuse is not None:          # growth served by a dropped, still-mapped block
+                # growth served by a dropped, still-mapped block: the smallest one that fits
+                # (at most 2x — the policy still accounts the class it asked for)
+                fits = [(r[2], i) for i, r in enumerate(self._released) if b.class_bytes <= r[2] <= 2 * b.class_bytes]
+                reuse = min(fits)[1] if fits else None
+                if reuse is not None:
                     vid, ptr, nb, rf = self._released.pop(reuse)
                     m = self._mapped[b.block_id] = (vid, ptr, nb)
                     fences = tuple(fences) + tuple(rf)
                     self.grow_events += 1
+                    self._want_spare(int(b.class_bytes))
             if m is None:
                 vid, ptr = C.c_uint64(), C.c_void_p()
                 try:
@@ -322,6 +378,7 @@ class DevicePool:
                 with self._lock:
                     m = self._mapped[b.block_id] = (vid.value, ptr.value, b.class_bytes)
                     self.grow_events += 1
+                    self._want_spare(int(b.class_bytes))
         return PoolBlock(b, m[0], m[1], m[2], self.device, fences, self)
 
     def base_tensor(self, blk: PoolBlock) -> torch.Tensor:
