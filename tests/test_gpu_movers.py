@@ -102,7 +102,7 @@ def test_h2g_striped_staging_route(dev):
 
 
 def test_vmm_pool_map_unmap(dev):
-    pool = dev.DevicePool(0, "autoscale", floor_bytes=0.0)
+    pool = dev.DevicePool(0, "autoscale", floor_bytes=0.0, spare_cap_bytes=0)   # exact physical accounting
     blocks = [pool.allocate(n) for n in (1, 2 * 10**6, 64 << 20, 3 * 10**6)]
     for i, b in enumerate(blocks):
         t = dev.as_tensor(b.ptr, b.nbytes, 0)
@@ -177,3 +177,26 @@ def test_copy_batch_segments(dev):
     for d, x, n, sh, sh2 in zip(dsts, srcs, sizes, shifts, reversed(shifts)):
         assert torch.equal(d[sh:sh + n], x[sh2:sh2 + n])
         assert not d[:sh].any() and not d[sh + n:].any()
+
+
+def test_pool_spares_serve_growth(dev):
+    """After a growth of a class, a background thread maps one spare of it; the
+    next growth of that class (the policy's new block) is served by the spare,
+    and the bytes are the new holder's (fenced, writable)."""
+    import time
+    pool = dev.DevicePool(0, "autoscale", floor_bytes=0.0)
+    a = pool.allocate(32 << 20)
+    deadline = time.time() + 5
+    while pool.spares_mapped < 1 and time.time() < deadline:
+        time.sleep(0.01)
+    assert pool.spares_mapped == 1 and pool.released_bytes >= 32 << 20
+    blocks_before = pool.stats()["blocks"]
+    b = pool.allocate(32 << 20)                     # growth: a second live block of the class
+    assert b.ptr != a.ptr and pool.stats()["blocks"] in (blocks_before, blocks_before + 1)
+    t = dev.as_tensor(b.ptr, 32 << 20, 0)
+    t.fill_(9)
+    torch.cuda.synchronize()
+    assert int(t.float().mean()) == 9
+    pool.free(a)
+    pool.free(b)
+    pool.close()
