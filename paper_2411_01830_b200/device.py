@@ -17,6 +17,7 @@ kernels or on the copy engines.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import threading
 import weakref
 
@@ -281,7 +282,7 @@ class DevicePool:
         # that class into the parked list, so the next growth of the class is a reuse.
         # cuMemMap waits for the GPU's running kernels (measured 30-80 ms while tenants
         # compute) — a cost for this thread, not for the request that needs the block
-        self.spare_cap_bytes = spare_cap_bytes
+        self.spare_cap_bytes = int(os.environ.get("FT_SPARE_CAP_BYTES", spare_cap_bytes))
         self._spare_q = []
         self._spare_cv = threading.Condition(self._lock)
         self._spare_thread = None

@@ -102,13 +102,25 @@ def build_requests_for(wf: Workflow, pattern: str, rate: float, duration_s: floa
     return build_requests(wf, gen_workload(pattern, rate, duration_s, seed), seed)
 
 
+_MODELS = {}
+_MODELS_LOCK = threading.Lock()
+
+
+def _models(gpu: int) -> "_Models":
+    """One set of random-init stand-in models per GPU for the process (fixed seed)."""
+    with _MODELS_LOCK:
+        m = _MODELS.get(gpu)
+        if m is None:
+            m = _MODELS[gpu] = _Models(f"cuda:{gpu}")
+        return m
+
+
 class Runtime:
     def __init__(self, tube, compute: str = "sleep", workers: int = 32):
         self.tube = tube
         self.compute = compute
         self.pool = ThreadPoolExecutor(workers)
         self.gpu_locks = {g: threading.Lock() for g in tube.gpus}
-        self.models = {}
         self._host_bufs = {}
         self.records: list[Record] = []
         self._rec_lock = threading.Lock()
@@ -127,9 +139,7 @@ class Runtime:
 
     def _compute(self, fid, gpu, ms, x, out_bytes):
         if self.compute == "model":
-            if gpu not in self.models:
-                self.models[gpu] = _Models(f"cuda:{gpu}")
-            return self.models[gpu].run(fid, x, out_bytes)
+            return _models(gpu).run(fid, x, out_bytes)
         dev.LIB.ft_spin_ns(int(ms * 1e6), int(gpu), C.c_void_p(torch.cuda.current_stream(gpu).cuda_stream))
         return dev.empty_shared(out_bytes, gpu).fill_(len(fid) & 0xFF)
 
@@ -288,10 +298,25 @@ class Runtime:
     def _run(self, jobs, duration_s, drain_s, sample_ms, idle_s) -> dict:
         events = sorted(((r.arrival_ms, i, wf, where, r) for i, (wf, where, reqs) in enumerate(jobs) for r in reqs),
                         key=lambda e: (e[0], e[1], e[4].rid))
-        # warm-up outside the trace: spin up every worker thread's CUDA state and
-        # run one request per workflow (pool blocks, pinned buffers, kernels loaded)
-        list(self.pool.map(lambda _: torch.cuda.current_stream(self.tube.gpus[0]).synchronize(),
-                           range(self.pool._max_workers)))  # noqa: SLF001
+        # warm-up outside the trace: every worker thread sets up its CUDA state — its
+        # streams and, with model compute, its cuDNN/cuBLAS handles and workspaces (per
+        # thread in torch: a worker's first conv otherwise costs 0.3-2 s inside the trace)
+        n_workers = self.pool._max_workers  # noqa: SLF001
+        barrier = threading.Barrier(n_workers)
+        gfuncs = sorted({(fid, g) for _, where, _ in jobs for fid, (kind, g) in where.items() if kind == "gpu"})
+
+        def warm_worker(_):
+            barrier.wait(timeout=60)         # one task per worker thread
+            for g in self.tube.gpus:
+                with torch.cuda.stream(self._stream(g)):
+                    if self.compute == "model":
+                        for fid, fg in gfuncs:
+                            if fg == g:
+                                self._compute(fid, g, 0.0, torch.zeros(1 << 20, dtype=torch.uint8,
+                                                                       device=f"cuda:{g}"), 1 << 20)
+                    torch.cuda.current_stream(g).synchronize()
+
+        list(self.pool.map(warm_worker, range(n_workers)))
         for wf, where, reqs in jobs:
             if reqs:
                 r0 = reqs[0]

@@ -1,1 +1,2 @@
-for i in 1 2 3; do timeout -k 10 200 python tools/diag_slow1.py > gpurun_out/diag_slow1_$i.txt 2>&1; done
+timeout -k 10 300 python tools/diag_cfg5.py c4 > gpurun_out/diag_c4_spares.txt 2>&1
+FT_SPARE_CAP_BYTES=0 timeout -k 10 300 python tools/diag_cfg5.py c4 > gpurun_out/diag_c4_nospares.txt 2>&1

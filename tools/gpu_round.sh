@@ -13,3 +13,4 @@ timeout -k 10 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$T.csv python bench.py --steps 3 --warmup 3 --no-extras --cpu-sample-s 1 > gpurun_out/ncu_bench_$T.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_copy_bulk -s 2 -c 2 -o gpurun_out/prof_copy_$T python tools/prof_copy.py > gpurun_out/ncu_copy_$T.log 2>&1
 ls -la gpurun_out
+timeout -k 10 1200 python tools/diag_maxrps.py 10 > gpurun_out/maxrps_$T.txt 2>&1
