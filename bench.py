@@ -198,7 +198,13 @@ def run_ours(args):
     from paper_2411_01830_b200 import device as dev
     from paper_2411_01830_b200.tube import FaaSTube
 
-    tube = FaaSTube("faastube", topology=_single_gpu_topology(g) if world > 1 else None, gpus=[g])
+    if world > 1:
+        # one process per GPU, each driving only its own GPU: its host->GPU legs use its own
+        # PCIe root (replicas; no striping through GPUs another rank drives)
+        from paper_2411_01830_b200.strategies import strategy_preset
+        tube = FaaSTube(strategy_preset("faastube", parallel_pcie=False), topology=_single_gpu_topology(g), gpus=[g])
+    else:
+        tube = FaaSTube("faastube")            # drives every visible GPU: H2G stripes over all their roots
     gen = torch.Generator(device="cpu").manual_seed(0)
     x = torch.randn(PAYLOAD_SHAPE, generator=gen).half().to(f"cuda:{g}")   # producer output (in HBM)
     nbytes = x.nbytes

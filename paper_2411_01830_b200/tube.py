@@ -638,6 +638,9 @@ class FaaSTube:
         routes = []
         for b, (off, n) in zip(br, ranges):
             sg = _staging_gpu_d2h(b.links, g)
+            if sg not in self._d2h_pairs:
+                from ._lib import NotSupported
+                raise NotSupported(f"the plan routes through GPU {sg}, which this tube does not drive")
             ce, fw = self._d2h_pairs[sg][slot % len(self._d2h_pairs[sg])]
             routes.append((sg, 0, off, n, ce.cuda_stream, fw.cuda_stream))
             if sg != g:
@@ -784,7 +787,10 @@ class FaaSTube:
             obj.readers.append(ev)
 
     def _pair(self, g, slot=None):
-        pairs = self._ce_pairs[g]
+        pairs = self._ce_pairs.get(g)
+        if pairs is None:
+            from ._lib import NotSupported
+            raise NotSupported(f"the plan routes through GPU {g}, which this tube does not drive (gpus={self.gpus})")
         return pairs[(next(self._ce_rr) if slot is None else slot) % len(pairs)]
 
     def _host_to_gpu(self, obj, plan, dst, out, slo_ms, infer_ms):
