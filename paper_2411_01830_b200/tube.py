@@ -33,6 +33,7 @@ fetch has landed.
 
 from __future__ import annotations
 
+import collections
 import heapq
 import itertools
 import math
@@ -138,6 +139,8 @@ class FaaSTube:
         self._ce_rr = itertools.count()
         self._keepalive = []         # (event, buffers) released once the event has completed
         self._last_op_ms = 0.0       # last store/fetch (idle detection for physical reclaim)
+        self._live = collections.Counter()    # (producer, gpu) -> live objects (see _account)
+        self._stored = collections.Counter()  # gpu -> bytes of live objects in its store
         self._pending_release = []   # (event, plan): NVLink claims held until the copy lands
         self._shrink_due = []        # heap of (due_ms, gpu)
         self._managed_ids = itertools.count(1)
@@ -306,8 +309,7 @@ class FaaSTube:
                 obj.gpu = obj.home = g
                 pool = self.pools[g]
                 blk = getattr(t, "_ft_block", None)
-                live_here = sum(1 for o in self._objs.values() if o.producer == producer and o.gpu == g
-                                and not o.retired)
+                live_here = self._live[(producer, g)]     # this producer's live objects here
                 if blk is not None and blk.ptr == t.data_ptr():
                     obj.block = blk                      # zero-copy store of a pool-backed output
                     obj.ready = dev.Ev(g).record(self._stream(g))
@@ -363,6 +365,7 @@ class FaaSTube:
                 obj.host = host
                 self.index.store(data_id, self._loc(None), nbytes, now, producer, response)
             self._objs[data_id] = obj
+            self._account(obj, 1)
             self.stats["stores"] += 1
             if obj.block is not None and self.strategy.migration != "none" and \
                     self._stored_on(obj.gpu) > self.capacity_limit:
@@ -371,7 +374,27 @@ class FaaSTube:
 
     # ------------------------------------------------ queue-aware migration (§8f row 1)
     def _stored_on(self, g) -> int:
-        return sum(o.nbytes for o in self._objs.values() if o.block is not None and o.gpu == g)
+        """Bytes of live objects held in GPU g's store (kept as a running sum)."""
+        return self._stored[g]
+
+    def _accounts_consistent(self) -> bool:
+        """The running counters equal a recount of the table (tests)."""
+        live, stored = collections.Counter(), collections.Counter()
+        for o in self._objs.values():
+            if o.gpu is not None:
+                live[(o.producer, o.gpu)] += 1
+                if o.block is not None:
+                    stored[o.gpu] += o.nbytes
+        return (+self._live == +live) and (+self._stored == +stored)
+
+    def _account(self, o: _Obj, sign: int):
+        """Running per-(producer, GPU) live counts and per-GPU stored bytes of the
+        objects in the table (the policy's concurrency samples and the store cap
+        check read them on every store instead of scanning the table)."""
+        if o.gpu is not None:
+            self._live[(o.producer, o.gpu)] += sign
+            if o.block is not None:
+                self._stored[o.gpu] += sign * o.nbytes
 
     def _policy_objs(self, g):
         from .datastore import StoredObject
@@ -408,10 +431,12 @@ class FaaSTube:
         o.ready.wait(ce)
         dev.pcie_copy(host.data_ptr(), o.block.ptr, o.nbytes, False, g, ce)
         ev = dev.Ev(g).record(ce)
+        self._account(o, -1)
         blk, o.block = o.block, None
         self.pools[g].free(blk, [ev] + o.readers)            # later writers of the block wait for the D2H
         o.readers = []
         o.host, o.ready, o.gpu = host, ev, None
+        self._account(o, 1)
         self.index.relocate(o.did, self._loc(None))
         self.stats["migrated_bytes"] += o.nbytes
         self.stats["bytes_d2h"] += o.nbytes
@@ -437,7 +462,9 @@ class FaaSTube:
             blk.wait_fences(ce)
             dev.pcie_copy(blk.ptr, o.host.data_ptr(), o.nbytes, True, g, ce)
             ev = dev.Ev(g).record(ce)
+            self._account(o, -1)
             o.block, o.ready, o.gpu, o.host = blk, ev, g, None
+            self._account(o, 1)
             self.index.relocate(o.did, self._loc(g))
             self.stats["reload_bytes"] += o.nbytes
             self.stats["bytes_h2d"] += o.nbytes
@@ -662,7 +689,8 @@ class FaaSTube:
             return
         obj.retired = True
         self.index.drop(obj.did)
-        self._objs.pop(obj.did, None)
+        if self._objs.pop(obj.did, None) is not None:
+            self._account(obj, -1)
         self._maybe_free(obj)
 
     def _maybe_free(self, obj: _Obj):

@@ -32,6 +32,7 @@ def test_migrate_then_prefetch_bit_exact():
     torch.cuda.synchronize()
     for g, x in zip((got0, got1, got2), xs):
         assert torch.equal(g, x)
+    assert tube._accounts_consistent()
     tube.close()
 
 
@@ -50,4 +51,5 @@ def test_lru_policy_evicts_oldest():
     got = tube.fetch(ids[0], device=0, out=torch.empty_like(xs[0]))        # served from host memory
     torch.cuda.synchronize()
     assert torch.equal(got, xs[0])
+    assert tube._accounts_consistent()
     tube.close()

@@ -17,6 +17,7 @@ def tube():
     from paper_2411_01830_b200.tube import FaaSTube
     t = FaaSTube("faastube", pool_floor_bytes=0.0)
     yield t
+    assert t._accounts_consistent()
     t.close()
 
 
