@@ -220,3 +220,30 @@ def test_managed_response_and_host_fetch():
         assert torch.equal(got.reshape(-1).view(torch.uint8), x.cpu())
     assert t.pacer.stats()["managed_stages"] == before + 4
     t.close()
+
+
+def test_inter_gpu_paths_on_one_gpu(tube):
+    """The cross-GPU fetch executor driven on one GPU with hand-built plans
+    (src == dst GPU): a striped GPU-oriented plan (a direct NVLink-pull branch
+    and a 2-hop relay branch, fractional shares) and the host-oriented
+    two-stage plan (D2H then H2D, dataplane.py:265-272) — bytes exact, source
+    block fenced by its readers."""
+    from types import SimpleNamespace
+    from paper_2411_01830_b200.dataplane import Branch, Location, Stage
+    n = (20 << 20) + 123
+    x = torch.randint(0, 256, (n,), dtype=torch.uint8, device="cuda:0")
+    for stages in ([Stage([Branch([("nv", 0, 0)], n * 0.37), Branch([("nv", 0, 0), ("nv", 0, 0)], n * 0.63)])],
+                   [Stage([Branch([("d2h", 0, 0)], float(n))]), Stage([Branch([("h2d", 0, 0)], float(n))])]):
+        d = tube.unique_id()
+        tube.store(d, x, producer="p")
+        obj = tube._objs[d]
+        plan = SimpleNamespace(method="inter_gpu", stages=stages, claimed_func=None)
+        out = torch.zeros_like(x)
+        with tube._lock:
+            res = tube._inter_gpu(obj, plan, Location(0, 0), Location(0, 0), out)
+        digest = res.to(torch.int64).sum()        # ordered after the transfer on the consumer stream
+        torch.cuda.synchronize()
+        assert torch.equal(res, x) and int(digest) == int(x.to(torch.int64).sum())
+        assert obj.readers                        # the source block is fenced by the pull / D2H
+        tube.release(d)
+    tube.maintain()
