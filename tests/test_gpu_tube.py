@@ -247,3 +247,38 @@ def test_inter_gpu_paths_on_one_gpu(tube):
         assert obj.readers                        # the source block is fenced by the pull / D2H
         tube.release(d)
     tube.maintain()
+
+
+def test_full_size_round_trips():
+    """BASELINE sizes through the public API: a 1 GiB host payload (config 2)
+    host -> GPU (managed pacer stage) -> store -> GPU -> host (managed d2h stage)
+    comes back bit-identical, and the device digest of the GPU copy equals the
+    host digest of the payload; the 64 MiB config-1 pass copy-fetch and
+    zero-copy view carry the same digest."""
+    from paper_2411_01830_b200 import device as dev
+    from paper_2411_01830_b200.tube import FaaSTube
+    t = FaaSTube("faastube", pool_floor_bytes=0.0, capacity_limit_bytes=64e9)
+    n = 1 << 30
+    host = torch.randint(0, 256, (n,), dtype=torch.uint8, device="cuda:0").cpu().pin_memory()
+    d = t.unique_id()
+    t.store(d, host, producer="gateway")
+    g = t.fetch(d, device=0, consumer="f")                        # H2G
+    fp = dev.Fingerprint(0)
+    fp.launch(g.data_ptr(), n, torch.cuda.current_stream(0))
+    assert fp.value() == dev.fingerprint_host(host)
+    d2 = t.unique_id()
+    t.store(d2, g, producer="f")
+    back = torch.empty(n, dtype=torch.uint8).pin_memory()
+    t.fetch(d2, device=None, out=back, consumer="sink")           # D2H
+    assert torch.equal(back, host)
+    x = payload(3)                                                # config 1: 64 MiB fp16
+    want = dev.fingerprint_host(x.cpu())
+    for zero_copy in (False, True):
+        d3 = t.unique_id()
+        t.store(d3, x, producer="p")
+        y = t.fetch(d3, device=0) if zero_copy else t.fetch(d3, out=torch.empty_like(x))
+        fp.launch(y.data_ptr(), y.nbytes, torch.cuda.current_stream(0))
+        assert fp.value() == want
+        del y
+    assert t._accounts_consistent()
+    t.close()
