@@ -52,3 +52,27 @@ def test_missing_library_is_loud(tmp_path, monkeypatch):
     monkeypatch.setattr(_lib, "LIB_PATH", str(tmp_path / "nope.so"))
     with pytest.raises(_lib.LibraryMissing):
         lib.load()
+
+
+def test_device_entry_points_fail_cleanly_without_a_gpu():
+    """Without a GPU every device entry point returns a status (raised as an
+    exception) — no crash, no CPU fallback: the pacer, raw streams/events,
+    batched copies and the VMM pool."""
+    import ctypes as C
+
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    from paper_2411_01830_b200._lib import LIB, FaasTubeError, RouteC, SegmentC
+    h = C.c_void_p()
+    for call in (lambda: LIB.ft_pacer_create(50.0, 1, 5, 2_000_000, 4, 0, 0, C.byref(h)),
+                 lambda: LIB.ft_stream_create(0, C.byref(h)),
+                 lambda: LIB.ft_event_create(0, C.byref(h)),
+                 lambda: LIB.ft_vmm_pool_create(0, 1 << 30, C.byref(h)),
+                 lambda: LIB.ft_copy_batch((SegmentC * 1)(SegmentC(None, None, 16)), 1, 0, None)):
+        with pytest.raises((FaasTubeError, RuntimeError, ValueError)):
+            call()
+    # argument validation happens before any device work
+    with pytest.raises(ValueError):
+        LIB.ft_pacer_submit(None, b"", 1, 1e9, 0.0, 50.0, None, 0, None, 16, 1, 1, (RouteC * 1)(), None,
+                            C.byref(C.c_uint64()))
