@@ -204,6 +204,14 @@ typedef struct {
 int ft_strategy_preset(const char* name, ft_strategy* out);
 
 typedef struct ft_index ft_index;
+/* request-path bookkeeping in one call each (the tube's hot path):
+ * store  = ft_index_store + ft_pool_policy_record + ft_pool_policy_hist
+ * retire = ft_index_drop + ft_pool_policy_free (block_id >= 0) + ft_pool_policy_hist */
+int ft_store_commit(ft_index* x, ft_pool_policy* p, int64_t data_id, int node, int gpu, double size_bytes,
+                    double now_ms, const char* producer, int response, double concurrency, double* r_window,
+                    double* last);
+int ft_retire_commit(ft_index* x, ft_pool_policy* p, int64_t data_id, int64_t block_id, const char* producer,
+                     double* r_window, double* last);
 /* DataIndex                                         dataplane.py:55-107 */
 int ft_index_create(double sync_period_ms, double local_lookup_ms, double global_lookup_ms, ft_index** out);
 void ft_index_destroy(ft_index* x);

@@ -240,6 +240,8 @@ _SIGS = {
     "ft_wait": (None, [vp, C.c_uint32, C.c_int, vp]),
     "ft_wait_timeout": (None, [vp, C.c_uint32, u64, vp, C.c_int, vp]),
     "ft_copy_batch": (None, [P(SegmentC), C.c_int, C.c_int, vp]),
+    "ft_store_commit": (None, [vp, vp, i64, C.c_int, C.c_int, dbl, dbl, cstr, C.c_int, dbl, P(dbl), P(dbl)]),
+    "ft_retire_commit": (None, [vp, vp, i64, i64, cstr, P(dbl), P(dbl)]),
     "ft_stream_create": (None, [C.c_int, P(vp)]),
     "ft_stream_destroy": (None, [vp]),
     "ft_event_create": (None, [C.c_int, P(vp)]),

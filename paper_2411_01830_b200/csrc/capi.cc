@@ -340,6 +340,36 @@ int ft_pool_policy_shrink(ft_pool_policy* p, double now, int64_t* dropped, int c
   }
   FT_CATCH
 }
+// The request path's bookkeeping of one store in one call: the index entry
+// (dataplane.py:72-83), the producer's histogram sample (datastore.py:51-62) and
+// its reservation window for the shrink timer (engine.py:656-659).
+int ft_store_commit(ft_index* x, ft_pool_policy* p, int64_t id, int node, int gpu, double size, double now,
+                    const char* producer, int response, double concurrency, double* r_window, double* last) {
+  NEED(x);
+  NEED(p);
+  FT_TRY
+  x->x.store(id, node, gpu, size, now, sfunc(producer), response != 0);
+  Hist& h = p->p.hist(sfunc(producer));
+  h.record(now, size, concurrency);
+  if (r_window) *r_window = h.r_window;
+  if (last) *last = h.has_last ? h.last : none();
+  FT_CATCH
+}
+// ... and of one retire: drop the index entry (dataplane.py:98-101), return the
+// block to the policy when it is free (datastore.py:146-149; block_id < 0: still
+// pinned by a view), and the producer's window.
+int ft_retire_commit(ft_index* x, ft_pool_policy* p, int64_t id, int64_t block_id, const char* producer,
+                     double* r_window, double* last) {
+  NEED(x);
+  NEED(p);
+  FT_TRY
+  x->x.drop(id);
+  if (block_id >= 0) p->p.free_block(block_id);
+  const Hist* h = p->p.hists.find(sfunc(producer));
+  if (r_window) *r_window = h ? h->r_window : 0.0;
+  if (last) *last = h && h->has_last ? h->last : none();
+  FT_CATCH
+}
 int ft_pool_policy_target(ft_pool_policy* p, double now, double* out) { NEED(p); *out = p->p.target(now); return FT_OK; }
 int ft_pool_policy_hist(const ft_pool_policy* p, const char* func, double* rw, double* last) {
   NEED(p);

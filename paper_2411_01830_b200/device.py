@@ -398,6 +398,32 @@ class DevicePool:
             if self.policy.mode == "none":           # temporary allocations: give it back now
                 self._unmap(blk.policy_block.block_id)
 
+    def commit_store(self, index, data_id: int, node: int, gpu: int, nbytes: int, now_ms: float, producer: str,
+                     response: bool, concurrency: float):
+        """Index entry + histogram sample + the producer's window in one call
+        (``ft_store_commit``); returns (R_window, last_request_ms | None)."""
+        rw, last = C.c_double(), C.c_double()
+        with self._lock:
+            LIB.ft_store_commit(index._h, self.policy._h, int(data_id), int(node), int(gpu), float(nbytes),
+                                float(now_ms), producer.encode(), int(bool(response)), float(concurrency),
+                                C.byref(rw), C.byref(last))
+        return rw.value, (None if last.value != last.value else last.value)
+
+    def commit_retire(self, index, data_id: int, blk: "PoolBlock", fences, producer: str):
+        """Index drop + block back to the policy (fenced) + the producer's window
+        in one call (``ft_retire_commit``); returns (R_window, last | None)."""
+        rw, last = C.c_double(), C.c_double()
+        with self._lock:
+            LIB.ft_retire_commit(index._h, self.policy._h, int(data_id), int(blk.policy_block.block_id),
+                                 producer.encode(), C.byref(rw), C.byref(last))
+            blk.policy_block.in_use = False
+            if fences:
+                self._fences[blk.policy_block.block_id] = tuple(fences)
+            if self.policy.mode == "none":
+                self.policy._blocks.pop(blk.policy_block.block_id, None)
+                self._unmap(blk.policy_block.block_id)
+        return rw.value, (None if last.value != last.value else last.value)
+
     def record(self, func: str, now_ms: float, size: float, concurrency: float):
         with self._lock:
             self.policy.histogram(func).record_execution(now_ms, size, concurrency)

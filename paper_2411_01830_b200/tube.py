@@ -327,9 +327,11 @@ class FaaSTube:
                                      obj.ready)
                     t.record_stream(so)
                     self.stats["bytes_local"] += nbytes
-                pool.record(producer, now, nbytes, live_here + 1)   # datastore.py:51-62
-                self._push_shrink(g, producer, now)
-                self.index.store(data_id, self._loc(g), nbytes, now, producer, response)
+                # index entry (dataplane.py:72-83) + histogram sample (datastore.py:51-62) +
+                # the shrink timer at last_request + R_window (engine.py:656-659): one FFI call
+                rw, last = pool.commit_store(self.index, data_id, self.node, g, nbytes, now, producer, response,
+                                             live_here + 1)
+                self._push_due(g, rw, last, now)
                 if response:
                     resp = self._respond(obj, pre_host)
                     if resp is not None:
@@ -624,6 +626,9 @@ class FaaSTube:
     def _push_shrink(self, g, func, now):
         """Shrink timer at last_request + R_window (engine.py:656-659)."""
         r_window, last = self.pools[g].hist_window(func)
+        self._push_due(g, r_window, last, now)
+
+    def _push_due(self, g, r_window, last, now):
         due = (last if last is not None else now) + r_window
         with self._maint_cv:
             wake = not self._shrink_due or due < self._shrink_due[0][0]
@@ -688,9 +693,23 @@ class FaaSTube:
         if obj.retired:
             return
         obj.retired = True
-        self.index.drop(obj.did)
         if self._objs.pop(obj.did, None) is not None:
             self._account(obj, -1)
+        blk = obj.block
+        if blk is not None and obj.pins == 0:
+            # drop the index entry, return the block (fenced on its last users) and re-arm
+            # the shrink timer in one FFI call (dataplane.py:98-101, datastore.py:146-149)
+            obj.block = None
+            ev = dev.Ev(blk.device).record(self._stream(blk.device))
+            fences = [ev] + obj.readers + ([obj.ready] if obj.ready is not None else [])
+            obj.readers = []
+            self.index._meta.pop(obj.did, None)
+            rw, last = self.pools[blk.device].commit_retire(self.index, obj.did, blk, fences, obj.producer)
+            self._push_due(blk.device, rw, last, self.now_ms())
+            if self.strategy.migration != "none":
+                self._maybe_prefetch(blk.device)             # engine.py:678-679, 717-736
+            return
+        self.index.drop(obj.did)
         self._maybe_free(obj)
 
     def _maybe_free(self, obj: _Obj):
