@@ -19,16 +19,18 @@ bytes move on real links:
                   kernel into the target, chunk-pipelined (dataplane.py:203-250),
                   issued by the native pacer (``device.Pacer``: managed stages
                   at their bandwidth share, engine.py:537-646);
-* GPU -> host   — copy-engine DMA;
+* GPU -> host   — copy-engine DMA out of the source GPU's root (plus staging
+                  routes), a managed d2h stage with the PCIe scheduler
+                  (responses and host fetches, engine.py:414-423);
 * host-oriented strategies (infless_plus, deepplan_plus) stage GPU->GPU
   through pinned host memory, as the reference's baselines do.
 
 Stream semantics: ``store`` orders after the producer's current stream;
 ``fetch`` enqueues on the consumer device's current stream, so consumer
-kernels issued afterwards see the data (host->GPU stages park that stream on
-the stage's completion word). No call synchronizes the host unless the
-caller asks for a host tensor; ``FaaSTube.wait`` blocks until a host->GPU
-fetch has landed.
+kernels issued afterwards see the data (a host->GPU fetch returns once its
+stage's last batch is issued; the consumer stream waits on the routes' last
+ops). No call synchronizes the host unless the caller asks for a host tensor;
+``FaaSTube.wait`` blocks until every host->GPU stage has landed.
 """
 
 from __future__ import annotations
