@@ -244,10 +244,16 @@ def run_ours(args):
     with Clocks(g) as clk:
         t_w = time.perf_counter()
         i = 0
-        while i < max(3, args.warmup) or time.perf_counter() - t_w < 0.5:
+        # N > 1: the producer->consumer ring counts steps on both ends, so every rank runs
+        # the same number of warm-up passes (a time-based count differed by one between
+        # ranks and left a doorbell waiting for a step its peer never ran)
+        while i < max(3, args.warmup) or (world == 1 and time.perf_counter() - t_w < 0.5):
             flush_l2(i)
             one_pass()
             i += 1
+        if world > 1:
+            while time.perf_counter() - t_w < 0.5:   # same clock-sampling window, no extra passes
+                time.sleep(0.01)
         torch.cuda.synchronize()
         assert torch.equal(inp.view(torch.uint8), x.view(torch.uint8)), "delivered bytes differ"
         if world > 1:
