@@ -1,1 +1,1 @@
-for i in 1 2 3; do timeout -k 10 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 2953$i bench.py --gpus 2 --steps 50 --warmup 5 --no-extras --cpu-sample-s 1 > gpurun_out/n2_$i.json 2> gpurun_out/n2_$i.err; echo "rc=$?" >> gpurun_out/n2_$i.err; done
+for i in 1 2 3; do timeout -k 10 200 python tools/diag_slow1.py trial > gpurun_out/diag_slow1_$i.txt 2>&1; done
