@@ -54,6 +54,15 @@ def test_copy_1gib(dev):
     assert torch.equal(dst, src)
 
 
+@pytest.mark.parametrize("shift", [0, 3, 8])
+def test_fingerprint_any_alignment(dev, shift):
+    n = (1 << 20) + 13
+    src = rnd(n + 16, 77)
+    fp = dev.Fingerprint(0)
+    fp.launch(src.data_ptr() + shift, n)
+    assert fp.value() == dev.fingerprint_host(src[shift:shift + n].cpu())
+
+
 @pytest.mark.parametrize("n", [1, 7, 8, 9, 4096, 12345677, 64 << 20])
 def test_fingerprint_matches_host(dev, n):
     src = rnd(n, n + 1)
