@@ -263,6 +263,7 @@ class DevicePool:
                  physical_bytes: float | None = None, spare_cap_bytes: int = 4 * GiB):
         require_cuda()
         self.device = device
+        self.on_unmap = []           # callbacks(vmm_id) after a block is unmapped (daemon.py)
         if physical_bytes is None:
             physical_bytes = float(torch.cuda.get_device_properties(device).total_memory)
         self.policy = datastore.MemoryPool(device, mode, floor_bytes, native_alloc_ms, physical_bytes)
@@ -454,7 +455,12 @@ class DevicePool:
         for vid, _ptr, _n, _f in gone:
             self._bases.pop(vid, None)
             LIB.ft_vmm_block_unmap(self._h, vid)
+            self._notify_unmap(vid)
         return sum(r[2] for r in gone)
+
+    def _notify_unmap(self, vid):
+        for fn in self.on_unmap:     # importers of an exported block drop their mapping
+            fn(vid)
 
     @property
     def released_bytes(self) -> int:
@@ -472,6 +478,7 @@ class DevicePool:
             ev.synchronize()
         self._bases.pop(m[0], None)
         LIB.ft_vmm_block_unmap(self._h, m[0])
+        self._notify_unmap(m[0])
         return m[2]
 
     def export_fd(self, blk: PoolBlock) -> int:

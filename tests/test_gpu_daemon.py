@@ -1,0 +1,120 @@
+"""Function process <-> per-box daemon: a spawned function
+process drives Listing 1 (unique_id / store / fetch) through ``TubeClient``
+against a ``TubeDaemon`` owning the FaaSTube in this process. GPU payloads
+cross as exported VMM pool blocks (zero copy on the daemon side), host payloads
+as memfds; every byte is checked against the seeded source in both processes."""
+
+import multiprocessing as mp
+import os
+import sys
+import tempfile
+import time
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SIZES = [1, 4097, 3 * 10**6 + 7, 64 << 20]
+
+
+def payload(n, seed):
+    g = torch.Generator().manual_seed(seed)
+    return torch.randint(0, 256, (n,), dtype=torch.uint8, generator=g)
+
+
+def _function(path, q, phase1, phase2):
+    sys.path.insert(0, ROOT)
+    try:
+        from paper_2411_01830_b200.daemon import DaemonError, TubeClient
+        c = TubeClient(path, 0)
+        ids = {}
+        for i, n in enumerate(SIZES):
+            src = payload(n, i).cuda()
+            did = c.unique_id()
+            c.store(did, src, consumers=3)           # the daemon also reads it, and fetch_host
+            got = c.fetch(did)                        # same GPU: the stored block itself, mapped here
+            assert torch.equal(got, src), ("gpu->gpu", n)
+            host = c.fetch(did, out=torch.empty(n, dtype=torch.uint8))
+            assert torch.equal(host, src.cpu()), ("gpu->host", n)
+            ids[n] = did
+        # typed tensor keeps dtype and shape
+        x = torch.randn(3, 5, 7, device="cuda:0", dtype=torch.float16)
+        did = c.unique_id()
+        c.store(did, x)
+        y = c.fetch(did)
+        assert y.dtype == x.dtype and y.shape == x.shape and torch.equal(x, y)
+        # a host (cFunc) payload: memfd to the daemon, staged host->GPU by its pacer on fetch
+        h = payload(5 * 10**6 + 3, 77)
+        did = c.unique_id()
+        c.store(did, h)
+        out = torch.empty_like(h, device="cuda:0")
+        c.fetch(did, out=out)
+        assert torch.equal(out.cpu(), h)
+        # steady state: pool blocks are reused by size class, so nothing new is mapped
+        before = len(c._imports)
+        t0 = time.perf_counter()
+        reps = 50
+        m = torch.randint(0, 256, (1 << 20,), dtype=torch.uint8, device="cuda:0")
+        for _ in range(reps):
+            did = c.unique_id()
+            c.store(did, m)
+            r = c.fetch(did)
+        us = (time.perf_counter() - t0) / reps * 1e6
+        assert torch.equal(r, m)
+        grown = len(c._imports) - before
+        # errors travel back as typed messages
+        try:
+            c.fetch(10**12)
+            missing = None
+        except DaemonError as e:
+            missing = str(e)
+        # the daemon's pool unmaps its free blocks: the next reply tells this process
+        # to unmap its imports of them (they would keep the physical memory alive)
+        mapped = len(c._imports)
+        phase1.set()
+        assert phase2.wait(120)
+        c.unique_id()
+        after = len(c._imports)
+        c.close()
+        q.put(("ok", {"ids": ids, "us_store_fetch_1MiB": us, "imports_grown": grown, "missing": missing,
+                      "mapped": mapped, "after_shrink": after}))
+    except Exception as exc:  # noqa: BLE001
+        import traceback
+        q.put(("err", traceback.format_exc() + repr(exc)))
+
+
+def test_function_process_through_daemon():
+    from paper_2411_01830_b200.daemon import TubeDaemon
+    from paper_2411_01830_b200.tube import FaaSTube
+    tube = FaaSTube(pcie_gbps=50.0, gpus=[0], pool_floor_bytes=0.0)
+    path = os.path.join(tempfile.mkdtemp(), "faastube.sock")
+    d = TubeDaemon(tube, path)
+    ctx = mp.get_context("spawn")
+    q, phase1, phase2 = ctx.Queue(), ctx.Event(), ctx.Event()
+    p = ctx.Process(target=_function, args=(path, q, phase1, phase2))
+    p.start()
+    while not phase1.wait(1):
+        assert p.is_alive() or not q.empty(), "function process died"
+        if not q.empty():
+            break
+    if phase1.is_set():
+        torch.cuda.synchronize()
+        dropped = tube.pools[0].shrink(tube.now_ms() + 1e9)
+        phase2.set()
+    status, res = q.get(timeout=600)
+    p.join(timeout=60)
+    assert status == "ok", res
+    print("daemon round trip (store+fetch 1 MiB, GPU, cross-process):", f"{res['us_store_fetch_1MiB']:.1f} us")
+    assert res["imports_grown"] <= 2, res
+    assert res["missing"] and "MissingData" in res["missing"], res
+    assert dropped > 0 and res["after_shrink"] < res["mapped"], (dropped, res)
+    # the daemon side holds the function's bytes (third consumer)
+    for i, n in enumerate(SIZES):
+        t = tube.fetch(res["ids"][n], device=0)
+        assert torch.equal(t.cpu(), payload(n, i)), n
+        del t
+    torch.cuda.synchronize()
+    d.close()
+    tube.close()
