@@ -13,7 +13,7 @@ import ctypes as C
 import math
 from dataclasses import dataclass, field
 
-from ._lib import LIB, destroyer, DuplicateStore, MissingData, enc, json_out
+from ._lib import LIB, BranchC, destroyer, DuplicateStore, MissingData, enc, json_out
 from .strategies import Strategy
 from .topology import BandwidthMatrix, Topology
 
@@ -132,6 +132,9 @@ class Stage:
     pinned_bytes: float = 0.0
 
 
+_LINK_KINDS = ("h2d", "d2h", "nv", "nvp_out", "nvp_in", "net")   # ft_link_kind
+
+
 class TransferPlan:
     """dataplane.py:153-160, backed by a C plan (``_h``)."""
 
@@ -150,13 +153,41 @@ class TransferPlan:
             d["stages"] = [Stage([Branch([tuple(l) for l in b["links"]], b["bytes_share"], b["cap_gbps"],
                                          b["reserved_gbps"], b["fill_ms"], b["hop_caps"]) for b in s["branches"]],
                                  s["managed"], s["pinned_bytes"]) for s in d["stages"]]
+            if "_stages" in self.__dict__:
+                d["stages"] = self._stages          # one set of objects per plan
             self._d = d
         return self._d
 
     size_bytes = property(lambda self: self._full()["size_bytes"])
     claimed_func = property(lambda self: self._full()["claimed_func"])
     note = property(lambda self: self._full()["note"])
-    stages = property(lambda self: self._full()["stages"])
+
+    @property
+    def stages(self) -> list:
+        """Stages read through the struct accessors (ft_plan_stage/_branch): the
+        request path needs only these, and a JSON round trip of the whole plan
+        cost more than building it."""
+        if self._d is not None:
+            return self._d["stages"]
+        st = self.__dict__.get("_stages")
+        if st is None:
+            n = C.c_int()
+            LIB.ft_plan_method(self._h, None, None, C.byref(n))
+            st = []
+            man, pinned, nb, b = C.c_int(), C.c_double(), C.c_int(), BranchC()
+            for si in range(n.value):
+                LIB.ft_plan_stage(self._h, si, C.byref(man), C.byref(pinned), C.byref(nb))
+                brs = []
+                for bi in range(nb.value):
+                    LIB.ft_plan_branch(self._h, si, bi, C.byref(b))
+                    links = [(_LINK_KINDS[lk.kind], lk.a) if lk.kind in (3, 4) else (_LINK_KINDS[lk.kind], lk.a, lk.b)
+                             for lk in b.links[:b.n_links]]
+                    brs.append(Branch(links, b.bytes_share, None if b.cap_gbps != b.cap_gbps else b.cap_gbps,
+                                      None if b.reserved_gbps != b.reserved_gbps else b.reserved_gbps, b.fill_ms,
+                                      list(b.hop_caps[:b.n_caps])))
+                st.append(Stage(brs, bool(man.value), pinned.value))
+            self._stages = st
+        return st
 
     def __del__(self, _destroy=destroyer("ft_plan_destroy")):
         h = getattr(self, "_h", None)

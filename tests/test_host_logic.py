@@ -70,3 +70,25 @@ def test_histogram_windows_match_oracle_with_eviction():
             h.record_execution(now, size, con)
             o.record(now, size, con)
             assert (h.r_window_ms, h.r_size_bytes, h.r_con) == (o.r_window, o.r_size, o.r_con), (window, i)
+
+
+def test_plan_stage_accessors_match_json():
+    """TransferPlan.stages (struct accessors, the request path) equals the
+    stages of the plan's JSON form for every method on several topologies."""
+    from paper_2411_01830_b200 import dataplane, strategies, topology
+    for n in (1, 2, 8):
+        topo = topology.build_preset("b200", n_gpus=n, pcie_gbps=55.0)
+        for strat in ("faastube", "infless_plus"):
+            m = topology.snapshot_matrix(topo)
+            dp = dataplane.Dataplane(topo, strategies.strategy_preset(strat), m, 2e6)
+            locs = [dataplane.Location(0, None)] + [dataplane.Location(0, g) for g in range(n)]
+            for a in locs:
+                for b in locs:
+                    for size in (1.0, 4096.0, 64 * 2.0**20, 2.0**30):
+                        fast = dp.fetch_plan(a, b, size)
+                        fast.stages
+                        dp.release_claim(fast)      # an inter-GPU plan claims its NVLink path
+                        slow = dp.fetch_plan(a, b, size)
+                        slow._full()
+                        dp.release_claim(slow)
+                        assert fast.stages == slow.stages, (n, strat, a, b, size)

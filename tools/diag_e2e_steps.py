@@ -39,5 +39,15 @@ for tk, ev in st.items():
     k = dict((b, a) for a, b in ev)
     if "start" in k and "land" in k:
         ds.append((k["land"] - k["start"], ev[1][0] - k["start"] if len(ev) > 1 else 0))
-print("pacer stage start->land ms", med([d[0] for d in ds]), "start->first event ms", med([d[1] for d in ds]))
+if ds:
+    print("pacer stage start->land ms", med([d[0] for d in ds]), "start->first event ms", med([d[1] for d in ds]))
 tube.close()
+# the link itself: one 64 MiB pinned H2D per step (cudaMemcpyAsync), same box
+raw = []
+for i in range(40):
+    t0 = time.perf_counter()
+    prod_out.view(-1).view(torch.uint8).copy_(host_in, non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    if i >= 5:
+        raw.append(1e3 * (time.perf_counter() - t0))
+print("raw 64 MiB H2D copy+sync ms", med(raw), "-> GB/s", round(n / med(raw) / 1e6, 1))
