@@ -370,6 +370,7 @@ def run_ours(args):
 
     if rank == 0:
         cpu = cpu_host_path(args.cpu_sample_s, nbytes) if world == 1 else None
+        cpu1 = cpu_host_path(min(3.0, args.cpu_sample_s), nbytes, threads=1) if world == 1 else None
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(total_ms_max / args.steps, 5), "higher_is_better": True,
@@ -410,7 +411,10 @@ def run_ours(args):
             line["cpu_baseline"] = {"value": round(cpu["gbps"], 3), "unit": "GB/s", "cores": cpu["threads"],
                                     "kind": "port", "sample": f"{cpu['passes']} store+fetch passes of 64 MiB "
                                                               f"through host memory ({args.cpu_sample_s:.0f} s)",
-                                    "p99_pass_ms": round(cpu["pass_ms_p99"], 3)}
+                                    "p99_pass_ms": round(cpu["pass_ms_p99"], 3),
+                                    "single_thread": {"value": round(cpu1["gbps"], 3), "cores": 1,
+                                                      "p99_pass_ms": round(cpu1["pass_ms_p99"], 3),
+                                                      "sample": f"{cpu1['passes']} passes"}}
         line.update(extras)
         print(json.dumps(line), flush=True)
     if pair is not None:

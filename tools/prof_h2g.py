@@ -41,5 +41,6 @@ pr = cProfile.Profile()
 pr.enable()
 loop(2000)
 pr.disable()
-pstats.Stats(pr).sort_stats("tottime").print_stats(25)
+pstats.Stats(pr).sort_stats("tottime").print_stats(22)
+pstats.Stats(pr).sort_stats("cumulative").print_stats(22)
 tube.close()
