@@ -118,3 +118,66 @@ def test_function_process_through_daemon():
     torch.cuda.synchronize()
     d.close()
     tube.close()
+
+
+def _producer(path, q, count):
+    sys.path.insert(0, ROOT)
+    try:
+        from paper_2411_01830_b200.daemon import TubeClient
+        c = TubeClient(path, 0)
+        ids = []
+        for i in range(count):
+            n = (i * 7919) % (3 << 20) + 1
+            did = c.unique_id()
+            c.store(did, payload(n, 1000 + i).cuda(), producer="prod")
+            ids.append((did, n, 1000 + i))
+        c.close()
+        q.put(("ok", ids))
+    except Exception:  # noqa: BLE001
+        import traceback
+        q.put(("err", traceback.format_exc()))
+
+
+def _consumer(path, ids, q):
+    sys.path.insert(0, ROOT)
+    try:
+        from paper_2411_01830_b200.daemon import TubeClient
+        c = TubeClient(path, 0)
+        bad = []
+        for did, n, seed in ids:
+            got = c.fetch(did, consumer="cons")
+            if not torch.equal(got.cpu(), payload(n, seed)):
+                bad.append(did)
+        c.close()
+        q.put(("ok", bad))
+    except Exception:  # noqa: BLE001
+        import traceback
+        q.put(("err", traceback.format_exc()))
+
+
+def test_producer_and_consumer_processes():
+    """Two function processes: the producer's outputs (written through its mapping
+    of daemon pool blocks) are fetched by a separate consumer process — every
+    object bit-exact, and the daemon retires each after its one consumer."""
+    from paper_2411_01830_b200.daemon import TubeDaemon
+    from paper_2411_01830_b200.tube import FaaSTube
+    tube = FaaSTube(pcie_gbps=50.0, gpus=[0])
+    path = os.path.join(tempfile.mkdtemp(), "faastube.sock")
+    d = TubeDaemon(tube, path)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    prod = ctx.Process(target=_producer, args=(path, q, 40))
+    prod.start()
+    status, ids = q.get(timeout=600)
+    prod.join(timeout=60)
+    assert status == "ok", ids
+    cons = ctx.Process(target=_consumer, args=(path, ids, q))
+    cons.start()
+    status, bad = q.get(timeout=600)
+    cons.join(timeout=60)
+    assert status == "ok", bad
+    assert bad == []
+    assert all(did not in tube._objs for did, _, _ in ids)       # consumed -> retired
+    assert tube._accounts_consistent()
+    d.close()
+    tube.close()
