@@ -103,7 +103,7 @@ class TubeDaemon:
                 return
             th = threading.Thread(target=self._serve, args=(ch,), name="faastube-daemon-conn", daemon=True)
             th.start()
-            self._threads.append(th)
+            self._threads = [t for t in self._threads if t.is_alive()] + [th]
 
     def _dropped(self, g, vid):
         with self._lock:
@@ -126,12 +126,17 @@ class TubeDaemon:
 
     def _unhold(self, conn, tok):
         t = self._take(conn, tok)
-        keep = getattr(t, "_ft_keep", None)
+        # a daemon-side fetch buffer, or an output block never committed (the client
+        # died between alloc and commit), goes back to the pool
+        keep = getattr(t, "_ft_keep", None) if not getattr(t, "_ft_alloc", False) else t
         del t
-        if keep is not None:                   # a daemon-side buffer goes back to the pool
-            blk = keep._ft_block  # noqa: SLF001
-            del keep
-            self.tube.pools[blk.device].free(blk)
+        if keep is not None:
+            self._free(keep)
+
+    def _free(self, t):
+        blk = t._ft_block  # noqa: SLF001
+        del t
+        self.tube.pools[blk.device].free(blk)
 
     def _serve(self, ch: Channel):
         conn = _Conn(ch)
@@ -184,6 +189,7 @@ class TubeDaemon:
         elif op == "alloc":
             g, n = int(msg["gpu"]), int(msg["nbytes"])
             t = tube.empty((max(1, n),), torch.uint8, device=g)              # pool-backed output
+            t._ft_alloc = True  # noqa: SLF001
             dev.Ev(g).record(tube._stream(g)).synchronize()  # noqa: SLF001 - its previous users are done
             self._reply_block(conn, g, t._ft_block, {"token": self._hold(conn, t), "nbytes": n})  # noqa: SLF001
         elif op == "commit":
@@ -194,8 +200,13 @@ class TubeDaemon:
             dt = _DTYPES[msg["dtype"]]
             out = t[:math.prod(msg["shape"]) * dt.itemsize].view(dt).view(msg["shape"])
             out._ft_block = blk  # noqa: SLF001 - still the pool block: a zero-copy store
-            tube.store(int(msg["id"]), out, response=bool(msg.get("response")), producer=msg.get("producer", "func"),
-                       consumers=int(msg.get("consumers", 1)))
+            try:
+                tube.store(int(msg["id"]), out, response=bool(msg.get("response")),
+                           producer=msg.get("producer", "func"), consumers=int(msg.get("consumers", 1)))
+            except BaseException:
+                del out
+                self._free(t)                  # not published (e.g. DuplicateStore): back to the pool
+                raise
             self._reply(conn, {})
         elif op == "store_host":
             fd, _ = ch.recv_fd()
@@ -246,7 +257,22 @@ class TubeDaemon:
             raise ValueError(f"unknown op {op!r}")
 
     def close(self):
+        """Stop accepting, drop every connection (their loans go back to the pool)."""
         self._closing = True
+        try:
+            self.server.shutdown(2)            # wakes the acceptor blocked in accept()
+        except OSError:
+            pass
+        self._acceptor.join(timeout=5)
+        with self._lock:
+            conns = list(self._conns)
+        for conn in conns:
+            try:
+                conn.ch.sock.shutdown(2)
+            except OSError:
+                pass
+        for th in self._threads:
+            th.join(timeout=5)
         try:
             self.server.close()
         finally:

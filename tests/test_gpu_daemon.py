@@ -181,3 +181,37 @@ def test_producer_and_consumer_processes():
     assert tube._accounts_consistent()
     d.close()
     tube.close()
+
+
+def _dies_after_alloc(path, q):
+    sys.path.insert(0, ROOT)
+    from paper_2411_01830_b200.daemon import TubeClient
+    c = TubeClient(path, 0)
+    rep = c._call({"op": "alloc", "gpu": 0, "nbytes": 8 << 20})   # a loan it never commits
+    q.put(rep["token"])
+    q.close()
+    q.join_thread()                                                  # flushed before the hard exit
+    os._exit(0)                                                      # no close, no commit
+
+
+def test_dead_client_loans_return_to_the_pool():
+    from paper_2411_01830_b200.daemon import TubeDaemon
+    from paper_2411_01830_b200.tube import FaaSTube
+    tube = FaaSTube(pcie_gbps=50.0, gpus=[0])
+    path = os.path.join(tempfile.mkdtemp(), "faastube.sock")
+    d = TubeDaemon(tube, path)
+    before = tube.pools[0].policy.in_use_bytes
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_dies_after_alloc, args=(path, q))
+    p.start()
+    q.get(timeout=120)
+    p.join(timeout=60)
+    deadline = time.time() + 10
+    while tube.pools[0].policy.in_use_bytes != before and time.time() < deadline:
+        time.sleep(0.05)
+    assert tube.pools[0].policy.in_use_bytes == before
+    assert not d._held
+    d.close()
+    assert not d._acceptor.is_alive()
+    tube.close()
