@@ -63,7 +63,8 @@ constexpr int kInflightBatches = 4;  // issued-but-not-landed batches per stage
 constexpr double kLookahead = 2.0;   // batches issued ahead of the rate schedule (host jitter)
 constexpr int kOwnerCoalesce = 2;     // batches per DMA op for a stage that holds the whole link
 constexpr int kMaxDev = 64;
-constexpr int kWorkers = 4;          // pageable staging threads (8 measured no faster: the ring, not the memcpy, limits)
+constexpr int kWorkers = 8;  // pageable staging threads (1 GiB pageable -> GPU with a 40 MB ring: 4 workers
+                             // 28-37 GB/s, 8: 44-47, 12: 41-45, 16: 37-42; profiles/r01/sweep_pageable.txt)
 
 struct DevGuard {
   int prev = -1;
@@ -795,7 +796,9 @@ int ft_pacer_create(double bw_all_gbps, int links, int batch_chunks, int64_t chu
   p->hslots = std::vector<HostSlot>(slots);
   ft_pacer* raw = p.get();
   raw->pacer = std::thread([raw] { raw->run(); });
-  for (int i = 0; i < kWorkers; ++i) raw->workers.emplace_back([raw] { raw->work(); });
+  int nw = kWorkers;
+  if (const char* w = std::getenv("FT_PACER_WORKERS")) nw = std::max(1, std::atoi(w));
+  for (int i = 0; i < nw; ++i) raw->workers.emplace_back([raw] { raw->work(); });
   *out = p.release();
   return FT_OK;
 }

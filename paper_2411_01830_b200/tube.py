@@ -123,9 +123,14 @@ class FaaSTube:
         roots = self.topo.roots()
         bw_all = self.topo.pcie_gbps * len(roots)  # engine.py:186-190
         # every host->GPU leg goes through the native pacer (managed stages paced at
-        # their share; pageable payloads staged through its warm pinned ring)
+        # their share; pageable payloads staged through its warm pinned ring). The
+        # physical ring is twice the reference's modelled warm capacity
+        # (pcie_sched.py:155-162): at 1x the ring, not the 8 memcpy workers, capped a
+        # pageable 1 GiB fetch at 28-42 GB/s; at 2x it runs at 44-47 GB/s
+        # (profiles/r01/sweep_pageable.txt)
         self.pacer = dev.Pacer(bw_all, batch_chunks, chunk_bytes, staging_slots=4,
-                               host_ring_bytes=default_ring_capacity(len(roots), batch_chunks * chunk_bytes),
+                               host_ring_bytes=int(os.environ.get("FT_HOST_RING_BYTES", 0)) or
+                               2 * default_ring_capacity(len(roots), batch_chunks * chunk_bytes),
                                logging=bool(os.environ.get("FT_TRACE")), links=len(roots))
         self._tickets = []           # (ticket, keep-alive refs) until the stage has landed
         self._t0 = time.perf_counter()
