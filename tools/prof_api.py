@@ -39,4 +39,5 @@ pr.enable()
 loop(2000, False)
 pr.disable()
 pstats.Stats(pr).sort_stats("tottime").print_stats(30)
+pstats.Stats(pr).sort_stats("cumulative").print_stats(30)
 torch.cuda.synchronize()
