@@ -255,8 +255,14 @@ class Runtime:
             rep = rt.run([(wf, where, reqs)], duration_s, drain_s=30, idle_s=0.0)
             ok = not reqs or (rep["requests_completed"] >= 0.95 * len(reqs) and rep.get("p99_ms") is not None
                               and rep["p99_ms"] <= slo)       # no arrival drawn: vacuously met
+            done = [r for r in rt.records if r.end_ms is not None]
+            worst = max(done, key=lambda r: r.end_ms - r.arrival_ms, default=None)
             trials.append({"rate": round(rate, 3), "ok": ok, "p99_ms": rep.get("p99_ms"),
-                           "completed": rep["requests_completed"], "offered": len(reqs)})
+                           "completed": rep["requests_completed"], "offered": len(reqs),
+                           **({"worst": {"rid": worst.rid, "arrival_ms": round(worst.arrival_ms, 1),
+                                         "latency_ms": round(worst.end_ms - worst.arrival_ms, 2),
+                                         "phases": {k: round(v, 2) for k, v in worst.phases.items() if v}}}
+                              if worst is not None and not ok else {})})
             return ok, rep
 
         lo, hi, last = 0.0, None, None
