@@ -467,6 +467,27 @@ def run_extras(tube, g, dev, torch, max_throughput=False):
                   "links": k, "value": round(h2g_gbps, 3), "unit": "GB/s", "peak": round(k * ce_peak, 3),
                   "peak_source": f"live: best-of-3 cudaMemcpyAsync 1 GiB pinned H2D on the target's link x {k}",
                   "frac": round(h2g_gbps / (k * ce_peak), 4)}
+    # config 2 at k=1 across sizes: p50/p99 of one pinned host -> GPU fetch (device events)
+    sweep = []
+    for sz in (4096, 65536, 1 << 20, 16 << 20, 256 << 20, 1 << 30):
+        reps = 60 if sz <= (1 << 20) else (20 if sz <= (256 << 20) else 6)
+        ts = []
+        for i in range(reps + 2):
+            did = tube.unique_id()
+            tube.store(did, host[:sz], producer="decode")
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(s)
+            tube.fetch(did, device=g, out=dst[:sz], consumer="preproc")
+            b.record(s)
+            b.synchronize()
+            if i >= 2:
+                ts.append(a.elapsed_time(b))
+        ts.sort()
+        p50 = nearest_rank(ts, 50)
+        sweep.append({"bytes": sz, "ms_p50": round(p50, 4), "ms_p99": round(nearest_rank(ts, 99), 4),
+                      "gbps_p50": round(sz / (p50 * 1e-3) / 1e9, 2), "frac_p50": round(sz / (p50 * 1e-3) / 1e9 / ce_peak, 4)})
+    out["h2g_sweep"] = {"workload": "config2 at k=1: pinned host -> GPU via FaaSTube.fetch (managed stage), "
+                                    "device-event time per fetch", "peak_gbps": round(ce_peak, 3), "points": sweep}
     # config 2's striping machinery on one GPU: the same 1 GiB split over a direct route and a
     # staged route (CE into the staging chunk ring + forward kernel, here staging GPU == target,
     # so both routes share one PCIe link): the ring/forward pipeline must not cost link rate
