@@ -282,3 +282,72 @@ def test_full_size_round_trips():
         del y
     assert t._accounts_consistent()
     t.close()
+
+
+def _edge_payloads():
+    g = torch.Generator(device="cpu").manual_seed(11)
+    special = torch.tensor([float("nan"), float("inf"), -float("inf"), -0.0, 0.0, 65504.0, 6e-8, 1.0],
+                           dtype=torch.float16)
+    nan_payloads = torch.cat([special, torch.randn(4093, generator=g).half()])
+    nan_bits = torch.randint(0, 1 << 16, (4097,), generator=g, dtype=torch.int32).to(torch.int16).view(torch.float16)
+    return {
+        "empty": torch.empty(0, dtype=torch.float16),
+        "empty_3d": torch.empty(3, 0, 5, dtype=torch.int32),
+        "fp16_specials": nan_payloads,
+        "fp16_any_bits": nan_bits,                   # signalling/quiet NaNs of every payload
+        "bool_odd": torch.rand(1001, generator=g) > 0.5,
+        "int8_ragged": torch.randint(-128, 128, (7, 13, 3), generator=g, dtype=torch.int8),
+        "transposed": torch.randn(64, 48, generator=g).t(),     # non-contiguous producer output
+    }
+
+
+@pytest.mark.parametrize("name", list(_edge_payloads()))
+def test_edge_payloads_every_path(tube, name):
+    """Empty, ragged, non-contiguous and NaN-carrying payloads through every
+    path (GPU copy-fetch, zero-copy view, GPU -> host, host -> GPU): the bytes
+    equal the oracle host path's as uint8 (so NaN bit patterns count)."""
+    src = _edge_payloads()[name]
+    want = oracle_bytes(src.contiguous()) if src.numel() else np.empty(0, dtype=np.uint8)
+    x = src.to("cuda:0")
+    # GPU producer: copy-fetch, zero-copy view and host fetch of one object
+    did = tube.unique_id()
+    tube.store(did, x, producer="p", consumers=3)
+    a = tube.fetch(did, device=0, out=torch.empty(x.shape, dtype=x.dtype, device="cuda:0"), consumer="c")
+    b = tube.fetch(did, device=0, consumer="c")
+    h = tube.fetch(did, device=None, consumer="c")
+    torch.cuda.synchronize()
+    for got in (a, b, h):
+        assert got.shape == src.shape and got.dtype == src.dtype
+        assert np.array_equal(as_u8(got), want), name
+    del b
+    # host producer (cFunc output) -> GPU consumer
+    hid = tube.unique_id()
+    tube.store(hid, src.contiguous(), producer="decode")
+    g = tube.fetch(hid, device=0, consumer="c")
+    torch.cuda.synchronize()
+    assert g.shape == src.shape and np.array_equal(as_u8(g), want), name
+
+
+def test_object_larger_than_4gib_same_gpu():
+    """5 GiB + 4097 B through store (snapshot copy) and fetch (copy into the input
+    buffer): byte offsets past 2^32 in the copy kernels, digest-checked against
+    the producer tensor and spot-checked at the tail."""
+    from paper_2411_01830_b200 import device as dev
+    from paper_2411_01830_b200.tube import FaaSTube
+    t = FaaSTube("faastube", pool_floor_bytes=0.0, capacity_limit_bytes=64e9)
+    n = (5 << 30) + 4097
+    x = torch.empty(n, dtype=torch.uint8, device="cuda:0")
+    x.view(-1)[: n // 8 * 8].view(torch.int64).copy_(torch.arange(n // 8, device="cuda:0") * 0x9E3779B97F4A7C15)
+    x[n // 8 * 8:] = 0xA5
+    fp = dev.Fingerprint(0)
+    fp.launch(x.data_ptr(), n, torch.cuda.current_stream(0))
+    want = fp.value()
+    did = t.unique_id()
+    t.store(did, x, producer="p")
+    y = t.fetch(did, device=0, out=torch.empty_like(x), consumer="c")
+    fp.launch(y.data_ptr(), n, torch.cuda.current_stream(0))
+    assert fp.value() == want
+    assert torch.equal(y[-(1 << 20):], x[-(1 << 20):])
+    del x, y
+    assert t._accounts_consistent()
+    t.close()
