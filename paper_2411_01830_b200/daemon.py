@@ -214,7 +214,8 @@ class TubeDaemon:
                 host = _from_memfd(fd, int(msg["nbytes"]))
             finally:
                 os.close(fd)
-            host = host.view(_DTYPES[msg["dtype"]]).view(msg["shape"]) if host.numel() else host
+            dt = _DTYPES[msg["dtype"]]
+            host = host.view(dt).view(msg["shape"]) if host.numel() else torch.empty(msg["shape"], dtype=dt)
             tube.store(int(msg["id"]), host, producer=msg.get("producer", "func"),
                        consumers=int(msg.get("consumers", 1)))
             self._reply(conn, {})

@@ -45,6 +45,15 @@ def _function(path, q, phase1, phase2):
         c.store(did, x)
         y = c.fetch(did)
         assert y.dtype == x.dtype and y.shape == x.shape and torch.equal(x, y)
+        # empty and NaN-bit payloads, GPU and host producers
+        for t in (torch.empty(0, dtype=torch.float16), torch.empty(2, 0, dtype=torch.int32),
+                  torch.randint(0, 1 << 16, (4097,), dtype=torch.int32).to(torch.int16).view(torch.float16)):
+            for dev_t in (t.cuda(), t):
+                did = c.unique_id()
+                c.store(did, dev_t)
+                y = c.fetch(did)
+                assert y.shape == t.shape and y.dtype == t.dtype
+                assert torch.equal(y.cpu().reshape(-1).view(torch.uint8), t.reshape(-1).view(torch.uint8))
         # a host (cFunc) payload: memfd to the daemon, staged host->GPU by its pacer on fetch
         h = payload(5 * 10**6 + 3, 77)
         did = c.unique_id()
