@@ -247,6 +247,11 @@ int ft_plan_method(const ft_plan* plan, int* method, double* fixed_ms, int* n_st
 int ft_plan_add_fixed_ms(ft_plan* plan, double ms); /* engine.py:451-452 */
 int ft_plan_stage(const ft_plan* plan, int stage, int* managed, double* pinned_bytes, int* n_branches);
 int ft_plan_branch(const ft_plan* plan, int stage, int branch, ft_branch* out);
+/* every stage and branch in one call, as doubles (the request path reads
+ * these): [n_stages, {managed, pinned_bytes, n_branches, {n_links, {kind, a, b}
+ * x n_links, n_caps, caps..., bytes_share, cap_gbps, reserved_gbps, fill_ms}
+ * x n_branches} x n_stages]; FT_E_TRUNCATED with *need set when cap is short */
+int ft_plan_pack(const ft_plan* plan, double* buf, size_t cap, size_t* need);
 /* full plan as JSON (method, size_bytes, fixed_ms, claimed_func, note, stages, latency) */
 int ft_plan_json(const ft_plan* plan, char* buf, size_t cap, size_t* need);
 /* plan_latency_model                                dataplane.py:351-369 */

@@ -207,6 +207,7 @@ _SIGS = {
     "ft_plan_add_fixed_ms": (None, [vp, dbl]),
     "ft_plan_stage": (None, [vp, C.c_int, P(C.c_int), P(dbl), P(C.c_int)]),
     "ft_plan_branch": (None, [vp, C.c_int, C.c_int, P(BranchC)]),
+    "ft_plan_pack": (None, [vp, P(dbl), sz, P(sz)]),
     "ft_plan_json": (None, [vp, C.c_char_p, sz, P(sz)]),
     "ft_plan_latency": (None, [vp, P(dbl)]),
     "ft_release_claim": (None, [vp, vp]),

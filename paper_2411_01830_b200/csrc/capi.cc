@@ -517,6 +517,37 @@ int ft_plan_branch(const ft_plan* plan, int s, int b, ft_branch* out) {
   out->fill_ms = br.fill;
   return FT_OK;
 }
+int ft_plan_pack(const ft_plan* plan, double* buf, size_t cap, size_t* need) {
+  NEED(plan);
+  std::vector<double> v;
+  v.push_back((double)plan->p.stages.size());
+  for (auto& st : plan->p.stages) {
+    v.push_back(st.managed ? 1.0 : 0.0);
+    v.push_back(st.pinned);
+    v.push_back((double)st.branches.size());
+    for (auto& br : st.branches) {
+      v.push_back((double)br.links.size());
+      for (auto& l : br.links) {
+        v.push_back(l.kind);
+        v.push_back(l.a);
+        v.push_back(l.b);
+      }
+      v.push_back((double)br.hop_caps.size());
+      for (double c : br.hop_caps) v.push_back(c);
+      v.push_back(br.share);
+      v.push_back(br.cap);
+      v.push_back(br.reserved);
+      v.push_back(br.fill);
+    }
+  }
+  if (need) *need = v.size();
+  if (v.size() > cap || !buf) {
+    ft::set_last_error("ft_plan_pack: buffer too small");
+    return FT_E_TRUNCATED;
+  }
+  std::memcpy(buf, v.data(), v.size() * sizeof(double));
+  return FT_OK;
+}
 int ft_plan_json(const ft_plan* plan, char* buf, size_t cap, size_t* need) {
   NEED(plan);
   return emit_json(plan->p.json(), buf, cap, need);

@@ -44,12 +44,20 @@ struct Topo {
   double pair_bandwidth(int u, int v) const;
   std::vector<int> sorted_roots() const;
   const std::vector<int64_t>& group(int root) const;
+  // candidate_paths results per (src, dst, max_hops): the topology is immutable,
+  // and the enumeration (157 paths on an 8-GPU mesh) dominated every select
+  struct CandCache;
+  std::shared_ptr<CandCache> cand_cache;
 };
 
 // --------------------------------------------------- BandwidthMatrix
 struct Matrix {
   const Topo* topo;
   std::map<std::pair<int, int>, double> capacity, residual;
+  // dense mirrors of capacity/residual (NaN = no edge): res()/idle() are called
+  // for every hop of every candidate on each select
+  int n = 0;
+  std::vector<double> dcap, dres;
   std::map<int, double> egress, ingress;
   std::map<std::pair<int, int>, std::vector<std::string>> owners;
   ODict<std::vector<std::pair<Path, double>>> held;
@@ -77,7 +85,7 @@ struct SelectTrace {
   Path shared;
   std::string json() const;
 };
-std::vector<Path> candidate_paths(const Topo& t, int s, int d, int max_hops = 4);
+const std::vector<Path>& candidate_paths(const Topo& t, int s, int d, int max_hops = 4);
 std::vector<NvPath> select_paths(Matrix& m, const std::string& func, int s, int d, bool allow_busy,
                                  SelectTrace* tr);
 std::string claim_direct(Matrix& m, const std::vector<std::pair<int, int>>& pairs, const std::string& wf);

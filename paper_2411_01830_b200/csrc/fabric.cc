@@ -1,5 +1,7 @@
 // Topology, bandwidth matrix and Alg. 1 NVLink path selection.
 // Restates tubesim topology.py:65-443 and nvlink_sched.py:42-302.
+#include <mutex>
+#include <tuple>
 #include <algorithm>
 
 #include "decisions.h"
@@ -217,12 +219,18 @@ const std::vector<int64_t>& Topo::group(int root) const {
 
 // ------------------------------------------------------------ Matrix
 Matrix::Matrix(const Topo* t) : topo(t) {
+  n = t->gpu_count;
+  for (auto& kv : t->nv) n = std::max(n, std::max(kv.first.first, kv.first.second) + 1);
+  dcap.assign((size_t)n * n, NAN);
+  dres.assign((size_t)n * n, NAN);
   for (auto& kv : t->nv) {
     auto [u, v] = kv.first;
     for (auto e : {std::make_pair(u, v), std::make_pair(v, u)}) {
       capacity[e] = kv.second;
       residual[e] = kv.second;
       owners[e];
+      dcap[(size_t)e.first * n + e.second] = kv.second;
+      dres[(size_t)e.first * n + e.second] = kv.second;
     }
   }
   for (int g = 0; g < t->gpu_count; ++g) {
@@ -232,12 +240,14 @@ Matrix::Matrix(const Topo* t) : topo(t) {
   }
 }
 double Matrix::res(int u, int v) const {
-  auto it = residual.find({u, v});
-  return it == residual.end() ? 0.0 : it->second;
+  if (u < 0 || v < 0 || u >= n || v >= n) return 0.0;
+  double r = dres[(size_t)u * n + v];
+  return std::isnan(r) ? 0.0 : r;
 }
 bool Matrix::idle(int u, int v) const {
-  auto it = residual.find({u, v});
-  return it != residual.end() && it->second == capacity.at({u, v});
+  if (u < 0 || v < 0 || u >= n || v >= n) return false;
+  double r = dres[(size_t)u * n + v];
+  return !std::isnan(r) && r == dcap[(size_t)u * n + v];
 }
 void Matrix::hold(const std::string& f, const Path& p, double rate) {
   for (size_t i = 0; i + 1 < p.size(); ++i)
@@ -247,6 +257,7 @@ void Matrix::hold(const std::string& f, const Path& p, double rate) {
     auto it = residual.find({p[i], p[i + 1]});
     if (it == residual.end()) fail(FT_E_KEY, "hold on a missing edge");
     it->second -= rate;
+    dres[(size_t)p[i] * n + p[i + 1]] = it->second;
     owners[{p[i], p[i + 1]}].push_back(f);
   }
   if (!egress.count(p.front()) || !ingress.count(p.back())) fail(FT_E_KEY, "hold endpoint is not a GPU");
@@ -258,7 +269,9 @@ void Matrix::hold(const std::string& f, const Path& p, double rate) {
 }
 void Matrix::give_back(const std::string& f, const Path& p, double rate) {
   for (size_t i = 0; i + 1 < p.size(); ++i) {
-    residual[{p[i], p[i + 1]}] += rate;
+    double& r = residual[{p[i], p[i + 1]}];
+    r += rate;
+    if (p[i] >= 0 && p[i + 1] >= 0 && p[i] < n && p[i + 1] < n) dres[(size_t)p[i] * n + p[i + 1]] = r;
     auto& ow = owners[{p[i], p[i + 1]}];
     auto it = std::find(ow.begin(), ow.end(), f);
     if (it != ow.end()) ow.erase(it);
@@ -350,7 +363,28 @@ std::string Matrix::state_json() const {
 }
 
 // ------------------------------------------------------------ Alg. 1
-std::vector<Path> candidate_paths(const Topo& t, int s, int d, int max_hops) {
+struct Topo::CandCache {
+  std::mutex mu;
+  std::map<std::tuple<int, int, int>, std::vector<Path>> paths;  // node-based: references stay valid
+};
+
+static std::vector<Path> enumerate_paths(const Topo& t, int s, int d, int max_hops);
+
+const std::vector<Path>& candidate_paths(const Topo& t, int s, int d, int max_hops) {
+  auto& cc = const_cast<Topo&>(t).cand_cache;
+  {
+    static std::mutex init_mu;
+    std::lock_guard<std::mutex> lk(init_mu);
+    if (!cc) cc = std::make_shared<Topo::CandCache>();
+  }
+  std::lock_guard<std::mutex> lk(cc->mu);
+  auto key = std::make_tuple(s, d, max_hops);
+  auto it = cc->paths.find(key);
+  if (it == cc->paths.end()) it = cc->paths.emplace(key, enumerate_paths(t, s, d, max_hops)).first;
+  return it->second;
+}
+
+static std::vector<Path> enumerate_paths(const Topo& t, int s, int d, int max_hops) {
   std::vector<Path> out;
   std::vector<std::pair<int, Path>> stack{{s, Path{s}}};
   while (!stack.empty()) {
@@ -510,7 +544,7 @@ std::vector<NvPath> select_paths(Matrix& m, const std::string& func, int s, int 
   if (s == d) fail(FT_E_TOPOLOGY, "select_paths needs two distinct GPUs");
   t.check(s);
   t.check(d);
-  auto cands = candidate_paths(t, s, d);
+  const auto& cands = candidate_paths(t, s, d);
   SelectTrace local;
   SelectTrace& T = tr ? *tr : local;
   T = SelectTrace{};

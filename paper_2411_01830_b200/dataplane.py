@@ -11,9 +11,10 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import threading
 from dataclasses import dataclass, field
 
-from ._lib import LIB, BranchC, destroyer, DuplicateStore, MissingData, enc, json_out
+from ._lib import LIB, destroyer, DuplicateStore, MissingData, enc, json_out
 from .strategies import Strategy
 from .topology import BandwidthMatrix, Topology
 
@@ -133,6 +134,7 @@ class Stage:
 
 
 _LINK_KINDS = ("h2d", "d2h", "nv", "nvp_out", "nvp_in", "net")   # ft_link_kind
+_tls = threading.local()
 
 
 class TransferPlan:
@@ -171,21 +173,36 @@ class TransferPlan:
             return self._d["stages"]
         st = self.__dict__.get("_stages")
         if st is None:
-            n = C.c_int()
-            LIB.ft_plan_method(self._h, None, None, C.byref(n))
-            st = []
-            man, pinned, nb, b = C.c_int(), C.c_double(), C.c_int(), BranchC()
-            for si in range(n.value):
-                LIB.ft_plan_stage(self._h, si, C.byref(man), C.byref(pinned), C.byref(nb))
+            buf = getattr(_tls, "buf", None)
+            if buf is None:
+                buf = _tls.buf = (C.c_double * 4096)()
+            need = C.c_size_t()
+            if LIB.raw("ft_plan_pack")(self._h, buf, len(buf), C.byref(need)):
+                buf = (C.c_double * need.value)()
+                LIB.ft_plan_pack(self._h, buf, len(buf), C.byref(need))
+            v = memoryview(buf).cast("B")[:8 * need.value].cast("d").tolist()   # one C-level conversion
+            st, i = [], 1
+            for _ in range(int(v[0])):
+                managed, pinned, nb = v[i] != 0.0, v[i + 1], int(v[i + 2])
+                i += 3
                 brs = []
-                for bi in range(nb.value):
-                    LIB.ft_plan_branch(self._h, si, bi, C.byref(b))
-                    links = [(_LINK_KINDS[lk.kind], lk.a) if lk.kind in (3, 4) else (_LINK_KINDS[lk.kind], lk.a, lk.b)
-                             for lk in b.links[:b.n_links]]
-                    brs.append(Branch(links, b.bytes_share, None if b.cap_gbps != b.cap_gbps else b.cap_gbps,
-                                      None if b.reserved_gbps != b.reserved_gbps else b.reserved_gbps, b.fill_ms,
-                                      list(b.hop_caps[:b.n_caps])))
-                st.append(Stage(brs, bool(man.value), pinned.value))
+                for _ in range(nb):
+                    nl = int(v[i])
+                    i += 1
+                    links = []
+                    for _ in range(nl):
+                        k = int(v[i])
+                        links.append((_LINK_KINDS[k], int(v[i + 1])) if k in (3, 4)
+                                     else (_LINK_KINDS[k], int(v[i + 1]), int(v[i + 2])))
+                        i += 3
+                    nc = int(v[i])
+                    caps = v[i + 1:i + 1 + nc]
+                    i += 1 + nc
+                    share, cap, res, fill = v[i:i + 4]
+                    i += 4
+                    brs.append(Branch(links, share, None if cap != cap else cap, None if res != res else res, fill,
+                                      caps))
+                st.append(Stage(brs, managed, pinned))
             self._stages = st
         return st
 

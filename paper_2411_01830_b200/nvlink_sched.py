@@ -9,6 +9,7 @@ non-uniform fabrics and for decision parity with the reference.
 from __future__ import annotations
 
 import ctypes as C
+import threading
 import json
 from dataclasses import dataclass, field
 
@@ -59,13 +60,20 @@ def candidate_paths(topo: Topology, g_s: int, g_d: int, max_hops: int = MAX_HOPS
 _candidate_paths = candidate_paths
 
 
+_tls = threading.local()
+
+
 def select_paths(query: PathQuery) -> list:
     """nvlink_sched.py:64-133"""
     cap = MAX_CANDIDATES
-    buf = (NvPathC * cap)()
+    bufs = getattr(_tls, "bufs", None)
+    if bufs is None:
+        # per-thread output buffers (1000 paths + a 64 KiB trace: allocating and
+        # zeroing them on every call cost more than the selection itself)
+        bufs = _tls.bufs = ((NvPathC * cap)(), C.create_string_buffer(1 << 16))
+    buf, tbuf = bufs
+    tcap = len(tbuf)
     n = C.c_int()
-    tcap = 1 << 16
-    tbuf = C.create_string_buffer(tcap)
     LIB.ft_select_paths(query.matrix.handle, enc(query.func), int(query.g_s), int(query.g_d),
                         1 if query.allow_busy else 0, buf, cap, C.byref(n), tbuf, tcap)
     tr = json.loads(tbuf.value.decode())
