@@ -172,6 +172,8 @@ struct ft_pacer {
   int batch_chunks = 5;
   uint64_t chunk = 2000000;
   int staging_slots = 4;
+  uint64_t stage_chunk = 0;        // staging ring slot (bytes): 4 chunks, or FT_STAGE_CHUNK
+  bool fixed_stage_chunk = false;  // FT_STAGE_CHUNK: every piece is one full slot
   bool logging = false;
   ft::Arbiter arbs[2];  // per direction (engine.py:186-190)
   ft::Arbiter& arb_of(const Stage& st) { return arbs[st.dir]; }
@@ -295,7 +297,7 @@ struct ft_pacer {
     StagingRing r;
     DevGuard g(dev);
     void* p = nullptr;
-    ck(cudaMalloc(&p, (size_t)staging_slots * chunk), "staging ring cudaMalloc");
+    ck(cudaMalloc(&p, (size_t)staging_slots * stage_chunk), "staging ring cudaMalloc");
     r.buf = static_cast<uint8_t*>(p);
     r.slots = staging_slots;
     r.landed.resize(r.slots);
@@ -322,11 +324,17 @@ struct ft_pacer {
       return;
     }
     StagingRing& R = ring(r.dev);
-    for (uint64_t o = 0; o < n; o += chunk) {
-      uint64_t c = std::min<uint64_t>(chunk, n - o);
+    // pieces per route: 1/32 of it, between one chunk and a full slot. Each piece is
+    // a CE op + forward kernel; a 2 MB piece loses ~9 % of the link to per-op gaps
+    // (1 GiB through one staged route: 49.6 GB/s at 2 MB, 52.4 at 4, 53.4 at 8,
+    // 54.1 at 16, direct 54.5), a big one costs pipeline fill: 1/32 balances both
+    const uint64_t step = fixed_stage_chunk ? stage_chunk
+                                            : std::clamp<uint64_t>(r.len / 32 / 65536 * 65536, chunk, stage_chunk);
+    for (uint64_t o = 0; o < n; o += step) {
+      uint64_t c = std::min<uint64_t>(step, n - o);
       int s = R.next;
       R.next = (s + 1) % R.slots;
-      uint8_t* slot = R.buf + (uint64_t)s * chunk;
+      uint8_t* slot = R.buf + (uint64_t)s * stage_chunk;
       if (dir == 0) {
         // CE into the staging slot, forward kernel (NVLink push) into the target
         if (R.used[s]) ck(cudaStreamWaitEvent(r.ce, R.freed[s], 0), "wait slot freed");
@@ -777,6 +785,11 @@ int ft_pacer_create(double bw_all_gbps, int links, int batch_chunks, int64_t chu
   p->batch_chunks = batch_chunks;
   p->chunk = (uint64_t)chunk_bytes;
   p->staging_slots = std::max(2, staging_slots);
+  p->stage_chunk = 4 * (uint64_t)chunk_bytes;
+  if (const char* c = std::getenv("FT_STAGE_CHUNK")) {
+    p->stage_chunk = std::max<uint64_t>(1 << 16, std::atoll(c));
+    p->fixed_stage_chunk = true;
+  }
   p->logging = logging != 0;
   p->links = std::max(1, links);
   p->link_gbps[0] = p->link_gbps[1] = bw_all_gbps / p->links;
