@@ -213,6 +213,7 @@ struct ft_pacer {
   std::mutex hmu;
   std::condition_variable hcv;
   uint8_t* hring = nullptr;
+  uint64_t host_chunk = 0;  // pinned-ring slot = one worker memcpy + one DMA op (FT_HOST_CHUNK)
   std::vector<HostSlot> hslots;
   int hnext = 0;
 
@@ -388,8 +389,8 @@ struct ft_pacer {
       }
       return;
     }
-    for (uint64_t k = 0; k < n; k += chunk) {
-      jobs.push_back(Job{st.ticket, i, o + k, std::min<uint64_t>(chunk, n - k)});
+    for (uint64_t k = 0; k < n; k += host_chunk) {
+      jobs.push_back(Job{st.ticket, i, o + k, std::min<uint64_t>(host_chunk, n - k)});
       ++st.jobs;
     }
     jcv.notify_all();
@@ -639,7 +640,8 @@ struct ft_pacer {
     if (!owner && t < st.next_t - kLookahead * dur) return st.next_t - kLookahead * dur;
     int queued = 0;
     for (auto& b : st.inflight) queued += b.batches;
-    bool full = st.pinned ? queued + mult > kInflightBatches : st.jobs >= 2 * batch_chunks;
+    bool full = st.pinned ? queued + mult > kInflightBatches
+                          : st.jobs * host_chunk >= 2 * (uint64_t)batch_chunks * chunk;
     if (full) {
       if (!st.was_full) note(st, "full", (double)st.inflight.size());
       st.was_full = true;
@@ -715,7 +717,7 @@ struct ft_pacer {
       }
       HostSlot& hs = hslots[k];
       if (hs.last_dev >= 0) cudaEventSynchronize(hs.ev[hs.last_dev]);  // its previous DMA drained it
-      uint8_t* slot = hring + (uint64_t)k * chunk;
+      uint8_t* slot = hring + (uint64_t)k * host_chunk;
       const uint8_t* src = nullptr;
       {
         std::lock_guard<std::mutex> lk(mu);
@@ -798,9 +800,11 @@ int ft_pacer_create(double bw_all_gbps, int links, int batch_chunks, int64_t chu
     a.share = ft::PcieState{bw_all_gbps, batch_chunks, chunk_bytes, {}};
     a.batch_bytes = (double)(chunk_bytes * batch_chunks);
   }
-  uint64_t slots = std::max<uint64_t>(4, host_ring_bytes / p->chunk);
+  p->host_chunk = (uint64_t)chunk_bytes;
+  if (const char* c = std::getenv("FT_HOST_CHUNK")) p->host_chunk = std::max<uint64_t>(1 << 16, std::atoll(c));
+  uint64_t slots = std::max<uint64_t>(4, host_ring_bytes / p->host_chunk);
   void* h = nullptr;
-  cudaError_t e = cudaHostAlloc(&h, slots * p->chunk, cudaHostAllocPortable);
+  cudaError_t e = cudaHostAlloc(&h, slots * p->host_chunk, cudaHostAllocPortable);
   if (e != cudaSuccess) {
     ft::set_last_error(std::string("ft_pacer_create: pinned ring: ") + cudaGetErrorString(e));
     return FT_E_CUDA;
