@@ -51,6 +51,7 @@ class Record:
     start_ms: float = 0.0
     end_ms: float | None = None
     phases: dict = field(default_factory=lambda: {p: 0.0 for p in PHASES})
+    extra: dict = field(default_factory=dict)   # time outside the reference's phases (cFunc host compute)
 
 
 class _Models:
@@ -206,6 +207,7 @@ class Runtime:
             if gpu is None:
                 time.sleep(f.compute_ms / 1e3)              # cFunc on a host core
                 y = self._host_out(fid, out_bytes)
+                rec.extra["cfunc"] = rec.extra.get("cfunc", 0.0) + now() - t_c
             else:
                 with self.gpu_locks[gpu], torch.cuda.device(gpu):   # GPU FIFO (temporal sharing)
                     t_q = now()
@@ -261,7 +263,12 @@ class Runtime:
                            "completed": rep["requests_completed"], "offered": len(reqs),
                            **({"worst": {"rid": worst.rid, "arrival_ms": round(worst.arrival_ms, 1),
                                          "latency_ms": round(worst.end_ms - worst.arrival_ms, 2),
-                                         "phases": {k: round(v, 2) for k, v in worst.phases.items() if v}}}
+                                         "dispatch_ms": round(worst.start_ms - worst.arrival_ms, 2),
+                                         "cfunc_ms": round(worst.extra.get("cfunc", 0.0), 2),
+                                         "phases": {k: round(v, 2) for k, v in worst.phases.items() if v},
+                                         "unaccounted_ms": round(worst.end_ms - worst.start_ms
+                                                                 - sum(worst.phases.values())
+                                                                 - worst.extra.get("cfunc", 0.0), 2)}}
                               if worst is not None and not ok else {})})
             return ok, rep
 
