@@ -924,7 +924,10 @@ def measure_pcie_gbps(gpus, nbytes: int = 64 << 20, reps: int = 12, margin: floa
     times ``margin``. The pacer must not hand out more than the link delivers
     (its shares would stop isolating tenants) nor much less (a lone stage
     would be throttled below the link)."""
-    host = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    # a pinned buffer the CPU never wrote: DMA out of lines the CPU holds dirty in its
+    # caches runs at ~21 GB/s on the B200 hosts (vs 55 from DRAM), and a calibration
+    # from a just-written buffer read 20-38 GB/s (tools/diag_calib2.py)
+    host = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
     rates = []
     for g in gpus:
         dst = torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{g}")
