@@ -34,7 +34,6 @@ writing before ``commit``; the daemon's fetch has landed before it replies.
 
 from __future__ import annotations
 
-import ctypes as C
 import itertools
 import math
 import mmap
@@ -190,7 +189,7 @@ class TubeDaemon:
             g, n = int(msg["gpu"]), int(msg["nbytes"])
             t = tube.empty((max(1, n),), torch.uint8, device=g)              # pool-backed output
             t._ft_alloc = True  # noqa: SLF001
-            dev.Ev(g).record(tube._stream(g)).synchronize()  # noqa: SLF001 - its previous users are done
+            tube.sync_stream(g)                # the block's previous users are done before the client writes
             self._reply_block(conn, g, t._ft_block, {"token": self._hold(conn, t), "nbytes": n})  # noqa: SLF001
         elif op == "commit":
             t = self._take(conn, int(msg["token"]))
@@ -239,7 +238,7 @@ class TubeDaemon:
                 blk = dst._ft_block  # noqa: SLF001
             # the consumer stream is ordered after the bytes (a host->GPU stage's last
             # batch is issued before fetch returns; the stream waits on its join events)
-            torch.cuda.current_stream(g).synchronize()
+            tube.sync_stream(g)
             self._reply_block(conn, g, blk, {"token": self._hold(conn, t), "nbytes": t.nbytes,
                                              "dtype": str(t.dtype), "shape": list(t.shape)})
         elif op == "fetch_host":

@@ -586,6 +586,11 @@ class FaaSTube:
             self.fetch(did, out=out, consumer=consumer)
         return [out for _, out in items]
 
+    def sync_stream(self, g: int):
+        """Block the host until the caller's current stream on GPU ``g`` drained
+        (another process is about to touch what it ordered)."""
+        dev.Ev(g).record(self._stream(g)).synchronize()
+
     def wait(self, timeout_ms: float = -1.0):
         """Block the host until every host->GPU stage submitted so far has landed."""
         with self._lock:
