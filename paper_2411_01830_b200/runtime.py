@@ -257,19 +257,9 @@ class Runtime:
             rep = rt.run([(wf, where, reqs)], duration_s, drain_s=30, idle_s=0.0)
             ok = not reqs or (rep["requests_completed"] >= 0.95 * len(reqs) and rep.get("p99_ms") is not None
                               and rep["p99_ms"] <= slo)       # no arrival drawn: vacuously met
-            done = [r for r in rt.records if r.end_ms is not None]
-            worst = max(done, key=lambda r: r.end_ms - r.arrival_ms, default=None)
             trials.append({"rate": round(rate, 3), "ok": ok, "p99_ms": rep.get("p99_ms"),
                            "completed": rep["requests_completed"], "offered": len(reqs),
-                           **({"worst": {"rid": worst.rid, "arrival_ms": round(worst.arrival_ms, 1),
-                                         "latency_ms": round(worst.end_ms - worst.arrival_ms, 2),
-                                         "dispatch_ms": round(worst.start_ms - worst.arrival_ms, 2),
-                                         "cfunc_ms": round(worst.extra.get("cfunc", 0.0), 2),
-                                         "phases": {k: round(v, 2) for k, v in worst.phases.items() if v},
-                                         "unaccounted_ms": round(worst.end_ms - worst.start_ms
-                                                                 - sum(worst.phases.values())
-                                                                 - worst.extra.get("cfunc", 0.0), 2)}}
-                              if worst is not None and not ok else {})})
+                           **({"worst": rep["worst"]} if "worst" in rep and not ok else {})})
             return ok, rep
 
         lo, hi, last = 0.0, None, None
@@ -409,4 +399,15 @@ class Runtime:
             for r in done:
                 per.setdefault(r.workflow, []).append(r.end_ms - r.arrival_ms)
             out["per_workflow_p99_ms"] = {k: round(nearest_rank(v, 99), 4) for k, v in sorted(per.items())}
+            out["worst"] = self.breakdown(max(done, key=lambda r: r.end_ms - r.arrival_ms))
         return out
+
+    @staticmethod
+    def breakdown(r: Record) -> dict:
+        """Where one request's latency went: dispatch delay, the reference's
+        phases, cFunc host compute and what no phase covers."""
+        return {"rid": r.rid, "workflow": r.workflow, "arrival_ms": round(r.arrival_ms, 1),
+                "latency_ms": round(r.end_ms - r.arrival_ms, 2), "dispatch_ms": round(r.start_ms - r.arrival_ms, 2),
+                "cfunc_ms": round(r.extra.get("cfunc", 0.0), 2),
+                "phases": {k: round(v, 2) for k, v in r.phases.items() if v},
+                "unaccounted_ms": round(r.end_ms - r.start_ms - sum(r.phases.values()) - r.extra.get("cfunc", 0.0), 2)}
