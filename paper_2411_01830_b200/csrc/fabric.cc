@@ -41,8 +41,14 @@ void path_json(JsonOut& o, const Path& p) {
 }  // namespace
 
 // ------------------------------------------------------------ Topo
+struct Topo::CandCache {
+  std::mutex mu;
+  std::map<std::tuple<int, int, int>, std::vector<Path>> paths;  // node-based: references stay valid
+};
+
 std::unique_ptr<Topo> Topo::from_json(const std::string& text) {
   auto t = std::make_unique<Topo>();
+  t->cand_cache = std::make_shared<Topo::CandCache>();
   JVal doc = json_parse(text);
   if (doc.t != JVal::OBJ) fail(FT_E_TOPOLOGY, "malformed topology document: not an object");
   const JVal* name = doc.get("name");
@@ -363,20 +369,10 @@ std::string Matrix::state_json() const {
 }
 
 // ------------------------------------------------------------ Alg. 1
-struct Topo::CandCache {
-  std::mutex mu;
-  std::map<std::tuple<int, int, int>, std::vector<Path>> paths;  // node-based: references stay valid
-};
-
 static std::vector<Path> enumerate_paths(const Topo& t, int s, int d, int max_hops);
 
 const std::vector<Path>& candidate_paths(const Topo& t, int s, int d, int max_hops) {
-  auto& cc = const_cast<Topo&>(t).cand_cache;
-  {
-    static std::mutex init_mu;
-    std::lock_guard<std::mutex> lk(init_mu);
-    if (!cc) cc = std::make_shared<Topo::CandCache>();
-  }
+  Topo::CandCache* cc = t.cand_cache.get();  // created with the topology (Topo::from_json)
   std::lock_guard<std::mutex> lk(cc->mu);
   auto key = std::make_tuple(s, d, max_hops);
   auto it = cc->paths.find(key);
