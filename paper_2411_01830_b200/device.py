@@ -284,7 +284,6 @@ class DevicePool:
         # cuMemMap waits for the GPU's running kernels (measured 30-80 ms while tenants
         # compute) — a cost for this thread, not for the request that needs the block
         self.spare_cap_bytes = int(os.environ.get("FT_SPARE_CAP_BYTES", spare_cap_bytes))
-        self._peak_in_use = {}     # class bytes -> most blocks of it in use at once (spares to keep)
         self._spare_q = []
         self._spare_cv = threading.Condition(self._lock)
         self._spare_thread = None
@@ -305,23 +304,20 @@ class DevicePool:
 
     # ---- spare mappings (background growth)
     def _want_spare(self, class_bytes: int):
-        """Called with the lock held after a growth of ``class_bytes``: keep as
-        many mapped spares of the class as it ever had blocks in use at once
-        (1-4) — a burst of same-class tenants otherwise maps one block each on
-        the request path (60-100 ms stores under load in config 5)."""
+        """Called with the lock held after a growth of ``class_bytes``: map one
+        spare of the class in the background (the next growth takes it instead
+        of mapping on the request path). More spares per class were tried —
+        as many as the class ever had in use at once — and did not remove the
+        first-burst stalls (the concurrent tenants of a burst each grow before
+        any spare exists) while doubling the mapped memory of bursty classes."""
         if self._spare_q is None or self.spare_cap_bytes <= 0:
             return
-        in_use = sum(1 for b in self.policy._blocks.values() if b.in_use and b.class_bytes == class_bytes)  # noqa: SLF001
-        peak = self._peak_in_use[class_bytes] = max(self._peak_in_use.get(class_bytes, 0), in_use)
-        want = max(1, min(4, peak))
-        have = sum(1 for r in self._released if r[2] == class_bytes) + self._spare_q.count(class_bytes)
-        parked = sum(r[2] for r in self._released) + sum(self._spare_q)
-        while have < want and parked + class_bytes <= self.spare_cap_bytes:
-            self._spare_q.append(class_bytes)
-            have += 1
-            parked += class_bytes
-        if not self._spare_q:
+        parked = sum(r[2] for r in self._released)
+        if parked + class_bytes > self.spare_cap_bytes:
             return
+        if any(r[2] == class_bytes for r in self._released) or class_bytes in self._spare_q:
+            return
+        self._spare_q.append(class_bytes)
         if self._spare_thread is None:
             self._spare_thread = threading.Thread(target=self._spare_loop, name=f"faastube-spares{self.device}",
                                                   daemon=True)
