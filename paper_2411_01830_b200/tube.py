@@ -133,6 +133,8 @@ class FaaSTube:
                                2 * default_ring_capacity(len(roots), batch_chunks * chunk_bytes),
                                logging=bool(os.environ.get("FT_TRACE")), links=len(roots))
         self._tickets = []           # (ticket, keep-alive refs) until the stage has landed
+        self.slow_stores = collections.deque(maxlen=64)   # stores over 10 ms: (alloc ms, locked ms, bytes)
+        self._pending = set()        # ("pressure" | "prefetch", gpu): decided under the lock, run after it
         self._t0 = time.perf_counter()
         self._objs: dict[int, _Obj] = {}
         self._lock = threading.RLock()
@@ -269,6 +271,7 @@ class FaaSTube:
         migration under memory pressure (datastore.py:192-222)."""
         # pinned host buffers are allocated before taking the tube lock (cudaHostAlloc
         # can take milliseconds and must not stall other tenants' calls)
+        t0 = time.perf_counter()
         pre_host = pre_blk = None
         if output.is_cuda and (response or not self.strategy.gpu_store()):
             pre_host = self._pinned(output.nbytes)
@@ -278,8 +281,14 @@ class FaaSTube:
                 # the pool block for the snapshot: growth maps physical memory, which
                 # must not happen under the tube lock
                 pre_blk = self.pools[output.device.index].allocate(output.nbytes)
+        t1 = time.perf_counter()
         try:
             stage = self._store_locked(data_id, output, response, producer, consumers, queue_pos, pre_host, pre_blk)
+            if self._pending:
+                self._drain_pending()
+            t2 = time.perf_counter()
+            if t2 - t0 > 0.01:   # slow stores, for diagnosis: (ms allocating, ms in the locked part, bytes)
+                self.slow_stores.append((round(1e3 * (t1 - t0), 2), round(1e3 * (t2 - t1), 2), output.nbytes))
         except BaseException:
             if pre_blk is not None:
                 self.pools[output.device.index].free(pre_blk, list(pre_blk.fences))
@@ -380,7 +389,7 @@ class FaaSTube:
             self.stats["stores"] += 1
             if obj.block is not None and self.strategy.migration != "none" and \
                     self._stored_on(obj.gpu) > self.capacity_limit:
-                self._check_pressure(obj.gpu)                # engine.py:685-702
+                self._pending.add(("pressure", obj.gpu))      # engine.py:685-702, after the lock
         return stage
 
     # ------------------------------------------------ queue-aware migration (§8f row 1)
@@ -416,28 +425,64 @@ class FaaSTube:
                 for o in objs]
         return objs, recs
 
-    def _check_pressure(self, g):
-        """Store cap exceeded -> migrate the objects whose consumers sit farthest
-        back in the queue to host memory (datastore.py:192-222)."""
+    def _drain_pending(self):
+        """Migration (store cap exceeded) and prefetch (room freed) decided under
+        the tube lock, executed after it: the victims / candidates are chosen
+        and pinned under the lock, their pinned host buffers or pool blocks are
+        allocated outside it (cudaHostAlloc of a 512 MB buffer or a VMM growth
+        under the lock stalled every tenant's store and fetch for 40-110 ms in
+        config 5), then the moves are issued under the lock again. Runs in
+        the caller's thread before its store/fetch/release returns, so the
+        reference's synchronous semantics hold for the caller."""
+        while True:
+            with self._lock:
+                if not self._pending:
+                    return
+                kind, g = self._pending.pop()
+                chosen = self._plan_migration(g) if kind == "pressure" else self._plan_prefetch(g)
+                for o in chosen:
+                    o.pins += 1
+            if not chosen:
+                continue
+            bufs = []
+            try:
+                for o in chosen:
+                    bufs.append(self._pinned(o.nbytes) if kind == "pressure" else self.pools[g].allocate(o.nbytes))
+            finally:
+                with self._lock:
+                    for i, o in enumerate(chosen):
+                        o.pins -= 1
+                        buf = bufs[i] if i < len(bufs) else None
+                        if kind == "pressure":
+                            if buf is not None and o.block is not None and o.pins == 0 and not o.retired:
+                                self._migrate_out(o, buf)
+                            else:
+                                self._maybe_free(o)
+                        else:
+                            if buf is not None and o.host is not None and o.block is None and not o.retired:
+                                self._reload(o, g, buf)
+                            elif buf is not None:
+                                self.pools[g].free(buf, list(buf.fences))
+
+    def _plan_migration(self, g) -> list:
+        """Store cap exceeded -> the objects whose consumers sit farthest back in
+        the queue go to host memory (datastore.py:192-222)."""
         stored = self._stored_on(g)
         if stored <= self.capacity_limit:
-            return
+            return []
         from .datastore import migration_plan
         objs, recs = self._policy_objs(g)
         try:
             plan = migration_plan(recs, stored - self.capacity_limit, self.strategy.migration)
         except Exception:  # noqa: BLE001 - HardPressure: nothing migratable (engine.py:696-697)
-            return
+            return []
         by_id = {o.did: o for o in objs}
-        for action, rec in plan:
-            o = by_id[rec.data_id]
-            if action == "migrate" and o.block is not None and o.pins == 0:
-                self._migrate_out(o)
+        return [by_id[rec.data_id] for action, rec in plan
+                if action == "migrate" and by_id[rec.data_id].block is not None and by_id[rec.data_id].pins == 0]
 
-    def _migrate_out(self, o: _Obj):
+    def _migrate_out(self, o: _Obj, host: torch.Tensor):
         """D2H on the GPU's own link, then the block goes back to the pool (engine.py:704-715)."""
         g = o.gpu
-        host = self._pinned(o.nbytes)
         ce = self._ce[g][1]
         o.ready.wait(ce)
         dev.pcie_copy(host.data_ptr(), o.block.ptr, o.nbytes, False, g, ce)
@@ -452,36 +497,44 @@ class FaaSTube:
         self.stats["migrated_bytes"] += o.nbytes
         self.stats["bytes_d2h"] += o.nbytes
 
-    def _maybe_prefetch(self, g):
+    def _plan_prefetch(self, g) -> list:
         """Room freed -> reload migrated objects, nearest consumer first (datastore.py:225-238)."""
         if not any(o.home == g and o.block is None and o.host is not None for o in self._objs.values()):
-            return                                    # nothing migrated off this GPU
+            return []                                 # nothing migrated off this GPU
         free = self.capacity_limit - self._stored_on(g)
         if free <= 0:
-            return
+            return []
         from .datastore import prefetch_back
         objs, recs = self._policy_objs(g)
         by_id = {o.did: o for o in objs}
-        for rec in prefetch_back(recs, free):
-            o = by_id[rec.data_id]
-            if o.host is None or o.block is not None:
-                continue
-            blk = self.pools[g].allocate(o.nbytes)
-            ce = self._ce[g][0]
-            if o.ready is not None:
-                o.ready.wait(ce)
-            blk.wait_fences(ce)
-            dev.pcie_copy(blk.ptr, o.host.data_ptr(), o.nbytes, True, g, ce)
-            ev = dev.Ev(g).record(ce)
-            self._account(o, -1)
-            o.block, o.ready, o.gpu, o.host = blk, ev, g, None
-            self._account(o, 1)
-            self.index.relocate(o.did, self._loc(g))
-            self.stats["reload_bytes"] += o.nbytes
-            self.stats["bytes_h2d"] += o.nbytes
+        return [by_id[rec.data_id] for rec in prefetch_back(recs, free)
+                if by_id[rec.data_id].host is not None and by_id[rec.data_id].block is None]
+
+    def _reload(self, o: _Obj, g: int, blk):
+        ce = self._ce[g][0]
+        if o.ready is not None:
+            o.ready.wait(ce)
+        blk.wait_fences(ce)
+        dev.pcie_copy(blk.ptr, o.host.data_ptr(), o.nbytes, True, g, ce)
+        ev = dev.Ev(g).record(ce)
+        self._account(o, -1)
+        o.block, o.ready, o.gpu, o.host = blk, ev, g, None
+        self._account(o, 1)
+        self.index.relocate(o.did, self._loc(g))
+        self.stats["reload_bytes"] += o.nbytes
+        self.stats["bytes_h2d"] += o.nbytes
 
     def fetch(self, data_id: int, device: int | None = None, out: torch.Tensor | None = None,
               consumer: str = "func", slo_ms: float | None = None, infer_ms: float | None = None) -> torch.Tensor:
+        """FaaSTube.fetch(index, input) — see ``_fetch``."""
+        try:
+            return self._fetch(data_id, device, out, consumer, slo_ms, infer_ms)
+        finally:
+            if self._pending:
+                self._drain_pending()
+
+    def _fetch(self, data_id: int, device: int | None = None, out: torch.Tensor | None = None,
+               consumer: str = "func", slo_ms: float | None = None, infer_ms: float | None = None) -> torch.Tensor:
         """FaaSTube.fetch(index, input) — dataplane.py:176-186 + engine.py:440-511.
 
         ``device=None`` fetches into host memory. With ``out`` the bytes land
@@ -607,6 +660,8 @@ class FaaSTube:
             if obj is not None:
                 obj.remaining = 0
                 self._retire(obj)
+        if self._pending:
+            self._drain_pending()
 
     def response(self, data_id: int) -> torch.Tensor:
         """Host copy of a ``store(..., response=True)`` output (waits for it)."""
@@ -721,7 +776,7 @@ class FaaSTube:
             rw, last = self.pools[blk.device].commit_retire(self.index, obj.did, blk, fences, obj.producer)
             self._push_due(blk.device, rw, last, self.now_ms())
             if self.strategy.migration != "none":
-                self._maybe_prefetch(blk.device)             # engine.py:678-679, 717-736
+                self._pending.add(("prefetch", blk.device))  # engine.py:678-679, 717-736
             return
         self.index.drop(obj.did)
         self._maybe_free(obj)
@@ -736,7 +791,7 @@ class FaaSTube:
             self.pools[blk.device].free(blk, fences)
             self._push_shrink(blk.device, obj.producer, self.now_ms())
             if self.strategy.migration != "none":
-                self._maybe_prefetch(blk.device)             # engine.py:678-679, 717-736
+                self._pending.add(("prefetch", blk.device))  # engine.py:678-679, 717-736
 
     def _unpin(self, obj):
         with self._lock:
