@@ -312,12 +312,20 @@ class DevicePool:
         any spare exists) while doubling the mapped memory of bursty classes."""
         if self._spare_q is None or self.spare_cap_bytes <= 0:
             return
-        parked = sum(r[2] for r in self._released)
-        if parked + class_bytes > self.spare_cap_bytes:
+        # the spare is rounded up to a power of two of the 2 MiB granule: growth reuses a
+        # parked block of up to twice its class, so one spare serves every class in
+        # (P/2, P] — payload sizes drawn per request (config 4's detector outputs) land
+        # in classes never seen before, and each new class otherwise mapped on the
+        # request path (25 ms under load, one request over its SLO)
+        gran = 2 << 20
+        spare = gran << max(0, (int(class_bytes) - 1) // gran).bit_length()
+        parked = sum(r[2] for r in self._released) + sum(self._spare_q)
+        if parked + spare > self.spare_cap_bytes:
             return
-        if any(r[2] == class_bytes for r in self._released) or class_bytes in self._spare_q:
+        if any(class_bytes <= r[2] <= 2 * class_bytes for r in self._released) or \
+                any(class_bytes <= q <= 2 * class_bytes for q in self._spare_q):
             return
-        self._spare_q.append(class_bytes)
+        self._spare_q.append(spare)
         if self._spare_thread is None:
             self._spare_thread = threading.Thread(target=self._spare_loop, name=f"faastube-spares{self.device}",
                                                   daemon=True)
