@@ -209,3 +209,25 @@ def test_pool_spares_serve_growth(dev):
     pool.free(a)
     pool.free(b)
     pool.close()
+
+
+def test_pool_spare_is_rounded_up_and_serves_nearby_classes(dev):
+    """A growth of a 40 MB class maps a 64 MB spare (a power of two of the 2 MiB
+    granule); a later growth of any class in (32, 64] MB takes it instead of
+    mapping on the request path."""
+    import time
+    pool = dev.DevicePool(0, "autoscale", floor_bytes=0.0)
+    a = pool.allocate(40 << 20)
+    deadline = time.time() + 5
+    while pool.spares_mapped < 1 and time.time() < deadline:
+        time.sleep(0.01)
+    assert pool.spares_mapped == 1 and pool.released_bytes == 64 << 20
+    b = pool.allocate(60 << 20)                     # a class never seen: served by the spare
+    assert pool.released_bytes < 64 << 20 or pool.spares_mapped > 1
+    t = dev.as_tensor(b.ptr, 60 << 20, 0)
+    t.fill_(5)
+    torch.cuda.synchronize()
+    assert int(t.float().mean()) == 5
+    pool.free(a)
+    pool.free(b)
+    pool.close()
