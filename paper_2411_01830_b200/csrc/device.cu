@@ -9,6 +9,7 @@
 // read+write vs 6.40). So PCIe legs run on the CE, everything after the PCIe
 // hop runs in our kernels.
 #include <cuda.h>
+#include <chrono>
 #include <cuda_runtime.h>
 #include <sys/socket.h>
 #include <sys/un.h>
@@ -682,36 +683,66 @@ int ft_vmm_block_map(ft_vmm_pool* p, uint64_t bytes, uint64_t* block, void** dpt
   }
   Drv* d = drv();
   size_t sz = (bytes + p->gran - 1) / p->gran * p->gran;
-  std::lock_guard<std::mutex> lk(p->mu);
   size_t off = SIZE_MAX;
-  for (auto& kv : p->free_va)
-    if (kv.second >= sz) {
-      off = kv.first;
-      break;
+  {
+    // only the VA bookkeeping is under the pool mutex: cuMemCreate/Map/SetAccess can
+    // take tens of ms while the GPU is busy, and a request's growth must not queue
+    // behind the background spare thread's mapping
+    std::lock_guard<std::mutex> lk(p->mu);
+    for (auto& kv : p->free_va)
+      if (kv.second >= sz) {
+        off = kv.first;
+        break;
+      }
+    if (off == SIZE_MAX) {
+      ft::set_last_error("VMM pool virtual range exhausted");
+      return FT_E_OOM;
     }
-  if (off == SIZE_MAX) {
-    ft::set_last_error("VMM pool virtual range exhausted");
-    return FT_E_OOM;
+    size_t len = p->free_va[off];
+    p->free_va.erase(off);
+    if (len > sz) p->free_va[off + sz] = len - sz;
   }
-  CU_RT(cudaSetDevice(p->device));
+  auto give_back_va = [&] {
+    std::lock_guard<std::mutex> lk(p->mu);
+    p->free_va[off] = sz;  // (not coalesced with neighbours: the range stays usable for its size)
+  };
+  static const bool trace = std::getenv("FT_VMM_TRACE") != nullptr;
+  auto t0 = std::chrono::steady_clock::now();
+  cudaError_t ce = cudaSetDevice(p->device);
+  if (ce != cudaSuccess) {
+    give_back_va();
+    return cuda_fail(ce, "cudaSetDevice");
+  }
   CUmemAllocationProp prop = block_prop(p->device);
   CUmemGenericAllocationHandle h;
-  CU_DRV(d->create(&h, sz, &prop, 0));
+  CUresult r = d->create(&h, sz, &prop, 0);
+  if (r != CUDA_SUCCESS) {
+    give_back_va();
+    return cu_fail(r, "cuMemCreate");
+  }
+  auto t1 = std::chrono::steady_clock::now();
   CUdeviceptr va = p->base + off;
-  CUresult r = d->map(va, sz, 0, h, 0);
+  r = d->map(va, sz, 0, h, 0);
   if (r != CUDA_SUCCESS) {
     d->release(h);
+    give_back_va();
     return cu_fail(r, "cuMemMap");
   }
+  auto t2 = std::chrono::steady_clock::now();
   int rc = grant_access(d, va, sz, p->device, true);
   if (rc) {
     d->unmap(va, sz);
     d->release(h);
+    give_back_va();
     return rc;
   }
-  size_t len = p->free_va[off];
-  p->free_va.erase(off);
-  if (len > sz) p->free_va[off + sz] = len - sz;
+  auto t3 = std::chrono::steady_clock::now();
+  if (trace) {
+    auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+    std::fprintf(stderr, "[ft_vmm] map %zu MB: create %.2f ms, map %.2f ms, access %.2f ms\n", sz >> 20,
+                 ms(t0, t1), ms(t1, t2), ms(t2, t3));
+  }
+  std::lock_guard<std::mutex> lk(p->mu);
   uint64_t id = p->next_id++;
   p->blocks[id] = Block{h, va, sz};
   p->mapped += sz;
