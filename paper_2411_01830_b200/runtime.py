@@ -270,10 +270,14 @@ class Runtime:
 
         def trial(rate):
             reqs = build_requests_for(wf, pattern, rate, duration_s, seed)
-            # a daemon that has been serving this rate: replay the trace's first
-            # requests untimed (the pool may have shrunk while the previous trial drained)
-            Runtime.warm_daemon(tube, [(wf, where, build_requests_for(wf, pattern, max(rate, 4.0), 0.5, seed + 1))],
-                                compute, 0.5)
+            # a daemon that has been serving this traffic: the trial's own requests
+            # replayed untimed first, 5x compressed in time. Payload sizes are drawn per
+            # request, and the first store of a size class the pool never held maps a
+            # block (a cuMemCreate of up to 192 MB: 25-95 ms) — one such store decided
+            # whole trials (p99 of 15 requests is their maximum)
+            warm = [Request(r.rid, r.workflow, r.arrival_ms / 5.0, r.edge_bytes, r.fired, r.input_bytes,
+                            r.response_bytes) for r in reqs]
+            Runtime(tube, compute=compute).run([(wf, where, warm)], duration_s / 5.0, drain_s=60, idle_s=0.0)
             rt = Runtime(tube, compute=compute)
             rep = rt.run([(wf, where, reqs)], duration_s, drain_s=30, idle_s=0.0)
             ok = not reqs or (rep["requests_completed"] >= 0.95 * len(reqs) and rep.get("p99_ms") is not None
