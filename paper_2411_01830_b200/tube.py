@@ -631,12 +631,15 @@ class FaaSTube:
                 s = self._stream(g)
                 dev.wait_events(s, [o.ready for o, _ in group])
                 dev.copy_batch([(out.data_ptr(), o.block.ptr, o.nbytes) for o, out in group], g, s)
+                done = dev.Ev(g).record(s)     # one fence for every block the batch read
                 for o, _ in group:
                     self.stats["bytes_local"] += o.nbytes
                     self.stats["fetches"] += 1
-                    self._consumed(o)          # frees fence on this stream, after the batch copy
+                    self._consumed(o, done)
         for did, out in rest:
             self.fetch(did, out=out, consumer=consumer)
+        if self._pending:
+            self._drain_pending()
         return [out for _, out in items]
 
     def sync_stream(self, g: int):
@@ -752,12 +755,12 @@ class FaaSTube:
                 slo_ms if slo_ms else 1e9, infer_ms if infer_ms is not None else 0.0,
                 min(min(b.hop_caps) for b in br), host.data_ptr(), obj.block.ptr, g, obj.nbytes, routes, s)
 
-    def _consumed(self, obj: _Obj):
+    def _consumed(self, obj: _Obj, fence=None):
         obj.remaining -= 1
         if obj.remaining <= 0:
-            self._retire(obj)
+            self._retire(obj, fence)
 
-    def _retire(self, obj: _Obj):
+    def _retire(self, obj: _Obj, fence=None):
         """engine.py:667-679: last consumer done -> drop index entry, free block."""
         if obj.retired:
             return
@@ -769,7 +772,9 @@ class FaaSTube:
             # drop the index entry, return the block (fenced on its last users) and re-arm
             # the shrink timer in one FFI call (dataplane.py:98-101, datastore.py:146-149)
             obj.block = None
-            ev = dev.Ev(blk.device).record(self._stream(blk.device))
+            # the caller's last read of the block: an event on its stream (or the one
+            # a batched fetch recorded after its copy)
+            ev = fence if fence is not None else dev.Ev(blk.device).record(self._stream(blk.device))
             fences = [ev] + obj.readers + ([obj.ready] if obj.ready is not None else [])
             obj.readers = []
             self.index._meta.pop(obj.did, None)
