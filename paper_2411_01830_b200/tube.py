@@ -284,15 +284,13 @@ class FaaSTube:
         t1 = time.perf_counter()
         try:
             stage = self._store_locked(data_id, output, response, producer, consumers, queue_pos, pre_host, pre_blk)
-            if self._pending:
-                self._drain_pending()
-            t2 = time.perf_counter()
-            if t2 - t0 > 0.01:   # slow stores, for diagnosis: (ms allocating, ms in the locked part, bytes)
-                self.slow_stores.append((round(1e3 * (t1 - t0), 2), round(1e3 * (t2 - t1), 2), output.nbytes))
         except BaseException:
             if pre_blk is not None:
                 self.pools[output.device.index].free(pre_blk, list(pre_blk.fences))
             raise
+        t2 = time.perf_counter()
+        if t2 - t0 > 0.01:   # slow stores, for diagnosis: (ms allocating, ms in the locked part, bytes)
+            self.slow_stores.append((round(1e3 * (t1 - t0), 2), round(1e3 * (t2 - t1), 2), output.nbytes))
         if stage is not None:
             # managed GPU->host response stage (engine.py:414-423 -> 537-575), paced
             # by the d2h arbiter outside the tube lock; the object stays pinned
@@ -306,6 +304,8 @@ class FaaSTube:
                     self._tickets.append((ticket, obj.response_host, None))
             finally:
                 self._unpin(obj)
+        if self._pending:
+            self._drain_pending()                         # migration decided by this store
 
     def _store_locked(self, data_id, output, response, producer, consumers, queue_pos, pre_host, pre_blk):
         """Returns (obj, pacer.submit_d2h args) when a managed response stage must be submitted."""
@@ -527,11 +527,10 @@ class FaaSTube:
     def fetch(self, data_id: int, device: int | None = None, out: torch.Tensor | None = None,
               consumer: str = "func", slo_ms: float | None = None, infer_ms: float | None = None) -> torch.Tensor:
         """FaaSTube.fetch(index, input) — see ``_fetch``."""
-        try:
-            return self._fetch(data_id, device, out, consumer, slo_ms, infer_ms)
-        finally:
-            if self._pending:
-                self._drain_pending()
+        res = self._fetch(data_id, device, out, consumer, slo_ms, infer_ms)
+        if self._pending:
+            self._drain_pending()          # prefetch made possible by this consumer's retire
+        return res
 
     def _fetch(self, data_id: int, device: int | None = None, out: torch.Tensor | None = None,
                consumer: str = "func", slo_ms: float | None = None, infer_ms: float | None = None) -> torch.Tensor:
