@@ -135,6 +135,7 @@ class FaaSTube:
         self._tickets = []           # (ticket, keep-alive refs) until the stage has landed
         self.slow_stores = collections.deque(maxlen=64)   # stores over 10 ms: (alloc ms, locked ms, bytes)
         self._pending = set()        # ("pressure" | "prefetch", gpu): decided under the lock, run after it
+        self._migrating = {}         # gpu -> bytes of migration victims being moved out
         self._t0 = time.perf_counter()
         self._objs: dict[int, _Obj] = {}
         self._lock = threading.RLock()
@@ -442,6 +443,8 @@ class FaaSTube:
                 chosen = self._plan_migration(g) if kind == "pressure" else self._plan_prefetch(g)
                 for o in chosen:
                     o.pins += 1
+                moving = sum(o.nbytes for o in chosen) if kind == "pressure" else 0
+                self._migrating[g] = self._migrating.get(g, 0) + moving   # a concurrent plan sees them gone
             if not chosen:
                 continue
             bufs = []
@@ -450,6 +453,7 @@ class FaaSTube:
                     bufs.append(self._pinned(o.nbytes) if kind == "pressure" else self.pools[g].allocate(o.nbytes))
             finally:
                 with self._lock:
+                    self._migrating[g] -= moving
                     for i, o in enumerate(chosen):
                         o.pins -= 1
                         buf = bufs[i] if i < len(bufs) else None
@@ -467,7 +471,7 @@ class FaaSTube:
     def _plan_migration(self, g) -> list:
         """Store cap exceeded -> the objects whose consumers sit farthest back in
         the queue go to host memory (datastore.py:192-222)."""
-        stored = self._stored_on(g)
+        stored = self._stored_on(g) - self._migrating.get(g, 0)    # minus moves already under way
         if stored <= self.capacity_limit:
             return []
         from .datastore import migration_plan
