@@ -53,3 +53,41 @@ def test_lru_policy_evicts_oldest():
     assert torch.equal(got, xs[0])
     assert tube._accounts_consistent()
     tube.close()
+
+
+def test_concurrent_stores_under_pressure():
+    """Four tenants store 40 MB objects at once against a 100 MB store cap: the
+    migration planned under the tube lock and executed outside it keeps every
+    object fetchable and bit-exact, and the store accounting consistent."""
+    import threading
+    from paper_2411_01830_b200.tube import FaaSTube
+    tube = FaaSTube("faastube", pool_floor_bytes=0.0, capacity_limit_bytes=100 * MB)
+    xs = [torch.randint(0, 256, (40 * MB,), dtype=torch.uint8, device="cuda:0") for _ in range(8)]
+    torch.cuda.synchronize()
+    ids = [None] * len(xs)
+    errs = []
+
+    def tenant(k):
+        try:
+            for i in range(k, len(xs), 4):
+                d = tube.unique_id()
+                tube.store(d, xs[i], producer=f"p{k}", queue_pos=i)
+                torch.cuda.current_stream().synchronize()
+                ids[i] = d
+        except Exception as e:  # noqa: BLE001
+            errs.append(e)
+
+    th = [threading.Thread(target=tenant, args=(k,)) for k in range(4)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
+    assert tube.stats["migrated_bytes"] >= 4 * 40 * MB        # 320 MB stored against a 100 MB cap
+    assert tube._accounts_consistent()
+    for i, d in enumerate(ids):
+        got = tube.fetch(d, device=0, out=torch.empty_like(xs[i]))
+        torch.cuda.synchronize()
+        assert torch.equal(got, xs[i]), i
+    assert tube._accounts_consistent()
+    tube.close()
