@@ -431,6 +431,60 @@ def _single_gpu_topology(g):
     return build_preset("b200", n_gpus=g + 1)
 
 
+def _daemon_client(path, g, q):
+    """A function process: Listing 1 through the daemon (daemon.TubeClient)."""
+    sys.path.insert(0, ROOT)
+    try:
+        import torch
+        from paper_2411_01830_b200.daemon import TubeClient
+        c = TubeClient(path, g)
+        res = {}
+        for n in (4096, 1 << 20, 64 << 20):
+            x = torch.randint(0, 256, (n,), dtype=torch.uint8, device=f"cuda:{g}")
+            out = torch.empty_like(x)
+            st, ft = [], []
+            for i in range(30):
+                did = c.unique_id()
+                t0 = time.perf_counter()
+                c.store(did, x)
+                t1 = time.perf_counter()
+                c.fetch(did, out=out)
+                t2 = time.perf_counter()
+                if i >= 5:
+                    st.append(t1 - t0)
+                    ft.append(t2 - t1)
+            assert torch.equal(out, x)
+            res[str(n)] = {"store_us_p50": round(1e6 * statistics.median(st), 1),
+                           "fetch_us_p50": round(1e6 * statistics.median(ft), 1)}
+        c.close()
+        q.put(("ok", res))
+    except Exception as exc:  # noqa: BLE001
+        q.put(("err", repr(exc)))
+
+
+def run_daemon(tube, g):
+    """Function process -> per-box daemon (daemon.py): store + fetch latency of a
+    spawned client against a TubeDaemon on this tube (same GPU, bit-checked)."""
+    import multiprocessing as mp
+    import tempfile
+    from paper_2411_01830_b200.daemon import TubeDaemon
+    path = os.path.join(tempfile.mkdtemp(), "faastube.sock")
+    d = TubeDaemon(tube, path)
+    try:
+        ctx = mp.get_context("spawn")
+        q = ctx.Queue()
+        p = ctx.Process(target=_daemon_client, args=(path, g, q))
+        p.start()
+        status, res = q.get(timeout=180)
+        p.join(timeout=30)
+    finally:
+        d.close()
+    if status != "ok":
+        return {"error": res}
+    return {"workload": "spawned function process: TubeClient.store then fetch(out=) through the daemon, "
+                        "GPU payloads as exported VMM pool blocks (same GPU)", "sizes": res}
+
+
 def run_extras(tube, g, dev, torch, max_throughput=False):
     out = {}
     # config 2 at k = 1: 1 GiB pinned -> GPU through tube.fetch vs the live CE peak
@@ -608,6 +662,10 @@ def run_extras(tube, g, dev, torch, max_throughput=False):
     out["g2g_same_gpu_batched"] = batched
     out["g2g_same_gpu_sweep"] = sweep
     out["g2g_same_gpu_sweep_store_cap_bytes"] = 64e9
+    try:
+        out["daemon_put_get"] = run_daemon(tube, g)
+    except Exception as exc:  # noqa: BLE001 - extras never hide the headline line
+        out["daemon_put_get"] = {"error": repr(exc)}
     try:
         out.update(run_workflows(max_throughput=max_throughput))
     except Exception as exc:  # noqa: BLE001 - extras never hide the headline line
