@@ -92,3 +92,17 @@ def test_plan_stage_accessors_match_json():
                         slow._full()
                         dp.release_claim(slow)
                         assert fast.stages == slow.stages, (n, strat, a, b, size)
+
+
+def test_request_breakdown_accounts_every_millisecond():
+    """Runtime.breakdown: dispatch delay + the reference's phases + cFunc host
+    time + stores + the remainder add up to the request's latency."""
+    from paper_2411_01830_b200.runtime import Record, Runtime
+    r = Record(7, "traffic", arrival_ms=100.0, slo_ms=90.0, start_ms=100.4, end_ms=180.0)
+    r.phases.update({"queuing": 10.0, "host_to_gfunc": 5.0, "gfunc_to_gfunc": 0.5, "compute": 40.0})
+    r.extra.update({"cfunc": 12.0, "store": 3.0})
+    b = Runtime.breakdown(r)
+    assert b["latency_ms"] == 80.0 and b["dispatch_ms"] == 0.4
+    total = b["dispatch_ms"] + sum(b["phases"].values()) + b["cfunc_ms"] + b["store_ms"] + b["unaccounted_ms"]
+    assert abs(total - b["latency_ms"]) < 0.02, b
+    assert b["unaccounted_ms"] == 9.1
