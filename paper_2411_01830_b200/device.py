@@ -89,8 +89,20 @@ class Ev:
     (CUDA defers the destruction of an event still pending)."""
 
     __slots__ = ("h", "device", "__weakref__")
+    # handles of dropped events, per device, reused by new ones: a request makes
+    # several (ready, fences) and create + destroy cost ~2 us of driver time each.
+    # Reuse is safe: a wait already enqueued on a stream captured the old record.
+    _free: dict = {}
+    _FREE_MAX = 1024
 
     def __init__(self, device: int):
+        free = Ev._free.get(device)
+        if free:
+            try:
+                self.h, self.device = free.pop(), device
+                return
+            except IndexError:               # another thread took the last one
+                pass
         h = C.c_void_p()
         LIB.ft_event_create(int(device), C.byref(h))
         self.h, self.device = h.value, device
@@ -116,6 +128,10 @@ class Ev:
         if h:
             self.h = None
             try:
+                free = Ev._free.setdefault(self.device, [])
+                if len(free) < Ev._FREE_MAX:
+                    free.append(h)
+                    return
                 LIB.raw("ft_event_destroy")(C.c_void_p(h))
             except Exception:  # noqa: BLE001 - interpreter teardown
                 pass
