@@ -234,3 +234,28 @@ def test_d2h_stage_bit_exact(dev, managed, n, kinds):
     assert (calls.count("d2h:start"), calls.count("d2h:finish")) == ((1, 1) if managed else (0, 0)), calls
     assert "start" not in calls
     p.close()
+
+
+def test_startup_calibration_matches_the_link(dev):
+    """measure_pcie_gbps (the pacer's start-up link rate) reads a buffer the CPU
+    never wrote: within 10 % of a 1 GiB copy from a cold pinned buffer, run
+    after a host write that would have dragged a dirty-buffer calibration to
+    ~21 GB/s on these hosts (profiles/r01/diag_calib.txt)."""
+    from paper_2411_01830_b200.tube import measure_pcie_gbps
+    scratch = torch.empty(64 << 20, dtype=torch.uint8, pin_memory=True)
+    scratch.fill_(3)                                   # the CPU just wrote pinned memory
+    got = measure_pcie_gbps([0])
+    n = 1 << 30
+    host = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    dst = torch.empty(n, dtype=torch.uint8, device="cuda:0")
+    s = torch.cuda.Stream(0)
+    best = 1e9
+    for _ in range(3):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(s)
+        dev.pcie_copy(dst.data_ptr(), host.data_ptr(), n, True, 0, s)
+        b.record(s)
+        b.synchronize()
+        best = min(best, a.elapsed_time(b))
+    link = n / (best * 1e-3) / 1e9
+    assert got > 0.9 * link, (got, link)
