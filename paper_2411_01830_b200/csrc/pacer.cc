@@ -84,7 +84,8 @@ static void stream_copy(uint8_t* dst, const uint8_t* src, uint64_t n) {
 
 constexpr int kInflightBatches = 4;  // issued-but-not-landed batches per stage
 constexpr double kLookahead = 2.0;   // batches issued ahead of the rate schedule (host jitter)
-constexpr int kOwnerCoalesce = 2;     // batches per DMA op for a stage that holds the whole link
+constexpr int kOwnerCoalesce = 2;
+constexpr uint64_t kMinSampleBytes = 4ull << 20;  // smallest DMA the link estimator samples     // batches per DMA op for a stage that holds the whole link
 constexpr int kMaxDev = 64;
 constexpr int kWorkers = 8;  // pageable staging threads (1 GiB pageable -> GPU with a 40 MB ring: 4 workers
                              // 28-37 GB/s, 8: 44-47, 12: 41-45, 16: 37-42; profiles/r01/sweep_pageable.txt)
@@ -388,10 +389,13 @@ struct ft_pacer {
     Route& r = st.routes[i];
     uint64_t o = r.off + rel;
     if (st.pinned) {
-      if (track && !r.staged() && n && (samples[st.dir][r.dev].size() < 6 || ++timed_skip % 8 == 0)) {
+      if (track && !r.staged() && n >= kMinSampleBytes &&
+          (samples[st.dir][r.dev].size() < 6 || ++timed_skip % 8 == 0)) {
         // direct route: bracket the DMA with timing events (service-rate sample) —
         // every batch until the estimator has its window, then every 8th (a timed
-        // event between two DMAs costs copy-engine time)
+        // event between two DMAs costs copy-engine time). Small DMAs are not
+        // sampled: their fixed cost says nothing about the link (a 4 KiB copy
+        // "runs" at ~1 GB/s) and a window of them would drag the estimate down
         DevGuard g(r.dev);
         Timing tm{get_tevent(r.dev), nullptr, st.dir, r.dev, n, now(), link_busy(st.dir, r.dev, st.ticket)};
         ck(cudaEventRecord(tm.t0, r.ce), "record t0");
