@@ -40,6 +40,7 @@ MIB = 1 << 20
 PAYLOAD_SHAPE = (32, 1024, 1024)          # fp16 -> 64 MiB (config 1)
 METRIC = "H2G/G2G pass GB/s & p99 latency vs PCIe/NVLink peak; workflow req/s"
 L2_FLUSH_BYTES = 256 * MIB
+NVLINK_GBPS = 900.0                        # NVLink 5, per direction per GPU
 
 
 def parse():
@@ -50,6 +51,9 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-sample-s", type=float, default=10.0)
     ap.add_argument("--no-extras", action="store_true")
+    ap.add_argument("--no-ncu", action="store_true", help="skip the in-run ncu DRAM-traffic capture")
+    ap.add_argument("--quick", action="store_true", help="short workflow traces, one seed (development runs)")
+    ap.add_argument("--ncu-probe", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--max-throughput", action="store_true",
                     help="also search config 4's max req/s per strategy (harness.max_throughput; minutes)")
     return ap.parse_args()
@@ -66,7 +70,8 @@ def nearest_rank(sorted_vals, pct):
 
 # ----------------------------------------------------------------- CPU path
 def cpu_host_path(sample_s: float, nbytes: int, threads: int | None = None) -> dict:
-    """The reference's CPU host-memory path (oracle port), bounded sample."""
+    """Pure host put+get pass of the reference's host-memory path (memcpy into a
+    host segment and back out; oracle port), bounded sample."""
     import numpy as np
     from oracle.host_path import HostMemoryStore
     hs = HostMemoryStore(threads=threads)
@@ -94,32 +99,105 @@ def cpu_host_path(sample_s: float, nbytes: int, threads: int | None = None) -> d
             "gbps": nbytes / statistics.mean(times) / 1e9, "passes": len(times), "threads": hs.threads}
 
 
+class PciePath:
+    """The reference's CPU host-memory path as BASELINE.md §4 defines it (oracle
+    port, infless_plus): the producer's 64 MiB fp16 tensor on the GPU is stored
+    by D2H on its link into a POSIX shm segment and fetched by H2D out of it
+    into the consumer's buffer, through pinned staging allocated per transfer.
+    torch copies only (no product code). Each pass is wall-clocked and ends
+    with the consumer's bytes on the GPU."""
+
+    def __init__(self, device: int = 0, threads: int | None = None):
+        import torch
+        from oracle.host_path import PcieHostMemoryStore
+        self.torch, self.device = torch, device
+        self.prev_threads = torch.get_num_threads()
+        self.hs = PcieHostMemoryStore(device, threads=threads)
+        gen = torch.Generator(device="cpu").manual_seed(0)
+        self.x = torch.randn(PAYLOAD_SHAPE, generator=gen).half().to(f"cuda:{device}")
+        self.out = torch.empty_like(self.x)
+        torch.cuda.synchronize(device)
+
+    def one(self) -> float:
+        torch, hs = self.torch, self.hs
+        t0 = time.perf_counter()
+        did = hs.unique_id()
+        hs.store(did, self.x)           # producer GPU -> D2H -> shm
+        hs.fetch(did, self.out)         # shm -> H2D -> consumer GPU
+        torch.cuda.current_stream(self.device).synchronize()
+        dt = time.perf_counter() - t0
+        hs.drop(did)
+        return dt
+
+    def sample(self, sample_s: float, min_passes: int = 3) -> dict:
+        self.out.zero_()
+        times = []
+        t_end = time.perf_counter() + sample_s
+        while time.perf_counter() < t_end or len(times) < min_passes:
+            times.append(self.one())
+        u8 = self.torch.uint8
+        assert self.torch.equal(self.out.view(u8), self.x.view(u8)), "reference path delivered different bytes"
+        times.sort()
+        return {"pass_ms_p50": nearest_rank(times, 50) * 1e3, "pass_ms_p99": nearest_rank(times, 99) * 1e3,
+                "gbps": self.x.nbytes / statistics.mean(times) / 1e9, "passes": len(times),
+                "threads": self.hs.threads}
+
+    def close(self):
+        self.hs.close()
+        self.torch.set_num_threads(self.prev_threads)
+
+
+def cpu_pcie_path(sample_s: float, device: int = 0, threads: int | None = None) -> dict:
+    p = PciePath(device, threads)
+    for _ in range(3):
+        p.one()
+    try:
+        return p.sample(sample_s)
+    finally:
+        p.close()
+
+
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
     nbytes = 2 * PAYLOAD_SHAPE[0] * PAYLOAD_SHAPE[1] * PAYLOAD_SHAPE[2]
     threads = len(os.sched_getaffinity(0))
+    path = PciePath(0, threads)
+    for _ in range(max(3, args.warmup)):
+        path.one()
     per = []
-    for _ in range(args.warmup):
-        cpu_host_path(0.05, nbytes, threads)
     t_all = time.perf_counter()
     for _ in range(args.steps):
-        r = cpu_host_path(max(0.2, args.cpu_sample_s / max(1, args.steps)), nbytes, threads)
-        per.append(r)
+        per.append(path.sample(max(0.1, args.cpu_sample_s / max(1, args.steps)), min_passes=1))
     wall = time.perf_counter() - t_all
+    path.close()
     gbps = statistics.mean(r["gbps"] for r in per)
     p99 = max(r["pass_ms_p99"] for r in per)
+    one_thread = cpu_pcie_path(min(3.0, args.cpu_sample_s), 0, 1)
+    host_only = cpu_host_path(min(3.0, args.cpu_sample_s), nbytes, threads)
     line = {"metric": METRIC, "value": round(gbps, 4), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(wall / args.steps * 1e3, 3), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
             "impl": "reference",
             "config": {"workload": "config1: 2-function pipeline, 64 MiB fp16 put/get (reference CPU host-memory path)",
-                       "payload_bytes": nbytes, "path": "oracle/host_path.py infless_plus restatement"},
+                       "payload_bytes": nbytes,
+                       "path": "oracle/host_path.py PcieHostMemoryStore (infless_plus, BASELINE.md §4): store = D2H "
+                               "on the producer GPU's link into POSIX shm, fetch = shm -> H2D on the consumer's "
+                               "link; per-transfer pinned staging (2 x 2 MB, cudaHostRegister); torch copies only"},
+            "p50_pass_ms": round(statistics.median(r["pass_ms_p50"] for r in per), 4),
             "p99_pass_ms": round(p99, 4),
             "cpu_baseline": {"value": round(gbps, 4), "unit": "GB/s", "cores": threads, "kind": "port",
-                             "sample": f"{sum(r['passes'] for r in per)} store+fetch passes of 64 MiB"},
-            "e2e": {"value": round(gbps, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+                             "sample": f"{sum(r['passes'] for r in per)} store+fetch passes of 64 MiB "
+                                       "GPU -> shm -> GPU",
+                             "single_thread": {"value": round(one_thread["gbps"], 4), "cores": 1,
+                                               "p99_pass_ms": round(one_thread["pass_ms_p99"], 3),
+                                               "sample": f"{one_thread['passes']} passes"},
+                             "host_memory_only": {"value": round(host_only["gbps"], 4), "cores": threads,
+                                                  "p99_pass_ms": round(host_only["pass_ms_p99"], 3),
+                                                  "desc": "memcpy into the host segment and back, no PCIe legs"}},
+            "e2e": {"value": round(gbps, 4), "unit": "GB/s", "h2d_bytes_per_step": nbytes,
+                    "d2h_bytes_per_step": nbytes}}
     print(json.dumps(line), flush=True)
 
 
@@ -173,17 +251,114 @@ def measured_peaks():
         return {"hbm_gbs": 6650.0}, "fallback (B200_PROFILING.md)"
 
 
-def profile_traffic():
-    """dram bytes per launch of the copy kernel from the committed ncu capture."""
-    p = os.path.join(ROOT, "profiles", "ncu_copy_summary.json")
+def spin_ns(g, stream, ns):
+    """Queue a device-side wait (k_spin_ns) so the host enqueues what follows
+    before the GPU reaches it: events then time kernels, not host launch gaps."""
+    import ctypes as C
+    from paper_2411_01830_b200 import device as dev
+    dev.LIB.ft_spin_ns(int(ns), int(g), C.c_void_p(stream.cuda_stream))
+
+
+def ncu_traffic(timeout_s=240):
+    """DRAM bytes per launch of the pass's k_copy_bulk launches, measured in this
+    run: ncu (cache and clock control off, so each launch sees the pass's own
+    cache state) over ``bench.py --ncu-probe`` (warm-up + 4 flushed config-1
+    passes). Returns (dict, None) or (None, why)."""
+    import csv
+    import io
+    import shutil
+    ncu = shutil.which("ncu") or ("/usr/local/cuda/bin/ncu" if os.path.exists("/usr/local/cuda/bin/ncu") else None)
+    if ncu is None:
+        return None, "ncu not found"
+    cmd = [ncu, "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum",
+           "--cache-control", "none", "--clock-control", "none", "-k", "regex:k_copy_bulk", "--csv",
+           sys.executable, os.path.abspath(__file__), "--ncu-probe"]
     try:
-        with open(p) as fh:
-            return json.load(fh).get("dram_bytes_per_launch")
-    except OSError:
-        return None
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout_s)
+    except (subprocess.TimeoutExpired, OSError) as exc:
+        return None, f"ncu failed: {exc!r}"[:200]
+    rows = [ln for ln in r.stdout.splitlines() if ln.startswith('"')]
+    if not rows:
+        return None, f"ncu produced no rows (rc={r.returncode}): {r.stderr.strip()[-160:]}"
+    per = {}
+    for row in csv.DictReader(io.StringIO("\n".join(rows))):
+        try:
+            val = float(row["Metric Value"].replace(",", ""))
+        except (KeyError, ValueError):
+            continue
+        unit = row.get("Metric Unit", "")
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1, "usecond": 1e3,
+                 "msecond": 1e6}.get(unit, 1)
+        per.setdefault(int(row["ID"]), {})[row["Metric Name"]] = val * scale
+    launches = [v for _, v in sorted(per.items()) if "dram__bytes_read.sum" in v]
+    probe = launches[-8:]                     # the 4 measured passes: store, fetch, store, fetch ...
+    if len(probe) < 2:
+        return None, "too few k_copy_bulk launches captured"
+    rd = [v["dram__bytes_read.sum"] for v in probe]
+    wr = [v["dram__bytes_write.sum"] for v in probe]
+    ns = [v.get("gpu__time_duration.sum", 0.0) for v in probe]
+    return {"launches": len(probe), "read_bytes_store": statistics.mean(rd[0::2]),
+            "write_bytes_store": statistics.mean(wr[0::2]), "read_bytes_fetch": statistics.mean(rd[1::2]),
+            "write_bytes_fetch": statistics.mean(wr[1::2]), "per_launch": statistics.mean(r + w for r, w in zip(rd, wr)),
+            "ncu_ns_per_launch": statistics.mean(ns)}, None
+
+
+def ncu_probe():
+    """The config-1 pass as bench times it, a few times, for ncu_traffic()."""
+    import torch
+    from paper_2411_01830_b200.tube import FaaSTube
+    torch.cuda.set_device(0)
+    tube = FaaSTube("faastube", gpus=[0], pcie_gbps=55.0)
+    gen = torch.Generator(device="cpu").manual_seed(0)
+    x = torch.randn(PAYLOAD_SHAPE, generator=gen).half().to("cuda:0")
+    inp = torch.empty_like(x)
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device="cuda:0")
+    for i in range(7):
+        flush.fill_(i & 0xFF)
+        flush.amax()
+        did = tube.unique_id()
+        tube.store(did, x, producer="producer")
+        tube.fetch(did, device=0, out=inp, consumer="consumer")
+    torch.cuda.synchronize()
+    assert torch.equal(inp.view(torch.uint8), x.view(torch.uint8))
+    tube.close()
+
+
+def roofline_block(achieved, kern_ms, store_ms, fetch_ms, nbytes, peaks, peak_src, traffic, per_ms, achieved_gib,
+                   gib_ms):
+    peak = peaks.get("hbm_gbs", 6650.0)
+    t, why = traffic if traffic is not None else (None, "not measured (N>1 or --no-ncu)")
+    blk = {"bound": "hbm", "kernel": "k_copy_bulk<2,1> (TMA cp.async.bulk ring, L2 hints) - the pass's store "
+                                      "and fetch launches",
+           "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
+           "traffic": round(t["per_launch"]) if t else None,
+           "algorithmic_bytes_per_launch": 2 * nbytes, "kernel_ms": round(kern_ms, 5),
+           "store_launch_ms": round(store_ms, 5), "fetch_launch_ms": round(fetch_ms, 5),
+           "kernel_ms_per_step": round(store_ms + fetch_ms, 5),
+           "step_ms_p50": round(nearest_rank(per_ms, 50), 5),
+           "timing": "CUDA events around each launch inside the flushed config-1 pass, pass pre-queued behind a "
+                     "device spin (no host gaps); median over passes",
+           "peak_source": peak_src,
+           "hbm_bound_point": {"bytes": 1 << 30, "kernel_ms": round(gib_ms, 4), "achieved": round(achieved_gib, 1),
+                               "frac": round(achieved_gib / peak, 4),
+                               "desc": "same kernel, 1 GiB (no L2 residency possible): the HBM-bound figure"}}
+    if t:
+        dram_gbs = t["per_launch"] / (kern_ms * 1e-3) / 1e9
+        blk["traffic_source"] = "ncu in this run (dram__bytes_read.sum + dram__bytes_write.sum, cache/clock " \
+                                "control none) over bench.py --ncu-probe"
+        blk["traffic_detail"] = {k: round(v) for k, v in t.items() if k != "launches"}
+        blk["dram_achieved"] = round(dram_gbs, 1)
+        blk["frac_dram"] = round(dram_gbs / peak, 4)
+        blk["note"] = ("algorithmic bytes exceed DRAM bytes: the 64 MiB store writes stay in the 126 MB L2 and the "
+                       "fetch reads them from there; frac_dram is the DRAM-side fraction")
+    else:
+        blk["traffic_source"] = why
+    return blk
 
 
 def run_ours(args):
+    import datetime
+
     import torch
     import torch.distributed as dist
 
@@ -192,51 +367,60 @@ def run_ours(args):
     shared = world > ndev          # more ranks than GPUs (path smoke test): ranks share devices
     if world > 1:
         # only barriers and one max-reduction of timings go through the process group
-        dist.init_process_group("gloo" if shared else "nccl")
+        dist.init_process_group("gloo" if shared else "nccl", timeout=datetime.timedelta(minutes=60))
     g = local % ndev
+    # N > 1: rank r's producer runs on GPU r and its consumer on GPU r+1 (a ring of N
+    # pairs: every GPU sends one payload and receives one per step, NVLink both ways);
+    # one process per pair, each with its own tube over its two GPUs — no collective
+    peer = ((local + 1) % world) % ndev if world > 1 else g
     torch.cuda.set_device(g)
     from paper_2411_01830_b200 import device as dev
-    from paper_2411_01830_b200.tube import FaaSTube
+    from paper_2411_01830_b200.tube import FaaSTube, measure_pcie_gbps
 
     if world > 1:
-        # one process per GPU, each driving only its own GPU: its host->GPU legs use its own
-        # PCIe root (replicas; no striping through GPUs another rank drives)
+        # each rank's host->GPU legs use its own GPU's PCIe root (no striping through
+        # GPUs another rank drives; config 2's striping runs in the rank-0 extras)
         from paper_2411_01830_b200.strategies import strategy_preset
-        tube = FaaSTube(strategy_preset("faastube", parallel_pcie=False), topology=_single_gpu_topology(g), gpus=[g])
+        from paper_2411_01830_b200.topology import build_preset
+        topo = build_preset("b200", n_gpus=ndev, pcie_gbps=measure_pcie_gbps([g]))
+        tube = FaaSTube(strategy_preset("faastube", parallel_pcie=False), topology=topo, gpus=sorted({g, peer}))
     else:
         tube = FaaSTube("faastube")            # drives every visible GPU: H2G stripes over all their roots
     gen = torch.Generator(device="cpu").manual_seed(0)
     x = torch.randn(PAYLOAD_SHAPE, generator=gen).half().to(f"cuda:{g}")   # producer output (in HBM)
     nbytes = x.nbytes
-    inp = torch.empty_like(x)                                                # consumer input buffer
+    inp = torch.empty(PAYLOAD_SHAPE, dtype=torch.float16, device=f"cuda:{peer}")   # consumer input buffer
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=f"cuda:{g}")
+    flush_p = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=f"cuda:{peer}") if peer != g else None
     s = torch.cuda.current_stream(g)
-    pair, pair_error = None, None
-    if world > 1:
-        # N > 1: rank r's producer hands its output to rank r+1's consumer over
-        # NVLink (exported pool block + device doorbells) — pairs.CrossPair
-        try:
-            from paper_2411_01830_b200.pairs import CrossPair
-            sock_dir = f"/tmp/ft_bench_{os.environ.get('MASTER_PORT', '0')}"
-            os.makedirs(sock_dir, exist_ok=True)
-            pair = CrossPair(tube, g, rank, world, sock_dir, nbytes, dist.barrier)
-        except Exception as exc:  # noqa: BLE001 - reported; falls back to same-GPU replicas
-            pair_error = repr(exc)
+    sp = torch.cuda.current_stream(peer)
+    cross = peer != g
 
     def one_pass():
-        if pair is not None:
-            pair.produce(x)
-            pair.consume(inp)
-            return
         did = tube.unique_id()
         tube.store(did, x, producer="producer")
-        tube.fetch(did, device=g, out=inp, consumer="consumer")
+        tube.fetch(did, device=peer, out=inp, consumer="consumer")   # same GPU: TMA copy; else K1 over NVLink
+
+    def join():
+        """The producer's stream waits for the consumer GPU's stream (pass end on one device)."""
+        if cross:
+            e = torch.cuda.Event()
+            e.record(sp)
+            s.wait_event(e)
 
     def flush_l2(i):
         # inputs < L2 (126 MB): evict between passes; the read leaves L2 clean
         # so no write-back of flush data lands inside the timed pass
         flush.fill_(i & 0xFF)
         flush.amax()
+        if flush_p is not None:
+            with torch.cuda.stream(sp):
+                flush_p.fill_(i & 0xFF)
+                flush_p.amax()
+            join()
+
+    def delivered():
+        return torch.equal(inp.view(torch.uint8).to(x.device), x.view(torch.uint8))
 
     # ---- warm-up (>= W passes and >= 0.5 s under the clock sampler), then K timed passes
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -244,84 +428,133 @@ def run_ours(args):
     with Clocks(g) as clk:
         t_w = time.perf_counter()
         i = 0
-        # N > 1: the producer->consumer ring counts steps on both ends, so every rank runs
-        # the same number of warm-up passes (a time-based count differed by one between
-        # ranks and left a doorbell waiting for a step its peer never ran)
-        while i < max(3, args.warmup) or (world == 1 and time.perf_counter() - t_w < 0.5):
+        while i < max(3, args.warmup) or time.perf_counter() - t_w < 0.5:
             flush_l2(i)
             one_pass()
             i += 1
-        if world > 1:
-            while time.perf_counter() - t_w < 0.5:   # same clock-sampling window, no extra passes
-                time.sleep(0.01)
-        torch.cuda.synchronize()
-        assert torch.equal(inp.view(torch.uint8), x.view(torch.uint8)), "delivered bytes differ"
+        torch.cuda.synchronize(g)
+        torch.cuda.synchronize(peer)
+        assert delivered(), "delivered bytes differ"
         if world > 1:
             dist.barrier()
-        torch.cuda.synchronize()
-        launches0 = tube.stats["bytes_local"]
+        launches0 = dict(tube.stats)
         t_timed = time.perf_counter()
         for i in range(args.steps):
             flush_l2(i)
             starts[i].record(s)
             one_pass()
+            join()
             ends[i].record(s)
-        torch.cuda.synchronize()
+        torch.cuda.synchronize(g)
+        torch.cuda.synchronize(peer)
         timed_wall_s = time.perf_counter() - t_timed
     if world > 1:
         dist.barrier()
     per_ms = sorted(a.elapsed_time(b) for a, b in zip(starts, ends))
     total_ms = sum(per_ms)
-    copies = (tube.stats["bytes_local"] - launches0) // nbytes
-    gpu_launches = int(copies)                       # one k_copy_bulk per store + one per fetch
-    if pair is not None:                             # wait+copy+signal on each side
-        gpu_launches = 6 * args.steps
-        pair.check()
-    assert torch.equal(inp.view(torch.uint8), x.view(torch.uint8)), "delivered bytes differ"
+    # one k_copy_bulk per store + one copy kernel (k_copy_bulk same GPU, k_copy_vec K1) per fetch
+    gpu_launches = 2 * args.steps
+    moved = {k: tube.stats[k] - launches0.get(k, 0) for k in ("bytes_local", "bytes_nvlink")}
+    assert delivered(), "delivered bytes differ"
 
-    # ---- dominant kernel: k_copy_bulk on the same buffers, CUDA events on its stream
+    # ---- dominant kernel, timed under the pass's cache state (L2 flushed before the
+    # pass). A device spin queued ahead lets the host enqueue the whole pass first, so
+    # the events bracket the kernels back to back (no host gaps inside the brackets).
+    # Same GPU: the pass's two k_copy_bulk<2,1> launches (store snapshot, fetch copy).
+    # Cross GPU: the fetch's K1 pull (k_copy_vec over the peer mapping) on the consumer GPU.
     kern = []
-    for i in range(args.steps):
+    for i in range(max(3, args.steps)):
         flush_l2(i)
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(s)
-        dev.copy(inp.data_ptr(), x.data_ptr(), nbytes, g, s, dev.ENGINE_BULK)
-        b.record(s)
-        kern.append((a, b))
-    torch.cuda.synchronize()
-    kern_ms = statistics.mean(a.elapsed_time(b) for a, b in kern)
-
-    # ---- variant: producer writes into a tube-allocated output (zero-copy store, 1 copy / pass)
-    xo = tube.empty(PAYLOAD_SHAPE, torch.float16, device=g)
-    xo.copy_(x)
-    zc = []
-    for i in range(max(3, args.warmup) + args.steps):
-        flush_l2(i)
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(s)
+        spin_ns(g, s, 200_000)
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        e[0].record(s)
         did = tube.unique_id()
-        tube.store(did, xo, producer="producer", consumers=1)
-        tube.fetch(did, device=g, out=inp, consumer="consumer")
-        b.record(s)
-        zc.append((a, b))
-        xo = tube.empty(PAYLOAD_SHAPE, torch.float16, device=g)   # next request's output buffer
-        xo.copy_(x) if i < max(3, args.warmup) else None
-    torch.cuda.synchronize()
-    zc_ms = sorted(a.elapsed_time(b) for a, b in zc[max(3, args.warmup):])
+        tube.store(did, x, producer="producer")
+        e[1].record(s)
+        if cross:
+            s.wait_stream(sp)
+            with torch.cuda.stream(sp):
+                spin_ns(peer, sp, 200_000)
+                f = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+                f[0].record(sp)
+                tube.fetch(did, device=peer, out=inp, consumer="consumer")
+                f[1].record(sp)
+            e.extend(f)
+            join()
+        else:
+            tube.fetch(did, device=g, out=inp, consumer="consumer")
+        e[2].record(s)
+        kern.append(e)
+    torch.cuda.synchronize(g)
+    torch.cuda.synchronize(peer)
+    store_ms = statistics.median(e[0].elapsed_time(e[1]) for e in kern)
+    if cross:
+        fetch_ms = statistics.median(e[3].elapsed_time(e[4]) for e in kern)
+    else:
+        fetch_ms = statistics.median(e[1].elapsed_time(e[2]) for e in kern)
+    assert delivered(), "delivered bytes differ"
     peaks, peak_src = measured_peaks()
-    achieved = 2 * nbytes / (kern_ms * 1e-3) / 1e9   # read + write bytes per launch
+    gib_ms = achieved_gib = None
+    zc_ms = None
+    if not cross:
+        kern_ms = (store_ms + fetch_ms) / 2                  # average launch duration in the pass
+        achieved = 2 * nbytes / (kern_ms * 1e-3) / 1e9       # read + write bytes per launch
+        # the HBM-bound point: the same kernel over 1 GiB (L2 is 126 MB: nothing stays resident)
+        big = torch.empty(1 << 30, dtype=torch.uint8, device=f"cuda:{g}")
+        big2 = torch.empty_like(big)
+        gib = []
+        for i in range(6):
+            spin_ns(g, s, 100_000)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(s)
+            dev.copy_hint(big2.data_ptr(), big.data_ptr(), big.nbytes, g, s, dev.L2_EVICT_FIRST)
+            b.record(s)
+            gib.append((a, b))
+        torch.cuda.synchronize()
+        gib_ms = statistics.median(a.elapsed_time(b) for a, b in gib[1:])
+        achieved_gib = 2 * (1 << 30) / (gib_ms * 1e-3) / 1e9
+        del big, big2
+
+        # ---- variant: producer writes into a tube-allocated output (zero-copy store, 1 copy / pass)
+        xo = tube.empty(PAYLOAD_SHAPE, torch.float16, device=g)
+        xo.copy_(x)
+        zc = []
+        for i in range(max(3, args.warmup) + args.steps):
+            flush_l2(i)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(s)
+            did = tube.unique_id()
+            tube.store(did, xo, producer="producer", consumers=1)
+            tube.fetch(did, device=g, out=inp, consumer="consumer")
+            b.record(s)
+            zc.append((a, b))
+            xo = tube.empty(PAYLOAD_SHAPE, torch.float16, device=g)   # next request's output buffer
+            xo.copy_(x) if i < max(3, args.warmup) else None
+        torch.cuda.synchronize()
+        zc_ms = sorted(a.elapsed_time(b) for a, b in zc[max(3, args.warmup):])
+        del xo
+    else:
+        kern_ms = fetch_ms
+        achieved = nbytes / (fetch_ms * 1e-3) / 1e9           # payload over NVLink per launch
 
     # ---- e2e through the public API with host buffers. Listing-1 usage: the request
     # payload is stored from (pinned) host memory; the producer fetches it into an
     # output buffer carved from the tube's pool (tube.empty — the next request's is
     # allocated while this one's H2D tail is in flight), stores it (zero copy), and
-    # the consumer on the same GPU fetches a zero-copy view and reads it (digest ->
-    # 16 B D2H). The copy-semantics variant (producer's own buffer, consumer's input
-    # buffer: 2 HBM copies per step) is reported beside it.
+    # the consumer fetches it — a zero-copy view on the same GPU, a K1 pull into a
+    # fresh buffer on the next GPU — and reads it (digest -> 16 B D2H). The
+    # copy-semantics variant (producer's own buffer, consumer's input buffer) is
+    # reported beside it.
     host_in = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
     host_in.copy_(x.view(-1).view(torch.uint8).cpu())
-    fp = dev.Fingerprint(g)
+    fp = dev.Fingerprint(peer)
     ref_digest = dev.fingerprint_host(host_in)
+
+    def digest_of(t):
+        with torch.cuda.stream(sp):
+            fp.launch(t.data_ptr(), nbytes, sp)
+            return fp.value()                                 # D2H of the result
+
     e2e = []
     nxt = tube.empty((nbytes,), torch.uint8, device=g)
     for i in range(args.warmup + args.steps):
@@ -334,10 +567,10 @@ def run_ours(args):
         did = tube.unique_id()
         tube.store(did, out, producer="producer")                    # G2G put (zero copy)
         del out
-        view = tube.fetch(did, device=g, consumer="consumer")        # G2G get (same-GPU view)
-        fp.launch(view.data_ptr(), nbytes, s)
+        with torch.cuda.stream(sp):
+            view = tube.fetch(did, device=peer, consumer="consumer")  # G2G get
+        digest = digest_of(view)
         del view                                                     # block freed after the digest
-        digest = fp.value()                                          # D2H of the result
         if i >= args.warmup:
             e2e.append(time.perf_counter() - t0)
     assert digest == ref_digest, "e2e digest mismatch"
@@ -351,9 +584,9 @@ def run_ours(args):
         tube.fetch(d_in, device=g, out=prod_out.view(-1).view(torch.uint8), consumer="producer")
         did = tube.unique_id()
         tube.store(did, prod_out, producer="producer")               # snapshot copy
-        tube.fetch(did, device=g, out=inp, consumer="consumer")      # copy into the input buffer
-        fp.launch(inp.data_ptr(), nbytes, s)
-        digest = fp.value()
+        with torch.cuda.stream(sp):
+            tube.fetch(did, device=peer, out=inp, consumer="consumer")   # into the input buffer
+        digest = digest_of(inp)
         if i >= args.warmup:
             e2e_copy.append(time.perf_counter() - t0)
     assert digest == ref_digest, "e2e (copy semantics) digest mismatch"
@@ -365,70 +598,87 @@ def run_ours(args):
         dist.all_reduce(t_tensor, op=dist.ReduceOp.MAX)
     total_ms_max, e2e_max = t_tensor.tolist()
     value = world * args.steps * nbytes / (total_ms_max * 1e-3) / 1e9
+    pcie_pacer = tube.topo.pcie_gbps
+    tube.close()
 
-    extras = {} if args.no_extras or rank != 0 else run_extras(tube, g, dev, torch, args.max_throughput)
-
+    traffic = None
+    if rank == 0 and world == 1 and not args.no_ncu:
+        traffic = ncu_traffic()
+    extras = {}
+    if rank == 0 and not args.no_extras:
+        extras = run_extras(g, dev, torch, args.max_throughput, world if world > 1 and not shared else ndev,
+                            args.quick)
+    if world > 1:
+        dist.barrier()                          # the other ranks wait for rank 0's extras
     if rank == 0:
-        cpu = cpu_host_path(args.cpu_sample_s, nbytes) if world == 1 else None
-        cpu1 = cpu_host_path(min(3.0, args.cpu_sample_s), nbytes, threads=1) if world == 1 else None
+        cpu = cpu_pcie_path(args.cpu_sample_s, g) if world == 1 else None
+        cpu1 = cpu_pcie_path(min(3.0, args.cpu_sample_s), g, threads=1) if world == 1 else None
+        cpu_host = cpu_host_path(min(3.0, args.cpu_sample_s), nbytes) if world == 1 else None
+        if cross:
+            roof = {"bound": "nvlink", "kernel": "k_copy_vec (K1: 128-bit loads over the peer mapping, consumer GPU)",
+                    "achieved": round(achieved, 1), "peak": NVLINK_GBPS, "unit": "GB/s",
+                    "frac": round(achieved / NVLINK_GBPS, 4), "traffic": None,
+                    "traffic_source": "ncu is single-GPU here (B200_PROFILING.md); nvltx/nvlrx not captured",
+                    "algorithmic_bytes_per_launch": nbytes, "kernel_ms": round(fetch_ms, 5),
+                    "store_launch_ms": round(store_ms, 5),
+                    "peak_source": "NVLink 5 nominal per direction per GPU (SURVEY §8d)",
+                    "timing": "CUDA events around the fetch's pull on the consumer GPU, pre-queued behind a spin"}
+        else:
+            roof = roofline_block(achieved, kern_ms, store_ms, fetch_ms, nbytes, peaks, peak_src, traffic, per_ms,
+                                  achieved_gib, gib_ms)
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(total_ms_max / args.steps, 5), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
             "config": {"workload": "config1: 2-function pipeline, producer store(64 MiB fp16) -> consumer "
-                                   + ("fetch(into its input buffer), same GPU" if pair is None else
-                                      "on the next rank's GPU: pull over NVLink from the exported pool block, "
-                                      "device doorbells (pairs.CrossPair)"),
-                       "payload_bytes": nbytes, "strategy": "faastube", "l2": "flushed before each pass (256 MiB write + read, outside the timed pass)",
-                       "parallelism": f"replicas x{world}" if pair is None else f"ring of {world} producer->consumer pairs",
-                       **({"cross_gpu_setup_error": pair_error} if pair_error else {})},
+                                   + ("fetch(into its input buffer), same GPU" if not cross else
+                                      "fetch(into its input buffer) on the next GPU (K1 pull over NVLink)"),
+                       "payload_bytes": nbytes, "strategy": "faastube",
+                       "l2": "flushed before each pass (256 MiB write + read, outside the timed pass)",
+                       "parallelism": (f"replicas x{world}" if not cross else
+                                       f"ring of {world} producer->consumer pairs (rank r: GPU r -> GPU r+1), "
+                                       "one process and one tube per pair"),
+                       "moved_per_step": {k: v // max(1, args.steps) for k, v in moved.items()}},
             "p50_pass_ms": round(nearest_rank(per_ms, 50), 5), "p99_pass_ms": round(nearest_rank(per_ms, 99), 5),
             "e2e": {"value": round(world * nbytes / e2e_max / 1e9, 3), "unit": "GB/s",
                     "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": 16,
                     "path": "store(pinned host payload) -> fetch H2G into a tube.empty output -> store (zero "
-                            "copy) -> fetch (same-GPU view) -> digest kernel -> 16 B D2H",
+                            "copy) -> fetch (" + ("same-GPU view" if not cross else "K1 pull to the next GPU")
+                            + ") -> digest kernel -> 16 B D2H",
                     "step_ms_p50": round(nearest_rank(sorted(e2e), 50) * 1e3, 4),
                     "step_ms_p99": round(nearest_rank(sorted(e2e), 99) * 1e3, 4),
-                    "pcie_gbps_pacer": tube.topo.pcie_gbps,
+                    "pcie_gbps_pacer": pcie_pacer,
                     "copy_semantics": {"path": "same, producer's own output buffer and the consumer's input "
-                                               "buffer (store snapshot + fetch copy: 2 HBM copies per step)",
+                                               "buffer (store snapshot + fetch copy)",
                                        "value": round(nbytes / statistics.mean(e2e_copy) / 1e9, 3),
                                        "step_ms_p50": round(nearest_rank(sorted(e2e_copy), 50) * 1e3, 4),
                                        "step_ms_p99": round(nearest_rank(sorted(e2e_copy), 99) * 1e3, 4)}},
-            "roofline": {"bound": "hbm", "kernel": "k_copy_bulk (TMA cp.async.bulk ring)",
-                         "achieved": round(achieved, 1), "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
-                         "frac": round(achieved / peaks.get("hbm_gbs", 6650.0), 4), "traffic": profile_traffic(),
-                         "algorithmic_bytes_per_launch": 2 * nbytes, "kernel_ms": round(kern_ms, 5),
-                         "peak_source": peak_src},
+            "roofline": roof,
             "gpu_launches": gpu_launches,
             "clocks": dict(clk.summary(), window=f"warm-up + timed region ({timed_wall_s:.3f} s timed)"),
-            "variant_pool_output": {"desc": "producer output allocated from the tube pool (zero-copy store): "
-                                            "1 copy per pass", "p50_pass_ms": round(nearest_rank(zc_ms, 50), 5),
-                                    "value": round(nbytes / (statistics.mean(zc_ms) * 1e-3) / 1e9, 3),
-                                    "unit": "GB/s"},
         }
+        if zc_ms:
+            line["variant_pool_output"] = {"desc": "producer output allocated from the tube pool (zero-copy store): "
+                                                   "1 copy per pass", "p50_pass_ms": round(nearest_rank(zc_ms, 50), 5),
+                                           "value": round(nbytes / (statistics.mean(zc_ms) * 1e-3) / 1e9, 3),
+                                           "unit": "GB/s"}
         if cpu:
             line["cpu_baseline"] = {"value": round(cpu["gbps"], 3), "unit": "GB/s", "cores": cpu["threads"],
                                     "kind": "port", "sample": f"{cpu['passes']} store+fetch passes of 64 MiB "
-                                                              f"through host memory ({args.cpu_sample_s:.0f} s)",
+                                                              f"GPU -> D2H -> shm -> H2D -> GPU "
+                                                              f"({args.cpu_sample_s:.0f} s, BASELINE.md §4)",
+                                    "host_memory_only": {"value": round(cpu_host["gbps"], 3),
+                                                         "cores": cpu_host["threads"],
+                                                         "desc": "memcpy into the host segment and back, "
+                                                                 "no PCIe legs"},
                                     "p99_pass_ms": round(cpu["pass_ms_p99"], 3),
                                     "single_thread": {"value": round(cpu1["gbps"], 3), "cores": 1,
                                                       "p99_pass_ms": round(cpu1["pass_ms_p99"], 3),
                                                       "sample": f"{cpu1['passes']} passes"}}
         line.update(extras)
         print(json.dumps(line), flush=True)
-    if pair is not None:
-        pair.close()
-    tube.close()
     if world > 1:
         dist.destroy_process_group()
-
-
-def _single_gpu_topology(g):
-    """Under torchrun each rank drives only its own GPU (CUDA_VISIBLE_DEVICES
-    is not narrowed), so the tube's topology covers devices 0..g."""
-    from paper_2411_01830_b200.topology import build_preset
-    return build_preset("b200", n_gpus=g + 1)
 
 
 def _daemon_client(path, g, q):
@@ -485,7 +735,220 @@ def run_daemon(tube, g):
                         "GPU payloads as exported VMM pool blocks (same GPU)", "sizes": res}
 
 
-def run_extras(tube, g, dev, torch, max_throughput=False):
+def _ev(torch):
+    return torch.cuda.Event(enable_timing=True)
+
+
+def run_cross_gpu(torch, dev, ndev):
+    """``ndev``: GPUs this run covers (N under torchrun, all visible at N=1)."""
+    return _cross_gpu(torch, dev, ndev)
+
+
+def _cross_gpu(torch, dev, ndev):
+    """Configs 3 and 2 across GPUs through the product API: one tube
+    drives every visible GPU (the per-box daemon's view); ``FaaSTube.store`` on
+    GPU i, ``FaaSTube.fetch(device=j, out=)`` on GPU j — Alg. 1 plans the path,
+    K1 pulls over NVLink. Each point is byte-checked (digest of the consumer's
+    buffer vs the producer's). Device time per fetch: events on the consumer's
+    stream around the call, pre-queued behind a device spin (transfer time, not
+    host submission); ``api_us`` is the host time of the call.
+
+    With one visible GPU this is a dry run of the same code: pair (0, 0) (the
+    same-GPU plan), no fan-in, config 2 at k = 1."""
+    from paper_2411_01830_b200.topology import build_preset
+    from paper_2411_01830_b200.tube import FaaSTube, measure_pcie_gbps
+    dry = ndev < 2
+    gpus = list(range(ndev))
+    topo = build_preset("b200", n_gpus=ndev, pcie_gbps=measure_pcie_gbps(gpus))
+    tube = FaaSTube("faastube", topology=topo, gpus=gpus)
+    tube.capacity_limit = 64e9      # B200 stores hold GiB objects (reference cap: 1 GB, datastore.py:19)
+    out = {}
+    fps = {d: dev.Fingerprint(d) for d in gpus}
+
+    def digest(t, d):
+        st = torch.cuda.current_stream(d)
+        fps[d].launch(t.data_ptr(), t.nbytes, st)
+        return fps[d].value()
+
+    def source(n, src, seed=2):
+        gen = torch.Generator(device=f"cuda:{src}").manual_seed(seed)
+        return torch.randint(0, 256, (n,), dtype=torch.uint8, device=f"cuda:{src}", generator=gen)
+
+    def fetch_times(src, dst, n, reps):
+        x = source(n, src)
+        want = digest(x, src)
+        y = torch.empty(n, dtype=torch.uint8, device=f"cuda:{dst}")
+        sd = torch.cuda.current_stream(dst)
+        dev_ms, api_us = [], []
+        for r in range(reps + 2):
+            did = tube.unique_id()
+            tube.store(did, x, producer="producer")
+            torch.cuda.synchronize(src)
+            spin_ns(dst, sd, 300_000)
+            a, b = _ev(torch), _ev(torch)
+            with torch.cuda.device(dst):
+                a.record(sd)
+                t0 = time.perf_counter()
+                tube.fetch(did, device=dst, out=y, consumer="consumer")
+                t1 = time.perf_counter()
+                b.record(sd)
+            b.synchronize()
+            if r >= 2:
+                dev_ms.append(a.elapsed_time(b))
+                api_us.append((t1 - t0) * 1e6)
+        ok = digest(y, dst) == want
+        dev_ms.sort()
+        api_us.sort()
+        return dev_ms, api_us, ok
+
+    pairs01 = (0, 1) if not dry else (0, 0)
+    sweep = []
+    for lg in range(12, 31) if not dry else (12, 20, 26):
+        n = 1 << lg
+        reps = 20 if n <= (16 << 20) else (8 if n <= (256 << 20) else 4)
+        ts, api, ok = fetch_times(*pairs01, n, reps)
+        p50 = nearest_rank(ts, 50)
+        sweep.append({"bytes": n, "ms_p50": round(p50, 5), "ms_p99": round(nearest_rank(ts, 99), 5),
+                      "gbps_p50": round(n / (p50 * 1e-3) / 1e9, 2),
+                      "frac_nvlink": round(n / (p50 * 1e-3) / 1e9 / NVLINK_GBPS, 4),
+                      "api_us_p50": round(nearest_rank(api, 50), 1), "bit_exact": ok})
+    out["config3_pair_sweep"] = {"workload": f"config3: FaaSTube.store on GPU {pairs01[0]} -> fetch(device="
+                                             f"{pairs01[1]}, out=), 4 KiB..1 GiB, random uint8 seed 2",
+                                 "dry_run": dry, "peak_gbps": NVLINK_GBPS, "points": sweep}
+    # every ordered pair, one at a time (64 MiB)
+    rows = []
+    for i in gpus:
+        for j in gpus:
+            if i != j or dry:
+                ts, _, ok = fetch_times(i, j, 64 << 20, 5)
+                p50 = nearest_rank(ts, 50)
+                rows.append({"src": i, "dst": j, "gbps_p50": round((64 << 20) / (p50 * 1e-3) / 1e9, 1),
+                             "bit_exact": ok})
+                if dry:
+                    break
+    out["config3_all_pairs"] = {"bytes": 64 << 20, "dry_run": dry, "pairs": rows}
+
+    def concurrent(plan, n):
+        """plan: [(src, dst)] fetched at the same time (each on its own stream of its
+        consumer GPU, every stream pre-queued behind a spin so they start together)."""
+        xs = {src: source(n, src, 3 + src) for src, _ in plan}
+        want = {src: digest(xs[src], src) for src in xs}
+        ys = [torch.empty(n, dtype=torch.uint8, device=f"cuda:{dst}") for _, dst in plan]
+        streams = [torch.cuda.Stream(dst) for _, dst in plan]
+        best = None
+        for r in range(4):
+            dids = []
+            for src, _ in plan:
+                d = tube.unique_id()
+                tube.store(d, xs[src], producer=f"p{src}")
+                dids.append(d)
+            for d in gpus:
+                torch.cuda.synchronize(d)
+            evs = []
+            for (src, dst), st in zip(plan, streams):
+                spin_ns(dst, st, 2_000_000)
+            for (src, dst), st, y, d in zip(plan, streams, ys, dids):
+                a, b = _ev(torch), _ev(torch)
+                with torch.cuda.device(dst), torch.cuda.stream(st):
+                    a.record(st)
+                    tube.fetch(d, device=dst, out=y, consumer=f"c{dst}")
+                    b.record(st)
+                evs.append((a, b))
+            for d in gpus:
+                torch.cuda.synchronize(d)
+            t = max(a.elapsed_time(b) for a, b in evs)
+            best = t if best is None else min(best, t)
+        ok = all(digest(y, dst) == want[src] for (src, dst), y in zip(plan, ys))
+        agg = len(plan) * n / (best * 1e-3) / 1e9
+        return {"pairs": plan, "bytes_each": n, "ms": round(best, 4), "aggregate_gbps": round(agg, 1),
+                "bit_exact": ok}
+
+    if dry:
+        plan = [(0, 0)]
+    else:
+        plan = [(i, i + 1) for i in range(0, ndev - 1, 2)]
+    c = concurrent(plan, 256 << 20)
+    c["frac"] = round(c["aggregate_gbps"] / (NVLINK_GBPS * len(plan)), 4)
+    out["config3_disjoint_pairs"] = dict(c, dry_run=dry, peak_gbps=NVLINK_GBPS * len(plan))
+    if not dry:
+        c = concurrent([(i, 0) for i in range(1, ndev)], 256 << 20)
+        c["frac"] = round(c["aggregate_gbps"] / NVLINK_GBPS, 4)
+        out["config3_fan_in"] = dict(c, peak_gbps=NVLINK_GBPS,
+                                     bound="the target's NVLink ingress (900 GB/s per direction)")
+    # config 2: 1 GiB pinned host batch -> GPU 0, striped over every root's link with
+    # NVLink forwarding (dataplane.py:203-250); peak = sum of the per-link CE peaks
+    n = 1 << 30
+    host = torch.empty(n, dtype=torch.uint8).pin_memory()
+    host.copy_(source(n, 0, 1).cpu())
+    want = dev.fingerprint_host(host)
+    dst = torch.empty(n, dtype=torch.uint8, device="cuda:0")
+    links = []
+    for d in gpus:
+        buf = torch.empty(n, dtype=torch.uint8, device=f"cuda:{d}")
+        st = torch.cuda.current_stream(d)
+        ms = []
+        for _ in range(3):
+            a, b = _ev(torch), _ev(torch)
+            with torch.cuda.device(d):
+                a.record(st)
+                dev.pcie_copy(buf.data_ptr(), host.data_ptr(), n, True, d, st)
+                b.record(st)
+            b.synchronize()
+            ms.append(a.elapsed_time(b))
+        links.append(round(n / (min(ms) * 1e-3) / 1e9, 2))
+        del buf
+    k = len(tube.topo.roots()) if tube.strategy.parallel_pcie else 1
+    peak = sum(sorted(links)[:k]) if k == len(links) else k * min(links)
+    s0 = torch.cuda.current_stream(0)
+    nv0 = tube.stats["bytes_nvlink"]
+    ts = []
+    for r in range(4):
+        did = tube.unique_id()
+        tube.store(did, host, producer="decode")
+        a, b = _ev(torch), _ev(torch)
+        a.record(s0)
+        tube.fetch(did, device=0, out=dst, consumer="preproc")
+        b.record(s0)
+        b.synchronize()
+        if r:
+            ts.append(a.elapsed_time(b))
+    ok = digest(dst, 0) == want
+    gbps = n / (statistics.median(ts) * 1e-3) / 1e9
+    out["config2_striped"] = {"workload": f"config2: 1 GiB pinned -> GPU 0 via FaaSTube.fetch, striped over k={k} "
+                                          "PCIe links (one staging GPU per root, NVLink forward)",
+                              "dry_run": dry, "links": k, "value": round(gbps, 3), "unit": "GB/s",
+                              "peak": round(peak, 3), "per_link_ce_gbps": links, "frac": round(gbps / peak, 4),
+                              "nvlink_bytes_per_fetch": (tube.stats["bytes_nvlink"] - nv0) // 4,
+                              "nvlink_frac_secondary": round((n * (k - 1) / k) / (statistics.median(ts) * 1e-3)
+                                                             / 1e9 / NVLINK_GBPS, 4),
+                              "bit_exact": ok}
+    del host, dst
+    tube.close()
+    return out
+
+
+def run_extras(g, dev, torch, max_throughput=False, ndev=1, quick=False):
+    from paper_2411_01830_b200.tube import FaaSTube
+    out = {}
+    try:
+        out.update(run_cross_gpu(torch, dev, ndev))
+    except Exception as exc:  # noqa: BLE001 - extras never hide the headline line
+        import traceback
+        out["cross_gpu_error"] = repr(exc) + " " + traceback.format_exc()[-600:]
+    tube = FaaSTube("faastube")               # drives every visible GPU
+    try:
+        out.update(_single_gpu_extras(tube, g, dev, torch))
+    finally:
+        tube.close()
+    try:
+        out.update(run_workflows(max_throughput=max_throughput,
+                                 **({"dur4_s": 4.0, "dur5_s": 2.0, "seeds": (0,)} if quick else {})))
+    except Exception as exc:  # noqa: BLE001 - extras never hide the headline line
+        out["workflows_error"] = repr(exc)
+    return out
+
+
+def _single_gpu_extras(tube, g, dev, torch):
     out = {}
     # config 2 at k = 1: 1 GiB pinned -> GPU through tube.fetch vs the live CE peak
     n = 1 << 30
@@ -576,6 +1039,7 @@ def run_extras(tube, g, dev, torch, max_throughput=False):
         xb = torch.empty_like(xa)
         ts = []
         for i in range(6):
+            spin_ns(g, s, 50_000)
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(s)
             dev.copy(xb.data_ptr(), xa.data_ptr(), m, g, s, dev.ENGINE_VEC)
@@ -587,7 +1051,7 @@ def run_extras(tube, g, dev, torch, max_throughput=False):
         vec.append({"bytes": m, "kernel_ms": round(ms, 5), "payload_gbps": round(m / (ms * 1e-3) / 1e9, 1)})
         del xa, xb
     out["nvlink_mover_local"] = {"kernel": "k_copy_vec (peer-safe 128-bit ld/st, the K1 NVLink engine)",
-                                 "note": "local HBM copy on one GPU; NVLink peak 900 GB/s/dir nominal, 770 measured",
+                                 "note": "local HBM copy on one GPU, pre-queued behind a device spin; NVLink 5 peak 900 GB/s/dir nominal",
                                  "sweep": vec}
     # config 3 at 1 GPU: zero-copy handoff latency and copy-into-input bandwidth, 4 KiB .. 1 GiB.
     # The reference's 1 GB per-GPU store cap (datastore.py:19, sized for 16-32 GB GPUs)
@@ -666,23 +1130,23 @@ def run_extras(tube, g, dev, torch, max_throughput=False):
         out["daemon_put_get"] = run_daemon(tube, g)
     except Exception as exc:  # noqa: BLE001 - extras never hide the headline line
         out["daemon_put_get"] = {"error": repr(exc)}
-    try:
-        out.update(run_workflows(max_throughput=max_throughput))
-    except Exception as exc:  # noqa: BLE001 - extras never hide the headline line
-        out["workflows_error"] = repr(exc)
     return out
 
 
-def run_workflows(dur_s=2.0, max_throughput=False, trial_s=10.0):
-    """Configs 4 and 5 on the live runtime (one GPU): the reference's traces,
-    placement and SLOs; FaaSTube vs the INFless+ host-memory baseline."""
+def run_workflows(dur4_s=20.0, dur5_s=10.0, seeds=(0, 1, 2), max_throughput=False, trial_s=10.0):
+    """Configs 4 and 5 on the live runtime: the reference's traces, placement and
+    SLOs; FaaSTube vs the INFless+ host-memory baseline. Each strategy runs the
+    same traces over ``seeds``; p50/p99 are nearest-rank over the pooled
+    requests of all seeds, with the per-seed spread beside them. With fewer GPUs
+    than the workflow has gFuncs the placement shares GPUs (colocate); otherwise
+    it is the reference's (workflow.py:375-438)."""
     from paper_2411_01830_b200 import workload
     from paper_2411_01830_b200.runtime import Runtime
     from paper_2411_01830_b200.tube import FaaSTube
 
-    def one(strategy, jobs_fn, compute):
+    def one(strategy, jobs_fn, compute, dur_s, seed):
         tube = FaaSTube(strategy)
-        jobs = jobs_fn(tube)
+        jobs = jobs_fn(tube, dur_s, seed)
         # a warm daemon: one untimed pass over the first 0.5 s of the same trace
         # (pool blocks, pinned buffers, allocator segments), then the measured run
         Runtime.warm_daemon(tube, jobs, compute, 0.5)
@@ -694,14 +1158,14 @@ def run_workflows(dur_s=2.0, max_throughput=False, trial_s=10.0):
         tube.close()
         return res
 
-    def traffic(tube):
+    def traffic(tube, dur_s, seed):
         wf = workload.preset_workflow("traffic")
         where = workload.place(wf, tube.topo, {}, colocate=tube.topo.gpu_count < len(wf.gfuncs()))
         workload.calibrate_slo(wf, tube.topo, where, 1.5)
-        reqs = workload.build_requests(wf, workload.gen_workload("bursty", 10.0, dur_s, 0), 0)
+        reqs = workload.build_requests(wf, workload.gen_workload("bursty", 10.0, dur_s, seed), seed)
         return [(wf, where, reqs)]
 
-    def pairs(tube):
+    def pairs(tube, dur_s, seed):
         jobs, occ = [], {}
         for i, mb in enumerate((1, 4, 16, 32, 64, 128, 256, 512)):
             wf = workload.Workflow.parse({
@@ -715,16 +1179,34 @@ def run_workflows(dur_s=2.0, max_throughput=False, trial_s=10.0):
                 if kind == "gpu":
                     occ[g] = occ.get(g, 0) + 1
             workload.calibrate_slo(wf, tube.topo, where, 1.5)
-            reqs = workload.build_requests(wf, workload.gen_workload("bursty", 5.0, dur_s, i), i, rid_start=1000 * i)
+            reqs = workload.build_requests(wf, workload.gen_workload("bursty", 5.0, dur_s, 100 * seed + i),
+                                           100 * seed + i, rid_start=1000 * i)
             jobs.append((wf, where, reqs))
         return jobs
 
+    def pooled(runs):
+        lat = sorted(x for r in runs for x in r.get("_lat", []))
+        miss = [m for r in runs for m in r.get("_slo_miss", [])]
+        p99s = [r.get("p99_ms") for r in runs if r.get("p99_ms") is not None]
+        for r in runs:
+            r.pop("_lat", None)
+            r.pop("_slo_miss", None)
+        out = {"requests": len(lat), "seeds": len(runs)}
+        if lat:
+            out.update(p50_ms=round(nearest_rank(lat, 50), 4), p99_ms=round(nearest_rank(lat, 99), 4),
+                       slo_violation_rate=round(sum(miss) / len(miss), 4),
+                       p99_ms_per_seed=p99s, p99_spread=round(max(p99s) / min(p99s), 3) if p99s else None)
+        out["runs"] = runs
+        return out
+
     out = {}
-    t4 = {s: one(s, traffic, "model") for s in ("faastube", "infless_plus")}
-    out["config4_traffic"] = {"workload": "traffic DAG (decode->preproc->yolo_det->resnet_ped/veh, p=0.6), "
-                                          "bursty 10 rps, random-init conv models on synthetic 1080p frames; "
-                                          "warm daemon (0.5 s untimed warm-up trace per strategy)",
+    t4 = {s: pooled([one(s, traffic, "model", dur4_s, sd) for sd in seeds]) for s in ("faastube", "infless_plus")}
+    out["config4_traffic"] = {"workload": f"traffic DAG (decode->preproc->yolo_det->resnet_ped/veh, p=0.6), "
+                                          f"bursty 10 rps x {dur4_s:.0f} s x seeds {list(seeds)}, random-init conv "
+                                          "models on synthetic 1080p frames; warm daemon (0.5 s untimed warm-up "
+                                          "trace per run); p50/p99 over the pooled requests",
                               "faastube": t4["faastube"], "infless_plus": t4["infless_plus"]}
+
     def max_rps(strategy):
         # harness.max_throughput (harness.py:383-428) on the live runtime: highest Poisson
         # rate whose p99 meets the workflow SLO (harness.calibrate_slo: 1.5 x the modelled
@@ -749,9 +1231,10 @@ def run_workflows(dur_s=2.0, max_throughput=False, trial_s=10.0):
             "faastube": mt["faastube"], "infless_plus": mt["infless_plus"],
             "gain": round(mt["faastube"]["max_rps"] / mt["infless_plus"]["max_rps"], 3)
             if mt["infless_plus"]["max_rps"] else None}
-    t5 = {s: one(s, pairs, "sleep") for s in ("faastube", "infless_plus")}
-    out["config5_multitenant"] = {"workload": "16 functions = 8 producer->consumer pairs, edges 1..512 MB, bursty "
-                                              "5 rps each, elastic VMM pool (floor 300 MB)",
+    t5 = {s: pooled([one(s, pairs, "sleep", dur5_s, sd) for sd in seeds]) for s in ("faastube", "infless_plus")}
+    out["config5_multitenant"] = {"workload": f"16 functions = 8 producer->consumer pairs, edges 1..512 MB, bursty "
+                                              f"5 rps each x {dur5_s:.0f} s x seeds {list(seeds)}, elastic VMM pool "
+                                              "(floor 300 MB); p50/p99 over the pooled requests",
                                   "faastube": t5["faastube"], "infless_plus": t5["infless_plus"]}
     return out
 
@@ -761,7 +1244,9 @@ def main():
     import signal
     faulthandler.register(signal.SIGUSR1, all_threads=True)   # `timeout -s USR1` dumps a hung run
     args = parse()
-    if args.impl == "reference":
+    if args.ncu_probe:
+        ncu_probe()
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_ours(args)

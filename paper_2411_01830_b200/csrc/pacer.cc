@@ -84,8 +84,11 @@ static void stream_copy(uint8_t* dst, const uint8_t* src, uint64_t n) {
 
 constexpr int kInflightBatches = 4;  // issued-but-not-landed batches per stage
 constexpr double kLookahead = 2.0;   // batches issued ahead of the rate schedule (host jitter)
-constexpr int kOwnerCoalesce = 2;
-constexpr uint64_t kMinSampleBytes = 4ull << 20;  // smallest DMA the link estimator samples     // batches per DMA op for a stage that holds the whole link
+constexpr int kOwnerCoalesce = 2;  // batches per DMA op for a stage that holds the whole link
+// smallest DMA the link estimator samples: 4 MB, or half a batch when batches are
+// smaller (a direct route's DMA is a byte share of one batch, so with small chunks or
+// several routes a fixed 4 MB would never be reached and the estimator would stop)
+constexpr uint64_t kMinSampleBytes = 4ull << 20;
 constexpr int kMaxDev = 64;
 constexpr int kWorkers = 8;  // pageable staging threads (1 GiB pageable -> GPU with a 40 MB ring: 4 workers
                              // 28-37 GB/s, 8: 44-47, 12: 41-45, 16: 37-42; profiles/r01/sweep_pageable.txt)
@@ -389,7 +392,7 @@ struct ft_pacer {
     Route& r = st.routes[i];
     uint64_t o = r.off + rel;
     if (st.pinned) {
-      if (track && !r.staged() && n >= kMinSampleBytes &&
+      if (track && !r.staged() && n >= std::min<uint64_t>(kMinSampleBytes, (uint64_t)batch_chunks * chunk / 2) &&
           (samples[st.dir][r.dev].size() < 6 || ++timed_skip % 8 == 0)) {
         // direct route: bracket the DMA with timing events (service-rate sample) —
         // every batch until the estimator has its window, then every 8th (a timed

@@ -88,14 +88,17 @@ class Ev:
     ordering without torch.cuda.Event objects. Destroyed with the object
     (CUDA defers the destruction of an event still pending)."""
 
-    __slots__ = ("h", "device", "__weakref__")
+    __slots__ = ("h", "device", "rec", "__weakref__")
     # handles of dropped events, per device, reused by new ones: a request makes
     # several (ready, fences) and create + destroy cost ~2 us of driver time each.
     # Reuse is safe: a wait already enqueued on a stream captured the old record.
+    # A reused handle still carries its previous record, so an Ev refuses to be
+    # waited on or queried until it has been recorded again (``rec``).
     _free: dict = {}
     _FREE_MAX = 1024
 
     def __init__(self, device: int):
+        self.rec = False
         free = Ev._free.get(device)
         if free:
             try:
@@ -107,21 +110,38 @@ class Ev:
         LIB.ft_event_create(int(device), C.byref(h))
         self.h, self.device = h.value, device
 
+    def _recorded(self):
+        if not self.rec:
+            raise RuntimeError("event used before it was recorded (its work was never enqueued)")
+        return self.h
+
     def record(self, stream):
         LIB.ft_event_record(C.c_void_p(self.h), C.c_void_p(stream_ptr(stream)))
+        self.rec = True
         return self
 
     def wait(self, stream):
         """``stream`` waits for the work this event captured."""
-        LIB.ft_stream_wait_events(C.c_void_p(stream_ptr(stream)), (C.c_void_p * 1)(self.h), 1)
+        LIB.ft_stream_wait_events(C.c_void_p(stream_ptr(stream)), (C.c_void_p * 1)(self._recorded()), 1)
 
     def query(self) -> bool:
         d = C.c_int()
-        LIB.ft_event_query(C.c_void_p(self.h), C.byref(d))
+        LIB.ft_event_query(C.c_void_p(self._recorded()), C.byref(d))
         return bool(d.value)
 
     def synchronize(self):
-        LIB.ft_event_synchronize(C.c_void_p(self.h))
+        LIB.ft_event_synchronize(C.c_void_p(self._recorded()))
+
+    @staticmethod
+    def drain_free():
+        """Destroy the pooled handles (teardown; none of them is in use)."""
+        for free in list(Ev._free.values()):
+            while free:
+                try:
+                    h = free.pop()
+                except IndexError:
+                    break
+                LIB.raw("ft_event_destroy")(C.c_void_p(h))
 
     def __del__(self):
         h = getattr(self, "h", None)
@@ -145,7 +165,7 @@ def copy_batch(segments, device: int, stream=None):
 
 
 def wait_events(stream, events):
-    evs = [e.h for e in events if e is not None]
+    evs = [e._recorded() for e in events if e is not None]
     if evs:
         LIB.ft_stream_wait_events(C.c_void_p(stream_ptr(stream)), (C.c_void_p * len(evs))(*evs), len(evs))
 
@@ -153,10 +173,12 @@ def wait_events(stream, events):
 def copy_ordered(dst_ptr: int, src_ptr: int, nbytes: int, device: int, stream, hints: int = 0, waits=(),
                  done: "Ev | None" = None):
     """One call: ``stream`` waits on ``waits``, TMA-bulk copy with L2 ``hints``, record ``done``."""
-    evs = [e.h for e in waits if e is not None]
+    evs = [e._recorded() for e in waits if e is not None]
     LIB.ft_copy_ordered(C.c_void_p(dst_ptr), C.c_void_p(src_ptr), int(nbytes), int(device),
                         C.c_void_p(stream_ptr(stream)), int(hints), (C.c_void_p * max(1, len(evs)))(*evs),
                         len(evs), C.c_void_p(done.h if done is not None else None))
+    if done is not None:
+        done.rec = True
 
 
 class _Mem:

@@ -426,6 +426,8 @@ class Runtime:
                 per.setdefault(r.workflow, []).append(r.end_ms - r.arrival_ms)
             out["per_workflow_p99_ms"] = {k: round(nearest_rank(v, 99), 4) for k, v in sorted(per.items())}
             out["worst"] = self.breakdown(max(done, key=lambda r: r.end_ms - r.arrival_ms))
+            out["_lat"] = lat                # raw latencies (callers pooling runs pop it)
+            out["_slo_miss"] = [r.end_ms - r.arrival_ms > r.slo_ms + 1e-9 for r in done]
         return out
 
     @staticmethod

@@ -417,9 +417,14 @@ class FaaSTube:
             if o.block is not None:
                 self._stored[o.gpu] += sign * o.nbytes
 
-    def _policy_objs(self, g):
+    def _policy_objs(self, g, movable_only=False):
+        """The policy's view of GPU g's store. ``movable_only`` leaves out pinned
+        objects (live zero-copy views, victims another migration is already
+        moving out): their bytes are discounted by the caller, and a plan that
+        picked them would be dropped by the pins filter and cover nothing."""
         from .datastore import StoredObject
-        objs = sorted((o for o in self._objs.values() if o.home == g), key=lambda o: o.did)
+        objs = sorted((o for o in self._objs.values() if o.home == g and not (movable_only and o.pins)),
+                      key=lambda o: o.did)
         recs = [StoredObject(o.did, float(o.nbytes), o.producer, g, o.stored_at,
                              "gpu" if o.block is not None else "host",
                              {("c", i): o.queue_pos for i in range(max(1, o.remaining))}, not o.retired)
@@ -454,6 +459,7 @@ class FaaSTube:
             finally:
                 with self._lock:
                     self._migrating[g] -= moving
+                    skipped = False
                     for i, o in enumerate(chosen):
                         o.pins -= 1
                         buf = bufs[i] if i < len(bufs) else None
@@ -461,12 +467,16 @@ class FaaSTube:
                             if buf is not None and o.block is not None and o.pins == 0 and not o.retired:
                                 self._migrate_out(o, buf)
                             else:
+                                skipped = skipped or (o.block is not None and not o.retired)
                                 self._maybe_free(o)
                         else:
                             if buf is not None and o.host is not None and o.block is None and not o.retired:
                                 self._reload(o, g, buf)
                             elif buf is not None:
                                 self.pools[g].free(buf, list(buf.fences))
+                    if skipped and self._stored_on(g) - self._migrating.get(g, 0) > self.capacity_limit:
+                        # a victim was pinned (zero-copy view) meanwhile: plan again without it
+                        self._pending.add(("pressure", g))
 
     def _plan_migration(self, g) -> list:
         """Store cap exceeded -> the objects whose consumers sit farthest back in
@@ -475,7 +485,7 @@ class FaaSTube:
         if stored <= self.capacity_limit:
             return []
         from .datastore import migration_plan
-        objs, recs = self._policy_objs(g)
+        objs, recs = self._policy_objs(g, movable_only=True)     # in-flight victims are discounted above
         try:
             plan = migration_plan(recs, stored - self.capacity_limit, self.strategy.migration)
         except Exception:  # noqa: BLE001 - HardPressure: nothing migratable (engine.py:696-697)
@@ -639,6 +649,8 @@ class FaaSTube:
                     self.stats["bytes_local"] += o.nbytes
                     self.stats["fetches"] += 1
                     self._consumed(o, done)
+                    if not o.retired:
+                        self._hold_until(o, done)   # the last consumer's retire fences on this read
         for did, out in rest:
             self.fetch(did, out=out, consumer=consumer)
         if self._pending:
@@ -696,6 +708,7 @@ class FaaSTube:
         for g in self.gpus:
             for st in self._ce[g] + [x for pr in self._ce_pairs[g] + self._d2h_pairs[g] for x in pr]:
                 dev.destroy_stream(st)
+        dev.Ev.drain_free()
 
     # ------------------------------------------------------------ internals
     def _push_shrink(self, g, func, now):
@@ -826,9 +839,14 @@ class FaaSTube:
                 obj.ready.wait(s)
                 return self._view(obj)
             last = obj.remaining <= 1
-            # wait for the stored bytes and copy into the caller's input: one call
+            # wait for the stored bytes and copy into the caller's input: one call. A
+            # consumer that is not the last one leaves its read's event on the object:
+            # the last consumer's retire (maybe on another stream) fences the block on it
+            done = None if last else dev.Ev(dst.gpu)
             dev.copy_ordered(out.data_ptr(), obj.block.ptr, obj.nbytes, dst.gpu, s,
-                             dev.L2_EVICT_FIRST if last else dev.L2_NORMAL, (obj.ready,))
+                             dev.L2_EVICT_FIRST if last else dev.L2_NORMAL, (obj.ready,), done)
+            if done is not None:
+                self._hold_until(obj, done)
             self.stats["bytes_local"] += obj.nbytes
             return out
         if m == "inter_gpu":

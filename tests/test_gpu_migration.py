@@ -85,9 +85,49 @@ def test_concurrent_stores_under_pressure():
     assert not errs, errs
     assert tube.stats["migrated_bytes"] >= 4 * 40 * MB        # 320 MB stored against a 100 MB cap
     assert tube._accounts_consistent()
+    assert tube._stored_on(0) <= 100 * MB                      # no in-flight victim counted twice
     for i, d in enumerate(ids):
         got = tube.fetch(d, device=0, out=torch.empty_like(xs[i]))
         torch.cuda.synchronize()
         assert torch.equal(got, xs[i]), i
     assert tube._accounts_consistent()
+    tube.close()
+
+
+@pytest.mark.parametrize("order", ["rising", "falling"])
+def test_concurrent_stores_respect_cap(order):
+    """Concurrent tenants against a 100 MB cap, with the newest stores nearest
+    the queue front ("falling") or farthest ("rising"): after every store has
+    returned the GPU store holds at most the cap (a plan never re-picks a
+    victim another migration is already moving out), bytes stay exact."""
+    import threading
+    from paper_2411_01830_b200.tube import FaaSTube
+    tube = FaaSTube("faastube", pool_floor_bytes=0.0, capacity_limit_bytes=100 * MB)
+    xs = [torch.randint(0, 256, (40 * MB,), dtype=torch.uint8, device="cuda:0") for _ in range(12)]
+    torch.cuda.synchronize()
+    ids = [None] * len(xs)
+    errs = []
+
+    def tenant(k):
+        try:
+            for i in range(k, len(xs), 4):
+                d = tube.unique_id()
+                pos = i if order == "rising" else len(xs) - i
+                tube.store(d, xs[i], producer=f"p{k}", queue_pos=pos)
+                ids[i] = d
+        except Exception as e:  # noqa: BLE001
+            errs.append(e)
+
+    th = [threading.Thread(target=tenant, args=(k,)) for k in range(4)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
+    assert tube._stored_on(0) <= 100 * MB, tube._stored_on(0)
+    assert tube._accounts_consistent()
+    for i, d in enumerate(ids):
+        got = tube.fetch(d, device=0, out=torch.empty_like(xs[i]))
+        torch.cuda.synchronize()
+        assert torch.equal(got, xs[i]), i
     tube.close()

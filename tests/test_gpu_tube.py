@@ -351,3 +351,58 @@ def test_object_larger_than_4gib_same_gpu():
     del x, y
     assert t._accounts_consistent()
     t.close()
+
+
+def _spin(ms, stream):
+    import ctypes as C
+    from paper_2411_01830_b200 import device as dev
+    dev.LIB.ft_spin_ns(int(ms * 1e6), 0, C.c_void_p(stream.cuda_stream))
+
+
+@pytest.mark.parametrize("batched", [False, True])
+def test_early_consumer_read_fences_block_reuse(batched):
+    """Two consumers copy the same object into their inputs on different
+    streams. The first one's copy is still queued (its stream is busy) when the
+    second, last consumer retires the object and a new store reuses the block:
+    the reuse must wait for the first consumer's read (the read of a
+    consumer that is not the last one is a fence of the block)."""
+    from paper_2411_01830_b200.tube import FaaSTube
+    tube = FaaSTube("faastube", pool_floor_bytes=0.0, gpus=[0])
+    x = torch.randint(0, 256, (8 * MB,), dtype=torch.uint8, device="cuda:0")
+    y = torch.randint(0, 256, (8 * MB,), dtype=torch.uint8, device="cuda:0")
+    a, b = torch.cuda.Stream(0), torch.cuda.Stream(0)
+    out_a, out_b = torch.empty_like(x), torch.empty_like(x)
+    torch.cuda.synchronize()
+    did = tube.unique_id()
+    tube.store(did, x, consumers=2)
+    with torch.cuda.stream(a):
+        _spin(50, a)                                  # consumer A's stream is busy for 50 ms
+        if batched:
+            tube.fetch_many([(did, out_a)])
+        else:
+            tube.fetch(did, device=0, out=out_a)
+    with torch.cuda.stream(b):
+        tube.fetch(did, device=0, out=out_b)          # last consumer: retires, the block is free
+        did2 = tube.unique_id()
+        tube.store(did2, y)                           # same size class: reuses (overwrites) the block
+    torch.cuda.synchronize()
+    assert torch.equal(out_a, x) and torch.equal(out_b, x)
+    got = tube.fetch(did2, device=0, out=torch.empty_like(y))
+    torch.cuda.synchronize()
+    assert torch.equal(got, y)
+    assert tube._accounts_consistent()
+    tube.close()
+
+
+def test_event_unrecorded_is_refused():
+    """A pooled event handle carries its previous record: an Ev that was never
+    recorded must not be waited on (it would report unrelated work done)."""
+    from paper_2411_01830_b200 import device as dev
+    e = dev.Ev(0)
+    with pytest.raises(RuntimeError):
+        e.wait(torch.cuda.current_stream(0))
+    with pytest.raises(RuntimeError):
+        e.query()
+    e.record(torch.cuda.current_stream(0))
+    e.synchronize()
+    assert e.query()
