@@ -220,19 +220,14 @@ class TubeDaemon:
             self._reply(conn, {})
         elif op == "fetch":
             g, did = int(msg["gpu"]), int(msg["id"])
-            # zero-copy or not is decided under the tube lock, together with the fetch: a
-            # concurrent store could otherwise migrate the object to host memory between
-            # the check and the fetch. The view pins the block, so it cannot move after.
-            with tube._lock:  # noqa: SLF001
-                obj = tube._objs.get(did)  # noqa: SLF001
-                zero_copy = obj is not None and obj.gpu == g and obj.block is not None
-                if zero_copy:
-                    t = tube._fetch(did, device=g, consumer=msg.get("consumer", "func"))  # noqa: SLF001
-                    blk = obj.block
-            if zero_copy:
-                if tube._pending:  # noqa: SLF001 - prefetch made possible by this consumer's retire
-                    tube._drain_pending()  # noqa: SLF001
+            # zero-copy or not is decided atomically with the fetch (a concurrent store
+            # could otherwise migrate the object to host memory between a check and the
+            # fetch); the view pins the block, so it cannot move after
+            res = tube.fetch_resident(did, g, consumer=msg.get("consumer", "func"))
+            if res is not None:
+                t, blk = res
             else:
+                obj = tube._objs.get(did)  # noqa: SLF001
                 nbytes = obj.nbytes if obj is not None else 0
                 dst = tube.empty((max(1, nbytes),), torch.uint8, device=g)
                 try:

@@ -618,6 +618,21 @@ class FaaSTube:
             self._tickets.append((ticket, obj.host, res))
         return res
 
+    def fetch_resident(self, data_id: int, device: int, consumer: str = "func"):
+        """Zero-copy fetch if the object is stored in GPU ``device``'s pool right
+        now: (view, pool block) — decided and fetched under the tube lock, so a
+        concurrent migration cannot move it in between (the view pins the block).
+        None if it lives elsewhere (the caller fetches into a buffer instead)."""
+        with self._lock:
+            obj = self._objs.get(data_id)
+            if obj is None or obj.gpu != device or obj.block is None:
+                return None
+            view = self._fetch(data_id, device=device, consumer=consumer)
+            blk = obj.block
+        if self._pending:
+            self._drain_pending()          # prefetch made possible by this consumer's retire
+        return view, blk
+
     def fetch_many(self, items, consumer: str = "func") -> list:
         """Batched fetch (an extension of Listing 1): ``[(data_id, out)]`` into
         the callers' input buffers. Every object stored on ``out``'s own GPU

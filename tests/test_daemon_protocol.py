@@ -75,6 +75,12 @@ class _Tube:
             return self.stored[did]
         return self._objs[did].t
 
+    def fetch_resident(self, did, device, consumer="func"):
+        o = self._objs.get(did)
+        if o is None or o.gpu != device or o.block is None:
+            return None
+        return self.fetch(did, device, consumer=consumer), o.block
+
     def release(self, did):
         self._objs.pop(did, None)
 
