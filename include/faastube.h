@@ -212,6 +212,22 @@ int ft_store_commit(ft_index* x, ft_pool_policy* p, int64_t data_id, int node, i
                     double* last);
 int ft_retire_commit(ft_index* x, ft_pool_policy* p, int64_t data_id, int64_t block_id, const char* producer,
                      double* r_window, double* last);
+/* the same-GPU put in one call (engine.py:383-409, dataplane.py:72-83, datastore.py:51-62):
+ * `stream` waits on `waits` (the block's previous users), TMA copy src -> block_ptr
+ * (size_bytes, L2 `hints`), records `ready`, then ft_store_commit */
+int ft_store_local(ft_index* x, ft_pool_policy* p, int64_t data_id, int node, int gpu, double size_bytes,
+                   double now_ms, const char* producer, int response, double concurrency, void* block_ptr,
+                   const void* src, void* stream, uint32_t hints, void* const* waits, int nwaits, void* ready,
+                   double* r_window, double* last);
+/* the same-GPU get into the consumer's input in one call (dataplane.py:184-185,
+ * engine.py:667-679): wait `waits`, copy block_ptr -> dst, record `done`; when
+ * `retire` (last consumer) also ft_retire_commit */
+int ft_fetch_local(ft_index* x, ft_pool_policy* p, int64_t data_id, int64_t block_id, const char* producer,
+                   int retire, void* dst, const void* block_ptr, uint64_t bytes, int device, void* stream,
+                   uint32_t hints, void* const* waits, int nwaits, void* done, double* r_window, double* last);
+/* n x ft_retire_commit (batched fetch) */
+int ft_retire_many(ft_index* x, ft_pool_policy* p, int n, const int64_t* data_ids, const int64_t* block_ids,
+                   const char* const* producers, double* r_windows, double* lasts);
 /* DataIndex                                         dataplane.py:55-107 */
 int ft_index_create(double sync_period_ms, double local_lookup_ms, double global_lookup_ms, ft_index** out);
 void ft_index_destroy(ft_index* x);

@@ -370,6 +370,42 @@ int ft_retire_commit(ft_index* x, ft_pool_policy* p, int64_t id, int64_t block_i
   if (last) *last = h && h->has_last ? h->last : none();
   FT_CATCH
 }
+// the same-GPU put in one call: wait the block's previous users, TMA copy of the
+// producer's output into the block, record `ready`, then the store commit above
+int ft_store_local(ft_index* x, ft_pool_policy* p, int64_t id, int node, int gpu, double size, double now,
+                   const char* producer, int response, double concurrency, void* block_ptr, const void* src,
+                   void* stream, uint32_t hints, void* const* waits, int nwaits, void* ready, double* r_window,
+                   double* last) {
+  NEED(x);
+  NEED(p);
+  int rc = ft_copy_ordered(block_ptr, src, (uint64_t)size, gpu, stream, hints, waits, nwaits, ready);
+  if (rc != FT_OK) return rc;
+  return ft_store_commit(x, p, id, node, gpu, size, now, producer, response, concurrency, r_window, last);
+}
+// the same-GPU get into the caller's input in one call: wait `waits` (the stored
+// bytes), copy block -> dst, record `done`; the last consumer also retires
+// (block_id < 0: a view still pins the block)
+int ft_fetch_local(ft_index* x, ft_pool_policy* p, int64_t id, int64_t block_id, const char* producer, int retire,
+                   void* dst, const void* block_ptr, uint64_t bytes, int device, void* stream, uint32_t hints,
+                   void* const* waits, int nwaits, void* done, double* r_window, double* last) {
+  NEED(x);
+  NEED(p);
+  int rc = ft_copy_ordered(dst, block_ptr, bytes, device, stream, hints, waits, nwaits, done);
+  if (rc != FT_OK || !retire) return rc;
+  return ft_retire_commit(x, p, id, block_id, producer, r_window, last);
+}
+// n retires in one call (batched fetch)
+int ft_retire_many(ft_index* x, ft_pool_policy* p, int n, const int64_t* ids, const int64_t* block_ids,
+                   const char* const* producers, double* r_windows, double* lasts) {
+  NEED(x);
+  NEED(p);
+  for (int i = 0; i < n; ++i) {
+    int rc = ft_retire_commit(x, p, ids[i], block_ids[i], producers[i], r_windows ? r_windows + i : nullptr,
+                              lasts ? lasts + i : nullptr);
+    if (rc != FT_OK) return rc;
+  }
+  return FT_OK;
+}
 int ft_pool_policy_target(ft_pool_policy* p, double now, double* out) { NEED(p); *out = p->p.target(now); return FT_OK; }
 int ft_pool_policy_hist(const ft_pool_policy* p, const char* func, double* rw, double* last) {
   NEED(p);

@@ -26,6 +26,7 @@
 #include <vector>
 
 #include "../../include/faastube.h"
+#include "forward.h"
 
 namespace ft {
 void set_last_error(const std::string& msg);
@@ -59,6 +60,8 @@ struct Drv {
   decltype(&cuMemImportFromShareableHandle) import_handle;
   decltype(&cuMemGetAllocationGranularity) granularity;
   decltype(&cuGetErrorString) err;
+  decltype(&cuStreamWaitValue32) wait32;
+  decltype(&cuStreamWriteValue32) write32;
 };
 Drv g_drv;
 std::once_flag g_drv_once;
@@ -79,7 +82,8 @@ Drv* drv() {
            sym("cuMemMap", &d.map) && sym("cuMemUnmap", &d.unmap) && sym("cuMemSetAccess", &d.set_access) &&
            sym("cuMemExportToShareableHandle", &d.export_handle) &&
            sym("cuMemImportFromShareableHandle", &d.import_handle) &&
-           sym("cuMemGetAllocationGranularity", &d.granularity) && sym("cuGetErrorString", &d.err);
+           sym("cuMemGetAllocationGranularity", &d.granularity) && sym("cuGetErrorString", &d.err) &&
+           sym("cuStreamWaitValue32", &d.wait32) && sym("cuStreamWriteValue32", &d.write32);
   });
   return g_drv.ok ? &g_drv : nullptr;
 }
@@ -447,6 +451,73 @@ __global__ void k_spin_ns(uint64_t ns) {
   } while (t - t0 < ns);
 }
 
+// K2 forward: chunks of a staging ring -> destination (over NVLink when the
+// destination is a peer's memory). See forward.h for the protocol. Every CTA
+// walks the batch's chunks in order: thread 0 polls the slot's landed word
+// (acquire, bounded), the CTA pulls its tiles of the chunk with 16-byte loads
+// (4 in flight per thread), then thread 0 counts the CTA's share read
+// (release add on the slot's freed word: the CE may overwrite it once all
+// kFwdCtas CTAs have counted).
+__global__ void __launch_bounds__(256) k_forward(uint8_t* __restrict__ dst, const uint8_t* __restrict__ ring,
+                                                 uint64_t slot_bytes, const uint32_t* landed, uint32_t* freed,
+                                                 uint32_t* err, const __grid_constant__ ft::FwdBatch b) {
+  constexpr uint64_t kTile = 256 * 4 * 16;  // bytes per CTA step
+  __shared__ int ok;
+  for (int c = 0; c < b.n; ++c) {
+    const ft::FwdChunk ch = b.c[c];
+    if (threadIdx.x == 0) {
+      uint32_t v;
+      uint64_t t0, t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+      int good = 1;
+      for (;;) {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(landed + ch.slot) : "memory");
+        if ((int32_t)(v - ch.gen) >= 0) break;
+        __nanosleep(64);
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (t - t0 > 10000000000ull) {  // 10 s: the DMA never landed; report, do not hang
+          good = 0;
+          if (err) atomicExch(err, 1u);
+          break;
+        }
+      }
+      ok = good;
+    }
+    __syncthreads();
+    const uint8_t* src = ring + (uint64_t)ch.slot * slot_bytes;
+    uint8_t* d = dst + ch.dst_off;
+    if (ok && (reinterpret_cast<uintptr_t>(d) & 15)) {  // misaligned destination: bytewise
+      for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ch.len;
+           i += (uint64_t)gridDim.x * blockDim.x)
+        d[i] = src[i];
+    } else if (ok) {
+      const uint64_t n16 = ch.len / 16;
+      const int4* s4 = reinterpret_cast<const int4*>(src);
+      int4* d4 = reinterpret_cast<int4*>(d);
+      for (uint64_t base = (uint64_t)blockIdx.x * (kTile / 16); base < n16; base += (uint64_t)gridDim.x * (kTile / 16)) {
+        int4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          uint64_t i = base + threadIdx.x + u * 256;
+          if (i < n16) v[u] = __ldcs(s4 + i);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          uint64_t i = base + threadIdx.x + u * 256;
+          if (i < n16) __stcs(d4 + i, v[u]);
+        }
+      }
+      if (blockIdx.x == 0)
+        for (uint64_t i = n16 * 16 + threadIdx.x; i < ch.len; i += blockDim.x) d[i] = src[i];
+    }
+    __syncthreads();  // every load of this CTA's share has returned (its values were stored)
+    if (threadIdx.x == 0) {
+      __threadfence();
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(freed + ch.slot) : "memory");
+    }
+  }
+}
+
 // ------------------------------------------------------------ launch config
 struct DevInfo {
   int sms = 0;
@@ -513,8 +584,22 @@ int launch_bulk(uint8_t* dst, const uint8_t* src, uint64_t bytes, int device, cu
     default: return launch_bulk_h<2>(dst, src, bytes, device, st, grid, c.tile, c.ctas_per_sm, hints);
   }
 }
+// Small copies (<= kVecWide): the whole payload in flight at once — 2 x 16 B per
+// thread, 256-thread CTAs, one CTA per 8 KiB (1 MiB -> 128 CTAs). A peer pull is
+// latency-bound at these sizes (900 GB/s x ~1.5 us of NVLink round trip is ~1.3 MB
+// in flight), so every load must be issued in the first wave; the grid-stride
+// shape below (4 x 16 B per thread, 2 CTAs/SM of 512) would put only 32 CTAs on
+// a 1 MiB copy. Larger copies: persistent grid-stride.
+constexpr uint64_t kVecWide = 4ull << 20;
 int launch_vec(uint8_t* dst, const uint8_t* src, uint64_t bytes, int device, cudaStream_t st, int grid) {
   uint64_t n16 = bytes / 16;
+  if (grid <= 0 && bytes <= kVecWide) {
+    uint64_t ctas = (n16 + 256 * 2 - 1) / (256 * 2);
+    k_copy_vec<2><<<(int)(ctas ? ctas : 1), 256, 0, st>>>(reinterpret_cast<int4*>(dst),
+                                                          reinterpret_cast<const int4*>(src), n16);
+    CU_RT(cudaGetLastError());
+    return FT_OK;
+  }
   if (grid <= 0) grid = 2 * dev_sms(device);
   uint64_t need = (n16 + 512 * 4 - 1) / (512 * 4);
   if (need < (uint64_t)grid) grid = (int)(need ? need : 1);
@@ -577,6 +662,35 @@ std::mutex g_imp_mu;
 std::map<uint64_t, Import> g_imports;
 std::atomic<uint64_t> g_imp_next{1};
 
+// VA ranges of the pools (reserved per GPU): a pointer inside one is device memory
+// of that GPU, so ft_copy picks its engine without cudaPointerGetAttributes (two
+// driver queries, ~1 us each) for pool blocks — the request path's usual operands.
+struct VaRange {
+  uintptr_t lo, hi;
+  int device;
+};
+std::mutex g_va_mu;
+std::vector<VaRange> g_va;
+std::atomic<int> g_va_n{0};
+int va_device(const void* p) {
+  if (!g_va_n.load(std::memory_order_acquire)) return -1;
+  uintptr_t a = (uintptr_t)p;
+  std::lock_guard<std::mutex> lk(g_va_mu);
+  for (const VaRange& r : g_va)
+    if (a >= r.lo && a < r.hi) return r.device;
+  return -1;
+}
+void va_add(uintptr_t lo, size_t n, int device) {
+  std::lock_guard<std::mutex> lk(g_va_mu);
+  g_va.push_back({lo, lo + n, device});
+  g_va_n.store((int)g_va.size(), std::memory_order_release);
+}
+void va_remove(uintptr_t lo) {
+  std::lock_guard<std::mutex> lk(g_va_mu);
+  g_va.erase(std::remove_if(g_va.begin(), g_va.end(), [&](const VaRange& r) { return r.lo == lo; }), g_va.end());
+  g_va_n.store((int)g_va.size(), std::memory_order_release);
+}
+
 }  // namespace
 
 struct ft_vmm_pool {
@@ -590,6 +704,77 @@ struct ft_vmm_pool {
   size_t mapped = 0;
   std::mutex mu;
 };
+
+namespace ft {
+
+int fwd_ring_words(int device, int slots, uint32_t** landed, uint32_t** freed, uint32_t** err_host) {
+  int cur = 0;
+  CU_RT(cudaGetDevice(&cur));
+  if (cur != device) CU_RT(cudaSetDevice(device));
+  void* w = nullptr;
+  void* e = nullptr;
+  cudaError_t r = cudaMalloc(&w, 2 * sizeof(uint32_t) * (size_t)slots);
+  if (r == cudaSuccess) r = cudaMemset(w, 0, 2 * sizeof(uint32_t) * (size_t)slots);
+  if (r == cudaSuccess) r = cudaHostAlloc(&e, sizeof(uint32_t), cudaHostAllocMapped | cudaHostAllocPortable);
+  if (cur != device) cudaSetDevice(cur);
+  if (r != cudaSuccess) {
+    if (w) cudaFree(w);
+    return cuda_fail(r, "forward ring words");
+  }
+  *static_cast<uint32_t*>(e) = 0;
+  *landed = static_cast<uint32_t*>(w);
+  *freed = static_cast<uint32_t*>(w) + slots;
+  *err_host = static_cast<uint32_t*>(e);
+  return FT_OK;
+}
+void fwd_ring_words_free(int device, uint32_t* landed, uint32_t* err_host) {
+  int cur = 0;
+  cudaGetDevice(&cur);
+  cudaSetDevice(device);
+  if (landed) cudaFree(landed);
+  if (err_host) cudaFreeHost(err_host);
+  cudaSetDevice(cur);
+}
+int fwd_preload(int device) {
+  int cur = 0;
+  CU_RT(cudaGetDevice(&cur));
+  if (cur != device) CU_RT(cudaSetDevice(device));
+  cudaFuncAttributes a;
+  cudaError_t r = cudaFuncGetAttributes(&a, k_forward);
+  if (cur != device) cudaSetDevice(cur);
+  return r == cudaSuccess ? FT_OK : cuda_fail(r, "k_forward preload");
+}
+int mem_write32(cudaStream_t st, uint32_t* addr, uint32_t value) {
+  Drv* d = drv();
+  if (!d) {
+    set_last_error("CUDA driver stream memory operations unavailable");
+    return FT_E_NOT_SUPPORTED;
+  }
+  CU_DRV(d->write32((CUstream)st, (CUdeviceptr)addr, value, CU_STREAM_WRITE_VALUE_DEFAULT));
+  return FT_OK;
+}
+int mem_wait_geq32(cudaStream_t st, uint32_t* addr, uint32_t value) {
+  Drv* d = drv();
+  if (!d) {
+    set_last_error("CUDA driver stream memory operations unavailable");
+    return FT_E_NOT_SUPPORTED;
+  }
+  CU_DRV(d->wait32((CUstream)st, (CUdeviceptr)addr, value, CU_STREAM_WAIT_VALUE_GEQ));
+  return FT_OK;
+}
+int fwd_launch(int device, cudaStream_t st, uint8_t* dst, const uint8_t* ring, uint64_t slot_bytes,
+               const uint32_t* landed, uint32_t* freed, uint32_t* err, const FwdBatch& b) {
+  if (b.n <= 0) return FT_OK;
+  int cur = 0;
+  CU_RT(cudaGetDevice(&cur));
+  if (cur != device) CU_RT(cudaSetDevice(device));
+  k_forward<<<kFwdCtas, 256, 0, st>>>(dst, ring, slot_bytes, landed, freed, err, b);
+  cudaError_t e = cudaGetLastError();
+  if (cur != device) cudaSetDevice(cur);
+  return e == cudaSuccess ? FT_OK : cuda_fail(e, "k_forward");
+}
+
+}  // namespace ft
 
 extern "C" {
 
@@ -659,6 +844,7 @@ int ft_vmm_pool_create(int device, uint64_t va_bytes, ft_vmm_pool** out) {
   p->base = base;
   p->va_bytes = va_bytes;
   p->free_va[0] = va_bytes;
+  va_add((uintptr_t)base, va_bytes, device);
   *out = p;
   return FT_OK;
 }
@@ -671,6 +857,7 @@ void ft_vmm_pool_destroy(ft_vmm_pool* p) {
       d->unmap(kv.second.va, kv.second.bytes);
       d->release(kv.second.h);
     }
+    va_remove((uintptr_t)p->base);
     d->addr_free(p->base, p->va_bytes);
   }
   delete p;
@@ -916,7 +1103,10 @@ int ft_fd_recv(int sock, int* fd, uint64_t* tag) {
 
 int ft_copy(void* dst, const void* src, uint64_t bytes, int device, void* stream) {
   // auto engine: TMA bulk when both sides are memory of `device`, else the
-  // peer-safe vector engine.
+  // peer-safe vector engine. Pool blocks are recognised by their VA range.
+  const int vd = va_device(dst), vs = va_device(src);
+  if (vd >= 0 && vs >= 0) return copy_impl(dst, src, bytes, device, (cudaStream_t)stream,
+                                           vd == device && vs == device ? 1 : 2, 0);
   cudaPointerAttributes a{}, b{};
   int engine = 1;
   if (cudaPointerGetAttributes(&a, dst) != cudaSuccess || cudaPointerGetAttributes(&b, src) != cudaSuccess) {

@@ -42,6 +42,8 @@
 // slots without holding `mu`.
 #include <cuda_runtime.h>
 #include <emmintrin.h>
+
+#include "forward.h"
 #include <sys/prctl.h>
 
 #include <algorithm>
@@ -179,6 +181,15 @@ struct StagingRing {  // chunk ring on a staging GPU
   std::vector<char> used;
 };
 
+struct KRing {  // K2 chunk ring on a staging GPU (host->GPU staged routes, forward.h)
+  uint8_t* buf = nullptr;
+  int slots = 0, next = 0;
+  uint64_t slot_bytes = 0;
+  uint32_t *landed = nullptr, *freed = nullptr, *err = nullptr;
+  std::vector<uint32_t> uses;  // per slot: chunks issued into it so far
+  uint64_t alt = 0;            // CE ops issued (alternates the two CE streams)
+};
+
 struct HostSlot {
   bool busy = false;
   int last_dev = -1;  // device of the event guarding the slot's last DMA
@@ -227,7 +238,10 @@ struct ft_pacer {
   uint64_t last_issue_ticket[2][kMaxDev] = {};
   bool adapt = true;
   uint64_t timed_skip = 0;
-  std::map<int, StagingRing> rings;
+  std::map<int, StagingRing> rings;  // GPU->host staged routes
+  std::map<int, KRing> krings;       // host->GPU staged routes (K2)
+  std::map<cudaStream_t, cudaStream_t> ce2;  // second CE stream of each route CE stream
+  bool k2 = true;                    // FT_K2=0: the per-piece event chain (previous design)
   std::map<std::string, double> guarded;  // last early boundary per stage key (A2 guard)
   uint64_t n_stages = 0, n_managed = 0, n_batches = 0, n_bytes = 0, n_errors = 0;
   std::vector<std::string> trace, log;
@@ -338,10 +352,78 @@ struct ft_pacer {
     return rings.emplace(dev, std::move(r)).first->second;
   }
 
+  KRing& kring(int dev) {
+    auto it = krings.find(dev);
+    if (it != krings.end()) return it->second;
+    KRing K;
+    DevGuard g(dev);
+    // same memory as the event-chained ring: staging_slots x stage_chunk, cut into
+    // chunk-sized slots (pcie_sched.py:14's 2 MB)
+    K.slot_bytes = (chunk + 255) / 256 * 256;
+    K.slots = (int)std::max<uint64_t>(2, (uint64_t)staging_slots * stage_chunk / K.slot_bytes);
+    K.slots = std::min(K.slots, ft::kFwdMaxChunks);
+    void* p = nullptr;
+    ck(cudaMalloc(&p, (size_t)K.slots * K.slot_bytes), "K2 ring cudaMalloc");
+    K.buf = static_cast<uint8_t*>(p);
+    if (ft::fwd_ring_words(dev, K.slots, &K.landed, &K.freed, &K.err) != FT_OK ||
+        ft::fwd_preload(dev) != FT_OK)
+      throw CudaFail{std::string("K2 ring: ") + ft_last_error()};
+    K.uses.assign(K.slots, 0);
+    return krings.emplace(dev, std::move(K)).first->second;
+  }
+  cudaStream_t ce_pair(cudaStream_t ce, int dev) {
+    auto it = ce2.find(ce);
+    if (it != ce2.end()) return it->second;
+    DevGuard g(dev);
+    cudaStream_t s2;
+    ck(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking), "second CE stream");
+    ce2.emplace(ce, s2);
+    return s2;
+  }
+
+  // K2: the staged host->GPU leg. Chunks alternate over two CE streams (one op's
+  // fixed cost hides behind the other's transfer), each followed by a device-side
+  // write of the slot's landed word; one forward kernel per <= slots chunks pulls
+  // them as they land and counts each slot free. Returns the CE stream of the last op.
+  cudaStream_t issue_k2(Route& r, uint8_t* dptr, uint8_t* hptr, uint64_t n) {
+    KRing& K = kring(r.dev);
+    cudaStream_t c2 = ce_pair(r.ce, r.dev), last = r.ce;
+    ft::FwdBatch b;
+    b.n = 0;
+    auto flush = [&] {
+      if (!b.n) return;
+      if (ft::fwd_launch(r.dev, r.fw, dptr, K.buf, K.slot_bytes, K.landed, K.freed, K.err, b) != FT_OK)
+        throw CudaFail{std::string("forward: ") + ft_last_error()};
+      b.n = 0;
+    };
+    for (uint64_t o = 0; o < n; o += K.slot_bytes) {
+      const uint64_t c = std::min<uint64_t>(K.slot_bytes, n - o);
+      const int s = K.next;
+      K.next = (s + 1) % K.slots;
+      cudaStream_t cs = (K.alt++ & 1) ? c2 : r.ce;
+      // the slot's previous chunk has been read by every CTA of its forward launch
+      // (that launch was enqueued before: a launch holds at most one chunk per slot)
+      if (K.uses[s] && ft::mem_wait_geq32(cs, K.freed + s, K.uses[s] * (uint32_t)ft::kFwdCtas) != FT_OK)
+        throw CudaFail{std::string("wait slot freed: ") + ft_last_error()};
+      const uint32_t gen = ++K.uses[s];
+      ck(cudaMemcpyAsync(K.buf + (uint64_t)s * K.slot_bytes, hptr + o, c, cudaMemcpyHostToDevice, cs),
+         "staging H2D");
+      if (ft::mem_write32(cs, K.landed + s, gen) != FT_OK)
+        throw CudaFail{std::string("write landed: ") + ft_last_error()};
+      b.c[b.n++] = ft::FwdChunk{o, (uint32_t)s, gen, c};
+      n_bytes += c;
+      last = cs;
+      if (b.n == K.slots) flush();
+    }
+    flush();
+    return last;
+  }
+
   // n bytes between the GPU buffer `dptr` and the pinned host buffer `hptr` over
-  // route r: host->GPU (dir 0) or GPU->host (dir 1)
-  void issue(Route& r, uint8_t* dptr, uint8_t* hptr, uint64_t n, int dir) {
-    if (n == 0) return;
+  // route r: host->GPU (dir 0) or GPU->host (dir 1). Returns the stream of the
+  // last copy-engine op (the one that reads / writes host memory last).
+  cudaStream_t issue(Route& r, uint8_t* dptr, uint8_t* hptr, uint64_t n, int dir) {
+    if (n == 0) return r.ce;
     DevGuard g(r.dev);
     if (!r.staged()) {
       if (dir == 0)
@@ -349,8 +431,9 @@ struct ft_pacer {
       else
         ck(cudaMemcpyAsync(hptr, dptr, n, cudaMemcpyDeviceToHost, r.ce), "D2H");
       n_bytes += n;
-      return;
+      return r.ce;
     }
+    if (dir == 0 && k2) return issue_k2(r, dptr, hptr, n);
     StagingRing& R = ring(r.dev);
     // pieces per route: 1/32 of it, between one chunk and a full slot. Each piece is
     // a CE op + forward kernel; a 2 MB piece loses ~9 % of the link to per-op gaps
@@ -385,6 +468,7 @@ struct ft_pacer {
       R.used[s] = 1;
       n_bytes += c;
     }
+    return r.ce;
   }
 
   // hand bytes [rel, rel+n) of route i to the movers (direct DMA or worker jobs)
@@ -478,6 +562,15 @@ struct ft_pacer {
         pending = true;
         continue;
       }
+      if (st.dir == 0 && st.err == FT_OK)
+        for (auto& r : st.routes)
+          if (r.staged()) {
+            auto k = krings.find(r.dev);
+            if (k != krings.end() && *(volatile uint32_t*)k->second.err) {
+              st.err = FT_E_TIMEOUT;
+              st.msg = "forward kernel: a staged chunk never landed (10 s)";
+            }
+          }
       for (auto& e : st.landing) put_event(e.second, e.first);
       st.landing.clear();
       std::lock_guard<std::mutex> lk(lmu);
@@ -763,10 +856,10 @@ struct ft_pacer {
           Route& r = st.routes[j.route];
           try {
             if (st.err == FT_OK) {
-              issue(r, st.dst + j.obj_off, slot, j.n, 0);  // pageable: host->GPU only
+              cudaStream_t rd = issue(r, st.dst + j.obj_off, slot, j.n, 0);  // pageable: host->GPU only
               DevGuard g(r.dev);
               if (!hs.ev[r.dev]) ck(cudaEventCreateWithFlags(&hs.ev[r.dev], cudaEventDisableTiming), "event");
-              ck(cudaEventRecord(hs.ev[r.dev], r.ce), "record slot");  // the CE read of the slot
+              ck(cudaEventRecord(hs.ev[r.dev], rd), "record slot");  // the CE read of the slot
               hs.last_dev = r.dev;
             }
             --st.jobs;
@@ -818,6 +911,7 @@ int ft_pacer_create(double bw_all_gbps, int links, int batch_chunks, int64_t chu
   p->chunk = (uint64_t)chunk_bytes;
   p->staging_slots = std::max(2, staging_slots);
   p->stage_chunk = 4 * (uint64_t)chunk_bytes;
+  if (const char* c = std::getenv("FT_K2")) p->k2 = std::atoi(c) != 0;
   if (const char* c = std::getenv("FT_STAGE_CHUNK")) {
     p->stage_chunk = std::max<uint64_t>(1 << 16, std::atoll(c));
     p->fixed_stage_chunk = true;
@@ -867,6 +961,16 @@ int ft_pacer_destroy(ft_pacer* p) {
   p->jcv.notify_all();
   p->pacer.join();
   for (auto& t : p->workers) t.join();
+  for (auto& kv : p->krings) {
+    DevGuard g(kv.first);
+    cudaDeviceSynchronize();
+    cudaFree(kv.second.buf);
+    ft::fwd_ring_words_free(kv.first, kv.second.landed, kv.second.err);
+  }
+  for (auto& kv : p->ce2) {
+    cudaStreamSynchronize(kv.second);
+    cudaStreamDestroy(kv.second);
+  }
   for (auto& kv : p->rings) {
     DevGuard g(kv.first);
     cudaDeviceSynchronize();
@@ -952,7 +1056,10 @@ static int submit_impl(ft_pacer* p, int dir, const char* key, int managed, doubl
     for (auto& r : st.routes) {
       DevGuard gr(r.dev);
       ck(cudaStreamWaitEvent(r.ce, e, 0), "route waits consumer");
-      if (r.staged()) ck(cudaStreamWaitEvent(r.fw, e, 0), "forward waits consumer");
+      if (r.staged()) {
+        ck(cudaStreamWaitEvent(r.fw, e, 0), "forward waits consumer");
+        if (dir == 0 && p->k2) ck(cudaStreamWaitEvent(p->ce_pair(r.ce, r.dev), e, 0), "CE pair waits consumer");
+      }
     }
     p->put_event(dst_dev, e);
     ++p->n_stages;

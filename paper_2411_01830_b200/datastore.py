@@ -113,6 +113,7 @@ class MemoryPool:
         self._h = h
         self._blocks = {}
         self.histograms = {}
+        self._out = (C.c_int64(), C.c_int64(), C.c_double())
 
     def __del__(self, _destroy=destroyer("ft_pool_policy_destroy")):
         h = getattr(self, "_h", None)
@@ -160,8 +161,8 @@ class MemoryPool:
 
     def allocate(self, size_bytes: float):
         """-> (block, latency_ms)   datastore.py:130-144"""
-        bid, cls, cost = C.c_int64(), C.c_int64(), C.c_double()
-        LIB.ft_pool_policy_allocate(self._h, float(size_bytes), C.byref(bid), C.byref(cls), C.byref(cost))
+        bid, cls, cost = self._out                      # reused out-params (callers serialise)
+        LIB.ft_pool_policy_allocate(self._h, float(size_bytes), bid, cls, cost)
         b = self._blocks.get(bid.value)
         if b is None:
             b = self._blocks[bid.value] = Block(cls.value, True, bid.value)

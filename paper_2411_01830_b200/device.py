@@ -316,6 +316,8 @@ class DevicePool:
         # every CUDA call of the process for 100s of ms — measured)
         self._released = []  # [(vmm id, ptr, bytes, fences)]
         self._lock = threading.Lock()
+        self._names = {}             # producer name -> bytes (encoded once)
+        self._rw, self._last = C.c_double(), C.c_double()   # out-params of the hot calls (under _lock)
         self.grow_events = 0
         # spares: after growth of a class, a background thread maps one more block of
         # that class into the parked list, so the next growth of the class is a reuse.
@@ -460,6 +462,70 @@ class DevicePool:
                                 float(now_ms), producer.encode(), int(bool(response)), float(concurrency),
                                 C.byref(rw), C.byref(last))
         return rw.value, (None if last.value != last.value else last.value)
+
+    def _enc(self, func: str) -> bytes:
+        b = self._names.get(func)
+        if b is None:
+            b = self._names[func] = func.encode()
+        return b
+
+    def store_local(self, index, data_id: int, node: int, nbytes: int, now_ms: float, producer: str,
+                    response: bool, concurrency: float, blk: "PoolBlock", src_ptr: int, stream: int, hints: int,
+                    ready: "Ev"):
+        """The same-GPU put in one native call (``ft_store_local``): the stream
+        waits on the block's fences, copies the output into it, records
+        ``ready``; index entry + histogram sample. Returns (R_window, last | None)."""
+        evs = [e._recorded() for e in blk.fences if e is not None]
+        with self._lock:
+            LIB.ft_store_local(index._h, self.policy._h, int(data_id), int(node), self.device, float(nbytes),
+                               float(now_ms), self._enc(producer), int(bool(response)), float(concurrency),
+                               C.c_void_p(blk.ptr), C.c_void_p(src_ptr), C.c_void_p(stream), int(hints),
+                               (C.c_void_p * max(1, len(evs)))(*evs), len(evs), C.c_void_p(ready.h),
+                               self._rw, self._last)
+            ready.rec = True
+            blk.fences = ()                  # the copy waited on them
+            rw, last = self._rw.value, self._last.value
+        return rw, (None if last != last else last)
+
+    def fetch_local(self, index, data_id: int, blk: "PoolBlock", producer: str, retire: bool, dst_ptr: int,
+                    nbytes: int, stream: int, hints: int, waits, done: "Ev", fences=()):
+        """The same-GPU get into the consumer's input in one native call
+        (``ft_fetch_local``): wait ``waits``, copy, record ``done``; with
+        ``retire`` the index entry goes and the block returns to the policy,
+        fenced on ``done`` + ``fences``. Returns (R_window, last | None)."""
+        evs = [e._recorded() for e in waits if e is not None]
+        with self._lock:
+            LIB.ft_fetch_local(index._h, self.policy._h, int(data_id),
+                               blk.policy_block.block_id if retire else -1, self._enc(producer), int(retire),
+                               C.c_void_p(dst_ptr), C.c_void_p(blk.ptr), int(nbytes), self.device,
+                               C.c_void_p(stream), int(hints), (C.c_void_p * max(1, len(evs)))(*evs), len(evs),
+                               C.c_void_p(done.h), self._rw, self._last)
+            done.rec = True
+            if retire:
+                blk.policy_block.in_use = False
+                self._fences[blk.policy_block.block_id] = (done,) + tuple(fences)
+                if self.policy.mode == "none":
+                    self.policy._blocks.pop(blk.policy_block.block_id, None)
+                    self._unmap(blk.policy_block.block_id)
+            rw, last = self._rw.value, self._last.value
+        return rw, (None if last != last else last)
+
+    def retire_many(self, index, items):
+        """Batched retire: [(data_id, block, producer, fences)] -> [(R_window, last | None)]."""
+        n = len(items)
+        ids = (C.c_int64 * n)(*[d for d, _, _, _ in items])
+        bids = (C.c_int64 * n)(*[b.policy_block.block_id for _, b, _, _ in items])
+        names = (C.c_char_p * n)(*[self._enc(f) for _, _, f, _ in items])
+        rws, lasts = (C.c_double * n)(), (C.c_double * n)()
+        with self._lock:
+            LIB.ft_retire_many(index._h, self.policy._h, n, ids, bids, names, rws, lasts)
+            for _, b, _, f in items:
+                b.policy_block.in_use = False
+                self._fences[b.policy_block.block_id] = tuple(f)
+                if self.policy.mode == "none":
+                    self.policy._blocks.pop(b.policy_block.block_id, None)
+                    self._unmap(b.policy_block.block_id)
+        return [(rws[i], None if lasts[i] != lasts[i] else lasts[i]) for i in range(n)]
 
     def commit_retire(self, index, data_id: int, blk: "PoolBlock", fences, producer: str):
         """Index drop + block back to the policy (fenced) + the producer's window

@@ -136,6 +136,7 @@ class FaaSTube:
         self.slow_stores = collections.deque(maxlen=64)   # stores over 10 ms: (alloc ms, locked ms, bytes)
         self._pending = set()        # ("pressure" | "prefetch", gpu): decided under the lock, run after it
         self._migrating = {}         # gpu -> bytes of migration victims being moved out
+        self._off_gpu = collections.Counter()   # home gpu -> live objects migrated off it (prefetch candidates)
         self._t0 = time.perf_counter()
         self._objs: dict[int, _Obj] = {}
         self._lock = threading.RLock()
@@ -153,6 +154,7 @@ class FaaSTube:
         self._stored = collections.Counter()  # gpu -> bytes of live objects in its store
         self._pending_release = []   # (event, plan): NVLink claims held until the copy lands
         self._shrink_due = []        # heap of (due_ms, gpu)
+        self._last_due = None        # the newest (due, gpu) pushed (a retire repeats its store's)
         self._managed_ids = itertools.count(1)
         self._queue = itertools.count(1)
         self._maint_cv = threading.Condition()
@@ -330,6 +332,9 @@ class FaaSTube:
                 if blk is not None and blk.ptr == t.data_ptr():
                     obj.block = blk                      # zero-copy store of a pool-backed output
                     obj.ready = dev.Ev(g).record(self._stream(g))
+                    # index entry (dataplane.py:72-83) + histogram sample (datastore.py:51-62)
+                    rw, last = pool.commit_store(self.index, data_id, self.node, g, nbytes, now, producer,
+                                                 response, live_here + 1)
                 else:
                     blk = pre_blk                        # datastore.py:130-144 (allocated above)
                     obj.block = blk
@@ -341,15 +346,13 @@ class FaaSTube:
                     # measured 5% slower per pass (tools/sweep_hints.py: 37.9 vs 35.8 us)
                     hints = dev.L2_EVICT_FIRST if nbytes <= _L2_KEEP else 0
                     obj.ready = dev.Ev(g)
-                    # waits for the block's previous users, copies, records `ready`: one call
-                    dev.copy_ordered(blk.ptr, t.data_ptr(), nbytes, g, so.cuda_stream, hints, blk.take_fences(),
-                                     obj.ready)
+                    # one native call: wait the block's previous users, copy, record `ready`,
+                    # index entry (dataplane.py:72-83) + histogram sample (datastore.py:51-62)
+                    rw, last = pool.store_local(self.index, data_id, self.node, nbytes, now, producer, response,
+                                                live_here + 1, blk, t.data_ptr(), so.cuda_stream, hints, obj.ready)
                     t.record_stream(so)
                     self.stats["bytes_local"] += nbytes
-                # index entry (dataplane.py:72-83) + histogram sample (datastore.py:51-62) +
-                # the shrink timer at last_request + R_window (engine.py:656-659): one FFI call
-                rw, last = pool.commit_store(self.index, data_id, self.node, g, nbytes, now, producer, response,
-                                             live_here + 1)
+                # the shrink timer at last_request + R_window (engine.py:656-659)
                 self._push_due(g, rw, last, now)
                 if response:
                     resp = self._respond(obj, pre_host)
@@ -400,13 +403,15 @@ class FaaSTube:
 
     def _accounts_consistent(self) -> bool:
         """The running counters equal a recount of the table (tests)."""
-        live, stored = collections.Counter(), collections.Counter()
+        live, stored, off = collections.Counter(), collections.Counter(), collections.Counter()
         for o in self._objs.values():
             if o.gpu is not None:
                 live[(o.producer, o.gpu)] += 1
                 if o.block is not None:
                     stored[o.gpu] += o.nbytes
-        return (+self._live == +live) and (+self._stored == +stored)
+            if o.home is not None and o.block is None and o.host is not None:
+                off[o.home] += 1
+        return (+self._live == +live) and (+self._stored == +stored) and (+self._off_gpu == +off)
 
     def _account(self, o: _Obj, sign: int):
         """Running per-(producer, GPU) live counts and per-GPU stored bytes of the
@@ -507,13 +512,14 @@ class FaaSTube:
         o.readers = []
         o.host, o.ready, o.gpu = host, ev, None
         self._account(o, 1)
+        self._off_gpu[o.home] += 1
         self.index.relocate(o.did, self._loc(None))
         self.stats["migrated_bytes"] += o.nbytes
         self.stats["bytes_d2h"] += o.nbytes
 
     def _plan_prefetch(self, g) -> list:
         """Room freed -> reload migrated objects, nearest consumer first (datastore.py:225-238)."""
-        if not any(o.home == g and o.block is None and o.host is not None for o in self._objs.values()):
+        if not self._off_gpu[g]:
             return []                                 # nothing migrated off this GPU
         free = self.capacity_limit - self._stored_on(g)
         if free <= 0:
@@ -534,6 +540,7 @@ class FaaSTube:
         self._account(o, -1)
         o.block, o.ready, o.gpu, o.host = blk, ev, g, None
         self._account(o, 1)
+        self._off_gpu[o.home] -= 1
         self.index.relocate(o.did, self._loc(g))
         self.stats["reload_bytes"] += o.nbytes
         self.stats["bytes_h2d"] += o.nbytes
@@ -578,6 +585,10 @@ class FaaSTube:
             dst = self._loc(device)
             if src.node == dst.node and src.gpu is not None and src.gpu == dst.gpu:
                 plan = _INTRA_GPU        # dataplane.py:184-185: same GPU -> map only (no plan object)
+                if out is not None and obj.block is not None and not obj.retired:
+                    self._fetch_local(obj, out)          # copy into the consumer's input: one native call
+                    self.stats["fetches"] += 1
+                    return out
             else:
                 plan = self.plane.fetch_plan(src, dst, obj.nbytes)
             h2g = plan.method == "host_gpu" and not dst.on_host
@@ -617,6 +628,38 @@ class FaaSTube:
         with self._lock:
             self._tickets.append((ticket, obj.host, res))
         return res
+
+    def _fetch_local(self, obj: _Obj, out: torch.Tensor):
+        """Same-GPU fetch into the consumer's input (dataplane.py:184-185 +
+        engine.py:667-679), one native call: the consumer's stream waits for the
+        stored bytes, copies them, records ``done``; the last consumer also
+        drops the index entry and returns the block to the pool, fenced on
+        ``done`` (its read) and every earlier reader. A consumer that is not
+        the last one leaves ``done`` on the object for that retire."""
+        g = obj.gpu
+        blk = obj.block
+        obj.remaining -= 1
+        retire = obj.remaining <= 0 and obj.pins == 0
+        done = dev.Ev(g)
+        fences = tuple(obj.readers) + ((obj.ready,) if obj.ready is not None else ())
+        rw, last = self.pools[g].fetch_local(
+            self.index, obj.did, blk, obj.producer, retire, out.data_ptr(), obj.nbytes, dev.current_stream(g),
+            dev.L2_EVICT_FIRST if obj.remaining <= 0 else dev.L2_NORMAL, (obj.ready,), done, fences)
+        self.stats["bytes_local"] += obj.nbytes
+        if not retire:
+            self._hold_until(obj, done)
+            if obj.remaining <= 0:
+                self._retire(obj, done)                # pinned by a view: the view's release frees it
+            return
+        obj.retired = True
+        obj.readers = []
+        if self._objs.pop(obj.did, None) is not None:
+            self._account(obj, -1)                     # (block still set: its bytes leave the store)
+        obj.block = None
+        self.index._meta.pop(obj.did, None)
+        self._push_due(g, rw, last, self._last_op_ms)
+        if self.strategy.migration != "none" and self._off_gpu[g]:
+            self._pending.add(("prefetch", g))         # engine.py:678-679, 717-736
 
     def fetch_resident(self, data_id: int, device: int, consumer: str = "func"):
         """Zero-copy fetch if the object is stored in GPU ``device``'s pool right
@@ -660,12 +703,38 @@ class FaaSTube:
                 dev.wait_events(s, [o.ready for o, _ in group])
                 dev.copy_batch([(out.data_ptr(), o.block.ptr, o.nbytes) for o, out in group], g, s)
                 done = dev.Ev(g).record(s)     # one fence for every block the batch read
+                retiring = []
+                nb = 0
                 for o, _ in group:
-                    self.stats["bytes_local"] += o.nbytes
-                    self.stats["fetches"] += 1
-                    self._consumed(o, done)
-                    if not o.retired:
+                    nb += o.nbytes
+                    o.remaining -= 1
+                    if o.remaining <= 0 and o.pins == 0 and not o.retired:
+                        retiring.append(o)
+                    else:
                         self._hold_until(o, done)   # the last consumer's retire fences on this read
+                        if o.remaining <= 0:
+                            self._retire(o, done)
+                self.stats["bytes_local"] += nb
+                self.stats["fetches"] += len(group)
+                if retiring:
+                    # every last consumer's retire in one native call (dataplane.py:98-101,
+                    # datastore.py:146-149), fenced on the batch's read + earlier readers
+                    res = self.pools[g].retire_many(self.index, [
+                        (o.did, o.block, o.producer, (done,) + tuple(o.readers) + ((o.ready,) if o.ready else ()))
+                        for o in retiring])
+                    due = {}
+                    for o, (rw, last) in zip(retiring, res):
+                        o.retired = True
+                        o.readers = []
+                        if self._objs.pop(o.did, None) is not None:
+                            self._account(o, -1)
+                        o.block = None
+                        self.index._meta.pop(o.did, None)
+                        due[o.producer] = (rw, last)      # one shrink timer per producer
+                    for rw, last in due.values():
+                        self._push_due(g, rw, last, self._last_op_ms)
+                    if self.strategy.migration != "none" and self._off_gpu[g]:
+                        self._pending.add(("prefetch", g))
         for did, out in rest:
             self.fetch(did, out=out, consumer=consumer)
         if self._pending:
@@ -733,6 +802,9 @@ class FaaSTube:
 
     def _push_due(self, g, r_window, last, now):
         due = (last if last is not None else now) + r_window
+        if self._last_due == (due, g):
+            return                                    # the same deadline is queued already
+        self._last_due = (due, g)
         with self._maint_cv:
             wake = not self._shrink_due or due < self._shrink_due[0][0]
             heapq.heappush(self._shrink_due, (due, g))
@@ -798,6 +870,8 @@ class FaaSTube:
         obj.retired = True
         if self._objs.pop(obj.did, None) is not None:
             self._account(obj, -1)
+            if obj.home is not None and obj.block is None and obj.host is not None:
+                self._off_gpu[obj.home] -= 1          # a migrated object left the table
         blk = obj.block
         if blk is not None and obj.pins == 0:
             # drop the index entry, return the block (fenced on its last users) and re-arm
@@ -811,7 +885,7 @@ class FaaSTube:
             self.index._meta.pop(obj.did, None)
             rw, last = self.pools[blk.device].commit_retire(self.index, obj.did, blk, fences, obj.producer)
             self._push_due(blk.device, rw, last, self.now_ms())
-            if self.strategy.migration != "none":
+            if self.strategy.migration != "none" and self._off_gpu[blk.device]:
                 self._pending.add(("prefetch", blk.device))  # engine.py:678-679, 717-736
             return
         self.index.drop(obj.did)
@@ -826,7 +900,7 @@ class FaaSTube:
             obj.readers = []
             self.pools[blk.device].free(blk, fences)
             self._push_shrink(blk.device, obj.producer, self.now_ms())
-            if self.strategy.migration != "none":
+            if self.strategy.migration != "none" and self._off_gpu[blk.device]:
                 self._pending.add(("prefetch", blk.device))  # engine.py:678-679, 717-736
 
     def _unpin(self, obj):

@@ -259,3 +259,47 @@ def test_startup_calibration_matches_the_link(dev):
         best = min(best, a.elapsed_time(b))
     link = n / (best * 1e-3) / 1e9
     assert got > 0.9 * link, (got, link)
+
+
+@pytest.mark.parametrize("managed", [False, True])
+def test_k2_forward_aliased_streams_and_misaligned_dst(dev, managed):
+    """K2 (device flags between the CE legs and one forward kernel per batch):
+    the route's CE and forward streams may be the SAME stream (torch's stream
+    pool aliases), the destination may be misaligned, and a route longer than
+    the ring cycles every slot several times — still bit-exact."""
+    p = dev.Pacer(55.0, 5, 2 * MB, staging_slots=2, host_ring_bytes=8 * MB)
+    n = 40 * MB + 13
+    host = host_bytes(n, 7)
+    buf = torch.zeros(n + 16, dtype=torch.uint8, device="cuda:0")
+    dst = buf[3:3 + n]                                   # 3 bytes off the 16-byte grid
+    one = torch.cuda.Stream(0)
+    routes = [(0, 1, 0, n, one.cuda_stream, one.cuda_stream)]
+    s = torch.cuda.current_stream(0)
+    t = p.submit("", managed, 1e9, 0.0, 55.0, dst.data_ptr(), 0, host.data_ptr(), n, True, routes, s.cuda_stream)
+    torch.cuda.synchronize()
+    p.wait(t, 10000.0)
+    assert torch.equal(dst.cpu(), host)
+    assert int(buf[:3].sum()) == 0 and int(buf[3 + n:].sum()) == 0
+    assert p.stats()["failed"] == 0
+    p.close()
+
+
+def test_k2_matches_event_chain(dev, monkeypatch):
+    """The K2 forward and the previous per-piece event chain (FT_K2=0) deliver
+    the same bytes for the same staged stage."""
+    n = (24 << 20) + 4097
+    host = host_bytes(n, 11)
+    outs = []
+    for k2 in ("1", "0"):
+        monkeypatch.setenv("FT_K2", k2)
+        p = dev.Pacer(55.0, 5, 2 * MB, staging_slots=3, host_ring_bytes=8 * MB)
+        streams = [(torch.cuda.Stream(0), torch.cuda.Stream(0)) for _ in range(2)]
+        dst = torch.zeros(n, dtype=torch.uint8, device="cuda:0")
+        s = torch.cuda.current_stream(0)
+        t = p.submit("", True, 1e9, 0.0, 55.0, dst.data_ptr(), 0, host.data_ptr(), n, True,
+                     routes_for(n, "ss", streams), s.cuda_stream)
+        torch.cuda.synchronize()
+        p.wait(t, 10000.0)
+        outs.append(dst.cpu())
+        p.close()
+    assert torch.equal(outs[0], host) and torch.equal(outs[1], host)
