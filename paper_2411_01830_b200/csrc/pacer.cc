@@ -568,7 +568,16 @@ struct ft_pacer {
             auto k = krings.find(r.dev);
             if (k != krings.end() && *(volatile uint32_t*)k->second.err) {
               st.err = FT_E_TIMEOUT;
-              st.msg = "forward kernel: a staged chunk never landed (10 s)";
+              st.msg = "forward kernel: a staged chunk never landed (60 s)";
+              const KRing& K = k->second;
+              std::vector<uint32_t> w(2 * K.slots);
+              DevGuard g(r.dev);
+              if (cudaMemcpy(w.data(), K.landed, w.size() * 4, cudaMemcpyDeviceToHost) == cudaSuccess) {
+                st.msg += "; slot uses/landed/freed:";
+                for (int i = 0; i < K.slots; ++i)
+                  st.msg += " " + std::to_string(K.uses[i]) + "/" + std::to_string(w[i]) + "/" +
+                            std::to_string(w[K.slots + i]);
+              }
             }
           }
       for (auto& e : st.landing) put_event(e.second, e.first);
