@@ -692,20 +692,35 @@ def _daemon_client(path, g, q):
         for n in (4096, 1 << 20, 64 << 20):
             x = torch.randint(0, 256, (n,), dtype=torch.uint8, device=f"cuda:{g}")
             out = torch.empty_like(x)
-            st, ft = [], []
-            for i in range(30):
+            st, ft, vt, rt = [], [], [], []
+            for i in range(60):
                 did = c.unique_id()
                 t0 = time.perf_counter()
                 c.store(did, x)
                 t1 = time.perf_counter()
-                c.fetch(did, out=out)
+                c.fetch(did, out=out)                  # copy into the function's input buffer
                 t2 = time.perf_counter()
-                if i >= 5:
+                did = c.unique_id()
+                c.store(did, x)
+                t3 = time.perf_counter()
+                v = c.fetch(did)                       # zero-copy view of the stored block
+                t4 = time.perf_counter()
+                ok = bool(torch.equal(v, x)) if i in (0, 59) else True
+                t5 = time.perf_counter()
+                del v                                  # release (done + read event) to the daemon
+                t6 = time.perf_counter()
+                assert ok
+                if i >= 10:
                     st.append(t1 - t0)
                     ft.append(t2 - t1)
+                    vt.append(t4 - t3)
+                    rt.append(t6 - t5)
+            torch.cuda.synchronize()
             assert torch.equal(out, x)
             res[str(n)] = {"store_us_p50": round(1e6 * statistics.median(st), 1),
-                           "fetch_us_p50": round(1e6 * statistics.median(ft), 1)}
+                           "fetch_out_us_p50": round(1e6 * statistics.median(ft), 1),
+                           "fetch_view_us_p50": round(1e6 * statistics.median(vt), 1),
+                           "view_release_us_p50": round(1e6 * statistics.median(rt), 1)}
         c.close()
         q.put(("ok", res))
     except Exception as exc:  # noqa: BLE001
@@ -731,8 +746,9 @@ def run_daemon(tube, g):
         d.close()
     if status != "ok":
         return {"error": res}
-    return {"workload": "spawned function process: TubeClient.store then fetch(out=) through the daemon, "
-                        "GPU payloads as exported VMM pool blocks (same GPU)", "sizes": res}
+    return {"workload": "spawned function process through the daemon (same GPU, msgpack frames, IPC-event "
+                        "ordering, lent output blocks): store; fetch(out=) copy; fetch() zero-copy view + its "
+                        "release; host wall time per call", "sizes": res}
 
 
 def _ev(torch):

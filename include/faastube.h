@@ -318,6 +318,11 @@ int ft_vmm_pool_stats(const ft_vmm_pool* p, uint64_t* mapped_bytes, uint64_t* re
 int ft_vmm_import_fd(int device, int fd, uint64_t bytes, void** dptr, uint64_t* handle);
 int ft_vmm_unimport(uint64_t handle);
 /* SCM_RIGHTS fd passing over a connected AF_UNIX socket (PAPER.md:568 channel) */
+/* interprocess CUDA events (function <-> daemon ordering without host syncs):
+ * create one exportable event (64-byte handle out) / open a peer's handle; use
+ * them with ft_event_record / ft_stream_wait_events / ft_event_destroy */
+int ft_ipc_event_create(int device, void** ev, void* handle64);
+int ft_ipc_event_open(int device, const void* handle64, void** ev);
 int ft_fd_send(int sock, int fd, uint64_t tag);
 int ft_fd_recv(int sock, int* fd, uint64_t* tag);
 

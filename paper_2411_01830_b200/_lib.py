@@ -232,6 +232,8 @@ _SIGS = {
     "ft_vmm_pool_stats": (None, [vp, P(u64), P(u64), P(C.c_int)]),
     "ft_vmm_import_fd": (None, [C.c_int, C.c_int, u64, P(vp), P(u64)]),
     "ft_vmm_unimport": (None, [u64]),
+    "ft_ipc_event_create": (None, [C.c_int, P(vp), C.c_char_p]),
+    "ft_ipc_event_open": (None, [C.c_int, C.c_char_p, P(vp)]),
     "ft_fd_send": (None, [C.c_int, C.c_int, u64]),
     "ft_fd_recv": (None, [C.c_int, P(C.c_int), P(u64)]),
     "ft_copy": (None, [vp, vp, u64, C.c_int, vp]),

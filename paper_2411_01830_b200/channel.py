@@ -1,18 +1,21 @@
 """Function <-> daemon channel: AF_UNIX stream sockets carrying pool-block
-file descriptors (SCM_RIGHTS, ``ft_fd_send``/``ft_fd_recv``) plus a JSON
-descriptor. This is the paper's fast local channel (a Linux
+file descriptors (SCM_RIGHTS, ``ft_fd_send``/``ft_fd_recv``) plus binary
+(msgpack) messages, length-prefixed. This is the paper's fast local channel (a Linux
 pipe there) and the CUDA-IPC handoff of GPU buffers:
 bytes never cross the socket — the receiver maps the exported VMM block.
 """
 
 from __future__ import annotations
 
-import json
 import os
 import socket
 import struct
 
+import msgpack
+
 from . import device as dev
+
+_HDR = struct.Struct("<I")
 
 
 class Channel:
@@ -49,36 +52,35 @@ class Channel:
 
     def send_fd(self, fd: int, meta: dict):
         """One descriptor + its metadata (size, dtype, shape, data id ...)."""
-        body = json.dumps(meta).encode()
+        body = msgpack.packb(meta)
         dev.send_fd(self.sock, fd, len(body))
         self.sock.sendall(body)
 
     def recv_fd(self):
         fd, n = dev.recv_fd(self.sock)
-        body = b""
-        while len(body) < n:
-            chunk = self.sock.recv(n - len(body))
-            if not chunk:
-                raise ConnectionError("channel closed mid-message")
-            body += chunk
-        return fd, json.loads(body.decode())
+        return fd, msgpack.unpackb(self._recv_exact(n))
 
     def send_msg(self, meta: dict):
-        body = json.dumps(meta).encode()
-        self.sock.sendall(struct.pack("<Q", len(body)) + body)
+        body = msgpack.packb(meta)
+        self.sock.sendall(_HDR.pack(len(body)) + body)
 
     def recv_msg(self) -> dict:
-        hdr = self._recv_exact(8)
-        return json.loads(self._recv_exact(struct.unpack("<Q", hdr)[0]).decode())
+        n = _HDR.unpack(self._recv_exact(4))[0]
+        return msgpack.unpackb(self._recv_exact(n))
 
     def _recv_exact(self, n):
-        buf = b""
-        while len(buf) < n:
-            chunk = self.sock.recv(n - len(buf))
-            if not chunk:
+        buf = self.sock.recv(n)
+        if len(buf) == n:
+            return buf
+        parts = [buf]
+        got = len(buf)
+        while got < n:
+            if not buf:
                 raise ConnectionError("channel closed")
-            buf += chunk
-        return buf
+            buf = self.sock.recv(n - got)
+            parts.append(buf)
+            got += len(buf)
+        return b"".join(parts)
 
     def close(self):
         self.sock.close()

@@ -1057,6 +1057,39 @@ int ft_vmm_unimport(uint64_t handle) {
   return FT_OK;
 }
 
+// ---- interprocess events: cross-process stream ordering without host syncs
+int ft_ipc_event_create(int device, void** ev, void* handle64) {
+  int cur = 0;
+  CU_RT(cudaGetDevice(&cur));
+  if (cur != device) CU_RT(cudaSetDevice(device));
+  cudaEvent_t e = nullptr;
+  cudaError_t r = cudaEventCreateWithFlags(&e, cudaEventInterprocess | cudaEventDisableTiming);
+  cudaIpcEventHandle_t h;
+  if (r == cudaSuccess) r = cudaIpcGetEventHandle(&h, e);
+  if (cur != device) cudaSetDevice(cur);
+  if (r != cudaSuccess) {
+    if (e) cudaEventDestroy(e);
+    return cuda_fail(r, "ft_ipc_event_create");
+  }
+  static_assert(sizeof(h) == 64, "cudaIpcEventHandle_t is 64 bytes");
+  memcpy(handle64, &h, 64);
+  *ev = e;
+  return FT_OK;
+}
+int ft_ipc_event_open(int device, const void* handle64, void** ev) {
+  int cur = 0;
+  CU_RT(cudaGetDevice(&cur));
+  if (cur != device) CU_RT(cudaSetDevice(device));
+  cudaIpcEventHandle_t h;
+  memcpy(&h, handle64, 64);
+  cudaEvent_t e = nullptr;
+  cudaError_t r = cudaIpcOpenEventHandle(&e, h);
+  if (cur != device) cudaSetDevice(cur);
+  if (r != cudaSuccess) return cuda_fail(r, "ft_ipc_event_open");
+  *ev = e;
+  return FT_OK;
+}
+
 int ft_fd_send(int sock, int fd, uint64_t tag) {
   struct msghdr msg = {};
   char cbuf[CMSG_SPACE(sizeof(int))];

@@ -6,39 +6,56 @@ exported as POSIX fds (``cuMemExportToShareableHandle``, SCM_RIGHTS over
 AF_UNIX, ``channel.py``) and mapped by the function process; host payloads
 travel as a sealed memfd. The socket carries only small JSON messages.
 
-Protocol: every request gets one reply message; a reply with ``"fd": true``
-is followed by one descriptor (SCM_RIGHTS). Replies also carry ``"drop"``:
-block ids the daemon's pool has unmapped since, which the client unmaps too
-(its mappings would otherwise keep the physical memory alive).
+Protocol (msgpack frames): every request gets one reply message; a reply
+with ``"fd": true`` is followed by one descriptor (SCM_RIGHTS). Replies also
+carry ``"drop"``: block ids the daemon's pool has unmapped since, which the
+client unmaps too (its mappings would otherwise keep the physical memory
+alive), and ``"acked"``: how many of the client's messages were served.
+
+Ordering across processes is stream-ordered, not host-synchronised, once the
+client has said ``hello`` with its interprocess events: each side owns a ring
+of CUDA IPC events (``ft_ipc_event_create``) whose handles were exchanged at
+``hello``. A message may name one of the sender's events (``"ev"``): the
+receiver's stream waits on it before touching the block. So a store is: the
+client's stream waits the daemon's "block free" event, copies into the
+mapped block, records its event; ``commit`` makes the daemon's stream wait
+on it before publishing. A fetch reply names the daemon's "bytes ready"
+event; ``done`` names the client's "read finished" event, which fences the
+block's reuse. A connection without ``hello`` gets host synchronisation
+instead (the daemon syncs its stream before replying).
+
+  {"op": "hello", "gpu", "ev": [64-byte handles]}     -> {"ev": [handles]}
 
   {"op": "unique_id"}                                -> {"id"}
   {"op": "alloc", "gpu", "nbytes"}                   -> {"token", "block", "fd"} [+ fd]
       a pool block for the producer's output; the client writes it and commits
-  {"op": "commit", "token", "id", "dtype", "shape", "producer", "consumers", "response"}
-      -> {}   (tube.store of the pool-backed block: zero copy)
+  {"op": "commit", "token", "id", "dtype", "shape", "producer", "consumers", "response", "ev", "next"}
+      -> {} or {"loan": <alloc reply>} (tube.store of the pool-backed block: zero copy; "next":
+         the byte count of the producer's next output — its block is lent in the reply, so a
+         steady producer pays one round trip per store)
   {"op": "store_host", "id", "nbytes", ...} + memfd  -> {}
   {"op": "fetch", "id", "gpu", "consumer", "slo_ms", "infer_ms"}
       -> {"token", "block", "nbytes", "dtype", "shape", "fd"} [+ fd]: a block
          holding the bytes on the consumer's GPU (the stored block itself for a
          same-GPU object — zero copy — else a pool block the daemon fetched into)
   {"op": "fetch_host", "id", ...}                    -> {"nbytes", "dtype", "shape"} + memfd
-  {"op": "done", "token"}                            -> no reply (the client has read it)
+  {"op": "done", "token", "ev"}                      -> no reply (the client has read it)
   {"op": "release", "id"}                            -> {}
 
 A block's fd is exported and sent once per connection
 (``cuMemExportToShareableHandle`` costs ~1 ms): pool blocks are reused by
 size class, so a steady stream of requests maps and exports nothing new.
-Ordering across processes is by host synchronization: the client finishes
-writing before ``commit``; the daemon's fetch has landed before it replies.
 """
 
 from __future__ import annotations
 
+import contextlib
 import itertools
 import math
 import mmap
 import os
 import threading
+import weakref
 
 import torch
 
@@ -68,13 +85,43 @@ def _from_memfd(fd: int, nbytes: int) -> torch.Tensor:
 
 
 class _Conn:
-    __slots__ = ("ch", "tokens", "mapped", "drop")
+    __slots__ = ("ch", "tokens", "mapped", "drop", "gpu", "stream", "mine", "peer", "served")
 
     def __init__(self, ch):
         self.ch = ch
         self.tokens = set()      # loans of this connection (dropped if the client dies)
         self.mapped = set()      # (gpu, block id) the client has mapped
         self.drop = []           # block ids to unmap, sent with the next reply
+        self.gpu = None          # after hello: the client's GPU, a private stream, both event rings
+        self.stream = None
+        self.mine = None         # dev.IpcEventRing (the daemon's events, exported to the client)
+        self.peer = None         # dev.PeerEvents (the client's events)
+        self.served = 0          # messages handled (acknowledged in every reply)
+
+    def ctx(self):
+        """Request handling runs on the connection's private stream (after hello)."""
+        if self.stream is None:
+            return contextlib.nullcontext()
+        return torch.cuda.stream(self.stream)
+
+    def mark(self) -> int:
+        """Record one of the daemon's events on the connection stream (-1: no events)."""
+        if self.mine is None:
+            return -1
+        i = self.mine.take()
+        self.mine.record(i, self.stream)
+        return i
+
+    def wait_peer(self, i):
+        if self.peer is not None and i is not None and i >= 0:
+            self.peer.wait(int(i), self.stream)
+
+    def close(self):
+        for x in (self.mine, self.peer):
+            if x is not None:
+                x.close()
+        if self.stream is not None:
+            dev.destroy_stream(self.stream)
 
 
 class TubeDaemon:
@@ -126,16 +173,21 @@ class TubeDaemon:
     def _unhold(self, conn, tok):
         t = self._take(conn, tok)
         # a daemon-side fetch buffer, or an output block never committed (the client
-        # died between alloc and commit), goes back to the pool
+        # died between alloc and commit), goes back to the pool — fenced on the
+        # connection's stream, which waited for the client's last access
         keep = getattr(t, "_ft_keep", None) if not getattr(t, "_ft_alloc", False) else t
-        del t
+        del t                                  # a zero-copy view: its release fences the block
         if keep is not None:
-            self._free(keep)
+            self._free(keep, conn)
 
-    def _free(self, t):
+    def _free(self, t, conn=None):
+        """Back to the pool; with stream-ordered connections fenced on the connection's
+        stream (it waited for the client's last access), else the client synchronised."""
         blk = t._ft_block  # noqa: SLF001
         del t
-        self.tube.pools[blk.device].free(blk)
+        g = blk.device
+        fences = [dev.Ev(g).record(conn.stream)] if conn is not None and conn.stream is not None else []
+        self.tube.pools[g].free(blk, fences)
 
     def _serve(self, ch: Channel):
         conn = _Conn(ch)
@@ -145,24 +197,31 @@ class TubeDaemon:
             while True:
                 msg = ch.recv_msg()
                 try:
-                    self._handle(conn, msg)
+                    with conn.ctx():
+                        self._handle(conn, msg)
                 except Exception as exc:  # noqa: BLE001 - the error travels back to the caller
                     if msg.get("op") == "done":        # fire-and-forget: nobody waits for a reply
                         continue
-                    ch.send_msg({"ok": False, "error": type(exc).__name__, "msg": str(exc)})
+                    conn.served += 1
+                    ch.send_msg({"ok": False, "error": type(exc).__name__, "msg": str(exc), "acked": conn.served})
         except (ConnectionError, OSError):
             pass
         finally:
             with self._lock:
                 self._conns.remove(conn)
-            for tok in list(conn.tokens):      # a client that died drops its loans
-                self._unhold(conn, tok)
+            with conn.ctx():
+                for tok in list(conn.tokens):      # a client that died drops its loans
+                    self._unhold(conn, tok)
+            if conn.stream is not None:
+                conn.stream.synchronize()
+            conn.close()
             ch.close()
 
     def _reply(self, conn, meta, fd=None):
         with self._lock:
             drop, conn.drop = conn.drop, []
-        conn.ch.send_msg(dict(meta, ok=True, fd=fd is not None, drop=drop))
+        conn.served += 1
+        conn.ch.send_msg(dict(meta, ok=True, fd=fd is not None, drop=drop, acked=conn.served))
         if fd is not None:
             conn.ch.send_fd(fd, {})
 
@@ -181,20 +240,38 @@ class TubeDaemon:
         finally:
             os.close(fd)
 
+    def _lend(self, conn, g: int, n: int) -> dict:
+        """A pool block for a producer's output: its previous users are fenced on
+        the connection's stream, then marked (the client's stream waits on the
+        mark before writing; without events the stream is synchronised)."""
+        t = self.tube.empty((max(1, n),), torch.uint8, device=g)       # pool-backed output
+        t._ft_alloc = True  # noqa: SLF001
+        ev = conn.mark()
+        if ev < 0:
+            self.tube.sync_stream(g)           # the block's previous users are done before the client writes
+        return {"token": self._hold(conn, t), "nbytes": n, "ev": ev, "_blk": t._ft_block}  # noqa: SLF001
+
     def _handle(self, conn, msg: dict):
         tube, op, ch = self.tube, msg["op"], conn.ch
         if op == "unique_id":
             self._reply(conn, {"id": tube.unique_id()})
+        elif op == "hello":
+            g = int(msg["gpu"])
+            conn.gpu = g
+            conn.stream = dev.new_stream(g)
+            conn.peer = dev.PeerEvents(g, msg.get("ev", []))
+            conn.mine = dev.IpcEventRing(g)
+            self._reply(conn, {"ev": conn.mine.handles})
         elif op == "alloc":
             g, n = int(msg["gpu"]), int(msg["nbytes"])
-            t = tube.empty((max(1, n),), torch.uint8, device=g)              # pool-backed output
-            t._ft_alloc = True  # noqa: SLF001
-            tube.sync_stream(g)                # the block's previous users are done before the client writes
-            self._reply_block(conn, g, t._ft_block, {"token": self._hold(conn, t), "nbytes": n})  # noqa: SLF001
+            with conn.ctx():
+                meta = self._lend(conn, g, n)
+            self._reply_block(conn, g, meta.pop("_blk"), meta)
         elif op == "commit":
             t = self._take(conn, int(msg["token"]))
             if t is None:
                 raise KeyError(f"unknown token {msg['token']}")
+            conn.wait_peer(msg.get("ev"))      # the client's copy into the block is done (stream-ordered)
             blk = t._ft_block  # noqa: SLF001
             dt = _DTYPES[msg["dtype"]]
             out = t[:math.prod(msg["shape"]) * dt.itemsize].view(dt).view(msg["shape"])
@@ -204,9 +281,15 @@ class TubeDaemon:
                            producer=msg.get("producer", "func"), consumers=int(msg.get("consumers", 1)))
             except BaseException:
                 del out
-                self._free(t)                  # not published (e.g. DuplicateStore): back to the pool
+                self._free(t, conn)            # not published (e.g. DuplicateStore): back to the pool
                 raise
-            self._reply(conn, {})
+            nxt = msg.get("next")
+            if nxt is not None and conn.gpu is not None:
+                # lend the block of the producer's next output now: its next store is one round trip
+                meta = self._lend(conn, conn.gpu, int(nxt))
+                self._reply_block(conn, conn.gpu, meta.pop("_blk"), dict(meta, loan=True))
+            else:
+                self._reply(conn, {})
         elif op == "store_host":
             fd, _ = ch.recv_fd()
             try:
@@ -240,9 +323,12 @@ class TubeDaemon:
                 t._ft_keep = dst  # noqa: SLF001
                 blk = dst._ft_block  # noqa: SLF001
             # the consumer stream is ordered after the bytes (a host->GPU stage's last
-            # batch is issued before fetch returns; the stream waits on its join events)
-            tube.sync_stream(g)
-            self._reply_block(conn, g, blk, {"token": self._hold(conn, t), "nbytes": t.nbytes,
+            # batch is issued before fetch returns; the stream waits on its join events):
+            # the client's stream waits on a mark of it, or the stream is synchronised
+            ev = conn.mark()
+            if ev < 0:
+                tube.sync_stream(g)
+            self._reply_block(conn, g, blk, {"token": self._hold(conn, t), "nbytes": t.nbytes, "ev": ev,
                                              "dtype": str(t.dtype), "shape": list(t.shape)})
         elif op == "fetch_host":
             t = tube.fetch(int(msg["id"]), device=None, consumer=msg.get("consumer", "func"))
@@ -252,6 +338,8 @@ class TubeDaemon:
             finally:
                 os.close(fd)
         elif op == "done":                     # no reply (the client does not wait for it)
+            conn.wait_peer(msg.get("ev"))      # the client's last read of the block (stream-ordered)
+            conn.served += 1
             self._unhold(conn, int(msg["token"]))
         elif op == "release":
             tube.release(int(msg["id"]))
@@ -287,22 +375,59 @@ class DaemonError(RuntimeError):
     pass
 
 
+class _Release:
+    """Owner of a zero-copy view's mapping: when the last tensor over it dies,
+    the client tells the daemon (``done``) so the loan's block can be reused."""
+
+    __slots__ = ("__weakref__",)
+
+
 class TubeClient:
     """Listing 1 in a function process: ``unique_id`` / ``store`` / ``fetch``
-    through the daemon at ``path``, for a function running on ``device``."""
+    through the daemon at ``path``, for a function running on ``device``.
 
-    def __init__(self, path: str, device: int = 0):
+    With ``events`` (default) the client and the daemon order each other's
+    GPU work with interprocess events instead of host synchronisation (see the
+    module doc): ``store`` returns once the copy into the lent block is
+    enqueued and committed; ``fetch()`` without ``out`` returns a zero-copy
+    view of the stored block itself (same GPU), released back to the daemon
+    when the last tensor over it dies; ``fetch(out=)`` copies on the caller's
+    current stream. Consumer kernels issued afterwards on the caller's current
+    stream see the bytes."""
+
+    def __init__(self, path: str, device: int = 0, events: bool = True):
         self.ch = Channel.connect(path)
         self.device = device
         self._imports = {}           # daemon block id -> ImportedBlock (until the daemon drops it)
-        self._stream = dev.new_stream(device)
+        self._loans = {}             # nbytes -> a lent block for the producer's next output
+        self._io = threading.RLock()  # one frame at a time on the socket (releases come from finalizers)
+        self._sent = 0               # messages sent
+        self._acked = 0              # messages the daemon has served (from its replies)
+        self._mine = self._peer = None
+        self._closed = False
+        self._views = 0              # zero-copy views handed out and not yet released
+        if events:
+            self._mine = dev.IpcEventRing(device)
+            self._used = [0] * self._mine.k        # message number that carried each event's last record
+            rep = self._call({"op": "hello", "gpu": device, "ev": self._mine.handles})
+            self._peer = dev.PeerEvents(device, rep["ev"])
+        else:
+            self._stream = dev.new_stream(device)
+
+    # ---- framing
+    def _send(self, msg: dict):
+        with self._io:
+            self.ch.send_msg(msg)
+            self._sent += 1
 
     def _call(self, msg: dict):
-        self.ch.send_msg(msg)
-        return self._recv()
+        with self._io:
+            self._send(msg)
+            return self._recv()
 
     def _recv(self):
         rep = self.ch.recv_msg()
+        self._acked = max(self._acked, rep.get("acked", 0))
         if not rep.get("ok"):
             raise DaemonError(f"{rep.get('error')}: {rep.get('msg')}")
         for bid in rep.get("drop", ()):
@@ -314,7 +439,7 @@ class TubeClient:
         return rep
 
     def _mapped(self, rep: dict) -> dev.ImportedBlock:
-        bid, fd = rep["block"], rep.get("_fd")
+        bid, fd = rep["block"], rep.pop("_fd", None)
         if fd is None:
             return self._imports[bid]
         try:
@@ -325,6 +450,29 @@ class TubeClient:
         finally:
             os.close(fd)
 
+    # ---- stream ordering
+    def _mark(self, stream) -> int:
+        """Record one of our events on ``stream`` for the next message (-1: the
+        daemon may still have a wait on that event's previous record to enqueue —
+        synchronise ``stream`` instead)."""
+        if self._mine is None:
+            stream.synchronize()
+            return -1
+        with self._io:
+            i = self._mine.take()
+            if self._used[i] > self._acked:
+                stream.synchronize()
+                return -1
+            self._mine.record(i, stream)
+            self._used[i] = self._sent + 1
+            return i
+
+    def _after_daemon(self, rep: dict, stream):
+        """``stream`` waits for the daemon's mark in ``rep`` (host-synced connections: nothing)."""
+        ev = rep.get("ev", -1)
+        if self._peer is not None and ev is not None and ev >= 0:
+            self._peer.wait(int(ev), stream)
+
     def unique_id(self) -> int:
         return self._call({"op": "unique_id"})["id"]
 
@@ -334,28 +482,45 @@ class TubeClient:
         if not output.is_cuda:
             fd = _memfd(output)
             try:
-                self.ch.send_msg({"op": "store_host", "id": data_id, "nbytes": output.nbytes,
-                                  "dtype": str(output.dtype), "shape": list(output.shape), "producer": producer,
-                                  "consumers": consumers})
-                self.ch.send_fd(fd, {})
+                with self._io:
+                    self._send({"op": "store_host", "id": data_id, "nbytes": output.nbytes,
+                                "dtype": str(output.dtype), "shape": list(output.shape), "producer": producer,
+                                "consumers": consumers})
+                    self.ch.send_fd(fd, {})
+                    self._recv()
             finally:
                 os.close(fd)
-            self._recv()
             return
         t = output.contiguous()
-        rep = self._call({"op": "alloc", "gpu": self.device, "nbytes": t.nbytes})
-        imp = self._mapped(rep)
-        self._stream.wait_stream(torch.cuda.current_stream(self.device))
-        dev.copy(imp.ptr, t.data_ptr(), t.nbytes, self.device, self._stream)
-        self._stream.synchronize()                     # written before the daemon publishes it
-        self._call({"op": "commit", "token": rep["token"], "id": data_id, "dtype": str(t.dtype),
-                    "shape": list(t.shape), "producer": producer, "consumers": consumers, "response": response})
+        n = t.nbytes
+        rep = self._loans.pop(n, None)
+        if rep is None:
+            rep = self._call({"op": "alloc", "gpu": self.device, "nbytes": n})
+            imp = self._mapped(rep)
+        else:
+            imp = self._imports[rep["block"]]
+        if self._mine is None:
+            cur = self._stream
+            cur.wait_stream(torch.cuda.current_stream(self.device))
+        else:
+            cur = torch.cuda.current_stream(self.device)
+        self._after_daemon(rep, cur)                  # the block's previous users are done
+        dev.copy(imp.ptr, t.data_ptr(), n, self.device, cur)
+        ev = self._mark(cur)                          # written (or synchronised) before the daemon publishes it
+        if t is not output or self._mine is None:
+            t.record_stream(cur)
+        rep = self._call({"op": "commit", "token": rep["token"], "id": data_id, "dtype": str(t.dtype),
+                          "shape": list(t.shape), "producer": producer, "consumers": consumers,
+                          "response": response, "ev": ev, **({"next": n} if self._mine is not None else {})})
+        if rep.get("loan"):
+            self._mapped(rep)
+            self._loans[n] = rep
 
     def fetch(self, data_id: int, out: torch.Tensor | None = None, host: bool = False, consumer: str = "func",
               slo_ms: float | None = None, infer_ms: float | None = None) -> torch.Tensor:
-        """FaaSTube.fetch(index, input): the bytes land in ``out`` (or a new
-        tensor on this function's GPU; in host memory with ``host=True`` or a
-        host ``out``)."""
+        """FaaSTube.fetch(index, input): the bytes land in ``out`` (or, without
+        ``out``, a zero-copy view of the block on this function's GPU; in host
+        memory with ``host=True`` or a host ``out``)."""
         if host or (out is not None and not out.is_cuda):
             rep = self._call({"op": "fetch_host", "id": data_id, "consumer": consumer})
             try:
@@ -370,25 +535,61 @@ class TubeClient:
         rep = self._call({"op": "fetch", "id": data_id, "gpu": self.device, "consumer": consumer,
                           "slo_ms": slo_ms, "infer_ms": infer_ms})
         imp = self._mapped(rep)
-        if out is None:
-            out = torch.empty(rep["shape"], dtype=_DTYPES[rep["dtype"]], device=f"cuda:{self.device}")
-        elif not out.is_contiguous() or out.nbytes != rep["nbytes"]:
-            self.ch.send_msg({"op": "done", "token": rep["token"]})
+        dt, shape, n = _DTYPES[rep["dtype"]], rep["shape"], rep["nbytes"]
+        if out is not None and (not out.is_contiguous() or out.nbytes != n):
+            self._send({"op": "done", "token": rep["token"], "ev": -1})
             raise ValueError("out must be contiguous with exactly the stored byte count")
+        if self._mine is not None:
+            cur = torch.cuda.current_stream(self.device)
+            self._after_daemon(rep, cur)               # the bytes are in place
+            if out is None:
+                # zero copy: a view of the stored block itself, released to the daemon
+                # (with a mark of the releasing thread's stream) when the last tensor
+                # over it dies
+                owner = _Release()
+                self._views += 1
+                weakref.finalize(owner, self._release, rep["token"])
+                return dev.as_tensor(imp.ptr, n, self.device, dt, tuple(shape), owner=owner)
+            dev.copy(out.data_ptr(), imp.ptr, n, self.device, cur)
+            self._send({"op": "done", "token": rep["token"], "ev": self._mark(cur)})
+            return out
+        # host-synced connection: copy on the private stream, synchronise, release
+        if out is None:
+            out = torch.empty(shape, dtype=dt, device=f"cuda:{self.device}")
         cur = torch.cuda.current_stream(self.device)
         self._stream.wait_stream(cur)
-        dev.copy(out.data_ptr(), imp.ptr, rep["nbytes"], self.device, self._stream)
+        dev.copy(out.data_ptr(), imp.ptr, n, self.device, self._stream)
         self._stream.synchronize()                     # read before the daemon may reuse the block
-        self.ch.send_msg({"op": "done", "token": rep["token"]})   # no reply: served before the next request
+        self._send({"op": "done", "token": rep["token"]})
         cur.wait_stream(self._stream)
         return out
+
+    def _release(self, token):
+        self._views -= 1
+        if self._closed:
+            return
+        try:
+            cur = torch.cuda.current_stream(self.device)
+            self._send({"op": "done", "token": token, "ev": self._mark(cur)})
+        except Exception:  # noqa: BLE001 - the daemon drops a dead connection's loans itself
+            pass
 
     def release(self, data_id: int):
         self._call({"op": "release", "id": data_id})
 
     def close(self):
-        for imp in self._imports.values():
-            imp.close()
+        import gc
+        gc.collect()                                   # views dropped by the caller send their done now
+        self._closed = True
+        if not self._views:                            # a live view keeps its mapping (until exit)
+            for imp in self._imports.values():
+                imp.close()
         self._imports.clear()
-        dev.destroy_stream(self._stream)
+        self._loans.clear()
+        if self._mine is None:
+            dev.destroy_stream(self._stream)
+        else:
+            torch.cuda.synchronize(self.device)
+            self._peer.close()
+            self._mine.close()
         self.ch.close()

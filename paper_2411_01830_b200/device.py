@@ -627,6 +627,54 @@ class ImportedBlock:
         self._fin()
 
 
+class IpcEventRing:
+    """``k`` interprocess CUDA events of this process on ``device``, handed out
+    round-robin; ``handles`` (64 bytes each) let a peer process open them."""
+
+    def __init__(self, device: int, k: int = 16):
+        self.device, self.k = device, k
+        self.h, self.handles = [], []
+        for _ in range(k):
+            ev, buf = C.c_void_p(), C.create_string_buffer(64)
+            LIB.ft_ipc_event_create(int(device), C.byref(ev), buf)
+            self.h.append(ev.value)
+            self.handles.append(buf.raw)
+        self._next = 0
+
+    def take(self) -> int:
+        i = self._next
+        self._next = (i + 1) % self.k
+        return i
+
+    def record(self, i: int, stream):
+        LIB.ft_event_record(C.c_void_p(self.h[i]), C.c_void_p(stream_ptr(stream)))
+
+    def close(self):
+        for h in self.h:
+            LIB.raw("ft_event_destroy")(C.c_void_p(h))
+        self.h = []
+
+
+class PeerEvents:
+    """A peer process's interprocess events, opened from their handles."""
+
+    def __init__(self, device: int, handles):
+        self.h = []
+        for hd in handles:
+            ev = C.c_void_p()
+            LIB.ft_ipc_event_open(int(device), bytes(hd), C.byref(ev))
+            self.h.append(ev.value)
+
+    def wait(self, i: int, stream):
+        """``stream`` waits for the peer's latest record of its event ``i``."""
+        LIB.ft_stream_wait_events(C.c_void_p(stream_ptr(stream)), (C.c_void_p * 1)(self.h[i]), 1)
+
+    def close(self):
+        for h in self.h:
+            LIB.raw("ft_event_destroy")(C.c_void_p(h))
+        self.h = []
+
+
 def send_fd(sock, fd: int, tag: int = 0):
     LIB.ft_fd_send(sock.fileno(), int(fd), int(tag))
 

@@ -26,7 +26,7 @@ class _Pool:
         self.exports += 1
         return os.open("/dev/null", os.O_RDONLY)
 
-    def free(self, blk):
+    def free(self, blk, fences=()):
         self.freed.append(blk.vmm_id)
 
     def unmap(self, vid):
