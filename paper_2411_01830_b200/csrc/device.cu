@@ -647,6 +647,32 @@ int copy_impl(void* dst_, const void* src_, uint64_t bytes, int device, cudaStre
   return e == cudaSuccess ? FT_OK : cuda_fail(e, "ft_copy");
 }
 
+// event pool for the one-shot striped copy (ft_h2g_striped)
+std::mutex g_evp_mu;
+std::map<int, std::vector<cudaEvent_t>> g_evp;
+std::vector<cudaEvent_t> take_events(int device, int n) {
+  std::vector<cudaEvent_t> out;
+  {
+    std::lock_guard<std::mutex> lk(g_evp_mu);
+    auto& v = g_evp[device];
+    while ((int)out.size() < n && !v.empty()) {
+      out.push_back(v.back());
+      v.pop_back();
+    }
+  }
+  while ((int)out.size() < n) {  // current device is `device` (the caller set it)
+    cudaEvent_t e = nullptr;
+    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) break;
+    out.push_back(e);
+  }
+  return out;
+}
+void put_events(int device, const std::vector<cudaEvent_t>& evs) {
+  std::lock_guard<std::mutex> lk(g_evp_mu);
+  auto& v = g_evp[device];
+  v.insert(v.end(), evs.begin(), evs.end());
+}
+
 // ------------------------------------------------------------ VMM pool
 struct Block {
   CUmemGenericAllocationHandle h;
@@ -1390,10 +1416,16 @@ int ft_h2g_striped(void* dst_, int dst_dev, const void* host_, uint64_t bytes, i
       break;
     }
     cudaSetDevice(sd);
-    std::vector<cudaEvent_t> landed(ring), freed(ring);
-    for (int i = 0; i < ring; ++i) {
-      cudaEventCreateWithFlags(&landed[i], cudaEventDisableTiming);
-      cudaEventCreateWithFlags(&freed[i], cudaEventDisableTiming);
+    // ring events from a per-device pool (re-recording an event is safe once every
+    // wait on its previous record is enqueued, i.e. after this call): no create /
+    // destroy per call
+    std::vector<cudaEvent_t> landed = take_events(sd, ring), freed = take_events(sd, ring);
+    if ((int)landed.size() < ring || (int)freed.size() < ring) {
+      put_events(sd, landed);
+      put_events(sd, freed);
+      ft::set_last_error("ft_h2g_striped: cudaEventCreate failed");
+      rc = FT_E_CUDA;
+      break;
     }
     uint8_t* stg = static_cast<uint8_t*>(staging[r]);
     uint64_t nch = (len[r] + chunk - 1) / chunk;
@@ -1411,10 +1443,8 @@ int ft_h2g_striped(void* dst_, int dst_dev, const void* host_, uint64_t bytes, i
       rc = copy_impl(dst + off[r] + o, stg + (uint64_t)slot * chunk, n, sd, fw, 2, 0);  // push over NVLink
       cudaEventRecord(freed[slot], fw);
     }
-    for (int i = 0; i < ring; ++i) {
-      cudaEventDestroy(landed[i]);  // destruction is deferred until the event completes
-      cudaEventDestroy(freed[i]);
-    }
+    put_events(sd, landed);
+    put_events(sd, freed);
   }
   cudaSetDevice(cur);
   return rc;

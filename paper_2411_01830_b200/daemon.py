@@ -84,6 +84,22 @@ def _from_memfd(fd: int, nbytes: int) -> torch.Tensor:
     return t
 
 
+class _Pin:
+    """A daemon-side loan of a stored block to a client's zero-copy read: looks
+    like the tensor it stands for (nbytes / dtype / shape) and unpins the block
+    when the daemon drops it (client ``done`` or a dead connection)."""
+
+    __slots__ = ("release", "nbytes", "dtype", "shape")
+
+    def __init__(self, release, nbytes, dtype, shape):
+        self.release, self.nbytes, self.dtype, self.shape = release, nbytes, dtype, shape
+
+    def __del__(self):
+        rel, self.release = self.release, None
+        if rel is not None:
+            rel()
+
+
 class _Conn:
     __slots__ = ("ch", "tokens", "mapped", "drop", "gpu", "stream", "mine", "peer", "served")
 
@@ -308,7 +324,8 @@ class TubeDaemon:
             # fetch); the view pins the block, so it cannot move after
             res = tube.fetch_resident(did, g, consumer=msg.get("consumer", "func"))
             if res is not None:
-                t, blk = res
+                blk, nbytes, dtype, shape, release = res
+                t = _Pin(release, nbytes, dtype, shape)   # the loan: unpins the block when dropped
             else:
                 obj = tube._objs.get(did)  # noqa: SLF001
                 nbytes = obj.nbytes if obj is not None else 0

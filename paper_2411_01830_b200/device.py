@@ -158,10 +158,12 @@ class Ev:
 
 
 def copy_batch(segments, device: int, stream=None):
-    """[(dst_ptr, src_ptr, nbytes)] in one launch per 64 segments (ft_copy_batch)."""
+    """[(dst_ptr, src_ptr, nbytes)] in one launch per 64 segments (ft_copy_batch).
+    The segment array is built as one flat u64 array (ft_segment = 3 x 8 bytes)."""
     from ._lib import SegmentC
-    arr = (SegmentC * len(segments))(*[SegmentC(d, x, int(n)) for d, x, n in segments])
-    LIB.ft_copy_batch(arr, len(segments), int(device), C.c_void_p(stream_ptr(stream)))
+    flat = [v for seg in segments for v in seg]
+    arr = (C.c_uint64 * len(flat))(*flat)
+    LIB.ft_copy_batch(C.cast(arr, C.POINTER(SegmentC)), len(segments), int(device), C.c_void_p(stream_ptr(stream)))
 
 
 def wait_events(stream, events):

@@ -662,19 +662,29 @@ class FaaSTube:
             self._pending.add(("prefetch", g))         # engine.py:678-679, 717-736
 
     def fetch_resident(self, data_id: int, device: int, consumer: str = "func"):
-        """Zero-copy fetch if the object is stored in GPU ``device``'s pool right
-        now: (view, pool block) — decided and fetched under the tube lock, so a
-        concurrent migration cannot move it in between (the view pins the block).
-        None if it lives elsewhere (the caller fetches into a buffer instead)."""
+        """Zero-copy fetch for another process (the daemon's same-GPU path), if the
+        object is stored in GPU ``device``'s pool right now: the caller's stream
+        is ordered after the stored bytes, the block is pinned, and this counts
+        as the consumer's fetch (dataplane.py:184-185). Decided under the tube
+        lock, so a concurrent migration cannot move it in between. Returns
+        (pool block, nbytes, dtype, shape, release) — ``release()`` unpins the
+        block once the reader is done (the caller's current stream must be
+        ordered after the read by then). None if it lives elsewhere."""
         with self._lock:
             obj = self._objs.get(data_id)
             if obj is None or obj.gpu != device or obj.block is None:
                 return None
-            view = self._fetch(data_id, device=device, consumer=consumer)
-            blk = obj.block
+            self._reap()
+            self._last_op_ms = self.now_ms()
+            obj.ready.wait(self._stream(device))
+            obj.pins += 1
+            self.stats["zero_copy"] += 1
+            self.stats["fetches"] += 1
+            self._consumed(obj)
+            res = (obj.block, obj.nbytes, obj.dtype, obj.shape, lambda: self._unpin(obj))
         if self._pending:
             self._drain_pending()          # prefetch made possible by this consumer's retire
-        return view, blk
+        return res
 
     def fetch_many(self, items, consumer: str = "func") -> list:
         """Batched fetch (an extension of Listing 1): ``[(data_id, out)]`` into
@@ -684,20 +694,19 @@ class FaaSTube:
         launch once; anything else goes through ``fetch``."""
         if not items:
             return []
-        batch, rest = [], []
+        rest = []
         with self._lock:
             self._reap()
             self._last_op_ms = self.now_ms()
+            objs = self._objs
+            by_gpu = {}
             for did, out in items:
-                obj = self._objs.get(did)
-                if (obj is not None and obj.block is not None and out.is_cuda and obj.gpu == out.device.index
-                        and out.is_contiguous() and out.nbytes == obj.nbytes):
-                    batch.append((obj, out))
+                obj = objs.get(did)
+                if (obj is not None and obj.block is not None and obj.gpu == out.get_device()
+                        and out.nbytes == obj.nbytes and out.is_contiguous()):
+                    by_gpu.setdefault(obj.gpu, []).append((obj, out))
                 else:
                     rest.append((did, out))
-            by_gpu = {}
-            for obj, out in batch:
-                by_gpu.setdefault(obj.gpu, []).append((obj, out))
             for g, group in by_gpu.items():
                 s = self._stream(g)
                 dev.wait_events(s, [o.ready for o, _ in group])

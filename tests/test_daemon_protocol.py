@@ -79,7 +79,8 @@ class _Tube:
         o = self._objs.get(did)
         if o is None or o.gpu != device or o.block is None:
             return None
-        return self.fetch(did, device, consumer=consumer), o.block
+        t = self.fetch(did, device, consumer=consumer)
+        return o.block, t.nbytes, t.dtype, tuple(t.shape), lambda: None
 
     def release(self, did):
         self._objs.pop(did, None)

@@ -63,4 +63,17 @@ pr.enable()
 loop(2000)
 pr.disable()
 pstats.Stats(pr).sort_stats("tottime").print_stats(25)
+pr = cProfile.Profile()
+for r in range(10):
+    ids = []
+    for j in range(64):
+        d = tube.unique_id()
+        tube.store(d, xs[j])
+        ids.append(d)
+    torch.cuda.synchronize()
+    pr.enable()
+    tube.fetch_many([(d, ys[j]) for j, d in enumerate(ids)])
+    pr.disable()
+print("---- fetch_many profile")
+pstats.Stats(pr).sort_stats("tottime").print_stats(20)
 tube.close()
