@@ -776,7 +776,9 @@ int mem_write32(cudaStream_t st, uint32_t* addr, uint32_t value) {
     set_last_error("CUDA driver stream memory operations unavailable");
     return FT_E_NOT_SUPPORTED;
   }
-  CU_DRV(d->write32((CUstream)st, (CUdeviceptr)addr, value, CU_STREAM_WRITE_VALUE_DEFAULT));
+  static const unsigned flags =
+      std::getenv("FT_K2_NOBAR") ? CU_STREAM_WRITE_VALUE_NO_MEMORY_BARRIER : CU_STREAM_WRITE_VALUE_DEFAULT;
+  CU_DRV(d->write32((CUstream)st, (CUdeviceptr)addr, value, flags));
   return FT_OK;
 }
 int mem_wait_geq32(cudaStream_t st, uint32_t* addr, uint32_t value) {

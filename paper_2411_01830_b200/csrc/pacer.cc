@@ -241,7 +241,12 @@ struct ft_pacer {
   std::map<int, StagingRing> rings;  // GPU->host staged routes
   std::map<int, KRing> krings;       // host->GPU staged routes (K2)
   std::map<cudaStream_t, cudaStream_t> ce2;  // second CE stream of each route CE stream
-  bool k2 = true;                    // FT_K2=0: the per-piece event chain (previous design)
+  // K2 (one forward kernel per batch on device flags) or the per-piece event chain:
+  // measured on one link, 1 GiB staged, the chain is 1-4 % faster at every piece
+  // size (a stream memory op costs the CE more than an event record/wait:
+  // profiles/r02/sweep_k2.txt), so it is the default; FT_K2=1 selects K2
+  bool k2 = false;
+  bool ce_alt = true;                // K2: alternate two CE streams per route (FT_K2_CE2=0: one)
   std::map<std::string, double> guarded;  // last early boundary per stage key (A2 guard)
   uint64_t n_stages = 0, n_managed = 0, n_batches = 0, n_bytes = 0, n_errors = 0;
   std::vector<std::string> trace, log;
@@ -357,11 +362,11 @@ struct ft_pacer {
     if (it != krings.end()) return it->second;
     KRing K;
     DevGuard g(dev);
-    // same memory as the event-chained ring: staging_slots x stage_chunk, cut into
-    // chunk-sized slots (pcie_sched.py:14's 2 MB)
-    K.slot_bytes = (chunk + 255) / 256 * 256;
-    K.slots = (int)std::max<uint64_t>(2, (uint64_t)staging_slots * stage_chunk / K.slot_bytes);
-    K.slots = std::min(K.slots, ft::kFwdMaxChunks);
+    // staging_slots slots of one staging piece each (stage_chunk: up to 4 chunks of
+    // pcie_sched.py:14's 2 MB): a copy-engine op carries one piece — the CE loses
+    // ~10 % of the link to per-op cost at 2 MB ops (profiles/r02/sweep_k2.txt)
+    K.slot_bytes = (stage_chunk + 255) / 256 * 256;
+    K.slots = std::clamp(staging_slots, 2, ft::kFwdMaxChunks);
     void* p = nullptr;
     ck(cudaMalloc(&p, (size_t)K.slots * K.slot_bytes), "K2 ring cudaMalloc");
     K.buf = static_cast<uint8_t*>(p);
@@ -396,11 +401,15 @@ struct ft_pacer {
         throw CudaFail{std::string("forward: ") + ft_last_error()};
       b.n = 0;
     };
-    for (uint64_t o = 0; o < n; o += K.slot_bytes) {
-      const uint64_t c = std::min<uint64_t>(K.slot_bytes, n - o);
+    // pieces: 1/32 of the route, between one chunk and a full slot (a long route
+    // moves in big CE ops, a short one keeps its pipeline fill short)
+    const uint64_t step = fixed_stage_chunk ? K.slot_bytes
+                                            : std::clamp<uint64_t>(r.len / 32 / 65536 * 65536, chunk, K.slot_bytes);
+    for (uint64_t o = 0; o < n; o += step) {
+      const uint64_t c = std::min<uint64_t>(step, n - o);
       const int s = K.next;
       K.next = (s + 1) % K.slots;
-      cudaStream_t cs = (K.alt++ & 1) ? c2 : r.ce;
+      cudaStream_t cs = (ce_alt && (K.alt++ & 1)) ? c2 : r.ce;
       // the slot's previous chunk has been read by every CTA of its forward launch
       // (that launch was enqueued before: a launch holds at most one chunk per slot)
       if (K.uses[s] && ft::mem_wait_geq32(cs, K.freed + s, K.uses[s] * (uint32_t)ft::kFwdCtas) != FT_OK)
@@ -921,6 +930,7 @@ int ft_pacer_create(double bw_all_gbps, int links, int batch_chunks, int64_t chu
   p->staging_slots = std::max(2, staging_slots);
   p->stage_chunk = 4 * (uint64_t)chunk_bytes;
   if (const char* c = std::getenv("FT_K2")) p->k2 = std::atoi(c) != 0;
+  if (const char* c = std::getenv("FT_K2_CE2")) p->ce_alt = std::atoi(c) != 0;
   if (const char* c = std::getenv("FT_STAGE_CHUNK")) {
     p->stage_chunk = std::max<uint64_t>(1 << 16, std::atoll(c));
     p->fixed_stage_chunk = true;

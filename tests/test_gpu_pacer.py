@@ -65,9 +65,12 @@ def test_stage_bit_exact(dev, managed, pinned, n, kinds):
     p.close()
 
 
-def test_concurrent_stages_share_staging_ring(dev):
+@pytest.mark.parametrize("k2", ["0", "1"])
+def test_concurrent_stages_share_staging_ring(dev, k2, monkeypatch):
     """Several tenants' staged routes through one staging GPU ring, each on its
-    own stream pair: slots are reused only after their forward drained them."""
+    own stream pair: slots are reused only after their forward drained them
+    (event chain and K2)."""
+    monkeypatch.setenv("FT_K2", k2)
     p = dev.Pacer(55.0, 5, 2 * MB, staging_slots=2, host_ring_bytes=8 * MB)
     n = 24 * MB + 333
     payload = [host_bytes(n, 100 + i, pinned=i % 2 == 0) for i in range(6)]
@@ -261,12 +264,14 @@ def test_startup_calibration_matches_the_link(dev):
     assert got > 0.9 * link, (got, link)
 
 
+@pytest.mark.parametrize("k2", ["1", "0"])
 @pytest.mark.parametrize("managed", [False, True])
-def test_k2_forward_aliased_streams_and_misaligned_dst(dev, managed):
+def test_k2_forward_aliased_streams_and_misaligned_dst(dev, managed, k2, monkeypatch):
     """K2 (device flags between the CE legs and one forward kernel per batch):
     the route's CE and forward streams may be the SAME stream (torch's stream
     pool aliases), the destination may be misaligned, and a route longer than
     the ring cycles every slot several times — still bit-exact."""
+    monkeypatch.setenv("FT_K2", k2)
     p = dev.Pacer(55.0, 5, 2 * MB, staging_slots=2, host_ring_bytes=8 * MB)
     n = 40 * MB + 13
     host = host_bytes(n, 7)
