@@ -334,10 +334,12 @@ def roofline_block(achieved, kern_ms, store_ms, fetch_ms, nbytes, peaks, peak_sr
            "traffic": round(t["per_launch"]) if t else None,
            "algorithmic_bytes_per_launch": 2 * nbytes, "kernel_ms": round(kern_ms, 5),
            "store_launch_ms": round(store_ms, 5), "fetch_launch_ms": round(fetch_ms, 5),
-           "kernel_ms_per_step": round(store_ms + fetch_ms, 5),
+           "kernel_ms_per_step": round(2 * kern_ms, 5),
            "step_ms_p50": round(nearest_rank(per_ms, 50), 5),
-           "timing": "CUDA events around each launch inside the flushed config-1 pass, pass pre-queued behind a "
-                     "device spin (no host gaps); median over passes",
+           "timing": "CUDA events around the flushed config-1 pass (its store and fetch launches back to back), "
+                     "pre-queued behind a device spin so no host gap is inside; average launch = half the "
+                     "bracket; median over passes. store/fetch_launch_ms: the same with an event between the "
+                     "two launches (each bracket carries the event pair's own floor, event_floor_ms)",
            "peak_source": peak_src,
            "hbm_bound_point": {"bytes": 1 << 30, "kernel_ms": round(gib_ms, 4), "achieved": round(achieved_gib, 1),
                                "frac": round(achieved_gib / peak, 4),
@@ -492,12 +494,37 @@ def run_ours(args):
         fetch_ms = statistics.median(e[3].elapsed_time(e[4]) for e in kern)
     else:
         fetch_ms = statistics.median(e[1].elapsed_time(e[2]) for e in kern)
+    pair_ms = None
+    if not cross:
+        # both launches between two events only (an event between kernels costs a few us
+        # of its own): the average launch duration is half of this bracket
+        pair = []
+        for i in range(max(3, args.steps)):
+            flush_l2(i)
+            spin_ns(g, s, 200_000)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(s)
+            one_pass()
+            b.record(s)
+            pair.append((a, b))
+        torch.cuda.synchronize(g)
+        pair_ms = statistics.median(a.elapsed_time(b) for a, b in pair)
+        # the same bracket with nothing inside: the event pair's own floor on this GPU
+        nil = []
+        for i in range(8):
+            spin_ns(g, s, 50_000)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(s)
+            b.record(s)
+            nil.append((a, b))
+        torch.cuda.synchronize(g)
+        event_floor_ms = statistics.median(a.elapsed_time(b) for a, b in nil)
     assert delivered(), "delivered bytes differ"
     peaks, peak_src = measured_peaks()
     gib_ms = achieved_gib = None
     zc_ms = None
     if not cross:
-        kern_ms = (store_ms + fetch_ms) / 2                  # average launch duration in the pass
+        kern_ms = pair_ms / 2                                # average launch duration in the pass
         achieved = 2 * nbytes / (kern_ms * 1e-3) / 1e9       # read + write bytes per launch
         # the HBM-bound point: the same kernel over 1 GiB (L2 is 126 MB: nothing stays resident)
         big = torch.empty(1 << 30, dtype=torch.uint8, device=f"cuda:{g}")
@@ -652,6 +679,7 @@ def run_ours(args):
         else:
             roof = roofline_block(achieved, kern_ms, store_ms, fetch_ms, nbytes, peaks, peak_src, traffic, per_ms,
                                   achieved_gib, gib_ms)
+            roof["event_floor_ms"] = round(event_floor_ms, 5)
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(total_ms_max / args.steps, 5), "higher_is_better": True,

@@ -32,4 +32,30 @@ p.wait(t)
 torch.cuda.synchronize()
 assert torch.equal(d.cpu(), h)
 p.close()
+# K2 forward (device flags + one forward kernel per batch), misaligned destination too
+os.environ["FT_K2"] = "1"
+p = dev.Pacer(50.0, 5, 2 * 10**6, staging_slots=2)
+for off in (0, 3):
+    d = torch.zeros(h.numel() + 16, dtype=torch.uint8, device="cuda:0")
+    t = p.submit("", off == 0, 1e9, 0.0, 50.0, d.data_ptr() + off, 0, h.data_ptr(), h.numel(), True,
+                 [(0, 1, 0, h.numel(), st[0][0].cuda_stream, st[0][1].cuda_stream)], s.cuda_stream)
+    p.wait(t)
+    torch.cuda.synchronize()
+    assert torch.equal(d[off:off + h.numel()].cpu(), h)
+p.close()
+# fused request-path calls and the batched retire
+from paper_2411_01830_b200.tube import FaaSTube  # noqa: E402
+tube = FaaSTube("faastube", gpus=[0], pcie_gbps=50.0, pool_floor_bytes=0.0)
+xs = [torch.randint(0, 256, (n,), dtype=torch.uint8, device="cuda:0") for n in (1, 4097, 1 << 20)]
+ids = []
+for x in xs:
+    ids.append(tube.unique_id())
+    tube.store(ids[-1], x, consumers=2)
+outs = [torch.empty_like(x) for x in xs]
+for i, o in zip(ids, outs):
+    tube.fetch(i, device=0, out=o)
+tube.fetch_many([(i, torch.empty_like(x)) for i, x in zip(ids, xs)])
+torch.cuda.synchronize()
+assert all(torch.equal(a, b) for a, b in zip(xs, outs))
+tube.close()
 print("kernels exercised ok")
