@@ -310,8 +310,18 @@ typedef struct ft_vmm_pool ft_vmm_pool;
 int ft_vmm_pool_create(int device, uint64_t va_bytes, ft_vmm_pool** out);
 void ft_vmm_pool_destroy(ft_vmm_pool* p);
 int ft_vmm_granularity(int device, uint64_t* out);
+/* blocks are ranges of arenas (one cuMemCreate each, mapped once with every
+ * peer's access): map/unmap of a block is bookkeeping; a new arena (FT_POOL_ARENA_BYTES,
+ * default 1 GiB, or the block if larger) is mapped only when none has room */
 int ft_vmm_block_map(ft_vmm_pool* p, uint64_t bytes, uint64_t* block, void** dptr);
 int ft_vmm_block_unmap(ft_vmm_pool* p, uint64_t block);
+/* map an arena of `bytes` now, never trimmed (the pool's up-front reservation) */
+int ft_vmm_pool_reserve(ft_vmm_pool* p, uint64_t bytes);
+/* unmap every unreserved arena no block uses; their ids out (call when idle) */
+int ft_vmm_pool_trim(ft_vmm_pool* p, uint64_t* arenas, int cap, int* n);
+/* the arena a block lives in, its offset there, the arena's size */
+int ft_vmm_block_locate(ft_vmm_pool* p, uint64_t block, uint64_t* arena, uint64_t* offset, uint64_t* arena_bytes);
+/* POSIX fd of the block's ARENA (map it whole, add the block's offset) */
 int ft_vmm_block_export_fd(ft_vmm_pool* p, uint64_t block, int* fd);
 int ft_vmm_pool_stats(const ft_vmm_pool* p, uint64_t* mapped_bytes, uint64_t* reserved_bytes, int* blocks);
 /* import a block exported by another process; map it for `device` */

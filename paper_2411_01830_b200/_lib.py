@@ -229,6 +229,9 @@ _SIGS = {
     "ft_vmm_block_map": (None, [vp, u64, P(u64), P(vp)]),
     "ft_vmm_block_unmap": (None, [vp, u64]),
     "ft_vmm_block_export_fd": (None, [vp, u64, P(C.c_int)]),
+    "ft_vmm_pool_reserve": (None, [vp, u64]),
+    "ft_vmm_pool_trim": (None, [vp, P(u64), C.c_int, P(C.c_int)]),
+    "ft_vmm_block_locate": (None, [vp, u64, P(u64), P(u64), P(u64)]),
     "ft_vmm_pool_stats": (None, [vp, P(u64), P(u64), P(C.c_int)]),
     "ft_vmm_import_fd": (None, [C.c_int, C.c_int, u64, P(vp), P(u64)]),
     "ft_vmm_unimport": (None, [u64]),

@@ -674,9 +674,24 @@ void put_events(int device, const std::vector<cudaEvent_t>& evs) {
 }
 
 // ------------------------------------------------------------ VMM pool
-struct Block {
+// A pool block is a range of an arena: one physical allocation (cuMemCreate),
+// mapped once into the pool's VA range with every peer's access. Blocks are
+// carved out of arenas and given back to them without any driver call; only a
+// new arena maps memory (and only an idle trim unmaps). cuMemMap / cuMemUnmap
+// wait for the GPU's running kernels and stall every CUDA call of the process
+// meanwhile (0.3-1 s under load, profiles/r01/diag_vmm_map_unmap.txt), so they
+// must not happen per block on the request path.
+struct Arena {
   CUmemGenericAllocationHandle h;
   CUdeviceptr va;
+  size_t bytes;
+  size_t used = 0;
+  bool keep = false;                 // reserved up front: never trimmed
+  std::map<size_t, size_t> free;     // offset -> length (coalesced)
+};
+struct Block {
+  uint64_t arena;
+  size_t off;
   size_t bytes;
 };
 struct Import {
@@ -724,12 +739,121 @@ struct ft_vmm_pool {
   size_t gran;
   CUdeviceptr base;
   size_t va_bytes;
-  std::map<size_t, size_t> free_va;  // offset -> length
+  std::map<size_t, size_t> free_va;  // offset -> length (arena VA ranges)
+  std::map<uint64_t, Arena> arenas;
   std::map<uint64_t, Block> blocks;
-  uint64_t next_id = 1;
+  uint64_t next_id = 1, next_arena = 1;
   size_t mapped = 0;
+  size_t arena_bytes = 1ull << 30;   // growth unit (FT_POOL_ARENA_BYTES)
   std::mutex mu;
 };
+
+namespace {
+// carve sz bytes (granule multiple) out of the first arena with a fitting free range
+bool carve(ft_vmm_pool* p, size_t sz, uint64_t* arena, size_t* off) {
+  for (auto& kv : p->arenas) {
+    Arena& a = kv.second;
+    if (a.bytes - a.used < sz) continue;
+    for (auto it = a.free.begin(); it != a.free.end(); ++it) {
+      if (it->second < sz) continue;
+      size_t o = it->first, len = it->second;
+      a.free.erase(it);
+      if (len > sz) a.free[o + sz] = len - sz;
+      a.used += sz;
+      *arena = kv.first;
+      *off = o;
+      return true;
+    }
+  }
+  return false;
+}
+void give_back(Arena& a, size_t off, size_t len) {
+  a.used -= len;
+  auto nxt = a.free.lower_bound(off);
+  if (nxt != a.free.end() && nxt->first == off + len) {
+    len += nxt->second;
+    a.free.erase(nxt);
+  }
+  auto prv = a.free.lower_bound(off);
+  if (prv != a.free.begin()) {
+    --prv;
+    if (prv->first + prv->second == off) {
+      off = prv->first;
+      len += prv->second;
+      a.free.erase(prv);
+    }
+  }
+  a.free[off] = len;
+}
+// map a new arena of `bytes` (outside the pool mutex: the driver calls are slow)
+int map_arena(ft_vmm_pool* p, size_t bytes, bool keep, uint64_t* id_out) {
+  Drv* d = drv();
+  size_t off = SIZE_MAX;
+  {
+    std::lock_guard<std::mutex> lk(p->mu);
+    for (auto& kv : p->free_va)
+      if (kv.second >= bytes) {
+        off = kv.first;
+        break;
+      }
+    if (off == SIZE_MAX) {
+      ft::set_last_error("VMM pool virtual range exhausted");
+      return FT_E_OOM;
+    }
+    size_t len = p->free_va[off];
+    p->free_va.erase(off);
+    if (len > bytes) p->free_va[off + bytes] = len - bytes;
+  }
+  auto give_back_va = [&] {
+    std::lock_guard<std::mutex> lk(p->mu);
+    p->free_va[off] = bytes;
+  };
+  static const bool trace = std::getenv("FT_VMM_TRACE") != nullptr;
+  auto t0 = std::chrono::steady_clock::now();
+  cudaError_t ce = cudaSetDevice(p->device);
+  if (ce != cudaSuccess) {
+    give_back_va();
+    return cuda_fail(ce, "cudaSetDevice");
+  }
+  CUmemAllocationProp prop = block_prop(p->device);
+  CUmemGenericAllocationHandle h;
+  CUresult r = d->create(&h, bytes, &prop, 0);
+  if (r != CUDA_SUCCESS) {
+    give_back_va();
+    return cu_fail(r, "cuMemCreate");
+  }
+  CUdeviceptr va = p->base + off;
+  r = d->map(va, bytes, 0, h, 0);
+  if (r != CUDA_SUCCESS) {
+    d->release(h);
+    give_back_va();
+    return cu_fail(r, "cuMemMap");
+  }
+  int rc = grant_access(d, va, bytes, p->device, true);
+  if (rc) {
+    d->unmap(va, bytes);
+    d->release(h);
+    give_back_va();
+    return rc;
+  }
+  if (trace) {
+    auto ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    std::fprintf(stderr, "[ft_vmm] arena %zu MB mapped in %.2f ms\n", bytes >> 20, ms);
+  }
+  std::lock_guard<std::mutex> lk(p->mu);
+  uint64_t id = p->next_arena++;
+  Arena a;
+  a.h = h;
+  a.va = va;
+  a.bytes = bytes;
+  a.keep = keep;
+  a.free[0] = bytes;
+  p->arenas.emplace(id, std::move(a));
+  p->mapped += bytes;
+  if (id_out) *id_out = id;
+  return FT_OK;
+}
+}  // namespace
 
 namespace ft {
 
@@ -872,6 +996,8 @@ int ft_vmm_pool_create(int device, uint64_t va_bytes, ft_vmm_pool** out) {
   p->base = base;
   p->va_bytes = va_bytes;
   p->free_va[0] = va_bytes;
+  if (const char* e = std::getenv("FT_POOL_ARENA_BYTES")) p->arena_bytes = std::max<size_t>(gran, std::atoll(e));
+  p->arena_bytes = (p->arena_bytes + gran - 1) / gran * gran;
   va_add((uintptr_t)base, va_bytes, device);
   *out = p;
   return FT_OK;
@@ -881,7 +1007,7 @@ void ft_vmm_pool_destroy(ft_vmm_pool* p) {
   if (!p) return;
   Drv* d = drv();
   if (d) {
-    for (auto& kv : p->blocks) {
+    for (auto& kv : p->arenas) {
       d->unmap(kv.second.va, kv.second.bytes);
       d->release(kv.second.h);
     }
@@ -891,83 +1017,45 @@ void ft_vmm_pool_destroy(ft_vmm_pool* p) {
   delete p;
 }
 
+int ft_vmm_pool_reserve(ft_vmm_pool* p, uint64_t bytes) {
+  if (!p || !bytes) {
+    ft::set_last_error("ft_vmm_pool_reserve: bad arguments");
+    return FT_E_VALUE;
+  }
+  size_t sz = (bytes + p->gran - 1) / p->gran * p->gran;
+  return map_arena(p, sz, true, nullptr);
+}
+
 int ft_vmm_block_map(ft_vmm_pool* p, uint64_t bytes, uint64_t* block, void** dptr) {
   if (!p || !bytes) {
     ft::set_last_error("ft_vmm_block_map: bad arguments");
     return FT_E_VALUE;
   }
-  Drv* d = drv();
   size_t sz = (bytes + p->gran - 1) / p->gran * p->gran;
-  size_t off = SIZE_MAX;
-  {
-    // only the VA bookkeeping is under the pool mutex: cuMemCreate/Map/SetAccess can
-    // take tens of ms while the GPU is busy, and a request's growth must not queue
-    // behind the background spare thread's mapping
-    std::lock_guard<std::mutex> lk(p->mu);
-    for (auto& kv : p->free_va)
-      if (kv.second >= sz) {
-        off = kv.first;
-        break;
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    {
+      std::lock_guard<std::mutex> lk(p->mu);
+      uint64_t ar = 0;
+      size_t off = 0;
+      if (carve(p, sz, &ar, &off)) {
+        uint64_t id = p->next_id++;
+        p->blocks[id] = Block{ar, off, sz};
+        *block = id;
+        *dptr = reinterpret_cast<void*>(p->arenas[ar].va + off);
+        return FT_OK;
       }
-    if (off == SIZE_MAX) {
-      ft::set_last_error("VMM pool virtual range exhausted");
-      return FT_E_OOM;
     }
-    size_t len = p->free_va[off];
-    p->free_va.erase(off);
-    if (len > sz) p->free_va[off + sz] = len - sz;
+    if (attempt) break;
+    // no arena has room: map a new one (the growth unit, or the block if larger)
+    int rc = map_arena(p, std::max(sz, p->arena_bytes), false, nullptr);
+    if (rc == FT_E_OOM && sz < p->arena_bytes) rc = map_arena(p, sz, false, nullptr);  // near the memory limit
+    if (rc) return rc;
   }
-  auto give_back_va = [&] {
-    std::lock_guard<std::mutex> lk(p->mu);
-    p->free_va[off] = sz;  // (not coalesced with neighbours: the range stays usable for its size)
-  };
-  static const bool trace = std::getenv("FT_VMM_TRACE") != nullptr;
-  auto t0 = std::chrono::steady_clock::now();
-  cudaError_t ce = cudaSetDevice(p->device);
-  if (ce != cudaSuccess) {
-    give_back_va();
-    return cuda_fail(ce, "cudaSetDevice");
-  }
-  CUmemAllocationProp prop = block_prop(p->device);
-  CUmemGenericAllocationHandle h;
-  CUresult r = d->create(&h, sz, &prop, 0);
-  if (r != CUDA_SUCCESS) {
-    give_back_va();
-    return cu_fail(r, "cuMemCreate");
-  }
-  auto t1 = std::chrono::steady_clock::now();
-  CUdeviceptr va = p->base + off;
-  r = d->map(va, sz, 0, h, 0);
-  if (r != CUDA_SUCCESS) {
-    d->release(h);
-    give_back_va();
-    return cu_fail(r, "cuMemMap");
-  }
-  auto t2 = std::chrono::steady_clock::now();
-  int rc = grant_access(d, va, sz, p->device, true);
-  if (rc) {
-    d->unmap(va, sz);
-    d->release(h);
-    give_back_va();
-    return rc;
-  }
-  auto t3 = std::chrono::steady_clock::now();
-  if (trace) {
-    auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
-    std::fprintf(stderr, "[ft_vmm] map %zu MB: create %.2f ms, map %.2f ms, access %.2f ms\n", sz >> 20,
-                 ms(t0, t1), ms(t1, t2), ms(t2, t3));
-  }
-  std::lock_guard<std::mutex> lk(p->mu);
-  uint64_t id = p->next_id++;
-  p->blocks[id] = Block{h, va, sz};
-  p->mapped += sz;
-  *block = id;
-  *dptr = reinterpret_cast<void*>(va);
-  return FT_OK;
+  ft::set_last_error("ft_vmm_block_map: no room after growth");
+  return FT_E_OOM;
 }
 
 int ft_vmm_block_unmap(ft_vmm_pool* p, uint64_t block) {
-  Drv* d = drv();
   std::lock_guard<std::mutex> lk(p->mu);
   auto it = p->blocks.find(block);
   if (it == p->blocks.end()) {
@@ -976,30 +1064,72 @@ int ft_vmm_block_unmap(ft_vmm_pool* p, uint64_t block) {
   }
   Block b = it->second;
   p->blocks.erase(it);
-  CU_DRV(d->unmap(b.va, b.bytes));
-  CU_DRV(d->release(b.h));
-  p->mapped -= b.bytes;
-  // return the VA range, coalescing neighbours
-  size_t off = b.va - p->base, len = b.bytes;
-  auto nxt = p->free_va.lower_bound(off);
-  if (nxt != p->free_va.end() && nxt->first == off + len) {
-    len += nxt->second;
-    p->free_va.erase(nxt);
-  }
-  auto prv = p->free_va.lower_bound(off);
-  if (prv != p->free_va.begin()) {
-    --prv;
-    if (prv->first + prv->second == off) {
-      off = prv->first;
-      len += prv->second;
-      p->free_va.erase(prv);
+  give_back(p->arenas[b.arena], b.off, b.bytes);  // no driver call: the arena stays mapped
+  return FT_OK;
+}
+
+int ft_vmm_pool_trim(ft_vmm_pool* p, uint64_t* arenas_out, int cap, int* n_out) {
+  // unmap every arena no block uses (and not reserved): physical memory back to
+  // the driver. Call when the GPU is quiet (the unmap stalls the process otherwise)
+  Drv* d = drv();
+  std::vector<std::pair<uint64_t, Arena>> gone;
+  {
+    std::lock_guard<std::mutex> lk(p->mu);
+    for (auto it = p->arenas.begin(); it != p->arenas.end();) {
+      if (it->second.used == 0 && !it->second.keep) {
+        gone.emplace_back(it->first, std::move(it->second));
+        it = p->arenas.erase(it);
+      } else {
+        ++it;
+      }
     }
   }
-  p->free_va[off] = len;
+  int n = 0, rc = FT_OK;
+  for (auto& g : gone) {
+    CUresult r = d->unmap(g.second.va, g.second.bytes);
+    if (r == CUDA_SUCCESS) r = d->release(g.second.h);
+    if (r != CUDA_SUCCESS && rc == FT_OK) rc = cu_fail(r, "trim");
+    std::lock_guard<std::mutex> lk(p->mu);
+    p->mapped -= g.second.bytes;
+    size_t off = g.second.va - p->base, len = g.second.bytes;
+    auto nxt = p->free_va.lower_bound(off);
+    if (nxt != p->free_va.end() && nxt->first == off + len) {
+      len += nxt->second;
+      p->free_va.erase(nxt);
+    }
+    auto prv = p->free_va.lower_bound(off);
+    if (prv != p->free_va.begin()) {
+      --prv;
+      if (prv->first + prv->second == off) {
+        off = prv->first;
+        len += prv->second;
+        p->free_va.erase(prv);
+      }
+    }
+    p->free_va[off] = len;
+    if (arenas_out && n < cap) arenas_out[n] = g.first;
+    ++n;
+  }
+  if (n_out) *n_out = n;
+  return rc;
+}
+
+int ft_vmm_block_locate(ft_vmm_pool* p, uint64_t block, uint64_t* arena, uint64_t* offset, uint64_t* arena_bytes) {
+  std::lock_guard<std::mutex> lk(p->mu);
+  auto it = p->blocks.find(block);
+  if (it == p->blocks.end()) {
+    ft::set_last_error("unknown VMM block");
+    return FT_E_KEY;
+  }
+  if (arena) *arena = it->second.arena;
+  if (offset) *offset = it->second.off;
+  if (arena_bytes) *arena_bytes = p->arenas[it->second.arena].bytes;
   return FT_OK;
 }
 
 int ft_vmm_block_export_fd(ft_vmm_pool* p, uint64_t block, int* fd) {
+  // the block's arena (the unit of physical memory); the importer maps the whole
+  // arena once and finds the block at its offset (ft_vmm_block_locate)
   Drv* d = drv();
   std::lock_guard<std::mutex> lk(p->mu);
   auto it = p->blocks.find(block);
@@ -1008,7 +1138,7 @@ int ft_vmm_block_export_fd(ft_vmm_pool* p, uint64_t block, int* fd) {
     return FT_E_KEY;
   }
   int f = -1;
-  CU_DRV(d->export_handle(&f, it->second.h, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0));
+  CU_DRV(d->export_handle(&f, p->arenas[it->second.arena].h, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0));
   *fd = f;
   return FT_OK;
 }

@@ -242,8 +242,11 @@ class TubeDaemon:
             conn.ch.send_fd(fd, {})
 
     def _reply_block(self, conn, g, blk, meta):
-        key = (g, int(blk.vmm_id))
-        meta = dict(meta, block=key[1], block_bytes=int(blk.nbytes))
+        # the client maps the block's arena once (the unit of physical memory) and
+        # finds the block at its offset
+        arena, off, abytes = self.tube.pools[g].locate(blk)
+        key = (g, int(arena))
+        meta = dict(meta, block=key[1], off=int(off), block_bytes=int(abytes))
         with self._lock:
             known = key in conn.mapped
             conn.mapped.add(key)
@@ -462,7 +465,7 @@ class TubeClient:
         try:
             imp = self._imports.get(bid)
             if imp is None:
-                imp = self._imports[bid] = dev.ImportedBlock(self.device, fd, rep["block_bytes"])
+                imp = self._imports[bid] = dev.ImportedBlock(self.device, fd, rep["block_bytes"])   # the arena
             return imp
         finally:
             os.close(fd)
@@ -516,13 +519,14 @@ class TubeClient:
             imp = self._mapped(rep)
         else:
             imp = self._imports[rep["block"]]
+        ptr = imp.ptr + rep.get("off", 0)
         if self._mine is None:
             cur = self._stream
             cur.wait_stream(torch.cuda.current_stream(self.device))
         else:
             cur = torch.cuda.current_stream(self.device)
         self._after_daemon(rep, cur)                  # the block's previous users are done
-        dev.copy(imp.ptr, t.data_ptr(), n, self.device, cur)
+        dev.copy(ptr, t.data_ptr(), n, self.device, cur)
         ev = self._mark(cur)                          # written (or synchronised) before the daemon publishes it
         if t is not output or self._mine is None:
             t.record_stream(cur)
@@ -552,6 +556,7 @@ class TubeClient:
         rep = self._call({"op": "fetch", "id": data_id, "gpu": self.device, "consumer": consumer,
                           "slo_ms": slo_ms, "infer_ms": infer_ms})
         imp = self._mapped(rep)
+        ptr = imp.ptr + rep.get("off", 0)
         dt, shape, n = _DTYPES[rep["dtype"]], rep["shape"], rep["nbytes"]
         if out is not None and (not out.is_contiguous() or out.nbytes != n):
             self._send({"op": "done", "token": rep["token"], "ev": -1})
@@ -566,8 +571,8 @@ class TubeClient:
                 owner = _Release()
                 self._views += 1
                 weakref.finalize(owner, self._release, rep["token"])
-                return dev.as_tensor(imp.ptr, n, self.device, dt, tuple(shape), owner=owner)
-            dev.copy(out.data_ptr(), imp.ptr, n, self.device, cur)
+                return dev.as_tensor(ptr, n, self.device, dt, tuple(shape), owner=owner)
+            dev.copy(out.data_ptr(), ptr, n, self.device, cur)
             self._send({"op": "done", "token": rep["token"], "ev": self._mark(cur)})
             return out
         # host-synced connection: copy on the private stream, synchronise, release
@@ -575,7 +580,7 @@ class TubeClient:
             out = torch.empty(shape, dtype=dt, device=f"cuda:{self.device}")
         cur = torch.cuda.current_stream(self.device)
         self._stream.wait_stream(cur)
-        dev.copy(out.data_ptr(), imp.ptr, n, self.device, self._stream)
+        dev.copy(out.data_ptr(), ptr, n, self.device, self._stream)
         self._stream.synchronize()                     # read before the daemon may reuse the block
         self._send({"op": "done", "token": rep["token"]})
         cur.wait_stream(self._stream)

@@ -300,16 +300,24 @@ class DevicePool:
 
     def __init__(self, device: int, mode: str = "autoscale", floor_bytes: float = datastore.POOL_FLOOR_BYTES,
                  native_alloc_ms: float = datastore.NATIVE_ALLOC_MS, va_bytes: int = 256 * GiB,
-                 physical_bytes: float | None = None, spare_cap_bytes: int = 4 * GiB):
+                 physical_bytes: float | None = None, spare_cap_bytes: int = 0, reserve_bytes: int | None = None):
         require_cuda()
         self.device = device
-        self.on_unmap = []           # callbacks(vmm_id) after a block is unmapped (daemon.py)
+        self.on_unmap = []           # callbacks(arena id) after an arena is unmapped (daemon.py)
         if physical_bytes is None:
             physical_bytes = float(torch.cuda.get_device_properties(device).total_memory)
         self.policy = datastore.MemoryPool(device, mode, floor_bytes, native_alloc_ms, physical_bytes)
         h = C.c_void_p()
         LIB.ft_vmm_pool_create(int(device), int(va_bytes), C.byref(h))
         self._h = h
+        # physical memory is mapped in arenas (csrc/device.cu): blocks are ranges of
+        # them, so growth and shrink of the policy's blocks cost no driver call; an up-front
+        # arena covers the common working set (a new one is mapped only when none has
+        # room, and unused ones are unmapped only when the GPU is quiet — reclaim())
+        if reserve_bytes is None:
+            reserve_bytes = int(os.environ.get("FT_POOL_RESERVE_BYTES", 2 * GiB))
+        if mode != "none" and reserve_bytes > 0:
+            LIB.ft_vmm_pool_reserve(h, int(reserve_bytes))
         self._mapped = {}  # policy block id -> (vmm id, ptr, bytes)
         self._fences = {}  # policy block id -> events the freed block's last users recorded
         self._bases = {}   # vmm id -> uint8 tensor over the whole mapping (zero-copy views slice it)
@@ -564,8 +572,9 @@ class DevicePool:
         return n
 
     def reclaim(self) -> int:
-        """Unmap every released block (after its last users' events) — the
-        physical memory goes back to the driver. Returns bytes unmapped."""
+        """Give every released block back to its arena (after its last users'
+        events), then unmap the arenas no block uses — the physical memory goes
+        back to the driver. Returns the bytes of the released blocks."""
         with self._lock:
             gone, self._released = self._released, []
         for _vid, _ptr, _n, fences in gone:
@@ -574,8 +583,23 @@ class DevicePool:
         for vid, _ptr, _n, _f in gone:
             self._bases.pop(vid, None)
             LIB.ft_vmm_block_unmap(self._h, vid)
-            self._notify_unmap(vid)
+        self.trim()
         return sum(r[2] for r in gone)
+
+    def trim(self) -> int:
+        """Unmap the arenas no block uses (driver calls: only when the GPU is quiet)."""
+        cap = 256
+        ids, n = (C.c_uint64 * cap)(), C.c_int()
+        LIB.ft_vmm_pool_trim(self._h, ids, cap, C.byref(n))
+        for i in range(min(n.value, cap)):
+            self._notify_unmap(ids[i])
+        return n.value
+
+    def locate(self, blk: "PoolBlock") -> tuple:
+        """(arena id, offset of the block in it, arena bytes): what another process maps."""
+        a, o, n = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        LIB.ft_vmm_block_locate(self._h, blk.vmm_id, C.byref(a), C.byref(o), C.byref(n))
+        return a.value, o.value, n.value
 
     def _notify_unmap(self, vid):
         for fn in self.on_unmap:     # importers of an exported block drop their mapping
@@ -596,14 +620,19 @@ class DevicePool:
         for ev in self._fences.pop(block_id, ()):  # no in-flight kernel may touch it
             ev.synchronize()
         self._bases.pop(m[0], None)
-        LIB.ft_vmm_block_unmap(self._h, m[0])
-        self._notify_unmap(m[0])
+        LIB.ft_vmm_block_unmap(self._h, m[0])            # back to its arena (no driver call)
         return m[2]
 
     def export_fd(self, blk: PoolBlock) -> int:
+        """POSIX fd of the block's arena (pair it with ``locate`` / use ``export``)."""
         fd = C.c_int()
         LIB.ft_vmm_block_export_fd(self._h, blk.vmm_id, C.byref(fd))
         return fd.value
+
+    def export(self, blk: PoolBlock) -> tuple:
+        """(fd, arena bytes, offset of the block): ImportedBlock(device, fd, arena_bytes, offset, n)."""
+        _arena, off, abytes = self.locate(blk)
+        return self.export_fd(blk), abytes, off
 
     def stats(self) -> dict:
         mapped, reserved, n = C.c_uint64(), C.c_uint64(), C.c_int()
@@ -614,12 +643,15 @@ class DevicePool:
 
 
 class ImportedBlock:
-    """A pool block exported by another process and mapped here (zero copy)."""
+    """A pool arena exported by another process and mapped here whole (zero
+    copy); ``ptr`` is the block at ``offset`` in it, ``nbytes`` long."""
 
-    def __init__(self, device: int, fd: int, nbytes: int):
-        ptr, h = C.c_void_p(), C.c_uint64()
-        LIB.ft_vmm_import_fd(int(device), int(fd), int(nbytes), C.byref(ptr), C.byref(h))
-        self.device, self.nbytes, self.ptr, self._h = device, nbytes, ptr.value, h.value
+    def __init__(self, device: int, fd: int, arena_bytes: int, offset: int = 0, nbytes: int | None = None):
+        base, h = C.c_void_p(), C.c_uint64()
+        LIB.ft_vmm_import_fd(int(device), int(fd), int(arena_bytes), C.byref(base), C.byref(h))
+        self.device, self.base, self._h = device, base.value, h.value
+        self.ptr = base.value + int(offset)
+        self.nbytes = int(nbytes) if nbytes is not None else int(arena_bytes) - int(offset)
         self._fin = weakref.finalize(self, LIB.ft_vmm_unimport, h.value)
 
     def tensor(self, dtype=torch.uint8, shape=None) -> torch.Tensor:

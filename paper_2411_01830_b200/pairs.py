@@ -45,18 +45,26 @@ class CrossPair:
         barrier()
         # to the next rank (my consumer): payload + my flags (for its ACK writes)
         out = Channel.connect(os.path.join(sock_dir, f"r{nxt}.sock"))
-        mine = [pool.export_fd(self.payload), pool.export_fd(self.flags), pool.export_fd(self.flags)]
-        out.send_fd(mine[0], {"kind": "payload", "nbytes": self.payload.nbytes})
-        out.send_fd(mine[1], {"kind": "flags", "nbytes": self.flags.nbytes})
+        exp = [pool.export(self.payload), pool.export(self.flags), pool.export(self.flags)]
+        mine = [e[0] for e in exp]
+
+        def meta(kind, blk, e):
+            return {"kind": kind, "nbytes": blk.nbytes, "arena_bytes": e[1], "off": e[2]}
+
+        def imp(fd, m):
+            return dev.ImportedBlock(device, fd, m["arena_bytes"], m["off"], m["nbytes"])
+
+        out.send_fd(mine[0], meta("payload", self.payload, exp[0]))
+        out.send_fd(mine[1], meta("flags", self.flags, exp[1]))
         # from the previous rank (my producer): its payload + flags; reply with mine
         inc = Channel.accept(srv)
         fd_p, meta_p = inc.recv_fd()
         fd_f, meta_f = inc.recv_fd()
-        self.peer_payload = dev.ImportedBlock(device, fd_p, meta_p["nbytes"])
-        self.peer_flags = dev.ImportedBlock(device, fd_f, meta_f["nbytes"])   # previous rank's flags
-        inc.send_fd(mine[2], {"kind": "flags", "nbytes": self.flags.nbytes})
+        self.peer_payload = imp(fd_p, meta_p)
+        self.peer_flags = imp(fd_f, meta_f)                                   # previous rank's flags
+        inc.send_fd(mine[2], meta("flags", self.flags, exp[2]))
         fd_n, meta_n = out.recv_fd()
-        self.next_flags = dev.ImportedBlock(device, fd_n, meta_n["nbytes"])   # next rank's flags
+        self.next_flags = imp(fd_n, meta_n)                                   # next rank's flags
         for fd in (fd_p, fd_f, fd_n, *mine):
             os.close(fd)
         barrier()

@@ -426,6 +426,11 @@ class Runtime:
                 per.setdefault(r.workflow, []).append(r.end_ms - r.arrival_ms)
             out["per_workflow_p99_ms"] = {k: round(nearest_rank(v, 99), 4) for k, v in sorted(per.items())}
             out["worst"] = self.breakdown(max(done, key=lambda r: r.end_ms - r.arrival_ms))
+            st = self.tube.stats
+            out["tube"] = {"migrated_bytes": st.get("migrated_bytes", 0), "reload_bytes": st.get("reload_bytes", 0),
+                           "grow_events": sum(p.grow_events for p in self.tube.pools.values()),
+                           "spares_mapped": sum(p.spares_mapped for p in self.tube.pools.values()),
+                           "slow_stores": [list(x) for x in list(self.tube.slow_stores)[-6:]]}
             out["_lat"] = lat                # raw latencies (callers pooling runs pop it)
             out["_slo_miss"] = [r.end_ms - r.arrival_ms > r.slo_ms + 1e-9 for r in done]
         return out

@@ -133,7 +133,7 @@ class FaaSTube:
                                2 * default_ring_capacity(len(roots), batch_chunks * chunk_bytes),
                                logging=bool(os.environ.get("FT_TRACE")), links=len(roots))
         self._tickets = []           # (ticket, keep-alive refs) until the stage has landed
-        self.slow_stores = collections.deque(maxlen=64)   # stores over 10 ms: (alloc ms, locked ms, bytes)
+        self.slow_stores = collections.deque(maxlen=64)   # stores over 10 ms: (alloc, locked, migrate ms, bytes)
         self._pending = set()        # ("pressure" | "prefetch", gpu): decided under the lock, run after it
         self._migrating = {}         # gpu -> bytes of migration victims being moved out
         self._off_gpu = collections.Counter()   # home gpu -> live objects migrated off it (prefetch candidates)
@@ -292,8 +292,6 @@ class FaaSTube:
                 self.pools[output.device.index].free(pre_blk, list(pre_blk.fences))
             raise
         t2 = time.perf_counter()
-        if t2 - t0 > 0.01:   # slow stores, for diagnosis: (ms allocating, ms in the locked part, bytes)
-            self.slow_stores.append((round(1e3 * (t1 - t0), 2), round(1e3 * (t2 - t1), 2), output.nbytes))
         if stage is not None:
             # managed GPU->host response stage (engine.py:414-423 -> 537-575), paced
             # by the d2h arbiter outside the tube lock; the object stays pinned
@@ -309,6 +307,10 @@ class FaaSTube:
                 self._unpin(obj)
         if self._pending:
             self._drain_pending()                         # migration decided by this store
+        t3 = time.perf_counter()
+        if t3 - t0 > 0.01:   # slow stores, for diagnosis: ms allocating / in the locked part / migrating, bytes
+            self.slow_stores.append((round(1e3 * (t1 - t0), 2), round(1e3 * (t2 - t1), 2),
+                                     round(1e3 * (t3 - t2), 2), output.nbytes))
 
     def _store_locked(self, data_id, output, response, producer, consumers, queue_pos, pre_host, pre_blk):
         """Returns (obj, pacer.submit_d2h args) when a managed response stage must be submitted."""

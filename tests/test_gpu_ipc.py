@@ -16,12 +16,12 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def _child(s, nbytes, q):
+def _child(s, arena_bytes, off, nbytes, q):
     sys.path.insert(0, ROOT)
     try:
         from paper_2411_01830_b200 import device
         fd, tag = device.recv_fd(s)
-        blk = device.ImportedBlock(0, fd, nbytes)
+        blk = device.ImportedBlock(0, fd, arena_bytes, off, nbytes)
         t = blk.tensor()
         fp = device.Fingerprint(0)
         fp.launch(t.data_ptr(), tag)
@@ -44,11 +44,11 @@ def test_export_import_across_processes():
     view = device.as_tensor(blk.ptr, n, 0)
     view.copy_(src)
     torch.cuda.synchronize()
-    fd = pool.export_fd(blk)
+    fd, arena_bytes, off = pool.export(blk)        # the block's arena + its offset there
     a, b = socket.socketpair(socket.AF_UNIX, socket.SOCK_STREAM)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    p = ctx.Process(target=_child, args=(b, blk.nbytes, q))   # socket is duplicated into the child
+    p = ctx.Process(target=_child, args=(b, arena_bytes, off, blk.nbytes, q))   # socket duplicated into the child
     p.start()
     device.send_fd(a, fd, n)
     status, val = q.get(timeout=300)

@@ -193,7 +193,7 @@ def test_pool_spares_serve_growth(dev):
     next growth of that class (the policy's new block) is served by the spare,
     and the bytes are the new holder's (fenced, writable)."""
     import time
-    pool = dev.DevicePool(0, "autoscale", floor_bytes=0.0)
+    pool = dev.DevicePool(0, "autoscale", floor_bytes=0.0, spare_cap_bytes=4 << 30)
     a = pool.allocate(32 << 20)
     deadline = time.time() + 5
     while pool.spares_mapped < 1 and time.time() < deadline:
@@ -216,7 +216,7 @@ def test_pool_spare_is_rounded_up_and_serves_nearby_classes(dev):
     granule); a later growth of any class in (32, 64] MB takes it instead of
     mapping on the request path."""
     import time
-    pool = dev.DevicePool(0, "autoscale", floor_bytes=0.0)
+    pool = dev.DevicePool(0, "autoscale", floor_bytes=0.0, spare_cap_bytes=4 << 30)
     a = pool.allocate(40 << 20)
     deadline = time.time() + 5
     while pool.spares_mapped < 1 and time.time() < deadline:
@@ -230,4 +230,36 @@ def test_pool_spare_is_rounded_up_and_serves_nearby_classes(dev):
     assert int(t.float().mean()) == 5
     pool.free(a)
     pool.free(b)
+    pool.close()
+
+
+def test_pool_arenas_map_rarely_and_trim_when_idle(dev, monkeypatch):
+    """Blocks are ranges of arenas: growth inside the reservation maps nothing,
+    growth past it maps one arena (not one per block), a freed range is reused,
+    and only an unused, unreserved arena is unmapped by the idle trim — its id
+    reported to the unmap listeners (daemon clients drop their import)."""
+    monkeypatch.setenv("FT_POOL_ARENA_BYTES", str(256 << 20))
+    pool = dev.DevicePool(0, "autoscale", floor_bytes=0.0, reserve_bytes=128 << 20)
+    dropped = []
+    pool.on_unmap.append(dropped.append)
+    assert pool.stats()["mapped_bytes"] == 128 << 20
+    small = [pool.allocate(2 * 10**6) for _ in range(32)]            # 32 x 2 MiB inside the reservation
+    assert pool.stats()["mapped_bytes"] == 128 << 20
+    big = [pool.allocate(64 * 10**6) for _ in range(3)]              # past it: ONE 256 MiB arena
+    assert pool.stats()["mapped_bytes"] == (128 << 20) + (256 << 20)
+    for i, b in enumerate(small + big):
+        dev.as_tensor(b.ptr, b.nbytes, 0).fill_(i % 251)
+    torch.cuda.synchronize()
+    for i, b in enumerate(small + big):
+        assert int(dev.as_tensor(b.ptr, b.nbytes, 0)[:4096].float().mean()) == i % 251
+    a, off, abytes = pool.locate(big[0])
+    assert abytes == 256 << 20 and off % (2 << 20) == 0
+    for b in big:
+        pool.free(b)
+    pool.shrink(1e9)                                                 # policy drops the idle blocks, reclaim trims
+    assert pool.stats()["mapped_bytes"] == 128 << 20 and a in dropped
+    for b in small:
+        pool.free(b)
+    pool.shrink(1e9)
+    assert pool.stats()["mapped_bytes"] == 128 << 20                 # the reservation stays
     pool.close()
