@@ -94,9 +94,13 @@ def _function(path, q, phase1, phase2):
         q.put(("err", traceback.format_exc() + repr(exc)))
 
 
-def test_function_process_through_daemon():
+def test_function_process_through_daemon(monkeypatch):
     from paper_2411_01830_b200.daemon import TubeDaemon
     from paper_2411_01830_b200.tube import FaaSTube
+    # one arena per block and no reservation: the shrink below must unmap arenas, so
+    # the client is told to drop its imports of them
+    monkeypatch.setenv("FT_POOL_RESERVE_BYTES", "0")
+    monkeypatch.setenv("FT_POOL_ARENA_BYTES", str(2 << 20))
     tube = FaaSTube(pcie_gbps=50.0, gpus=[0], pool_floor_bytes=0.0)
     path = os.path.join(tempfile.mkdtemp(), "faastube.sock")
     d = TubeDaemon(tube, path)

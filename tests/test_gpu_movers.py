@@ -252,7 +252,7 @@ def test_pool_arenas_map_rarely_and_trim_when_idle(dev, monkeypatch):
     torch.cuda.synchronize()
     for i, b in enumerate(small + big):
         assert int(dev.as_tensor(b.ptr, b.nbytes, 0)[:4096].float().mean()) == i % 251
-    a, off, abytes = pool.locate(big[0])
+    a, off, abytes = pool.locate(big[-1])              # (big[0] still fit in the reservation)
     assert abytes == 256 << 20 and off % (2 << 20) == 0
     for b in big:
         pool.free(b)
