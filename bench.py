@@ -601,32 +601,6 @@ def run_ours(args):
         if i >= args.warmup:
             e2e.append(time.perf_counter() - t0)
     assert digest == ref_digest, "e2e digest mismatch"
-    # the same steps back to back, two in flight: step i's digest is read back (D2H)
-    # after step i+1 has been issued, so the host work and the digest of one step
-    # overlap the next step's PCIe leg (a stream of requests, not one at a time)
-    fps = [fp, dev.Fingerprint(peer)]
-    pend = None
-    t_pipe = time.perf_counter()
-    for i in range(args.warmup + args.steps):
-        if i == args.warmup:
-            t_pipe = time.perf_counter()
-        out = nxt
-        d_in = tube.unique_id()
-        tube.store(d_in, host_in, producer="decode")
-        tube.fetch(d_in, device=g, out=out, consumer="producer")
-        nxt = tube.empty((nbytes,), torch.uint8, device=g)
-        did = tube.unique_id()
-        tube.store(did, out, producer="producer")
-        del out
-        with torch.cuda.stream(sp):
-            view = tube.fetch(did, device=peer, consumer="consumer")
-            fps[i & 1].launch(view.data_ptr(), nbytes, sp)
-        del view
-        if pend is not None:
-            assert fps[pend & 1].value() == ref_digest, "pipelined e2e digest mismatch"
-        pend = i
-    assert fps[pend & 1].value() == ref_digest, "pipelined e2e digest mismatch"
-    e2e_pipe_s = (time.perf_counter() - t_pipe) / args.steps
     del nxt
     prod_out = torch.empty_like(x)
     e2e_copy = []
@@ -702,9 +676,7 @@ def run_ours(args):
                     "step_ms_p50": round(nearest_rank(sorted(e2e), 50) * 1e3, 4),
                     "step_ms_p99": round(nearest_rank(sorted(e2e), 99) * 1e3, 4),
                     "pcie_gbps_pacer": pcie_pacer,
-                    "pipelined": {"desc": "same steps, two in flight (step i's digest read after step i+1 is "
-                                          "issued)", "value": round(world * nbytes / e2e_pipe_s / 1e9, 3),
-                                  "step_ms": round(e2e_pipe_s * 1e3, 4)},
+
                     "copy_semantics": {"path": "same, producer's own output buffer and the consumer's input "
                                                "buffer (store snapshot + fetch copy)",
                                        "value": round(nbytes / statistics.mean(e2e_copy) / 1e9, 3),

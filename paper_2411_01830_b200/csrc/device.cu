@@ -253,7 +253,10 @@ __global__ void __launch_bounds__(kBulkThreads) k_copy_bulk(uint8_t* __restrict_
 // Vector engine (also the peer-safe engine): 16-byte loads/stores, UNROLL
 // independent requests in flight per thread, grid-stride. `bytes` multiple
 // of 16 and both pointers 16-byte aligned.
-template <int UNROLL>
+// STREAM: .cs (evict-first) loads/stores for large copies that must not displace
+// the L2; small copies use plain ones (0.3-0.6 us less per 1 MiB launch on B200,
+// profiles/r02/probe_small.txt)
+template <int UNROLL, bool STREAM = true>
 __global__ void __launch_bounds__(512) k_copy_vec(int4* __restrict__ dst, const int4* __restrict__ src,
                                                   uint64_t n16) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -261,11 +264,21 @@ __global__ void __launch_bounds__(512) k_copy_vec(int4* __restrict__ dst, const 
   for (; i + (UNROLL - 1) * stride < n16; i += UNROLL * stride) {
     int4 v[UNROLL];
 #pragma unroll
-    for (int u = 0; u < UNROLL; ++u) v[u] = __ldcs(src + i + u * stride);
+    for (int u = 0; u < UNROLL; ++u) v[u] = STREAM ? __ldcs(src + i + u * stride) : src[i + u * stride];
 #pragma unroll
-    for (int u = 0; u < UNROLL; ++u) __stcs(dst + i + u * stride, v[u]);
+    for (int u = 0; u < UNROLL; ++u) {
+      if (STREAM)
+        __stcs(dst + i + u * stride, v[u]);
+      else
+        dst[i + u * stride] = v[u];
+    }
   }
-  for (; i < n16; i += stride) __stcs(dst + i, __ldcs(src + i));
+  for (; i < n16; i += stride) {
+    if (STREAM)
+      __stcs(dst + i, __ldcs(src + i));
+    else
+      dst[i] = src[i];
+  }
 }
 
 // Many segments in one launch (batched small-message passing): the launch is
@@ -595,8 +608,8 @@ int launch_vec(uint8_t* dst, const uint8_t* src, uint64_t bytes, int device, cud
   uint64_t n16 = bytes / 16;
   if (grid <= 0 && bytes <= kVecWide) {
     uint64_t ctas = (n16 + 256 * 2 - 1) / (256 * 2);
-    k_copy_vec<2><<<(int)(ctas ? ctas : 1), 256, 0, st>>>(reinterpret_cast<int4*>(dst),
-                                                          reinterpret_cast<const int4*>(src), n16);
+    k_copy_vec<2, false><<<(int)(ctas ? ctas : 1), 256, 0, st>>>(reinterpret_cast<int4*>(dst),
+                                                                 reinterpret_cast<const int4*>(src), n16);
     CU_RT(cudaGetLastError());
     return FT_OK;
   }
