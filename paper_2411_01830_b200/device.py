@@ -17,6 +17,7 @@ kernels or on the copy engines.
 from __future__ import annotations
 
 import ctypes as C
+import itertools
 import os
 import threading
 import weakref
@@ -83,12 +84,17 @@ def destroy_stream(stream: torch.cuda.ExternalStream):
     LIB.ft_stream_destroy(C.c_void_p(stream.cuda_stream))
 
 
+# every event record (and the seq it gets) happens under this lock, so a later seq
+# on a stream is a later record there — wait dedup relies on it (_needed)
+REC_LOCK = threading.Lock()
+
+
 class Ev:
     """A raw CUDA event (libfaastube ``ft_event_*``): request-path stream
     ordering without torch.cuda.Event objects. Destroyed with the object
     (CUDA defers the destruction of an event still pending)."""
 
-    __slots__ = ("h", "device", "rec", "__weakref__")
+    __slots__ = ("h", "device", "rec", "stream", "seq", "__weakref__")
     # handles of dropped events, per device, reused by new ones: a request makes
     # several (ready, fences) and create + destroy cost ~2 us of driver time each.
     # Reuse is safe: a wait already enqueued on a stream captured the old record.
@@ -97,8 +103,12 @@ class Ev:
     _free: dict = {}
     _FREE_MAX = 1024
 
+    _seq = itertools.count(1)        # record order (a later record on a stream covers earlier ones)
+
     def __init__(self, device: int):
         self.rec = False
+        self.stream = None
+        self.seq = 0
         free = Ev._free.get(device)
         if free:
             try:
@@ -116,9 +126,16 @@ class Ev:
         return self.h
 
     def record(self, stream):
-        LIB.ft_event_record(C.c_void_p(self.h), C.c_void_p(stream_ptr(stream)))
-        self.rec = True
+        sp = stream_ptr(stream)
+        with REC_LOCK:
+            LIB.ft_event_record(C.c_void_p(self.h), C.c_void_p(sp))
+            self._recorded_on(sp)
         return self
+
+    def _recorded_on(self, sp: int):
+        """Mark recorded on stream ``sp``; callers hold REC_LOCK around the record
+        call and this, so ``seq`` follows the order of the records."""
+        self.rec, self.stream, self.seq = True, sp, next(Ev._seq)
 
     def wait(self, stream):
         """``stream`` waits for the work this event captured."""
@@ -166,21 +183,42 @@ def copy_batch(segments, device: int, stream=None):
     LIB.ft_copy_batch(C.cast(arr, C.POINTER(SegmentC)), len(segments), int(device), C.c_void_p(stream_ptr(stream)))
 
 
+def _needed(stream: int, events) -> list:
+    """The waits ``stream`` needs for ``events``: none for one recorded on the
+    stream itself (stream order), and per other stream only the newest record
+    (it covers that stream's earlier ones)."""
+    last = {}
+    for e in events:
+        if e is None:
+            continue
+        e._recorded()
+        if e.stream == stream and stream is not None:
+            continue
+        k = e.stream if e.stream is not None else id(e)
+        cur = last.get(k)
+        if cur is None or e.seq > cur.seq:
+            last[k] = e
+    return [e.h for e in last.values()]
+
+
 def wait_events(stream, events):
-    evs = [e._recorded() for e in events if e is not None]
+    sp = stream_ptr(stream)
+    evs = _needed(sp, events)
     if evs:
-        LIB.ft_stream_wait_events(C.c_void_p(stream_ptr(stream)), (C.c_void_p * len(evs))(*evs), len(evs))
+        LIB.ft_stream_wait_events(C.c_void_p(sp), (C.c_void_p * len(evs))(*evs), len(evs))
 
 
 def copy_ordered(dst_ptr: int, src_ptr: int, nbytes: int, device: int, stream, hints: int = 0, waits=(),
                  done: "Ev | None" = None):
     """One call: ``stream`` waits on ``waits``, TMA-bulk copy with L2 ``hints``, record ``done``."""
-    evs = [e._recorded() for e in waits if e is not None]
-    LIB.ft_copy_ordered(C.c_void_p(dst_ptr), C.c_void_p(src_ptr), int(nbytes), int(device),
-                        C.c_void_p(stream_ptr(stream)), int(hints), (C.c_void_p * max(1, len(evs)))(*evs),
-                        len(evs), C.c_void_p(done.h if done is not None else None))
-    if done is not None:
-        done.rec = True
+    sp = stream_ptr(stream)
+    evs = _needed(sp, waits)
+    with REC_LOCK:
+        LIB.ft_copy_ordered(C.c_void_p(dst_ptr), C.c_void_p(src_ptr), int(nbytes), int(device),
+                            C.c_void_p(sp), int(hints), (C.c_void_p * max(1, len(evs)))(*evs),
+                            len(evs), C.c_void_p(done.h if done is not None else None))
+        if done is not None:
+            done._recorded_on(sp)
 
 
 class _Mem:
@@ -485,14 +523,14 @@ class DevicePool:
         """The same-GPU put in one native call (``ft_store_local``): the stream
         waits on the block's fences, copies the output into it, records
         ``ready``; index entry + histogram sample. Returns (R_window, last | None)."""
-        evs = [e._recorded() for e in blk.fences if e is not None]
-        with self._lock:
+        evs = _needed(stream, blk.fences)
+        with self._lock, REC_LOCK:
             LIB.ft_store_local(index._h, self.policy._h, int(data_id), int(node), self.device, float(nbytes),
                                float(now_ms), self._enc(producer), int(bool(response)), float(concurrency),
                                C.c_void_p(blk.ptr), C.c_void_p(src_ptr), C.c_void_p(stream), int(hints),
                                (C.c_void_p * max(1, len(evs)))(*evs), len(evs), C.c_void_p(ready.h),
                                self._rw, self._last)
-            ready.rec = True
+            ready._recorded_on(stream)
             blk.fences = ()                  # the copy waited on them
             rw, last = self._rw.value, self._last.value
         return rw, (None if last != last else last)
@@ -503,14 +541,14 @@ class DevicePool:
         (``ft_fetch_local``): wait ``waits``, copy, record ``done``; with
         ``retire`` the index entry goes and the block returns to the policy,
         fenced on ``done`` + ``fences``. Returns (R_window, last | None)."""
-        evs = [e._recorded() for e in waits if e is not None]
-        with self._lock:
+        evs = _needed(stream, waits)
+        with self._lock, REC_LOCK:
             LIB.ft_fetch_local(index._h, self.policy._h, int(data_id),
                                blk.policy_block.block_id if retire else -1, self._enc(producer), int(retire),
                                C.c_void_p(dst_ptr), C.c_void_p(blk.ptr), int(nbytes), self.device,
                                C.c_void_p(stream), int(hints), (C.c_void_p * max(1, len(evs)))(*evs), len(evs),
                                C.c_void_p(done.h), self._rw, self._last)
-            done.rec = True
+            done._recorded_on(stream)
             if retire:
                 blk.policy_block.in_use = False
                 self._fences[blk.policy_block.block_id] = (done,) + tuple(fences)
