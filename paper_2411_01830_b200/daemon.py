@@ -101,7 +101,7 @@ class _Pin:
 
 
 class _Conn:
-    __slots__ = ("ch", "tokens", "mapped", "drop", "gpu", "stream", "mine", "peer", "served")
+    __slots__ = ("ch", "tokens", "mapped", "drop", "gpu", "stream", "mine", "peer", "served", "seen")
 
     def __init__(self, ch):
         self.ch = ch
@@ -113,6 +113,7 @@ class _Conn:
         self.mine = None         # dev.IpcEventRing (the daemon's events, exported to the client)
         self.peer = None         # dev.PeerEvents (the client's events)
         self.served = 0          # messages handled (acknowledged in every reply)
+        self.seen = 0            # messages received
 
     def ctx(self):
         """Request handling runs on the connection's private stream (after hello)."""
@@ -212,11 +213,13 @@ class TubeDaemon:
         try:
             while True:
                 msg = ch.recv_msg()
+                conn.seen += 1
                 try:
                     with conn.ctx():
                         self._handle(conn, msg)
                 except Exception as exc:  # noqa: BLE001 - the error travels back to the caller
                     if msg.get("op") == "done":        # fire-and-forget: nobody waits for a reply
+                        conn.served = max(conn.served, conn.seen)
                         continue
                     conn.served += 1
                     ch.send_msg({"ok": False, "error": type(exc).__name__, "msg": str(exc), "acked": conn.served})
@@ -527,12 +530,13 @@ class TubeClient:
             cur = torch.cuda.current_stream(self.device)
         self._after_daemon(rep, cur)                  # the block's previous users are done
         dev.copy(ptr, t.data_ptr(), n, self.device, cur)
-        ev = self._mark(cur)                          # written (or synchronised) before the daemon publishes it
         if t is not output or self._mine is None:
             t.record_stream(cur)
-        rep = self._call({"op": "commit", "token": rep["token"], "id": data_id, "dtype": str(t.dtype),
-                          "shape": list(t.shape), "producer": producer, "consumers": consumers,
-                          "response": response, "ev": ev, **({"next": n} if self._mine is not None else {})})
+        with self._io:                                # the mark rides on the very next message
+            ev = self._mark(cur)                      # written (or synchronised) before the daemon publishes it
+            rep = self._call({"op": "commit", "token": rep["token"], "id": data_id, "dtype": str(t.dtype),
+                              "shape": list(t.shape), "producer": producer, "consumers": consumers,
+                              "response": response, "ev": ev, **({"next": n} if self._mine is not None else {})})
         if rep.get("loan"):
             self._mapped(rep)
             self._loans[n] = rep
@@ -573,7 +577,8 @@ class TubeClient:
                 weakref.finalize(owner, self._release, rep["token"])
                 return dev.as_tensor(ptr, n, self.device, dt, tuple(shape), owner=owner)
             dev.copy(out.data_ptr(), ptr, n, self.device, cur)
-            self._send({"op": "done", "token": rep["token"], "ev": self._mark(cur)})
+            with self._io:
+                self._send({"op": "done", "token": rep["token"], "ev": self._mark(cur)})
             return out
         # host-synced connection: copy on the private stream, synchronise, release
         if out is None:
@@ -592,7 +597,8 @@ class TubeClient:
             return
         try:
             cur = torch.cuda.current_stream(self.device)
-            self._send({"op": "done", "token": token, "ev": self._mark(cur)})
+            with self._io:
+                self._send({"op": "done", "token": token, "ev": self._mark(cur)})
         except Exception:  # noqa: BLE001 - the daemon drops a dead connection's loans itself
             pass
 

@@ -228,3 +228,58 @@ def test_dead_client_loans_return_to_the_pool():
     d.close()
     assert not d._acceptor.is_alive()
     tube.close()
+
+
+def _views_and_loans(path, q):
+    sys.path.insert(0, ROOT)
+    try:
+        from paper_2411_01830_b200.daemon import TubeClient
+        c = TubeClient(path, 0)
+        n = 3 * 10**6 + 5
+        a = payload(n, 1).cuda()
+        did = c.unique_id()
+        c.store(did, a)
+        v = c.fetch(did)                                    # zero-copy view of the stored block (last consumer)
+        sent0 = c._sent
+        for k in range(20):                                 # same size: lent blocks, never the viewed one
+            d = c.unique_id()
+            c.store(d, payload(n, 100 + k).cuda())
+            w = c.fetch(d)
+            assert torch.equal(w, payload(n, 100 + k).cuda()), k
+            del w
+        per_store = (c._sent - sent0) / 20                  # unique_id + commit + fetch + done (+ no alloc)
+        torch.cuda.synchronize()
+        ok_view = torch.equal(v, a)                          # untouched while alive
+        derived = v[7:1000].clone()
+        del v                                                # release -> the daemon may reuse the block
+        q.put(("ok", {"ok_view": ok_view, "derived": torch.equal(derived, a[7:1000]), "per_store": per_store,
+                      "acked": c._acked, "sent": c._sent}))
+        c.close()
+    except Exception as exc:  # noqa: BLE001
+        import traceback
+        q.put(("err", traceback.format_exc() + repr(exc)))
+
+
+def test_zero_copy_views_and_lent_blocks():
+    """A client's zero-copy view pins the stored block until the last tensor
+    over it dies (later same-size stores, served from lent blocks, never land
+    in it); a steady producer needs no alloc round trip (the commit reply lends
+    the next block); every message is acknowledged (IPC-event ring reuse)."""
+    from paper_2411_01830_b200.daemon import TubeDaemon
+    from paper_2411_01830_b200.tube import FaaSTube
+    tube = FaaSTube(pcie_gbps=50.0, gpus=[0], pool_floor_bytes=0.0)
+    path = os.path.join(tempfile.mkdtemp(), "faastube.sock")
+    d = TubeDaemon(tube, path)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_views_and_loans, args=(path, q))
+    p.start()
+    status, res = q.get(timeout=300)
+    p.join(timeout=60)
+    assert status == "ok", res
+    assert res["ok_view"] and res["derived"], res
+    assert res["per_store"] <= 4.0, res
+    assert res["acked"] >= res["sent"] - 1, res
+    d.close()
+    assert tube._accounts_consistent()
+    tube.close()
