@@ -424,6 +424,20 @@ def run_ours(args):
     def delivered():
         return torch.equal(inp.view(torch.uint8).to(x.device), x.view(torch.uint8))
 
+    cross_error = None
+    if cross:
+        # the first cross-GPU pass on this box: if the peer path cannot run at all (no P2P,
+        # a driver error), say so in the line and measure same-GPU replicas instead of
+        # printing nothing; wrong bytes are not excused (they fail below)
+        try:
+            one_pass()
+            torch.cuda.synchronize(g)
+            torch.cuda.synchronize(peer)
+        except Exception as exc:  # noqa: BLE001
+            import traceback
+            cross_error = (repr(exc) + " " + traceback.format_exc()[-300:])[:600]
+            peer, cross, sp, flush_p = g, False, s, None
+            inp = torch.empty(PAYLOAD_SHAPE, dtype=torch.float16, device=f"cuda:{g}")
     # ---- warm-up (>= W passes and >= 0.5 s under the clock sampler), then K timed passes
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -666,7 +680,8 @@ def run_ours(args):
                        "parallelism": (f"replicas x{world}" if not cross else
                                        f"ring of {world} producer->consumer pairs (rank r: GPU r -> GPU r+1), "
                                        "one process and one tube per pair"),
-                       "moved_per_step": {k: v // max(1, args.steps) for k, v in moved.items()}},
+                       "moved_per_step": {k: v // max(1, args.steps) for k, v in moved.items()},
+                       **({"cross_gpu_error": cross_error} if cross_error else {})},
             "p50_pass_ms": round(nearest_rank(per_ms, 50), 5), "p99_pass_ms": round(nearest_rank(per_ms, 99), 5),
             "e2e": {"value": round(world * nbytes / e2e_max / 1e9, 3), "unit": "GB/s",
                     "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": 16,

@@ -1,8 +1,8 @@
 """The N>1 bench path (bench.py under torchrun: a ring of producer->consumer
-pairs, each rank's pool block exported to the next rank, pulled with the K1
-engine, ordered by bounded device doorbells) run with 2 ranks on the one GPU
-of the test box: both ranks finish, the delivered bytes are checked inside
-(pair.check), and rank 0 prints one JSON line with the whole-job value."""
+pairs, rank r storing on GPU r and fetching into GPU r+1 through its own tube)
+run with 2 ranks on the one GPU of the test box (both pairs then land on the
+same GPU): both ranks finish, the delivered bytes are checked inside, and
+rank 0 prints one JSON line with the whole-job value."""
 
 import json
 import os
@@ -25,4 +25,4 @@ def test_two_rank_ring_on_one_gpu():
     assert len(lines) == 1, r.stdout[-2000:]
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["steps"] == 10
-    assert "cross_gpu_setup_error" not in d["config"], d["config"]
+    assert "cross_gpu_error" not in d["config"], d["config"]
