@@ -103,6 +103,8 @@ class FaaSTube:
         if self.topo.gpu_count > n:
             raise ValueError(f"topology has {self.topo.gpu_count} GPUs but only {n} are visible")
         self.strategy = strategy_preset(strategy) if isinstance(strategy, str) else strategy
+        self._gpu_store = bool(self.strategy.gpu_store())
+        self._so_cache = {}          # (gpu, raw stream pointer) -> torch stream object
         self.node = node
         self.chunk_bytes, self.batch_chunks = int(chunk_bytes), int(batch_chunks)
         self.matrix = snapshot_matrix(self.topo)
@@ -233,6 +235,15 @@ class FaaSTube:
         """Raw pointer of the caller's current stream on GPU ``g``."""
         return dev.current_stream(g)
 
+    def _torch_stream(self, g):
+        """The caller's current stream on GPU ``g`` as a torch stream object (for
+        ``record_stream``), cached by raw pointer (building one costs ~1.5 us)."""
+        key = (g, dev.current_stream(g))
+        st = self._so_cache.get(key)
+        if st is None:
+            st = self._so_cache[key] = torch.cuda.current_stream(g)
+        return st
+
     @staticmethod
     def _stripes(nbytes, shares):
         """Integer byte ranges for fractional shares (dataplane.py:215/288)."""
@@ -276,20 +287,20 @@ class FaaSTube:
         # can take milliseconds and must not stall other tenants' calls)
         t0 = time.perf_counter()
         pre_host = pre_blk = None
-        if output.is_cuda and (response or not self.strategy.gpu_store()):
+        if output.is_cuda and (response or not self._gpu_store):
             pre_host = self._pinned(output.nbytes)
-        if output.is_cuda and self.strategy.gpu_store():
+        if output.is_cuda and self._gpu_store:
             fb = getattr(output, "_ft_block", None)
             if fb is None or fb.ptr != output.data_ptr():
                 # the pool block for the snapshot: growth maps physical memory, which
                 # must not happen under the tube lock
-                pre_blk = self.pools[output.device.index].allocate(output.nbytes)
+                pre_blk = self.pools[output.get_device()].allocate(output.nbytes)
         t1 = time.perf_counter()
         try:
             stage = self._store_locked(data_id, output, response, producer, consumers, queue_pos, pre_host, pre_blk)
         except BaseException:
             if pre_blk is not None:
-                self.pools[output.device.index].free(pre_blk, list(pre_blk.fences))
+                self.pools[output.get_device()].free(pre_blk, list(pre_blk.fences))
             raise
         t2 = time.perf_counter()
         if stage is not None:
@@ -325,8 +336,8 @@ class FaaSTube:
             self._last_op_ms = now = self.now_ms()
             obj = _Obj(data_id, nbytes, t.dtype, tuple(t.shape), None, producer, consumers, now)
             obj.queue_pos = queue_pos if queue_pos is not None else next(self._queue)
-            if t.is_cuda and self.strategy.gpu_store():
-                g = t.device.index
+            if t.is_cuda and self._gpu_store:
+                g = t.get_device()
                 obj.gpu = obj.home = g
                 pool = self.pools[g]
                 blk = getattr(t, "_ft_block", None)
@@ -342,7 +353,7 @@ class FaaSTube:
                     obj.block = blk
                     # snapshot on the producer's stream: ordered after the kernels that
                     # wrote the output AND before any later kernel that overwrites it
-                    so = torch.cuda.current_stream(g)
+                    so = self._torch_stream(g)
                     # stream the producer's output through L2 (evict_first); the block itself is
                     # written with the normal policy — pinning it (evict_last) for the fetch
                     # measured 5% slower per pass (tools/sweep_hints.py: 37.9 vs 35.8 us)
