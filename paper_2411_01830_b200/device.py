@@ -353,16 +353,21 @@ class DevicePool:
         # arena covers the common working set (a new one is mapped only when none has
         # room, and unused ones are unmapped only when the GPU is quiet — reclaim())
         if reserve_bytes is None:
-            reserve_bytes = int(os.environ.get("FT_POOL_RESERVE_BYTES", 2 * GiB))
+            reserve_bytes = int(os.environ.get("FT_POOL_RESERVE_BYTES", 4 * GiB))
+        self.reserved_bytes = 0
         if mode != "none" and reserve_bytes > 0:
             LIB.ft_vmm_pool_reserve(h, int(reserve_bytes))
+            mapped = C.c_uint64()
+            LIB.ft_vmm_pool_stats(h, C.byref(mapped), None, None)
+            self.reserved_bytes = mapped.value
         self._mapped = {}  # policy block id -> (vmm id, ptr, bytes)
         self._fences = {}  # policy block id -> events the freed block's last users recorded
         self._bases = {}   # vmm id -> uint8 tensor over the whole mapping (zero-copy views slice it)
         # physical blocks the policy dropped, still mapped: reused by growth of the same
         # class, unmapped by reclaim() when the GPU is quiet (cuMemUnmap under load stalls
         # every CUDA call of the process for 100s of ms — measured)
-        self._released = []  # [(vmm id, ptr, bytes, fences)]
+        self._released = []  # [(vmm id, ptr, bytes, fences)]: spare mappings awaiting a holder
+        self._range_fences = []  # [(lo, hi, fences)]: ranges given back to their arenas, last users
         self._lock = threading.Lock()
         self._names = {}             # producer name -> bytes (encoded once)
         self._rw, self._last = C.c_double(), C.c_double()   # out-params of the hot calls (under _lock)
@@ -480,6 +485,7 @@ class DevicePool:
                     LIB.ft_vmm_block_map(self._h, int(b.class_bytes), C.byref(vid), C.byref(ptr))
                 with self._lock:
                     m = self._mapped[b.block_id] = (vid.value, ptr.value, b.class_bytes)
+                    fences = tuple(fences) + self._fences_over(ptr.value, b.class_bytes)
                     self.grow_events += 1
                     self._want_spare(int(b.class_bytes))
         return PoolBlock(b, m[0], m[1], m[2], self.device, fences, self)
@@ -603,11 +609,35 @@ class DevicePool:
             for b in dropped:
                 m = self._mapped.pop(b.block_id, None)
                 if m is not None:
-                    self._released.append((m[0], m[1], m[2], self._fences.pop(b.block_id, ())))
+                    # the range goes back to its arena now (no driver call); its last
+                    # users' fences stay with the range for whoever is carved there next
+                    self._release_range(m, self._fences.pop(b.block_id, ()))
             n = sum(b.class_bytes for b in dropped)
         if reclaim:
             self.reclaim()
         return n
+
+    def _release_range(self, m, fences):
+        """(lock held) Give a mapped block's range back to its arena; remember its fences."""
+        vid, ptr, nb = m
+        self._bases.pop(vid, None)
+        LIB.ft_vmm_block_unmap(self._h, vid)
+        if fences:
+            self._range_fences.append((ptr, ptr + nb, tuple(fences)))
+            if len(self._range_fences) > 256:            # drop the ranges whose users are done
+                self._range_fences = [r for r in self._range_fences if not all(e.query() for e in r[2])]
+
+    def _fences_over(self, ptr, nb) -> tuple:
+        """(lock held) Fences of released ranges a new block at [ptr, ptr+nb) overlaps."""
+        out = ()
+        for lo, hi, f in self._range_fences:
+            if lo < ptr + nb and ptr < hi:
+                out += f
+        return out
+
+    @property
+    def reclaimable(self) -> bool:
+        return bool(self._released or self._range_fences)
 
     def reclaim(self) -> int:
         """Give every released block back to its arena (after its last users'
@@ -615,7 +645,11 @@ class DevicePool:
         back to the driver. Returns the bytes of the released blocks."""
         with self._lock:
             gone, self._released = self._released, []
+            ranges, self._range_fences = self._range_fences, []
         for _vid, _ptr, _n, fences in gone:
+            for ev in fences:
+                ev.synchronize()
+        for _lo, _hi, fences in ranges:           # nothing may still touch a range of an arena to unmap
             for ev in fences:
                 ev.synchronize()
         for vid, _ptr, _n, _f in gone:
@@ -655,10 +689,7 @@ class DevicePool:
         m = self._mapped.pop(block_id, None)
         if m is None:
             return 0
-        for ev in self._fences.pop(block_id, ()):  # no in-flight kernel may touch it
-            ev.synchronize()
-        self._bases.pop(m[0], None)
-        LIB.ft_vmm_block_unmap(self._h, m[0])            # back to its arena (no driver call)
+        self._release_range(m, self._fences.pop(block_id, ()))   # back to its arena (no driver call)
         return m[2]
 
     def export_fd(self, blk: PoolBlock) -> int:

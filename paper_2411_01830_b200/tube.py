@@ -211,7 +211,7 @@ class FaaSTube:
                     due.add(heapq.heappop(self._shrink_due)[1])
                 if not due:
                     wait = (self._shrink_due[0][0] - now) / 1e3 if self._shrink_due else 0.1
-                    if any(p.released_bytes for p in self.pools.values()):
+                    if any(p.reclaimable for p in self.pools.values()):
                         wait = min(wait, RECLAIM_IDLE_MS / 1e3)
                     self._maint_cv.wait(min(0.1, max(0.001, wait)))
                     continue
@@ -227,7 +227,7 @@ class FaaSTube:
         the GPU is busy; growth meanwhile reuses parked blocks of its class)."""
         if now - self._last_op_ms >= RECLAIM_IDLE_MS:
             for p in self.pools.values():
-                if p.released_bytes:
+                if p.reclaimable or p.stats()["mapped_bytes"] > p.reserved_bytes:
                     p.reclaim()
 
     @staticmethod
