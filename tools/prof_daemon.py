@@ -1,0 +1,153 @@
+"""Where a function process's put/get through the daemon spends its time:
+transport ping (unique_id round trip), client-side segments of store/fetch,
+daemon-side handler time per op, and the CUDA cost of interprocess vs plain
+event records/waits.   python tools/prof_daemon.py"""
+import multiprocessing as mp
+import os
+import statistics
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def med(xs):
+    return round(1e6 * statistics.median(xs), 1) if xs else None
+
+
+def client(path, q):
+    sys.path.insert(0, ROOT)
+    import torch
+    from paper_2411_01830_b200 import device as dev
+    from paper_2411_01830_b200.daemon import TubeClient
+    c = TubeClient(path, 0)
+    res = {}
+    ping = []
+    for i in range(500):
+        t0 = time.perf_counter()
+        c.unique_id()
+        ping.append(time.perf_counter() - t0)
+    res["ping_unique_id_us"] = med(ping[50:])
+    x = torch.randint(0, 256, (1 << 20,), dtype=torch.uint8, device="cuda:0")
+    out = torch.empty_like(x)
+    st, ft, vt = [], [], []
+    for i in range(300):
+        did = c.unique_id()
+        t0 = time.perf_counter()
+        c.store(did, x)
+        t1 = time.perf_counter()
+        c.fetch(did, out=out)
+        t2 = time.perf_counter()
+        did = c.unique_id()
+        c.store(did, x)
+        t3 = time.perf_counter()
+        v = c.fetch(did)
+        t4 = time.perf_counter()
+        del v
+        if i >= 50:
+            st.append(t1 - t0)
+            ft.append(t2 - t1)
+            vt.append(t4 - t3)
+    res["store_us"], res["fetch_out_us"], res["fetch_view_us"] = med(st), med(ft), med(vt)
+    # CUDA cost of the ordering primitives in this process
+    s = torch.cuda.current_stream(0).cuda_stream
+    ring = dev.IpcEventRing(0, 4)
+    plain = dev.Ev(0)
+    rec_ipc, rec_plain, wait_ipc, wait_plain, copy = [], [], [], [], []
+    for i in range(500):
+        t0 = time.perf_counter()
+        ring.record(i % 4, s)
+        t1 = time.perf_counter()
+        plain.record(s)
+        t2 = time.perf_counter()
+        dev.wait_events(s, [ring.h[i % 4]]) if False else dev.LIB.ft_stream_wait_events(
+            dev.C.c_void_p(s), (dev.C.c_void_p * 1)(ring.h[i % 4]), 1)
+        t3 = time.perf_counter()
+        plain.wait(s)
+        t4 = time.perf_counter()
+        dev.copy(out.data_ptr(), x.data_ptr(), 4096, 0, s)
+        t5 = time.perf_counter()
+        rec_ipc.append(t1 - t0)
+        rec_plain.append(t2 - t1)
+        wait_ipc.append(t3 - t2)
+        wait_plain.append(t4 - t3)
+        copy.append(t5 - t4)
+    torch.cuda.synchronize()
+    res["cuda_us"] = {"record_ipc": med(rec_ipc), "record_plain": med(rec_plain), "wait_ipc": med(wait_ipc),
+                      "wait_plain": med(wait_plain), "copy_4k_launch": med(copy)}
+    import msgpack
+    m = {"op": "commit", "token": 12, "id": 99, "dtype": "torch.uint8", "shape": [1 << 20], "producer": "func",
+         "consumers": 1, "response": False, "ev": 3, "next": 1 << 20}
+    pk, up = [], []
+    for i in range(2000):
+        t0 = time.perf_counter()
+        b = msgpack.packb(m)
+        t1 = time.perf_counter()
+        msgpack.unpackb(b)
+        t2 = time.perf_counter()
+        pk.append(t1 - t0)
+        up.append(t2 - t1)
+    res["msgpack_us"] = {"pack": med(pk), "unpack": med(up)}
+    c.close()
+    q.put(res)
+
+
+def main():
+    import torch
+    from paper_2411_01830_b200.daemon import TubeDaemon
+    from paper_2411_01830_b200.tube import FaaSTube
+    tube = FaaSTube(pcie_gbps=55.0, gpus=[0])
+    path = os.path.join(tempfile.mkdtemp(), "faastube.sock")
+    d = TubeDaemon(tube, path)
+    times = {}
+    orig = d._handle
+
+    def timed(conn, msg):
+        t0 = time.perf_counter()
+        try:
+            return orig(conn, msg)
+        finally:
+            times.setdefault(msg["op"], []).append(time.perf_counter() - t0)
+    d._handle = timed
+    ost, ofe = tube.store, tube.fetch_resident
+    tin = {"tube.store": [], "tube.fetch_resident": [], "tube.empty": []}
+
+    def st(*a, **k):
+        t0 = time.perf_counter()
+        try:
+            return ost(*a, **k)
+        finally:
+            tin["tube.store"].append(time.perf_counter() - t0)
+
+    def fr(*a, **k):
+        t0 = time.perf_counter()
+        try:
+            return ofe(*a, **k)
+        finally:
+            tin["tube.fetch_resident"].append(time.perf_counter() - t0)
+    oem = tube.empty
+
+    def em(*a, **k):
+        t0 = time.perf_counter()
+        try:
+            return oem(*a, **k)
+        finally:
+            tin["tube.empty"].append(time.perf_counter() - t0)
+    tube.store, tube.fetch_resident, tube.empty = st, fr, em
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=client, args=(path, q))
+    p.start()
+    res = q.get(timeout=300)
+    p.join(timeout=60)
+    res["daemon_handler_us"] = {k: med(v[50:]) for k, v in times.items()}
+    res["daemon_tube_us"] = {k: med(v[50:]) for k, v in tin.items()}
+    print(res)
+    d.close()
+    tube.close()
+
+
+if __name__ == "__main__":
+    main()
