@@ -44,7 +44,8 @@ enum ft_status {
   FT_E_TRUNCATED = 9,     /* caller buffer too small */
   FT_E_KEY = 10,          /* KeyError (unknown id / func) */
   FT_E_NOT_SUPPORTED = 11, /* feature unavailable on this device/driver */
-  FT_E_TIMEOUT = 12        /* a host wait ran out of time */
+  FT_E_TIMEOUT = 12,       /* a host wait ran out of time */
+  FT_E_CLOSED = 13         /* the peer closed the function<->daemon channel */
 };
 
 #define FT_MAX_PATH 8   /* GPUs per NVLink path (MAX_HOPS 4 => 5)  nvlink_sched.py:17 */
@@ -335,6 +336,18 @@ int ft_ipc_event_create(int device, void** ev, void* handle64);
 int ft_ipc_event_open(int device, const void* handle64, void** ev);
 int ft_fd_send(int sock, int fd, uint64_t tag);
 int ft_fd_recv(int sock, int* fd, uint64_t* tag);
+/* shared-memory message channel between a function process and the daemon
+ * (PAPER.md:568 fast local channel; replaces the reference's in-process calls of
+ * engine.py:342-511 by a cross-process request/reply): two SPSC rings of
+ * `slots` slots of `slot_bytes` (dir 0 requests, dir 1 replies) in a memfd the
+ * creator passes to the peer (SCM_RIGHTS). recv spins `spin_us`, then sleeps
+ * on a futex; timeouts in us (<0: none). FT_E_CLOSED once the peer closed. */
+typedef struct ft_chan ft_chan;
+int ft_chan_create(uint32_t slot_bytes, uint32_t slots, int* memfd, ft_chan** out);
+int ft_chan_attach(int memfd, ft_chan** out);
+int ft_chan_send(ft_chan* c, int dir, const void* buf, uint32_t n, int64_t timeout_us);
+int ft_chan_recv(ft_chan* c, int dir, void* buf, uint32_t cap, uint32_t* n, int64_t spin_us, int64_t timeout_us);
+int ft_chan_close(ft_chan* c);
 
 /* ---- movers
  * K1/K3 ft_copy: SM-driven bulk copy (TMA cp.async.bulk global->smem->global,

@@ -80,6 +80,7 @@ _ERRORS = {
     10: KeyError,
     11: NotSupported,
     12: WaitTimeout,
+    13: ConnectionError,
 }
 
 i32, i64, u64, dbl, sz = C.c_int32, C.c_int64, C.c_uint64, C.c_double, C.c_size_t
@@ -239,6 +240,11 @@ _SIGS = {
     "ft_ipc_event_open": (None, [C.c_int, C.c_char_p, P(vp)]),
     "ft_fd_send": (None, [C.c_int, C.c_int, u64]),
     "ft_fd_recv": (None, [C.c_int, P(C.c_int), P(u64)]),
+    "ft_chan_create": (None, [C.c_uint32, C.c_uint32, P(C.c_int), P(vp)]),
+    "ft_chan_attach": (None, [C.c_int, P(vp)]),
+    "ft_chan_send": (None, [vp, C.c_int, C.c_char_p, C.c_uint32, i64]),
+    "ft_chan_recv": (None, [vp, C.c_int, vp, C.c_uint32, P(C.c_uint32), i64, i64]),
+    "ft_chan_close": (None, [vp]),
     "ft_copy": (None, [vp, vp, u64, C.c_int, vp]),
     "ft_copy_ex": (None, [vp, vp, u64, C.c_int, vp, C.c_int, C.c_int]),
     "ft_copy_hint": (None, [vp, vp, u64, C.c_int, vp, C.c_uint32]),

@@ -1,12 +1,15 @@
-"""Function <-> daemon channel: AF_UNIX stream sockets carrying pool-block
-file descriptors (SCM_RIGHTS, ``ft_fd_send``/``ft_fd_recv``) plus binary
-(msgpack) messages, length-prefixed. This is the paper's fast local channel (a Linux
-pipe there) and the CUDA-IPC handoff of GPU buffers:
-bytes never cross the socket — the receiver maps the exported VMM block.
+"""Function <-> daemon channel: an AF_UNIX stream socket carrying pool-block
+file descriptors (SCM_RIGHTS, ``ft_fd_send``/``ft_fd_recv``), and binary
+(msgpack) messages over a shared-memory ring pair (``ft_chan_*``, csrc/chan.cc)
+once the client upgraded the connection. This is the paper's fast local
+channel (a Linux pipe there) and the CUDA-IPC handoff of GPU
+buffers: bytes never cross the channel — the receiver maps
+the exported VMM block.
 """
 
 from __future__ import annotations
 
+import ctypes as C
 import os
 import socket
 import struct
@@ -14,13 +17,53 @@ import struct
 import msgpack
 
 from . import device as dev
+from ._lib import LIB, raise_status
 
 _HDR = struct.Struct("<I")
 
 
+_SLOT = 8192            # bytes per ring slot (the largest message: hello's 16 x 64-byte event handles)
+_SLOTS = 16
+# a receiver spins this long for the next message before it sleeps on a futex (a
+# futex wake-up measured ~75 us in a VM, a spinning receiver ~7 us round trip)
+SPIN_US = int(os.environ.get("FT_CHAN_SPIN_US", 2000))
+_POLL_US = 200_000      # how often a blocked receiver checks that the peer is alive
+
+
 class Channel:
+    """Messages go over a shared-memory ring pair once ``upgrade`` (client) /
+    ``attach`` (daemon) ran (``ft_chan_*``); before that, and for descriptors
+    always, over the socket."""
+
     def __init__(self, sock: socket.socket):
         self.sock = sock
+        self._chan = None
+        self._dir = 0           # ring this side sends on (0: client requests, 1: daemon replies)
+        self._buf = None
+        self._n = None
+
+    def _use(self, h, send_dir):
+        self._chan, self._dir = h, send_dir
+        self._buf = C.create_string_buffer(_SLOT)
+        self._n = C.c_uint32()
+
+    def upgrade(self):
+        """Client: create the ring pair and hand it to the daemon (which attaches on ``chan``)."""
+        fd, h = C.c_int(), C.c_void_p()
+        LIB.ft_chan_create(_SLOT, _SLOTS, C.byref(fd), C.byref(h))
+        self.send_msg({"op": "chan"})
+        dev.send_fd(self.sock, fd.value, 0)
+        self._use(h, 0)
+
+    def attach(self):
+        """Daemon: map the client's ring pair (its memfd follows the ``chan`` message)."""
+        fd, _ = dev.recv_fd(self.sock)
+        h = C.c_void_p()
+        try:
+            LIB.ft_chan_attach(fd, C.byref(h))
+        finally:
+            os.close(fd)
+        self._use(h, 1)
 
     @classmethod
     def connect(cls, path: str, timeout: float = 60.0) -> "Channel":
@@ -62,11 +105,35 @@ class Channel:
 
     def send_msg(self, meta: dict):
         body = msgpack.packb(meta)
+        if self._chan is not None:
+            rc = LIB.raw("ft_chan_send")(self._chan, self._dir, body, len(body), -1)
+            if rc == 13:
+                raise ConnectionError("channel closed")
+            if rc:
+                raise_status(rc)
+            return
         self.sock.sendall(_HDR.pack(len(body)) + body)
 
-    def recv_msg(self) -> dict:
-        n = _HDR.unpack(self._recv_exact(4))[0]
-        return msgpack.unpackb(self._recv_exact(n))
+    def recv_msg(self, spin_us: int = SPIN_US) -> dict:
+        if self._chan is None:
+            n = _HDR.unpack(self._recv_exact(4))[0]
+            return msgpack.unpackb(self._recv_exact(n))
+        while True:
+            rc = LIB.raw("ft_chan_recv")(self._chan, 1 - self._dir, self._buf, _SLOT, self._n, spin_us, _POLL_US)
+            if rc == 0:
+                return msgpack.unpackb(self._buf.raw[:self._n.value])
+            if rc == 13:
+                raise ConnectionError("channel closed")
+            if rc != 12:
+                raise_status(rc)
+            self._check_peer()                        # timeout: is the peer still there?
+
+    def _check_peer(self):
+        try:
+            if self.sock.recv(1, socket.MSG_PEEK | socket.MSG_DONTWAIT) == b"":
+                raise ConnectionError("peer went away")
+        except (BlockingIOError, InterruptedError):
+            pass
 
     def _recv_exact(self, n):
         buf = self.sock.recv(n)
@@ -83,4 +150,7 @@ class Channel:
         return b"".join(parts)
 
     def close(self):
+        h, self._chan = self._chan, None
+        if h is not None:
+            LIB.ft_chan_close(h)
         self.sock.close()

@@ -100,6 +100,16 @@ class _Pin:
             rel()
 
 
+class _Lend:
+    """A pool block lent to a client for its next output (``alloc`` / a commit's
+    ``loan``) until the client commits it; returned to the pool otherwise."""
+
+    __slots__ = ("blk",)
+
+    def __init__(self, blk):
+        self.blk = blk
+
+
 class _Conn:
     __slots__ = ("ch", "tokens", "mapped", "drop", "gpu", "stream", "mine", "peer", "served", "seen")
 
@@ -192,16 +202,21 @@ class TubeDaemon:
         # a daemon-side fetch buffer, or an output block never committed (the client
         # died between alloc and commit), goes back to the pool — fenced on the
         # connection's stream, which waited for the client's last access
-        keep = getattr(t, "_ft_keep", None) if not getattr(t, "_ft_alloc", False) else t
-        del t                                  # a zero-copy view: its release fences the block
-        if keep is not None:
-            self._free(keep, conn)
+        if isinstance(t, _Lend):
+            self._free(t.blk, conn)
+        elif isinstance(t, _Pin):              # a zero-copy read: unpin, fenced on the connection's stream
+            rel, t.release = t.release, None
+            if rel is not None:
+                rel(conn.stream)
+        elif t is not None:
+            keep = getattr(t, "_ft_keep", None)
+            del t
+            if keep is not None:
+                self._free(keep._ft_block, conn)  # noqa: SLF001
 
-    def _free(self, t, conn=None):
+    def _free(self, blk, conn=None):
         """Back to the pool; with stream-ordered connections fenced on the connection's
         stream (it waited for the client's last access), else the client synchronised."""
-        blk = t._ft_block  # noqa: SLF001
-        del t
         g = blk.device
         fences = [dev.Ev(g).record(conn.stream)] if conn is not None and conn.stream is not None else []
         self.tube.pools[g].free(blk, fences)
@@ -215,8 +230,7 @@ class TubeDaemon:
                 msg = ch.recv_msg()
                 conn.seen += 1
                 try:
-                    with conn.ctx():
-                        self._handle(conn, msg)
+                    self._handle(conn, msg)
                 except Exception as exc:  # noqa: BLE001 - the error travels back to the caller
                     if msg.get("op") == "done":        # fire-and-forget: nobody waits for a reply
                         conn.served = max(conn.served, conn.seen)
@@ -266,17 +280,23 @@ class TubeDaemon:
         """A pool block for a producer's output: its previous users are fenced on
         the connection's stream, then marked (the client's stream waits on the
         mark before writing; without events the stream is synchronised)."""
-        t = self.tube.empty((max(1, n),), torch.uint8, device=g)       # pool-backed output
-        t._ft_alloc = True  # noqa: SLF001
+        blk = self.tube.lend_block(g, max(1, n))
+        # the block's previous users are done before the client writes: the connection's
+        # stream waits on them and is marked, or (no events) the device's default stream
+        # waits and is synchronised
+        blk.wait_fences(conn.stream if conn.stream is not None else 0)
         ev = conn.mark()
         if ev < 0:
-            self.tube.sync_stream(g)           # the block's previous users are done before the client writes
-        return {"token": self._hold(conn, t), "nbytes": n, "ev": ev, "_blk": t._ft_block}  # noqa: SLF001
+            self.tube.sync_stream(g)
+        return {"token": self._hold(conn, _Lend(blk)), "nbytes": n, "ev": ev, "_blk": blk}
 
     def _handle(self, conn, msg: dict):
         tube, op, ch = self.tube, msg["op"], conn.ch
         if op == "unique_id":
             self._reply(conn, {"id": tube.unique_id()})
+        elif op == "chan":                     # messages move to the client's shared-memory rings
+            ch.attach()
+            self._reply(conn, {})
         elif op == "hello":
             g = int(msg["gpu"])
             conn.gpu = g
@@ -286,24 +306,25 @@ class TubeDaemon:
             self._reply(conn, {"ev": conn.mine.handles})
         elif op == "alloc":
             g, n = int(msg["gpu"]), int(msg["nbytes"])
-            with conn.ctx():
-                meta = self._lend(conn, g, n)
+            meta = self._lend(conn, g, n)
             self._reply_block(conn, g, meta.pop("_blk"), meta)
         elif op == "commit":
             t = self._take(conn, int(msg["token"]))
-            if t is None:
+            if not isinstance(t, _Lend):
                 raise KeyError(f"unknown token {msg['token']}")
             conn.wait_peer(msg.get("ev"))      # the client's copy into the block is done (stream-ordered)
-            blk = t._ft_block  # noqa: SLF001
-            dt = _DTYPES[msg["dtype"]]
-            out = t[:math.prod(msg["shape"]) * dt.itemsize].view(dt).view(msg["shape"])
-            out._ft_block = blk  # noqa: SLF001 - still the pool block: a zero-copy store
-            try:
-                tube.store(int(msg["id"]), out, response=bool(msg.get("response")),
-                           producer=msg.get("producer", "func"), consumers=int(msg.get("consumers", 1)))
+            dt, shape = _DTYPES[msg["dtype"]], msg["shape"]
+            nbytes = math.prod(shape) * dt.itemsize
+            if nbytes > t.blk.nbytes:
+                self._free(t.blk, conn)
+                raise ValueError(f"commit of {nbytes} B into a {t.blk.nbytes} B block")
+            stream = conn.stream if conn.stream is not None else 0     # 0: the legacy default stream
+            try:                               # the pool block itself is published: a zero-copy store
+                tube.store_block(int(msg["id"]), t.blk, nbytes, dt, shape, stream,
+                                 response=bool(msg.get("response")), producer=msg.get("producer", "func"),
+                                 consumers=int(msg.get("consumers", 1)))
             except BaseException:
-                del out
-                self._free(t, conn)            # not published (e.g. DuplicateStore): back to the pool
+                self._free(t.blk, conn)        # not published (e.g. DuplicateStore): back to the pool
                 raise
             nxt = msg.get("next")
             if nxt is not None and conn.gpu is not None:
@@ -328,23 +349,13 @@ class TubeDaemon:
             # zero-copy or not is decided atomically with the fetch (a concurrent store
             # could otherwise migrate the object to host memory between a check and the
             # fetch); the view pins the block, so it cannot move after
-            res = tube.fetch_resident(did, g, consumer=msg.get("consumer", "func"))
+            res = tube.fetch_resident(did, g, consumer=msg.get("consumer", "func"), stream=conn.stream)
             if res is not None:
                 blk, nbytes, dtype, shape, release = res
                 t = _Pin(release, nbytes, dtype, shape)   # the loan: unpins the block when dropped
             else:
-                obj = tube._objs.get(did)  # noqa: SLF001
-                nbytes = obj.nbytes if obj is not None else 0
-                dst = tube.empty((max(1, nbytes),), torch.uint8, device=g)
-                try:
-                    t = tube.fetch(did, out=dst[:nbytes].view(obj.dtype).view(obj.shape) if obj is not None else dst,
-                                   consumer=msg.get("consumer", "func"), slo_ms=msg.get("slo_ms"),
-                                   infer_ms=msg.get("infer_ms"))
-                except BaseException:
-                    tube.pools[g].free(dst._ft_block)  # noqa: SLF001
-                    raise
-                t._ft_keep = dst  # noqa: SLF001
-                blk = dst._ft_block  # noqa: SLF001
+                with conn.ctx():
+                    t, blk = self._fetch_into_block(conn, g, did, msg)
             # the consumer stream is ordered after the bytes (a host->GPU stage's last
             # batch is issued before fetch returns; the stream waits on its join events):
             # the client's stream waits on a mark of it, or the stream is synchronised
@@ -354,7 +365,8 @@ class TubeDaemon:
             self._reply_block(conn, g, blk, {"token": self._hold(conn, t), "nbytes": t.nbytes, "ev": ev,
                                              "dtype": str(t.dtype), "shape": list(t.shape)})
         elif op == "fetch_host":
-            t = tube.fetch(int(msg["id"]), device=None, consumer=msg.get("consumer", "func"))
+            with conn.ctx():
+                t = tube.fetch(int(msg["id"]), device=None, consumer=msg.get("consumer", "func"))
             fd = _memfd(t.reshape(-1).view(torch.uint8))
             try:
                 self._reply(conn, {"nbytes": t.nbytes, "dtype": str(t.dtype), "shape": list(t.shape)}, fd)
@@ -365,10 +377,29 @@ class TubeDaemon:
             conn.served += 1
             self._unhold(conn, int(msg["token"]))
         elif op == "release":
-            tube.release(int(msg["id"]))
+            with conn.ctx():
+                tube.release(int(msg["id"]))
             self._reply(conn, {})
         else:
             raise ValueError(f"unknown op {op!r}")
+
+    def _fetch_into_block(self, conn, g, did, msg):
+        """A fetch that is not a same-GPU zero-copy read: into a pool block the
+        client maps (on the connection's stream)."""
+        tube = self.tube
+        obj = tube._objs.get(did)  # noqa: SLF001
+        nbytes = obj.nbytes if obj is not None else 0
+        dst = tube.empty((max(1, nbytes),), torch.uint8, device=g)
+        try:
+            t = tube.fetch(did, out=dst[:nbytes].view(obj.dtype).view(obj.shape) if obj is not None else dst,
+                           consumer=msg.get("consumer", "func"), slo_ms=msg.get("slo_ms"),
+                           infer_ms=msg.get("infer_ms"))
+        except BaseException:
+            tube.pools[g].free(dst._ft_block)  # noqa: SLF001
+            raise
+        t._ft_keep = dst  # noqa: SLF001
+        blk = dst._ft_block  # noqa: SLF001
+        return t, blk
 
     def close(self):
         """Stop accepting, drop every connection (their loans go back to the pool)."""
@@ -418,7 +449,7 @@ class TubeClient:
     current stream. Consumer kernels issued afterwards on the caller's current
     stream see the bytes."""
 
-    def __init__(self, path: str, device: int = 0, events: bool = True):
+    def __init__(self, path: str, device: int = 0, events: bool = True, shm: bool = True):
         self.ch = Channel.connect(path)
         self.device = device
         self._imports = {}           # daemon block id -> ImportedBlock (until the daemon drops it)
@@ -429,6 +460,11 @@ class TubeClient:
         self._mine = self._peer = None
         self._closed = False
         self._views = 0              # zero-copy views handed out and not yet released
+        if shm:                      # messages over shared-memory rings from here on (channel.py)
+            with self._io:
+                self.ch.upgrade()
+                self._sent += 1
+                self._recv()
         if events:
             self._mine = dev.IpcEventRing(device)
             self._used = [0] * self._mine.k        # message number that carried each event's last record
@@ -620,4 +656,5 @@ class TubeClient:
             torch.cuda.synchronize(self.device)
             self._peer.close()
             self._mine.close()
+        self.ch.close()
         self.ch.close()

@@ -276,6 +276,13 @@ class FaaSTube:
         t._ft_block = blk  # noqa: SLF001 - marks pool-backed outputs
         return t
 
+    def lend_block(self, device: int, nbytes: int):
+        """A pool block for an output another process writes (the daemon's
+        ``alloc`` / loan): the caller waits on its ``fences`` before handing it
+        out, then publishes it with ``store_block`` or gives it back with
+        ``pools[device].free``."""
+        return self.pools[device].allocate(nbytes)
+
     def store(self, data_id: int, output: torch.Tensor, response: bool = False, producer: str = "func",
               consumers: int = 1, queue_pos: int | None = None) -> None:
         """FaaSTube.store(index, output, response) — engine.py:342-423.
@@ -303,10 +310,18 @@ class FaaSTube:
                 self.pools[output.get_device()].free(pre_blk, list(pre_blk.fences))
             raise
         t2 = time.perf_counter()
+        self._after_store(stage)
+        t3 = time.perf_counter()
+        if t3 - t0 > 0.01:   # slow stores, for diagnosis: ms allocating / in the locked part / migrating, bytes
+            self.slow_stores.append((round(1e3 * (t1 - t0), 2), round(1e3 * (t2 - t1), 2),
+                                     round(1e3 * (t3 - t2), 2), output.nbytes))
+
+    def _after_store(self, stage):
+        """The part of a store after the tube lock: a managed GPU->host response
+        stage (engine.py:414-423 -> 537-575) is paced by the d2h arbiter outside
+        the lock (the object stays pinned until its block's readers include the
+        stage), then the migration the store decided runs."""
         if stage is not None:
-            # managed GPU->host response stage (engine.py:414-423 -> 537-575), paced
-            # by the d2h arbiter outside the tube lock; the object stays pinned
-            # until its block's readers include the stage
             obj, args = stage
             try:
                 ticket = self.pacer.submit_d2h(*args)
@@ -318,10 +333,48 @@ class FaaSTube:
                 self._unpin(obj)
         if self._pending:
             self._drain_pending()                         # migration decided by this store
-        t3 = time.perf_counter()
-        if t3 - t0 > 0.01:   # slow stores, for diagnosis: ms allocating / in the locked part / migrating, bytes
-            self.slow_stores.append((round(1e3 * (t1 - t0), 2), round(1e3 * (t2 - t1), 2),
-                                     round(1e3 * (t3 - t2), 2), output.nbytes))
+
+    def store_block(self, data_id: int, blk, nbytes: int, dtype, shape, stream, response: bool = False,
+                    producer: str = "func", consumers: int = 1) -> None:
+        """``store`` of a pool block another process wrote (the daemon's commit of
+        a lent block): zero copy, the object's bytes ready after
+        ``stream``'s current work — no tensor is built on this path."""
+        pre_host = self._pinned(nbytes) if response else None
+        with self._lock:
+            self._reap()
+            if data_id in self._objs:
+                from ._lib import DuplicateStore
+                raise DuplicateStore(f"data id {data_id} already stored")
+            self._last_op_ms = now = self.now_ms()
+            g = blk.device
+            obj = _Obj(data_id, nbytes, dtype, tuple(shape), g, producer, consumers, now)
+            obj.home = g
+            obj.queue_pos = next(self._queue)
+            stage = self._commit_block(obj, blk, dev.stream_ptr(stream), response, pre_host, now)
+        self._after_store(stage)
+
+    def _commit_block(self, obj, blk, stream: int, response, pre_host, now):
+        """(lock held) Publish a pool-backed object: ``ready`` on ``stream``, index
+        entry (dataplane.py:72-83) + histogram sample (datastore.py:51-62), the
+        shrink timer, the response leg. Returns the response stage to submit."""
+        g = obj.gpu
+        obj.block = blk
+        obj.ready = dev.Ev(g).record(stream)
+        rw, last = self.pools[g].commit_store(self.index, obj.did, self.node, g, obj.nbytes, now, obj.producer,
+                                              response, self._live[(obj.producer, g)] + 1)
+        self._push_due(g, rw, last, now)
+        stage = None
+        if response:
+            resp = self._respond(obj, pre_host)
+            if resp is not None:
+                obj.pins += 1                    # released once the stage is submitted
+                stage = (obj, resp)
+        self._objs[obj.did] = obj
+        self._account(obj, 1)
+        self.stats["stores"] += 1
+        if self.strategy.migration != "none" and self._stored_on(g) > self.capacity_limit:
+            self._pending.add(("pressure", g))          # engine.py:685-702, after the lock
+        return stage
 
     def _store_locked(self, data_id, output, response, producer, consumers, queue_pos, pre_host, pre_blk):
         """Returns (obj, pacer.submit_d2h args) when a managed response stage must be submitted."""
@@ -343,11 +396,8 @@ class FaaSTube:
                 blk = getattr(t, "_ft_block", None)
                 live_here = self._live[(producer, g)]     # this producer's live objects here
                 if blk is not None and blk.ptr == t.data_ptr():
-                    obj.block = blk                      # zero-copy store of a pool-backed output
-                    obj.ready = dev.Ev(g).record(self._stream(g))
-                    # index entry (dataplane.py:72-83) + histogram sample (datastore.py:51-62)
-                    rw, last = pool.commit_store(self.index, data_id, self.node, g, nbytes, now, producer,
-                                                 response, live_here + 1)
+                    # zero-copy store of a pool-backed output
+                    return self._commit_block(obj, blk, self._stream(g), response, pre_host, now)
                 else:
                     blk = pre_blk                        # datastore.py:130-144 (allocated above)
                     obj.block = blk
@@ -674,27 +724,29 @@ class FaaSTube:
         if self.strategy.migration != "none" and self._off_gpu[g]:
             self._pending.add(("prefetch", g))         # engine.py:678-679, 717-736
 
-    def fetch_resident(self, data_id: int, device: int, consumer: str = "func"):
+    def fetch_resident(self, data_id: int, device: int, consumer: str = "func", stream=None):
         """Zero-copy fetch for another process (the daemon's same-GPU path), if the
         object is stored in GPU ``device``'s pool right now: the caller's stream
         is ordered after the stored bytes, the block is pinned, and this counts
         as the consumer's fetch (dataplane.py:184-185). Decided under the tube
         lock, so a concurrent migration cannot move it in between. Returns
-        (pool block, nbytes, dtype, shape, release) — ``release()`` unpins the
-        block once the reader is done (the caller's current stream must be
-        ordered after the read by then). None if it lives elsewhere."""
+        (pool block, nbytes, dtype, shape, release) — ``release(stream)`` unpins
+        the block once the reader is done (``stream``, default the caller's
+        current one, must be ordered after the read by then). ``stream``: the
+        reader's stream (default the current one). None if it lives elsewhere."""
         with self._lock:
             obj = self._objs.get(data_id)
             if obj is None or obj.gpu != device or obj.block is None:
                 return None
             self._reap()
             self._last_op_ms = self.now_ms()
-            obj.ready.wait(self._stream(device))
+            s = dev.stream_ptr(stream) if stream is not None else self._stream(device)
+            obj.ready.wait(s)
             obj.pins += 1
             self.stats["zero_copy"] += 1
             self.stats["fetches"] += 1
-            self._consumed(obj)
-            res = (obj.block, obj.nbytes, obj.dtype, obj.shape, lambda: self._unpin(obj))
+            self._consumed(obj, stream=s)
+            res = (obj.block, obj.nbytes, obj.dtype, obj.shape, lambda st=None: self._unpin(obj, st))
         if self._pending:
             self._drain_pending()          # prefetch made possible by this consumer's retire
         return res
@@ -880,12 +932,12 @@ class FaaSTube:
                 slo_ms if slo_ms else 1e9, infer_ms if infer_ms is not None else 0.0,
                 min(min(b.hop_caps) for b in br), host.data_ptr(), obj.block.ptr, g, obj.nbytes, routes, s)
 
-    def _consumed(self, obj: _Obj, fence=None):
+    def _consumed(self, obj: _Obj, fence=None, stream=None):
         obj.remaining -= 1
         if obj.remaining <= 0:
-            self._retire(obj, fence)
+            self._retire(obj, fence, stream)
 
-    def _retire(self, obj: _Obj, fence=None):
+    def _retire(self, obj: _Obj, fence=None, stream=None):
         """engine.py:667-679: last consumer done -> drop index entry, free block."""
         if obj.retired:
             return
@@ -901,7 +953,8 @@ class FaaSTube:
             obj.block = None
             # the caller's last read of the block: an event on its stream (or the one
             # a batched fetch recorded after its copy)
-            ev = fence if fence is not None else dev.Ev(blk.device).record(self._stream(blk.device))
+            ev = fence if fence is not None else dev.Ev(blk.device).record(
+                stream if stream is not None else self._stream(blk.device))
             fences = [ev] + obj.readers + ([obj.ready] if obj.ready is not None else [])
             obj.readers = []
             self.index._meta.pop(obj.did, None)
@@ -911,13 +964,13 @@ class FaaSTube:
                 self._pending.add(("prefetch", blk.device))  # engine.py:678-679, 717-736
             return
         self.index.drop(obj.did)
-        self._maybe_free(obj)
+        self._maybe_free(obj, stream)
 
-    def _maybe_free(self, obj: _Obj):
+    def _maybe_free(self, obj: _Obj, stream=None):
         if obj.block is not None and obj.pins == 0 and obj.retired:
             blk, obj.block = obj.block, None
             # later writers of this block must order after our readers
-            ev = dev.Ev(blk.device).record(self._stream(blk.device))
+            ev = dev.Ev(blk.device).record(stream if stream is not None else self._stream(blk.device))
             fences = [ev] + obj.readers + ([obj.ready] if obj.ready is not None else [])
             obj.readers = []
             self.pools[blk.device].free(blk, fences)
@@ -925,10 +978,10 @@ class FaaSTube:
             if self.strategy.migration != "none" and self._off_gpu[blk.device]:
                 self._pending.add(("prefetch", blk.device))  # engine.py:678-679, 717-736
 
-    def _unpin(self, obj):
+    def _unpin(self, obj, stream=None):
         with self._lock:
             obj.pins -= 1
-            self._maybe_free(obj)
+            self._maybe_free(obj, stream)
 
     def _view(self, obj: _Obj) -> torch.Tensor:
         obj.pins += 1

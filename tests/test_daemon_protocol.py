@@ -16,6 +16,10 @@ import torch
 class _Blk:
     def __init__(self, vid, nbytes, device=0):
         self.vmm_id, self.nbytes, self.device = vid, nbytes, device
+        self.data = torch.zeros(nbytes, dtype=torch.uint8)    # stands in for the device memory
+
+    def wait_fences(self, stream):
+        pass
 
 
 class _Pool:
@@ -38,8 +42,8 @@ class _Pool:
 
 
 class _Obj:
-    def __init__(self, t, gpu):
-        self.t, self.gpu, self.block = t, gpu, t._ft_block
+    def __init__(self, t, gpu, block):
+        self.t, self.gpu, self.block = t, gpu, block
         self.nbytes, self.dtype, self.shape = t.nbytes, t.dtype, tuple(t.shape)
 
 
@@ -54,9 +58,21 @@ class _Tube:
         return next(self._ids)
 
     def empty(self, shape, dtype, device=0):
-        t = torch.zeros(shape, dtype=dtype)
-        t._ft_block = _Blk(next(self.pools[device]._ids), t.nbytes, device)
+        blk = self.lend_block(device, torch.zeros((), dtype=dtype).element_size() * int(torch.tensor(shape).prod()))
+        t = blk.data.view(dtype).view(shape)
+        t._ft_block = blk
         return t
+
+    def lend_block(self, device, nbytes):
+        return _Blk(next(self.pools[device]._ids), nbytes, device)
+
+    def store_block(self, did, blk, nbytes, dtype, shape, stream, response=False, producer="func", consumers=1):
+        from paper_2411_01830_b200 import DuplicateStore
+        if did in self._objs:
+            raise DuplicateStore(f"data id {did} already stored")
+        t = blk.data[:nbytes].view(dtype).view(shape)
+        self._objs[did] = _Obj(t, blk.device, blk)
+        self.stored[did] = t.clone()
 
     def sync_stream(self, g):
         pass
@@ -67,7 +83,7 @@ class _Tube:
             raise DuplicateStore(f"data id {did} already stored")
         blk = getattr(t, "_ft_block", None)
         if blk is not None:
-            self._objs[did] = _Obj(t, 0)
+            self._objs[did] = _Obj(t, 0, blk)
         self.stored[did] = t.clone()
 
     def fetch(self, did, device=None, out=None, consumer="func", slo_ms=None, infer_ms=None):
@@ -78,24 +94,36 @@ class _Tube:
             return self.stored[did]
         return self._objs[did].t
 
-    def fetch_resident(self, did, device, consumer="func"):
+    def fetch_resident(self, did, device, consumer="func", stream=None):
         o = self._objs.get(did)
         if o is None or o.gpu != device or o.block is None:
             return None
         t = self.fetch(did, device, consumer=consumer)
-        return o.block, t.nbytes, t.dtype, tuple(t.shape), lambda: None
+        return o.block, t.nbytes, t.dtype, tuple(t.shape), lambda stream=None: None
 
     def release(self, did):
         self._objs.pop(did, None)
 
 
-@pytest.fixture()
-def daemon():
+@pytest.fixture(params=["socket", "shm"])
+def daemon(request):
+    """The daemon over a stand-in tube; connections speak over the socket or,
+    after ``upgrade``, over the shared-memory rings (channel.py)."""
     from paper_2411_01830_b200.daemon import TubeDaemon
     tube = _Tube()
     d = TubeDaemon(tube, os.path.join(tempfile.mkdtemp(), "d.sock"))
+    d.shm = request.param == "shm"
     yield d, tube
     d.close()
+
+
+def _connect(d):
+    from paper_2411_01830_b200.channel import Channel
+    ch = Channel.connect(d.path)
+    if d.shm:
+        ch.upgrade()
+        assert ch.recv_msg()["ok"]
+    return ch
 
 
 def _call(ch, msg):
@@ -108,9 +136,8 @@ def _call(ch, msg):
 
 
 def test_put_get_over_the_channel(daemon):
-    from paper_2411_01830_b200.channel import Channel
     d, tube = daemon
-    ch = Channel.connect(d.path)
+    ch = _connect(d)
     ids = [_call(ch, {"op": "unique_id"})["id"] for _ in range(3)]
     assert ids == sorted(ids) and len(set(ids)) == 3
     rep = _call(ch, {"op": "alloc", "gpu": 0, "nbytes": 24})
@@ -127,7 +154,7 @@ def test_put_get_over_the_channel(daemon):
     assert rep["dtype"] == "torch.float32" and rep["shape"] == [2, 3]
     ch.send_msg({"op": "done", "token": rep["token"]})            # fire and forget
     # a second connection has not mapped it: the fd crosses once for it too
-    ch2 = Channel.connect(d.path)
+    ch2 = _connect(d)
     rep2 = _call(ch2, {"op": "fetch", "id": ids[0], "gpu": 0})
     assert rep2["fd"] and rep2["block"] == blk
     os.close(rep2["_fd"])
@@ -145,9 +172,8 @@ def test_put_get_over_the_channel(daemon):
 
 
 def test_unmap_notice_and_refetch(daemon):
-    from paper_2411_01830_b200.channel import Channel
     d, tube = daemon
-    ch = Channel.connect(d.path)
+    ch = _connect(d)
     rep = _call(ch, {"op": "alloc", "gpu": 0, "nbytes": 8})
     os.close(rep["_fd"])
     blk = rep["block"]
@@ -163,9 +189,8 @@ def test_unmap_notice_and_refetch(daemon):
 
 
 def test_duplicate_commit_returns_block_and_dead_client_loans(daemon):
-    from paper_2411_01830_b200.channel import Channel
     d, tube = daemon
-    ch = Channel.connect(d.path)
+    ch = _connect(d)
     did = _call(ch, {"op": "unique_id"})["id"]
     for i in range(2):
         rep = _call(ch, {"op": "alloc", "gpu": 0, "nbytes": 4})
@@ -185,10 +210,9 @@ def test_duplicate_commit_returns_block_and_dead_client_loans(daemon):
 
 
 def test_host_payload_as_memfd(daemon):
-    from paper_2411_01830_b200.channel import Channel
     from paper_2411_01830_b200.daemon import _from_memfd, _memfd
     d, tube = daemon
-    ch = Channel.connect(d.path)
+    ch = _connect(d)
     x = torch.arange(1000, dtype=torch.int16).reshape(10, 100)
     did = _call(ch, {"op": "unique_id"})["id"]
     fd = _memfd(x)
