@@ -458,6 +458,16 @@ int ft_pacer_submit(ft_pacer* p, const char* key, int managed, double slo_ms, do
 int ft_pacer_submit_d2h(ft_pacer* p, const char* key, int managed, double slo_ms, double infer_ms,
                         double per_branch_cap_gbps, void* host_dst, const void* src, int src_dev, uint64_t bytes,
                         int k, const ft_route* routes, void* producer_stream, uint64_t* ticket);
+/* the routes of a host->GPU fetch in one call (tube._host_to_gpu's planning step):
+ * plan it (ft_fetch_plan, dataplane.py:190-250), cut the object into each branch's
+ * byte range (shares accumulated in float64, boundaries floored to 256 B), take each
+ * route's stream pair on the GPU whose PCIe root carries it from the pairs registered
+ * with ft_plane_set_pairs (slot keyed by the consumer stream). Out: k routes, whether
+ * the stage is managed (strategy.pcie_sched && stage.managed), the smallest hop cap,
+ * bytes the routes forward over NVLink. Feed them to ft_pacer_submit. */
+int ft_plane_set_pairs(ft_plane* p, int gpu, int n, void* const* ce_streams, void* const* fw_streams);
+int ft_h2g_routes(ft_plane* p, int node, int dst_gpu, uint64_t bytes, void* consumer_stream, ft_route* routes,
+                  int cap, int* k, int* managed, double* per_branch_cap, uint64_t* nvlink_bytes);
 /* host wait for a ticket's last byte (timeout_ms < 0: forever); returns the stage's status */
 int ft_pacer_wait(ft_pacer* p, uint64_t ticket, double timeout_ms);
 int ft_pacer_done(ft_pacer* p, uint64_t ticket, int* done);

@@ -240,6 +240,9 @@ _SIGS = {
     "ft_ipc_event_open": (None, [C.c_int, C.c_char_p, P(vp)]),
     "ft_fd_send": (None, [C.c_int, C.c_int, u64]),
     "ft_fd_recv": (None, [C.c_int, P(C.c_int), P(u64)]),
+    "ft_plane_set_pairs": (None, [vp, C.c_int, C.c_int, P(vp), P(vp)]),
+    "ft_h2g_routes": (None, [vp, C.c_int, C.c_int, u64, vp, vp, C.c_int, P(C.c_int), P(C.c_int), P(dbl),
+                             P(u64)]),
     "ft_chan_create": (None, [C.c_uint32, C.c_uint32, P(C.c_int), P(vp)]),
     "ft_chan_attach": (None, [C.c_int, P(vp)]),
     "ft_chan_send": (None, [vp, C.c_int, C.c_char_p, C.c_uint32, i64]),

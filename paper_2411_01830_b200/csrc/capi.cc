@@ -1,5 +1,7 @@
 // extern "C" boundary for the decision side (include/faastube.h).
+#include <cmath>
 #include <cstring>
+#include <map>
 
 #include "decisions.h"
 
@@ -12,7 +14,11 @@ struct ft_ring { Ring r; };
 struct ft_hist { Hist h; };
 struct ft_pool_policy { PoolPolicy p; };
 struct ft_index { Index x; };
-struct ft_plane { Plane p; };
+struct ft_plane {
+  Plane p;
+  // route stream pairs per GPU (the tube's per-transfer CE pairs), for ft_h2g_routes
+  std::map<int, std::vector<std::pair<void*, void*>>> pairs;
+};
 struct ft_plan { Plan p; };
 struct ft_arbiter { Arbiter a; };
 
@@ -648,6 +654,82 @@ int ft_arbiter_next_event(const ft_arbiter* a, double* t, char* key, size_t key_
     snprintf(key, key_cap, "%s", k.c_str());
   }
   return FT_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------- host->GPU fetch, one call
+extern "C" {
+
+int ft_plane_set_pairs(ft_plane* p, int gpu, int n, void* const* ce, void* const* fw) {
+  NEED(p);
+  if (n <= 0 || !ce || !fw) {
+    ft::set_last_error("ft_plane_set_pairs: bad arguments");
+    return FT_E_VALUE;
+  }
+  auto& v = p->pairs[gpu];
+  v.clear();
+  for (int i = 0; i < n; ++i) v.emplace_back(ce[i], fw[i]);
+  return FT_OK;
+}
+
+// tube._host_to_gpu's plan -> routes step in one call: plan a host->GPU transfer
+// (dataplane.py:190-250), cut the object into each branch's contiguous byte range
+// (tube._stripes: shares accumulate in float64, boundaries floored to 256 B), pick
+// each route's stream pair on the GPU whose PCIe root carries it (slot keyed by the
+// consumer stream, as tube._pair), and return what ft_pacer_submit takes.
+int ft_h2g_routes(ft_plane* p, int node, int dst_gpu, uint64_t bytes, void* consumer_stream, ft_route* routes,
+                  int cap, int* k, int* managed, double* per_branch_cap, uint64_t* nvlink_bytes) {
+  NEED(p);
+  NEED(routes);
+  NEED(k);
+  FT_TRY
+  Plan plan = p->p.fetch_plan(node, -1, node, dst_gpu, (double)bytes);
+  if (plan.method != FT_HOST_GPU || plan.stages.size() != 1) throw Error(FT_E_VALUE, "not a host->GPU plan");
+  const Stage& st = plan.stages[0];
+  const int nb = (int)st.branches.size();
+  if (nb > cap) throw Error(FT_E_TRUNCATED, "ft_h2g_routes: more branches than route slots");
+  // byte ranges (tube._stripes)
+  const double total = py_sum(st.branches.begin(), st.branches.end(), [](const Branch& b) { return b.share; });
+  std::vector<uint64_t> bounds{0};
+  if (total <= 0 || bytes == 0) {
+    for (int i = 0; i < nb; ++i) bounds.push_back(bytes);
+  } else {
+    double acc = 0.0;
+    for (int i = 0; i + 1 < nb; ++i) {
+      acc += st.branches[i].share;
+      const uint64_t b = (uint64_t)std::floor((double)bytes * (acc / total)) / 256 * 256;
+      bounds.push_back(std::max(bounds.back(), std::min(bytes, b)));
+    }
+    bounds.push_back(bytes);
+  }
+  const uint64_t sp = (uint64_t)(uintptr_t)consumer_stream;
+  const unsigned __int128 slot = ((unsigned __int128)(sp >> 4) * 0x9E3779B1ull) >> 16;
+  double capmin = INFINITY;
+  uint64_t nv = 0;
+  for (int i = 0; i < nb; ++i) {
+    const Branch& b = st.branches[i];
+    int sg = dst_gpu;  // tube._staging_gpu: the first GPU the branch lands on
+    for (auto& l : b.links)
+      if (l.kind == FT_LINK_NVP_OUT || l.kind == FT_LINK_NV) {
+        sg = l.a;
+        break;
+      }
+    auto it = p->pairs.find(sg);
+    if (it == p->pairs.end() || it->second.empty())
+      throw Error(FT_E_NOT_SUPPORTED, "the plan routes through GPU " + std::to_string(sg) +
+                                          ", which this tube does not drive");
+    const auto& pr = it->second[(size_t)(slot % it->second.size())];
+    const uint64_t off = bounds[i], len = bounds[i + 1] - bounds[i];
+    routes[i] = ft_route{sg, 0, off, len, pr.first, pr.second};
+    if (sg != dst_gpu) nv += len;
+    for (double c : b.hop_caps) capmin = std::min(capmin, c);
+  }
+  *k = nb;
+  if (managed) *managed = p->p.s.pcie_sched && st.managed;
+  if (per_branch_cap) *per_branch_cap = capmin;
+  if (nvlink_bytes) *nvlink_bytes = nv;
+  FT_CATCH
 }
 
 }  // extern "C"

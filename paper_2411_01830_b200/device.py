@@ -820,6 +820,16 @@ class Pacer:
                             C.byref(t))
         return t.value
 
+    def submit_routes(self, key: str, managed: bool, slo_ms: float, infer_ms: float, per_branch_cap_gbps: float,
+                      dst_ptr: int, dst_dev: int, host_ptr: int, nbytes: int, host_pinned: bool, k: int, routes,
+                      consumer_stream: int) -> int:
+        """``submit`` with the routes already in a ft_route array (``ft_h2g_routes``) -> ticket"""
+        t = C.c_uint64()
+        LIB.ft_pacer_submit(self._h, key.encode(), int(managed), float(slo_ms), float(infer_ms),
+                            float(per_branch_cap_gbps), C.c_void_p(dst_ptr), int(dst_dev), C.c_void_p(host_ptr),
+                            int(nbytes), int(host_pinned), int(k), routes, C.c_void_p(consumer_stream), C.byref(t))
+        return t.value
+
     def submit_d2h(self, key: str, managed: bool, slo_ms: float, infer_ms: float, per_branch_cap_gbps: float,
                    host_ptr: int, src_ptr: int, src_dev: int, nbytes: int, routes: list, producer_stream: int) -> int:
         """GPU -> pinned host; routes as for submit (stage_dev == src_dev: direct) -> ticket"""

@@ -149,6 +149,11 @@ class FaaSTube:
         # GPU->host stages get their own pairs: a D2H op queued behind another
         # tenant's H2D batches on a shared stream would wait for them
         self._d2h_pairs = {g: [(dev.new_stream(g), dev.new_stream(g)) for _ in range(8)] for g in self.gpus}
+        for g, prs in self._ce_pairs.items():        # the same pairs, for the native host->GPU planning call
+            n = len(prs)
+            dev.LIB.ft_plane_set_pairs(self.plane._h, g, n, (dev.C.c_void_p * n)(*[a.cuda_stream for a, _ in prs]),
+                                       (dev.C.c_void_p * n)(*[b.cuda_stream for _, b in prs]))
+        self._tls = threading.local()                # per-thread route arrays of that call
         self._ce_rr = itertools.count()
         self._keepalive = []         # (event, buffers) released once the event has completed
         self._last_op_ms = 0.0       # last store/fetch (idle detection for physical reclaim)
@@ -652,11 +657,13 @@ class FaaSTube:
                     self._fetch_local(obj, out)          # copy into the consumer's input: one native call
                     self.stats["fetches"] += 1
                     return out
+            elif src.gpu is None and dst.gpu is not None and src.node == dst.node:
+                plan = None                  # host -> GPU: planned in one native call (_host_to_gpu)
             else:
                 plan = self.plane.fetch_plan(src, dst, obj.nbytes)
-            h2g = plan.method == "host_gpu" and not dst.on_host
-            d2h = (plan.method == "host_gpu" and dst.on_host and obj.block is not None and self.strategy.pcie_sched
-                   and plan.stages[0].managed)
+            h2g = plan is None or (plan.method == "host_gpu" and not dst.on_host)
+            d2h = (plan is not None and plan.method == "host_gpu" and dst.on_host and obj.block is not None
+                   and self.strategy.pcie_sched and plan.stages[0].managed)
             if h2g:
                 res, stage = self._host_to_gpu(obj, plan, dst, out, slo_ms, infer_ms)
             elif d2h:
@@ -687,7 +694,7 @@ class FaaSTube:
             return res.view(torch.uint8).view(obj.dtype).view(obj.shape)
         # host->GPU stage: the pacer returns once its last batch is issued — outside
         # the tube lock, so concurrent tenants' stages are paced side by side
-        ticket = self.pacer.submit(*stage)
+        ticket = self.pacer.submit_routes(*stage)
         with self._lock:
             self._tickets.append((ticket, obj.host, res))
         return res
@@ -1105,33 +1112,29 @@ class FaaSTube:
         the target's own root, or CE into the staging GPU's chunk ring + NVLink
         forward. Managed stages (strategy.pcie_sched) enter the SLO partition and
         are paced in batches at their rate (engine.py:537-646); the consumer's
-        stream is ordered after the last byte. Returns (result, pacer.submit
-        arguments); the caller submits outside the tube lock."""
+        stream is ordered after the last byte. The plan, the byte ranges and the
+        route streams come from one native call (``ft_h2g_routes``). Returns
+        (result, Pacer.submit_routes arguments); the caller submits outside the
+        tube lock (the routes live in this thread's array until then)."""
         res = self._out(obj, dst.gpu, out)
-        st = plan.stages[0]
-        br = st.branches
-        ranges = self._stripes(obj.nbytes, [b.bytes_share for b in br])
         s = self._stream(dst.gpu)
         if obj.ready is not None:
             obj.ready.wait(s)
-        # CE streams keyed by the consumer's stream: a tenant's stages stay in its own
-        # FIFO, other tenants' stages (other streams) do not queue behind them
-        slot = (s >> 4) * 0x9E3779B1 >> 16
-        routes = []
-        for b, (off, n) in zip(br, ranges):
-            sg = _staging_gpu(b.links, dst.gpu)
-            ce, fw = self._pair(sg, slot)
-            routes.append((sg, 0, off, n, ce.cuda_stream, fw.cuda_stream))
-            if sg != dst.gpu:
-                self.stats["bytes_nvlink"] += n
-        managed = bool(self.strategy.pcie_sched and st.managed)
+        tl = self._tls
+        if not hasattr(tl, "routes"):
+            from ._lib import RouteC
+            tl.routes, tl.k, tl.managed = (RouteC * 16)(), dev.C.c_int(), dev.C.c_int()
+            tl.cap, tl.nv = dev.C.c_double(), dev.C.c_uint64()
+        dev.LIB.ft_h2g_routes(self.plane._h, self.node, dst.gpu, obj.nbytes, dev.C.c_void_p(s), tl.routes, 16,
+                              dev.C.byref(tl.k), dev.C.byref(tl.managed), dev.C.byref(tl.cap), dev.C.byref(tl.nv))
+        managed = bool(tl.managed.value)
         host = obj.host
         stage = (f"m{next(self._managed_ids)}" if managed else "", managed,
                  slo_ms if slo_ms else 1e9,                       # engine.py:546-547
-                 infer_ms if infer_ms is not None else 0.0,
-                 min(min(b.hop_caps) for b in br), res.data_ptr(), dst.gpu, host.data_ptr(), obj.nbytes,
-                 host.is_pinned(), routes, s)
+                 infer_ms if infer_ms is not None else 0.0, tl.cap.value, res.data_ptr(), dst.gpu,
+                 host.data_ptr(), obj.nbytes, host.is_pinned(), tl.k.value, tl.routes, s)
         self.stats["bytes_h2d"] += obj.nbytes
+        self.stats["bytes_nvlink"] += tl.nv.value
         if managed:
             self.stats["managed_stages"] = self.stats.get("managed_stages", 0) + 1
         return res, stage
@@ -1218,13 +1221,3 @@ def _staging_gpu_d2h(links, source):
         if l[0] == "nv":
             return l[2]
     return source
-
-
-def _staging_gpu(links, target):
-    """First GPU a host->GPU branch lands on (its PCIe root's staging GPU)."""
-    for l in links:
-        if l[0] == "nvp_out":
-            return l[1]
-        if l[0] == "nv":
-            return l[1]
-    return target

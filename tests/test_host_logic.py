@@ -18,11 +18,68 @@ def test_stripes_cover_exactly():
 
 
 def test_branch_link_parsing():
-    from paper_2411_01830_b200.tube import _hops, _staging_gpu
+    from paper_2411_01830_b200.tube import _hops
     assert _hops([("nvp_out", 3), ("nvp_in", 0)]) == [(3, 0)]
     assert _hops([("nv", 1, 2), ("nv", 2, 5)]) == [(1, 2), (2, 5)]
-    assert _staging_gpu([("h2d", 0, 2), ("nvp_out", 2), ("nvp_in", 0)], 0) == 2
-    assert _staging_gpu([("h2d", 0, 0)], 0) == 0
+
+
+def _staging_gpu(links, target):
+    """tube.py's host->GPU staging GPU: the first GPU a branch lands on (its
+    PCIe root's staging GPU), restated for the native planner's check."""
+    for l in links:
+        if l[0] in ("nvp_out", "nv"):
+            return l[1]
+    return target
+
+
+@pytest.mark.parametrize("preset,strategy", [("b200", "faastube"), ("b200", "infless_plus"),
+                                             ("dgx_v100", "faastube"), ("dgx_a100", "faastube"),
+                                             ("quad_a10", "faastube"), ("b200", "deepplan_plus")])
+def test_native_h2g_routes_match_the_plan(preset, strategy):
+    """ft_h2g_routes (tube._host_to_gpu's planning step in one native call) gives
+    the routes the Python restatement builds from the same plan: the plan's
+    branches cut into byte ranges by FaaSTube._stripes, each route on its staging
+    GPU's stream pair picked by the consumer stream's slot (no GPU needed: the
+    streams are opaque handles here)."""
+    import ctypes as C
+
+    from paper_2411_01830_b200._lib import LIB, RouteC
+    from paper_2411_01830_b200.dataplane import Dataplane, Location
+    from paper_2411_01830_b200.strategies import strategy_preset
+    from paper_2411_01830_b200.topology import build_preset, snapshot_matrix
+    from paper_2411_01830_b200.tube import FaaSTube
+    topo = build_preset(preset) if preset != "b200" else build_preset("b200", n_gpus=8)
+    strat = strategy_preset(strategy)
+    plane = Dataplane(topo, strat, snapshot_matrix(topo), 2e6)
+    ref = Dataplane(topo, strat, snapshot_matrix(topo), 2e6)
+    pairs = {g: [(0x1000 * (g + 1) + 16 * i, 0x9000 * (g + 1) + 16 * i) for i in range(16)] for g in topo.gpus()}
+    for g, prs in pairs.items():
+        LIB.ft_plane_set_pairs(plane._h, g, len(prs), (C.c_void_p * len(prs))(*[a for a, _ in prs]),
+                               (C.c_void_p * len(prs))(*[b for _, b in prs]))
+    routes, k, managed, cap, nv = (RouteC * 16)(), C.c_int(), C.c_int(), C.c_double(), C.c_uint64()
+    for dst in topo.gpus():
+        for n in (0, 1, 4096, 3 * 10**6 + 5, 1 << 30):
+            stream = 0x7F3A00000000 + 0x1230 * (dst + 1) + n % 977 * 16
+            LIB.ft_h2g_routes(plane._h, 0, dst, n, C.c_void_p(stream), routes, 16, C.byref(k), C.byref(managed),
+                              C.byref(cap), C.byref(nv))
+            plan = ref.fetch_plan(Location(0, None), Location(0, dst), n)
+            st = plan.stages[0]
+            br = st.branches
+            ranges = FaaSTube._stripes(n, [b.bytes_share for b in br])
+            slot = (stream >> 4) * 0x9E3779B1 >> 16
+            want, want_nv = [], 0
+            for b, (off, m) in zip(br, ranges):
+                sg = _staging_gpu(b.links, dst)
+                ce, fw = pairs[sg][slot % len(pairs[sg])]
+                want.append((sg, m, ce, fw) if m else (sg, 0, ce, fw))
+                want_nv += m if sg != dst else 0
+            got = [(routes[i].stage_dev, routes[i].len, routes[i].ce_stream, routes[i].fw_stream) for i in range(k.value)]
+            assert got == want, (preset, strategy, dst, n)
+            offs = [routes[i].off for i in range(k.value) if routes[i].len]
+            assert offs == [o for o, m in ranges if m]
+            assert nv.value == want_nv
+            assert bool(managed.value) == bool(strat.pcie_sched and st.managed)
+            assert cap.value == min(min(b.hop_caps) for b in br)
 
 
 def test_host_path_identity_threads():

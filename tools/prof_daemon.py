@@ -103,23 +103,34 @@ def main():
     d = TubeDaemon(tube, path)
     times = {}
     orig = d._handle
+    import cProfile
+    import pstats
+    prof, calls = {}, {}
 
     def timed(conn, msg):
+        op = msg["op"]
+        calls[op] = calls.get(op, 0) + 1
+        pr = prof.setdefault(op, cProfile.Profile()) if calls[op] % 2 else None
         t0 = time.perf_counter()
+        if pr is not None:
+            pr.enable()
         try:
             return orig(conn, msg)
         finally:
-            times.setdefault(msg["op"], []).append(time.perf_counter() - t0)
+            if pr is not None:
+                pr.disable()
+            else:
+                times.setdefault(op, []).append(time.perf_counter() - t0)
     d._handle = timed
-    ost, ofe = tube.store, tube.fetch_resident
-    tin = {"tube.store": [], "tube.fetch_resident": [], "tube.empty": []}
+    ost, ofe = tube.store_block, tube.fetch_resident
+    tin = {"tube.store_block": [], "tube.fetch_resident": [], "tube.lend_block": []}
 
     def st(*a, **k):
         t0 = time.perf_counter()
         try:
             return ost(*a, **k)
         finally:
-            tin["tube.store"].append(time.perf_counter() - t0)
+            tin["tube.store_block"].append(time.perf_counter() - t0)
 
     def fr(*a, **k):
         t0 = time.perf_counter()
@@ -127,15 +138,15 @@ def main():
             return ofe(*a, **k)
         finally:
             tin["tube.fetch_resident"].append(time.perf_counter() - t0)
-    oem = tube.empty
+    oem = tube.lend_block
 
     def em(*a, **k):
         t0 = time.perf_counter()
         try:
             return oem(*a, **k)
         finally:
-            tin["tube.empty"].append(time.perf_counter() - t0)
-    tube.store, tube.fetch_resident, tube.empty = st, fr, em
+            tin["tube.lend_block"].append(time.perf_counter() - t0)
+    tube.store_block, tube.fetch_resident, tube.lend_block = st, fr, em
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     p = ctx.Process(target=client, args=(path, q))
@@ -145,6 +156,10 @@ def main():
     res["daemon_handler_us"] = {k: med(v[50:]) for k, v in times.items()}
     res["daemon_tube_us"] = {k: med(v[50:]) for k, v in tin.items()}
     print(res)
+    for op in ("commit", "fetch", "done"):
+        if op in prof:
+            print("==== daemon handler profile:", op)
+            pstats.Stats(prof[op]).sort_stats("tottime").print_stats(14)
     d.close()
     tube.close()
 
