@@ -1169,7 +1169,7 @@ def _single_gpu_extras(tube, g, dev, torch):
         xs = torch.empty(n, dtype=torch.uint8, device=f"cuda:{g}").fill_(3)
         ys = torch.empty_like(xs)
         reps = 30 if n <= (64 << 20) else 6
-        zc, cp = [], []
+        zc, cp, cpd = [], [], []
         for r in range(reps + 2):
             did = tube.unique_id()
             tube.store(did, xs)
@@ -1186,12 +1186,27 @@ def _single_gpu_extras(tube, g, dev, torch):
             tube.fetch(did, device=g, out=ys)
             b.record(s)
             b.synchronize()
+            # the same fetch's device time alone: enqueued while the stream is busy
+            # with a spin, so no host time sits between the events
+            did = tube.unique_id()
+            tube.store(did, xs)
+            torch.cuda.synchronize()
+            spin_ns(g, s, 300_000)
+            c, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            c.record(s)
+            tube.fetch(did, device=g, out=ys)
+            e.record(s)
+            e.synchronize()
             if r >= 2:
                 zc.append((t1 - t0) * 1e3)
                 cp.append(a.elapsed_time(b))
+                cpd.append(c.elapsed_time(e))
         zc.sort()
         cp.sort()
-        sweep.append({"bytes": n, "zero_copy_ms_p50": round(nearest_rank(zc, 50), 4),
+        cpd.sort()
+        sweep.append({"bytes": n, "copy_device_ms_p50": round(nearest_rank(cpd, 50), 5),
+                      "copy_device_gbps": round(n / (nearest_rank(cpd, 50) * 1e-3) / 1e9, 2),
+                      "zero_copy_ms_p50": round(nearest_rank(zc, 50), 4),
                       "zero_copy_ms_p99": round(nearest_rank(zc, 99), 4),
                       "copy_ms_p50": round(nearest_rank(cp, 50), 5), "copy_ms_p99": round(nearest_rank(cp, 99), 5),
                       "copy_gbps": round(n / (nearest_rank(cp, 50) * 1e-3) / 1e9, 2)})
@@ -1205,19 +1220,19 @@ def _single_gpu_extras(tube, g, dev, torch):
         for mode in ("one_by_one", "fetch_many"):
             ts = []
             for r in range(4):
-                ids = []
+                items = []
                 for j in range(k):
                     d = tube.unique_id()
                     tube.store(d, xs[j], producer="p")
-                    ids.append(d)
+                    items.append((d, ys[j]))              # the consumers' input buffers exist already
                 torch.cuda.synchronize()
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a.record(s)
                 if mode == "fetch_many":
-                    tube.fetch_many([(d, ys[j]) for j, d in enumerate(ids)])
+                    tube.fetch_many(items)
                 else:
-                    for j, d in enumerate(ids):
-                        tube.fetch(d, device=g, out=ys[j])
+                    for d, y in items:
+                        tube.fetch(d, device=g, out=y)
                 b.record(s)
                 b.synchronize()
                 if r:

@@ -183,6 +183,13 @@ def copy_batch(segments, device: int, stream=None):
     LIB.ft_copy_batch(C.cast(arr, C.POINTER(SegmentC)), len(segments), int(device), C.c_void_p(stream_ptr(stream)))
 
 
+def copy_batch_flat(flat, device: int, stream=None):
+    """``copy_batch`` with the segments already flat: [dst, src, nbytes, dst, src, nbytes, ...]."""
+    from ._lib import SegmentC
+    arr = (C.c_uint64 * len(flat))(*flat)
+    LIB.ft_copy_batch(C.cast(arr, C.POINTER(SegmentC)), len(flat) // 3, int(device), C.c_void_p(stream_ptr(stream)))
+
+
 def _needed(stream: int, events) -> list:
     """The waits ``stream`` needs for ``events``: none for one recorded on the
     stream itself (stream order), and per other stream only the newest record

@@ -776,42 +776,52 @@ class FaaSTube:
                 obj = objs.get(did)
                 if (obj is not None and obj.block is not None and obj.gpu == out.get_device()
                         and out.nbytes == obj.nbytes and out.is_contiguous()):
-                    by_gpu.setdefault(obj.gpu, []).append((obj, out))
+                    g = by_gpu.get(obj.gpu)
+                    if g is None:
+                        g = by_gpu[obj.gpu] = ([], [], [])     # objects, ready events, flat segments
+                    g[0].append(obj)
+                    g[1].append(obj.ready)
+                    g[2] += (out.data_ptr(), obj.block.ptr, obj.nbytes)
                 else:
                     rest.append((did, out))
-            for g, group in by_gpu.items():
+            for g, (group, readies, flat) in by_gpu.items():
                 s = self._stream(g)
-                dev.wait_events(s, [o.ready for o, _ in group])
-                dev.copy_batch([(out.data_ptr(), o.block.ptr, o.nbytes) for o, out in group], g, s)
+                dev.wait_events(s, readies)
+                dev.copy_batch_flat(flat, g, s)
                 done = dev.Ev(g).record(s)     # one fence for every block the batch read
                 retiring = []
                 nb = 0
-                for o, _ in group:
+                for o in group:
                     nb += o.nbytes
                     o.remaining -= 1
                     if o.remaining <= 0 and o.pins == 0 and not o.retired:
                         retiring.append(o)
                     else:
-                        self._hold_until(o, done)   # the last consumer's retire fences on this read
+                        o.readers.append(done)      # the last consumer's retire fences on this read
                         if o.remaining <= 0:
                             self._retire(o, done)
                 self.stats["bytes_local"] += nb
                 self.stats["fetches"] += len(group)
                 if retiring:
                     # every last consumer's retire in one native call (dataplane.py:98-101,
-                    # datastore.py:146-149), fenced on the batch's read + earlier readers
+                    # datastore.py:146-149), fenced on the batch's read + earlier readers (the
+                    # batch's stream waited on each object's `ready` before `done`)
+                    fence1 = (done,)
                     res = self.pools[g].retire_many(self.index, [
-                        (o.did, o.block, o.producer, (done,) + tuple(o.readers) + ((o.ready,) if o.ready else ()))
+                        (o.did, o.block, o.producer, fence1 + tuple(o.readers) if o.readers else fence1)
                         for o in retiring])
                     due = {}
-                    for o, (rw, last) in zip(retiring, res):
+                    meta, live, freed = self.index._meta, self._live, 0
+                    for o, rl in zip(retiring, res):
                         o.retired = True
                         o.readers = []
-                        if self._objs.pop(o.did, None) is not None:
-                            self._account(o, -1)
+                        if objs.pop(o.did, None) is not None:
+                            live[(o.producer, g)] -= 1
+                            freed += o.nbytes
                         o.block = None
-                        self.index._meta.pop(o.did, None)
-                        due[o.producer] = (rw, last)      # one shrink timer per producer
+                        meta.pop(o.did, None)
+                        due[o.producer] = rl                  # one shrink timer per producer
+                    self._stored[g] -= freed
                     for rw, last in due.values():
                         self._push_due(g, rw, last, self._last_op_ms)
                     if self.strategy.migration != "none" and self._off_gpu[g]:

@@ -51,9 +51,10 @@ for r in range(20):
         d = tube.unique_id()
         tube.store(d, xs[j])
         ids.append(d)
+    items = [(d, ys[j]) for j, d in enumerate(ids)]
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    tube.fetch_many([(d, ys[j]) for j, d in enumerate(ids)])
+    tube.fetch_many(items)
     ts.append(time.perf_counter() - t0)
 torch.cuda.synchronize()
 assert torch.equal(xs, ys)
@@ -70,9 +71,10 @@ for r in range(10):
         d = tube.unique_id()
         tube.store(d, xs[j])
         ids.append(d)
+    items = [(d, ys[j]) for j, d in enumerate(ids)]
     torch.cuda.synchronize()
     pr.enable()
-    tube.fetch_many([(d, ys[j]) for j, d in enumerate(ids)])
+    tube.fetch_many(items)
     pr.disable()
 print("---- fetch_many profile")
 pstats.Stats(pr).sort_stats("tottime").print_stats(20)

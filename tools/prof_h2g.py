@@ -37,6 +37,32 @@ for n in (4096, 1 << 20):
             st.append(t1 - t0)
             ft.append(t2 - t1)
             dv.append(a.elapsed_time(b))
+    # A/B: the same stage submitted straight to the pacer (no tube bookkeeping), routes
+    # from the native planner vs a Python-built route list
+    from paper_2411_01830_b200._lib import RouteC
+    import ctypes as C
+    routes, k, mg, cap, nv = (RouteC * 16)(), C.c_int(), C.c_int(), C.c_double(), C.c_uint64()
+    ab = {"native": [], "python": []}
+    for i in range(400):
+        mode = "native" if i % 2 else "python"
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(s)
+        sp = s.cuda_stream
+        if mode == "native":
+            dev.LIB.ft_h2g_routes(tube.plane._h, 0, 0, n, C.c_void_p(sp), routes, 16, C.byref(k), C.byref(mg),
+                                  C.byref(cap), C.byref(nv))
+            tube.pacer.submit_routes("", bool(mg.value), 1e9, 0.0, cap.value, dst.data_ptr(), 0, host.data_ptr(), n,
+                                     True, k.value, routes, sp)
+        else:
+            ce, fw = tube._pair(0, (sp >> 4) * 0x9E3779B1 >> 16)
+            tube.pacer.submit("", True, 1e9, 0.0, 55.0, dst.data_ptr(), 0, host.data_ptr(), n, True,
+                              [(0, 0, 0, n, ce.cuda_stream, fw.cuda_stream)], sp)
+        b.record(s)
+        b.synchronize()
+        if i >= 100:
+            ab[mode].append(a.elapsed_time(b))
+    print(f"bytes={n} pacer-only dev_ms native={statistics.median(ab['native']):.4f} "
+          f"python={statistics.median(ab['python']):.4f} (managed={mg.value} cap={cap.value})")
     plan_t = []
     for i in range(600):
         t0 = time.perf_counter()
