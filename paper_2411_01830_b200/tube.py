@@ -781,7 +781,7 @@ class FaaSTube:
                         g = by_gpu[obj.gpu] = ([], [], [])     # objects, ready events, flat segments
                     g[0].append(obj)
                     g[1].append(obj.ready)
-                    g[2] += (out.data_ptr(), obj.block.ptr, obj.nbytes)
+                    g[2].extend((out.data_ptr(), obj.block.ptr, obj.nbytes))
                 else:
                     rest.append((did, out))
             for g, (group, readies, flat) in by_gpu.items():
