@@ -349,6 +349,66 @@ int ft_chan_send(ft_chan* c, int dir, const void* buf, uint32_t n, int64_t timeo
 int ft_chan_recv(ft_chan* c, int dir, void* buf, uint32_t cap, uint32_t* n, int64_t spin_us, int64_t timeout_us);
 int ft_chan_close(ft_chan* c);
 
+/* The daemon's native lane (csrc/lane.cc): one C++ worker
+ * per function connection serves the hot requests that arrive as binary messages on
+ * the connection's rings — unique_id (dataplane.py:69-70), commit of a lent pool
+ * block = FaaSTube.store zero copy (engine.py:342-360) + the lend of the producer's
+ * next block, same-GPU zero-copy fetch (dataplane.py:184-185, engine.py:667-679) and
+ * its release — and hands every other request to the connection's Python thread
+ * (ft_lane_conn_next, then one of reply / reply_bin / finish). The tube's decisions
+ * for lane objects (histogram sample, accounting, shrink timer, cap check, pool
+ * frees, stock refills) run in Python from the ordered event queue (ft_lane_events);
+ * index entries are written by the lane at once. The tube adopts a lane object into
+ * its own table with ft_lane_take. */
+typedef struct ft_lane ft_lane;
+typedef struct ft_lane_conn ft_lane_conn;
+#pragma pack(push, 1)
+typedef struct {         /* one event record (+ name_len bytes of producer name)         */
+  uint32_t kind;         /* 1 committed, 2 retired, 3 freed, 4 stock, 5 unpin            */
+  uint32_t name_len;
+  int64_t data_id;
+  int32_t gpu, consumers;
+  int64_t block_id;      /* pool policy block id                                          */
+  uint64_t nbytes;       /* object bytes (stock: the size class wanted)                   */
+  double now_ms;         /* committed: the store time on the tube's clock                 */
+  uint64_t event;        /* freed / unpin: cudaEvent_t fence, owned by the receiver       */
+} ft_lane_event;
+#pragma pack(pop)
+typedef struct {
+  int64_t data_id, block_id;
+  uint64_t nbytes;
+  double stored_at_ms;
+  void* ready;           /* cudaEvent_t, owned by the taker */
+  int32_t gpu, dtype, ndim, remaining, pins, consumers;
+} ft_lane_obj;
+int ft_lane_create(ft_index* index, int node, double t0_s, ft_lane** out);
+int ft_lane_set_pool(ft_lane* lane, int gpu, ft_vmm_pool* pool);
+int ft_lane_destroy(ft_lane* lane);
+int ft_lane_attach(ft_lane* lane, ft_chan* ch, int sock, ft_lane_conn** out);
+int ft_lane_conn_set_gpu(ft_lane_conn* c, int gpu, void* stream, void* const* mine, void* const* peer, int k);
+int ft_lane_conn_next(ft_lane_conn* c, void* buf, uint32_t cap, uint32_t* n, int64_t timeout_us);
+int ft_lane_conn_served(ft_lane_conn* c, uint32_t* next_acked);
+int ft_lane_conn_reply(ft_lane_conn* c, const void* msg, uint32_t n);
+int ft_lane_conn_reply_bin(ft_lane_conn* c, const void* payload, uint32_t n, int ok, int fd);
+int ft_lane_conn_finish(ft_lane_conn* c);
+int ft_lane_conn_mark(ft_lane_conn* c, int* ev);
+int ft_lane_conn_known(ft_lane_conn* c, int gpu, uint64_t arena, int* known);
+int ft_lane_conn_take_drops(ft_lane_conn* c, uint64_t* arenas, int cap, int* n);
+int ft_lane_conn_release(ft_lane_conn* c, uint64_t token);
+int ft_lane_conn_close(ft_lane_conn* c);
+int ft_lane_dropped(ft_lane* lane, int gpu, uint64_t arena);
+int ft_lane_lend(ft_lane_conn* c, int64_t block_id, uint64_t vmm_block, void* ptr, uint64_t class_bytes,
+                 uint64_t arena, uint64_t offset, uint64_t arena_bytes, uint64_t* token);
+int ft_lane_take_lend(ft_lane_conn* c, uint64_t token, int64_t* block_id);
+int ft_lane_stock_put(ft_lane* lane, int gpu, int64_t block_id, uint64_t vmm_block, void* ptr, uint64_t class_bytes,
+                      uint64_t arena, uint64_t offset, uint64_t arena_bytes, void* const* fences, int n_fences);
+int ft_lane_stock_drain(ft_lane* lane, int64_t* block_ids, int cap, int* n);
+int ft_lane_events(ft_lane* lane, void* buf, uint64_t cap, uint64_t* n, int64_t timeout_us);
+int ft_lane_take(ft_lane* lane, int64_t data_id, ft_lane_obj* out, int64_t* shape, char* producer, int producer_cap);
+int ft_lane_ids(ft_lane* lane, int gpu, int64_t* ids, int cap, int* n);
+/* commits, fetches, dones, unique ids, handed to Python, stock hits, stock misses, adopted */
+int ft_lane_stats(ft_lane* lane, uint64_t* out, int cap);
+
 /* ---- movers
  * K1/K3 ft_copy: SM-driven bulk copy (TMA cp.async.bulk global->smem->global,
  * mbarrier ring, persistent grid) for same-GPU handoff copies and NVLink

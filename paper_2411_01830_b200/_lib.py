@@ -243,6 +243,30 @@ _SIGS = {
     "ft_plane_set_pairs": (None, [vp, C.c_int, C.c_int, P(vp), P(vp)]),
     "ft_h2g_routes": (None, [vp, C.c_int, C.c_int, u64, vp, vp, C.c_int, P(C.c_int), P(C.c_int), P(dbl),
                              P(u64)]),
+    "ft_lane_create": (None, [vp, C.c_int, dbl, P(vp)]),
+    "ft_lane_set_pool": (None, [vp, C.c_int, vp]),
+    "ft_lane_destroy": (None, [vp]),
+    "ft_lane_attach": (None, [vp, vp, C.c_int, P(vp)]),
+    "ft_lane_conn_set_gpu": (None, [vp, C.c_int, vp, P(vp), P(vp), C.c_int]),
+    "ft_lane_conn_next": (None, [vp, vp, C.c_uint32, P(C.c_uint32), i64]),
+    "ft_lane_conn_served": (None, [vp, P(C.c_uint32)]),
+    "ft_lane_conn_reply": (None, [vp, C.c_char_p, C.c_uint32]),
+    "ft_lane_conn_reply_bin": (None, [vp, C.c_char_p, C.c_uint32, C.c_int, C.c_int]),
+    "ft_lane_conn_finish": (None, [vp]),
+    "ft_lane_conn_mark": (None, [vp, P(C.c_int)]),
+    "ft_lane_conn_known": (None, [vp, C.c_int, u64, P(C.c_int)]),
+    "ft_lane_conn_take_drops": (None, [vp, P(u64), C.c_int, P(C.c_int)]),
+    "ft_lane_conn_release": (None, [vp, u64]),
+    "ft_lane_conn_close": (None, [vp]),
+    "ft_lane_dropped": (None, [vp, C.c_int, u64]),
+    "ft_lane_lend": (None, [vp, i64, u64, vp, u64, u64, u64, u64, P(u64)]),
+    "ft_lane_take_lend": (None, [vp, u64, P(i64)]),
+    "ft_lane_stock_put": (None, [vp, C.c_int, i64, u64, vp, u64, u64, u64, u64, P(vp), C.c_int]),
+    "ft_lane_stock_drain": (None, [vp, P(i64), C.c_int, P(C.c_int)]),
+    "ft_lane_events": (None, [vp, vp, u64, P(u64), i64]),
+    "ft_lane_take": (None, [vp, i64, vp, P(i64), C.c_char_p, C.c_int]),
+    "ft_lane_ids": (None, [vp, C.c_int, P(i64), C.c_int, P(C.c_int)]),
+    "ft_lane_stats": (None, [vp, P(u64), C.c_int]),
     "ft_chan_create": (None, [C.c_uint32, C.c_uint32, P(C.c_int), P(vp)]),
     "ft_chan_attach": (None, [C.c_int, P(vp)]),
     "ft_chan_send": (None, [vp, C.c_int, C.c_char_p, C.c_uint32, i64]),

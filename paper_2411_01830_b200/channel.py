@@ -114,6 +114,25 @@ class Channel:
             return
         self.sock.sendall(_HDR.pack(len(body)) + body)
 
+    def send_raw(self, body: bytes):
+        """One binary message on the rings (the native lane's protocol)."""
+        rc = LIB.raw("ft_chan_send")(self._chan, self._dir, body, len(body), -1)
+        if rc == 13:
+            raise ConnectionError("channel closed")
+        if rc:
+            raise_status(rc)
+
+    def recv_raw(self, spin_us: int = SPIN_US) -> bytes:
+        while True:
+            rc = LIB.raw("ft_chan_recv")(self._chan, 1 - self._dir, self._buf, _SLOT, self._n, spin_us, _POLL_US)
+            if rc == 0:
+                return self._buf.raw[:self._n.value]
+            if rc == 13:
+                raise ConnectionError("channel closed")
+            if rc != 12:
+                raise_status(rc)
+            self._check_peer()
+
     def recv_msg(self, spin_us: int = SPIN_US) -> dict:
         if self._chan is None:
             n = _HDR.unpack(self._recv_exact(4))[0]

@@ -5,6 +5,7 @@
 
 #include <deque>
 #include <memory>
+#include <mutex>
 #include <set>
 #include <string>
 #include <vector>
@@ -164,7 +165,13 @@ struct Index {
   struct Entry { int64_t id; double size; int node, gpu; double created; std::string producer; bool response; double visible; };
   std::map<int, std::map<int64_t, std::shared_ptr<Entry>>> local;
   std::map<int64_t, std::shared_ptr<Entry>> table;
-  int64_t unique_id() { return counter++; }
+  // the daemon's native lane (lane.cc) stores, drops and mints ids from its worker
+  // threads while the tube calls in from Python: every method takes the lock
+  std::mutex mu;
+  int64_t unique_id() {
+    std::lock_guard<std::mutex> lk(mu);
+    return counter++;
+  }
   double store(int64_t id, int node, int gpu, double size, double now, const std::string& producer, bool resp);
   std::shared_ptr<Entry> resolve(int64_t id, int node, double now, double* cost, double* ready);
   void drop(int64_t id);

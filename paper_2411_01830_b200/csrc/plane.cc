@@ -10,6 +10,7 @@ namespace ft {
 // ------------------------------------------------------------ DataIndex
 double Index::store(int64_t id, int node, int gpu, double size, double now, const std::string& producer,
                     bool resp) {  // dataplane.py:72-83
+  std::lock_guard<std::mutex> lk(mu);
   auto& t = local[node];
   if (t.count(id) || table.count(id)) fail(FT_E_DUPLICATE, "data id " + std::to_string(id) + " already stored");
   double vis = sync > 0 ? (double)((int64_t)py_floordiv(now, sync) + 1) * sync : now;
@@ -20,6 +21,7 @@ double Index::store(int64_t id, int node, int gpu, double size, double now, cons
 }
 std::shared_ptr<Index::Entry> Index::resolve(int64_t id, int node, double now, double* cost,
                                              double* ready) {  // dataplane.py:85-96
+  std::lock_guard<std::mutex> lk(mu);
   auto lt = local.find(node);
   if (lt != local.end()) {
     auto it = lt->second.find(id);
@@ -36,6 +38,7 @@ std::shared_ptr<Index::Entry> Index::resolve(int64_t id, int node, double now, d
   return it->second;
 }
 void Index::drop(int64_t id) {  // dataplane.py:98-101
+  std::lock_guard<std::mutex> lk(mu);
   auto it = table.find(id);
   if (it == table.end()) return;
   auto e = it->second;
@@ -44,6 +47,7 @@ void Index::drop(int64_t id) {  // dataplane.py:98-101
   if (lt != local.end()) lt->second.erase(id);
 }
 void Index::relocate(int64_t id, int node, int gpu) {  // dataplane.py:103-107
+  std::lock_guard<std::mutex> lk(mu);
   auto it = table.find(id);
   if (it == table.end()) fail(FT_E_KEY, "data id " + std::to_string(id) + " not in the global table");
   auto e = it->second;

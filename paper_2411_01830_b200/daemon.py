@@ -50,20 +50,36 @@ size class, so a steady stream of requests maps and exports nothing new.
 from __future__ import annotations
 
 import contextlib
+import ctypes as C
 import itertools
 import math
 import mmap
 import os
+import struct
 import threading
 import weakref
 
 import torch
 
 from . import device as dev
+import msgpack
+
 from .channel import Channel
 
 _DTYPES = {str(t): t for t in (torch.uint8, torch.int8, torch.int16, torch.int32, torch.int64, torch.float16,
                                torch.bfloat16, torch.float32, torch.float64, torch.bool)}
+# binary messages of the native lane (csrc/lane.cc): dtype codes and packed structs
+_CODES = (torch.uint8, torch.int8, torch.int16, torch.int32, torch.int64, torch.float16, torch.bfloat16,
+          torch.float32, torch.float64, torch.bool)
+_CODE = {t: i for i, t in enumerate(_CODES)}
+OP_COMMIT, OP_FETCH, OP_DONE, OP_UID = 1, 2, 3, 4
+_COMMIT = struct.Struct("<BBBBiiIQqQ")
+_FETCH = struct.Struct("<B3xiqdd")
+_DONE = struct.Struct("<B3xiQ")
+_REPHDR = struct.Struct("<BBBxIII")
+_BLOCKREP = struct.Struct("<QQQQQiBBBx")
+_REP_KIND = 0xB1
+_NATIVE_TOKENS = 1 << 62       # tokens at or above are the lane's
 
 
 def _memfd(data: torch.Tensor) -> int:
@@ -111,10 +127,15 @@ class _Lend:
 
 
 class _Conn:
-    __slots__ = ("ch", "tokens", "mapped", "drop", "gpu", "stream", "mine", "peer", "served", "seen")
+    __slots__ = ("ch", "tokens", "mapped", "drop", "gpu", "stream", "mine", "peer", "served", "seen", "lc",
+                 "chan", "bin", "buf")
 
     def __init__(self, ch):
         self.ch = ch
+        self.lc = None           # ft_lane_conn: a native worker reads this connection's requests
+        self.chan = None         # its ft_chan (closed after the worker)
+        self.bin = False         # the request being served arrived as a binary message
+        self.buf = None
         self.tokens = set()      # loans of this connection (dropped if the client dies)
         self.mapped = set()      # (gpu, block id) the client has mapped
         self.drop = []           # block ids to unmap, sent with the next reply
@@ -135,6 +156,10 @@ class _Conn:
         """Record one of the daemon's events on the connection stream (-1: no events)."""
         if self.mine is None:
             return -1
+        if self.lc is not None:                # one mark ring, shared with the native worker
+            i = C.c_int()
+            dev.LIB.ft_lane_conn_mark(self.lc, C.byref(i))
+            return i.value
         i = self.mine.take()
         self.mine.record(i, self.stream)
         return i
@@ -154,7 +179,7 @@ class _Conn:
 class TubeDaemon:
     """Serves the put/get API of ``tube`` to function processes on ``path``."""
 
-    def __init__(self, tube, path: str):
+    def __init__(self, tube, path: str, lane: bool = True):
         self.tube, self.path = tube, path
         self.server = Channel.listen(path)
         self._tokens = itertools.count(1)
@@ -165,8 +190,29 @@ class TubeDaemon:
         self._conns = []
         for g, pool in tube.pools.items():
             pool.on_unmap.append(lambda vid, g=g: self._dropped(g, vid))
+        # the native lane serves the hot requests of upgraded connections (csrc/lane.cc);
+        # its events are applied to the tube by the service thread
+        self._lane = None
+        if lane and hasattr(tube, "attach_lane") and tube.pools:
+            h = C.c_void_p()
+            dev.LIB.ft_lane_create(tube.index._h, int(tube.node), float(tube._t0), C.byref(h))  # noqa: SLF001
+            for g, pool in tube.pools.items():
+                dev.LIB.ft_lane_set_pool(h, int(g), pool._h)  # noqa: SLF001
+            tube.attach_lane(h)
+            self._lane = h
+            self._service = threading.Thread(target=self._service_loop, name="faastube-lane", daemon=True)
+            self._service.start()
         self._acceptor = threading.Thread(target=self._accept_loop, name="faastube-daemon", daemon=True)
         self._acceptor.start()
+
+    def _service_loop(self):
+        import traceback
+        while not self._closing:
+            try:
+                if not self.tube.lane_service(50.0):
+                    return
+            except Exception:  # noqa: BLE001 - keep serving; the failure is visible in the log
+                traceback.print_exc()
 
     def _accept_loop(self):
         while not self._closing:
@@ -179,6 +225,8 @@ class TubeDaemon:
             self._threads = [t for t in self._threads if t.is_alive()] + [th]
 
     def _dropped(self, g, vid):
+        if self._lane is not None:
+            dev.LIB.ft_lane_dropped(self._lane, int(g), int(vid))
         with self._lock:
             for conn in self._conns:
                 if (g, vid) in conn.mapped:
@@ -227,30 +275,71 @@ class TubeDaemon:
             self._conns.append(conn)
         try:
             while True:
-                msg = ch.recv_msg()
+                msg = ch.recv_msg() if conn.lc is None else self._lane_recv(conn)
                 conn.seen += 1
                 try:
                     self._handle(conn, msg)
                 except Exception as exc:  # noqa: BLE001 - the error travels back to the caller
                     if msg.get("op") == "done":        # fire-and-forget: nobody waits for a reply
+                        if conn.lc is not None:
+                            dev.LIB.ft_lane_conn_finish(conn.lc)
                         conn.served = max(conn.served, conn.seen)
                         continue
-                    conn.served += 1
-                    ch.send_msg({"ok": False, "error": type(exc).__name__, "msg": str(exc), "acked": conn.served})
+                    self._reply_error(conn, msg, exc)
         except (ConnectionError, OSError):
             pass
         finally:
             with self._lock:
                 self._conns.remove(conn)
+            if conn.lc is not None:
+                # the worker stops (its native loans and views are released on the
+                # connection stream) before anything it uses is torn down
+                dev.LIB.ft_lane_conn_close(conn.lc)
+                conn.lc = None
             with conn.ctx():
                 for tok in list(conn.tokens):      # a client that died drops its loans
                     self._unhold(conn, tok)
             if conn.stream is not None:
                 conn.stream.synchronize()
             conn.close()
+            if conn.chan is not None:
+                dev.LIB.ft_chan_close(conn.chan)
+                conn.chan = None
             ch.close()
 
+    # ---- the native lane's connections
+    def _lane_recv(self, conn) -> dict:
+        """The next request the connection's worker handed over (binary or msgpack)."""
+        n = C.c_uint32()
+        rc = dev.LIB.raw("ft_lane_conn_next")(conn.lc, conn.buf, len(conn.buf), C.byref(n), -1)
+        if rc == 13:
+            raise ConnectionError("client gone")
+        if rc:
+            from ._lib import raise_status
+            raise_status(rc)
+        raw = conn.buf.raw[:n.value]
+        conn.bin = raw[:1] in (b"\x01", b"\x02", b"\x03", b"\x04")
+        return _decode_bin(raw) if conn.bin else msgpack.unpackb(raw)
+
+    def _reply_error(self, conn, msg, exc):
+        name, text = type(exc).__name__, str(exc)
+        if conn.lc is None:
+            conn.served += 1
+            conn.ch.send_msg({"ok": False, "error": name, "msg": text, "acked": conn.served})
+        elif conn.bin:
+            nb, tb = name.encode(), text.encode()
+            p = struct.pack("<I", len(nb)) + nb + struct.pack("<I", len(tb)) + tb
+            dev.LIB.ft_lane_conn_reply_bin(conn.lc, p, len(p), 0, -1)
+        else:
+            acked = C.c_uint32()
+            dev.LIB.ft_lane_conn_served(conn.lc, C.byref(acked))
+            body = msgpack.packb({"ok": False, "error": name, "msg": text, "acked": acked.value})
+            dev.LIB.ft_lane_conn_reply(conn.lc, body, len(body))
+
     def _reply(self, conn, meta, fd=None):
+        if conn.lc is not None:
+            self._lane_reply(conn, meta, fd)
+            return
         with self._lock:
             drop, conn.drop = conn.drop, []
         conn.served += 1
@@ -258,15 +347,36 @@ class TubeDaemon:
         if fd is not None:
             conn.ch.send_fd(fd, {})
 
+    def _lane_reply(self, conn, meta, fd):
+        """A reply to a request the worker handed over: binary for a binary request
+        (the lane adds the header: acked, unmap notices, the fd), else msgpack."""
+        if conn.bin:
+            p = _encode_bin_reply(meta)
+            dev.LIB.ft_lane_conn_reply_bin(conn.lc, p, len(p), 1, -1 if fd is None else int(fd))
+            return
+        ids, n = (C.c_uint64 * 256)(), C.c_int()
+        dev.LIB.ft_lane_conn_take_drops(conn.lc, ids, 256, C.byref(n))
+        acked = C.c_uint32()
+        dev.LIB.ft_lane_conn_served(conn.lc, C.byref(acked))
+        body = msgpack.packb(dict(meta, ok=True, fd=fd is not None, drop=list(ids[:n.value]), acked=acked.value))
+        if fd is not None:
+            conn.ch.send_fd(fd, {})            # ahead of the reply: the client reads it right after
+        dev.LIB.ft_lane_conn_reply(conn.lc, body, len(body))
+
     def _reply_block(self, conn, g, blk, meta):
         # the client maps the block's arena once (the unit of physical memory) and
         # finds the block at its offset
         arena, off, abytes = self.tube.pools[g].locate(blk)
         key = (g, int(arena))
         meta = dict(meta, block=key[1], off=int(off), block_bytes=int(abytes))
-        with self._lock:
-            known = key in conn.mapped
-            conn.mapped.add(key)
+        if conn.lc is not None:
+            k = C.c_int()
+            dev.LIB.ft_lane_conn_known(conn.lc, g, key[1], C.byref(k))
+            known = bool(k.value)
+        else:
+            with self._lock:
+                known = key in conn.mapped
+                conn.mapped.add(key)
         if known:                              # the client has it mapped already
             self._reply(conn, meta)
             return
@@ -288,28 +398,54 @@ class TubeDaemon:
         ev = conn.mark()
         if ev < 0:
             self.tube.sync_stream(g)
-        return {"token": self._hold(conn, _Lend(blk)), "nbytes": n, "ev": ev, "_blk": blk}
+        if conn.lc is not None and conn.gpu == g:
+            tok = self.tube.lane_lend(conn.lc, blk)    # its commit is served by the worker
+        else:
+            tok = self._hold(conn, _Lend(blk))
+        return {"token": tok, "nbytes": n, "ev": ev, "_blk": blk}
 
     def _handle(self, conn, msg: dict):
         tube, op, ch = self.tube, msg["op"], conn.ch
         if op == "unique_id":
             self._reply(conn, {"id": tube.unique_id()})
         elif op == "chan":                     # messages move to the client's shared-memory rings
-            ch.attach()
-            self._reply(conn, {})
+            if self._lane is None:
+                ch.attach()
+                self._reply(conn, {"lane": False})
+                return
+            fd, _ = dev.recv_fd(ch.sock)
+            h, lc = C.c_void_p(), C.c_void_p()
+            try:
+                dev.LIB.ft_chan_attach(fd, C.byref(h))
+            finally:
+                os.close(fd)
+            conn.chan = h
+            conn.buf = C.create_string_buffer(1 << 16)
+            dev.LIB.ft_lane_attach(self._lane, h, ch.sock.fileno(), C.byref(lc))
+            conn.lc = lc                       # a native worker reads the rings from here on
+            self._reply(conn, {"lane": True})
         elif op == "hello":
             g = int(msg["gpu"])
             conn.gpu = g
             conn.stream = dev.new_stream(g)
             conn.peer = dev.PeerEvents(g, msg.get("ev", []))
             conn.mine = dev.IpcEventRing(g)
+            if conn.lc is not None:
+                k = len(conn.mine.h)
+                dev.LIB.ft_lane_conn_set_gpu(conn.lc, g, C.c_void_p(conn.stream.cuda_stream),
+                                             (C.c_void_p * k)(*conn.mine.h), (C.c_void_p * k)(*conn.peer.h), k)
             self._reply(conn, {"ev": conn.mine.handles})
         elif op == "alloc":
             g, n = int(msg["gpu"]), int(msg["nbytes"])
             meta = self._lend(conn, g, n)
             self._reply_block(conn, g, meta.pop("_blk"), meta)
         elif op == "commit":
-            t = self._take(conn, int(msg["token"]))
+            tok = int(msg["token"])
+            t = self._take(conn, tok)
+            if t is None and conn.lc is not None and tok >= _NATIVE_TOKENS:
+                pbid = C.c_int64()                 # a lane loan this request needs served here
+                dev.LIB.ft_lane_take_lend(conn.lc, tok, C.byref(pbid))
+                t = _Lend(tube.lane_block(pbid.value))
             if not isinstance(t, _Lend):
                 raise KeyError(f"unknown token {msg['token']}")
             conn.wait_peer(msg.get("ev"))      # the client's copy into the block is done (stream-ordered)
@@ -374,8 +510,16 @@ class TubeDaemon:
                 os.close(fd)
         elif op == "done":                     # no reply (the client does not wait for it)
             conn.wait_peer(msg.get("ev"))      # the client's last read of the block (stream-ordered)
+            tok = int(msg["token"])
+            if conn.lc is not None:
+                if tok >= _NATIVE_TOKENS:
+                    dev.LIB.ft_lane_conn_release(conn.lc, tok)
+                else:
+                    self._unhold(conn, tok)
+                dev.LIB.ft_lane_conn_finish(conn.lc)
+                return
             conn.served += 1
-            self._unhold(conn, int(msg["token"]))
+            self._unhold(conn, tok)
         elif op == "release":
             with conn.ctx():
                 tube.release(int(msg["id"]))
@@ -387,7 +531,7 @@ class TubeDaemon:
         """A fetch that is not a same-GPU zero-copy read: into a pool block the
         client maps (on the connection's stream)."""
         tube = self.tube
-        obj = tube._objs.get(did)  # noqa: SLF001
+        obj = tube.peek(did)
         nbytes = obj.nbytes if obj is not None else 0
         dst = tube.empty((max(1, nbytes),), torch.uint8, device=g)
         try:
@@ -418,11 +562,56 @@ class TubeDaemon:
                 pass
         for th in self._threads:
             th.join(timeout=5)
+        if self._lane is not None:
+            self._service.join(timeout=5)
+            self.tube.detach_lane()            # its objects into the tube's table, stocked blocks back
+            dev.LIB.ft_lane_destroy(self._lane)
+            self._lane = None
         try:
             self.server.close()
         finally:
             if os.path.exists(self.path):
                 os.unlink(self.path)
+
+
+def _decode_bin(raw: bytes) -> dict:
+    """A binary request of the lane protocol (csrc/lane.cc) as the dict the handlers take."""
+    op = raw[0]
+    if op == OP_COMMIT:
+        _, dt, nd, resp, ev, cons, nl, tok, did, nxt = _COMMIT.unpack_from(raw)
+        shape = list(struct.unpack_from(f"<{nd}q", raw, _COMMIT.size))
+        name = raw[_COMMIT.size + 8 * nd:_COMMIT.size + 8 * nd + nl].decode()
+        return {"op": "commit", "token": tok, "id": did, "dtype": str(_CODES[dt]), "shape": shape,
+                "producer": name, "consumers": cons, "response": bool(resp), "ev": ev, "next": nxt or None}
+    if op == OP_FETCH:
+        _, g, did, slo, infer = _FETCH.unpack_from(raw)
+        return {"op": "fetch", "gpu": g, "id": did, "consumer": "func", "slo_ms": None if slo != slo else slo,
+                "infer_ms": None if infer != infer else infer}
+    if op == OP_DONE:
+        _, ev, tok = _DONE.unpack_from(raw)
+        return {"op": "done", "token": tok, "ev": ev}
+    return {"op": "unique_id"}
+
+
+def _encode_bin_reply(meta: dict) -> bytes:
+    """The payload of a binary reply (the lane prepends the header): a block
+    (fetch / alloc / a commit's loan), a bare commit, or an id."""
+    if "id" in meta and len(meta) == 1:
+        return struct.pack("<q", meta["id"])
+    if "block" not in meta:
+        return bytes(_BLOCKREP.size)                  # a commit without a loan
+    shape = meta.get("shape", [])
+    dt = _CODE[_DTYPES[meta["dtype"]]] if "dtype" in meta else 0
+    return _BLOCKREP.pack(meta["token"], meta["block"], meta["off"], meta["block_bytes"], meta["nbytes"],
+                          meta.get("ev", -1), dt, len(shape), int(bool(meta.get("loan")))) + \
+        struct.pack(f"<{len(shape)}q", *shape)
+
+
+def _parse_block_reply(p: bytes) -> dict:
+    tok, arena, off, abytes, nbytes, ev, dt, nd, loan = _BLOCKREP.unpack_from(p)
+    shape = list(struct.unpack_from(f"<{nd}q", p, _BLOCKREP.size))
+    return {"token": tok, "block": arena, "off": off, "block_bytes": abytes, "nbytes": nbytes, "ev": ev,
+            "dtype": str(_CODES[dt]), "shape": shape, "loan": bool(loan)}
 
 
 class DaemonError(RuntimeError):
@@ -460,11 +649,12 @@ class TubeClient:
         self._mine = self._peer = None
         self._closed = False
         self._views = 0              # zero-copy views handed out and not yet released
+        self._lane = False           # the daemon's native lane serves the hot requests (binary messages)
         if shm:                      # messages over shared-memory rings from here on (channel.py)
             with self._io:
                 self.ch.upgrade()
                 self._sent += 1
-                self._recv()
+                self._lane = bool(self._recv().get("lane"))
         if events:
             self._mine = dev.IpcEventRing(device)
             self._used = [0] * self._mine.k        # message number that carried each event's last record
@@ -472,6 +662,7 @@ class TubeClient:
             self._peer = dev.PeerEvents(device, rep["ev"])
         else:
             self._stream = dev.new_stream(device)
+        self._bin = self._lane and events      # binary requests need the stream-ordered protocol
 
     # ---- framing
     def _send(self, msg: dict):
@@ -483,6 +674,38 @@ class TubeClient:
         with self._io:
             self._send(msg)
             return self._recv()
+
+    def _call_bin(self, body: bytes) -> bytes:
+        """A binary request / reply of the native lane (csrc/lane.cc): header (acked,
+        unmap notices, an fd after the message), payload."""
+        with self._io:
+            self.ch.send_raw(body)
+            self._sent += 1
+            rep = self.ch.recv_raw()
+            kind, ok, has_fd, acked, n_drop, _ = _REPHDR.unpack_from(rep)
+            if kind != _REP_KIND:
+                raise DaemonError(f"unexpected reply kind {kind:#x}")
+            self._acked = max(self._acked, acked)
+            end = len(rep) - 8 * n_drop
+            for bid in struct.unpack_from(f"<{n_drop}Q", rep, end):
+                imp = self._imports.pop(bid, None)
+                if imp is not None:
+                    imp.close()
+            p = rep[_REPHDR.size:end]
+            if not ok:
+                n = struct.unpack_from("<I", p)[0]
+                name = p[4:4 + n].decode()
+                m = struct.unpack_from("<I", p, 4 + n)[0]
+                raise DaemonError(f"{name}: {p[8 + n:8 + n + m].decode()}")
+            fd = dev.recv_fd(self.ch.sock)[0] if has_fd else None
+        return p, fd
+
+    def _block_bin(self, body: bytes) -> dict:
+        p, fd = self._call_bin(body)
+        rep = _parse_block_reply(p)
+        if fd is not None:
+            rep["_fd"] = fd
+        return rep
 
     def _recv(self):
         rep = self.ch.recv_msg()
@@ -533,6 +756,8 @@ class TubeClient:
             self._peer.wait(int(ev), stream)
 
     def unique_id(self) -> int:
+        if self._bin:
+            return struct.unpack("<q", self._call_bin(b"\x04")[0])[0]
         return self._call({"op": "unique_id"})["id"]
 
     def store(self, data_id: int, output: torch.Tensor, response: bool = False, producer: str = "func",
@@ -568,11 +793,20 @@ class TubeClient:
         dev.copy(ptr, t.data_ptr(), n, self.device, cur)
         if t is not output or self._mine is None:
             t.record_stream(cur)
-        with self._io:                                # the mark rides on the very next message
-            ev = self._mark(cur)                      # written (or synchronised) before the daemon publishes it
-            rep = self._call({"op": "commit", "token": rep["token"], "id": data_id, "dtype": str(t.dtype),
-                              "shape": list(t.shape), "producer": producer, "consumers": consumers,
-                              "response": response, "ev": ev, **({"next": n} if self._mine is not None else {})})
+        if self._bin and not response and t.dtype in _CODE and t.dim() <= 8:
+            name = producer.encode()
+            with self._io:                            # the mark rides on the very next message
+                ev = self._mark(cur)
+                body = _COMMIT.pack(OP_COMMIT, _CODE[t.dtype], t.dim(), 0, ev, consumers, len(name), rep["token"],
+                                    data_id, n) + struct.pack(f"<{t.dim()}q", *t.shape) + name
+                rep = self._block_bin(body)
+        else:
+            with self._io:                            # the mark rides on the very next message
+                ev = self._mark(cur)                  # written (or synchronised) before the daemon publishes it
+                rep = self._call({"op": "commit", "token": rep["token"], "id": data_id, "dtype": str(t.dtype),
+                                  "shape": list(t.shape), "producer": producer, "consumers": consumers,
+                                  "response": response, "ev": ev,
+                                  **({"next": n} if self._mine is not None else {})})
         if rep.get("loan"):
             self._mapped(rep)
             self._loans[n] = rep
@@ -593,13 +827,18 @@ class TubeClient:
                 out.view(-1).view(torch.uint8).copy_(res.view(-1).view(torch.uint8))
                 return out
             return res
-        rep = self._call({"op": "fetch", "id": data_id, "gpu": self.device, "consumer": consumer,
-                          "slo_ms": slo_ms, "infer_ms": infer_ms})
+        if self._bin:
+            nan = float("nan")
+            rep = self._block_bin(_FETCH.pack(OP_FETCH, self.device, data_id, nan if slo_ms is None else slo_ms,
+                                              nan if infer_ms is None else infer_ms))
+        else:
+            rep = self._call({"op": "fetch", "id": data_id, "gpu": self.device, "consumer": consumer,
+                              "slo_ms": slo_ms, "infer_ms": infer_ms})
         imp = self._mapped(rep)
         ptr = imp.ptr + rep.get("off", 0)
         dt, shape, n = _DTYPES[rep["dtype"]], rep["shape"], rep["nbytes"]
         if out is not None and (not out.is_contiguous() or out.nbytes != n):
-            self._send({"op": "done", "token": rep["token"], "ev": -1})
+            self._done(rep["token"], -1)
             raise ValueError("out must be contiguous with exactly the stored byte count")
         if self._mine is not None:
             cur = torch.cuda.current_stream(self.device)
@@ -614,7 +853,7 @@ class TubeClient:
                 return dev.as_tensor(ptr, n, self.device, dt, tuple(shape), owner=owner)
             dev.copy(out.data_ptr(), ptr, n, self.device, cur)
             with self._io:
-                self._send({"op": "done", "token": rep["token"], "ev": self._mark(cur)})
+                self._done(rep["token"], self._mark(cur))
             return out
         # host-synced connection: copy on the private stream, synchronise, release
         if out is None:
@@ -634,9 +873,18 @@ class TubeClient:
         try:
             cur = torch.cuda.current_stream(self.device)
             with self._io:
-                self._send({"op": "done", "token": token, "ev": self._mark(cur)})
+                self._done(token, self._mark(cur))
         except Exception:  # noqa: BLE001 - the daemon drops a dead connection's loans itself
             pass
+
+    def _done(self, token: int, ev: int):
+        """Release a read block (no reply): binary to the lane, else msgpack."""
+        if self._bin:
+            with self._io:
+                self.ch.send_raw(_DONE.pack(OP_DONE, ev, token))
+                self._sent += 1
+        else:
+            self._send({"op": "done", "token": token, "ev": ev})
 
     def release(self, data_id: int):
         self._call({"op": "release", "id": data_id})

@@ -120,6 +120,14 @@ class Ev:
         LIB.ft_event_create(int(device), C.byref(h))
         self.h, self.device = h.value, device
 
+    @classmethod
+    def adopt(cls, handle: int, device: int) -> "Ev":
+        """An event recorded elsewhere (the daemon's native lane) whose handle this
+        process now owns: already recorded, on a stream unknown here."""
+        e = cls.__new__(cls)
+        e.h, e.device, e.rec, e.stream, e.seq = handle, device, True, None, next(Ev._seq)
+        return e
+
     def _recorded(self):
         if not self.rec:
             raise RuntimeError("event used before it was recorded (its work was never enqueued)")

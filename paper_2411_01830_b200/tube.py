@@ -40,6 +40,7 @@ import heapq
 import itertools
 import math
 import os
+import struct
 import threading
 import time
 import weakref
@@ -89,7 +90,14 @@ class _Obj:
         self.readers = []      # events of copies on other streams/GPUs that read the block
 
 
+_LANE_EV = struct.Struct("<IIqiiqQdQ")   # ft_lane_event (include/faastube.h)
+_LANE_DTYPES = (torch.uint8, torch.int8, torch.int16, torch.int32, torch.int64, torch.float16, torch.bfloat16,
+                torch.float32, torch.float64, torch.bool)
+
+
 class FaaSTube:
+    _lane = None                 # the daemon's native lane (attach_lane), if one serves this tube
+
     def __init__(self, strategy: str | Strategy = "faastube", topology: Topology | None = None,
                  pcie_gbps: float | str = "measure", chunk_bytes: int = CHUNK_BYTES, batch_chunks: int = BATCH_CHUNKS,
                  pool_floor_bytes: float = datastore.POOL_FLOOR_BYTES, node: int = 0, map_ms: float = 0.05,
@@ -471,6 +479,9 @@ class FaaSTube:
 
     def _accounts_consistent(self) -> bool:
         """The running counters equal a recount of the table (tests)."""
+        if self._lane is not None:
+            with self._lock:
+                self._lane_adopt(-1)
         live, stored, off = collections.Counter(), collections.Counter(), collections.Counter()
         for o in self._objs.values():
             if o.gpu is not None:
@@ -518,6 +529,8 @@ class FaaSTube:
                 if not self._pending:
                     return
                 kind, g = self._pending.pop()
+                if kind == "pressure" and self._lane is not None:
+                    self._lane_adopt(g)                   # the lane's objects on g are candidates too
                 chosen = self._plan_migration(g) if kind == "pressure" else self._plan_prefetch(g)
                 for o in chosen:
                     o.pins += 1
@@ -637,6 +650,8 @@ class FaaSTube:
         with self._lock:
             self._reap()
             obj = self._objs.get(data_id)
+            if obj is None and self._lane is not None:
+                obj = self._lane_take(data_id)
             self._last_op_ms = self.now_ms()
             if obj is None:
                 # the index's own miss (dataplane.py:85-96): MissingData / unknown id
@@ -743,6 +758,8 @@ class FaaSTube:
         reader's stream (default the current one). None if it lives elsewhere."""
         with self._lock:
             obj = self._objs.get(data_id)
+            if obj is None and self._lane is not None:
+                obj = self._lane_take(data_id)
             if obj is None or obj.gpu != device or obj.block is None:
                 return None
             self._reap()
@@ -850,6 +867,8 @@ class FaaSTube:
         """Drop a stored object regardless of remaining consumers."""
         with self._lock:
             obj = self._objs.get(data_id)
+            if obj is None and self._lane is not None:
+                obj = self._lane_take(data_id)
             if obj is not None:
                 obj.remaining = 0
                 self._retire(obj)
@@ -869,6 +888,8 @@ class FaaSTube:
         return obj.response_host.view(obj.dtype).view(obj.shape)
 
     def close(self):
+        if self._lane is not None:
+            self.detach_lane()
         self.pacer.close()                        # drains in-flight host->GPU stages
         self._tickets.clear()
         with self._maint_cv:
@@ -884,6 +905,185 @@ class FaaSTube:
             for st in self._ce[g] + [x for pr in self._ce_pairs[g] + self._d2h_pairs[g] for x in pr]:
                 dev.destroy_stream(st)
         dev.Ev.drain_free()
+
+    # ------------------------------------------------ the daemon's native lane
+    def attach_lane(self, lane):
+        """The daemon's native lane (csrc/lane.cc, ``ft_lane``) serves function
+        processes' hot requests — commits of lent blocks, same-GPU zero-copy fetches
+        and their releases — with C++ workers. Objects it commits live in its table
+        until their last view is released or this tube adopts them (``_lane_take``);
+        its events (committed / retired / freed / stock / unpin) are applied here in
+        order (``lane_service``)."""
+        self._lane = lane
+        self._lane_blocks = {}       # pool policy block id -> PoolBlock lent to / stocked in / stored by the lane
+        self._lane_adopted = {}      # data id -> adopted object whose lane views are still alive
+        self._lane_stock_todo = []   # (gpu, class bytes) the lane's stock asked for
+        self._lane_buf = dev.C.create_string_buffer(1 << 20)
+        self._lane_n = dev.C.c_uint64()
+
+    def detach_lane(self):
+        """Adopt every lane object and take the stocked blocks back (the daemon closed)."""
+        with self._lock:
+            self._lane_adopt(-1)
+            ids, n = (dev.C.c_int64 * 4096)(), dev.C.c_int()
+            dev.LIB.ft_lane_stock_drain(self._lane, ids, 4096, dev.C.byref(n))
+            for i in range(n.value):
+                blk = self._lane_blocks.pop(ids[i], None)
+                if blk is not None:
+                    self.pools[blk.device].free(blk, list(blk.fences))
+            self._lane_stock_todo = []
+            self._lane = None
+
+    def lane_service(self, timeout_ms: float = 50.0) -> bool:
+        """Wait for lane events, apply them, refill the stock it asked for (the
+        daemon's service thread calls this in a loop). False once detached."""
+        lane = self._lane
+        if lane is None:
+            return False
+        n = dev.C.c_uint64()
+        # cap 0: wait without consuming — events are consumed and applied under the tube
+        # lock so that the service thread and an adopting request apply them in order
+        dev.LIB.ft_lane_events(lane, None, 0, dev.C.byref(n), int(timeout_ms * 1e3))
+        with self._lock:
+            self._lane_sync()
+            todo, self._lane_stock_todo = self._lane_stock_todo, []
+        for g, cls in todo:
+            self._lane_stock(g, cls)
+        if self._pending:
+            self._drain_pending()
+        return True
+
+    def _lane_stock(self, g, cls):
+        """A lendable block of class ``cls`` for the lane's stock (allocated outside the
+        tube lock: growth may map memory)."""
+        lane = self._lane
+        if lane is None or g not in self.pools:
+            return
+        blk = self.pools[g].allocate(int(cls))
+        arena, off, abytes = self.pools[g].locate(blk)
+        fences = [e._recorded() for e in blk.fences]
+        with self._lock:
+            if self._lane is None:
+                self.pools[g].free(blk, list(blk.fences))
+                return
+            self._lane_blocks[blk.policy_block.block_id] = blk
+            dev.LIB.ft_lane_stock_put(lane, g, blk.policy_block.block_id, blk.vmm_id, dev.C.c_void_p(blk.ptr),
+                                      int(blk.policy_block.class_bytes), arena, off, abytes,
+                                      (dev.C.c_void_p * max(1, len(fences)))(*fences), len(fences))
+
+    def lane_lend(self, conn_lane, blk) -> int:
+        """Register a block lent through Python (the daemon's ``alloc``) with the lane:
+        the client's commit of it is then served natively. Returns the token."""
+        arena, off, abytes = self.pools[blk.device].locate(blk)
+        tok = dev.C.c_uint64()
+        with self._lock:
+            self._lane_blocks[blk.policy_block.block_id] = blk
+        dev.LIB.ft_lane_lend(conn_lane, blk.policy_block.block_id, blk.vmm_id, dev.C.c_void_p(blk.ptr),
+                             int(blk.policy_block.class_bytes), arena, off, abytes, dev.C.byref(tok))
+        return tok.value
+
+    def lane_block(self, block_id: int):
+        """(the daemon, serving a commit of a lane-lent block itself) the PoolBlock back."""
+        with self._lock:
+            return self._lane_blocks.pop(block_id)
+
+    def peek(self, data_id: int):
+        """The stored object's record (adopting it from the lane if it lives there), or None."""
+        with self._lock:
+            obj = self._objs.get(data_id)
+            if obj is None and self._lane is not None:
+                obj = self._lane_take(data_id)
+            return obj
+
+    def _lane_sync(self):
+        """(lock held) Apply the lane's queued events now, in order."""
+        n = self._lane_n
+        while True:
+            dev.LIB.ft_lane_events(self._lane, self._lane_buf, len(self._lane_buf), dev.C.byref(n), 0)
+            if not n.value:
+                return
+            self._lane_apply(self._lane_buf.raw[:n.value])
+
+    def _lane_apply(self, data: bytes):
+        """(lock held) COMMITTED: the histogram sample, live/stored accounting, the
+        shrink timer and the store cap check of a store (engine.py:342-360,
+        datastore.py:51-62, 685-702) — the index entry was written by the lane;
+        RETIRED: the accounting of a last consumer's retire (engine.py:667-679);
+        FREED: the block back to the pool policy, fenced on its reader's release;
+        STOCK: the lane wants a lendable block of a class; UNPIN: a lane view of an
+        adopted object was released."""
+        off, end, ev = 0, len(data), _LANE_EV
+        while off < end:
+            kind, nlen, did, g, _cons, pbid, nbytes, now, evh = ev.unpack_from(data, off)
+            off += ev.size
+            name = data[off:off + nlen].decode() if nlen else ""
+            off += nlen
+            if kind == 1:
+                live = self._live[(name, g)] + 1
+                self.pools[g].record(name, now, float(nbytes), float(live))
+                self._live[(name, g)] = live
+                self._stored[g] += nbytes
+                self.stats["stores"] += 1
+                self._push_shrink(g, name, now)
+                if self.strategy.migration != "none" and self._stored_on(g) > self.capacity_limit:
+                    self._pending.add(("pressure", g))
+            elif kind == 2:
+                self._live[(name, g)] -= 1
+                self._stored[g] -= nbytes
+                self.stats["fetches"] += 1
+                self.stats["zero_copy"] += 1
+                if self.strategy.migration != "none" and self._off_gpu[g]:
+                    self._pending.add(("prefetch", g))
+            elif kind == 3:
+                blk = self._lane_blocks.pop(pbid, None)
+                fences = [dev.Ev.adopt(evh, g)] if evh else []
+                if blk is not None:
+                    self.pools[g].free(blk, fences)
+                    if name:
+                        self._push_shrink(g, name, self.now_ms())
+            elif kind == 4:
+                self._lane_stock_todo.append((g, nbytes))
+            elif kind == 5:
+                o = self._lane_adopted.get(did)
+                if o is not None:
+                    if o.block is not None and evh:
+                        o.readers.append(dev.Ev.adopt(evh, g))
+                    if o.pins <= 1:
+                        self._lane_adopted.pop(did, None)
+                    self._unpin(o)
+
+    def _lane_take(self, did: int):
+        """(lock held) Adopt lane object ``did`` into the table (its queued events
+        applied first); None if the lane does not hold it (or it is already retired
+        and only pinned by views)."""
+        self._lane_sync()
+        C = dev.C
+        rec, shape, name = _lane_obj_t(), (C.c_int64 * 8)(), C.create_string_buffer(512)
+        if dev.LIB.raw("ft_lane_take")(self._lane, int(did), C.byref(rec), shape, name, 512):
+            return None
+        g = rec.gpu
+        obj = _Obj(did, rec.nbytes, _LANE_DTYPES[rec.dtype], tuple(shape[:rec.ndim]), g, name.value.decode(),
+                   rec.remaining, rec.stored_at_ms)
+        obj.home = g
+        obj.queue_pos = next(self._queue)
+        obj.block = self._lane_blocks.pop(rec.block_id)
+        obj.ready = dev.Ev.adopt(rec.ready, g) if rec.ready else None
+        obj.pins = rec.pins
+        if rec.pins:
+            self._lane_adopted[did] = obj
+        if rec.remaining <= 0:                 # retired (accounted already), kept only by views
+            obj.retired = True
+            return None
+        self._objs[did] = obj
+        return obj
+
+    def _lane_adopt(self, g: int):
+        """(lock held) Adopt every lane object (on GPU ``g``; all with g < 0)."""
+        C = dev.C
+        ids, n = (C.c_int64 * 65536)(), C.c_int()
+        dev.LIB.raw("ft_lane_ids")(self._lane, int(g), ids, 65536, C.byref(n))
+        for i in range(min(n.value, 65536)):
+            self._lane_take(ids[i])
 
     # ------------------------------------------------------------ internals
     def _push_shrink(self, g, func, now):
@@ -1231,3 +1431,11 @@ def _staging_gpu_d2h(links, source):
         if l[0] == "nv":
             return l[2]
     return source
+
+
+class _lane_obj_t(dev.C.Structure):
+    """ft_lane_obj (include/faastube.h)."""
+    _fields_ = [("data_id", dev.C.c_int64), ("block_id", dev.C.c_int64), ("nbytes", dev.C.c_uint64),
+                ("stored_at_ms", dev.C.c_double), ("ready", dev.C.c_void_p), ("gpu", dev.C.c_int32),
+                ("dtype", dev.C.c_int32), ("ndim", dev.C.c_int32), ("remaining", dev.C.c_int32),
+                ("pins", dev.C.c_int32), ("consumers", dev.C.c_int32)]

@@ -94,6 +94,9 @@ class _Tube:
             return self.stored[did]
         return self._objs[did].t
 
+    def peek(self, did):
+        return self._objs.get(did)
+
     def fetch_resident(self, did, device, consumer="func", stream=None):
         o = self._objs.get(did)
         if o is None or o.gpu != device or o.block is None:
