@@ -58,7 +58,10 @@ enum : uint32_t { EV_COMMITTED = 1, EV_RETIRED = 2, EV_FREED = 3, EV_STOCK = 4, 
 constexpr int kDtypes = 10;
 const int kItem[kDtypes] = {1, 1, 2, 4, 8, 2, 2, 4, 8, 1};  // uint8 int8 int16 int32 int64 f16 bf16 f32 f64 bool
 constexpr int kMaxDim = 8;
-constexpr size_t kStockDepth = 2;      // lendable blocks kept per (GPU, size class)
+// lendable blocks kept per (GPU, size class): a steady producer takes one per commit
+// while the tube refills asynchronously (a refill costs it ~0.1 ms), so one block of
+// headroom was not enough (most commits missed and paid an alloc round trip)
+constexpr size_t kStockDepth = 3;
 constexpr uint64_t kTokenBase = 1ull << 62;
 
 #pragma pack(push, 1)
@@ -299,6 +302,7 @@ bool take_stock(ft_lane* L, ft_lane_conn* c, uint64_t n, LBlock* out) {
     EvRec r{};
     r.kind = EV_STOCK;
     r.gpu = c->gpu;
+    r.consumers = (int32_t)(kStockDepth - dq.size());  // blocks wanted
     r.nbytes = cls;
     L->emit(r);
   }
@@ -777,7 +781,7 @@ int ft_lane_stock_put(ft_lane* L, int gpu, int64_t pbid, uint64_t vmm, void* ptr
   for (int i = 0; i < nf; ++i) b.fences.push_back(static_cast<cudaEvent_t>(fences[i]));
   auto key = std::make_pair(gpu, cap);
   L->stock[key].push_back(std::move(b));
-  L->stock_asked.erase(key);
+  L->stock_asked.erase(key);  // (the next take below depth asks again)
   return FT_OK;
 }
 

@@ -1014,7 +1014,7 @@ class FaaSTube:
         adopted object was released."""
         off, end, ev = 0, len(data), _LANE_EV
         while off < end:
-            kind, nlen, did, g, _cons, pbid, nbytes, now, evh = ev.unpack_from(data, off)
+            kind, nlen, did, g, cons, pbid, nbytes, now, evh = ev.unpack_from(data, off)
             off += ev.size
             name = data[off:off + nlen].decode() if nlen else ""
             off += nlen
@@ -1042,7 +1042,7 @@ class FaaSTube:
                     if name:
                         self._push_shrink(g, name, self.now_ms())
             elif kind == 4:
-                self._lane_stock_todo.append((g, nbytes))
+                self._lane_stock_todo.extend([(g, nbytes)] * max(1, cons))
             elif kind == 5:
                 o = self._lane_adopted.get(did)
                 if o is not None:

@@ -120,7 +120,10 @@ def test_function_process_through_daemon(monkeypatch):
     p.join(timeout=60)
     assert status == "ok", res
     print("daemon round trip (store+fetch 1 MiB, GPU, cross-process):", f"{res['us_store_fetch_1MiB']:.1f} us")
-    assert res["imports_grown"] <= 2, res
+    # the lane keeps a stock of lendable blocks per size class (lane.cc kStockDepth = 3):
+    # the blocks in rotation are the stock, the one lent and the one being read; each is
+    # imported once (one arena per block here), then nothing new is mapped
+    assert res["imports_grown"] <= 3 + 2, res
     assert res["missing"] and "MissingData" in res["missing"], res
     assert dropped > 0 and res["after_shrink"] < res["mapped"], (dropped, res)
     # the daemon side holds the function's bytes (third consumer)

@@ -51,6 +51,22 @@ def client(path, q):
             ft.append(t2 - t1)
             vt.append(t4 - t3)
     res["store_us"], res["fetch_out_us"], res["fetch_view_us"] = med(st), med(ft), med(vt)
+    if getattr(c, "_bin", False):
+        # client-side split of a zero-copy fetch: the binary round trip alone vs the rest
+        import cProfile
+        import pstats
+        pr = cProfile.Profile()
+        for i in range(300):
+            did = c.unique_id()
+            c.store(did, x)
+            pr.enable()
+            v = c.fetch(did)
+            del v
+            pr.disable()
+        import io
+        buf = io.StringIO()
+        pstats.Stats(pr, stream=buf).sort_stats("tottime").print_stats(16)
+        res["client_fetch_profile"] = buf.getvalue()
     # CUDA cost of the ordering primitives in this process
     s = torch.cuda.current_stream(0).cuda_stream
     ring = dev.IpcEventRing(0, 4)
@@ -155,7 +171,9 @@ def main():
     p.join(timeout=60)
     res["daemon_handler_us"] = {k: med(v[50:]) for k, v in times.items()}
     res["daemon_tube_us"] = {k: med(v[50:]) for k, v in tin.items()}
+    prof_txt = res.pop("client_fetch_profile", "")
     print(res)
+    print(prof_txt)
     for op in ("commit", "fetch", "done"):
         if op in prof:
             print("==== daemon handler profile:", op)
