@@ -365,6 +365,7 @@ typedef struct ft_lane_conn ft_lane_conn;
 #pragma pack(push, 1)
 typedef struct {         /* one event record (+ name_len bytes of producer name)         */
   uint32_t kind;         /* 1 committed, 2 retired, 3 freed, 4 stock, 5 unpin            */
+                         /* (stock: data_id = the connection id, consumers = blocks wanted) */
   uint32_t name_len;
   int64_t data_id;
   int32_t gpu, consumers;
@@ -400,9 +401,11 @@ int ft_lane_dropped(ft_lane* lane, int gpu, uint64_t arena);
 int ft_lane_lend(ft_lane_conn* c, int64_t block_id, uint64_t vmm_block, void* ptr, uint64_t class_bytes,
                  uint64_t arena, uint64_t offset, uint64_t arena_bytes, uint64_t* token);
 int ft_lane_take_lend(ft_lane_conn* c, uint64_t token, int64_t* block_id);
-int ft_lane_stock_put(ft_lane* lane, int gpu, int64_t block_id, uint64_t vmm_block, void* ptr, uint64_t class_bytes,
-                      uint64_t arena, uint64_t offset, uint64_t arena_bytes, void* const* fences, int n_fences);
-int ft_lane_stock_drain(ft_lane* lane, int64_t* block_ids, int cap, int* n);
+/* a lendable block for connection conn_id's stock (FT_E_KEY: the connection is gone) */
+int ft_lane_stock_put(ft_lane* lane, uint64_t conn_id, int gpu, int64_t block_id, uint64_t vmm_block, void* ptr,
+                      uint64_t class_bytes, uint64_t arena, uint64_t offset, uint64_t arena_bytes,
+                      void* const* fences, int n_fences);
+int ft_lane_conn_id(ft_lane_conn* c, uint64_t* id);
 int ft_lane_events(ft_lane* lane, void* buf, uint64_t cap, uint64_t* n, int64_t timeout_us);
 int ft_lane_take(ft_lane* lane, int64_t data_id, ft_lane_obj* out, int64_t* shape, char* producer, int producer_cap);
 int ft_lane_ids(ft_lane* lane, int gpu, int64_t* ids, int cap, int* n);

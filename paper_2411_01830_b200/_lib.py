@@ -261,8 +261,8 @@ _SIGS = {
     "ft_lane_dropped": (None, [vp, C.c_int, u64]),
     "ft_lane_lend": (None, [vp, i64, u64, vp, u64, u64, u64, u64, P(u64)]),
     "ft_lane_take_lend": (None, [vp, u64, P(i64)]),
-    "ft_lane_stock_put": (None, [vp, C.c_int, i64, u64, vp, u64, u64, u64, u64, P(vp), C.c_int]),
-    "ft_lane_stock_drain": (None, [vp, P(i64), C.c_int, P(C.c_int)]),
+    "ft_lane_stock_put": (None, [vp, u64, C.c_int, i64, u64, vp, u64, u64, u64, u64, P(vp), C.c_int]),
+    "ft_lane_conn_id": (None, [vp, P(u64)]),
     "ft_lane_events": (None, [vp, vp, u64, P(u64), i64]),
     "ft_lane_take": (None, [vp, i64, vp, P(i64), C.c_char_p, C.c_int]),
     "ft_lane_ids": (None, [vp, C.c_int, P(i64), C.c_int, P(C.c_int)]),

@@ -19,7 +19,7 @@
 //   COMMITTED  histogram sample + live/stored accounting + shrink timer + cap check
 //   RETIRED    accounting (the index entry is already gone)
 //   FREED      the block back to the pool policy, fenced on the reader's event
-//   STOCK      refill the stock of lendable blocks of a size class
+//   STOCK      refill a connection's stock of lendable blocks of a size class
 //   UNPIN      a view's release of an object the tube has since adopted
 //
 // Anything else (msgpack requests, misses, responses, host payloads) is handed to
@@ -156,11 +156,17 @@ struct ft_lane_conn {
   std::set<std::pair<int, uint64_t>> mapped;  // (gpu, arena) the client has mapped
   std::vector<uint64_t> drops;                // arenas to unmap, sent with the next reply
   std::set<uint64_t> tokens;                  // native tokens of this connection
+  uint64_t id = 0;                            // the lane's connection id (stock refills name it)
+  // lendable blocks per size class for this producer's next outputs: returned to the
+  // pool when the connection goes away
+  std::map<uint64_t, std::deque<LBlock>> stock;
+  std::set<uint64_t> stock_asked;
   // hand-off of one request to Python
   std::mutex fmu;
   std::condition_variable fcv;
   std::string fwd;
   bool has_fwd = false, py_busy = false, dead = false, stop = false;
+  bool gone = false;  // (lane->mu) the worker has released everything: no more stock
   std::thread worker;
   std::string rep;  // reply buffer (worker)
 };
@@ -172,11 +178,10 @@ struct ft_lane {
   ft_index* index = nullptr;
   std::map<int, ft_vmm_pool*> pools;
   std::unordered_map<int64_t, LObj> objs;
-  std::map<std::pair<int, uint64_t>, std::deque<LBlock>> stock;
-  std::set<std::pair<int, uint64_t>> stock_asked;
   std::unordered_map<uint64_t, Token> tokens;
   uint64_t next_token = kTokenBase;
   std::vector<ft_lane_conn*> conns;
+  uint64_t next_conn = 1;
   std::map<int, std::vector<cudaEvent_t>> evpool;
   // event queue to the tube
   std::mutex emu;
@@ -285,8 +290,7 @@ int arena_fd(ft_lane_conn* c, const LBlock& b, bool* need) {
 // users are waited on by the connection stream; nullopt-like (pbid < 0) on a miss
 bool take_stock(ft_lane* L, ft_lane_conn* c, uint64_t n, LBlock* out) {
   const uint64_t cls = size_class_bytes(n);
-  auto key = std::make_pair(c->gpu, cls);
-  auto& dq = L->stock[key];
+  auto& dq = c->stock[cls];
   bool hit = !dq.empty();
   if (hit) {
     *out = std::move(dq.front());
@@ -297,16 +301,31 @@ bool take_stock(ft_lane* L, ft_lane_conn* c, uint64_t n, LBlock* out) {
   } else {
     ++L->stats[6];
   }
-  if (dq.size() < kStockDepth && !L->stock_asked.count(key)) {
-    L->stock_asked.insert(key);
+  if (dq.size() < kStockDepth && !c->stock_asked.count(cls)) {
+    c->stock_asked.insert(cls);
     EvRec r{};
     r.kind = EV_STOCK;
+    r.did = (int64_t)c->id;                             // the connection to stock
     r.gpu = c->gpu;
     r.consumers = (int32_t)(kStockDepth - dq.size());  // blocks wanted
     r.nbytes = cls;
     L->emit(r);
   }
   return hit;
+}
+
+// (lane->mu held) a connection's stocked blocks go back to the pool (idle: no fence)
+void return_stock(ft_lane* L, ft_lane_conn* c) {
+  for (auto& kv : c->stock)
+    for (auto& b : kv.second) {
+      EvRec r{};
+      r.kind = EV_FREED;
+      r.gpu = b.gpu;
+      r.pbid = b.pbid;
+      L->emit(r);
+    }
+  c->stock.clear();
+  c->stock_asked.clear();
 }
 
 std::string block_payload(uint64_t token, const LBlock& b, uint64_t nbytes, int ev, uint8_t dtype,
@@ -595,6 +614,8 @@ void run_worker(ft_lane_conn* c) {
     std::vector<uint64_t> toks(c->tokens.begin(), c->tokens.end());
     if (c->gpu >= 0) cudaSetDevice(c->gpu);
     for (uint64_t t : toks) release_token(c->lane, c, t);
+    return_stock(c->lane, c);
+    c->gone = true;
   }
   std::lock_guard<std::mutex> lk(c->fmu);
   c->dead = true;
@@ -642,10 +663,17 @@ int ft_lane_attach(ft_lane* L, ft_chan* ch, int sock, ft_lane_conn** out) {
   c->sock = sock;
   {
     std::lock_guard<std::mutex> lk(L->mu);
+    c->id = L->next_conn++;
     L->conns.push_back(c);
   }
   c->worker = std::thread(run_worker, c);
   *out = c;
+  return FT_OK;
+}
+
+int ft_lane_conn_id(ft_lane_conn* c, uint64_t* id) {
+  if (!c || !id) return FT_E_VALUE;
+  *id = c->id;
   return FT_OK;
 }
 
@@ -772,32 +800,23 @@ int ft_lane_lend(ft_lane_conn* c, int64_t pbid, uint64_t vmm, void* ptr, uint64_
   return FT_OK;
 }
 
-// a lendable block for the stock (the tube allocated it; fences: its previous users)
-int ft_lane_stock_put(ft_lane* L, int gpu, int64_t pbid, uint64_t vmm, void* ptr, uint64_t cap, uint64_t arena,
-                      uint64_t off, uint64_t arena_bytes, void* const* fences, int nf) {
+// a lendable block for connection `conn_id`'s stock (the tube allocated it; fences: its
+// previous users). FT_E_KEY if the connection is gone (the tube keeps the block).
+int ft_lane_stock_put(ft_lane* L, uint64_t conn_id, int gpu, int64_t pbid, uint64_t vmm, void* ptr, uint64_t cap,
+                      uint64_t arena, uint64_t off, uint64_t arena_bytes, void* const* fences, int nf) {
   if (!L) return FT_E_VALUE;
   std::lock_guard<std::mutex> lk(L->mu);
+  ft_lane_conn* c = nullptr;
+  for (auto* x : L->conns)
+    if (x->id == conn_id && !x->gone) c = x;
+  if (!c) {
+    ft::set_last_error("no such connection");
+    return FT_E_KEY;
+  }
   LBlock b{pbid, vmm, static_cast<uint8_t*>(ptr), cap, arena, off, arena_bytes, gpu, {}};
   for (int i = 0; i < nf; ++i) b.fences.push_back(static_cast<cudaEvent_t>(fences[i]));
-  auto key = std::make_pair(gpu, cap);
-  L->stock[key].push_back(std::move(b));
-  L->stock_asked.erase(key);  // (the next take below depth asks again)
-  return FT_OK;
-}
-
-// every stocked block back (pbids out): the tube frees them
-int ft_lane_stock_drain(ft_lane* L, int64_t* pbids, int cap, int* n) {
-  if (!L || !n) return FT_E_VALUE;
-  std::lock_guard<std::mutex> lk(L->mu);
-  int k = 0;
-  for (auto& kv : L->stock) {
-    while (!kv.second.empty() && k < cap) {
-      pbids[k++] = kv.second.front().pbid;
-      kv.second.pop_front();
-    }
-  }
-  L->stock_asked.clear();
-  *n = k;
+  c->stock[cap].push_back(std::move(b));
+  c->stock_asked.erase(cap);  // (the next take below depth asks again)
   return FT_OK;
 }
 

@@ -128,7 +128,7 @@ class _Lend:
 
 class _Conn:
     __slots__ = ("ch", "tokens", "mapped", "drop", "gpu", "stream", "mine", "peer", "served", "seen", "lc",
-                 "chan", "bin", "buf")
+                 "chan", "bin", "buf", "stocked")
 
     def __init__(self, ch):
         self.ch = ch
@@ -136,6 +136,7 @@ class _Conn:
         self.chan = None         # its ft_chan (closed after the worker)
         self.bin = False         # the request being served arrived as a binary message
         self.buf = None
+        self.stocked = set()     # (gpu, size class) whose lane stock this connection filled
         self.tokens = set()      # loans of this connection (dropped if the client dies)
         self.mapped = set()      # (gpu, block id) the client has mapped
         self.drop = []           # block ids to unmap, sent with the next reply
@@ -400,6 +401,15 @@ class TubeDaemon:
             self.tube.sync_stream(g)
         if conn.lc is not None and conn.gpu == g:
             tok = self.tube.lane_lend(conn.lc, blk)    # its commit is served by the worker
+            cls = int(blk.policy_block.class_bytes)
+            if (g, cls) not in conn.stocked:
+                # the first output of this size on this connection: stock the class now, so
+                # the commit that follows lends the next block (no second alloc round trip)
+                conn.stocked.add((g, cls))
+                cid = C.c_uint64()
+                dev.LIB.ft_lane_conn_id(conn.lc, C.byref(cid))
+                for _ in range(3):                     # lane.cc kStockDepth
+                    self.tube._lane_stock(cid.value, g, cls)  # noqa: SLF001
         else:
             tok = self._hold(conn, _Lend(blk))
         return {"token": tok, "nbytes": n, "ev": ev, "_blk": blk}

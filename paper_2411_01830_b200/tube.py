@@ -924,13 +924,11 @@ class FaaSTube:
     def detach_lane(self):
         """Adopt every lane object and take the stocked blocks back (the daemon closed)."""
         with self._lock:
+            self._lane_sync()                   # the closed connections' loans and stock came back
             self._lane_adopt(-1)
-            ids, n = (dev.C.c_int64 * 4096)(), dev.C.c_int()
-            dev.LIB.ft_lane_stock_drain(self._lane, ids, 4096, dev.C.byref(n))
-            for i in range(n.value):
-                blk = self._lane_blocks.pop(ids[i], None)
-                if blk is not None:
-                    self.pools[blk.device].free(blk, list(blk.fences))
+            for blk in self._lane_blocks.values():   # (none expected: only blocks of live connections)
+                self.pools[blk.device].free(blk, list(blk.fences))
+            self._lane_blocks = {}
             self._lane_stock_todo = []
             self._lane = None
 
@@ -947,15 +945,15 @@ class FaaSTube:
         with self._lock:
             self._lane_sync()
             todo, self._lane_stock_todo = self._lane_stock_todo, []
-        for g, cls in todo:
-            self._lane_stock(g, cls)
+        for conn_id, g, cls in todo:
+            self._lane_stock(conn_id, g, cls)
         if self._pending:
             self._drain_pending()
         return True
 
-    def _lane_stock(self, g, cls):
-        """A lendable block of class ``cls`` for the lane's stock (allocated outside the
-        tube lock: growth may map memory)."""
+    def _lane_stock(self, conn_id, g, cls):
+        """A lendable block of class ``cls`` for connection ``conn_id``'s stock in the
+        lane (allocated outside the tube lock: growth may map memory)."""
         lane = self._lane
         if lane is None or g not in self.pools:
             return
@@ -963,13 +961,16 @@ class FaaSTube:
         arena, off, abytes = self.pools[g].locate(blk)
         fences = [e._recorded() for e in blk.fences]
         with self._lock:
-            if self._lane is None:
+            rc = 1
+            if self._lane is not None:
+                self._lane_blocks[blk.policy_block.block_id] = blk
+                rc = dev.LIB.raw("ft_lane_stock_put")(
+                    lane, int(conn_id), g, blk.policy_block.block_id, blk.vmm_id, dev.C.c_void_p(blk.ptr),
+                    int(blk.policy_block.class_bytes), arena, off, abytes,
+                    (dev.C.c_void_p * max(1, len(fences)))(*fences), len(fences))
+            if rc:                              # the connection (or the lane) is gone: the block goes back
+                self._lane_blocks.pop(blk.policy_block.block_id, None)
                 self.pools[g].free(blk, list(blk.fences))
-                return
-            self._lane_blocks[blk.policy_block.block_id] = blk
-            dev.LIB.ft_lane_stock_put(lane, g, blk.policy_block.block_id, blk.vmm_id, dev.C.c_void_p(blk.ptr),
-                                      int(blk.policy_block.class_bytes), arena, off, abytes,
-                                      (dev.C.c_void_p * max(1, len(fences)))(*fences), len(fences))
 
     def lane_lend(self, conn_lane, blk) -> int:
         """Register a block lent through Python (the daemon's ``alloc``) with the lane:
@@ -1036,13 +1037,14 @@ class FaaSTube:
                     self._pending.add(("prefetch", g))
             elif kind == 3:
                 blk = self._lane_blocks.pop(pbid, None)
-                fences = [dev.Ev.adopt(evh, g)] if evh else []
+                # (no fence: a stocked block nobody wrote — its previous users' fences stay)
+                fences = [dev.Ev.adopt(evh, g)] if evh else list(blk.fences if blk is not None else ())
                 if blk is not None:
                     self.pools[g].free(blk, fences)
                     if name:
                         self._push_shrink(g, name, self.now_ms())
             elif kind == 4:
-                self._lane_stock_todo.extend([(g, nbytes)] * max(1, cons))
+                self._lane_stock_todo.extend([(did, g, nbytes)] * max(1, cons))
             elif kind == 5:
                 o = self._lane_adopted.get(did)
                 if o is not None:

@@ -52,6 +52,52 @@ def client(path, q):
             vt.append(t4 - t3)
     res["store_us"], res["fetch_out_us"], res["fetch_view_us"] = med(st), med(ft), med(vt)
     if getattr(c, "_bin", False):
+        # per-step wall times of one zero-copy fetch + release, measured inside the client
+        from paper_2411_01830_b200 import daemon as dmod
+        steps = {"call": [], "after_daemon": [], "as_tensor": [], "mark": [], "done_send": []}
+        o_call, o_after, o_as, o_mark, o_done = (c._block_bin, c._after_daemon, dmod.dev.as_tensor, c._mark,
+                                                 c._done)
+
+        def timed(name, fn):
+            def w(*a, **k):
+                t0 = time.perf_counter()
+                try:
+                    return fn(*a, **k)
+                finally:
+                    steps[name].append(time.perf_counter() - t0)
+            return w
+        c._block_bin, c._after_daemon, c._mark = timed("call", o_call), timed("after_daemon", o_after), \
+            timed("mark", o_mark)
+        c._done = timed("done_send", o_done)
+        dmod.dev.as_tensor = timed("as_tensor", o_as)
+        for i in range(300):
+            did = c.unique_id()
+            c.store(did, x)
+            for k in steps:
+                steps[k] = steps[k][:i] if k != "mark" else steps[k]
+            v = c.fetch(did)
+            del v
+        c._block_bin, c._after_daemon, c._mark, c._done = o_call, o_after, o_mark, o_done
+        dmod.dev.as_tensor = o_as
+        res["client_fetch_steps_us"] = {k: med(v[50:]) for k, v in steps.items()}
+        # the same for a store: alloc round trips (msgpack), the binary commit, copy, mark
+        st_steps = {"alloc_call": [], "commit_call": [], "copy": [], "mark": [], "after_daemon": [], "total": []}
+        o_callm, o_copy = c._call, dmod.dev.copy
+        c._call = timed("alloc_call", o_callm)
+        steps.update(st_steps)
+        c._block_bin, c._mark, c._after_daemon = timed("commit_call", o_call), timed("mark", o_mark), \
+            timed("after_daemon", o_after)
+        dmod.dev.copy = timed("copy", o_copy)
+        for i in range(300):
+            did = c.unique_id()
+            t0 = time.perf_counter()
+            c.store(did, x)
+            steps["total"].append(time.perf_counter() - t0)
+            v = c.fetch(did)
+            del v
+        c._call, c._block_bin, c._mark, c._after_daemon = o_callm, o_call, o_mark, o_after
+        dmod.dev.copy = o_copy
+        res["client_store_steps"] = {k: (len(steps[k]), med(steps[k][50:])) for k in st_steps}
         # client-side split of a zero-copy fetch: the binary round trip alone vs the rest
         import cProfile
         import pstats
