@@ -332,6 +332,13 @@ int ft_vmm_unimport(uint64_t handle);
 /* interprocess CUDA events (function <-> daemon ordering without host syncs):
  * create one exportable event (64-byte handle out) / open a peer's handle; use
  * them with ft_event_record / ft_stream_wait_events / ft_event_destroy */
+/* stream memory operations on a word of device memory (cuStreamWriteValue32 after the
+ * stream's prior work, with a memory barrier / cuStreamWaitValue32 GEQ, cyclic): the
+ * function <-> daemon ordering of the native lane — a cross-process CUDA event
+ * dependency takes ~110 us to resolve on B200, a polled word a few us
+ * (tools/probe_ipc_latency.py) */
+int ft_stream_write32(void* stream, void* addr, uint32_t value);
+int ft_stream_wait32(void* stream, const void* addr, uint32_t value);
 int ft_ipc_event_create(int device, void** ev, void* handle64);
 int ft_ipc_event_open(int device, const void* handle64, void** ev);
 int ft_fd_send(int sock, int fd, uint64_t tag);
@@ -386,7 +393,11 @@ int ft_lane_create(ft_index* index, int node, double t0_s, ft_lane** out);
 int ft_lane_set_pool(ft_lane* lane, int gpu, ft_vmm_pool* pool);
 int ft_lane_destroy(ft_lane* lane);
 int ft_lane_attach(ft_lane* lane, ft_chan* ch, int sock, ft_lane_conn** out);
-int ft_lane_conn_set_gpu(ft_lane_conn* c, int gpu, void* stream, void* const* mine, void* const* peer, int k);
+/* after hello: the client's GPU, the connection stream and the connection's two sync
+ * words in pool memory the client maps (c2d: the client's marks, d2c: the daemon's) */
+int ft_lane_conn_set_gpu(ft_lane_conn* c, int gpu, void* stream, void* c2d, void* d2c);
+/* the connection stream waits for the client's mark `seq` (Python's slow paths) */
+int ft_lane_conn_wait(ft_lane_conn* c, uint32_t seq);
 int ft_lane_conn_next(ft_lane_conn* c, void* buf, uint32_t cap, uint32_t* n, int64_t timeout_us);
 int ft_lane_conn_served(ft_lane_conn* c, uint32_t* next_acked);
 int ft_lane_conn_reply(ft_lane_conn* c, const void* msg, uint32_t n);

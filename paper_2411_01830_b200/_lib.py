@@ -247,7 +247,10 @@ _SIGS = {
     "ft_lane_set_pool": (None, [vp, C.c_int, vp]),
     "ft_lane_destroy": (None, [vp]),
     "ft_lane_attach": (None, [vp, vp, C.c_int, P(vp)]),
-    "ft_lane_conn_set_gpu": (None, [vp, C.c_int, vp, P(vp), P(vp), C.c_int]),
+    "ft_lane_conn_set_gpu": (None, [vp, C.c_int, vp, vp, vp]),
+    "ft_lane_conn_wait": (None, [vp, C.c_uint32]),
+    "ft_stream_write32": (None, [vp, vp, C.c_uint32]),
+    "ft_stream_wait32": (None, [vp, vp, C.c_uint32]),
     "ft_lane_conn_next": (None, [vp, vp, C.c_uint32, P(C.c_uint32), i64]),
     "ft_lane_conn_served": (None, [vp, P(C.c_uint32)]),
     "ft_lane_conn_reply": (None, [vp, C.c_char_p, C.c_uint32]),

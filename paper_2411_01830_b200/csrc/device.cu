@@ -1458,6 +1458,13 @@ int ft_copy_ordered(void* dst, const void* src, uint64_t bytes, int device, void
   return FT_OK;
 }
 
+int ft_stream_write32(void* stream, void* addr, uint32_t value) {
+  return ft::mem_write32((cudaStream_t)stream, static_cast<uint32_t*>(addr), value);
+}
+int ft_stream_wait32(void* stream, const void* addr, uint32_t value) {
+  return ft::mem_wait_geq32((cudaStream_t)stream, const_cast<uint32_t*>(static_cast<const uint32_t*>(addr)), value);
+}
+
 int ft_spin_ns(uint64_t ns, int device, void* stream) {
   int cur = 0;
   CU_RT(cudaGetDevice(&cur));

@@ -49,6 +49,7 @@
 #include <vector>
 
 #include "common.h"
+#include "forward.h"
 
 namespace {
 
@@ -150,8 +151,14 @@ struct ft_lane_conn {
   int sock = -1;
   int gpu = -1;
   cudaStream_t stream = nullptr;
-  std::vector<cudaEvent_t> mine, peer;
-  int mark_next = 0;
+  // ordering with the client: two words of pool memory both processes map; each side
+  // writes its next sequence number after its work (stream memory op) and the other
+  // side's stream waits for it (a cross-process CUDA event took ~110 us to resolve)
+  uint32_t* c2d = nullptr;  // the client's marks
+  uint32_t* d2c = nullptr;  // ours
+  uint32_t seq_d = 0;       // our last mark
+  uint32_t seen_c = 0;      // the client's highest mark we waited for (a dead client's waits are released)
+  bool any_c = false;
   uint32_t served = 0;
   std::set<std::pair<int, uint64_t>> mapped;  // (gpu, arena) the client has mapped
   std::vector<uint64_t> drops;                // arenas to unmap, sent with the next reply
@@ -226,16 +233,34 @@ uint64_t size_class_bytes(uint64_t n) {
   return (uint64_t)c;
 }
 
-// mark: record one of the daemon's interprocess events on the connection stream
+// mark: our next sequence number, written to d2c after the connection stream's work
+// (0 and ~0 are never used: 0 means "no mark" in the protocol, ~0 is -1 as int32)
 int mark(ft_lane_conn* c) {
-  if (c->mine.empty()) return -1;
-  int i = c->mark_next;
-  c->mark_next = (i + 1) % (int)c->mine.size();
-  if (cudaEventRecord(c->mine[i], c->stream) != cudaSuccess) return -1;
-  return i;
+  if (!c->d2c) return 0;
+  uint32_t v = c->seq_d + 1;
+  if (v == 0 || v == 0xFFFFFFFFu) v = 1;
+  if (ft::mem_write32(c->stream, c->d2c, v) != FT_OK) return 0;
+  c->seq_d = v;
+  return (int)v;
 }
 void wait_peer(ft_lane_conn* c, int ev) {
-  if (ev >= 0 && ev < (int)c->peer.size()) cudaStreamWaitEvent(c->stream, c->peer[ev], 0);
+  if (!c->c2d || ev == 0 || ev == -1) return;
+  const uint32_t v = (uint32_t)ev;
+  ft::mem_wait_geq32(c->stream, c->c2d, v);
+  if (!c->any_c || (int32_t)(v - c->seen_c) > 0) c->seen_c = v;
+  c->any_c = true;
+}
+// a client that went away may never write the marks our stream waits for: write the
+// highest one from the host (a separate stream: the connection stream is parked)
+void release_waits(ft_lane_conn* c) {
+  if (!c->c2d || !c->any_c) return;
+  static thread_local uint32_t v;
+  v = c->seen_c;
+  cudaStream_t s = nullptr;
+  if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) return;
+  cudaMemcpyAsync(c->c2d, &v, 4, cudaMemcpyHostToDevice, s);
+  cudaStreamSynchronize(s);
+  cudaStreamDestroy(s);
 }
 
 struct Reply {
@@ -613,6 +638,7 @@ void run_worker(ft_lane_conn* c) {
     std::lock_guard<std::mutex> lk(c->lane->mu);
     std::vector<uint64_t> toks(c->tokens.begin(), c->tokens.end());
     if (c->gpu >= 0) cudaSetDevice(c->gpu);
+    release_waits(c);
     for (uint64_t t : toks) release_token(c->lane, c, t);
     return_stock(c->lane, c);
     c->gone = true;
@@ -677,14 +703,21 @@ int ft_lane_conn_id(ft_lane_conn* c, uint64_t* id) {
   return FT_OK;
 }
 
-// after hello: the client's GPU, the connection stream, both event rings (raw handles)
-int ft_lane_conn_set_gpu(ft_lane_conn* c, int gpu, void* stream, void* const* mine, void* const* peer, int k) {
+// after hello: the client's GPU, the connection stream, the two sync words
+int ft_lane_conn_set_gpu(ft_lane_conn* c, int gpu, void* stream, void* c2d, void* d2c) {
   if (!c) return FT_E_VALUE;
   std::lock_guard<std::mutex> lk(c->lane->mu);
   c->gpu = gpu;
   c->stream = (cudaStream_t)stream;
-  c->mine.assign(reinterpret_cast<cudaEvent_t const*>(mine), reinterpret_cast<cudaEvent_t const*>(mine) + k);
-  c->peer.assign(reinterpret_cast<cudaEvent_t const*>(peer), reinterpret_cast<cudaEvent_t const*>(peer) + k);
+  c->c2d = static_cast<uint32_t*>(c2d);
+  c->d2c = static_cast<uint32_t*>(d2c);
+  return FT_OK;
+}
+
+int ft_lane_conn_wait(ft_lane_conn* c, uint32_t seq) {
+  if (!c) return FT_E_VALUE;
+  std::lock_guard<std::mutex> lk(c->lane->mu);
+  wait_peer(c, (int)seq);
   return FT_OK;
 }
 

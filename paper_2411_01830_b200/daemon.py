@@ -128,7 +128,7 @@ class _Lend:
 
 class _Conn:
     __slots__ = ("ch", "tokens", "mapped", "drop", "gpu", "stream", "mine", "peer", "served", "seen", "lc",
-                 "chan", "bin", "buf", "stocked")
+                 "chan", "bin", "buf", "stocked", "slot")
 
     def __init__(self, ch):
         self.ch = ch
@@ -137,6 +137,7 @@ class _Conn:
         self.bin = False         # the request being served arrived as a binary message
         self.buf = None
         self.stocked = set()     # (gpu, size class) whose lane stock this connection filled
+        self.slot = None         # (gpu, index) of the connection's sync words (lane connections)
         self.tokens = set()      # loans of this connection (dropped if the client dies)
         self.mapped = set()      # (gpu, block id) the client has mapped
         self.drop = []           # block ids to unmap, sent with the next reply
@@ -154,18 +155,22 @@ class _Conn:
         return torch.cuda.stream(self.stream)
 
     def mark(self) -> int:
-        """Record one of the daemon's events on the connection stream (-1: no events)."""
-        if self.mine is None:
-            return -1
-        if self.lc is not None:                # one mark ring, shared with the native worker
+        """Mark the connection stream for the client (-1 / 0: no ordering — host sync)."""
+        if self.lc is not None and self.slot is not None:   # the daemon's sync word (shared with the worker)
             i = C.c_int()
             dev.LIB.ft_lane_conn_mark(self.lc, C.byref(i))
             return i.value
+        if self.mine is None:
+            return -1
         i = self.mine.take()
         self.mine.record(i, self.stream)
         return i
 
     def wait_peer(self, i):
+        if self.lc is not None and self.slot is not None:
+            if i is not None and i not in (0, -1):      # a mark of the client's sync word
+                dev.LIB.ft_lane_conn_wait(self.lc, int(i) & 0xFFFFFFFF)
+            return
         if self.peer is not None and i is not None and i >= 0:
             self.peer.wait(int(i), self.stream)
 
@@ -194,6 +199,7 @@ class TubeDaemon:
         # the native lane serves the hot requests of upgraded connections (csrc/lane.cc);
         # its events are applied to the tube by the service thread
         self._lane = None
+        self._sync = {}            # gpu -> (pool block of 256-byte sync slots, free slot indices)
         if lane and hasattr(tube, "attach_lane") and tube.pools:
             h = C.c_void_p()
             dev.LIB.ft_lane_create(tube.index._h, int(tube.node), float(tube._t0), C.byref(h))  # noqa: SLF001
@@ -302,6 +308,11 @@ class TubeDaemon:
                     self._unhold(conn, tok)
             if conn.stream is not None:
                 conn.stream.synchronize()
+            if conn.slot is not None:
+                g, i = conn.slot
+                with self._lock:
+                    self._sync[g][1].append(i)
+                conn.slot = None
             conn.close()
             if conn.chan is not None:
                 dev.LIB.ft_chan_close(conn.chan)
@@ -438,12 +449,17 @@ class TubeDaemon:
             g = int(msg["gpu"])
             conn.gpu = g
             conn.stream = dev.new_stream(g)
+            if conn.lc is not None and msg.get("memops"):
+                # ordering through two words of pool memory the client maps: a 256-byte
+                # slot of the lane's sync block on this GPU, zeroed before first use
+                blk, ptr = self._sync_slot(conn, g)
+                dev.LIB.ft_lane_conn_set_gpu(conn.lc, g, C.c_void_p(conn.stream.cuda_stream), C.c_void_p(ptr),
+                                             C.c_void_p(ptr + 128))
+                meta = {"sync_off": ptr - blk.ptr}
+                self._reply_block(conn, g, blk, meta)
+                return
             conn.peer = dev.PeerEvents(g, msg.get("ev", []))
             conn.mine = dev.IpcEventRing(g)
-            if conn.lc is not None:
-                k = len(conn.mine.h)
-                dev.LIB.ft_lane_conn_set_gpu(conn.lc, g, C.c_void_p(conn.stream.cuda_stream),
-                                             (C.c_void_p * k)(*conn.mine.h), (C.c_void_p * k)(*conn.peer.h), k)
             self._reply(conn, {"ev": conn.mine.handles})
         elif op == "alloc":
             g, n = int(msg["gpu"]), int(msg["nbytes"])
@@ -537,6 +553,27 @@ class TubeDaemon:
         else:
             raise ValueError(f"unknown op {op!r}")
 
+    def _sync_slot(self, conn, g):
+        """A zeroed 256-byte slot of the lane's sync block on GPU g for this connection
+        (c2d word at +0, d2c word at +128). Returns (block, slot pointer)."""
+        with self._lock:
+            ent = self._sync.get(g)
+            if ent is None:
+                blk = self.tube.lend_block(g, 2 << 20)
+                blk.wait_fences(conn.stream)           # its previous users, before the zeroing below
+                ent = self._sync[g] = (blk, list(range(blk.nbytes // 256 - 1, -1, -1)))
+            blk, free = ent
+            if not free:
+                raise MemoryError("no free sync slot (too many function connections on this GPU)")
+            i = free.pop()
+        conn.slot = (g, i)
+        ptr = blk.ptr + 256 * i
+        z = dev.as_tensor(ptr, 256, g)
+        with torch.cuda.stream(conn.stream):
+            z.zero_()
+        conn.stream.synchronize()
+        return blk, ptr
+
     def _fetch_into_block(self, conn, g, did, msg):
         """A fetch that is not a same-GPU zero-copy read: into a pool block the
         client maps (on the connection's stream)."""
@@ -574,6 +611,9 @@ class TubeDaemon:
             th.join(timeout=5)
         if self._lane is not None:
             self._service.join(timeout=5)
+            for g, (blk, _free) in self._sync.items():
+                self.tube.pools[g].free(blk, [])
+            self._sync = {}
             self.tube.detach_lane()            # its objects into the tube's table, stocked blocks back
             dev.LIB.ft_lane_destroy(self._lane)
             self._lane = None
@@ -657,6 +697,9 @@ class TubeClient:
         self._sent = 0               # messages sent
         self._acked = 0              # messages the daemon has served (from its replies)
         self._mine = self._peer = None
+        self._sync = None            # lane connections: (c2d, d2c) word pointers in the mapped sync slot
+        self._seq = 0                # our last mark (c2d)
+        self._events = events
         self._closed = False
         self._views = 0              # zero-copy views handed out and not yet released
         self._lane = False           # the daemon's native lane serves the hot requests (binary messages)
@@ -665,7 +708,12 @@ class TubeClient:
                 self.ch.upgrade()
                 self._sent += 1
                 self._lane = bool(self._recv().get("lane"))
-        if events:
+        if events and self._lane:
+            # the lane orders both sides through two words of a pool slot mapped here
+            rep = self._call({"op": "hello", "gpu": device, "memops": True})
+            p = self._mapped(rep).ptr + rep["off"] + rep["sync_off"]
+            self._sync = (p, p + 128)
+        elif events:
             self._mine = dev.IpcEventRing(device)
             self._used = [0] * self._mine.k        # message number that carried each event's last record
             rep = self._call({"op": "hello", "gpu": device, "ev": self._mine.handles})
@@ -747,6 +795,14 @@ class TubeClient:
         """Record one of our events on ``stream`` for the next message (-1: the
         daemon may still have a wait on that event's previous record to enqueue —
         synchronise ``stream`` instead)."""
+        if self._sync is not None:
+            with self._io:
+                v = (self._seq + 1) & 0xFFFFFFFF
+                if v in (0, 0xFFFFFFFF):
+                    v = 1
+                dev.LIB.ft_stream_write32(C.c_void_p(dev.stream_ptr(stream)), C.c_void_p(self._sync[0]), v)
+                self._seq = v
+                return v - (1 << 32) if v >= (1 << 31) else v      # int32 on the wire
         if self._mine is None:
             stream.synchronize()
             return -1
@@ -762,6 +818,11 @@ class TubeClient:
     def _after_daemon(self, rep: dict, stream):
         """``stream`` waits for the daemon's mark in ``rep`` (host-synced connections: nothing)."""
         ev = rep.get("ev", -1)
+        if self._sync is not None:
+            if ev is not None and ev not in (0, -1):
+                dev.LIB.ft_stream_wait32(C.c_void_p(dev.stream_ptr(stream)), C.c_void_p(self._sync[1]),
+                                         int(ev) & 0xFFFFFFFF)
+            return
         if self._peer is not None and ev is not None and ev >= 0:
             self._peer.wait(int(ev), stream)
 
@@ -794,14 +855,15 @@ class TubeClient:
         else:
             imp = self._imports[rep["block"]]
         ptr = imp.ptr + rep.get("off", 0)
-        if self._mine is None:
+        if not self._events:
             cur = self._stream
             cur.wait_stream(torch.cuda.current_stream(self.device))
         else:
             cur = torch.cuda.current_stream(self.device)
         self._after_daemon(rep, cur)                  # the block's previous users are done
-        dev.copy(ptr, t.data_ptr(), n, self.device, cur)
-        if t is not output or self._mine is None:
+        # the engine is known (the mapped block is memory of this GPU): no pointer queries
+        dev.copy(ptr, t.data_ptr(), n, self.device, cur, self._engine(t))
+        if t is not output or not self._events:
             t.record_stream(cur)
         if self._bin and not response and t.dtype in _CODE and t.dim() <= 8:
             name = producer.encode()
@@ -816,7 +878,7 @@ class TubeClient:
                 rep = self._call({"op": "commit", "token": rep["token"], "id": data_id, "dtype": str(t.dtype),
                                   "shape": list(t.shape), "producer": producer, "consumers": consumers,
                                   "response": response, "ev": ev,
-                                  **({"next": n} if self._mine is not None else {})})
+                                  **({"next": n} if self._events else {})})
         if rep.get("loan"):
             self._mapped(rep)
             self._loans[n] = rep
@@ -850,7 +912,7 @@ class TubeClient:
         if out is not None and (not out.is_contiguous() or out.nbytes != n):
             self._done(rep["token"], -1)
             raise ValueError("out must be contiguous with exactly the stored byte count")
-        if self._mine is not None:
+        if self._events:
             cur = torch.cuda.current_stream(self.device)
             self._after_daemon(rep, cur)               # the bytes are in place
             if out is None:
@@ -861,7 +923,7 @@ class TubeClient:
                 self._views += 1
                 weakref.finalize(owner, self._release, rep["token"])
                 return dev.as_tensor(ptr, n, self.device, dt, tuple(shape), owner=owner)
-            dev.copy(out.data_ptr(), ptr, n, self.device, cur)
+            dev.copy(out.data_ptr(), ptr, n, self.device, cur, self._engine(out))
             with self._io:
                 self._done(rep["token"], self._mark(cur))
             return out
@@ -870,7 +932,7 @@ class TubeClient:
             out = torch.empty(shape, dtype=dt, device=f"cuda:{self.device}")
         cur = torch.cuda.current_stream(self.device)
         self._stream.wait_stream(cur)
-        dev.copy(out.data_ptr(), ptr, n, self.device, self._stream)
+        dev.copy(out.data_ptr(), ptr, n, self.device, self._stream, self._engine(out))
         self._stream.synchronize()                     # read before the daemon may reuse the block
         self._send({"op": "done", "token": rep["token"]})
         cur.wait_stream(self._stream)
@@ -886,6 +948,11 @@ class TubeClient:
                 self._done(token, self._mark(cur))
         except Exception:  # noqa: BLE001 - the daemon drops a dead connection's loans itself
             pass
+
+    def _engine(self, t: torch.Tensor) -> int:
+        """TMA bulk between this GPU's memory and a mapped block; the peer-safe vector
+        engine when the tensor lives on another GPU."""
+        return dev.ENGINE_BULK if t.get_device() == self.device else dev.ENGINE_VEC
 
     def _done(self, token: int, ev: int):
         """Release a read block (no reply): binary to the lane, else msgpack."""
@@ -904,15 +971,19 @@ class TubeClient:
         gc.collect()                                   # views dropped by the caller send their done now
         self._closed = True
         if not self._views:                            # a live view keeps its mapping (until exit)
+            # copies into / out of the mapped blocks may still be queued: unmapping under
+            # them faults (an illegal address in this process)
+            torch.cuda.synchronize(self.device)
             for imp in self._imports.values():
                 imp.close()
         self._imports.clear()
         self._loans.clear()
-        if self._mine is None:
+        if not self._events:
             dev.destroy_stream(self._stream)
         else:
             torch.cuda.synchronize(self.device)
-            self._peer.close()
-            self._mine.close()
+            if self._mine is not None:
+                self._peer.close()
+                self._mine.close()
         self.ch.close()
         self.ch.close()

@@ -33,6 +33,22 @@ def client(path, q):
     x = torch.randint(0, 256, (1 << 20,), dtype=torch.uint8, device="cuda:0")
     out = torch.empty_like(x)
     st, ft, vt = [], [], []
+    # the first loop's stores, step by step (store after a fetch(out=) copy)
+    from paper_2411_01830_b200 import daemon as dmod
+    first = {"alloc_call": [], "commit_call": [], "copy": [], "mark": [], "after_daemon": [], "sync": []}
+    o_calls = (c._call, c._block_bin, dmod.dev.copy, c._mark, c._after_daemon)
+
+    def tm(name, fn):
+        def w(*a, **k):
+            t0 = time.perf_counter()
+            try:
+                return fn(*a, **k)
+            finally:
+                first[name].append(time.perf_counter() - t0)
+        return w
+    c._call, c._block_bin, dmod.dev.copy, c._mark, c._after_daemon = (
+        tm("alloc_call", o_calls[0]), tm("commit_call", o_calls[1]), tm("copy", o_calls[2]), tm("mark", o_calls[3]),
+        tm("after_daemon", o_calls[4]))
     for i in range(300):
         did = c.unique_id()
         t0 = time.perf_counter()
@@ -51,6 +67,10 @@ def client(path, q):
             ft.append(t2 - t1)
             vt.append(t4 - t3)
     res["store_us"], res["fetch_out_us"], res["fetch_view_us"] = med(st), med(ft), med(vt)
+    c._call, c._block_bin, dmod.dev.copy, c._mark, c._after_daemon = o_calls
+    res["first_loop_steps"] = {k: (len(v), med(v[100:])) for k, v in first.items()}
+    if hasattr(c, "_mine") and c._mine is not None:
+        res["acked_vs_sent"] = (c._acked, c._sent)
     if getattr(c, "_bin", False):
         # per-step wall times of one zero-copy fetch + release, measured inside the client
         from paper_2411_01830_b200 import daemon as dmod
