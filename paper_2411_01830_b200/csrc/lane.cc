@@ -113,6 +113,7 @@ struct LBlock {
   uint64_t arena = 0, off = 0, arena_bytes = 0;
   int gpu = -1;
   std::vector<cudaEvent_t> fences;  // the previous holder's last users (the tube keeps them alive)
+  cudaEvent_t own = nullptr;        // or: the lane's fence event of a recycled block's last users
 };
 
 struct LObj {
@@ -194,7 +195,7 @@ struct ft_lane {
   std::mutex emu;
   std::condition_variable ecv;
   std::string events;
-  uint64_t stats[8] = {};  // commits, fetches, dones, uids, forwarded, stock hits, stock misses, adopted
+  uint64_t stats[9] = {};  // commits, fetches, dones, uids, forwarded, stock hits, stock misses, adopted, recycled
 
   double now_ms() const { return ((double)now_us() * 1e-6 - t0) * 1e3; }
   cudaEvent_t get_event(int gpu) {
@@ -322,6 +323,11 @@ bool take_stock(ft_lane* L, ft_lane_conn* c, uint64_t n, LBlock* out) {
     dq.pop_front();
     for (cudaEvent_t f : out->fences) cudaStreamWaitEvent(c->stream, f, 0);
     out->fences.clear();
+    if (out->own) {  // (the wait captured the record: the event can be reused)
+      cudaStreamWaitEvent(c->stream, out->own, 0);
+      L->put_event(out->gpu, out->own);
+      out->own = nullptr;
+    }
     ++L->stats[5];
   } else {
     ++L->stats[6];
@@ -339,7 +345,8 @@ bool take_stock(ft_lane* L, ft_lane_conn* c, uint64_t n, LBlock* out) {
   return hit;
 }
 
-// (lane->mu held) a connection's stocked blocks go back to the pool (idle: no fence)
+// (lane->mu held) a connection's stocked blocks go back to the pool (a recycled one
+// with its last users' fence, whose ownership passes to the tube)
 void return_stock(ft_lane* L, ft_lane_conn* c) {
   for (auto& kv : c->stock)
     for (auto& b : kv.second) {
@@ -347,10 +354,30 @@ void return_stock(ft_lane* L, ft_lane_conn* c) {
       r.kind = EV_FREED;
       r.gpu = b.gpu;
       r.pbid = b.pbid;
+      r.handle = (uint64_t)(uintptr_t)b.own;
       L->emit(r);
     }
   c->stock.clear();
   c->stock_asked.clear();
+}
+
+// (lane->mu held) a block whose last users are fenced by the lane's event `f` goes
+// straight into the stock of a connection that lends its size class and is below
+// depth — the pool policy's exact-class reuse (datastore.py:130-144) without the
+// round trip through the tube; false: the caller returns it to the pool
+bool recycle(ft_lane* L, const LBlock& blk, cudaEvent_t f) {
+  for (auto* x : L->conns) {
+    if (x->gone || x->gpu != blk.gpu) continue;
+    auto it = x->stock.find(blk.cap);
+    if (it == x->stock.end() || it->second.size() >= kStockDepth) continue;
+    LBlock b = blk;
+    b.fences.clear();
+    b.own = f;
+    it->second.push_back(std::move(b));
+    ++L->stats[8];
+    return true;
+  }
+  return false;
 }
 
 std::string block_payload(uint64_t token, const LBlock& b, uint64_t nbytes, int ev, uint8_t dtype,
@@ -367,6 +394,11 @@ std::string block_payload(uint64_t token, const LBlock& b, uint64_t nbytes, int 
 void free_obj(ft_lane* L, ft_lane_conn* c, LObj& o) {
   cudaEvent_t f = L->get_event(c->gpu);
   cudaEventRecord(f, c->stream);
+  if (recycle(L, o.blk, f)) {
+    L->put_event(o.blk.gpu, o.ready);
+    L->objs.erase(o.did);
+    return;
+  }
   EvRec r{};
   r.kind = EV_FREED;
   r.did = o.did;
@@ -540,6 +572,7 @@ void release_token(ft_lane* L, ft_lane_conn* c, uint64_t tok) {
   if (t.kind == 1) {
     cudaEvent_t f = L->get_event(c->gpu);
     cudaEventRecord(f, c->stream);
+    if (!c->gone && recycle(L, t.blk, f)) return;
     EvRec r{};
     r.kind = EV_FREED;
     r.gpu = t.blk.gpu;
@@ -945,7 +978,7 @@ int ft_lane_ids(ft_lane* L, int gpu, int64_t* out, int cap, int* n) {
 int ft_lane_stats(ft_lane* L, uint64_t* out, int cap) {
   if (!L) return FT_E_VALUE;
   std::lock_guard<std::mutex> lk(L->mu);
-  for (int i = 0; i < cap && i < 8; ++i) out[i] = L->stats[i];
+  for (int i = 0; i < cap && i < 9; ++i) out[i] = L->stats[i];
   return FT_OK;
 }
 

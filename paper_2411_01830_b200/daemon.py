@@ -207,6 +207,13 @@ class TubeDaemon:
                 dev.LIB.ft_lane_set_pool(h, int(g), pool._h)  # noqa: SLF001
             tube.attach_lane(h)
             self._lane = h
+            for g in tube.pools:
+                # each connection's two sync words live in a 256-byte slot of this block
+                # (mapped by the client like any pool block); held for the daemon's life
+                blk = tube.lend_block(g, 2 * 10**6)
+                for e in blk.take_fences():
+                    e.synchronize()
+                self._sync[g] = (blk, list(range(blk.nbytes // 256 - 1, -1, -1)))
             self._service = threading.Thread(target=self._service_loop, name="faastube-lane", daemon=True)
             self._service.start()
         self._acceptor = threading.Thread(target=self._accept_loop, name="faastube-daemon", daemon=True)
@@ -557,12 +564,7 @@ class TubeDaemon:
         """A zeroed 256-byte slot of the lane's sync block on GPU g for this connection
         (c2d word at +0, d2c word at +128). Returns (block, slot pointer)."""
         with self._lock:
-            ent = self._sync.get(g)
-            if ent is None:
-                blk = self.tube.lend_block(g, 2 << 20)
-                blk.wait_fences(conn.stream)           # its previous users, before the zeroing below
-                ent = self._sync[g] = (blk, list(range(blk.nbytes // 256 - 1, -1, -1)))
-            blk, free = ent
+            blk, free = self._sync[g]
             if not free:
                 raise MemoryError("no free sync slot (too many function connections on this GPU)")
             i = free.pop()
