@@ -423,6 +423,30 @@ int ft_lane_ids(ft_lane* lane, int gpu, int64_t* ids, int cap, int* n);
 /* commits, fetches, dones, unique ids, handed to Python, stock hits, stock misses, adopted, recycled */
 int ft_lane_stats(ft_lane* lane, uint64_t* out, int cap);
 
+/* The function-process side of the lane (csrc/client.cc): one call per hot request
+ * of Listing 1 through the daemon — rings, the copy into / out of the mapped block,
+ * the sync-word ordering. Views are DLPack tensors whose deleter releases the block. */
+typedef struct ft_client ft_client;
+int ft_client_create(ft_chan* ch, void* c2d, void* d2c, int device, ft_client** out);
+int ft_client_destroy(ft_client* cl);
+int ft_client_sent(ft_client* cl, uint64_t* out);
+int ft_client_views(ft_client* cl, int* out);  /* live DLPack views */
+int ft_client_send(ft_client* cl, const void* msg, uint32_t n);
+int ft_client_call(ft_client* cl, const void* req, uint32_t n, void* rep, uint32_t cap, uint32_t* rep_len,
+                   int64_t spin_us);
+int ft_client_recv(ft_client* cl, void* rep, uint32_t cap, uint32_t* rep_len, int64_t spin_us);
+int ft_client_mark(ft_client* cl, void* stream, int32_t* ev);
+int ft_client_wait(ft_client* cl, void* stream, int32_t ev);
+int ft_client_store(ft_client* cl, void* stream, int32_t wait_ev, void* dst, const void* src, uint64_t n, int engine,
+                    void* req, uint32_t req_len, void* rep, uint32_t cap, uint32_t* rep_len, int64_t spin_us);
+int ft_client_fetch(ft_client* cl, void* stream, const void* req, uint32_t req_len, void* rep, uint32_t cap,
+                    uint32_t* rep_len, int64_t spin_us);
+int ft_client_copy_done(ft_client* cl, void* stream, void* dst, const void* src, uint64_t n, int engine,
+                        uint64_t token);
+int ft_client_done(ft_client* cl, void* stream, uint64_t token, int ordered);
+int ft_client_view(ft_client* cl, void* ptr, int dtype, int ndim, const int64_t* shape, uint64_t token,
+                   void** dlmanaged);
+
 /* ---- movers
  * K1/K3 ft_copy: SM-driven bulk copy (TMA cp.async.bulk global->smem->global,
  * mbarrier ring, persistent grid) for same-GPU handoff copies and NVLink

@@ -270,6 +270,21 @@ _SIGS = {
     "ft_lane_take": (None, [vp, i64, vp, P(i64), C.c_char_p, C.c_int]),
     "ft_lane_ids": (None, [vp, C.c_int, P(i64), C.c_int, P(C.c_int)]),
     "ft_lane_stats": (None, [vp, P(u64), C.c_int]),
+    "ft_client_create": (None, [vp, vp, vp, C.c_int, P(vp)]),
+    "ft_client_destroy": (None, [vp]),
+    "ft_client_sent": (None, [vp, P(u64)]),
+    "ft_client_views": (None, [vp, P(C.c_int)]),
+    "ft_client_send": (None, [vp, C.c_char_p, C.c_uint32]),
+    "ft_client_call": (None, [vp, C.c_char_p, C.c_uint32, vp, C.c_uint32, P(C.c_uint32), i64]),
+    "ft_client_recv": (None, [vp, vp, C.c_uint32, P(C.c_uint32), i64]),
+    "ft_client_mark": (None, [vp, vp, P(C.c_int32)]),
+    "ft_client_wait": (None, [vp, vp, C.c_int32]),
+    "ft_client_store": (None, [vp, vp, C.c_int32, vp, vp, u64, C.c_int, vp, C.c_uint32, vp, C.c_uint32,
+                               P(C.c_uint32), i64]),
+    "ft_client_fetch": (None, [vp, vp, C.c_char_p, C.c_uint32, vp, C.c_uint32, P(C.c_uint32), i64]),
+    "ft_client_copy_done": (None, [vp, vp, vp, vp, u64, C.c_int, u64]),
+    "ft_client_done": (None, [vp, vp, u64, C.c_int]),
+    "ft_client_view": (None, [vp, vp, C.c_int, C.c_int, P(i64), u64, P(vp)]),
     "ft_chan_create": (None, [C.c_uint32, C.c_uint32, P(C.c_int), P(vp)]),
     "ft_chan_attach": (None, [C.c_int, P(vp)]),
     "ft_chan_send": (None, [vp, C.c_int, C.c_char_p, C.c_uint32, i64]),

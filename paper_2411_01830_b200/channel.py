@@ -37,6 +37,7 @@ class Channel:
 
     def __init__(self, sock: socket.socket):
         self.sock = sock
+        self._client = None     # ft_client (the lane's function side) once it owns the rings
         self._chan = None
         self._dir = 0           # ring this side sends on (0: client requests, 1: daemon replies)
         self._buf = None
@@ -103,8 +104,15 @@ class Channel:
         fd, n = dev.recv_fd(self.sock)
         return fd, msgpack.unpackb(self._recv_exact(n))
 
+    def adopt_client(self, client):
+        """The native lane client takes the rings over (every send through its mutex)."""
+        self._client, self._chan = client, None
+
     def send_msg(self, meta: dict):
         body = msgpack.packb(meta)
+        if self._client is not None:
+            self._client_send(body)
+            return
         if self._chan is not None:
             rc = LIB.raw("ft_chan_send")(self._chan, self._dir, body, len(body), -1)
             if rc == 13:
@@ -114,8 +122,32 @@ class Channel:
             return
         self.sock.sendall(_HDR.pack(len(body)) + body)
 
+    def _client_send(self, body: bytes):
+        rc = LIB.raw("ft_client_send")(self._client, body, len(body))
+        if rc == 13:
+            raise ConnectionError("channel closed")
+        if rc:
+            raise_status(rc)
+
+    def client_reply(self, rc: int, buf=None, n=None, spin_us: int = SPIN_US) -> bytes:
+        """The reply a native client call left in ``buf`` (``n`` bytes) with status
+        ``rc``; on a timeout, wait longer while the daemon is alive."""
+        buf = self._buf if buf is None else buf
+        n = self._n if n is None else n
+        while rc == 12:
+            self._check_peer()
+            rc = LIB.raw("ft_client_recv")(self._client, buf, len(buf), C.byref(n), spin_us)
+        if rc == 13:
+            raise ConnectionError("channel closed")
+        if rc:
+            raise_status(rc)
+        return buf.raw[:n.value]
+
     def send_raw(self, body: bytes):
         """One binary message on the rings (the native lane's protocol)."""
+        if self._client is not None:
+            self._client_send(body)
+            return
         rc = LIB.raw("ft_chan_send")(self._chan, self._dir, body, len(body), -1)
         if rc == 13:
             raise ConnectionError("channel closed")
@@ -123,6 +155,8 @@ class Channel:
             raise_status(rc)
 
     def recv_raw(self, spin_us: int = SPIN_US) -> bytes:
+        if self._client is not None:
+            return self.client_reply(12, spin_us=spin_us)
         while True:
             rc = LIB.raw("ft_chan_recv")(self._chan, 1 - self._dir, self._buf, _SLOT, self._n, spin_us, _POLL_US)
             if rc == 0:
@@ -134,6 +168,8 @@ class Channel:
             self._check_peer()
 
     def recv_msg(self, spin_us: int = SPIN_US) -> dict:
+        if self._client is not None:
+            return msgpack.unpackb(self.client_reply(12, spin_us=spin_us))
         if self._chan is None:
             n = _HDR.unpack(self._recv_exact(4))[0]
             return msgpack.unpackb(self._recv_exact(n))
@@ -172,4 +208,7 @@ class Channel:
         h, self._chan = self._chan, None
         if h is not None:
             LIB.ft_chan_close(h)
+        cl, self._client = self._client, None
+        if cl is not None:                   # the rings close with the client's last view
+            LIB.ft_client_destroy(cl)
         self.sock.close()

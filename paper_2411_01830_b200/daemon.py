@@ -626,6 +626,18 @@ class TubeDaemon:
                 os.unlink(self.path)
 
 
+_SPIN = int(os.environ.get("FT_CHAN_SPIN_US", 2000))
+_PyCapsule_New = C.pythonapi.PyCapsule_New
+_PyCapsule_New.restype = C.py_object
+_PyCapsule_New.argtypes = [C.c_void_p, C.c_char_p, C.c_void_p]
+
+
+def _capsule(dlmanaged: int):
+    """A "dltensor" capsule over a DLManagedTensor the native client made (torch's
+    from_dlpack consumes it and calls its deleter when the storage is freed)."""
+    return _PyCapsule_New(dlmanaged, b"dltensor", None)
+
+
 def _decode_bin(raw: bytes) -> dict:
     """A binary request of the lane protocol (csrc/lane.cc) as the dict the handlers take."""
     op = raw[0]
@@ -696,7 +708,8 @@ class TubeClient:
         self._imports = {}           # daemon block id -> ImportedBlock (until the daemon drops it)
         self._loans = {}             # nbytes -> a lent block for the producer's next output
         self._io = threading.RLock()  # one frame at a time on the socket (releases come from finalizers)
-        self._sent = 0               # messages sent
+        self._sent_py = 0            # messages sent from Python (the native client counts its own)
+        self._cl = None              # ft_client: the lane's hot requests in one native call each
         self._acked = 0              # messages the daemon has served (from its replies)
         self._mine = self._peer = None
         self._sync = None            # lane connections: (c2d, d2c) word pointers in the mapped sync slot
@@ -708,13 +721,18 @@ class TubeClient:
         if shm:                      # messages over shared-memory rings from here on (channel.py)
             with self._io:
                 self.ch.upgrade()
-                self._sent += 1
+                self._sent_py += 1
                 self._lane = bool(self._recv().get("lane"))
         if events and self._lane:
             # the lane orders both sides through two words of a pool slot mapped here
             rep = self._call({"op": "hello", "gpu": device, "memops": True})
             p = self._mapped(rep).ptr + rep["off"] + rep["sync_off"]
             self._sync = (p, p + 128)
+            cl = C.c_void_p()
+            dev.LIB.ft_client_create(self.ch._chan, C.c_void_p(p), C.c_void_p(p + 128), device, C.byref(cl))  # noqa: SLF001
+            self.ch.adopt_client(cl)
+            self._cl = cl
+            self._rbuf, self._rn = C.create_string_buffer(8192), C.c_uint32()
         elif events:
             self._mine = dev.IpcEventRing(device)
             self._used = [0] * self._mine.k        # message number that carried each event's last record
@@ -725,10 +743,20 @@ class TubeClient:
         self._bin = self._lane and events      # binary requests need the stream-ordered protocol
 
     # ---- framing
+    @property
+    def _sent(self) -> int:
+        """Messages sent (Python's and the native client's)."""
+        if self._cl is None:
+            return self._sent_py
+        n = C.c_uint64()
+        dev.LIB.ft_client_sent(self._cl, C.byref(n))
+        return self._sent_py + n.value
+
     def _send(self, msg: dict):
         with self._io:
             self.ch.send_msg(msg)
-            self._sent += 1
+            if self._cl is None:
+                self._sent_py += 1
 
     def _call(self, msg: dict):
         with self._io:
@@ -739,25 +767,34 @@ class TubeClient:
         """A binary request / reply of the native lane (csrc/lane.cc): header (acked,
         unmap notices, an fd after the message), payload."""
         with self._io:
-            self.ch.send_raw(body)
-            self._sent += 1
-            rep = self.ch.recv_raw()
-            kind, ok, has_fd, acked, n_drop, _ = _REPHDR.unpack_from(rep)
-            if kind != _REP_KIND:
-                raise DaemonError(f"unexpected reply kind {kind:#x}")
-            self._acked = max(self._acked, acked)
-            end = len(rep) - 8 * n_drop
-            for bid in struct.unpack_from(f"<{n_drop}Q", rep, end):
-                imp = self._imports.pop(bid, None)
-                if imp is not None:
-                    imp.close()
-            p = rep[_REPHDR.size:end]
-            if not ok:
-                n = struct.unpack_from("<I", p)[0]
-                name = p[4:4 + n].decode()
-                m = struct.unpack_from("<I", p, 4 + n)[0]
-                raise DaemonError(f"{name}: {p[8 + n:8 + n + m].decode()}")
-            fd = dev.recv_fd(self.ch.sock)[0] if has_fd else None
+            if self._cl is not None:
+                rep = self.ch.client_reply(dev.LIB.raw("ft_client_call")(
+                    self._cl, body, len(body), self._rbuf, len(self._rbuf), C.byref(self._rn), _SPIN),
+                    self._rbuf, self._rn)
+            else:
+                self.ch.send_raw(body)
+                self._sent_py += 1
+                rep = self.ch.recv_raw()
+            return self._bin_reply(rep)
+
+    def _bin_reply(self, rep: bytes):
+        """(payload, fd) of a binary reply: acked, unmap notices, typed errors, the fd."""
+        kind, ok, has_fd, acked, n_drop, _ = _REPHDR.unpack_from(rep)
+        if kind != _REP_KIND:
+            raise DaemonError(f"unexpected reply kind {kind:#x}")
+        self._acked = max(self._acked, acked)
+        end = len(rep) - 8 * n_drop
+        for bid in struct.unpack_from(f"<{n_drop}Q", rep, end):
+            imp = self._imports.pop(bid, None)
+            if imp is not None:
+                imp.close()
+        p = rep[_REPHDR.size:end]
+        if not ok:
+            n = struct.unpack_from("<I", p)[0]
+            name = p[4:4 + n].decode()
+            m = struct.unpack_from("<I", p, 4 + n)[0]
+            raise DaemonError(f"{name}: {p[8 + n:8 + n + m].decode()}")
+        fd = dev.recv_fd(self.ch.sock)[0] if has_fd else None
         return p, fd
 
     def _block_bin(self, body: bytes) -> dict:
@@ -797,14 +834,10 @@ class TubeClient:
         """Record one of our events on ``stream`` for the next message (-1: the
         daemon may still have a wait on that event's previous record to enqueue —
         synchronise ``stream`` instead)."""
-        if self._sync is not None:
-            with self._io:
-                v = (self._seq + 1) & 0xFFFFFFFF
-                if v in (0, 0xFFFFFFFF):
-                    v = 1
-                dev.LIB.ft_stream_write32(C.c_void_p(dev.stream_ptr(stream)), C.c_void_p(self._sync[0]), v)
-                self._seq = v
-                return v - (1 << 32) if v >= (1 << 31) else v      # int32 on the wire
+        if self._cl is not None:
+            ev = C.c_int32()
+            dev.LIB.ft_client_mark(self._cl, C.c_void_p(dev.stream_ptr(stream)), C.byref(ev))
+            return ev.value
         if self._mine is None:
             stream.synchronize()
             return -1
@@ -820,10 +853,9 @@ class TubeClient:
     def _after_daemon(self, rep: dict, stream):
         """``stream`` waits for the daemon's mark in ``rep`` (host-synced connections: nothing)."""
         ev = rep.get("ev", -1)
-        if self._sync is not None:
+        if self._cl is not None:
             if ev is not None and ev not in (0, -1):
-                dev.LIB.ft_stream_wait32(C.c_void_p(dev.stream_ptr(stream)), C.c_void_p(self._sync[1]),
-                                         int(ev) & 0xFFFFFFFF)
+                dev.LIB.ft_client_wait(self._cl, C.c_void_p(dev.stream_ptr(stream)), int(ev))
             return
         if self._peer is not None and ev is not None and ev >= 0:
             self._peer.wait(int(ev), stream)
@@ -857,6 +889,31 @@ class TubeClient:
         else:
             imp = self._imports[rep["block"]]
         ptr = imp.ptr + rep.get("off", 0)
+        if self._cl is not None and not response and t.dtype in _CODE and t.dim() <= 8:
+            # wait for the loan's mark, copy, mark, commit, reply: one native call
+            name = producer.encode()
+            body = C.create_string_buffer(_COMMIT.pack(OP_COMMIT, _CODE[t.dtype], t.dim(), 0, 0, consumers,
+                                                       len(name), rep["token"], data_id, n)
+                                          + struct.pack(f"<{t.dim()}q", *t.shape) + name)
+            cur = dev.current_stream(self.device)
+            with self._io:
+                rc = dev.LIB.raw("ft_client_store")(self._cl, C.c_void_p(cur), int(rep.get("ev", 0) or 0),
+                                                    C.c_void_p(ptr), C.c_void_p(t.data_ptr()), n, self._engine(t),
+                                                    body, len(body) - 1, self._rbuf, len(self._rbuf),
+                                                    C.byref(self._rn), _SPIN)
+                if rc not in (0, 12, 13):
+                    from ._lib import raise_status
+                    raise_status(rc)
+                p, fd = self._bin_reply(self.ch.client_reply(rc, self._rbuf, self._rn))
+            if t is not output:
+                t.record_stream(torch.cuda.current_stream(self.device))
+            rep = _parse_block_reply(p)
+            if fd is not None:
+                rep["_fd"] = fd
+            if rep.get("loan"):
+                self._mapped(rep)
+                self._loans[n] = rep
+            return
         if not self._events:
             cur = self._stream
             cur.wait_stream(torch.cuda.current_stream(self.device))
@@ -901,6 +958,39 @@ class TubeClient:
                 out.view(-1).view(torch.uint8).copy_(res.view(-1).view(torch.uint8))
                 return out
             return res
+        if self._cl is not None:
+            # request, reply and the stream's wait for the daemon's mark: one native call
+            nan = float("nan")
+            req = _FETCH.pack(OP_FETCH, self.device, data_id, nan if slo_ms is None else slo_ms,
+                              nan if infer_ms is None else infer_ms)
+            cur = dev.current_stream(self.device)
+            with self._io:
+                rc = dev.LIB.raw("ft_client_fetch")(self._cl, C.c_void_p(cur), req, len(req), self._rbuf,
+                                                    len(self._rbuf), C.byref(self._rn), _SPIN)
+                if rc not in (0, 12, 13):
+                    from ._lib import raise_status
+                    raise_status(rc)
+                raw = self.ch.client_reply(rc, self._rbuf, self._rn)
+                if rc == 12 and raw[1]:                 # (the reply came late: wait for its mark here)
+                    self._after_daemon({"ev": struct.unpack_from("<i", raw, 56)[0]}, cur)
+                p, fd = self._bin_reply(raw)
+            rep = _parse_block_reply(p)
+            ptr = self._mapped(dict(rep, _fd=fd) if fd is not None else rep).ptr + rep["off"]
+            n = rep["nbytes"]
+            if out is None:
+                # zero copy: a DLPack view of the stored block itself; freeing it releases
+                # the block (marked on the legacy default stream by the native deleter)
+                shape = rep["shape"]
+                dl = C.c_void_p()
+                dev.LIB.ft_client_view(self._cl, C.c_void_p(ptr), _CODE[_DTYPES[rep["dtype"]]], len(shape),
+                                       (C.c_int64 * max(1, len(shape)))(*shape), rep["token"], C.byref(dl))
+                return torch.utils.dlpack.from_dlpack(_capsule(dl.value))
+            if not out.is_contiguous() or out.nbytes != n:
+                dev.LIB.ft_client_done(self._cl, None, rep["token"], 0)
+                raise ValueError("out must be contiguous with exactly the stored byte count")
+            dev.LIB.ft_client_copy_done(self._cl, C.c_void_p(cur), C.c_void_p(out.data_ptr()), C.c_void_p(ptr), n,
+                                        self._engine(out), rep["token"])
+            return out
         if self._bin:
             nan = float("nan")
             rep = self._block_bin(_FETCH.pack(OP_FETCH, self.device, data_id, nan if slo_ms is None else slo_ms,
@@ -961,7 +1051,8 @@ class TubeClient:
         if self._bin:
             with self._io:
                 self.ch.send_raw(_DONE.pack(OP_DONE, ev, token))
-                self._sent += 1
+                if self._cl is None:
+                    self._sent_py += 1
         else:
             self._send({"op": "done", "token": token, "ev": ev})
 
@@ -972,7 +1063,12 @@ class TubeClient:
         import gc
         gc.collect()                                   # views dropped by the caller send their done now
         self._closed = True
-        if not self._views:                            # a live view keeps its mapping (until exit)
+        views = self._views
+        if self._cl is not None:
+            nv = C.c_int()
+            dev.LIB.ft_client_views(self._cl, C.byref(nv))
+            views += nv.value
+        if not views:                                  # a live view keeps its mapping (until exit)
             # copies into / out of the mapped blocks may still be queued: unmapping under
             # them faults (an illegal address in this process)
             torch.cuda.synchronize(self.device)
@@ -987,5 +1083,4 @@ class TubeClient:
             if self._mine is not None:
                 self._peer.close()
                 self._mine.close()
-        self.ch.close()
         self.ch.close()
