@@ -820,11 +820,14 @@ def _daemon_client(path, g, q):
 def run_daemon(tube, g):
     """Function process -> per-box daemon (daemon.py): store + fetch latency of a
     spawned client against a TubeDaemon on this tube (same GPU, bit-checked)."""
+    import ctypes as C
     import multiprocessing as mp
     import tempfile
+    from paper_2411_01830_b200 import device as dev
     from paper_2411_01830_b200.daemon import TubeDaemon
     path = os.path.join(tempfile.mkdtemp(), "faastube.sock")
     d = TubeDaemon(tube, path)
+    st = (C.c_uint64 * 9)()
     try:
         ctx = mp.get_context("spawn")
         q = ctx.Queue()
@@ -832,13 +835,19 @@ def run_daemon(tube, g):
         p.start()
         status, res = q.get(timeout=180)
         p.join(timeout=30)
+        if d._lane is not None:  # noqa: SLF001
+            dev.LIB.ft_lane_stats(d._lane, st, 9)  # noqa: SLF001
     finally:
         d.close()
     if status != "ok":
         return {"error": res}
-    return {"workload": "spawned function process through the daemon (same GPU, msgpack frames, IPC-event "
-                        "ordering, lent output blocks): store; fetch(out=) copy; fetch() zero-copy view + its "
-                        "release; host wall time per call", "sizes": res}
+    return {"workload": "spawned function process through the daemon's native lane (C++ worker per connection, "
+                        "binary messages on shared-memory rings, stream-ordered through two sync words in pool "
+                        "memory, lent output blocks recycled per size class): store; fetch(out=) copy; fetch() "
+                        "zero-copy DLPack view + its release; host wall time per call in the function process",
+            "sizes": res,
+            "lane_stats": dict(zip(("commits", "fetches", "dones", "unique_ids", "handed_to_python", "stock_hits",
+                                    "stock_misses", "adopted", "recycled"), list(st)))}
 
 
 def _ev(torch):

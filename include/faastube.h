@@ -438,7 +438,7 @@ int ft_client_recv(ft_client* cl, void* rep, uint32_t cap, uint32_t* rep_len, in
 int ft_client_mark(ft_client* cl, void* stream, int32_t* ev);
 int ft_client_wait(ft_client* cl, void* stream, int32_t ev);
 int ft_client_store(ft_client* cl, void* stream, int32_t wait_ev, void* dst, const void* src, uint64_t n, int engine,
-                    void* req, uint32_t req_len, void* rep, uint32_t cap, uint32_t* rep_len, int64_t spin_us);
+                    const void* req, uint32_t req_len, void* rep, uint32_t cap, uint32_t* rep_len, int64_t spin_us);
 int ft_client_fetch(ft_client* cl, void* stream, const void* req, uint32_t req_len, void* rep, uint32_t cap,
                     uint32_t* rep_len, int64_t spin_us);
 int ft_client_copy_done(ft_client* cl, void* stream, void* dst, const void* src, uint64_t n, int engine,

@@ -279,7 +279,7 @@ _SIGS = {
     "ft_client_recv": (None, [vp, vp, C.c_uint32, P(C.c_uint32), i64]),
     "ft_client_mark": (None, [vp, vp, P(C.c_int32)]),
     "ft_client_wait": (None, [vp, vp, C.c_int32]),
-    "ft_client_store": (None, [vp, vp, C.c_int32, vp, vp, u64, C.c_int, vp, C.c_uint32, vp, C.c_uint32,
+    "ft_client_store": (None, [vp, vp, C.c_int32, vp, vp, u64, C.c_int, C.c_char_p, C.c_uint32, vp, C.c_uint32,
                                P(C.c_uint32), i64]),
     "ft_client_fetch": (None, [vp, vp, C.c_char_p, C.c_uint32, vp, C.c_uint32, P(C.c_uint32), i64]),
     "ft_client_copy_done": (None, [vp, vp, vp, vp, u64, C.c_int, u64]),

@@ -215,8 +215,11 @@ int ft_client_wait(ft_client* cl, void* stream, int32_t ev) {
 // output into the block, marks; the commit request (its ev field at byte 4 is filled
 // in here) goes out and its reply comes back into `rep`
 int ft_client_store(ft_client* cl, void* stream, int32_t wait_ev, void* dst, const void* src, uint64_t n, int engine,
-                    void* req, uint32_t req_len, void* rep, uint32_t cap, uint32_t* rep_len, int64_t spin_us) {
-  if (!cl || !req || req_len < 8 || !rep_len) return FT_E_VALUE;
+                    const void* req_in, uint32_t req_len, void* rep, uint32_t cap, uint32_t* rep_len,
+                    int64_t spin_us) {
+  uint8_t req[1024];
+  if (!cl || !req_in || req_len < 8 || req_len > sizeof req || !rep_len) return FT_E_VALUE;
+  memcpy(req, req_in, req_len);
   cudaStream_t st = (cudaStream_t)stream;
   int rc = cl->wait(st, wait_ev);
   if (rc == FT_OK && n) rc = ft_copy_ex(dst, src, n, cl->device, stream, engine, 0);
@@ -225,7 +228,7 @@ int ft_client_store(ft_client* cl, void* stream, int32_t wait_ev, void* dst, con
   int32_t ev = 0;
   rc = cl->mark(st, &ev);
   if (rc != FT_OK) return rc;
-  memcpy(static_cast<uint8_t*>(req) + 4, &ev, 4);
+  memcpy(req + 4, &ev, 4);
   rc = cl->send(req, req_len);
   if (rc != FT_OK) return rc;
   return cl->recv(rep, cap, rep_len, spin_us);

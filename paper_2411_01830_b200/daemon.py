@@ -733,6 +733,7 @@ class TubeClient:
             self.ch.adopt_client(cl)
             self._cl = cl
             self._rbuf, self._rn = C.create_string_buffer(8192), C.c_uint32()
+            self._rn_ref = C.byref(self._rn)
         elif events:
             self._mine = dev.IpcEventRing(device)
             self._used = [0] * self._mine.k        # message number that carried each event's last record
@@ -892,15 +893,13 @@ class TubeClient:
         if self._cl is not None and not response and t.dtype in _CODE and t.dim() <= 8:
             # wait for the loan's mark, copy, mark, commit, reply: one native call
             name = producer.encode()
-            body = C.create_string_buffer(_COMMIT.pack(OP_COMMIT, _CODE[t.dtype], t.dim(), 0, 0, consumers,
-                                                       len(name), rep["token"], data_id, n)
-                                          + struct.pack(f"<{t.dim()}q", *t.shape) + name)
+            body = _COMMIT.pack(OP_COMMIT, _CODE[t.dtype], t.dim(), 0, 0, consumers, len(name), rep["token"],
+                                data_id, n) + struct.pack(f"<{t.dim()}q", *t.shape) + name
             cur = dev.current_stream(self.device)
             with self._io:
-                rc = dev.LIB.raw("ft_client_store")(self._cl, C.c_void_p(cur), int(rep.get("ev", 0) or 0),
-                                                    C.c_void_p(ptr), C.c_void_p(t.data_ptr()), n, self._engine(t),
-                                                    body, len(body) - 1, self._rbuf, len(self._rbuf),
-                                                    C.byref(self._rn), _SPIN)
+                rc = dev.LIB.raw("ft_client_store")(self._cl, cur, rep.get("ev") or 0, ptr, t.data_ptr(), n,
+                                                    self._engine(t), body, len(body), self._rbuf, len(self._rbuf),
+                                                    self._rn_ref, _SPIN)
                 if rc not in (0, 12, 13):
                     from ._lib import raise_status
                     raise_status(rc)
@@ -965,8 +964,8 @@ class TubeClient:
                               nan if infer_ms is None else infer_ms)
             cur = dev.current_stream(self.device)
             with self._io:
-                rc = dev.LIB.raw("ft_client_fetch")(self._cl, C.c_void_p(cur), req, len(req), self._rbuf,
-                                                    len(self._rbuf), C.byref(self._rn), _SPIN)
+                rc = dev.LIB.raw("ft_client_fetch")(self._cl, cur, req, len(req), self._rbuf, len(self._rbuf),
+                                                    self._rn_ref, _SPIN)
                 if rc not in (0, 12, 13):
                     from ._lib import raise_status
                     raise_status(rc)
