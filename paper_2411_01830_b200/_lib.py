@@ -296,14 +296,14 @@ _SIGS = {
     "ft_signal": (None, [vp, C.c_uint32, C.c_int, vp]),
     "ft_wait": (None, [vp, C.c_uint32, C.c_int, vp]),
     "ft_wait_timeout": (None, [vp, C.c_uint32, u64, vp, C.c_int, vp]),
-    "ft_copy_batch": (None, [P(SegmentC), C.c_int, C.c_int, vp]),
+    "ft_copy_batch": (None, [vp, C.c_int, C.c_int, vp]),
     "ft_store_commit": (None, [vp, vp, i64, C.c_int, C.c_int, dbl, dbl, cstr, C.c_int, dbl, P(dbl), P(dbl)]),
     "ft_retire_commit": (None, [vp, vp, i64, i64, cstr, P(dbl), P(dbl)]),
     "ft_store_local": (None, [vp, vp, i64, C.c_int, C.c_int, dbl, dbl, cstr, C.c_int, dbl, vp, vp, vp, C.c_uint32,
                               P(vp), C.c_int, vp, P(dbl), P(dbl)]),
     "ft_fetch_local": (None, [vp, vp, i64, i64, cstr, C.c_int, vp, vp, u64, C.c_int, vp, C.c_uint32, P(vp), C.c_int,
                               vp, P(dbl), P(dbl)]),
-    "ft_retire_many": (None, [vp, vp, C.c_int, P(i64), P(i64), P(cstr), P(dbl), P(dbl)]),
+    "ft_retire_many": (None, [vp, vp, C.c_int, vp, vp, P(cstr), vp, vp]),
     "ft_stream_create": (None, [C.c_int, P(vp)]),
     "ft_stream_destroy": (None, [vp]),
     "ft_event_create": (None, [C.c_int, P(vp)]),

@@ -16,6 +16,7 @@ kernels or on the copy engines.
 
 from __future__ import annotations
 
+import array
 import ctypes as C
 import itertools
 import os
@@ -192,10 +193,11 @@ def copy_batch(segments, device: int, stream=None):
 
 
 def copy_batch_flat(flat, device: int, stream=None):
-    """``copy_batch`` with the segments already flat: [dst, src, nbytes, dst, src, nbytes, ...]."""
-    from ._lib import SegmentC
-    arr = (C.c_uint64 * len(flat))(*flat)
-    LIB.ft_copy_batch(C.cast(arr, C.POINTER(SegmentC)), len(flat) // 3, int(device), C.c_void_p(stream_ptr(stream)))
+    """``copy_batch`` with the segments already flat: [dst, src, nbytes, dst, src, nbytes, ...]
+    (packed by the array module: a ctypes array built element by element cost ~10 us at 64)."""
+    arr = array.array("Q", flat)
+    addr, _n = arr.buffer_info()
+    LIB.ft_copy_batch(C.c_void_p(addr), len(flat) // 3, int(device), C.c_void_p(stream_ptr(stream)))
 
 
 def _needed(stream: int, events) -> list:
@@ -582,12 +584,15 @@ class DevicePool:
     def retire_many(self, index, items):
         """Batched retire: [(data_id, block, producer, fences)] -> [(R_window, last | None)]."""
         n = len(items)
-        ids = (C.c_int64 * n)(*[d for d, _, _, _ in items])
-        bids = (C.c_int64 * n)(*[b.policy_block.block_id for _, b, _, _ in items])
-        names = (C.c_char_p * n)(*[self._enc(f) for _, _, f, _ in items])
-        rws, lasts = (C.c_double * n)(), (C.c_double * n)()
+        enc = self._names
+        ids = array.array("q", [d for d, _, _, _ in items])
+        bids = array.array("q", [b.policy_block.block_id for _, b, _, _ in items])
+        names = (C.c_char_p * n)(*[enc.get(f) or self._enc(f) for _, _, f, _ in items])
+        rws, lasts = array.array("d", bytes(8 * n)), array.array("d", bytes(8 * n))
         with self._lock:
-            LIB.ft_retire_many(index._h, self.policy._h, n, ids, bids, names, rws, lasts)
+            LIB.ft_retire_many(index._h, self.policy._h, n, C.c_void_p(ids.buffer_info()[0]),
+                                      C.c_void_p(bids.buffer_info()[0]), names, C.c_void_p(rws.buffer_info()[0]),
+                                      C.c_void_p(lasts.buffer_info()[0]))
             for _, b, _, f in items:
                 b.policy_block.in_use = False
                 self._fences[b.policy_block.block_id] = tuple(f)

@@ -795,15 +795,20 @@ class FaaSTube:
                         and out.nbytes == obj.nbytes and out.is_contiguous()):
                     g = by_gpu.get(obj.gpu)
                     if g is None:
-                        g = by_gpu[obj.gpu] = ([], [], [])     # objects, ready events, flat segments
+                        g = by_gpu[obj.gpu] = ([], {}, [])     # objects, newest ready per stream, segments
                     g[0].append(obj)
-                    g[1].append(obj.ready)
+                    r = obj.ready
+                    if r is not None:                          # (the newest record per stream covers the rest)
+                        k = r.stream if r.stream is not None else id(r)
+                        cur = g[1].get(k)
+                        if cur is None or r.seq > cur.seq:
+                            g[1][k] = r
                     g[2].extend((out.data_ptr(), obj.block.ptr, obj.nbytes))
                 else:
                     rest.append((did, out))
             for g, (group, readies, flat) in by_gpu.items():
                 s = self._stream(g)
-                dev.wait_events(s, readies)
+                dev.wait_events(s, readies.values())
                 dev.copy_batch_flat(flat, g, s)
                 done = dev.Ev(g).record(s)     # one fence for every block the batch read
                 retiring = []
