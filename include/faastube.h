@@ -371,7 +371,7 @@ typedef struct ft_lane ft_lane;
 typedef struct ft_lane_conn ft_lane_conn;
 #pragma pack(push, 1)
 typedef struct {         /* one event record (+ name_len bytes of producer name)         */
-  uint32_t kind;         /* 1 committed, 2 retired, 3 freed, 4 stock, 5 unpin, 6 fence   */
+  uint32_t kind;         /* 1 committed, 2 retired, 3 freed, 4 stock, 5 unpin            */
                          /* (stock: data_id = the connection id, consumers = blocks wanted) */
   uint32_t name_len;
   int64_t data_id;
@@ -388,9 +388,6 @@ typedef struct {
   double stored_at_ms;
   void* ready;           /* cudaEvent_t, owned by the taker */
   int32_t gpu, dtype, ndim, remaining, pins, consumers;
-  int64_t queue_pos;
-  void* readers[8];      /* earlier consumers' read events (owned by the taker) */
-  int32_t n_readers;
 } ft_lane_obj;
 int ft_lane_create(ft_index* index, int node, double t0_s, ft_lane** out);
 int ft_lane_set_pool(ft_lane* lane, int gpu, ft_vmm_pool* pool);
@@ -423,20 +420,6 @@ int ft_lane_conn_id(ft_lane_conn* c, uint64_t* id);
 int ft_lane_events(ft_lane* lane, void* buf, uint64_t cap, uint64_t* n, int64_t timeout_us);
 int ft_lane_take(ft_lane* lane, int64_t data_id, ft_lane_obj* out, int64_t* shape, char* producer, int producer_cap);
 int ft_lane_ids(ft_lane* lane, int gpu, int64_t* ids, int cap, int* n);
-/* the tube's in-process same-GPU path through the lane's table: store into a block the
- * tube allocated (= ft_store_local + the table; caller holds the pool lock), fetch into
- * the caller's buffer, batched fetch (one copy launch per 64, status per item:
- * FT_E_MISSING = not the lane's, the tube serves it)      engine.py:342-511, 667-679 */
-int ft_lane_store_local(ft_lane* lane, ft_pool_policy* policy, int64_t data_id, int gpu, int64_t block_id,
-                        uint64_t vmm_block, void* ptr, uint64_t class_bytes, uint64_t arena, uint64_t offset,
-                        uint64_t arena_bytes, const void* src, uint64_t nbytes, int dtype, int ndim,
-                        const int64_t* shape, const char* producer, int consumers, int64_t queue_pos, double now_ms,
-                        double concurrency, void* stream, uint32_t hints, void* const* waits, int nwaits,
-                        double* r_window, double* last);
-int ft_lane_fetch_local(ft_lane* lane, int64_t data_id, int gpu, void* dst, uint64_t nbytes, void* stream,
-                        uint32_t hints);
-int ft_lane_fetch_many_local(ft_lane* lane, int n, const int64_t* data_ids, const uint64_t* dsts,
-                             const uint64_t* sizes, int gpu, void* stream, int32_t* status);
 /* commits, fetches, dones, unique ids, handed to Python, stock hits, stock misses, adopted, recycled */
 int ft_lane_stats(ft_lane* lane, uint64_t* out, int cap);
 

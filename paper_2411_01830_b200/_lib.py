@@ -270,11 +270,6 @@ _SIGS = {
     "ft_lane_take": (None, [vp, i64, vp, P(i64), C.c_char_p, C.c_int]),
     "ft_lane_ids": (None, [vp, C.c_int, P(i64), C.c_int, P(C.c_int)]),
     "ft_lane_stats": (None, [vp, P(u64), C.c_int]),
-    "ft_lane_store_local": (None, [vp, vp, i64, C.c_int, i64, u64, vp, u64, u64, u64, u64, vp, u64, C.c_int, C.c_int,
-                                   P(i64), C.c_char_p, C.c_int, i64, dbl, dbl, vp, C.c_uint32, P(vp), C.c_int,
-                                   P(dbl), P(dbl)]),
-    "ft_lane_fetch_local": (None, [vp, i64, C.c_int, vp, u64, vp, C.c_uint32]),
-    "ft_lane_fetch_many_local": (None, [vp, C.c_int, vp, vp, vp, C.c_int, vp, vp]),
     "ft_client_create": (None, [vp, vp, vp, C.c_int, P(vp)]),
     "ft_client_destroy": (None, [vp]),
     "ft_client_sent": (None, [vp, P(u64)]),

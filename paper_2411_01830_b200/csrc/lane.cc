@@ -55,7 +55,7 @@ namespace {
 
 enum : uint8_t { OP_COMMIT = 1, OP_FETCH = 2, OP_DONE = 3, OP_UID = 4 };
 enum : uint8_t { REP_KIND = 0xB1 };
-enum : uint32_t { EV_COMMITTED = 1, EV_RETIRED = 2, EV_FREED = 3, EV_STOCK = 4, EV_UNPIN = 5, EV_FENCE = 6 };
+enum : uint32_t { EV_COMMITTED = 1, EV_RETIRED = 2, EV_FREED = 3, EV_STOCK = 4, EV_UNPIN = 5 };
 constexpr int kDtypes = 10;
 const int kItem[kDtypes] = {1, 1, 2, 4, 8, 2, 2, 4, 8, 1};  // uint8 int8 int16 int32 int64 f16 bf16 f32 f64 bool
 constexpr int kMaxDim = 8;
@@ -127,11 +127,7 @@ struct LObj {
   bool retired = false;
   bool adopted = false;  // the tube took it while views were alive (their releases go to it)
   cudaEvent_t ready = nullptr;
-  cudaStream_t ready_stream = nullptr;  // where `ready` was recorded, and in which order
-  uint64_t ready_seq = 0;               //   (a batched read waits on the newest per stream)
   double stored_at = 0.0;
-  int64_t queue_pos = 0;
-  std::vector<cudaEvent_t> readers;  // in-process reads by a consumer that was not the last
 };
 
 struct Token {
@@ -194,7 +190,6 @@ struct ft_lane {
   uint64_t next_token = kTokenBase;
   std::vector<ft_lane_conn*> conns;
   uint64_t next_conn = 1;
-  uint64_t rec_seq = 0;  // order of the objects' ready records
   std::map<int, std::vector<cudaEvent_t>> evpool;
   // event queue to the tube
   std::mutex emu;
@@ -394,34 +389,20 @@ std::string block_payload(uint64_t token, const LBlock& b, uint64_t nbytes, int 
   return p;
 }
 
-// (lane->mu held) a retired object with no view left: the block goes back to the pool
-// (or straight into a lend stock), fenced on `st` (which waited for the last read) and
-// on the in-process readers' events (FENCE records). `shared`: a fence event already
-// recorded for a whole batch — the tube adopts it once (FREED.consumers = 1)
-void free_obj(ft_lane* L, int gpu, cudaStream_t st, LObj& o, cudaEvent_t shared = nullptr) {
-  cudaEvent_t f = shared;
-  if (!f) {
-    f = L->get_event(gpu);
-    cudaEventRecord(f, st);
-    if (o.readers.empty() && recycle(L, o.blk, f)) {
-      L->put_event(o.blk.gpu, o.ready);
-      L->objs.erase(o.did);
-      return;
-    }
-  }
-  for (cudaEvent_t r : o.readers) {
-    EvRec x{};
-    x.kind = EV_FENCE;
-    x.gpu = o.blk.gpu;
-    x.pbid = o.blk.pbid;
-    x.handle = (uint64_t)(uintptr_t)r;
-    L->emit(x);
+// (lane->mu held) a retired object with no view left: the block goes back to the pool,
+// fenced on the connection stream (it waited for the reader's release)
+void free_obj(ft_lane* L, ft_lane_conn* c, LObj& o) {
+  cudaEvent_t f = L->get_event(c->gpu);
+  cudaEventRecord(f, c->stream);
+  if (recycle(L, o.blk, f)) {
+    L->put_event(o.blk.gpu, o.ready);
+    L->objs.erase(o.did);
+    return;
   }
   EvRec r{};
   r.kind = EV_FREED;
   r.did = o.did;
   r.gpu = o.blk.gpu;
-  r.consumers = shared ? 1 : 0;
   r.pbid = o.blk.pbid;
   r.nbytes = o.nbytes;
   r.handle = (uint64_t)(uintptr_t)f;
@@ -429,7 +410,6 @@ void free_obj(ft_lane* L, int gpu, cudaStream_t st, LObj& o, cudaEvent_t shared 
   L->put_event(o.blk.gpu, o.ready);
   L->objs.erase(o.did);
 }
-void free_obj(ft_lane* L, ft_lane_conn* c, LObj& o) { free_obj(L, c->gpu, c->stream, o); }
 
 void retire_obj(ft_lane* L, LObj& o) {  // (lane->mu held) engine.py:667-679
   o.retired = true;
@@ -511,8 +491,6 @@ bool handle_commit(ft_lane_conn* c, const std::string& m) {
   o.ready = L->get_event(c->gpu);
   o.stored_at = now;
   cudaEventRecord(o.ready, c->stream);
-  o.ready_stream = c->stream;
-  o.ready_seq = ++L->rec_seq;
   EvRec r{};
   r.kind = EV_COMMITTED;
   r.did = q.did;
@@ -947,13 +925,7 @@ int ft_lane_take(ft_lane* L, int64_t did, ft_lane_obj* out, int64_t* shape, char
   }
   LObj& o = it->second;
   *out = ft_lane_obj{o.did, o.blk.pbid, o.nbytes, o.stored_at, (void*)o.ready, o.blk.gpu, o.dtype,
-                     (int32_t)o.shape.size(), o.retired ? 0 : o.remaining, o.pins, o.consumers, o.queue_pos};
-  // in-process readers' events go with the object (the tube fences the block's reuse on them)
-  for (size_t i = 0; i < o.readers.size() && i < 8; ++i) out->readers[i] = (void*)o.readers[i];
-  out->n_readers = (int32_t)std::min<size_t>(o.readers.size(), 8);
-  for (size_t i = 8; i < o.readers.size(); ++i) cudaEventSynchronize(o.readers[i]);  // (rare: > 8 readers)
-  for (size_t i = 8; i < o.readers.size(); ++i) L->put_event(o.blk.gpu, o.readers[i]);
-  o.readers.clear();
+                     (int32_t)o.shape.size(), o.retired ? 0 : o.remaining, o.pins, o.consumers};
   memcpy(shape, o.shape.data(), 8 * o.shape.size());
   snprintf(producer, (size_t)producer_cap, "%s", o.producer.c_str());
   ++L->stats[7];
@@ -1001,163 +973,6 @@ int ft_lane_ids(ft_lane* L, int gpu, int64_t* out, int cap, int* n) {
     }
   *n = k;
   return k > cap ? FT_E_TRUNCATED : FT_OK;
-}
-
-// ---- the in-process same-GPU path (the tube's store / fetch / fetch_many) ----------
-
-// store into a pool block the tube allocated: ft_store_local (fence waits, TMA copy,
-// index entry, histogram sample — the caller holds the pool's lock) with the object
-// kept in the lane's table, so the fetches below and function processes find it
-int ft_lane_store_local(ft_lane* L, ft_pool_policy* policy, int64_t did, int gpu, int64_t pbid, uint64_t vmm,
-                        void* ptr, uint64_t cap, uint64_t arena, uint64_t off, uint64_t arena_bytes, const void* src,
-                        uint64_t nbytes, int dtype, int ndim, const int64_t* shape, const char* producer,
-                        int consumers, int64_t queue_pos, double now_ms, double concurrency, void* stream,
-                        uint32_t hints, void* const* waits, int nwaits, double* r_window, double* last) {
-  if (!L || !policy || dtype < 0 || dtype >= kDtypes || ndim < 0 || ndim > kMaxDim || nbytes > cap)
-    return FT_E_VALUE;
-  {
-    std::lock_guard<std::mutex> lk(L->mu);
-    if (L->objs.count(did)) {
-      ft::set_last_error("data id " + std::to_string(did) + " already stored");
-      return FT_E_DUPLICATE;
-    }
-  }
-  cudaEvent_t ready = nullptr;
-  {
-    std::lock_guard<std::mutex> lk(L->mu);
-    ready = L->get_event(gpu);
-  }
-  int rc = ft_copy_ordered(ptr, src, nbytes, gpu, stream, hints, waits, nwaits, ready);
-  if (rc == FT_OK)
-    rc = ft_store_commit(L->index, policy, did, L->node, gpu, (double)nbytes, now_ms, producer, 0, concurrency,
-                         r_window, last);
-  std::lock_guard<std::mutex> lk(L->mu);
-  if (rc != FT_OK) {
-    L->put_event(gpu, ready);
-    return rc;
-  }
-  LObj& o = L->objs[did];
-  o.did = did;
-  o.blk = LBlock{pbid, vmm, static_cast<uint8_t*>(ptr), cap, arena, off, arena_bytes, gpu, {}};
-  o.nbytes = nbytes;
-  o.dtype = (uint8_t)dtype;
-  o.shape.assign(shape, shape + ndim);
-  o.producer = producer ? producer : "";
-  o.consumers = o.remaining = consumers > 0 ? consumers : 1;
-  o.ready = ready;
-  o.ready_stream = (cudaStream_t)stream;
-  o.ready_seq = ++L->rec_seq;
-  o.stored_at = now_ms;
-  o.queue_pos = queue_pos;
-  ++L->stats[0];
-  return FT_OK;
-}
-
-namespace {
-// (lane->mu held) one consumer's read of `o` is enqueued on `st`: count it; the last
-// consumer retires the object (index entry dropped, RETIRED for the tube's accounting)
-// and frees the block once no view pins it; an earlier consumer leaves its read's event
-void consumed_local(ft_lane* L, LObj& o, int gpu, cudaStream_t st, cudaEvent_t shared) {
-  o.remaining -= 1;
-  if (o.remaining > 0) {
-    cudaEvent_t r = shared;
-    if (!r) {
-      r = L->get_event(gpu);
-      cudaEventRecord(r, st);
-    } else {
-      // a batch's shared read event: the object keeps its own copy of the ordering
-      cudaEvent_t own = L->get_event(gpu);
-      cudaEventRecord(own, st);
-      r = own;
-    }
-    o.readers.push_back(r);
-    return;
-  }
-  retire_obj(L, o);
-  if (o.pins <= 0) free_obj(L, gpu, st, o, shared);
-}
-bool local_ok(const LObj* o, int gpu, uint64_t nbytes) {
-  return o && !o->retired && !o->adopted && o->blk.gpu == gpu && o->nbytes == nbytes;
-}
-}  // namespace
-
-// fetch a lane object into the caller's buffer on `stream` (same GPU): FT_E_MISSING if
-// the lane does not hold it here with exactly `nbytes` (the tube's own path serves it)
-int ft_lane_fetch_local(ft_lane* L, int64_t did, int gpu, void* dst, uint64_t nbytes, void* stream, uint32_t hints) {
-  if (!L) return FT_E_VALUE;
-  std::lock_guard<std::mutex> lk(L->mu);
-  auto it = L->objs.find(did);
-  if (it == L->objs.end() || !local_ok(&it->second, gpu, nbytes)) {
-    ft::set_last_error("not in the lane");
-    return FT_E_MISSING;
-  }
-  LObj& o = it->second;
-  cudaStream_t st = (cudaStream_t)stream;
-  void* wait = o.ready_stream == st ? nullptr : (void*)o.ready;
-  // (the last consumer streams the block through L2 once: evict-first on its reads)
-  int rc = ft_copy_ordered(dst, o.blk.ptr, nbytes, gpu, stream, o.remaining <= 1 ? hints : 0u,
-                           wait ? &wait : nullptr, wait ? 1 : 0, nullptr);
-  if (rc != FT_OK) return rc;
-  ++L->stats[1];
-  consumed_local(L, o, gpu, st, nullptr);
-  return FT_OK;
-}
-
-// a batch of fetches into the callers' buffers: one copy launch per 64 objects, ordered
-// after each stream's newest ready record among them; status[i] FT_OK or FT_E_MISSING
-// (those the tube serves itself). Freed blocks share one fence event.
-int ft_lane_fetch_many_local(ft_lane* L, int n, const int64_t* dids, const uint64_t* dsts, const uint64_t* sizes,
-                             int gpu, void* stream, int32_t* status) {
-  if (!L || n < 0 || !status) return FT_E_VALUE;
-  cudaStream_t st = (cudaStream_t)stream;
-  std::lock_guard<std::mutex> lk(L->mu);
-  std::vector<LObj*> objs(n, nullptr);
-  std::vector<ft_segment> segs;
-  segs.reserve(n);
-  std::vector<std::pair<cudaStream_t, std::pair<uint64_t, cudaEvent_t>>> newest;  // per ready stream
-  for (int i = 0; i < n; ++i) {
-    auto it = L->objs.find(dids[i]);
-    LObj* o = it == L->objs.end() ? nullptr : &it->second;
-    if (!local_ok(o, gpu, sizes[i])) {
-      status[i] = FT_E_MISSING;
-      continue;
-    }
-    for (int j = 0; j < i; ++j)  // the same object twice in one batch: the second goes to the tube
-      if (objs[j] == o) o = nullptr;
-    if (!o) {
-      status[i] = FT_E_MISSING;
-      continue;
-    }
-    status[i] = FT_OK;
-    objs[i] = o;
-    segs.push_back(ft_segment{reinterpret_cast<void*>(dsts[i]), o->blk.ptr, sizes[i]});
-    if (o->ready_stream != st) {
-      bool found = false;
-      for (auto& e : newest)
-        if (e.first == o->ready_stream) {
-          found = true;
-          if (o->ready_seq > e.second.first) e.second = {o->ready_seq, o->ready};
-        }
-      if (!found) newest.push_back({o->ready_stream, {o->ready_seq, o->ready}});
-    }
-  }
-  if (segs.empty()) return FT_OK;
-  for (auto& e : newest) cudaStreamWaitEvent(st, e.second.second, 0);
-  int rc = ft_copy_batch(segs.data(), (int)segs.size(), gpu, stream);
-  if (rc != FT_OK) return rc;
-  cudaEvent_t shared = L->get_event(gpu);
-  cudaEventRecord(shared, st);
-  bool used = false;
-  for (int i = 0; i < n; ++i) {
-    LObj* o = objs[i];
-    if (!o) continue;
-    ++L->stats[1];
-    const bool frees = o->remaining <= 1 && o->pins <= 0;
-    used = used || frees;
-    consumed_local(L, *o, gpu, st, shared);
-  }
-  if (!used) L->put_event(gpu, shared);
-  return FT_OK;
 }
 
 int ft_lane_stats(ft_lane* L, uint64_t* out, int cap) {

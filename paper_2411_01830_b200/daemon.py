@@ -199,21 +199,14 @@ class TubeDaemon:
         # the native lane serves the hot requests of upgraded connections (csrc/lane.cc);
         # its events are applied to the tube by the service thread
         self._lane = None
-        self._own_lane = False     # the tube's lane (its table is shared) or one made here
         self._sync = {}            # gpu -> (pool block of 256-byte sync slots, free slot indices)
-        if lane and getattr(tube, "_lane", None) is not None:
-            self._lane = tube._lane  # noqa: SLF001 - the tube applies its events
-        elif lane and hasattr(tube, "attach_lane") and tube.pools:
-            self._own_lane = True
+        if lane and hasattr(tube, "attach_lane") and tube.pools:
             h = C.c_void_p()
             dev.LIB.ft_lane_create(tube.index._h, int(tube.node), float(tube._t0), C.byref(h))  # noqa: SLF001
             for g, pool in tube.pools.items():
                 dev.LIB.ft_lane_set_pool(h, int(g), pool._h)  # noqa: SLF001
             tube.attach_lane(h)
             self._lane = h
-            self._service = threading.Thread(target=self._service_loop, name="faastube-lane", daemon=True)
-            self._service.start()
-        if self._lane is not None:
             for g in tube.pools:
                 # each connection's two sync words live in a 256-byte slot of this block
                 # (mapped by the client like any pool block); held for the daemon's life
@@ -221,6 +214,8 @@ class TubeDaemon:
                 for e in blk.take_fences():
                     e.synchronize()
                 self._sync[g] = (blk, list(range(blk.nbytes // 256 - 1, -1, -1)))
+            self._service = threading.Thread(target=self._service_loop, name="faastube-lane", daemon=True)
+            self._service.start()
         self._acceptor = threading.Thread(target=self._accept_loop, name="faastube-daemon", daemon=True)
         self._acceptor.start()
 
@@ -617,13 +612,12 @@ class TubeDaemon:
         for th in self._threads:
             th.join(timeout=5)
         if self._lane is not None:
+            self._service.join(timeout=5)
             for g, (blk, _free) in self._sync.items():
                 self.tube.pools[g].free(blk, [])
             self._sync = {}
-            if self._own_lane:
-                self._service.join(timeout=5)
-                self.tube.detach_lane()        # its objects into the tube's table, stocked blocks back
-                dev.LIB.ft_lane_destroy(self._lane)
+            self.tube.detach_lane()            # its objects into the tube's table, stocked blocks back
+            dev.LIB.ft_lane_destroy(self._lane)
             self._lane = None
         try:
             self.server.close()

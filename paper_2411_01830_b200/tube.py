@@ -35,7 +35,6 @@ ops). No call synchronizes the host unless the caller asks for a host tensor;
 
 from __future__ import annotations
 
-import array
 import collections
 import heapq
 import itertools
@@ -94,7 +93,6 @@ class _Obj:
 _LANE_EV = struct.Struct("<IIqiiqQdQ")   # ft_lane_event (include/faastube.h)
 _LANE_DTYPES = (torch.uint8, torch.int8, torch.int16, torch.int32, torch.int64, torch.float16, torch.bfloat16,
                 torch.float32, torch.float64, torch.bool)
-_LANE_CODE = {t: i for i, t in enumerate(_LANE_DTYPES)}
 
 
 class FaaSTube:
@@ -181,18 +179,6 @@ class FaaSTube:
         self.capacity_limit = float(capacity_limit_bytes)   # per-GPU store cap (datastore.py:19)
         self.stats = {"stores": 0, "fetches": 0, "bytes_h2d": 0, "bytes_d2h": 0, "bytes_nvlink": 0,
                       "bytes_local": 0, "zero_copy": 0, "migrated_bytes": 0, "reload_bytes": 0}
-        # same-GPU objects live in the native lane's table (csrc/lane.cc): the in-process
-        # store / fetch / fetch_many are one native call each, and function processes
-        # served by a daemon on this tube share the table (FT_LANE_LOCAL=0: Python table only)
-        self._lane_thread = None
-        if self.pools and self._gpu_store and os.environ.get("FT_LANE_LOCAL", "1") != "0":
-            h = dev.C.c_void_p()
-            dev.LIB.ft_lane_create(self.index._h, int(self.node), float(self._t0), dev.C.byref(h))
-            for g, pool in self.pools.items():
-                dev.LIB.ft_lane_set_pool(h, int(g), pool._h)
-            self.attach_lane(h)
-            self._lane_thread = threading.Thread(target=self._lane_loop, name="faastube-lane", daemon=True)
-            self._lane_thread.start()
 
     # ------------------------------------------------------------ helpers
     def now_ms(self) -> float:
@@ -317,11 +303,6 @@ class FaaSTube:
         ``queue_pos``: request-queue position of the object's next consumer
         (the runtime knows it; default: store order) — drives queue-aware
         migration under memory pressure (datastore.py:192-222)."""
-        if (self._lane is not None and output.is_cuda and self._gpu_store and not response
-                and output.dtype in _LANE_CODE and output.dim() <= 8 and output.is_contiguous()
-                and getattr(output, "_ft_block", None) is None):
-            self._store_lane(data_id, output, producer, consumers, queue_pos)
-            return
         # pinned host buffers are allocated before taking the tube lock (cudaHostAlloc
         # can take milliseconds and must not stall other tenants' calls)
         t0 = time.perf_counter()
@@ -347,64 +328,6 @@ class FaaSTube:
         if t3 - t0 > 0.01:   # slow stores, for diagnosis: ms allocating / in the locked part / migrating, bytes
             self.slow_stores.append((round(1e3 * (t1 - t0), 2), round(1e3 * (t2 - t1), 2),
                                      round(1e3 * (t3 - t2), 2), output.nbytes))
-
-    def _store_lane(self, data_id, t, producer, consumers, queue_pos):
-        """The same-GPU store into the lane's table (engine.py:342-360): a pool block
-        (datastore.py:130-144, allocated outside the tube lock), then one native call —
-        wait the block's fences, TMA snapshot of the producer's output on its stream
-        (L2 evict-first on the reads), ready event, index entry (dataplane.py:72-83),
-        histogram sample (datastore.py:51-62) — then the running accounts, the shrink
-        timer and the store cap check (engine.py:685-702) here."""
-        g = t.get_device()
-        n = t.nbytes
-        pool = self.pools[g]
-        blk = pool.allocate(n)
-        so = self._torch_stream(g)
-        sp = so.cuda_stream
-        now = self.now_ms()
-        qp = queue_pos if queue_pos is not None else next(self._queue)
-        live = self._live[(producer, g)] + 1
-        shape = t.shape
-        evs = dev._needed(sp, blk.fences)
-        C = dev.C
-        try:
-            with pool._lock:  # noqa: SLF001 - the policy's histogram is the pool's state
-                dev.LIB.ft_lane_store_local(
-                    self._lane, pool.policy._h, int(data_id), g, blk.policy_block.block_id, blk.vmm_id,
-                    blk.ptr, int(blk.policy_block.class_bytes), *pool.locate(blk), t.data_ptr(), n,
-                    _LANE_CODE[t.dtype], len(shape), (C.c_int64 * max(1, len(shape)))(*shape), pool._enc(producer),
-                    int(consumers), int(qp), now, float(live), sp, dev.L2_EVICT_FIRST if n <= _L2_KEEP else 0,
-                    (C.c_void_p * max(1, len(evs)))(*evs), len(evs), pool._rw, pool._last)  # noqa: SLF001
-                rw, last = pool._rw.value, pool._last.value  # noqa: SLF001
-        except BaseException:
-            # not stored (e.g. DuplicateStore): the block goes back once the copy (if it ran) is done
-            pool.free(blk, list(blk.fences) + [dev.Ev(g).record(sp)])
-            raise
-        blk.fences = ()
-        t.record_stream(so)
-        with self._lock:
-            self._lane_blocks[blk.policy_block.block_id] = blk
-            self._last_op_ms = now
-            self._live[(producer, g)] += 1
-            self._stored[g] += n
-            self.stats["stores"] += 1
-            self.stats["bytes_local"] += n
-            self._push_due(g, rw, None if last != last else last, now)
-            if self.strategy.migration != "none" and self._stored_on(g) > self.capacity_limit:
-                self._lane_sync()                     # retires still queued may bring it back under
-                if self._stored_on(g) > self.capacity_limit:
-                    self._pending.add(("pressure", g))
-        if self._pending:
-            self._drain_pending()
-
-    def _lane_loop(self):
-        import traceback
-        while not self._closing:
-            try:
-                if not self.lane_service(50.0):
-                    return
-            except Exception:  # noqa: BLE001 - keep serving; the failure is visible in the log
-                traceback.print_exc()
 
     def _after_store(self, stage):
         """The part of a store after the tube lock: a managed GPU->host response
@@ -718,21 +641,6 @@ class FaaSTube:
         ``device=None`` fetches into host memory. With ``out`` the bytes land
         in the caller's buffer (Listing-1 semantics); without it a same-GPU
         fetch is a zero-copy view of the stored block."""
-        if out is not None and self._lane is not None and out.is_cuda and out.is_contiguous():
-            # a same-GPU object of the lane's table into the caller's input: one native call
-            # (wait `ready`, TMA copy, count the consumer; the last one retires the object and
-            # frees its block, fenced on this read — engine.py:667-679)
-            g = out.get_device()
-            rc = dev.LIB.raw("ft_lane_fetch_local")(self._lane, int(data_id), g, out.data_ptr(), out.nbytes,
-                                                    dev.current_stream(g), dev.L2_EVICT_FIRST)
-            if rc == 0:
-                self._last_op_ms = self.now_ms()
-                self.stats["fetches"] += 1
-                self.stats["bytes_local"] += out.nbytes
-                return out
-            if rc != 3:                                 # (3: not the lane's -> the tube's path)
-                from ._lib import raise_status
-                raise_status(rc)
         if out is None and device is not None:
             o = self._objs.get(data_id)
             if o is not None and o.gpu != device:
@@ -875,17 +783,13 @@ class FaaSTube:
         launch once; anything else goes through ``fetch``."""
         if not items:
             return []
-        if self._lane is not None:
-            todo = self._lane_fetch_many(items)
-        else:
-            todo = items
         rest = []
         with self._lock:
             self._reap()
             self._last_op_ms = self.now_ms()
             objs = self._objs
             by_gpu = {}
-            for did, out in todo:
+            for did, out in items:
                 obj = objs.get(did)
                 if (obj is not None and obj.block is not None and obj.gpu == out.get_device()
                         and out.nbytes == obj.nbytes and out.is_contiguous()):
@@ -950,44 +854,6 @@ class FaaSTube:
             self._drain_pending()
         return [out for _, out in items]
 
-    def _lane_fetch_many(self, items) -> list:
-        """The lane's objects among ``items``: one native batch per GPU (a copy launch
-        per 64, each stream's newest ready waited once, retires and frees fenced on one
-        event); returns the items it does not hold."""
-        by_gpu = {}
-        left = []
-        for it in items:
-            out = it[1]
-            if out.is_cuda and out.is_contiguous():
-                g = by_gpu.get(out.get_device())
-                if g is None:
-                    g = by_gpu[out.get_device()] = ([], [], [], [])
-                g[0].append(it)
-                g[1].append(it[0])
-                g[2].append(out.data_ptr())
-                g[3].append(out.nbytes)
-            else:
-                left.append(it)
-        C = dev.C
-        for g, (its, ids, dsts, sizes) in by_gpu.items():
-            n = len(ids)
-            ids, dsts, sizes = array.array("q", ids), array.array("Q", dsts), array.array("Q", sizes)
-            status = array.array("i", bytes(4 * n))
-            dev.LIB.ft_lane_fetch_many_local(self._lane, n, C.c_void_p(ids.buffer_info()[0]),
-                                             C.c_void_p(dsts.buffer_info()[0]), C.c_void_p(sizes.buffer_info()[0]),
-                                             g, dev.current_stream(g), C.c_void_p(status.buffer_info()[0]))
-            done = served = 0
-            for it, st in zip(its, status):
-                if st:
-                    left.append(it)
-                else:
-                    done += it[1].nbytes
-                    served += 1
-            self.stats["fetches"] += served
-            self.stats["bytes_local"] += done
-        self._last_op_ms = self.now_ms()
-        return left
-
     def sync_stream(self, g: int):
         """Block the host until the caller's current stream on GPU ``g`` drained
         (another process is about to touch what it ordered)."""
@@ -1027,15 +893,8 @@ class FaaSTube:
         return obj.response_host.view(obj.dtype).view(obj.shape)
 
     def close(self):
-        lane = self._lane
-        if lane is not None:
-            with self._maint_cv:
-                self._closing = True              # (also stops the lane's service thread)
-            if self._lane_thread is not None:
-                self._lane_thread.join(timeout=5)
+        if self._lane is not None:
             self.detach_lane()
-            if self._lane_thread is not None:     # the tube's own lane (a daemon's is its own)
-                dev.LIB.ft_lane_destroy(lane)
         self.pacer.close()                        # drains in-flight host->GPU stages
         self._tickets.clear()
         with self._maint_cv:
@@ -1064,8 +923,6 @@ class FaaSTube:
         self._lane_blocks = {}       # pool policy block id -> PoolBlock lent to / stocked in / stored by the lane
         self._lane_adopted = {}      # data id -> adopted object whose lane views are still alive
         self._lane_stock_todo = []   # (gpu, class bytes) the lane's stock asked for
-        self._lane_fences = {}       # block id -> readers' fences (FENCE records) for its FREED
-        self._lane_shared = (0, None)  # the last shared batch fence (handle, Ev)
         self._lane_buf = dev.C.create_string_buffer(1 << 20)
         self._lane_n = dev.C.c_uint64()
 
@@ -1185,25 +1042,14 @@ class FaaSTube:
                     self._pending.add(("prefetch", g))
             elif kind == 3:
                 blk = self._lane_blocks.pop(pbid, None)
-                if not evh:      # (no fence: a stocked block nobody wrote — its previous users' fences stay)
-                    fences = list(blk.fences if blk is not None else ())
-                elif cons == 1:  # one fence event shared by a batch's frees: adopted once
-                    if self._lane_shared[0] != evh:
-                        self._lane_shared = (evh, dev.Ev.adopt(evh, g))
-                    fences = [self._lane_shared[1]]
-                else:
-                    fences = [dev.Ev.adopt(evh, g)]
-                extra = self._lane_fences.pop(pbid, None)
-                if extra:
-                    fences += extra
+                # (no fence: a stocked block nobody wrote — its previous users' fences stay)
+                fences = [dev.Ev.adopt(evh, g)] if evh else list(blk.fences if blk is not None else ())
                 if blk is not None:
                     self.pools[g].free(blk, fences)
                     if name:
                         self._push_shrink(g, name, self.now_ms())
             elif kind == 4:
                 self._lane_stock_todo.extend([(did, g, nbytes)] * max(1, cons))
-            elif kind == 6:      # an earlier in-process reader of a block about to be freed
-                self._lane_fences.setdefault(pbid, []).append(dev.Ev.adopt(evh, g))
             elif kind == 5:
                 o = self._lane_adopted.get(did)
                 if o is not None:
@@ -1226,10 +1072,9 @@ class FaaSTube:
         obj = _Obj(did, rec.nbytes, _LANE_DTYPES[rec.dtype], tuple(shape[:rec.ndim]), g, name.value.decode(),
                    rec.remaining, rec.stored_at_ms)
         obj.home = g
-        obj.queue_pos = rec.queue_pos or next(self._queue)
+        obj.queue_pos = next(self._queue)
         obj.block = self._lane_blocks.pop(rec.block_id)
         obj.ready = dev.Ev.adopt(rec.ready, g) if rec.ready else None
-        obj.readers = [dev.Ev.adopt(rec.readers[i], g) for i in range(rec.n_readers)]
         obj.pins = rec.pins
         if rec.pins:
             self._lane_adopted[did] = obj
@@ -1600,5 +1445,4 @@ class _lane_obj_t(dev.C.Structure):
     _fields_ = [("data_id", dev.C.c_int64), ("block_id", dev.C.c_int64), ("nbytes", dev.C.c_uint64),
                 ("stored_at_ms", dev.C.c_double), ("ready", dev.C.c_void_p), ("gpu", dev.C.c_int32),
                 ("dtype", dev.C.c_int32), ("ndim", dev.C.c_int32), ("remaining", dev.C.c_int32),
-                ("pins", dev.C.c_int32), ("consumers", dev.C.c_int32), ("queue_pos", dev.C.c_int64),
-                ("readers", dev.C.c_void_p * 8), ("n_readers", dev.C.c_int32)]
+                ("pins", dev.C.c_int32), ("consumers", dev.C.c_int32)]
