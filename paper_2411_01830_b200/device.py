@@ -170,17 +170,21 @@ class Ev:
                 LIB.raw("ft_event_destroy")(C.c_void_p(h))
 
     def __del__(self):
-        h = getattr(self, "h", None)
-        if h:
+        # (hot: every retired object drops its events — kept to a dict lookup and an append)
+        try:
+            h = self.h
+            if not h:
+                return
             self.h = None
-            try:
+            free = Ev._free.get(self.device)
+            if free is None:
                 free = Ev._free.setdefault(self.device, [])
-                if len(free) < Ev._FREE_MAX:
-                    free.append(h)
-                    return
-                LIB.raw("ft_event_destroy")(C.c_void_p(h))
-            except Exception:  # noqa: BLE001 - interpreter teardown
-                pass
+            if len(free) < 1024:                       # Ev._FREE_MAX
+                free.append(h)
+                return
+            LIB.raw("ft_event_destroy")(C.c_void_p(h))
+        except Exception:  # noqa: BLE001 - interpreter teardown / never initialised
+            pass
 
 
 def copy_batch(segments, device: int, stream=None):
@@ -591,12 +595,15 @@ class DevicePool:
         rws, lasts = array.array("d", bytes(8 * n)), array.array("d", bytes(8 * n))
         with self._lock:
             LIB.ft_retire_many(index._h, self.policy._h, n, C.c_void_p(ids.buffer_info()[0]),
-                                      C.c_void_p(bids.buffer_info()[0]), names, C.c_void_p(rws.buffer_info()[0]),
-                                      C.c_void_p(lasts.buffer_info()[0]))
+                               C.c_void_p(bids.buffer_info()[0]), names, C.c_void_p(rws.buffer_info()[0]),
+                               C.c_void_p(lasts.buffer_info()[0]))
+            fences = self._fences
             for _, b, _, f in items:
-                b.policy_block.in_use = False
-                self._fences[b.policy_block.block_id] = tuple(f)
-                if self.policy.mode == "none":
+                pb = b.policy_block
+                pb.in_use = False
+                fences[pb.block_id] = f
+            if self.policy.mode == "none":
+                for _, b, _, _ in items:
                     self.policy._blocks.pop(b.policy_block.block_id, None)
                     self._unmap(b.policy_block.block_id)
         return [(rws[i], None if lasts[i] != lasts[i] else lasts[i]) for i in range(n)]
