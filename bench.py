@@ -1093,12 +1093,14 @@ def _single_gpu_extras(tube, g, dev, torch):
             h2g.append(a.elapsed_time(b))
     h2g_gbps = n / (statistics.mean(h2g) * 1e-3) / 1e9
     k = len(tube.topo.roots()) if tube.strategy.parallel_pcie else 1     # PCIe links the plan stripes over
+    # the link's peak is the best rate it delivered in this run: a best-of-few raw copy
+    # alone read a little below what a paced fetch later achieved (fractions above 1.0
+    # in round 1); every pinned H2D rate measured here raises it
+    best_seen = [ce_peak, n / (min(h2g) * 1e-3) / 1e9 / k]
     out["h2g"] = {"workload": f"config2 at k={k} ({k} PCIe link{'s' if k > 1 else ''}"
                               f"{', NVLink forwarding into the target' if k > 1 else ''}): 1 GiB pinned -> "
                               "GPU via FaaSTube.fetch",
-                  "links": k, "value": round(h2g_gbps, 3), "unit": "GB/s", "peak": round(k * ce_peak, 3),
-                  "peak_source": f"live: best-of-3 cudaMemcpyAsync 1 GiB pinned H2D on the target's link x {k}",
-                  "frac": round(h2g_gbps / (k * ce_peak), 4)}
+                  "links": k, "value": round(h2g_gbps, 3), "unit": "GB/s"}
     # config 2 at k=1 across sizes: p50/p99 of one pinned host -> GPU fetch (device events)
     sweep = []
     for sz in (4096, 65536, 1 << 20, 16 << 20, 256 << 20, 1 << 30):
@@ -1116,10 +1118,18 @@ def _single_gpu_extras(tube, g, dev, torch):
                 ts.append(a.elapsed_time(b))
         ts.sort()
         p50 = nearest_rank(ts, 50)
+        best_seen.append(sz / (ts[0] * 1e-3) / 1e9)
         sweep.append({"bytes": sz, "ms_p50": round(p50, 4), "ms_p99": round(nearest_rank(ts, 99), 4),
-                      "gbps_p50": round(sz / (p50 * 1e-3) / 1e9, 2), "frac_p50": round(sz / (p50 * 1e-3) / 1e9 / ce_peak, 4)})
+                      "gbps_p50": round(sz / (p50 * 1e-3) / 1e9, 2)})
+    link_peak = max(best_seen)
+    out["h2g"].update({"peak": round(k * link_peak, 3), "frac": round(h2g_gbps / (k * link_peak), 4),
+                       "peak_source": "the best pinned H2D rate the link delivered in this run (best-of-3 raw "
+                                      f"cudaMemcpyAsync 1 GiB: {ce_peak:.2f} GB/s, or a faster fetch) x {k}"})
+    for pt in sweep:
+        pt["frac_p50"] = round(pt["gbps_p50"] / link_peak, 4)
     out["h2g_sweep"] = {"workload": "config2 at k=1: pinned host -> GPU via FaaSTube.fetch (managed stage), "
-                                    "device-event time per fetch", "peak_gbps": round(ce_peak, 3), "points": sweep}
+                                    "device-event time per fetch", "peak_gbps": round(link_peak, 3),
+                        "raw_ce_best_of_3_gbps": round(ce_peak, 3), "points": sweep}
     # config 2's striping machinery on one GPU: the same 1 GiB split over a direct route and a
     # staged route (CE into the staging chunk ring + forward kernel, here staging GPU == target,
     # so both routes share one PCIe link): the ring/forward pipeline must not cost link rate
@@ -1141,10 +1151,12 @@ def _single_gpu_extras(tube, g, dev, torch):
     for o in (0, half - 8192, half, n - 8192):
         assert torch.equal(dst[o:o + 8192].cpu(), host[o:o + 8192]), "striped delivery differs"
     st_gbps = n / (statistics.mean(st_ms) * 1e-3) / 1e9
+    link_peak = max(link_peak, n / (min(st_ms) * 1e-3) / 1e9)
     out["h2g_striped_machinery"] = {
         "workload": "config2 machinery at k=2 on one GPU: 1 GiB = direct route + staged route (CE -> 4-slot "
                     "chunk ring -> forward kernel), both on the one PCIe link",
-        "value": round(st_gbps, 3), "unit": "GB/s", "peak": round(ce_peak, 3), "frac": round(st_gbps / ce_peak, 4)}
+        "value": round(st_gbps, 3), "unit": "GB/s", "peak": round(link_peak, 3),
+        "frac": round(st_gbps / link_peak, 4)}
     # the NVLink mover (K1, vector engine) on local HBM: it must feed far more than a
     # 900 GB/s/direction link, so cross-GPU passes are link-bound by construction
     vec = []
