@@ -827,7 +827,7 @@ def run_daemon(tube, g):
     from paper_2411_01830_b200.daemon import TubeDaemon
     path = os.path.join(tempfile.mkdtemp(), "faastube.sock")
     d = TubeDaemon(tube, path)
-    st = (C.c_uint64 * 9)()
+    st = (C.c_uint64 * 10)()
     try:
         ctx = mp.get_context("spawn")
         q = ctx.Queue()
@@ -836,7 +836,7 @@ def run_daemon(tube, g):
         status, res = q.get(timeout=180)
         p.join(timeout=30)
         if d._lane is not None:  # noqa: SLF001
-            dev.LIB.ft_lane_stats(d._lane, st, 9)  # noqa: SLF001
+            dev.LIB.ft_lane_stats(d._lane, st, 10)  # noqa: SLF001
     finally:
         d.close()
     if status != "ok":
@@ -847,7 +847,7 @@ def run_daemon(tube, g):
                         "zero-copy DLPack view + its release; host wall time per call in the function process",
             "sizes": res,
             "lane_stats": dict(zip(("commits", "fetches", "dones", "unique_ids", "handed_to_python", "stock_hits",
-                                    "stock_misses", "adopted", "recycled"), list(st)))}
+                                    "stock_misses", "adopted", "recycled", "lost"), list(st)))}
 
 
 def _ev(torch):

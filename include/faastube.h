@@ -420,7 +420,8 @@ int ft_lane_conn_id(ft_lane_conn* c, uint64_t* id);
 int ft_lane_events(ft_lane* lane, void* buf, uint64_t cap, uint64_t* n, int64_t timeout_us);
 int ft_lane_take(ft_lane* lane, int64_t data_id, ft_lane_obj* out, int64_t* shape, char* producer, int producer_cap);
 int ft_lane_ids(ft_lane* lane, int gpu, int64_t* ids, int cap, int* n);
-/* commits, fetches, dones, unique ids, handed to Python, stock hits, stock misses, adopted, recycled */
+/* commits, fetches, dones, unique ids, handed to Python, stock hits, stock misses, adopted, recycled,
+ * lost (committed by a client that died before its copy ran: dropped) */
 int ft_lane_stats(ft_lane* lane, uint64_t* out, int cap);
 
 /* The function-process side of the lane (csrc/client.cc): one call per hot request

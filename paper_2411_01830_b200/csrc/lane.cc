@@ -128,6 +128,9 @@ struct LObj {
   bool adopted = false;  // the tube took it while views were alive (their releases go to it)
   cudaEvent_t ready = nullptr;
   double stored_at = 0.0;
+  uint64_t conn = 0;        // the committing connection, and the client's mark the commit waited for
+  uint32_t commit_seq = 0;  //   (a client that dies before that mark executes never wrote the bytes)
+  bool has_seq = false;
 };
 
 struct Token {
@@ -195,7 +198,7 @@ struct ft_lane {
   std::mutex emu;
   std::condition_variable ecv;
   std::string events;
-  uint64_t stats[9] = {};  // commits, fetches, dones, uids, forwarded, stock hits, stock misses, adopted, recycled
+  uint64_t stats[10] = {};  // commits, fetches, dones, uids, forwarded, stock hits / misses, adopted, recycled, lost
 
   double now_ms() const { return ((double)now_us() * 1e-6 - t0) * 1e3; }
   cudaEvent_t get_event(int gpu) {
@@ -251,25 +254,38 @@ void wait_peer(ft_lane_conn* c, int ev) {
   if (!c->any_c || (int32_t)(v - c->seen_c) > 0) c->seen_c = v;
   c->any_c = true;
 }
-// a client that went away may never write the marks our stream waits for: write the
-// highest one from the host (a separate stream: the connection stream is parked)
-void release_waits(ft_lane_conn* c) {
+// (lane->mu held) a client that went away may never write the marks our stream waits
+// for. The last mark it did write is read back: objects it committed after that mark
+// were never written, so they are dropped (a later fetch misses, nobody reads garbage).
+// Then the highest mark is written from the host (a separate stream: the connection
+// stream is parked on it), releasing the waits.
+void retire_obj(ft_lane* L, LObj& o);
+void free_obj(ft_lane* L, ft_lane_conn* c, LObj& o);
+void release_dead(ft_lane* L, ft_lane_conn* c) {
   if (!c->c2d || !c->any_c) return;
-  static thread_local uint32_t v;
-  v = c->seen_c;
   cudaStream_t s = nullptr;
   if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) return;
+  uint32_t written = 0, v = c->seen_c;
+  cudaMemcpyAsync(&written, c->c2d, 4, cudaMemcpyDeviceToHost, s);
+  cudaStreamSynchronize(s);
+  std::vector<int64_t> lost;
+  for (auto& kv : L->objs) {
+    const LObj& o = kv.second;
+    if (o.conn == c->id && o.has_seq && !o.retired && !o.adopted && (int32_t)(o.commit_seq - written) > 0)
+      lost.push_back(kv.first);
+  }
   cudaMemcpyAsync(c->c2d, &v, 4, cudaMemcpyHostToDevice, s);
   cudaStreamSynchronize(s);
   cudaStreamDestroy(s);
+  for (int64_t did : lost) {
+    auto it = L->objs.find(did);
+    if (it == L->objs.end()) continue;
+    ++L->stats[9];
+    retire_obj(L, it->second);
+    if (it->second.pins <= 0) free_obj(L, c, it->second);
+  }
 }
 
-struct Reply {
-  std::string& b;
-  explicit Reply(std::string& buf) : b(buf) { b.clear(); }
-  template <class T>
-  void put(const T& v) { b.append(reinterpret_cast<const char*>(&v), sizeof v); }
-};
 
 // header + payload + drops; fd sent after the message when `fd >= 0`
 int send_reply(ft_lane_conn* c, const std::string& payload, bool ok, int fd) {
@@ -490,6 +506,9 @@ bool handle_commit(ft_lane_conn* c, const std::string& m) {
   o.consumers = o.remaining = q.consumers > 0 ? q.consumers : 1;
   o.ready = L->get_event(c->gpu);
   o.stored_at = now;
+  o.conn = c->id;
+  o.has_seq = q.ev != 0 && q.ev != -1;
+  o.commit_seq = (uint32_t)q.ev;
   cudaEventRecord(o.ready, c->stream);
   EvRec r{};
   r.kind = EV_COMMITTED;
@@ -671,7 +690,7 @@ void run_worker(ft_lane_conn* c) {
     std::lock_guard<std::mutex> lk(c->lane->mu);
     std::vector<uint64_t> toks(c->tokens.begin(), c->tokens.end());
     if (c->gpu >= 0) cudaSetDevice(c->gpu);
-    release_waits(c);
+    release_dead(c->lane, c);
     for (uint64_t t : toks) release_token(c->lane, c, t);
     return_stock(c->lane, c);
     c->gone = true;
@@ -978,7 +997,7 @@ int ft_lane_ids(ft_lane* L, int gpu, int64_t* out, int cap, int* n) {
 int ft_lane_stats(ft_lane* L, uint64_t* out, int cap) {
   if (!L) return FT_E_VALUE;
   std::lock_guard<std::mutex> lk(L->mu);
-  for (int i = 0; i < cap && i < 9; ++i) out[i] = L->stats[i];
+  for (int i = 0; i < cap && i < 10; ++i) out[i] = L->stats[i];
   return FT_OK;
 }
 
