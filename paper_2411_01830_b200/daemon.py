@@ -50,6 +50,7 @@ size class, so a steady stream of requests maps and exports nothing new.
 from __future__ import annotations
 
 import contextlib
+import functools
 import ctypes as C
 import itertools
 import math
@@ -632,6 +633,13 @@ _PyCapsule_New.restype = C.py_object
 _PyCapsule_New.argtypes = [C.c_void_p, C.c_char_p, C.c_void_p]
 
 
+@functools.lru_cache(maxsize=4096)
+def _class_of(n: int) -> int:
+    """The pool's size class of an n-byte output (datastore.py:24-29)."""
+    from .datastore import size_class
+    return size_class(max(1, n))
+
+
 def _capsule(dlmanaged: int):
     """A "dltensor" capsule over a DLManagedTensor the native client made (torch's
     from_dlpack consumes it and calls its deleter when the storage is freed)."""
@@ -706,7 +714,7 @@ class TubeClient:
         self.ch = Channel.connect(path)
         self.device = device
         self._imports = {}           # daemon block id -> ImportedBlock (until the daemon drops it)
-        self._loans = {}             # nbytes -> a lent block for the producer's next output
+        self._loans = {}             # size class -> a lent block for the producer's next output of that class
         self._io = threading.RLock()  # one frame at a time on the socket (releases come from finalizers)
         self._sent_py = 0            # messages sent from Python (the native client counts its own)
         self._cl = None              # ft_client: the lane's hot requests in one native call each
@@ -883,7 +891,8 @@ class TubeClient:
             return
         t = output.contiguous()
         n = t.nbytes
-        rep = self._loans.pop(n, None)
+        cls = _class_of(n)                            # a lent block holds any output of its size class
+        rep = self._loans.pop(cls, None)
         if rep is None:
             rep = self._call({"op": "alloc", "gpu": self.device, "nbytes": n})
             imp = self._mapped(rep)
@@ -911,7 +920,7 @@ class TubeClient:
                 rep["_fd"] = fd
             if rep.get("loan"):
                 self._mapped(rep)
-                self._loans[n] = rep
+                self._loans[cls] = rep
             return
         if not self._events:
             cur = self._stream
@@ -939,7 +948,7 @@ class TubeClient:
                                   **({"next": n} if self._events else {})})
         if rep.get("loan"):
             self._mapped(rep)
-            self._loans[n] = rep
+            self._loans[cls] = rep
 
     def fetch(self, data_id: int, out: torch.Tensor | None = None, host: bool = False, consumer: str = "func",
               slo_ms: float | None = None, infer_ms: float | None = None) -> torch.Tensor:

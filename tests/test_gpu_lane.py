@@ -32,36 +32,32 @@ def lane_stats(d):
                      "adopted", "recycled", "lost"), list(st)))
 
 
-def _producer(path, q_ids, count, seed0):
+def _producer(path, q, count, seed0):
     sys.path.insert(0, ROOT)
     from paper_2411_01830_b200.daemon import TubeClient
     try:
         c = TubeClient(path, 0)
+        ids = []
         for i in range(count):
-            n = (i * 7919 + seed0) % (3 << 20) + 1
+            # a function's outputs vary within one size class (ragged, odd byte counts)
+            n = 3 * 10**6 + (i * 7919 + seed0) % 900_000 + 1
             did = c.unique_id()
             c.store(did, payload(n, seed0 + i).cuda(), producer=f"p{seed0}")
-            q_ids.put((did, n, seed0 + i))
-        q_ids.put(None)
+            ids.append((did, n, seed0 + i))
         c.close()
+        q.put(("ok", ids))
     except Exception:  # noqa: BLE001
         import traceback
-        q_ids.put(("err", traceback.format_exc()))
+        q.put(("err", traceback.format_exc()))
 
 
-def _consumer(path, q_ids, q_res):
+def _consumer(path, ids, q_res):
     sys.path.insert(0, ROOT)
     from paper_2411_01830_b200.daemon import TubeClient
     try:
         c = TubeClient(path, 0)
         bad, k = [], 0
-        while True:
-            item = q_ids.get(timeout=300)
-            if item is None:
-                break
-            if item[0] == "err":
-                raise RuntimeError(item[1])
-            did, n, seed = item
+        for did, n, seed in ids:
             if k % 2:
                 got = c.fetch(did)                                  # zero-copy view
             else:
@@ -88,16 +84,21 @@ def test_lane_concurrent_function_pairs():
     d = TubeDaemon(tube, path)
     in_use0 = tube.pools[0].policy.in_use_bytes
     ctx = mp.get_context("spawn")
-    q_res = ctx.Queue()
-    procs = []
-    for pair in range(2):
-        q_ids = ctx.Queue()
-        procs.append(ctx.Process(target=_producer, args=(path, q_ids, 40, 1000 * (pair + 1))))
-        procs.append(ctx.Process(target=_consumer, args=(path, q_ids, q_res)))
-    for p in procs:
+    q = ctx.Queue()
+    # the two producers run at once, then the two consumers
+    prods = [ctx.Process(target=_producer, args=(path, q, 40, 1000 * (pair + 1))) for pair in range(2)]
+    for p in prods:
         p.start()
-    results = [q_res.get(timeout=600) for _ in range(2)]
-    for p in procs:
+    made = [q.get(timeout=600) for _ in prods]
+    for p in prods:
+        p.join(timeout=60)
+    for status, ids in made:
+        assert status == "ok", ids
+    cons = [ctx.Process(target=_consumer, args=(path, ids, q)) for _, ids in made]
+    for p in cons:
+        p.start()
+    results = [q.get(timeout=600) for _ in cons]
+    for p in cons:
         p.join(timeout=60)
     for status, res in results:
         assert status == "ok", res
@@ -268,7 +269,7 @@ def test_lane_objects_migrate_under_the_store_cap():
     kind, ids = q.get(timeout=300)
     assert kind == "ids", ids
     deadline = time.time() + 20
-    while tube.stats["migrated_bytes"] == 0 and time.time() < deadline:
+    while tube._stored_on(0) > tube.capacity_limit and time.time() < deadline:
         time.sleep(0.05)                                  # (the lane service applies the cap)
     assert tube.stats["migrated_bytes"] > 0
     assert tube._stored_on(0) <= tube.capacity_limit
