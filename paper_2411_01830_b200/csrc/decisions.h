@@ -230,6 +230,7 @@ struct Arbiter {
   ODict<StageSt> stages;
   int risk_flags = 0;
   std::string last_json;  // decisions of the last call
+  bool quiet = false;     // no decision record (the live pacer when it does not log)
   void start(double now, const std::string& key, double total, double slo, double infer, double arrival,
              double per_branch_cap, int n_branches);
   void boundary(double now, const std::string& key);

@@ -936,6 +936,7 @@ int ft_pacer_create(double bw_all_gbps, int links, int batch_chunks, int64_t chu
     p->fixed_stage_chunk = true;
   }
   p->logging = logging != 0;
+  for (auto& a : p->arbs) a.quiet = !p->logging;  // the decision JSON is only read by the log
   p->links = std::max(1, links);
   p->link_gbps[0] = p->link_gbps[1] = bw_all_gbps / p->links;
   p->adapt = !(flags & 2);

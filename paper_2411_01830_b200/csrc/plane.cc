@@ -356,15 +356,18 @@ double Arbiter::StageSt::next_boundary(double after, double bb) const {  // engi
   return anchor + (double)k * dur;
 }
 void Arbiter::begin() {
+  if (quiet) return;
   out_ = JsonOut{};
   out_.raw("[");
   first_ = true;
 }
 void Arbiter::end() {
+  if (quiet) return;
   out_.raw("]");
   last_json = out_.s;
 }
 void Arbiter::emit(const std::string& item) {
+  if (quiet) return;
   if (!first_) out_.raw(",");
   first_ = false;
   out_.s += item;
@@ -418,7 +421,7 @@ void Arbiter::boundary(double now, const std::string& key) {  // engine.py:637-6
 }
 void Arbiter::resync(double now) {  // engine.py:581-612
   ODict<double> targets = partition(share, now);
-  {
+  if (!quiet) {
     JsonOut o;
     o.raw("[\"partition\",{");
     for (size_t i = 0; i < targets.items.size(); ++i) {
@@ -470,13 +473,15 @@ void Arbiter::resync(double now) {  // engine.py:581-612
       }
     } else if (std::fabs(want - m.rate) > 1e-6) {
       m.pending = want;
-      JsonOut o;
-      o.raw("[\"pending\",");
-      o.str(m.key);
-      o.raw(",");
-      o.num(want);
-      o.raw("]");
-      emit(o.s);
+      if (!quiet) {
+        JsonOut o;
+        o.raw("[\"pending\",");
+        o.str(m.key);
+        o.raw(",");
+        o.num(want);
+        o.raw("]");
+        emit(o.s);
+      }
       arm(now, m, m.next_boundary(now, batch_bytes));
     }
   }
@@ -486,6 +491,7 @@ void Arbiter::set_rate(double now, StageSt& m, double rate) {  // engine.py:614-
   m.started = true;
   m.pending = none();
   m.anchor = now;
+  if (quiet) return;
   JsonOut o;
   o.raw("[\"set_rate\",");
   o.str(m.key);
@@ -500,6 +506,7 @@ void Arbiter::arm(double now, StageSt& m, double t) {  // engine.py:628-635
   if (is_none(t) || t <= now + 1e-9) return;
   if (!is_none(m.armed) && m.armed <= t + 1e-9) return;
   m.armed = t;
+  if (quiet) return;
   JsonOut o;
   o.raw("[\"arm\",");
   o.str(m.key);
