@@ -628,6 +628,7 @@ class TubeDaemon:
 
 
 _SPIN = int(os.environ.get("FT_CHAN_SPIN_US", 2000))
+_KEPT_IMPORTS = []   # mappings of closed clients whose zero-copy views were still alive (kept until exit)
 _PyCapsule_New = C.pythonapi.PyCapsule_New
 _PyCapsule_New.restype = C.py_object
 _PyCapsule_New.argtypes = [C.c_void_p, C.c_char_p, C.c_void_p]
@@ -1082,6 +1083,8 @@ class TubeClient:
             torch.cuda.synchronize(self.device)
             for imp in self._imports.values():
                 imp.close()
+        else:
+            _KEPT_IMPORTS.extend(self._imports.values())   # dropping them would unmap under the views
         self._imports.clear()
         self._loans.clear()
         if not self._events:
