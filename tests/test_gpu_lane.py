@@ -280,3 +280,52 @@ def test_lane_objects_migrate_under_the_store_cap():
     assert tube._accounts_consistent()
     d.close()
     tube.close()
+
+
+def _response_and_release(path, q):
+    sys.path.insert(0, ROOT)
+    from paper_2411_01830_b200.daemon import DaemonError, TubeClient
+    try:
+        c = TubeClient(path, 0)
+        x = payload(2 * 10**6 + 9, 21).cuda()
+        did = c.unique_id()
+        c.store(did, x, response=True)                # the slow path (Python) inside a lane connection
+        y = c.fetch(did, out=torch.empty_like(x))
+        ok_resp = torch.equal(y, x)
+        did2 = c.unique_id()
+        c.store(did2, x, consumers=3)
+        c.release(did2)                               # dropped regardless of consumers
+        try:
+            c.fetch(did2)
+            released = False
+        except DaemonError as e:
+            released = "MissingData" in str(e)
+        c.close()
+        q.put(("ok", (ok_resp, released, did)))
+    except Exception:  # noqa: BLE001
+        import traceback
+        q.put(("err", traceback.format_exc()))
+
+
+def test_lane_connection_slow_paths():
+    """Requests the lane hands to Python on a lane connection — a store with a
+    response leg (engine.py:414-423), release — keep their semantics: the response
+    lands in host memory, bit-exact; a released object misses."""
+    from paper_2411_01830_b200.daemon import TubeDaemon
+    from paper_2411_01830_b200.tube import FaaSTube
+    tube = FaaSTube(pcie_gbps=50.0, gpus=[0])
+    path = os.path.join(tempfile.mkdtemp(), "faastube.sock")
+    d = TubeDaemon(tube, path)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_response_and_release, args=(path, q))
+    p.start()
+    status, res = q.get(timeout=300)
+    p.join(timeout=60)
+    assert status == "ok", res
+    ok_resp, released, did = res
+    assert ok_resp and released
+    assert torch.equal(tube.response(did).view(torch.uint8).reshape(-1), payload(2 * 10**6 + 9, 21))
+    assert tube._accounts_consistent()
+    d.close()
+    tube.close()
