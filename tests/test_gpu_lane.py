@@ -289,7 +289,7 @@ def _response_and_release(path, q):
         c = TubeClient(path, 0)
         x = payload(2 * 10**6 + 9, 21).cuda()
         did = c.unique_id()
-        c.store(did, x, response=True)                # the slow path (Python) inside a lane connection
+        c.store(did, x, response=True, consumers=2)   # the slow path (Python) inside a lane connection
         y = c.fetch(did, out=torch.empty_like(x))
         ok_resp = torch.equal(y, x)
         did2 = c.unique_id()
