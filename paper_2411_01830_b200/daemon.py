@@ -4,7 +4,8 @@ interface: function processes call ``TubeClient.store`` /
 (index, pools, pacer). GPU payloads never cross the socket: pool blocks are
 exported as POSIX fds (``cuMemExportToShareableHandle``, SCM_RIGHTS over
 AF_UNIX, ``channel.py``) and mapped by the function process; host payloads
-travel as a sealed memfd. The socket carries only small JSON messages.
+travel as a sealed memfd. The socket carries small messages (msgpack) and the
+descriptors; with the native lane (below) messages move to shared memory.
 
 Protocol (msgpack frames): every request gets one reply message; a reply
 with ``"fd": true`` is followed by one descriptor (SCM_RIGHTS). Replies also
@@ -45,6 +46,29 @@ instead (the daemon syncs its stream before replying).
 A block's fd is exported and sent once per connection
 (``cuMemExportToShareableHandle`` costs ~1 ms): pool blocks are reused by
 size class, so a steady stream of requests maps and exports nothing new.
+
+The native lane (the default, csrc/lane.cc + client.cc). A client that sends
+``{"op": "chan"}`` + a memfd moves its messages to shared-memory rings
+(chan.cc); the daemon attaches a C++ worker to them. With ``hello`` +
+``"memops"`` the daemon hands back a 256-byte slot of a pool block (two sync
+words: the client's marks, the daemon's) instead of IPC event rings — a mark
+is a stream write of the sender's next sequence number, a wait is the
+receiver's stream waiting for it (``"ev"`` is that number; 0 / -1 = none).
+The hot requests are then binary (little-endian, packed):
+
+  unique_id  u8 op=4                                         -> i64 id
+  commit     u8 op=1, dtype, ndim, response; i32 ev, consumers; u32 name_len;
+             u64 token; i64 id; u64 next; i64 shape[ndim]; name
+                                                             -> BlockRep (loan=1: the next block)
+  fetch      u8 op=2; i32 gpu; i64 id; f64 slo_ms, infer_ms  -> BlockRep + i64 shape[ndim]
+  done       u8 op=3; i32 ev; u64 token                      -> no reply
+
+A binary reply is RepHdr (u8 0xB1, ok, has_fd; u32 acked, n_drop) + payload +
+u64 drop[n_drop]; BlockRep = u64 token, arena, off, arena_bytes, nbytes; i32
+ev; u8 dtype, ndim, loan. An error reply (ok=0) carries the exception's name
+and message. The worker answers these itself and hands everything else
+(msgpack, misses, responses, objects on another GPU) to the connection's
+Python thread, which replies in the request's own format.
 """
 
 from __future__ import annotations
