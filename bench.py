@@ -925,11 +925,12 @@ def _cross_gpu(torch, dev, ndev):
         p50 = nearest_rank(ts, 50)
         sweep.append({"bytes": n, "ms_p50": round(p50, 5), "ms_p99": round(nearest_rank(ts, 99), 5),
                       "gbps_p50": round(n / (p50 * 1e-3) / 1e9, 2),
-                      "frac_nvlink": round(n / (p50 * 1e-3) / 1e9 / NVLINK_GBPS, 4),
+                      # (a dry run on one GPU moves nothing over NVLink: no fraction of it)
+                      "frac_nvlink": None if dry else round(n / (p50 * 1e-3) / 1e9 / NVLINK_GBPS, 4),
                       "api_us_p50": round(nearest_rank(api, 50), 1), "bit_exact": ok})
     out["config3_pair_sweep"] = {"workload": f"config3: FaaSTube.store on GPU {pairs01[0]} -> fetch(device="
                                              f"{pairs01[1]}, out=), 4 KiB..1 GiB, random uint8 seed 2",
-                                 "dry_run": dry, "peak_gbps": NVLINK_GBPS, "points": sweep}
+                                 "dry_run": dry, "peak_gbps": None if dry else NVLINK_GBPS, "points": sweep}
     # every ordered pair, one at a time (64 MiB)
     rows = []
     for i in gpus:
@@ -983,8 +984,8 @@ def _cross_gpu(torch, dev, ndev):
     else:
         plan = [(i, i + 1) for i in range(0, ndev - 1, 2)]
     c = concurrent(plan, 256 << 20)
-    c["frac"] = round(c["aggregate_gbps"] / (NVLINK_GBPS * len(plan)), 4)
-    out["config3_disjoint_pairs"] = dict(c, dry_run=dry, peak_gbps=NVLINK_GBPS * len(plan))
+    c["frac"] = None if dry else round(c["aggregate_gbps"] / (NVLINK_GBPS * len(plan)), 4)
+    out["config3_disjoint_pairs"] = dict(c, dry_run=dry, peak_gbps=None if dry else NVLINK_GBPS * len(plan))
     if not dry:
         c = concurrent([(i, 0) for i in range(1, ndev)], 256 << 20)
         c["frac"] = round(c["aggregate_gbps"] / NVLINK_GBPS, 4)
