@@ -291,8 +291,11 @@ void release_dead(ft_lane* L, ft_lane_conn* c) {
 int send_reply(ft_lane_conn* c, const std::string& payload, bool ok, int fd) {
   std::vector<uint64_t> drops;
   {
+    // at most 256 notices per reply (the rest ride on the next ones): a reply fits a slot
     std::lock_guard<std::mutex> lk(c->lane->mu);
-    drops.swap(c->drops);
+    const size_t k = std::min<size_t>(c->drops.size(), 256);
+    drops.assign(c->drops.begin(), c->drops.begin() + k);
+    c->drops.erase(c->drops.begin(), c->drops.begin() + k);
   }
   c->served += 1;
   RepHdr h{REP_KIND, (uint8_t)ok, (uint8_t)(fd >= 0), 0, c->served, (uint32_t)drops.size(), 0};
