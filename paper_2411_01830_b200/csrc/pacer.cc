@@ -160,6 +160,7 @@ struct Stage {
   std::deque<Batch> inflight;  // issued, not yet landed batches
   int jobs = 0;         // pageable chunks queued to workers, not yet issued
   bool was_full = false;  // trace: inflight cap reached (the link, not the rate, limits)
+  bool inline_route = false;  // one direct route on the consumer's own stream (submit_impl)
   bool issued = false;  // every byte handed out
   bool sealed = false;  // every byte enqueued: join events recorded (or failed)
   std::vector<std::pair<cudaEvent_t, int>> join;     // last op of each route (the submitter's)
@@ -504,7 +505,9 @@ struct ft_pacer {
         return;
       }
       issue(r, st.dst + o, st.host + o, n, st.dir);
-      if (track) {
+      // (an inline stage's only batch: the landing event seal() records follows it on
+      // the same stream, nothing polls a batch event for it)
+      if (track && !(st.inline_route && rel + n == r.len)) {
         DevGuard g(r.dev);
         cudaEvent_t e = get_event(r.dev);
         ck(cudaEventRecord(e, r.last(st.dir)), "record batch");
@@ -539,10 +542,13 @@ struct ft_pacer {
     if (st.sealed) return;
     for (auto& r : st.routes) {
       DevGuard g(r.dev);
-      cudaEvent_t a = get_event(r.dev), b = get_event(r.dev);
-      ck(cudaEventRecord(a, r.last(st.dir)), "record join");
+      cudaEvent_t b = get_event(r.dev);
+      if (!st.inline_route) {  // (an inline route ran on the consumer's stream: nothing to join)
+        cudaEvent_t a = get_event(r.dev);
+        ck(cudaEventRecord(a, r.last(st.dir)), "record join");
+        st.join.emplace_back(a, r.dev);
+      }
       ck(cudaEventRecord(b, r.last(st.dir)), "record landing");
-      st.join.emplace_back(a, r.dev);
       st.landing.emplace_back(b, r.dev);
     }
     st.sealed = true;
@@ -1066,6 +1072,7 @@ static int submit_impl(ft_pacer* p, int dir, const char* key, int managed, doubl
                             st.routes[0].dev == dst_dev && bytes > 0 &&
                             bytes <= (uint64_t)p->batch_chunks * p->chunk;
   if (inline_route) st.routes[0].ce = cs;
+  st.inline_route = inline_route;
   std::unique_lock<std::mutex> lk(p->mu);
   // a stage that already landed but that the pacer thread has not polled yet (it
   // looks every 20 us) must leave the arbiter before this one starts: otherwise the
@@ -1135,8 +1142,7 @@ static int submit_impl(ft_pacer* p, int dir, const char* key, int managed, doubl
   if (rc == FT_OK) {
     try {
       DevGuard g(dst_dev);
-      if (!inline_route)  // (an inline route's join is on the consumer stream itself)
-        for (auto& e : st.join) ck(cudaStreamWaitEvent(cs, e.first, 0), "consumer waits route");
+      for (auto& e : st.join) ck(cudaStreamWaitEvent(cs, e.first, 0), "consumer waits route");
     } catch (const CudaFail& f) {
       rc = FT_E_CUDA;
       msg = f.msg;
