@@ -811,6 +811,33 @@ def _daemon_client(path, g, q):
                            "fetch_out_us_p50": round(1e6 * statistics.median(ft), 1),
                            "fetch_view_us_p50": round(1e6 * statistics.median(vt), 1),
                            "view_release_us_p50": round(1e6 * statistics.median(rt), 1)}
+        # config 1 between function processes: a 64 MiB output stored (copied into the
+        # lent block) and fetched as a zero-copy view, the pass timed on the device in
+        # this process (its stream carries the copy and the waits for the daemon's marks)
+        n = 64 << 20
+        x = torch.randn(n // 2, device=f"cuda:{g}").half().view(torch.uint8)
+        s = torch.cuda.current_stream(g)
+        passes = []
+        for i in range(30):
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(s)
+            did = c.unique_id()
+            c.store(did, x)
+            v = c.fetch(did)
+            b.record(s)
+            b.synchronize()
+            ok = bool(torch.equal(v, x)) if i in (0, 29) else True
+            del v
+            assert ok
+            if i >= 5:
+                passes.append(a.elapsed_time(b))
+        passes.sort()
+        res["config1_pass_64MiB"] = {"ms_p50": round(nearest_rank(passes, 50), 4),
+                                     "ms_p99": round(nearest_rank(passes, 99), 4),
+                                     "gbps_p50": round(n / (nearest_rank(passes, 50) * 1e-3) / 1e9, 1),
+                                     "desc": "unique_id + store (copy into the lent block) + zero-copy fetch, "
+                                             "device time in the function process (includes its host calls)"}
         c.close()
         q.put(("ok", res))
     except Exception as exc:  # noqa: BLE001
