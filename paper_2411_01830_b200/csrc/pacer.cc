@@ -1063,14 +1063,14 @@ static int submit_impl(ft_pacer* p, int dir, const char* key, int managed, doubl
     st.routes.push_back(r);
   }
   cudaStream_t cs = (cudaStream_t)consumer_stream;
-  // A stage of one direct pinned route no larger than one batch is issued at once
-  // whatever its rate (its first batch goes out on submission), so its DMA goes on the
-  // consumer's own stream: no cross-stream event hops (consumer -> CE stream ->
-  // consumer) around a copy that is a few microseconds long. Measured at 1 MiB: the
-  // hops cost ~10 us of device time over a raw copy (tools/prof_h2g.py).
+  // A stage of one direct pinned route issues its DMAs on the consumer's own stream:
+  // no cross-stream event hops (consumer -> CE stream -> consumer) around them —
+  // measured at 1 MiB the hops cost ~10 us of device time over a raw copy
+  // (tools/prof_h2g.py). The stage's batches still go out at its rate (the pacer
+  // thread issues them onto that stream while submit() waits for the last one), and
+  // tenants stay apart: each one's DMAs queue on its own stream.
   const bool inline_route = dir == 0 && st.pinned && k == 1 && !st.routes[0].staged() &&
-                            st.routes[0].dev == dst_dev && bytes > 0 &&
-                            bytes <= (uint64_t)p->batch_chunks * p->chunk;
+                            st.routes[0].dev == dst_dev && bytes > 0;
   if (inline_route) st.routes[0].ce = cs;
   st.inline_route = inline_route;
   std::unique_lock<std::mutex> lk(p->mu);
