@@ -585,28 +585,30 @@ class DevicePool:
             rw, last = self._rw.value, self._last.value
         return rw, (None if last != last else last)
 
-    def retire_many(self, index, items):
-        """Batched retire: [(data_id, block, producer, fences)] -> [(R_window, last | None)]."""
-        n = len(items)
+    def retire_many(self, index, ids, pblocks, producers, fences):
+        """Batched retire (``fetch_many``): parallel lists of data ids, policy blocks,
+        producers and each block's fences -> (R_window, last_request) float arrays
+        (NaN: no last request), one native call for the index drops, policy frees
+        and windows (``ft_retire_many``)."""
+        n = len(ids)
         enc = self._names
-        ids = array.array("q", [d for d, _, _, _ in items])
-        bids = array.array("q", [b.policy_block.block_id for _, b, _, _ in items])
-        names = (C.c_char_p * n)(*[enc.get(f) or self._enc(f) for _, _, f, _ in items])
+        ids_a = array.array("q", ids)
+        bids = array.array("q", [pb.block_id for pb in pblocks])
+        names = (C.c_char_p * n)(*[enc.get(f) or self._enc(f) for f in producers])
         rws, lasts = array.array("d", bytes(8 * n)), array.array("d", bytes(8 * n))
         with self._lock:
-            LIB.ft_retire_many(index._h, self.policy._h, n, C.c_void_p(ids.buffer_info()[0]),
+            LIB.ft_retire_many(index._h, self.policy._h, n, C.c_void_p(ids_a.buffer_info()[0]),
                                C.c_void_p(bids.buffer_info()[0]), names, C.c_void_p(rws.buffer_info()[0]),
                                C.c_void_p(lasts.buffer_info()[0]))
-            fences = self._fences
-            for _, b, _, f in items:
-                pb = b.policy_block
+            fd = self._fences
+            for pb, f in zip(pblocks, fences):
                 pb.in_use = False
-                fences[pb.block_id] = f
+                fd[pb.block_id] = f
             if self.policy.mode == "none":
-                for _, b, _, _ in items:
-                    self.policy._blocks.pop(b.policy_block.block_id, None)
-                    self._unmap(b.policy_block.block_id)
-        return [(rws[i], None if lasts[i] != lasts[i] else lasts[i]) for i in range(n)]
+                for pb in pblocks:
+                    self.policy._blocks.pop(pb.block_id, None)
+                    self._unmap(pb.block_id)
+        return rws, lasts
 
     def commit_retire(self, index, data_id: int, blk: "PoolBlock", fences, producer: str):
         """Index drop + block back to the policy (fenced) + the producer's window

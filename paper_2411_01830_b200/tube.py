@@ -811,41 +811,45 @@ class FaaSTube:
                 dev.wait_events(s, readies.values())
                 dev.copy_batch_flat(flat, g, s)
                 done = dev.Ev(g).record(s)     # one fence for every block the batch read
-                retiring = []
+                fence1 = (done,)
+                r_objs, r_ids, r_pbs, r_names, r_fences = [], [], [], [], []
                 nb = 0
                 for o in group:
                     nb += o.nbytes
                     o.remaining -= 1
                     if o.remaining <= 0 and o.pins == 0 and not o.retired:
-                        retiring.append(o)
+                        r_objs.append(o)
+                        r_ids.append(o.did)
+                        r_pbs.append(o.block.policy_block)
+                        r_names.append(o.producer)
+                        # the batch's stream waited on each object's `ready` before `done`
+                        r_fences.append(fence1 + tuple(o.readers) if o.readers else fence1)
                     else:
                         o.readers.append(done)      # the last consumer's retire fences on this read
                         if o.remaining <= 0:
                             self._retire(o, done)
                 self.stats["bytes_local"] += nb
                 self.stats["fetches"] += len(group)
-                if retiring:
+                if r_objs:
                     # every last consumer's retire in one native call (dataplane.py:98-101,
-                    # datastore.py:146-149), fenced on the batch's read + earlier readers (the
-                    # batch's stream waited on each object's `ready` before `done`)
-                    fence1 = (done,)
-                    res = self.pools[g].retire_many(self.index, [
-                        (o.did, o.block, o.producer, fence1 + tuple(o.readers) if o.readers else fence1)
-                        for o in retiring])
-                    due = {}
-                    meta, live, freed = self.index._meta, self._live, 0
-                    for o, rl in zip(retiring, res):
+                    # datastore.py:146-149)
+                    rws, lasts = self.pools[g].retire_many(self.index, r_ids, r_pbs, r_names, r_fences)
+                    live, freed, last_of = self._live, 0, {}
+                    for i, o in enumerate(r_objs):
                         o.retired = True
-                        o.readers = []
                         if objs.pop(o.did, None) is not None:
                             live[(o.producer, g)] -= 1
                             freed += o.nbytes
                         o.block = None
-                        meta.pop(o.did, None)
-                        due[o.producer] = rl                  # one shrink timer per producer
+                        last_of[o.producer] = i           # one shrink timer per producer
+                    meta = self.index._meta
+                    if meta:
+                        for did in r_ids:
+                            meta.pop(did, None)
                     self._stored[g] -= freed
-                    for rw, last in due.values():
-                        self._push_due(g, rw, last, self._last_op_ms)
+                    for i in last_of.values():
+                        last = lasts[i]
+                        self._push_due(g, rws[i], None if last != last else last, self._last_op_ms)
                     if self.strategy.migration != "none" and self._off_gpu[g]:
                         self._pending.add(("prefetch", g))
         for did, out in rest:
