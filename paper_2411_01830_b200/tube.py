@@ -788,24 +788,31 @@ class FaaSTube:
             self._reap()
             self._last_op_ms = self.now_ms()
             objs = self._objs
+            get = objs.get
             by_gpu = {}
+            last_g, grp = None, None
             for did, out in items:
-                obj = objs.get(did)
-                if (obj is not None and obj.block is not None and obj.gpu == out.get_device()
-                        and out.nbytes == obj.nbytes and out.is_contiguous()):
-                    g = by_gpu.get(obj.gpu)
-                    if g is None:
-                        g = by_gpu[obj.gpu] = ([], {}, [])     # objects, newest ready per stream, segments
-                    g[0].append(obj)
-                    r = obj.ready
-                    if r is not None:                          # (the newest record per stream covers the rest)
-                        k = r.stream if r.stream is not None else id(r)
-                        cur = g[1].get(k)
-                        if cur is None or r.seq > cur.seq:
-                            g[1][k] = r
-                    g[2].extend((out.data_ptr(), obj.block.ptr, obj.nbytes))
-                else:
+                obj = get(did)
+                if obj is None or obj.block is None:
                     rest.append((did, out))
+                    continue
+                og = obj.gpu
+                if og != out.get_device() or out.nbytes != obj.nbytes or not out.is_contiguous():
+                    rest.append((did, out))
+                    continue
+                if og != last_g:
+                    grp = by_gpu.get(og)
+                    if grp is None:
+                        grp = by_gpu[og] = ([], {}, [])        # objects, newest ready per stream, segments
+                    last_g = og
+                grp[0].append(obj)
+                r = obj.ready
+                if r is not None:                              # (the newest record per stream covers the rest)
+                    k = r.stream if r.stream is not None else id(r)
+                    cur = grp[1].get(k)
+                    if cur is None or r.seq > cur.seq:
+                        grp[1][k] = r
+                grp[2].extend((out.data_ptr(), obj.block.ptr, obj.nbytes))
             for g, (group, readies, flat) in by_gpu.items():
                 s = self._stream(g)
                 dev.wait_events(s, readies.values())
