@@ -90,13 +90,56 @@ def main():
     d = TubeDaemon(tube, path)
     in_use0 = tube.pools[0].policy.in_use_bytes
     ctx = mp.get_context("spawn")
-    qs = [ctx.Queue() for _ in range(nproc + 1)]
-    ps = [ctx.Process(target=worker, args=(path, w, nproc, dur, qs, qs[w])) for w in range(nproc)]
+    qs = [ctx.Queue() for _ in range(nproc + 2)]          # one per worker, results, the in-process tenant
+    ps = [ctx.Process(target=worker, args=(path, w, nproc + 1, dur, qs[:nproc + 1] + [qs[nproc + 1]], qs[w]))
+          for w in range(nproc)]
+    # the workers' results queue is qs[nproc + 1] (index nproc + 1 of their list); objects they
+    # address to "worker nproc" go to the in-process tenant below, which adopts them from the lane
     for p in ps:
         p.start()
-    res = [qs[nproc].get(timeout=dur + 300) for _ in ps]
+    import threading
+    local = {"made": 0, "fetched": 0, "bad": 0, "err": None}
+
+    def tenant():
+        rnd = random.Random(99)
+        try:
+            t_end = time.time() + dur
+            while time.time() < t_end:
+                n = rnd.choice((4096 + 5, 1 << 20, 5 * 10**6 + 3))
+                did = tube.unique_id()
+                x = payload(n, 777 + local["made"]).cuda()
+                tube.store(did, x, producer="local")
+                out = torch.empty(n, dtype=torch.uint8, device="cuda:0")
+                tube.fetch(did, out=out)
+                local["bad"] += not torch.equal(out, x)
+                local["made"] += 1
+                while not qs[nproc].empty():              # a function process's object, fetched here
+                    did, n, seed = qs[nproc].get_nowait()
+                    got = tube.fetch(did, device=0) if rnd.random() < 0.5 else \
+                        tube.fetch(did, out=torch.empty(n, dtype=torch.uint8, device="cuda:0"))
+                    local["bad"] += not torch.equal(got.cpu(), payload(n, seed))
+                    local["fetched"] += 1
+                    del got
+            t_drain = time.time() + 15
+            while time.time() < t_drain:
+                try:
+                    did, n, seed = qs[nproc].get(timeout=1.0)
+                except Exception:  # noqa: BLE001
+                    break
+                got = tube.fetch(did, out=torch.empty(n, dtype=torch.uint8, device="cuda:0"))
+                local["bad"] += not torch.equal(got.cpu(), payload(n, seed))
+                local["fetched"] += 1
+        except Exception:  # noqa: BLE001
+            import traceback
+            local["err"] = traceback.format_exc()
+
+    th = threading.Thread(target=tenant)
+    th.start()
+    res = [qs[nproc + 1].get(timeout=dur + 300) for _ in ps]
     for p in ps:
         p.join(timeout=60)
+    th.join(timeout=120)
+    res.append(("in-process tenant", local))
     st = (C.c_uint64 * 10)()
     LIB.ft_lane_stats(d._lane, st, 10)
     time.sleep(1.0)
