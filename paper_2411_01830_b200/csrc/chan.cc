@@ -10,6 +10,7 @@
 // (its AF_UNIX socket, which still carries SCM_RIGHTS descriptors).
 #include <linux/futex.h>
 #include <sys/mman.h>
+#include <sys/stat.h>
 #include <sys/syscall.h>
 #include <time.h>
 #include <unistd.h>
@@ -100,6 +101,9 @@ struct ft_chan {
   Hdr* hdr = nullptr;
   uint8_t* data[2] = {nullptr, nullptr};
   size_t bytes = 0;
+  // the geometry as this side mapped it: never re-read from the shared header,
+  // which the peer can write (a daemon must not index its mapping by a client's word)
+  uint32_t slot_bytes = 0, slots = 0;
   int fd = -1;  // the creator's memfd (closed by ft_chan_close)
 };
 
@@ -138,6 +142,8 @@ int ft_chan_create(uint32_t slot_bytes, uint32_t slots, int* memfd, ft_chan** ou
   auto* c = new ft_chan;
   c->hdr = h;
   c->bytes = bytes;
+  c->slot_bytes = slot_bytes;
+  c->slots = slots;
   c->fd = fd;
   c->data[0] = reinterpret_cast<uint8_t*>(m) + sizeof(Hdr);
   c->data[1] = c->data[0] + (size_t)slot_bytes * slots;
@@ -152,8 +158,18 @@ int ft_chan_attach(int memfd, ft_chan** out) {
     return FT_E_VALUE;
   }
   Hdr probe;
-  if (pread(memfd, &probe, sizeof probe, 0) != (ssize_t)sizeof probe || probe.magic != kMagic) {
+  struct stat sb;
+  if (pread(memfd, &probe, sizeof probe, 0) != (ssize_t)sizeof probe || probe.magic != kMagic ||
+      fstat(memfd, &sb) != 0) {
     ft::set_last_error("ft_chan_attach: not a channel");
+    return FT_E_VALUE;
+  }
+  // the creator's geometry, checked against the file it really sized (a mapping past
+  // the end of the memfd faults on first touch)
+  if (probe.slot_bytes < 64 || probe.slot_bytes % 8 || probe.slot_bytes > (1u << 24) || probe.slots < 2 ||
+      probe.slots > (1u << 16) ||
+      sizeof(Hdr) + 2 * (size_t)probe.slot_bytes * probe.slots > (size_t)sb.st_size) {
+    ft::set_last_error("ft_chan_attach: bad ring geometry");
     return FT_E_VALUE;
   }
   const size_t bytes = sizeof(Hdr) + 2 * (size_t)probe.slot_bytes * probe.slots;
@@ -165,8 +181,10 @@ int ft_chan_attach(int memfd, ft_chan** out) {
   auto* c = new ft_chan;
   c->hdr = reinterpret_cast<Hdr*>(m);
   c->bytes = bytes;
+  c->slot_bytes = probe.slot_bytes;
+  c->slots = probe.slots;
   c->data[0] = reinterpret_cast<uint8_t*>(m) + sizeof(Hdr);
-  c->data[1] = c->data[0] + (size_t)probe.slot_bytes * probe.slots;
+  c->data[1] = c->data[0] + (size_t)c->slot_bytes * c->slots;
   *out = c;
   return FT_OK;
 }
@@ -177,7 +195,8 @@ int ft_chan_send(ft_chan* c, int dir, const void* buf, uint32_t n, int64_t timeo
     return FT_E_VALUE;
   }
   Hdr* h = c->hdr;
-  if (n + 8 > h->slot_bytes) {
+  const uint32_t slots = c->slots, slot_bytes = c->slot_bytes;
+  if ((uint64_t)n + 8 > slot_bytes) {
     ft::set_last_error("ft_chan_send: message larger than a slot");
     return FT_E_VALUE;
   }
@@ -185,13 +204,13 @@ int ft_chan_send(ft_chan* c, int dir, const void* buf, uint32_t n, int64_t timeo
   const uint32_t head = r.head.v.load(std::memory_order_relaxed);
   int rc = wait_on(
       h, &r.tail.v, &r.psleep.v,
-      [&] { return head - r.tail.v.load(std::memory_order_acquire) < h->slots; },
+      [&] { return head - r.tail.v.load(std::memory_order_acquire) < slots; },
       [&] { return r.tail.v.load(std::memory_order_acquire); }, 50, timeout_us);
   if (rc != FT_OK) {
     ft::set_last_error(rc == FT_E_CLOSED ? "ft_chan_send: channel closed" : "ft_chan_send: ring full (timeout)");
     return rc;
   }
-  uint8_t* slot = c->data[dir] + (size_t)(head % h->slots) * h->slot_bytes;
+  uint8_t* slot = c->data[dir] + (size_t)(head % slots) * slot_bytes;
   std::memcpy(slot, &n, 4);
   if (n) std::memcpy(slot + 8, buf, n);
   r.head.v.store(head + 1, std::memory_order_seq_cst);
@@ -214,9 +233,13 @@ int ft_chan_recv(ft_chan* c, int dir, void* buf, uint32_t cap, uint32_t* n, int6
     ft::set_last_error(rc == FT_E_CLOSED ? "ft_chan_recv: channel closed" : "ft_chan_recv: timeout");
     return rc;
   }
-  const uint8_t* slot = c->data[dir] + (size_t)(tail % h->slots) * h->slot_bytes;
+  const uint8_t* slot = c->data[dir] + (size_t)(tail % c->slots) * c->slot_bytes;
   uint32_t len;
   std::memcpy(&len, slot, 4);
+  if ((uint64_t)len + 8 > c->slot_bytes) {  // a length the peer could not have sent
+    ft::set_last_error("ft_chan_recv: corrupt message length");
+    return FT_E_VALUE;
+  }
   *n = len;
   if (len > cap) {
     ft::set_last_error("ft_chan_recv: buffer too small");

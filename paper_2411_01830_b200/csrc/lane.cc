@@ -466,7 +466,8 @@ bool handle_commit(ft_lane_conn* c, const std::string& m) {
   memcpy(shape.data(), m.data() + sizeof q, 8 * (size_t)q.ndim);
   std::string name(m.data() + sizeof q + 8 * q.ndim, q.name_len);
   uint64_t nbytes = (uint64_t)kItem[q.dtype];
-  for (int64_t d : shape) nbytes *= (uint64_t)(d < 0 ? 0 : d);
+  for (int64_t d : shape)  // a negative or overflowing shape: Python rejects it
+    if (d < 0 || __builtin_mul_overflow(nbytes, (uint64_t)d, &nbytes)) return false;
   std::unique_lock<std::mutex> lk(L->mu);
   auto tk = L->tokens.find(q.token);
   if (tk == L->tokens.end() || tk->second.kind != 1) return false;  // a Python loan (or unknown): Python

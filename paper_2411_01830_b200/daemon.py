@@ -509,9 +509,9 @@ class TubeDaemon:
             conn.wait_peer(msg.get("ev"))      # the client's copy into the block is done (stream-ordered)
             dt, shape = _DTYPES[msg["dtype"]], msg["shape"]
             nbytes = math.prod(shape) * dt.itemsize
-            if nbytes > t.blk.nbytes:
+            if nbytes > t.blk.nbytes or any(d < 0 for d in shape):
                 self._free(t.blk, conn)
-                raise ValueError(f"commit of {nbytes} B into a {t.blk.nbytes} B block")
+                raise ValueError(f"commit of shape {shape} ({nbytes} B) into a {t.blk.nbytes} B block")
             stream = conn.stream if conn.stream is not None else 0     # 0: the legacy default stream
             try:                               # the pool block itself is published: a zero-copy store
                 tube.store_block(int(msg["id"]), t.blk, nbytes, dt, shape, stream,

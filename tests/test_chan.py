@@ -61,3 +61,39 @@ def test_full_ring_oversize_and_timeouts():
     assert buf.raw[:n.value] == b"bb"
     LIB.ft_chan_send(h, 0, b"ccc", 3, 1000)                # room again
     LIB.ft_chan_close(h)
+
+
+def test_peer_written_geometry_and_lengths_are_not_trusted():
+    """The daemon maps a ring pair its client created and the client can keep
+    writing the header: attach checks the geometry against the file's real size,
+    the mapped side indexes by the geometry it attached with, and a slot length no
+    sender could have written is an error, not an out-of-bounds copy."""
+    import mmap
+    import struct
+    from paper_2411_01830_b200._lib import LIB
+    fd, h = C.c_int(), C.c_void_p()
+    LIB.ft_chan_create(256, 4, C.byref(fd), C.byref(h))
+    m = mmap.mmap(fd.value, 640 + 2 * 256 * 4)
+    slot_bytes, slots = struct.unpack_from("<II", m, 4)
+    assert (slot_bytes, slots) == (256, 4)
+    struct.pack_into("<I", m, 8, 1 << 15)                  # more slots than the file holds
+    h2 = C.c_void_p()
+    with pytest.raises(ValueError, match="geometry"):
+        LIB.ft_chan_attach(fd.value, C.byref(h2))
+    struct.pack_into("<I", m, 8, 4)
+    LIB.ft_chan_attach(fd.value, C.byref(h2))
+    struct.pack_into("<II", m, 4, 1 << 20, 1 << 10)        # rewritten after attach: ignored
+    with pytest.raises(ValueError):                        # still 256-byte slots
+        LIB.ft_chan_send(h2, 1, b"x" * 300, 300, 1000)
+    LIB.ft_chan_send(h2, 1, b"ok", 2, 1000)
+    buf, n = C.create_string_buffer(256), C.c_uint32()
+    LIB.ft_chan_recv(h, 1, buf, 256, C.byref(n), 10, 1000)
+    assert buf.raw[:n.value] == b"ok"
+    # a forged message: ring 0's slot 0 claims 4 GiB, head bumped by hand
+    struct.pack_into("<I", m, 640, 0xFFFFFFFF)
+    struct.pack_into("<I", m, 128, 1)
+    with pytest.raises(ValueError, match="corrupt"):
+        LIB.ft_chan_recv(h2, 0, C.create_string_buffer(1 << 16), 1 << 16, C.byref(n), 10, 1000)
+    m.close()
+    LIB.ft_chan_close(h2)
+    LIB.ft_chan_close(h)
