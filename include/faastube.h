@@ -428,8 +428,10 @@ int ft_lane_stats(ft_lane* lane, uint64_t* out, int cap);
  * of Listing 1 through the daemon — rings, the copy into / out of the mapped block,
  * the sync-word ordering. Views are DLPack tensors whose deleter releases the block. */
 typedef struct ft_client ft_client;
-int ft_client_create(ft_chan* ch, void* c2d, void* d2c, int device, ft_client** out);
+int ft_client_create(ft_chan* ch, int sock, void* c2d, void* d2c, int device, ft_client** out);
 int ft_client_destroy(ft_client* cl);
+/* the daemon is gone: later sends fail, our streams' waits on its marks are released */
+int ft_client_abandon(ft_client* cl);
 int ft_client_sent(ft_client* cl, uint64_t* out);
 int ft_client_views(ft_client* cl, int* out);  /* live DLPack views */
 int ft_client_send(ft_client* cl, const void* msg, uint32_t n);

@@ -270,7 +270,8 @@ _SIGS = {
     "ft_lane_take": (None, [vp, i64, vp, P(i64), C.c_char_p, C.c_int]),
     "ft_lane_ids": (None, [vp, C.c_int, P(i64), C.c_int, P(C.c_int)]),
     "ft_lane_stats": (None, [vp, P(u64), C.c_int]),
-    "ft_client_create": (None, [vp, vp, vp, C.c_int, P(vp)]),
+    "ft_client_create": (None, [vp, C.c_int, vp, vp, C.c_int, P(vp)]),
+    "ft_client_abandon": (None, [vp]),
     "ft_client_destroy": (None, [vp]),
     "ft_client_sent": (None, [vp, P(u64)]),
     "ft_client_views": (None, [vp, P(C.c_int)]),

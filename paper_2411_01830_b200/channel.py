@@ -114,20 +114,34 @@ class Channel:
             self._client_send(body)
             return
         if self._chan is not None:
-            rc = LIB.raw("ft_chan_send")(self._chan, self._dir, body, len(body), -1)
-            if rc == 13:
-                raise ConnectionError("channel closed")
-            if rc:
-                raise_status(rc)
+            self._chan_send(body)
             return
         self.sock.sendall(_HDR.pack(len(body)) + body)
+
+    def _chan_send(self, body: bytes):
+        # a full ring waits for the peer to drain it while the peer lives
+        while True:
+            rc = LIB.raw("ft_chan_send")(self._chan, self._dir, body, len(body), _POLL_US)
+            if rc == 0:
+                return
+            if rc == 13:
+                raise ConnectionError("channel closed")
+            if rc != 12:
+                raise_status(rc)
+            self._check_peer()
 
     def _client_send(self, body: bytes):
         rc = LIB.raw("ft_client_send")(self._client, body, len(body))
         if rc == 13:
-            raise ConnectionError("channel closed")
+            self._daemon_gone("channel closed")
         if rc:
             raise_status(rc)
+
+    def _daemon_gone(self, why: str):
+        # our streams may wait on marks the daemon will never write: release them, so
+        # a later synchronise (or close) does not hang
+        LIB.ft_client_abandon(self._client)
+        raise ConnectionError(why)
 
     def client_reply(self, rc: int, buf=None, n=None, spin_us: int = SPIN_US) -> bytes:
         """The reply a native client call left in ``buf`` (``n`` bytes) with status
@@ -135,10 +149,13 @@ class Channel:
         buf = self._buf if buf is None else buf
         n = self._n if n is None else n
         while rc == 12:
-            self._check_peer()
+            try:
+                self._check_peer()
+            except ConnectionError as e:
+                self._daemon_gone(str(e))
             rc = LIB.raw("ft_client_recv")(self._client, buf, len(buf), C.byref(n), spin_us)
         if rc == 13:
-            raise ConnectionError("channel closed")
+            self._daemon_gone("channel closed")
         if rc:
             raise_status(rc)
         return buf.raw[:n.value]
@@ -148,11 +165,7 @@ class Channel:
         if self._client is not None:
             self._client_send(body)
             return
-        rc = LIB.raw("ft_chan_send")(self._chan, self._dir, body, len(body), -1)
-        if rc == 13:
-            raise ConnectionError("channel closed")
-        if rc:
-            raise_status(rc)
+        self._chan_send(body)
 
     def recv_raw(self, spin_us: int = SPIN_US) -> bytes:
         if self._client is not None:

@@ -9,6 +9,8 @@
 // and sends the release from whatever thread frees the tensor — every send goes
 // through the client's mutex, so the rings keep one producer at a time.
 #include <cuda_runtime.h>
+#include <poll.h>
+#include <sys/socket.h>
 
 #include <atomic>
 #include <cstring>
@@ -57,10 +59,23 @@ struct DoneReq {
 constexpr uint8_t OP_DONE = 3;
 constexpr size_t kRepHdr = 16, kEvOff = kRepHdr + 40;  // RepHdr, then BlockRep.ev
 
+bool sock_gone(int sock) {  // the daemon's end of the connection socket closed
+  pollfd p{sock, POLLIN, 0};
+  if (poll(&p, 1, 0) <= 0) return false;
+  if (p.revents & (POLLHUP | POLLERR | POLLNVAL)) return true;
+  char b;
+  return recv(sock, &b, 1, MSG_PEEK | MSG_DONTWAIT) == 0;
+}
+
 }  // namespace
 
 struct ft_client {
   ft_chan* ch = nullptr;
+  int sock = -1;          // the connection socket (liveness of the daemon; the caller owns it)
+  bool dead = false;      // the daemon went away: sends fail at once
+  bool abandoned = false;
+  std::atomic<uint32_t> newest_d{0};  // the newest daemon mark a stream of ours waits for
+  std::atomic<bool> any_d{false};
   uint32_t* c2d = nullptr;
   uint32_t* d2c = nullptr;
   int device = 0;
@@ -81,12 +96,50 @@ struct ft_client {
   }
   int wait(cudaStream_t st, int32_t ev) {  // st waits for the daemon's mark `ev`
     if (ev == 0 || ev == -1) return FT_OK;
-    return ft::mem_wait_geq32(st, d2c, (uint32_t)ev);
+    uint32_t v = (uint32_t)ev, cur = newest_d.load(std::memory_order_relaxed);
+    while ((!any_d.load(std::memory_order_relaxed) || (int32_t)(v - cur) > 0) &&
+           !newest_d.compare_exchange_weak(cur, v, std::memory_order_relaxed)) {
+    }
+    any_d.store(true, std::memory_order_relaxed);
+    return ft::mem_wait_geq32(st, d2c, v);
   }
-  int send(const void* b, uint32_t n) {  // (mu held)
-    int rc = ft_chan_send(ch, 0, b, n, -1);
-    if (rc == FT_OK) ++sent;
-    return rc;
+  // the daemon went away: the marks our streams wait for may never be written. The
+  // newest one waited for is written from here (a non-blocking stream: the waiting
+  // streams are parked), so they drain instead of hanging every later synchronise
+  // (the blocks they read stay mapped: the imports hold the memory)
+  void abandon() {
+    if (!any_d.load() || abandoned) return;
+    abandoned = true;
+    uint32_t v = newest_d.load();
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (cur != device) cudaSetDevice(device);
+    cudaStream_t s = nullptr;
+    if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) == cudaSuccess) {
+      cudaMemcpyAsync(d2c, &v, 4, cudaMemcpyHostToDevice, s);
+      cudaStreamSynchronize(s);
+      cudaStreamDestroy(s);
+    }
+    if (cur >= 0 && cur != device) cudaSetDevice(cur);
+  }
+  // (mu held) a full ring waits for the daemon to drain it while the daemon lives: a
+  // daemon that died never will (release messages get no reply, so they can fill it)
+  int send(const void* b, uint32_t n) {
+    if (dead) {
+      ft::set_last_error("ft_client: the daemon went away");
+      return FT_E_CLOSED;
+    }
+    for (;;) {
+      int rc = ft_chan_send(ch, 0, b, n, 200000);
+      if (rc == FT_OK) ++sent;
+      if (rc != FT_E_TIMEOUT) return rc;
+      if (sock >= 0 && sock_gone(sock)) {
+        dead = true;
+        abandon();
+        ft::set_last_error("ft_client: the daemon went away (request ring full)");
+        return FT_E_CLOSED;
+      }
+    }
   }
   // (mu held) FT_E_TIMEOUT after 200 ms without a reply: the caller checks the daemon
   int recv(void* b, uint32_t cap, uint32_t* n, int64_t spin_us) {
@@ -136,11 +189,14 @@ void view_deleter(DLManagedTensor* m) {
 
 extern "C" {
 
-// the function process's lane client over an upgraded connection (takes over `ch`)
-int ft_client_create(ft_chan* ch, void* c2d, void* d2c, int device, ft_client** out) {
+// the function process's lane client over an upgraded connection (takes over `ch`;
+// `sock`, the connection's socket, stays the caller's and only tells it the daemon
+// is alive — -1: never checked)
+int ft_client_create(ft_chan* ch, int sock, void* c2d, void* d2c, int device, ft_client** out) {
   if (!ch || !c2d || !d2c || !out) return FT_E_VALUE;
   auto* cl = new ft_client;
   cl->ch = ch;
+  cl->sock = sock;
   cl->c2d = static_cast<uint32_t*>(c2d);
   cl->d2c = static_cast<uint32_t*>(d2c);
   cl->device = device;
@@ -158,6 +214,16 @@ int ft_client_destroy(ft_client* cl) {
     now = cl->views == 0;
   }
   if (now) release_client(cl);
+  return FT_OK;
+}
+
+// the caller found the daemon gone: sends fail from now on and our streams' waits
+// on its marks are released
+int ft_client_abandon(ft_client* cl) {
+  if (!cl) return FT_E_VALUE;
+  std::lock_guard<std::mutex> lk(cl->mu);
+  cl->dead = true;
+  cl->abandon();
   return FT_OK;
 }
 

@@ -762,7 +762,8 @@ class TubeClient:
             p = self._mapped(rep).ptr + rep["off"] + rep["sync_off"]
             self._sync = (p, p + 128)
             cl = C.c_void_p()
-            dev.LIB.ft_client_create(self.ch._chan, C.c_void_p(p), C.c_void_p(p + 128), device, C.byref(cl))  # noqa: SLF001
+            dev.LIB.ft_client_create(self.ch._chan, self.ch.sock.fileno(), C.c_void_p(p), C.c_void_p(p + 128),
+                                     device, C.byref(cl))  # noqa: SLF001
             self.ch.adopt_client(cl)
             self._cl = cl
             self._rbuf, self._rn = C.create_string_buffer(8192), C.c_uint32()

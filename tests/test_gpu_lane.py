@@ -329,3 +329,80 @@ def test_lane_connection_slow_paths():
     assert tube._accounts_consistent()
     d.close()
     tube.close()
+
+
+def _daemon_only(path, q):
+    sys.path.insert(0, ROOT)
+    from paper_2411_01830_b200.daemon import TubeDaemon
+    from paper_2411_01830_b200.tube import FaaSTube
+    tube = FaaSTube(pcie_gbps=50.0, gpus=[0])
+    TubeDaemon(tube, path)
+    q.put("up")
+    time.sleep(600)
+
+
+def _outlives_its_daemon(path, q, go):
+    sys.path.insert(0, ROOT)
+    from paper_2411_01830_b200 import device as dev
+    from paper_2411_01830_b200.daemon import TubeClient
+    try:
+        c = TubeClient(path, 0)
+        n = 10**6 + 7
+        did = c.unique_id()
+        c.store(did, payload(n, 31).cuda(), consumers=24)
+        views = [c.fetch(did) for _ in range(24)]
+        ok = all(torch.equal(v[:4096].cpu(), payload(n, 31)[:4096]) for v in views[:2])
+        torch.cuda.synchronize()
+        q.put(("ready", ok))
+        assert go.wait(120)                               # the daemon is dead now
+        t0 = time.time()
+        # this process's stream waits on a mark the daemon will never write
+        s = torch.cuda.current_stream(0)
+        dev.LIB.ft_client_wait(c._cl, dev.stream_ptr(s), 100_000)  # noqa: SLF001
+        del views                                         # 24 releases: more than the ring holds
+        try:
+            c.unique_id()
+            raised = False
+        except ConnectionError:
+            raised = True
+        torch.cuda.synchronize()                          # the parked wait was released
+        c.close()
+        q.put(("ok", (raised, time.time() - t0)))
+    except Exception:  # noqa: BLE001
+        import traceback
+        q.put(("err", traceback.format_exc()))
+
+
+def test_function_process_outlives_its_daemon():
+    """The daemon dies (SIGKILL) under a function process holding zero-copy views and
+    a stream parked on one of the daemon's marks: releasing more views than the
+    request ring holds does not block, the next request raises ConnectionError, and
+    synchronising / closing the client returns (its waits on the dead daemon's marks
+    are released) instead of hanging the function."""
+    path = os.path.join(tempfile.mkdtemp(), "faastube.sock")
+    ctx = mp.get_context("spawn")
+    q, qc, go = ctx.Queue(), ctx.Queue(), ctx.Event()
+    dp = ctx.Process(target=_daemon_only, args=(path, q))
+    dp.start()
+    try:
+        assert q.get(timeout=300) == "up"
+        cp = ctx.Process(target=_outlives_its_daemon, args=(path, qc, go))
+        cp.start()
+        try:
+            status, ok = qc.get(timeout=300)
+            assert status == "ready" and ok, ok
+            dp.kill()
+            dp.join(timeout=60)
+            go.set()
+            status, res = qc.get(timeout=120)
+            assert status == "ok", res
+            raised, took = res
+            assert raised and took < 30, res
+            cp.join(timeout=60)
+            assert cp.exitcode == 0
+        finally:
+            if cp.is_alive():
+                cp.kill()
+    finally:
+        if dp.is_alive():
+            dp.kill()
