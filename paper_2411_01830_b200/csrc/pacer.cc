@@ -238,6 +238,7 @@ struct ft_pacer {
   double last_issue_t[2][kMaxDev] = {};
   uint64_t last_issue_ticket[2][kMaxDev] = {};
   bool adapt = true;
+  bool sampling = !std::getenv("FT_PACER_NOSAMPLE");  // (diagnostic switch)
   uint64_t timed_skip = 0;
   std::map<int, StagingRing> rings;  // GPU->host staged routes
   std::map<int, KRing> krings;       // host->GPU staged routes (K2)
@@ -486,7 +487,7 @@ struct ft_pacer {
     Route& r = st.routes[i];
     uint64_t o = r.off + rel;
     if (st.pinned) {
-      if (track && !r.staged() && n >= std::min<uint64_t>(kMinSampleBytes, (uint64_t)batch_chunks * chunk / 2) &&
+      if (track && sampling && !r.staged() && n >= std::min<uint64_t>(kMinSampleBytes, (uint64_t)batch_chunks * chunk / 2) &&
           (samples[st.dir][r.dev].size() < 6 || ++timed_skip % 8 == 0)) {
         // direct route: bracket the DMA with timing events (service-rate sample) —
         // every batch until the estimator has its window, then every 8th (a timed
@@ -520,6 +521,18 @@ struct ft_pacer {
       ++st.jobs;
     }
     jcv.notify_all();
+  }
+
+  // the link service rate of a landed batch's timed DMAs (unless another DMA of ours
+  // shared the link meanwhile)
+  void take_samples(const Stage& st, const Batch& b, double t) {
+    for (auto& tm : b.timing) {
+      float ms = 0.f;
+      bool overlapped = tm.contended || (last_issue_ticket[tm.dir][tm.dev] != st.ticket &&
+                                         last_issue_t[tm.dir][tm.dev] > tm.issued);
+      if (!overlapped && cudaEventElapsedTime(&ms, tm.t0, tm.t1) == cudaSuccess && ms > 0.f)
+        sample(tm.dir, tm.dev, (double)tm.bytes / ((double)ms * 1e6), t);
+    }
   }
 
   void release_batch(Batch& b) {
@@ -729,6 +742,12 @@ struct ft_pacer {
         guarded.erase(st.key);
       }
       note(st, "land", (double)st.bytes);
+      // the batches still listed landed with the stage: their timed DMAs are samples
+      // too (a stage's last batches, and all of a one-batch stage, are never stepped
+      // again — unread, the estimator's window would not fill from small stages and
+      // every one of their DMAs would keep paying for timing events)
+      if (st.err == FT_OK)
+        for (auto& b : st.inflight) take_samples(st, b, t);
       release_inflight(st);  // join events are returned by the submitter
       if (st.err != FT_OK) {
         errors[tk] = {st.err, st.msg};
@@ -752,13 +771,7 @@ struct ft_pacer {
       for (auto& tm : b.timing)
         if (cudaEventQuery(tm.t1) != cudaSuccess) ok = false;
       if (!ok) break;
-      for (auto& tm : b.timing) {
-        float ms = 0.f;
-        bool overlapped = tm.contended || (last_issue_ticket[tm.dir][tm.dev] != st.ticket &&
-                                           last_issue_t[tm.dir][tm.dev] > tm.issued);
-        if (!overlapped && cudaEventElapsedTime(&ms, tm.t0, tm.t1) == cudaSuccess && ms > 0.f)
-          sample(tm.dir, tm.dev, (double)tm.bytes / ((double)ms * 1e6), t);
-      }
+      take_samples(st, b, t);
       release_batch(b);
       st.inflight.pop_front();
       note(st, "done", (double)st.inflight.size());
@@ -1083,7 +1096,8 @@ static int submit_impl(ft_pacer* p, int dir, const char* key, int managed, doubl
     p->retire_landed();
   }
   st.ticket = p->next_ticket++;
-  st.key = key && *key ? std::string(key) : "m" + std::to_string(st.ticket);
+  // (an unnamed host->GPU stage is "h<ticket>": the tube's own names are "m<n>")
+  st.key = key && *key ? std::string(key) : (dir == 0 ? "h" : "m") + std::to_string(st.ticket);
   try {
     // the routes start after the consumer stream's prior work (object ready, dst free)
     DevGuard g(dst_dev);

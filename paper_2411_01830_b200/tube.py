@@ -691,7 +691,16 @@ class FaaSTube:
             else:
                 res = self._execute(obj, plan, src, dst, out, slo_ms, infer_ms)
             self.stats["fetches"] += 1
-            self._consumed(obj)
+            drop_after = False
+            if h2g and obj.block is None:
+                # the last consumer of a host object: out of the table now, its index entry
+                # dropped once the stage is issued (the DMA goes out first)
+                obj.remaining -= 1
+                if obj.remaining <= 0:
+                    drop_after = not obj.retired
+                    self._retire(obj, drop=False)
+            else:
+                self._consumed(obj)
             if not (h2g or d2h):
                 return res
         if d2h:
@@ -709,9 +718,16 @@ class FaaSTube:
             return res.view(torch.uint8).view(obj.dtype).view(obj.shape)
         # host->GPU stage: the pacer returns once its last batch is issued — outside
         # the tube lock, so concurrent tenants' stages are paced side by side
-        ticket = self.pacer.submit_routes(*stage)
+        tl = self._tls
+        rc = tl.submit(self.pacer._h, b"", *stage, tl.ticket)  # noqa: SLF001
         with self._lock:
-            self._tickets.append((ticket, obj.host, res))
+            if rc == 0:
+                self._tickets.append((tl.ticket.value, obj.host, res))
+            if drop_after:
+                self.index.drop(obj.did)
+        if rc:
+            from ._lib import raise_status
+            raise_status(rc)
         return res
 
     def _fetch_local(self, obj: _Obj, out: torch.Tensor):
@@ -1172,8 +1188,10 @@ class FaaSTube:
         if obj.remaining <= 0:
             self._retire(obj, fence, stream)
 
-    def _retire(self, obj: _Obj, fence=None, stream=None):
-        """engine.py:667-679: last consumer done -> drop index entry, free block."""
+    def _retire(self, obj: _Obj, fence=None, stream=None, drop: bool = True):
+        """engine.py:667-679: last consumer done -> drop index entry, free block.
+        ``drop=False`` (a block-less object): the caller drops the index entry itself
+        once its transfer is issued."""
         if obj.retired:
             return
         obj.retired = True
@@ -1198,7 +1216,8 @@ class FaaSTube:
             if self.strategy.migration != "none" and self._off_gpu[blk.device]:
                 self._pending.add(("prefetch", blk.device))  # engine.py:678-679, 717-736
             return
-        self.index.drop(obj.did)
+        if drop:
+            self.index.drop(obj.did)
         self._maybe_free(obj, stream)
 
     def _maybe_free(self, obj: _Obj, stream=None):
@@ -1342,7 +1361,7 @@ class FaaSTube:
         are paced in batches at their rate (engine.py:537-646); the consumer's
         stream is ordered after the last byte. The plan, the byte ranges and the
         route streams come from one native call (``ft_h2g_routes``). Returns
-        (result, Pacer.submit_routes arguments); the caller submits outside the
+        (result, ft_pacer_submit's arguments after the key); the caller submits outside the
         tube lock (the routes live in this thread's array until then)."""
         res = self._out(obj, dst.gpu, out)
         s = self._stream(dst.gpu)
@@ -1352,13 +1371,18 @@ class FaaSTube:
         if not hasattr(tl, "routes"):
             from ._lib import RouteC
             tl.routes, tl.k, tl.managed = (RouteC * 16)(), dev.C.c_int(), dev.C.c_int()
-            tl.cap, tl.nv = dev.C.c_double(), dev.C.c_uint64()
-        dev.LIB.ft_h2g_routes(self.plane._h, self.node, dst.gpu, obj.nbytes, dev.C.c_void_p(s), tl.routes, 16,
-                              dev.C.byref(tl.k), dev.C.byref(tl.managed), dev.C.byref(tl.cap), dev.C.byref(tl.nv))
-        managed = bool(tl.managed.value)
+            tl.cap, tl.nv, tl.ticket = dev.C.c_double(), dev.C.c_uint64(), dev.C.c_uint64()
+            tl.plan = dev.LIB.raw("ft_h2g_routes")
+            tl.submit = dev.LIB.raw("ft_pacer_submit")
+        rc = tl.plan(self.plane._h, self.node, dst.gpu, obj.nbytes, s, tl.routes, 16, tl.k, tl.managed, tl.cap,
+                     tl.nv)
+        if rc:
+            from ._lib import raise_status
+            raise_status(rc)
+        managed = tl.managed.value
         host = obj.host
-        stage = (f"m{next(self._managed_ids)}" if managed else "", managed,
-                 slo_ms if slo_ms else 1e9,                       # engine.py:546-547
+        # (the pacer names a managed stage itself: "h<ticket>")
+        stage = (managed, slo_ms if slo_ms else 1e9,                  # engine.py:546-547
                  infer_ms if infer_ms is not None else 0.0, tl.cap.value, res.data_ptr(), dst.gpu,
                  host.data_ptr(), obj.nbytes, host.is_pinned(), tl.k.value, tl.routes, s)
         self.stats["bytes_h2d"] += obj.nbytes
