@@ -304,7 +304,7 @@ _SIGS = {
                               P(vp), C.c_int, vp, P(dbl), P(dbl)]),
     "ft_fetch_local": (None, [vp, vp, i64, i64, cstr, C.c_int, vp, vp, u64, C.c_int, vp, C.c_uint32, P(vp), C.c_int,
                               vp, P(dbl), P(dbl)]),
-    "ft_retire_many": (None, [vp, vp, C.c_int, vp, vp, P(cstr), vp, vp]),
+    "ft_retire_many": (None, [vp, vp, C.c_int, vp, vp, vp, vp, vp]),
     "ft_stream_create": (None, [C.c_int, P(vp)]),
     "ft_stream_destroy": (None, [vp]),
     "ft_event_create": (None, [C.c_int, P(vp)]),

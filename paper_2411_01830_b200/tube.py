@@ -805,62 +805,66 @@ class FaaSTube:
             self._last_op_ms = self.now_ms()
             objs = self._objs
             get = objs.get
+            rest_add = rest.append
+            # one pass: validate, order (newest ready record per stream), segment, and
+            # count the consumer off — the last consumers' retires go after the launch
             by_gpu = {}
             last_g, grp = None, None
             for did, out in items:
                 obj = get(did)
                 if obj is None or obj.block is None:
-                    rest.append((did, out))
+                    rest_add((did, out))
                     continue
                 og = obj.gpu
                 if og != out.get_device() or out.nbytes != obj.nbytes or not out.is_contiguous():
-                    rest.append((did, out))
+                    rest_add((did, out))
                     continue
                 if og != last_g:
                     grp = by_gpu.get(og)
-                    if grp is None:
-                        grp = by_gpu[og] = ([], {}, [])        # objects, newest ready per stream, segments
+                    if grp is None:            # keep, retire, newest ready per stream, segments, bytes
+                        grp = by_gpu[og] = [[], [], {}, [], 0]
                     last_g = og
-                grp[0].append(obj)
                 r = obj.ready
                 if r is not None:                              # (the newest record per stream covers the rest)
                     k = r.stream if r.stream is not None else id(r)
-                    cur = grp[1].get(k)
+                    cur = grp[2].get(k)
                     if cur is None or r.seq > cur.seq:
-                        grp[1][k] = r
-                grp[2].extend((out.data_ptr(), obj.block.ptr, obj.nbytes))
-            for g, (group, readies, flat) in by_gpu.items():
+                        grp[2][k] = r
+                grp[3].extend((out.data_ptr(), obj.block.ptr, obj.nbytes))
+                grp[4] += obj.nbytes
+                obj.remaining -= 1
+                if obj.remaining <= 0 and obj.pins == 0 and not obj.retired:
+                    grp[1].append(obj)
+                else:
+                    grp[0].append(obj)
+            for g, (keep, retiring, readies, flat, nb) in by_gpu.items():
                 s = self._stream(g)
                 dev.wait_events(s, readies.values())
                 dev.copy_batch_flat(flat, g, s)
                 done = dev.Ev(g).record(s)     # one fence for every block the batch read
-                fence1 = (done,)
-                r_objs, r_ids, r_pbs, r_names, r_fences = [], [], [], [], []
-                nb = 0
-                for o in group:
-                    nb += o.nbytes
-                    o.remaining -= 1
-                    if o.remaining <= 0 and o.pins == 0 and not o.retired:
-                        r_objs.append(o)
-                        r_ids.append(o.did)
-                        r_pbs.append(o.block.policy_block)
-                        r_names.append(o.producer)
-                        # the batch's stream waited on each object's `ready` before `done`
-                        r_fences.append(fence1 + tuple(o.readers) if o.readers else fence1)
-                    else:
-                        o.readers.append(done)      # the last consumer's retire fences on this read
-                        if o.remaining <= 0:
-                            self._retire(o, done)
+                for o in keep:
+                    o.readers.append(done)          # the last consumer's retire fences on this read
+                    if o.remaining <= 0 and o.pins:
+                        # a pinned last consumer (an object listed twice whose second entry
+                        # retires is in `retiring`)
+                        self._retire(o, done)
                 self.stats["bytes_local"] += nb
-                self.stats["fetches"] += len(group)
-                if r_objs:
+                self.stats["fetches"] += len(keep) + len(retiring)
+                if retiring:
                     # every last consumer's retire in one native call (dataplane.py:98-101,
-                    # datastore.py:146-149)
-                    rws, lasts = self.pools[g].retire_many(self.index, r_ids, r_pbs, r_names, r_fences)
+                    # datastore.py:146-149), fenced on the batch's read (its stream waited on
+                    # each object's `ready` before `done`) and any earlier readers
+                    fence1 = (done,)
+                    r_ids = [o.did for o in retiring]
+                    rws, lasts = self.pools[g].retire_many(
+                        self.index, r_ids, [o.block.policy_block for o in retiring],
+                        [o.producer for o in retiring],
+                        [fence1 + tuple(o.readers) if o.readers else fence1 for o in retiring])
                     live, freed, last_of = self._live, 0, {}
-                    for i, o in enumerate(r_objs):
+                    pop = objs.pop
+                    for i, o in enumerate(retiring):
                         o.retired = True
-                        if objs.pop(o.did, None) is not None:
+                        if pop(o.did, None) is not None:
                             live[(o.producer, g)] -= 1
                             freed += o.nbytes
                         o.block = None

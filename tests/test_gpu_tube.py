@@ -201,6 +201,34 @@ def test_fetch_many_batched_handoff(tube):
         assert d not in tube._objs
 
 
+def test_fetch_many_repeated_and_pinned_objects():
+    """fetch_many with an object listed twice (its two consumers in one batch) and a
+    last consumer of an object a zero-copy view still pins: bytes exact, each block
+    returned to the pool exactly once (the view's release frees the pinned one)."""
+    from paper_2411_01830_b200.tube import FaaSTube
+    t = FaaSTube("faastube", pool_floor_bytes=0.0, gpus=[0])
+    x = torch.randint(0, 256, (3 << 20,), dtype=torch.uint8, device="cuda:0")
+    y = torch.randint(0, 256, (5 << 20,), dtype=torch.uint8, device="cuda:0")
+    torch.cuda.synchronize()
+    in_use0 = t.pools[0].policy.in_use_bytes
+    dx, dy = t.unique_id(), t.unique_id()
+    t.store(dx, x, consumers=2)
+    t.store(dy, y, consumers=2)
+    view = t.fetch(dy, device=0)                       # first consumer of y: a view (pins it)
+    o1, o2, o3 = torch.empty_like(x), torch.empty_like(x), torch.empty_like(y)
+    t.fetch_many([(dx, o1), (dx, o2), (dy, o3)])
+    torch.cuda.synchronize()
+    assert torch.equal(o1, x) and torch.equal(o2, x) and torch.equal(o3, y) and torch.equal(view, y)
+    assert dx not in t._objs and dy not in t._objs
+    del view
+    import gc
+    gc.collect()
+    torch.cuda.synchronize()
+    assert t.pools[0].policy.in_use_bytes == in_use0
+    assert t._accounts_consistent()
+    t.close()
+
+
 def test_managed_response_and_host_fetch():
     """With the PCIe scheduler, responses and GPU->host fetches are managed
     GPU->host stages (engine.py:414-423, 537-575) — bytes exact, caller's
