@@ -54,6 +54,7 @@ def parse():
     ap.add_argument("--no-ncu", action="store_true", help="skip the in-run ncu DRAM-traffic capture")
     ap.add_argument("--quick", action="store_true", help="short workflow traces, one seed (development runs)")
     ap.add_argument("--ncu-probe", action="store_true", help=argparse.SUPPRESS)
+    ap.add_argument("--peer-probe", type=int, nargs=2, metavar=("SRC", "DST"), help=argparse.SUPPRESS)
     ap.add_argument("--max-throughput", action="store_true",
                     help="also search config 4's max req/s per strategy (harness.max_throughput; minutes)")
     return ap.parse_args()
@@ -324,6 +325,40 @@ def ncu_probe():
     tube.close()
 
 
+def peer_probe(src: int, dst: int):
+    """A put on GPU ``src`` and a get into GPU ``dst`` through a tube over the two,
+    byte-checked, in a child process: a peer path that faults (a sticky CUDA error)
+    takes this process down, not the rank that asked."""
+    import torch
+    from paper_2411_01830_b200.strategies import strategy_preset
+    from paper_2411_01830_b200.tube import FaaSTube
+    torch.cuda.set_device(src)
+    tube = FaaSTube(strategy_preset("faastube", parallel_pcie=False), gpus=sorted({src, dst}), pcie_gbps=55.0)
+    for n in (4097, 1 << 20, 64 << 20):
+        x = torch.randint(0, 256, (n,), dtype=torch.uint8, device=f"cuda:{src}")
+        out = torch.empty(n, dtype=torch.uint8, device=f"cuda:{dst}")
+        did = tube.unique_id()
+        tube.store(did, x, producer="probe")
+        tube.fetch(did, device=dst, out=out, consumer="probe")
+        torch.cuda.synchronize(src)
+        torch.cuda.synchronize(dst)
+        assert torch.equal(out.cpu(), x.cpu()), f"{n} B: delivered bytes differ"
+    tube.close()
+    print("peer path ok")
+
+
+def probe_peer_path(src: int, dst: int):
+    """None if the cross-GPU put/get ran byte-exact in a child process, else why not."""
+    try:
+        r = subprocess.run([sys.executable, os.path.abspath(__file__), "--peer-probe", str(src), str(dst)],
+                           capture_output=True, text=True, timeout=300)
+    except subprocess.TimeoutExpired:
+        return f"peer probe {src}->{dst} timed out (300 s)"
+    if r.returncode == 0:
+        return None
+    return f"peer probe {src}->{dst} exit {r.returncode}: " + (r.stdout + r.stderr)[-400:]
+
+
 def roofline_block(achieved, kern_ms, store_ms, fetch_ms, nbytes, peaks, peak_src, traffic, per_ms, achieved_gib,
                    gib_ms):
     peak = peaks.get("hbm_gbs", 6650.0)
@@ -375,6 +410,12 @@ def run_ours(args):
     # pairs: every GPU sends one payload and receives one per step, NVLink both ways);
     # one process per pair, each with its own tube over its two GPUs — no collective
     peer = ((local + 1) % world) % ndev if world > 1 else g
+    cross_error = None
+    if peer != g:
+        # the peer path first runs in a child: a fault there cannot take this rank down
+        cross_error = probe_peer_path(g, peer)
+        if cross_error is not None:
+            peer = g
     torch.cuda.set_device(g)
     from paper_2411_01830_b200 import device as dev
     from paper_2411_01830_b200.tube import FaaSTube, measure_pcie_gbps
@@ -424,7 +465,6 @@ def run_ours(args):
     def delivered():
         return torch.equal(inp.view(torch.uint8).to(x.device), x.view(torch.uint8))
 
-    cross_error = None
     if cross:
         # the first cross-GPU pass on this box: if the peer path cannot run at all (no P2P,
         # a driver error), say so in the line and measure same-GPU replicas instead of
@@ -1418,6 +1458,8 @@ def main():
     args = parse()
     if args.ncu_probe:
         ncu_probe()
+    elif args.peer_probe:
+        peer_probe(*args.peer_probe)
     elif args.impl == "reference":
         run_reference(args)
     else:
