@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--quick", action="store_true", help="short workflow traces, one seed (development runs)")
     ap.add_argument("--ncu-probe", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--peer-probe", type=int, nargs=2, metavar=("SRC", "DST"), help=argparse.SUPPRESS)
+    ap.add_argument("--stripe-probe", action="store_true", help=argparse.SUPPRESS)
+    ap.add_argument("--cross-extras", type=int, metavar="NDEV", help=argparse.SUPPRESS)
     ap.add_argument("--max-throughput", action="store_true",
                     help="also search config 4's max req/s per strategy (harness.max_throughput; minutes)")
     return ap.parse_args()
@@ -347,16 +349,46 @@ def peer_probe(src: int, dst: int):
     print("peer path ok")
 
 
+def stripe_probe():
+    """A 64 MiB pinned host -> GPU 0 fetch striped over every visible GPU's PCIe root
+    (staged routes forwarded over NVLink), byte-checked — in a child process."""
+    import torch
+    from paper_2411_01830_b200.tube import FaaSTube
+    torch.cuda.set_device(0)
+    tube = FaaSTube("faastube")
+    for n in (1 << 20, 64 << 20):
+        host = torch.randint(0, 256, (n,), dtype=torch.uint8).pin_memory()
+        out = torch.empty(n, dtype=torch.uint8, device="cuda:0")
+        did = tube.unique_id()
+        tube.store(did, host, producer="probe")
+        tube.fetch(did, device=0, out=out, consumer="probe")
+        torch.cuda.synchronize()
+        assert torch.equal(out.cpu(), host), f"{n} B: delivered bytes differ"
+    tube.close()
+    print("striped path ok")
+
+
+def _child(flag_args, timeout_s, what):
+    """Run bench.py with hidden ``flag_args`` in a child: (None, stdout) if it exited 0,
+    else (why, stdout)."""
+    try:
+        r = subprocess.run([sys.executable, os.path.abspath(__file__), *flag_args], capture_output=True, text=True,
+                           timeout=timeout_s)
+    except subprocess.TimeoutExpired:
+        return f"{what} timed out ({timeout_s} s)", ""
+    if r.returncode == 0:
+        return None, r.stdout
+    return f"{what} exit {r.returncode}: " + (r.stdout + r.stderr)[-400:], r.stdout
+
+
 def probe_peer_path(src: int, dst: int):
     """None if the cross-GPU put/get ran byte-exact in a child process, else why not."""
-    try:
-        r = subprocess.run([sys.executable, os.path.abspath(__file__), "--peer-probe", str(src), str(dst)],
-                           capture_output=True, text=True, timeout=300)
-    except subprocess.TimeoutExpired:
-        return f"peer probe {src}->{dst} timed out (300 s)"
-    if r.returncode == 0:
-        return None
-    return f"peer probe {src}->{dst} exit {r.returncode}: " + (r.stdout + r.stderr)[-400:]
+    return _child(["--peer-probe", str(src), str(dst)], 300, f"peer probe {src}->{dst}")[0]
+
+
+def probe_striping():
+    """None if the striped host->GPU fetch ran byte-exact in a child process, else why not."""
+    return _child(["--stripe-probe"], 300, "striping probe")[0]
 
 
 def roofline_block(achieved, kern_ms, store_ms, fetch_ms, nbytes, peaks, peak_src, traffic, per_ms, achieved_gib,
@@ -418,17 +450,23 @@ def run_ours(args):
             peer = g
     torch.cuda.set_device(g)
     from paper_2411_01830_b200 import device as dev
+    from paper_2411_01830_b200.strategies import strategy_preset
     from paper_2411_01830_b200.tube import FaaSTube, measure_pcie_gbps
 
+    # on a box of several GPUs the striped host->GPU path (N = 1's tube, rank 0's
+    # extras) is probed in a child first — a fault there would take the headline run
+    # down; it falls back to one link
+    striping_error = probe_striping() if ndev > 1 and rank == 0 else None
     if world > 1:
         # each rank's host->GPU legs use its own GPU's PCIe root (no striping through
         # GPUs another rank drives; config 2's striping runs in the rank-0 extras)
-        from paper_2411_01830_b200.strategies import strategy_preset
         from paper_2411_01830_b200.topology import build_preset
         topo = build_preset("b200", n_gpus=ndev, pcie_gbps=measure_pcie_gbps([g]))
         tube = FaaSTube(strategy_preset("faastube", parallel_pcie=False), topology=topo, gpus=sorted({g, peer}))
-    else:
+    elif ndev > 1 and striping_error is None:
         tube = FaaSTube("faastube")            # drives every visible GPU: H2G stripes over all their roots
+    else:
+        tube = FaaSTube(strategy_preset("faastube", parallel_pcie=False) if ndev > 1 else "faastube")
     gen = torch.Generator(device="cpu").manual_seed(0)
     x = torch.randn(PAYLOAD_SHAPE, generator=gen).half().to(f"cuda:{g}")   # producer output (in HBM)
     nbytes = x.nbytes
@@ -730,7 +768,7 @@ def run_ours(args):
     extras = {}
     if rank == 0 and not args.no_extras:
         extras = run_extras(g, dev, torch, args.max_throughput, world if world > 1 and not shared else ndev,
-                            args.quick)
+                            args.quick, striping=striping_error is None)
     if world > 1:
         dist.barrier()                          # the other ranks wait for rank 0's extras
     if rank == 0:
@@ -763,7 +801,8 @@ def run_ours(args):
                                        f"ring of {world} producer->consumer pairs (rank r: GPU r -> GPU r+1), "
                                        "one process and one tube per pair"),
                        "moved_per_step": {k: v // max(1, args.steps) for k, v in moved.items()},
-                       **({"cross_gpu_error": cross_error} if cross_error else {})},
+                       **({"cross_gpu_error": cross_error} if cross_error else {}),
+                       **({"striping_error": striping_error} if striping_error else {})},
             "p50_pass_ms": round(nearest_rank(per_ms, 50), 5), "p99_pass_ms": round(nearest_rank(per_ms, 99), 5),
             "e2e": {"value": round(world * nbytes / e2e_max / 1e9, 3), "unit": "GB/s",
                     "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": 16,
@@ -924,8 +963,24 @@ def _ev(torch):
 
 
 def run_cross_gpu(torch, dev, ndev):
-    """``ndev``: GPUs this run covers (N under torchrun, all visible at N=1)."""
-    return _cross_gpu(torch, dev, ndev)
+    """``ndev``: GPUs this run covers (N under torchrun, all visible at N=1). Across
+    GPUs it runs in a child process (a fault on a peer path must not take the
+    headline run down); the one-GPU dry run runs here."""
+    if ndev < 2:
+        return _cross_gpu(torch, dev, ndev)
+    why, stdout = _child(["--cross-extras", str(ndev)], 1800, "cross-GPU extras")
+    lines = [ln for ln in stdout.splitlines() if ln.startswith("{")]
+    res = json.loads(lines[-1]) if lines else {}
+    if why is not None:
+        res["cross_gpu_error"] = why
+    return res
+
+
+def cross_extras(ndev: int):
+    import torch
+    from paper_2411_01830_b200 import device as dev
+    torch.cuda.set_device(0)
+    print(json.dumps(_cross_gpu(torch, dev, ndev)), flush=True)
 
 
 def _cross_gpu(torch, dev, ndev):
@@ -1112,7 +1167,8 @@ def _cross_gpu(torch, dev, ndev):
     return out
 
 
-def run_extras(g, dev, torch, max_throughput=False, ndev=1, quick=False):
+def run_extras(g, dev, torch, max_throughput=False, ndev=1, quick=False, striping=True):
+    from paper_2411_01830_b200.strategies import strategy_preset
     from paper_2411_01830_b200.tube import FaaSTube
     out = {}
     try:
@@ -1120,7 +1176,8 @@ def run_extras(g, dev, torch, max_throughput=False, ndev=1, quick=False):
     except Exception as exc:  # noqa: BLE001 - extras never hide the headline line
         import traceback
         out["cross_gpu_error"] = repr(exc) + " " + traceback.format_exc()[-600:]
-    tube = FaaSTube("faastube")               # drives every visible GPU
+    # drives every visible GPU (one link if the striping probe failed)
+    tube = FaaSTube("faastube" if striping else strategy_preset("faastube", parallel_pcie=False))
     try:
         out.update(_single_gpu_extras(tube, g, dev, torch))
     finally:
@@ -1460,6 +1517,10 @@ def main():
         ncu_probe()
     elif args.peer_probe:
         peer_probe(*args.peer_probe)
+    elif args.stripe_probe:
+        stripe_probe()
+    elif args.cross_extras:
+        cross_extras(args.cross_extras)
     elif args.impl == "reference":
         run_reference(args)
     else:
