@@ -26,7 +26,7 @@ import weakref
 import torch
 
 from . import datastore
-from ._lib import LIB
+from ._lib import LIB, raise_status
 
 GiB = 1 << 30
 ENGINE_AUTO, ENGINE_BULK, ENGINE_VEC = 0, 1, 2
@@ -393,6 +393,8 @@ class DevicePool:
         self._names = {}             # producer name -> bytes (encoded once)
         self._addrs = {}             # producer name -> address of those bytes
         self._rw, self._last = C.c_double(), C.c_double()   # out-params of the hot calls (under _lock)
+        self._noev = (C.c_void_p * 1)()
+        self._store_fn, self._fetch_fn = LIB.raw("ft_store_local"), LIB.raw("ft_fetch_local")
         self.grow_events = 0
         # spares: after growth of a class, a background thread maps one more block of
         # that class into the parked list, so the next growth of the class is a reuse.
@@ -559,13 +561,17 @@ class DevicePool:
         """The same-GPU put in one native call (``ft_store_local``): the stream
         waits on the block's fences, copies the output into it, records
         ``ready``; index entry + histogram sample. Returns (R_window, last | None)."""
-        evs = _needed(stream, blk.fences)
+        evs = _needed(stream, blk.fences) if blk.fences else ()
+        arr = (C.c_void_p * len(evs))(*evs) if evs else self._noev
+        name = self._names.get(producer) or self._enc(producer)
         with self._lock, REC_LOCK:
-            LIB.ft_store_local(index._h, self.policy._h, int(data_id), int(node), self.device, float(nbytes),
-                               float(now_ms), self._enc(producer), int(bool(response)), float(concurrency),
-                               C.c_void_p(blk.ptr), C.c_void_p(src_ptr), C.c_void_p(stream), int(hints),
-                               (C.c_void_p * max(1, len(evs)))(*evs), len(evs), C.c_void_p(ready.h),
-                               self._rw, self._last)
+            # (the raw entry point with plain ints / floats: ctypes converts them; the
+            # wrapper objects cost ~2 us a call on this path)
+            rc = self._store_fn(index._h, self.policy._h, data_id, node, self.device, nbytes, now_ms, name,
+                                bool(response), concurrency, blk.ptr, src_ptr, stream, hints, arr, len(evs),
+                                ready.h, self._rw, self._last)
+            if rc:
+                raise_status(rc)
             ready._recorded_on(stream)
             blk.fences = ()                  # the copy waited on them
             rw, last = self._rw.value, self._last.value
@@ -577,13 +583,15 @@ class DevicePool:
         (``ft_fetch_local``): wait ``waits``, copy, record ``done``; with
         ``retire`` the index entry goes and the block returns to the policy,
         fenced on ``done`` + ``fences``. Returns (R_window, last | None)."""
-        evs = _needed(stream, waits)
+        evs = _needed(stream, waits) if waits else ()
+        arr = (C.c_void_p * len(evs))(*evs) if evs else self._noev
+        name = self._names.get(producer) or self._enc(producer)
         with self._lock, REC_LOCK:
-            LIB.ft_fetch_local(index._h, self.policy._h, int(data_id),
-                               blk.policy_block.block_id if retire else -1, self._enc(producer), int(retire),
-                               C.c_void_p(dst_ptr), C.c_void_p(blk.ptr), int(nbytes), self.device,
-                               C.c_void_p(stream), int(hints), (C.c_void_p * max(1, len(evs)))(*evs), len(evs),
-                               C.c_void_p(done.h), self._rw, self._last)
+            rc = self._fetch_fn(index._h, self.policy._h, data_id, blk.policy_block.block_id if retire else -1,
+                                name, bool(retire), dst_ptr, blk.ptr, nbytes, self.device, stream, hints, arr,
+                                len(evs), done.h, self._rw, self._last)
+            if rc:
+                raise_status(rc)
             done._recorded_on(stream)
             if retire:
                 blk.policy_block.in_use = False

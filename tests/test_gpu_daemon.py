@@ -121,9 +121,11 @@ def test_function_process_through_daemon(monkeypatch):
     assert status == "ok", res
     print("daemon round trip (store+fetch 1 MiB, GPU, cross-process):", f"{res['us_store_fetch_1MiB']:.1f} us")
     # the lane keeps a stock of lendable blocks per size class (lane.cc kStockDepth = 3):
-    # the blocks in rotation are the stock, the one lent and the one being read; each is
-    # imported once (one arena per block here), then nothing new is mapped
-    assert res["imports_grown"] <= 3 + 2, res
+    # the blocks in rotation are the stock, the one lent, the one being read and one
+    # whose release the daemon has not applied yet when the next store takes from the
+    # stock (the release races the next commit); each is imported once (one arena per
+    # block here), then nothing new is mapped
+    assert res["imports_grown"] <= 3 + 3, res
     assert res["missing"] and "MissingData" in res["missing"], res
     assert dropped > 0 and res["after_shrink"] < res["mapped"], (dropped, res)
     # the daemon side holds the function's bytes (third consumer)
