@@ -235,8 +235,19 @@ struct ft_pacer {
   int links = 1;
   double link_gbps[2] = {0.0, 0.0};          // per-link capacity the partition assumes, per direction
   std::deque<double> samples[2][kMaxDev];
-  double last_issue_t[2][kMaxDev] = {};
+  // per link: the newest pinned DMA issue (ticket, time) and the newest by any other
+  // ticket than that one — so a sample can tell whether ANOTHER stage issued onto its
+  // link after it (timed or not)
+  double last_issue_t[2][kMaxDev] = {}, other_issue_t[2][kMaxDev] = {};
   uint64_t last_issue_ticket[2][kMaxDev] = {};
+  void note_issue(int dir, int dev, uint64_t ticket, double t) {
+    if (last_issue_ticket[dir][dev] != ticket) other_issue_t[dir][dev] = last_issue_t[dir][dev];
+    last_issue_ticket[dir][dev] = ticket;
+    last_issue_t[dir][dev] = t;
+  }
+  double newest_other_issue(int dir, int dev, uint64_t ticket) const {
+    return last_issue_ticket[dir][dev] != ticket ? last_issue_t[dir][dev] : other_issue_t[dir][dev];
+  }
   bool adapt = true;
   bool sampling = !std::getenv("FT_PACER_NOSAMPLE");  // (diagnostic switch)
   uint64_t timed_skip = 0;
@@ -501,11 +512,11 @@ struct ft_pacer {
         tm.t1 = get_tevent(r.dev);
         ck(cudaEventRecord(tm.t1, r.ce), "record t1");
         st.inflight.back().timing.push_back(tm);
-        last_issue_t[st.dir][r.dev] = tm.issued;
-        last_issue_ticket[st.dir][r.dev] = st.ticket;
+        note_issue(st.dir, r.dev, st.ticket, tm.issued);
         return;
       }
       issue(r, st.dst + o, st.host + o, n, st.dir);
+      note_issue(st.dir, r.dev, st.ticket, now());
       // (an inline stage's only batch: the landing event seal() records follows it on
       // the same stream, nothing polls a batch event for it)
       if (track && !(st.inline_route && rel + n == r.len)) {
@@ -528,8 +539,7 @@ struct ft_pacer {
   void take_samples(const Stage& st, const Batch& b, double t) {
     for (auto& tm : b.timing) {
       float ms = 0.f;
-      bool overlapped = tm.contended || (last_issue_ticket[tm.dir][tm.dev] != st.ticket &&
-                                         last_issue_t[tm.dir][tm.dev] > tm.issued);
+      bool overlapped = tm.contended || newest_other_issue(tm.dir, tm.dev, st.ticket) > tm.issued;
       if (!overlapped && cudaEventElapsedTime(&ms, tm.t0, tm.t1) == cudaSuccess && ms > 0.f)
         sample(tm.dir, tm.dev, (double)tm.bytes / ((double)ms * 1e6), t);
     }
