@@ -860,11 +860,21 @@ def _daemon_client(path, g, q):
         from paper_2411_01830_b200.daemon import TubeClient
         c = TubeClient(path, g)
         res = {}
+        # steady state: every size class's stock and mappings exist and the host cores
+        # are awake before any call is timed (the first size measured used to pay for it)
+        for n in (4096, 1 << 20, 64 << 20):
+            x = torch.empty(n, dtype=torch.uint8, device=f"cuda:{g}")
+            for _ in range(30):
+                did = c.unique_id()
+                c.store(did, x)
+                del x
+                x = c.fetch(did)
+            del x
         for n in (4096, 1 << 20, 64 << 20):
             x = torch.randint(0, 256, (n,), dtype=torch.uint8, device=f"cuda:{g}")
             out = torch.empty_like(x)
             st, ft, vt, rt = [], [], [], []
-            for i in range(60):
+            for i in range(110):
                 did = c.unique_id()
                 t0 = time.perf_counter()
                 c.store(did, x)
@@ -876,7 +886,7 @@ def _daemon_client(path, g, q):
                 t3 = time.perf_counter()
                 v = c.fetch(did)                       # zero-copy view of the stored block
                 t4 = time.perf_counter()
-                ok = bool(torch.equal(v, x)) if i in (0, 59) else True
+                ok = bool(torch.equal(v, x)) if i in (0, 109) else True
                 t5 = time.perf_counter()
                 del v                                  # release (done + read event) to the daemon
                 t6 = time.perf_counter()

@@ -194,10 +194,16 @@ struct ft_lane {
   std::vector<ft_lane_conn*> conns;
   uint64_t next_conn = 1;
   std::map<int, std::vector<cudaEvent_t>> evpool;
-  // event queue to the tube
+  // event queue to the tube. While events keep coming the service thread polls the
+  // queue (every kPollUs) instead of sleeping on `ecv`: a wake-up per event put a
+  // futex syscall into every request the workers answer (~5 us a request). After
+  // kIdleUs without an event it sleeps on `ecv` (`sleeping`) and the next emit wakes it.
+  static constexpr int64_t kPollUs = 500, kIdleUs = 20000;
   std::mutex emu;
   std::condition_variable ecv;
   std::string events;
+  bool sleeping = false;
+  int64_t last_emit_us = 0;
   uint64_t stats[10] = {};  // commits, fetches, dones, uids, forwarded, stock hits / misses, adopted, recycled, lost
 
   double now_ms() const { return ((double)now_us() * 1e-6 - t0) * 1e3; }
@@ -225,7 +231,8 @@ struct ft_lane {
     x.name_len = (uint32_t)name.size();
     events.append(reinterpret_cast<const char*>(&x), sizeof x);
     events.append(name);
-    ecv.notify_all();
+    last_emit_us = now_us();
+    if (sleeping) ecv.notify_all();
   }
 };
 
@@ -914,11 +921,21 @@ int ft_lane_events(ft_lane* L, void* buf, uint64_t cap, uint64_t* n, int64_t tim
   if (!L || !n) return FT_E_VALUE;
   std::unique_lock<std::mutex> lk(L->emu);
   if (L->events.empty() && timeout_us != 0) {
-    auto pred = [&] { return !L->events.empty(); };
-    if (timeout_us < 0)
-      L->ecv.wait(lk, pred);
-    else
-      L->ecv.wait_for(lk, std::chrono::microseconds(timeout_us), pred);
+    if (now_us() - L->last_emit_us < ft_lane::kIdleUs) {
+      // busy: look again shortly, without asking the emitters for a wake-up
+      lk.unlock();
+      std::this_thread::sleep_for(std::chrono::microseconds(
+          timeout_us < 0 ? ft_lane::kPollUs : std::min<int64_t>(timeout_us, ft_lane::kPollUs)));
+      lk.lock();
+    } else {
+      auto pred = [&] { return !L->events.empty(); };
+      L->sleeping = true;
+      if (timeout_us < 0)
+        L->ecv.wait(lk, pred);
+      else
+        L->ecv.wait_for(lk, std::chrono::microseconds(timeout_us), pred);
+      L->sleeping = false;
+    }
   }
   // whole records only
   uint64_t take = 0;
