@@ -343,7 +343,8 @@ class PoolBlock:
         t = base[:nbytes]
         if dtype != torch.uint8:
             t = t.view(dtype)
-        return t.view(shape) if shape is not None else t
+        # (a flat byte payload is the slice itself: each view costs ~1 us)
+        return t.view(shape) if shape is not None and (dtype != torch.uint8 or len(shape) != 1) else t
 
     def wait_fences(self, stream):
         wait_events(stream, self.fences)
@@ -395,6 +396,7 @@ class DevicePool:
         self._rw, self._last = C.c_double(), C.c_double()   # out-params of the hot calls (under _lock)
         self._noev = (C.c_void_p * 1)()
         self._store_fn, self._fetch_fn = LIB.raw("ft_store_local"), LIB.raw("ft_fetch_local")
+        self._retire_fn = LIB.raw("ft_retire_commit")
         self.grow_events = 0
         # spares: after growth of a class, a background thread maps one more block of
         # that class into the parked list, so the next growth of the class is a reuse.
@@ -633,17 +635,20 @@ class DevicePool:
     def commit_retire(self, index, data_id: int, blk: "PoolBlock", fences, producer: str):
         """Index drop + block back to the policy (fenced) + the producer's window
         in one call (``ft_retire_commit``); returns (R_window, last | None)."""
-        rw, last = C.c_double(), C.c_double()
+        name = self._names.get(producer) or self._enc(producer)
         with self._lock:
-            LIB.ft_retire_commit(index._h, self.policy._h, int(data_id), int(blk.policy_block.block_id),
-                                 producer.encode(), C.byref(rw), C.byref(last))
+            rc = self._retire_fn(index._h, self.policy._h, data_id, blk.policy_block.block_id, name, self._rw,
+                                 self._last)
+            if rc:
+                raise_status(rc)
             blk.policy_block.in_use = False
             if fences:
                 self._fences[blk.policy_block.block_id] = tuple(fences)
             if self.policy.mode == "none":
                 self.policy._blocks.pop(blk.policy_block.block_id, None)
                 self._unmap(blk.policy_block.block_id)
-        return rw.value, (None if last.value != last.value else last.value)
+            rw, last = self._rw.value, self._last.value
+        return rw, (None if last != last else last)
 
     def record(self, func: str, now_ms: float, size: float, concurrency: float):
         with self._lock:

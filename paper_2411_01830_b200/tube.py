@@ -1227,14 +1227,17 @@ class FaaSTube:
     def _maybe_free(self, obj: _Obj, stream=None):
         if obj.block is not None and obj.pins == 0 and obj.retired:
             blk, obj.block = obj.block, None
+            g = blk.device
             # later writers of this block must order after our readers
-            ev = dev.Ev(blk.device).record(stream if stream is not None else self._stream(blk.device))
+            ev = dev.Ev(g).record(stream if stream is not None else self._stream(g))
             fences = [ev] + obj.readers + ([obj.ready] if obj.ready is not None else [])
             obj.readers = []
-            self.pools[blk.device].free(blk, fences)
-            self._push_shrink(blk.device, obj.producer, self.now_ms())
-            if self.strategy.migration != "none" and self._off_gpu[blk.device]:
-                self._pending.add(("prefetch", blk.device))  # engine.py:678-679, 717-736
+            # the block back to the policy (fenced) and the producer's window in one
+            # native call — the index entry went at retire (id -1 drops nothing)
+            rw, last = self.pools[g].commit_retire(self.index, -1, blk, fences, obj.producer)
+            self._push_due(g, rw, last, self.now_ms())
+            if self.strategy.migration != "none" and self._off_gpu[g]:
+                self._pending.add(("prefetch", g))  # engine.py:678-679, 717-736
 
     def _unpin(self, obj, stream=None):
         with self._lock:
