@@ -1377,7 +1377,7 @@ def _single_gpu_extras(tube, g, dev, torch):
         row = {"bytes": m, "objects": k}
         for mode in ("one_by_one", "fetch_many"):
             ts = []
-            for r in range(4):
+            for r in range(10):                       # median of 9 (the first warms)
                 items = []
                 for j in range(k):
                     d = tube.unique_id()
