@@ -406,3 +406,64 @@ def test_function_process_outlives_its_daemon():
     finally:
         if dp.is_alive():
             dp.kill()
+
+
+def _bad_shapes(path, q):
+    sys.path.insert(0, ROOT)
+    import struct
+    from paper_2411_01830_b200 import daemon as dm
+    try:
+        c = dm.TubeClient(path, 0)
+        x = payload(4096, 1).cuda()
+        errors = []
+        for shape in ((1 << 62, 8), (-1, 8)):
+            did = c.unique_id()
+            c.store(did, x)                               # leaves the next 4 KiB-class block lent
+            rep = c._loans.pop(dm._class_of(4096))        # noqa: SLF001
+            name = b"evil"
+            body = dm._COMMIT.pack(dm.OP_COMMIT, dm._CODE[torch.uint8], 2, 0, 0, 1, len(name), rep["token"],
+                                   c.unique_id(), 0) + struct.pack("<2q", *shape) + name
+            try:
+                c._block_bin(body)                        # noqa: SLF001
+                errors.append(None)
+            except dm.DaemonError as e:
+                errors.append(str(e))
+            assert torch.equal(c.fetch(did), x)           # (its only consumer: the block goes back)
+        did = c.unique_id()                               # the daemon still serves this client
+        c.store(did, x)
+        ok = torch.equal(c.fetch(did), x)
+        c.close()
+        q.put(("ok", (errors, ok)))
+    except Exception:  # noqa: BLE001
+        import traceback
+        q.put(("err", traceback.format_exc()))
+
+
+def test_lane_rejects_forged_commit_shapes():
+    """A commit whose shape overflows the byte count or has a negative dimension (a
+    buggy or hostile function process) is refused with an error reply — not stored
+    with a byte count smaller than what its shape lets a consumer read — and the lent
+    block goes back to the pool; the connection keeps working."""
+    from paper_2411_01830_b200.daemon import TubeDaemon
+    from paper_2411_01830_b200.tube import FaaSTube
+    tube = FaaSTube(pcie_gbps=50.0, gpus=[0])
+    path = os.path.join(tempfile.mkdtemp(), "faastube.sock")
+    d = TubeDaemon(tube, path)
+    in_use0 = tube.pools[0].policy.in_use_bytes
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_bad_shapes, args=(path, q))
+    p.start()
+    status, res = q.get(timeout=300)
+    p.join(timeout=60)
+    assert status == "ok", res
+    errors, ok = res
+    assert ok
+    assert all(e is not None and "ValueError" in e for e in errors), errors
+    deadline = time.time() + 10
+    while tube.pools[0].policy.in_use_bytes > in_use0 and time.time() < deadline:
+        time.sleep(0.05)
+    assert tube.pools[0].policy.in_use_bytes == in_use0
+    assert tube._accounts_consistent()
+    d.close()
+    tube.close()
