@@ -97,3 +97,32 @@ def test_peer_written_geometry_and_lengths_are_not_trusted():
     m.close()
     LIB.ft_chan_close(h2)
     LIB.ft_chan_close(h)
+
+
+def test_counters_wrap_around_2_32():
+    """The ring's head / tail are free-running 32-bit counters: a channel that has
+    carried ~2^32 messages keeps its order and its full / empty tests across the wrap."""
+    import mmap
+    import struct
+    from paper_2411_01830_b200._lib import LIB, WaitTimeout
+    fd, h = C.c_int(), C.c_void_p()
+    LIB.ft_chan_create(256, 4, C.byref(fd), C.byref(h))
+    m = mmap.mmap(fd.value, 640 + 2 * 256 * 4)
+    start = 0xFFFFFFFE
+    struct.pack_into("<I", m, 128, start)                  # ring 0 head
+    struct.pack_into("<I", m, 192, start)                  # ring 0 tail
+    buf, n = C.create_string_buffer(256), C.c_uint32()
+    sent = 0
+    for i in range(10):
+        while sent < i + 4:                                # keep the ring full (4 slots)
+            msg = b"m%d" % sent
+            LIB.ft_chan_send(h, 0, msg, len(msg), 1000)
+            sent += 1
+        with pytest.raises(WaitTimeout):                   # full across the wrap
+            LIB.ft_chan_send(h, 0, b"x", 1, 2000)
+        LIB.ft_chan_recv(h, 0, buf, 256, C.byref(n), 10, 1000)
+        assert buf.raw[:n.value] == b"m%d" % i
+    head, tail = struct.unpack_from("<I", m, 128)[0], struct.unpack_from("<I", m, 192)[0]
+    assert head == (start + sent) & 0xFFFFFFFF and tail == (start + 10) & 0xFFFFFFFF
+    m.close()
+    LIB.ft_chan_close(h)
