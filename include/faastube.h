@@ -351,6 +351,8 @@ int ft_fd_recv(int sock, int* fd, uint64_t* tag);
  * on a futex; timeouts in us (<0: none). FT_E_CLOSED once the peer closed. */
 typedef struct ft_chan ft_chan;
 int ft_chan_create(uint32_t slot_bytes, uint32_t slots, int* memfd, ft_chan** out);
+/* maps a peer's ring pair: its geometry is checked against the memfd's size and kept
+ * privately (the peer can write the shared header) */
 int ft_chan_attach(int memfd, ft_chan** out);
 int ft_chan_send(ft_chan* c, int dir, const void* buf, uint32_t n, int64_t timeout_us);
 int ft_chan_recv(ft_chan* c, int dir, void* buf, uint32_t cap, uint32_t* n, int64_t spin_us, int64_t timeout_us);
@@ -428,6 +430,7 @@ int ft_lane_stats(ft_lane* lane, uint64_t* out, int cap);
  * of Listing 1 through the daemon — rings, the copy into / out of the mapped block,
  * the sync-word ordering. Views are DLPack tensors whose deleter releases the block. */
 typedef struct ft_client ft_client;
+/* sock: the connection's socket, read only to tell whether the daemon is alive (-1: never) */
 int ft_client_create(ft_chan* ch, int sock, void* c2d, void* d2c, int device, ft_client** out);
 int ft_client_destroy(ft_client* cl);
 /* the daemon is gone: later sends fail, our streams' waits on its marks are released */
