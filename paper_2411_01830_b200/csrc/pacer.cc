@@ -807,10 +807,29 @@ struct ft_pacer {
     const bool owner = adapt && st.pinned && arb.stages.items.size() == 1 &&
                        m->rate >= 0.95 * link_gbps[st.dir] * (double)st.routes.size();
     const int mult = owner ? kOwnerCoalesce : 1;
-    if (!owner && t < st.next_t - kLookahead * dur) return st.next_t - kLookahead * dur;
+    // A stage with slack (rate >= 2x its least) that shares the link with a stage
+    // running at its least rate yields: no lookahead and one batch on the engines at
+    // a time. The copy engines split the link evenly among streams with DMAs queued,
+    // whatever the batch schedule, so a loose stage that always has a batch queued
+    // takes 1/k of the link from a tight one whose least rate is more than that.
+    // ("tight": held at its least rate, and that rate is a real share of the link —
+    // a loose stage parked at a token least rate behind the earliest arrival is not)
+    bool yield = false;
+    if (!owner && arb.stages.items.size() > 1 && m->rate >= 2.0 * m->demand.least) {
+      const double floor_gbps = 0.1 * link_gbps[st.dir];
+      for (auto& kv : arb.stages.items) {
+        const auto& o = kv.second;
+        if (kv.first != st.key && o.started && o.rate < 1.2 * o.demand.least && o.demand.least >= floor_gbps) {
+          yield = true;
+          break;
+        }
+      }
+    }
+    const double la = yield ? 0.0 : kLookahead;
+    if (!owner && t < st.next_t - la * dur) return st.next_t - la * dur;
     int queued = 0;
     for (auto& b : st.inflight) queued += b.batches;
-    bool full = st.pinned ? queued + mult > kInflightBatches
+    bool full = st.pinned ? queued + mult > (yield ? 1 : kInflightBatches)
                           : st.jobs * host_chunk >= 2 * (uint64_t)batch_chunks * chunk;
     if (full) {
       if (!st.was_full) note(st, "full", (double)st.inflight.size());
