@@ -96,9 +96,10 @@ def test_isolation_tight_tenant_meets_its_window():
     info = (link, window, managed, shared)
     if not managed["T"] < min(shared["T"], 1.5 * window + 5.0):
         # T gets exactly its least rate (idle bandwidth goes to the earliest arrival,
-        # pcie_sched.py:49-55), so it has no slack: when the copy engines interleave
-        # the loose stages' already-queued batches with T's, T lags its schedule —
-        # measured 1 run in ~6 at 1.7-2x the window. A second run decides.
+        # pcie_sched.py:49-55), so it has no slack; the loose stages yield to it on the
+        # copy engines (pacer.cc), which took it from 17-18 ms to 9.7-9.8 ms on a
+        # 10.3 ms window (profiles/r02/probe_isolation.txt). A timing test: a second
+        # run decides.
         managed, _ = _contend("faastube", link)
         info = (link, window, managed, shared, "second run")
     assert managed["T"] < shared["T"], info
