@@ -813,7 +813,9 @@ struct ft_pacer {
     // whatever the batch schedule, so a loose stage that always has a batch queued
     // takes 1/k of the link from a tight one whose least rate is more than that.
     // ("tight": held at its least rate, and that rate is a real share of the link —
-    // a loose stage parked at a token least rate behind the earliest arrival is not)
+    // a loose stage parked at a token least rate behind the earliest arrival is not.
+    // Conservative across roots: one arbiter spans every link of a direction, so a
+    // stage also yields to a tight stage on another GPU's root; that only slows it.)
     bool yield = false;
     if (!owner && arb.stages.items.size() > 1 && m->rate >= 2.0 * m->demand.least) {
       const double floor_gbps = 0.1 * link_gbps[st.dir];
